@@ -1,0 +1,133 @@
+/* ppcg_b200.h — C ABI of the B200-native PPCG hot path (libppcg_b200.so).
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t (as void*), never
+ * allocates caller-visible memory, and returns a status code (BK_OK = 0).  Blocks are
+ * row-major (element (r, c) at p[r*ld + c]) — the C-order numpy layout of the reference
+ * package — and complex128 data is interleaved (re, im).
+ *
+ * The reference (blockeig, pure Python over numpy/scipy) has no FFI of its own; each
+ * function below replaces one numpy/scipy call site of its hot path, cited as
+ * file:line under /root/reference/pkg/src/blockeig.  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ */
+#ifndef PPCG_B200_H
+#define PPCG_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BK_OK 0
+#define BK_ERR_ARG (-1)
+#define BK_ERR_CUDA (-2)
+#define BK_ERR_SOLVER (-3)
+#define BK_ERR_UNSUPPORTED (-4)
+
+int bk_version(void);
+
+/* ---- operator apply: SparseHermitian.apply, problems.py:72-73 (scipy csr_matvecs) */
+int bk_spmm_csr_d(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, int m,
+                  const double* X, int64_t ldx, double* Y, int64_t ldy, void* stream);
+int bk_spmm_csr_z(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, int m,
+                  const double* X, int64_t ldx, double* Y, int64_t ldy, void* stream);
+
+/* ---- diagonal apply: DiagonalPreconditioner.apply operators.py:110, DiagonalOperator
+ *      operators.py:68-69 (real d; complex blocks as real views with 2m columns) */
+int bk_scale_rows_d(int64_t n, int m, const double* d, const double* X, int64_t ldx, double* Y,
+                    int64_t ldy, void* stream);
+
+/* ---- Gram X^T Y: block_inner, core.py:43-49 (complex: real Gram of interleaved views +
+ *      bk_cplx_gram_combine_d).  ws: see bk_gram_ws_bytes; must be zero-initialised once. */
+int64_t bk_gram_ws_bytes(int64_t n, int m1, int m2);
+int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+              double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream);
+int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1,
+               int64_t ldy1, double* C1, int64_t ldc1, int m1b, int m2b, const double* X2,
+               int64_t ldx2, const double* Y2, int64_t ldy2, double* C2, int64_t ldc2, void* ws,
+               int64_t ws_bytes, void* stream);
+int bk_cplx_gram_combine_d(int m1, int m2, const double* Cr, int64_t ldr, double* C, int64_t ldc,
+                           void* stream);
+
+/* ---- per-subblock pencil Grams: _solve_subblock_pencil, ppcg.py:206-211 */
+int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int has_p);
+int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const double* X, const double* W,
+                        const double* P, const double* AX, const double* AW, const double* AP,
+                        int64_t ld, int64_t c0, double* Araw, double* Braw, void* ws,
+                        int64_t ws_bytes, void* stream);
+
+/* ---- batched subblock update (block_update ppcg.py:278-378 incl. fallback 231-275,
+ *      solve_pencil core.py:175-202) and plain batched pencils */
+int bk_pencil_max_dim(void);
+int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
+                          double* coef, double* theta, int* info, double* cscale, int force_fallback,
+                          void* stream);
+int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
+                        double* omega, double* C, int* status, void* stream);
+
+/* ---- recombination: ppcg.py:365-369 and _run_subblocks ppcg.py:521-532 (+ breakdown
+ *      flags of ppcg.py:701-705) */
+int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double* coef,
+                            const double* X, const double* W, const double* P, const double* AX,
+                            const double* AW, const double* AP, double* Xo, double* Po,
+                            double* AXo, double* APo, int64_t ld, int64_t c0,
+                            unsigned long long* flags, void* stream);
+
+/* ---- tall update GEMM Y = s.*(alpha X G + beta Z): _apply_projection ppcg.py:443-445,
+ *      residual ppcg.py:630/758 (+Jacobi ppcg.py:678 as s), CholQR core.py:99 (flags bit0:
+ *      G upper triangular), RR ppcg.py:574-577, Taylor-polar ppcg.py:477-481; optional
+ *      fused stopping metric rayleigh_ritz.py:71-92 (ksplit/nsplit/metric_out) */
+int64_t bk_tsgemm_ws_bytes(int64_t n, int N);
+int bk_tsgemm_d(int64_t n, int K, int N, double alpha, const double* X, int64_t ldx, const double* G,
+                int64_t ldg, double beta, const double* Z, int64_t ldz, double* Y, int64_t ldy,
+                const double* rowscale, int flags, void* stream);
+int bk_tsgemm_batched_d(int nprob, int64_t n, int K, int N, double alpha, const double* const* Xs,
+                        int64_t ldx, const double* const* Gs, int64_t ldg, double beta,
+                        const double* const* Zs, int64_t ldz, double* const* Ys, int64_t ldy,
+                        const double* rowscale, int flags, int ksplit, int nsplit,
+                        double* metric_out, void* ws, int64_t ws_bytes, void* stream);
+int bk_cplx_expand_d(int K, int N, const double* G, int64_t ldg, double* Gr, int64_t ldr,
+                     void* stream);
+
+/* ---- reductions: norms of ppcg.py:689-691, rayleigh_ritz.py:83-85, ppcg.py:452 */
+int64_t bk_sumsq_ws_bytes(void);
+int bk_sumsq_d(int64_t n, int m, const double* X, int64_t ldx, double* out, void* ws,
+               int64_t ws_bytes, void* stream);
+int bk_small_stats_d(int m1, int m2, const double* C, int64_t ldc, int cplx, double* out,
+                     void* stream);
+
+/* ---- Rayleigh-Ritz residual: ppcg.py:576-582 (W hand-off ppcg.py:396-397) */
+int64_t bk_rr_residual_ws_bytes(int kt);
+int bk_rr_residual_d(int64_t n, int kt, int cplx, const double* V, int64_t ldv, const double* AV,
+                     int64_t ldav, const double* omega, const double* rowscale, double* W,
+                     int64_t ldw, double* colnorm2, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---- strided column-range copy / zero (P realignment, lock_and_compact ppcg.py:399-408) */
+int bk_copy_cols(int64_t n, int w, int elem_bytes, const void* src, int64_t lds, int64_t sc0,
+                 void* dst, int64_t ldd, int64_t dc0, void* stream);
+int bk_zero_cols(int64_t n, int w, int elem_bytes, void* dst, int64_t ldd, int64_t dc0,
+                 void* stream);
+
+/* ---- periodic dense work (north-star item 5, cuSOLVER inside; context owns workspace) */
+int bk_dense_create(void** ctx, void* stream);
+int bk_dense_destroy(void* ctx);
+int bk_dense_set_stream(void* ctx, void* stream);
+/* _cholesky_upper core.py:67-83: G -> R (row-major upper), fail_col (device) = first pivot
+ * <= 1e-14 max|diag G|, or -1 */
+int bk_chol_upper_floor_d(void* ctx, int m, double* G, int64_t ldg, int* fail_col);
+int bk_chol_upper_floor_z(void* ctx, int m, double* G, int64_t ldg, int* fail_col);
+int bk_tri_inv_upper_d(void* ctx, int m, double* R, int64_t ldr);
+int bk_tri_inv_upper_z(void* ctx, int m, double* R, int64_t ldr);
+/* solve_pencil core.py:175-202 at k_total (sygvd/hegvd); status[0] = 1 if singular */
+int bk_rr_pencil_d(void* ctx, int d, double* A, int64_t lda, double* B, int64_t ldb, double* omega,
+                   double* C, int64_t ldc, int* status);
+int bk_rr_pencil_z(void* ctx, int d, double* A, int64_t lda, double* B, int64_t ldb, double* omega,
+                   double* C, int64_t ldc, int* status);
+/* np.linalg.qr(x)[0] (recovery paths ppcg.py:567, 712, 756); tmp: n*m scratch elements */
+int bk_householder_q_d(void* ctx, int64_t n, int m, double* X, int64_t ldx, double* tmp);
+int bk_householder_q_z(void* ctx, int64_t n, int m, double* X, int64_t ldx, double* tmp);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPCG_B200_H */

@@ -1,0 +1,315 @@
+"""Torch-tensor wrappers over the C ABI (include/ppcg_b200.h).
+
+Tensors are 2-D row-major CUDA tensors, possibly column-sliced views (stride (ld, 1)).
+Complex128 tensors are passed as interleaved real views: a complex n x m block with
+leading dimension ld is a real n x 2m block with leading dimension 2*ld, so every FP64
+tensor-core kernel is real; complex products are assembled by small expand/combine kernels.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import DeviceError
+
+F64 = torch.float64
+C128 = torch.complex128
+
+
+def stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _check2d(t, name):
+    if t.dim() != 2:
+        raise DeviceError(f"{name}: expected 2-D tensor, got {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise DeviceError(f"{name}: expected a CUDA tensor")
+    if t.shape[0] > 0 and t.shape[1] > 0 and t.stride(1) != 1:
+        raise DeviceError(f"{name}: inner stride must be 1 (row-major view)")
+
+
+def ld_of(t):
+    """Leading dimension (in elements of t's dtype)."""
+    if t.shape[0] <= 1:
+        return max(t.shape[1], 1) if t.dim() == 2 else 1
+    return t.stride(0)
+
+
+def real_view(t):
+    """(ptr, rows, real_cols, real_ld) of a 2-D float64/complex128 tensor view."""
+    _check2d(t, "block")
+    if t.dtype == F64:
+        return t.data_ptr(), t.shape[0], t.shape[1], ld_of(t)
+    if t.dtype == C128:
+        return t.data_ptr(), t.shape[0], 2 * t.shape[1], 2 * ld_of(t)
+    raise DeviceError(f"unsupported dtype {t.dtype}")
+
+
+class Workspace:
+    """Zero-initialised scratch shared by the split-K / ticketed reductions (stream-ordered)."""
+
+    def __init__(self, device=None, nbytes=1 << 22):
+        self.device = device or torch.device("cuda")
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes):
+        nbytes = int(nbytes)
+        if nbytes > self.buf.numel():
+            grow = max(nbytes, int(self.buf.numel() * 1.5))
+            torch.cuda.current_stream().synchronize()
+            self.buf = torch.zeros(grow, dtype=torch.uint8, device=self.device)
+        return self.buf.data_ptr(), self.buf.numel()
+
+
+_WS = {}
+
+
+def workspace():
+    dev = torch.cuda.current_device()
+    ws = _WS.get(dev)
+    if ws is None:
+        ws = _WS[dev] = Workspace(torch.device("cuda", dev))
+    return ws
+
+
+# ----------------------------------------------------------------------------- Grams
+def gram(x, y, out=None, symmetric=False):
+    """out = X^H Y (m1 x m2).  symmetric=True requires x is y (same view)."""
+    n = x.shape[0]
+    if y.shape[0] != n:
+        raise DeviceError(f"row dimensions differ: {n} vs {y.shape[0]}")
+    m1, m2 = x.shape[1], y.shape[1]
+    if out is None:
+        out = torch.empty((m1, m2), dtype=x.dtype, device=x.device)
+    if m1 == 0 or m2 == 0:
+        return out
+    if x.dtype == F64:
+        px, _, _, lx = real_view(x)
+        py, _, _, ly = real_view(y)
+        nb = _lib.load().bk_gram_ws_bytes(n, m1, m2)
+        wp, wb = workspace().get(nb)
+        _lib.call("bk_gram_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out),
+                  1 if symmetric else 0, wp, wb, stream_ptr())
+        return out
+    # complex: real Gram of the interleaved views, then combine
+    px, _, r1, lx = real_view(x)
+    py, _, r2, ly = real_view(y)
+    tmp = torch.empty((r1, r2), dtype=F64, device=x.device)
+    nb = _lib.load().bk_gram_ws_bytes(n, r1, r2)
+    wp, wb = workspace().get(nb)
+    _lib.call("bk_gram_d", n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2,
+              1 if symmetric else 0, wp, wb, stream_ptr())
+    _lib.call("bk_cplx_gram_combine_d", m1, m2, tmp.data_ptr(), r2, out.data_ptr(), ld_of(out),
+              stream_ptr())
+    return out
+
+
+def gram2(x1, y1, out1, x2, y2, out2):
+    """Two independent Grams in one launch (real only; complex falls back to two launches)."""
+    if x1.dtype != F64:
+        gram(x1, y1, out1)
+        gram(x2, y2, out2)
+        return
+    n = x1.shape[0]
+    p1, _, _, l1 = real_view(x1)
+    q1, _, _, k1 = real_view(y1)
+    p2, _, _, l2 = real_view(x2)
+    q2, _, _, k2 = real_view(y2)
+    lib = _lib.load()
+    nb = 2 * max(lib.bk_gram_ws_bytes(n, x1.shape[1], y1.shape[1]), lib.bk_gram_ws_bytes(n, x2.shape[1], y2.shape[1]))
+    wp, wb = workspace().get(nb)
+    _lib.call("bk_gram2_d", n, x1.shape[1], y1.shape[1], p1, l1, q1, k1, out1.data_ptr(), ld_of(out1),
+              x2.shape[1], y2.shape[1], p2, l2, q2, k2, out2.data_ptr(), ld_of(out2), wp, wb, stream_ptr())
+
+
+# ----------------------------------------------------------------------------- tall GEMM
+def _expand_cplx(g):
+    K, N = g.shape
+    gr = torch.empty((2 * K, 2 * N), dtype=F64, device=g.device)
+    _lib.call("bk_cplx_expand_d", K, N, g.data_ptr(), ld_of(g), gr.data_ptr(), 2 * N, stream_ptr())
+    return gr
+
+
+def tsgemm(xs, gs, ys, alpha=1.0, beta=0.0, zs=None, rowscale=None, upper=False,
+           metric=None, ksplit=0, nsplit=0):
+    """Y_b = s (.) (alpha X_b G_b + beta Z_b) for up to 4 problems with equal shapes.
+
+    ``metric`` (a 1-element float64 CUDA tensor) receives
+    sum (alpha X_0[:, :ksplit] G_0[:ksplit] + beta Z_0)[:, :nsplit]^2.
+    Y may be None for metric-only launches.  Y must not alias X.
+    """
+    nprob = len(xs)
+    x0 = xs[0]
+    n, K = x0.shape
+    N = gs[0].shape[1]
+    cplx = x0.dtype == C128
+    if cplx:
+        gs = [_expand_cplx(g) for g in gs]
+        K, N, ksplit, nsplit = 2 * K, 2 * N, 2 * ksplit, 2 * nsplit
+    xp = [real_view(x)[0] for x in xs]
+    ldx = real_view(x0)[3]
+    gp = [g.data_ptr() for g in gs]
+    ldg = ld_of(gs[0]) if gs[0].dtype == F64 else 2 * ld_of(gs[0])
+    yp = [real_view(y)[0] if y is not None else 0 for y in ys]
+    ldy = real_view(ys[0])[3] if ys[0] is not None else 1
+    if zs is not None:
+        zp = [real_view(z)[0] for z in zs]
+        ldz = real_view(zs[0])[3]
+    else:
+        zp, ldz = None, 1
+    XP, _a = _lib.ptr_array(xp)
+    GP, _b = _lib.ptr_array(gp)
+    YP, _c = _lib.ptr_array(yp)
+    ZP, _d = _lib.ptr_array(zp) if zp is not None else (None, None)
+    if metric is not None:
+        nbytes = _lib.load().bk_tsgemm_ws_bytes(n, N)
+        wp, wb = workspace().get(nbytes)
+        mp = metric.data_ptr()
+    else:
+        wp, wb, mp = None, 0, None
+    if rowscale is not None and cplx:
+        pass  # rowscale is per row: identical on the real view
+    _lib.call("bk_tsgemm_batched_d", nprob, n, K, N, float(alpha), XP, ldx, GP, ldg, float(beta), ZP,
+              ldz, YP, ldy, rowscale.data_ptr() if rowscale is not None else None,
+              1 if upper else 0, int(ksplit), int(nsplit), mp, wp, wb, stream_ptr())
+
+
+# ----------------------------------------------------------------------------- elementwise / reductions
+def scale_rows(d, x, out):
+    px, n, mr, lx = real_view(x)
+    po, _, _, lo = real_view(out)
+    _lib.call("bk_scale_rows_d", n, mr, d.data_ptr(), px, lx, po, lo, stream_ptr())
+    return out
+
+
+def sumsq(x, out):
+    """out[0] = ||x||_F^2 (deterministic)."""
+    px, n, mr, lx = real_view(x)
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.bk_sumsq_ws_bytes())
+    _lib.call("bk_sumsq_d", n, mr, px, lx, out.data_ptr(), wp, wb, stream_ptr())
+    return out
+
+
+def small_stats(c, out):
+    """out[0:3] = (||C||_F^2, ||C - I||_F^2, Re tr C)."""
+    _check2d(c, "C")
+    cplx = 1 if c.dtype == C128 else 0
+    _lib.call("bk_small_stats_d", c.shape[0], c.shape[1], c.data_ptr(), ld_of(c), cplx, out.data_ptr(),
+              stream_ptr())
+    return out
+
+
+def copy_cols(src, dst):
+    """dst[:, :] = src[:, :] for equal-shaped column views of row-major buffers."""
+    es = 16 if src.dtype == C128 else 8
+    _lib.call("bk_copy_cols", src.shape[0], src.shape[1], es, src.data_ptr(), ld_of(src), 0,
+              dst.data_ptr(), ld_of(dst), 0, stream_ptr())
+
+
+def zero_cols(dst):
+    es = 16 if dst.dtype == C128 else 8
+    _lib.call("bk_zero_cols", dst.shape[0], dst.shape[1], es, dst.data_ptr(), ld_of(dst), 0, stream_ptr())
+
+
+def rr_residual(v, av, omega, rowscale, w_out, colnorm2):
+    """R = AV - V diag(omega); w_out = s (.) R (optional); colnorm2 = ||R(:, j)||^2."""
+    n, kt = v.shape
+    cplx = 1 if v.dtype == C128 else 0
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.bk_rr_residual_ws_bytes(kt))
+    _lib.call("bk_rr_residual_d", n, kt, cplx, v.data_ptr(), ld_of(v), av.data_ptr(), ld_of(av),
+              omega.data_ptr(), rowscale.data_ptr() if rowscale is not None else None,
+              w_out.data_ptr() if w_out is not None else None,
+              ld_of(w_out) if w_out is not None else 1, colnorm2.data_ptr(), wp, wb, stream_ptr())
+
+
+# ----------------------------------------------------------------------------- operator apply
+def spmm_csr(rowptr, col, val, x, y):
+    n = y.shape[0]
+    m = x.shape[1]
+    if x.dtype == F64:
+        _lib.call("bk_spmm_csr_d", n, rowptr.data_ptr(), col.data_ptr(), val.data_ptr(), m, x.data_ptr(),
+                  ld_of(x), y.data_ptr(), ld_of(y), stream_ptr())
+    else:
+        _lib.call("bk_spmm_csr_z", n, rowptr.data_ptr(), col.data_ptr(), val.data_ptr(), m, x.data_ptr(),
+                  ld_of(x), y.data_ptr(), ld_of(y), stream_ptr())
+    return y
+
+
+# ----------------------------------------------------------------------------- subblock path
+def subblock_grams(n, k_act, q, has_p, X, W, P, AX, AW, AP, ld, c0, araw, braw):
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.bk_subblock_grams_ws_bytes(n, k_act, q, 1 if has_p else 0))
+    _lib.call("bk_subblock_grams_d", n, k_act, q, 1 if has_p else 0, X, W, P if has_p else None, AX, AW,
+              AP if has_p else None, ld, c0, araw.data_ptr(), braw.data_ptr(), wp, wb, stream_ptr())
+
+
+def subblock_pencils(k_act, q, has_p, araw, braw, coef, theta, info, cscale, force_fallback=False):
+    _lib.call("bk_subblock_pencils_d", k_act, q, 1 if has_p else 0, araw.data_ptr(), braw.data_ptr(),
+              coef.data_ptr(), theta.data_ptr(), info.data_ptr(), cscale.data_ptr(),
+              1 if force_fallback else 0, stream_ptr())
+
+
+def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags):
+    _lib.call("bk_subblock_recombine_d", n, k_act, q, 1 if has_p else 0, coef.data_ptr(), X, W,
+              P if has_p else None, AX, AW, AP if has_p else None, Xo, Po, AXo, APo, ld, c0,
+              flags.data_ptr(), stream_ptr())
+
+
+def pencil_batched(a, b, want, omega, c, status):
+    """a, b: (nb, ldm, ldm) float64; solves nb pencils of dimension ldm."""
+    nb, d, _ = a.shape
+    _lib.call("bk_pencil_batched_d", nb, d, d, a.data_ptr(), b.data_ptr(), want, omega.data_ptr(),
+              c.data_ptr(), status.data_ptr(), stream_ptr())
+
+
+# ----------------------------------------------------------------------------- dense (cuSOLVER)
+class Dense:
+    """Owns a bk_dense context (cuSOLVER handle + workspace) bound to the current stream."""
+
+    def __init__(self):
+        import ctypes
+
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.call("bk_dense_create", ctypes.byref(h), stream_ptr())
+        self.h = h
+        self._lib = lib
+
+    def _sync_stream(self):
+        _lib.call("bk_dense_set_stream", self.h, stream_ptr())
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            self._lib.bk_dense_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def chol_upper_floor(self, g, fail_col):
+        self._sync_stream()
+        name = "bk_chol_upper_floor_z" if g.dtype == C128 else "bk_chol_upper_floor_d"
+        _lib.call(name, self.h, g.shape[0], g.data_ptr(), ld_of(g), fail_col.data_ptr())
+
+    def tri_inv_upper(self, r):
+        self._sync_stream()
+        name = "bk_tri_inv_upper_z" if r.dtype == C128 else "bk_tri_inv_upper_d"
+        _lib.call(name, self.h, r.shape[0], r.data_ptr(), ld_of(r))
+
+    def rr_pencil(self, a, b, omega, c, status):
+        self._sync_stream()
+        name = "bk_rr_pencil_z" if a.dtype == C128 else "bk_rr_pencil_d"
+        _lib.call(name, self.h, a.shape[0], a.data_ptr(), ld_of(a), b.data_ptr(), ld_of(b),
+                  omega.data_ptr(), c.data_ptr(), ld_of(c), status.data_ptr())
+
+    def householder_q(self, x, tmp):
+        self._sync_stream()
+        name = "bk_householder_q_z" if x.dtype == C128 else "bk_householder_q_d"
+        _lib.call(name, self.h, x.shape[0], x.shape[1], x.data_ptr(), ld_of(x), tmp.data_ptr())

@@ -1,0 +1,658 @@
+"""PPCG block eigensolver on B200: host orchestration of the device kernels.
+
+Drop-in for ``blockeig.ppcg.ppcg_solve`` (ppcg.py:587-787): same signature, options
+(``SolverOptions``, ppcg.py:48-103), result (``SolveReport``, ppcg.py:149-163), trace
+records and exceptions.  All n-length arithmetic runs in libppcg_b200.so; the host keeps
+only the control flow of the reference loop (ppcg.py:653-758) and reads a handful of
+scalars per iteration.
+
+Device state: every block is an n x k_total row-major CUDA buffer and a
+column keeps its global position for the whole run, so
+  * [X_lock | X] is one buffer ``XF`` (locked columns lead, ppcg.py:110-112) and the full
+    basis of _full_basis / _orth_loss / _extract_ritz is a free view (no concatenation);
+  * the active block is the column range [L, k_total) of XF, AXF, W, AW, P, AP;
+  * P realignment in lock_and_compact (ppcg.py:399-408) is a zeroing of re-activated
+    columns only;
+  * X/AX and P/AP are ping-pong pairs: the subblock update, CholQR and Rayleigh-Ritz write
+    the other buffer, so the pre-update blocks survive for the breakdown and
+    rank-deficiency recoveries (ppcg.py:694-717, 456-472) without copies.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import DimensionError, RankDeficiencyError, SingularGramError
+from .trace import TraceRecord
+
+__all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSolver"]
+
+_COEFF_REFRESH = 100.0   # ppcg.py:41
+_BREAKDOWN_MAX = 1e8     # ppcg.py:705
+_TAYLOR_OK = 0.1         # core.py:127
+
+
+@dataclass
+class SolverOptions:
+    """Tunables of the PPCG iteration; identical fields, defaults and validation to
+    blockeig SolverOptions (ppcg.py:48-103)."""
+
+    k: int
+    nbuf: int | None = None
+    sbsize: int = 5
+    rr_period: float = 5
+    tol: float = 1e-6
+    trace_tol: float | None = None
+    max_iter: int = 500
+    orth_policy: str = "every"
+    orth_period: int = 1
+    orth_threshold: float = 0.1
+    orth_scheme: str = "cholesky-qr"
+    taylor_terms: int = 4
+    seed: int = 0
+    project_w: bool = True
+    project_p: bool = True
+
+    def resolved_nbuf(self):
+        if self.nbuf is not None:
+            return self.nbuf
+        return math.ceil(0.02 * self.k)
+
+    def validate(self):
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if self.nbuf is not None and self.nbuf < 0:
+            raise ValueError("nbuf must be >= 0")
+        if self.sbsize < 1:
+            raise ValueError("sbsize must be >= 1")
+        if not (self.rr_period >= 1):
+            raise ValueError("rr_period must be >= 1 (math.inf disables RR)")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if self.trace_tol is not None and self.trace_tol <= 0:
+            raise ValueError("trace_tol must be positive")
+        if self.max_iter < 0:
+            raise ValueError("max_iter must be >= 0")
+        if self.orth_policy not in ("every", "periodic", "adaptive"):
+            raise ValueError(f"unknown orth_policy {self.orth_policy!r}")
+        if self.orth_period < 1:
+            raise ValueError("orth_period must be >= 1")
+        if self.orth_scheme not in ("cholesky-qr", "taylor-polar"):
+            raise ValueError(f"unknown orth_scheme {self.orth_scheme!r}")
+
+
+@dataclass
+class SolveReport:
+    """Final eigenpairs plus the convergence record (ppcg.py:149-163)."""
+
+    values: np.ndarray
+    vectors: np.ndarray = field(repr=False)
+    trace: list
+    status: str
+    iterations: int
+    matvecs: int
+    rr_count: int
+    breakdown_recoveries: int
+    wall_ms: float
+    values_history: list = field(default_factory=list, repr=False)
+    diagnostics: dict = field(default_factory=dict, repr=False)
+
+
+def split_blocks(k_act, sbsize):
+    """Contiguous column ranges of width sbsize; the last may be narrower (ppcg.py:189-195)."""
+    if k_act < 0:
+        raise ValueError("k_act must be >= 0")
+    if sbsize < 1:
+        raise ValueError("sbsize must be >= 1")
+    return [(lo, min(lo + sbsize, k_act)) for lo in range(0, k_act, sbsize)]
+
+
+def lock_count(values, rnorms, tol):
+    """Prefix-closed convergence (detect_converged, rayleigh_ritz.py:95-108)."""
+    n = 0
+    for th, rn in zip(values, rnorms):
+        if rn <= tol * max(abs(th), 1.0):
+            n += 1
+        else:
+            break
+    return n
+
+
+def draw_initial_block(n, kt, complex_field, seed, x0=None):
+    """Host draw of X0 exactly as _initial_block (ppcg.py:414-438) before orthonormalisation:
+    numpy PCG64 normals (real block then imaginary block), x0 padded on the right."""
+    dtype = np.complex128 if complex_field else np.float64
+    rng = np.random.default_rng(seed)
+
+    def draw(cols):
+        blk = rng.standard_normal((n, cols))
+        if complex_field:
+            blk = blk + 1j * rng.standard_normal((n, cols))
+        return blk
+
+    if x0 is None:
+        return draw(kt).astype(dtype)
+    x0 = np.asarray(x0, dtype=dtype)
+    if x0.ndim != 2 or x0.shape[0] != n:
+        raise DimensionError(f"x0 must be {n} x m, got {x0.shape}")
+    if x0.shape[1] > kt:
+        raise DimensionError(f"x0 has {x0.shape[1]} columns, at most k + nbuf = {kt} allowed")
+    if not np.all(np.isfinite(x0)):
+        raise ValueError("x0 contains non-finite entries")
+    pad = kt - x0.shape[1]
+    return np.column_stack([x0, draw(pad).astype(dtype)]) if pad else x0.copy()
+
+
+class PPCGSolver:
+    """Step-wise device PPCG (``start`` / ``step`` / ``finish``), used by ``ppcg_solve`` and
+    by bench.py to time single outer iterations."""
+
+    def __init__(self, a, t=None, x0=None, opts=None, comm=None):
+        import torch
+
+        from . import kernels as K
+        from .operators import as_device_operator, as_device_preconditioner
+
+        if opts is None:
+            raise ValueError("opts is required")
+        opts.validate()
+        self.torch, self.K = torch, K
+        self.opts = opts
+        self.a = a
+        self.dev_a = as_device_operator(a)
+        self.prec = as_device_preconditioner(t)
+        self.rowscale = self.prec[1] if self.prec is not None and self.prec[0] == "diag" else None
+        self.n = int(a.n)
+        self.cplx = bool(np.issubdtype(np.dtype(a.dtype), np.complexfloating)) or self.dev_a.complex
+        self.tdt = torch.complex128 if self.cplx else torch.float64
+        self.k = opts.k
+        self.kt = opts.k + opts.resolved_nbuf()
+        if self.kt > self.n:
+            raise DimensionError(f"k + nbuf = {self.kt} exceeds operator dimension {self.n}")
+        self.x0 = x0
+        self.comm = comm
+        self.matvecs = 0
+
+    # ------------------------------------------------------------------ helpers
+    def _A(self, x, y):
+        """y = A x on device, counted in matvec units (operators.py:122-124)."""
+        self.matvecs += x.shape[1]
+        if x.shape[1]:
+            self.dev_a.apply_into(x, y)
+
+    def _precond_general(self, w):
+        if self.prec is not None and self.prec[0] == "op":
+            tmp = self.torch.empty_like(w)
+            self.prec[1].apply_into(w, tmp)
+            w.copy_(tmp)
+
+    def _fetch(self, *pairs):
+        """Copy device tensors into pinned host mirrors and synchronise once."""
+        for dev, host in pairs:
+            host.copy_(dev, non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+
+    def _alloc(self):
+        torch = self.torch
+        n, kt = self.n, self.kt
+        z = lambda *s, dt=None: torch.zeros(s, dtype=dt or self.tdt, device="cuda")  # noqa: E731
+        self.XF = [z(n, kt), z(n, kt)]
+        self.AXF = [z(n, kt), z(n, kt)]
+        self.W = z(n, kt)
+        self.AW = z(n, kt)
+        self.P = [z(n, kt), z(n, kt)]
+        self.AP = [z(n, kt), z(n, kt)]
+        self.xi = 0   # current X/AX buffer
+        self.pi = 0   # current P/AP buffer
+        self.Gm = z(kt, kt)
+        self.Gl = z(kt, kt)
+        self.Gp = z(kt, kt)
+        self.Gp2 = z(kt, kt)
+        self.Gfull = z(kt, kt)
+        self.Rm = z(kt, kt)
+        self.Ahat = z(kt, kt)
+        self.Bhat = z(kt, kt)
+        self.Cm = z(kt, kt)
+        self.omega = z(kt, dt=torch.float64)
+        self.colnorm2 = z(kt, dt=torch.float64)
+        self.stats = z(32, dt=torch.float64)
+        self.iflags = torch.full((8,), -1, dtype=torch.int32, device="cuda")
+        self.flags64 = z(3, dt=torch.int64)
+        self.h_stats = torch.zeros(32, dtype=torch.float64).pin_memory()
+        self.h_iflags = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.h_flags64 = torch.zeros(3, dtype=torch.int64).pin_memory()
+        self.h_omega = torch.zeros(kt, dtype=torch.float64).pin_memory()
+        self.h_colnorm2 = torch.zeros(kt, dtype=torch.float64).pin_memory()
+        self.rr_status = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self.h_rr_status = torch.zeros(4, dtype=torch.int32).pin_memory()
+        q = self.opts.sbsize
+        nbmax = (kt + q - 1) // q
+        dmax = 3 * q
+        self.araw = z(nbmax * dmax * dmax)
+        self.braw = z(nbmax * dmax * dmax)
+        self.coef = z(nbmax * dmax * q)
+        self.theta = z(kt, dt=torch.float64)
+        self.info = torch.zeros(nbmax * 4, dtype=torch.int32, device="cuda")
+        self.cscale = z(nbmax, dt=torch.float64)
+        self.h_info = torch.zeros(nbmax * 4, dtype=torch.int32).pin_memory()
+        self.h_cscale = torch.zeros(nbmax, dtype=torch.float64).pin_memory()
+        self.eye = torch.eye(kt, dtype=self.tdt, device="cuda")
+        from .kernels import Dense
+
+        self.dense = Dense()
+
+    # views
+    def X(self):
+        return self.XF[self.xi][:, self.L:]
+
+    def AX(self):
+        return self.AXF[self.xi][:, self.L:]
+
+    def Pa(self):
+        return self.P[self.pi][:, self.L:]
+
+    def APa(self):
+        return self.AP[self.pi][:, self.L:]
+
+    # ------------------------------------------------------------------ orthonormalisation
+    def _cholqr_inplace_swap(self, gram_act, x_src_idx):
+        """CholQR of the active block (core.py:86-100 / ppcg.py:483-484): R from the Gram
+        with the pivot floor; X <- X R^{-1}, AX <- AX R^{-1} into the other buffer; swap.
+        Raises RankDeficiencyError(column) like _cholesky_upper."""
+        K = self.K
+        L, ka = self.L, self.kt - self.L
+        R = self.Rm[:ka, :ka]
+        R.copy_(gram_act)
+        self.dense.chol_upper_floor(R, self.iflags[0:1])
+        self._fetch((self.iflags, self.h_iflags))
+        col = int(self.h_iflags[0])
+        if col >= 0:
+            raise RankDeficiencyError(col)
+        self.dense.tri_inv_upper(R)
+        src, dst = x_src_idx, 1 - x_src_idx
+        K.tsgemm([self.XF[src][:, L:], self.AXF[src][:, L:]], [R, R],
+                 [self.XF[dst][:, L:], self.AXF[dst][:, L:]], upper=True)
+        self.xi = dst
+
+    def _taylor_swap(self, gram_act):
+        """Taylor-polar correction X <- X p(G - I) (core.py:106-124, ppcg.py:477-481)."""
+        K, torch = self.K, self.torch
+        L, ka = self.L, self.kt - self.L
+        terms = self.opts.taylor_terms
+        eye = self.eye[:ka, :ka]
+        y = (gram_act - eye).contiguous()
+        cf = [1.0]
+        for i in range(1, terms + 1):
+            cf.append(-cf[-1] * (2 * i - 1) / (2 * i))
+        p = (cf[-1] * eye).contiguous()
+        for c in reversed(cf[:-1]):
+            pn = torch.empty_like(p)
+            K.tsgemm([y], [p], [pn], alpha=1.0, beta=c, zs=[eye.contiguous()])
+            p = pn
+        src, dst = self.xi, 1 - self.xi
+        K.tsgemm([self.XF[src][:, L:], self.AXF[src][:, L:]], [p, p],
+                 [self.XF[dst][:, L:], self.AXF[dst][:, L:]])
+        self.xi = dst
+
+    def _residual_w(self):
+        """W = T(AX - X (X^H AX)) (ppcg.py:630, 716, 758) with the Jacobi apply of
+        ppcg.py:678 fused as a row scale and, when no column is locked, the next
+        iteration's stopping metric fused as a partial-K snapshot."""
+        K = self.K
+        L, ka, k = self.L, self.kt - self.L, self.k
+        x, ax = self.X(), self.AX()
+        G = self.Gm[:ka, :ka]
+        K.gram(x, ax, G)
+        w = self.W[:, L:]
+        if L == 0:
+            K.tsgemm([x], [G], [w], alpha=-1.0, beta=1.0, zs=[ax], rowscale=self.rowscale,
+                     metric=self.stats[0:1], ksplit=k, nsplit=k)
+            K.small_stats(G[:k, :k], self.stats[1:4])
+            self.metric_cached = True
+        else:
+            K.tsgemm([x], [G], [w], alpha=-1.0, beta=1.0, zs=[ax], rowscale=self.rowscale)
+            self.metric_cached = False
+        self._precond_general(w)
+
+    def _householder_refresh(self):
+        """X <- qr(X)[0], AX <- A X (ppcg.py:712-713, 756-757)."""
+        L = self.L
+        x = self.X()
+        self.dense.householder_q(x, self.AW)
+        self._A(x, self.AX())
+
+    # ------------------------------------------------------------------ Rayleigh-Ritz
+    def _ritz(self, fresh):
+        """_extract_ritz (ppcg.py:553-584) over [X_lock, X].  Writes the Ritz vectors (and
+        A V) into the other X buffer and returns host (omega, colnorm2)."""
+        K = self.K
+        kt = self.kt
+        for attempt in range(2):
+            S, AS = self.XF[self.xi], self.AXF[self.xi]
+            K.gram(S, AS, self.Ahat)
+            K.gram(S, S, self.Bhat, symmetric=True)
+            self.dense.rr_pencil(self.Ahat, self.Bhat, self.omega, self.Cm, self.rr_status)
+            self._fetch((self.rr_status, self.h_rr_status))
+            if int(self.h_rr_status[0]) == 0:
+                break
+            if attempt == 1:
+                raise SingularGramError("Gram matrix numerically singular in Rayleigh-Ritz")
+            # clean the active block and retry once (ppcg.py:558-572)
+            ka = kt - self.L
+            G = self.Gm[:ka, :ka]
+            K.gram(self.X(), self.X(), G, symmetric=True)
+            try:
+                self._cholqr_inplace_swap(G, self.xi)
+            except RankDeficiencyError:
+                self._householder_refresh()
+        src, dst = self.xi, 1 - self.xi
+        V = self.XF[dst]
+        AV = self.AXF[dst]
+        if fresh:
+            K.tsgemm([S], [self.Cm], [V])
+            self._A(V, AV)
+        else:
+            K.tsgemm([S, AS], [self.Cm, self.Cm], [V, AV])
+        return src, dst
+
+    def _rr_and_lock(self):
+        K = self.K
+        kt = self.kt
+        src, dst = self._ritz(fresh=True)
+        V, AV = self.XF[dst], self.AXF[dst]
+        K.rr_residual(V, AV, self.omega, self.rowscale, self.W, self.colnorm2)
+        self._fetch((self.omega, self.h_omega), (self.colnorm2, self.h_colnorm2))
+        omega = self.h_omega.numpy().copy()
+        rn = np.sqrt(self.h_colnorm2.numpy())
+        self.rr_count += 1
+        self.values_history.append(omega.copy())
+        L_old = self.L
+        L_new = lock_count(omega, rn, self.opts.tol)
+        # lock_and_compact (ppcg.py:381-411): W <- residual (already in W, global columns)
+        if self.has_p and L_new < L_old:
+            K.zero_cols(self.P[self.pi][:, L_new:L_old])
+            K.zero_cols(self.AP[self.pi][:, L_new:L_old])
+        self.xi = dst
+        if L_new > 0:
+            K.copy_cols(self.XF[dst][:, :L_new], self.XF[src][:, :L_new])
+            K.copy_cols(self.AXF[dst][:, :L_new], self.AXF[src][:, :L_new])
+        self.L = L_new
+        self.values_lock = omega[:L_new]
+        self._precond_general(self.W[:, L_new:])
+        self.metric_cached = False
+
+    # ------------------------------------------------------------------ run
+    def start(self):
+        torch, K = self.torch, self.K
+        self._alloc()
+        self.t0 = time.perf_counter()
+        self.L = 0
+        self.has_p = False
+        self.metric_cached = False
+        x_host = draw_initial_block(self.n, self.kt, self.cplx, self.opts.seed, self.x0)
+        # cholesky_qr of the initial block (ppcg.py:437-438)
+        raw = self.XF[1]
+        raw.copy_(torch.from_numpy(np.ascontiguousarray(x_host)).to("cuda", non_blocking=False))
+        G = self.Gm
+        K.gram(raw, raw, G, symmetric=True)
+        self.xi = 1
+        self._cholqr_inplace_swap(G, 1)
+        self._A(self.X(), self.AX())
+        self._residual_w()
+        self.trace, self.values_history = [], []
+        self.orth_loss, self.proj_defect = [], []
+        self.rr_count = self.recoveries = self.refreshes = 0
+        self.prev_trace = None
+        self.status, self.iterations = "max_iter", self.opts.max_iter
+        self.it = 0
+        self.values_lock = np.zeros(0)
+        self.done = self.opts.max_iter == 0
+        return self
+
+    def _metrics(self):
+        """Stopping metrics on the leading k columns (ppcg.py:655-664)."""
+        K = self.K
+        k = self.k
+        if not self.metric_cached:
+            xl, axl = self.XF[self.xi][:, :k], self.AXF[self.xi][:, :k]
+            Gk = self.Gl[:k, :k]
+            K.gram(xl, axl, Gk)
+            K.small_stats(Gk, self.stats[1:4])
+            K.tsgemm([xl], [Gk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[0:1],
+                     ksplit=k, nsplit=k)
+        self._fetch((self.stats, self.h_stats))
+        s = self.h_stats.numpy()
+        rel = math.sqrt(max(s[0], 0.0)) / max(math.sqrt(max(s[1], 0.0)), 1e-300)
+        return float(rel), float(s[3])
+
+    def step(self):
+        """One outer iteration (ppcg.py:653-758).  Returns True once the run has stopped."""
+        if self.done:
+            return True
+        K, torch, o = self.K, self.torch, self.opts
+        it = self.it = self.it + 1
+        rel, tr = self._metrics()
+        chg = math.inf if self.prev_trace is None else abs(tr - self.prev_trace) / max(abs(tr), 1e-300)
+        self.prev_trace = tr
+        done = rel <= o.tol or (o.trace_tol is not None and chg <= o.trace_tol)
+        L, kt = self.L, self.kt
+        ka = kt - L
+        if done or ka == 0:
+            self.status, self.iterations, self.done = "converged", it - 1, True
+            return True
+        self.trace.append(TraceRecord(iteration=it, trace_value=tr, rel_resid=rel, n_locked=L,
+                                      n_matvec=self.matvecs,
+                                      wall_ms=(time.perf_counter() - self.t0) * 1e3))
+        x, ax = self.X(), self.AX()
+        w, aw = self.W[:, L:], self.AW[:, L:]
+        # W = T(W) is already applied (fused into the producer); AW = A W  (ppcg.py:678-679)
+        self._A(w, aw)
+        # projections (ppcg.py:680-687), W and P batched, X then X_lock sequentially
+        wnorm_done = False
+        p, ap = (self.Pa(), self.APa()) if self.has_p else (None, None)
+        proj_p = self.has_p and o.project_p
+        G1 = self.Gm[:ka, :ka]
+        G3 = self.Gp2[:ka, :ka]
+        if o.project_w or proj_p:
+            last_w = o.project_w and L == 0
+            if o.project_w and proj_p:
+                K.gram2(x, w, G1, x, p, G3)
+                K.tsgemm([x, self.AX(), x, self.AX()], [G1, G1, G3, G3], [w, aw, p, ap], alpha=-1.0,
+                         beta=1.0, zs=[w, aw, p, ap], metric=self.stats[4:5] if last_w else None,
+                         ksplit=ka, nsplit=ka)
+            elif o.project_w:
+                K.gram(x, w, G1)
+                K.tsgemm([x, ax], [G1, G1], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
+                         metric=self.stats[4:5] if last_w else None, ksplit=ka, nsplit=ka)
+            else:
+                K.gram(x, p, G3)
+                K.tsgemm([x, ax], [G3, G3], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+            wnorm_done = last_w
+            if L:
+                xl, axl = self.XF[self.xi][:, :L], self.AXF[self.xi][:, :L]
+                G2 = self.Gl[:L, :ka]
+                G4 = self.Gp[:L, :ka]
+                if o.project_w and proj_p:
+                    K.gram2(xl, w, G2, xl, p, G4)
+                    K.tsgemm([xl, axl, xl, axl], [G2, G2, G4, G4], [w, aw, p, ap], alpha=-1.0, beta=1.0,
+                             zs=[w, aw, p, ap], metric=self.stats[4:5], ksplit=L, nsplit=ka)
+                    wnorm_done = True
+                elif o.project_w:
+                    K.gram(xl, w, G2)
+                    K.tsgemm([xl, axl], [G2, G2], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
+                             metric=self.stats[4:5], ksplit=L, nsplit=ka)
+                    wnorm_done = True
+                else:
+                    K.gram(xl, p, G4)
+                    K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+        if not wnorm_done:
+            K.sumsq(w, self.stats[4:5])
+        # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692)
+        Gd = self.Gp[:kt, :ka]
+        K.gram(self.XF[self.xi], w, Gd)
+        K.small_stats(Gd, self.stats[5:8])
+
+        # subblock updates (ppcg.py:694-696) -> other buffers
+        q = o.sbsize
+        src, dst = self.xi, 1 - self.xi
+        psrc, pdst = self.pi, 1 - self.pi
+        XFs, AXFs = self.XF[src], self.AXF[src]
+        Ps, APs = self.P[psrc], self.AP[psrc]
+        K.subblock_grams(self.n, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
+                         AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
+                         self.araw, self.braw)
+        K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
+                           self.cscale)
+        self.flags64.zero_()
+        K.subblock_recombine(self.n, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
+                             Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
+                             self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
+                             self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64)
+        nb = (ka + q - 1) // q
+        self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
+                    (self.stats, self.h_stats))
+        s = self.h_stats.numpy()
+        wn = math.sqrt(max(s[4], 0.0))
+        self.proj_defect.append(float(math.sqrt(max(s[5], 0.0)) / max(wn, 1e-300)))
+        info = self.h_info.numpy()[: 4 * nb].reshape(nb, 4)
+        if np.any(info[:, 2] != 0):
+            raise SingularGramError("Gram matrix numerically singular in a subblock pencil")
+        self.recoveries += int(np.sum(info[:, 0]))
+        cs = max(1.0, float(np.max(self.h_cscale.numpy()[:nb])))
+        f64 = self.h_flags64.numpy()
+        mx = float(np.frombuffer(np.int64(f64[1]).tobytes(), dtype=np.float64)[0])
+        mp = float(np.frombuffer(np.int64(f64[2]).tobytes(), dtype=np.float64)[0])
+        broken = bool(f64[0] != 0) or max(mx, mp) > _BREAKDOWN_MAX
+        prev_idx, prev_pidx = src, psrc
+        if broken:
+            # ppcg.py:706-717: restore pre-update X, Householder QR, drop P
+            self.recoveries += 1
+            self.orth_loss.append(math.inf)
+            self.xi = prev_idx
+            self._householder_refresh()
+            self.has_p = False
+            self._residual_w()
+            self._check_max_iter()
+            return self.done
+        self.xi, self.pi = dst, pdst
+        self.has_p = True
+        if cs > _COEFF_REFRESH:
+            # ppcg.py:718-724: refresh the cached products with real operator applications
+            self.refreshes += 1
+            self._A(self.X(), self.AX())
+            self._A(self.Pa(), self.APa())
+        # orthonormality loss of [X_lock, X] (ppcg.py:726-729)
+        K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
+        K.small_stats(self.Gfull, self.stats[8:11])
+        self._fetch((self.stats, self.h_stats))
+        loss = float(math.sqrt(max(self.h_stats.numpy()[9], 0.0)))
+        self.orth_loss.append(loss)
+        gact = self.Gfull[L:, L:]
+        if math.isfinite(o.rr_period) and it % int(o.rr_period) == 0:
+            self._rr_and_lock()
+        else:
+            do = (o.orth_policy == "every"
+                  or (o.orth_policy == "periodic" and it % o.orth_period == 0)
+                  or (o.orth_policy == "adaptive" and loss >= o.orth_threshold))
+            if do:
+                try:
+                    self._orth(gact, loss)
+                except RankDeficiencyError as err:
+                    self.recoveries += 1
+                    self._redo_without_p(prev_idx, prev_pidx, err.column)
+                    try:
+                        K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
+                        self._orth(self.Gfull[L:, L:], loss)
+                    except RankDeficiencyError:
+                        self._householder_refresh()
+            self._residual_w()
+        self._check_max_iter()
+        return self.done
+
+    def _orth(self, gact, loss):
+        """_orth_active (ppcg.py:475-484)."""
+        if self.opts.orth_scheme == "taylor-polar" and loss <= _TAYLOR_OK:
+            self._taylor_swap(gact)
+        else:
+            self._cholqr_inplace_swap(gact, self.xi)
+
+    def _redo_without_p(self, prev_idx, prev_pidx, column):
+        """_redo_subblock_without_p (ppcg.py:456-472): fallback_steepest_descent on the
+        pre-update subblock owning ``column``, written into the current buffers."""
+        K = self.K
+        q, L = self.opts.sbsize, self.L
+        ka = self.kt - L
+        lo = None
+        for a, b in split_blocks(ka, q):
+            if a <= column < b:
+                lo, hi = a, b
+        if lo is None:
+            raise RankDeficiencyError(column, "failing column outside the active partition")
+        w = hi - lo
+        c0 = self._c0r(L + lo)
+        XFp, AXFp = self.XF[prev_idx], self.AXF[prev_idx]
+        K.subblock_grams(self.n, w, w, False, XFp.data_ptr(), self.W.data_ptr(), 0, AXFp.data_ptr(),
+                         self.AW.data_ptr(), 0, self._ldr(), c0, self.araw, self.braw)
+        K.subblock_pencils(w, w, False, self.araw, self.braw, self.coef, self.theta, self.info, self.cscale,
+                           force_fallback=True)
+        self.flags64.zero_()
+        K.subblock_recombine(self.n, w, w, False, self.coef, XFp.data_ptr(), self.W.data_ptr(), 0,
+                             AXFp.data_ptr(), self.AW.data_ptr(), 0, self.XF[self.xi].data_ptr(),
+                             self.P[self.pi].data_ptr(), self.AXF[self.xi].data_ptr(),
+                             self.AP[self.pi].data_ptr(), self._ldr(), c0, self.flags64)
+        self._fetch((self.info, self.h_info))
+        if int(self.h_info.numpy()[2]) != 0:
+            raise SingularGramError("Gram matrix numerically singular in fallback pencil")
+
+    def _ldr(self):
+        return self.kt  # all state buffers share ld = k_total (complex: in complex elements)
+
+    def _c0r(self, c):
+        return c
+
+    def _check_max_iter(self):
+        if self.it >= self.opts.max_iter:
+            self.done = True
+
+    def finish(self):
+        """Final extraction (ppcg.py:760-787) and the host report."""
+        K, torch = self.K, self.torch
+        wall = (time.perf_counter() - self.t0) * 1e3
+        k = self.k
+        src, dst = self._ritz(fresh=False)
+        V, AV = self.XF[dst][:, :k], self.AXF[dst][:, :k]
+        K.rr_residual(V, AV, self.omega, None, None, self.colnorm2)
+        self.rr_count += 1
+        self._fetch((self.omega, self.h_omega), (self.colnorm2, self.h_colnorm2))
+        values = self.h_omega.numpy()[:k].copy()
+        rn = np.sqrt(self.h_colnorm2.numpy()[:k]).tolist()
+        vectors = V.cpu().numpy()
+        self.xi = dst
+        inc = [b.iteration for a_, b in zip(self.trace, self.trace[1:]) if b.trace_value > a_.trace_value]
+        self.dense.close()
+        return SolveReport(values=values, vectors=vectors, trace=self.trace, status=self.status,
+                           iterations=self.iterations, matvecs=self.matvecs, rr_count=self.rr_count,
+                           breakdown_recoveries=self.recoveries, wall_ms=wall,
+                           values_history=self.values_history,
+                           diagnostics={"orth_loss": self.orth_loss, "proj_defect": self.proj_defect,
+                                        "final_residual_norms": rn, "cache_refreshes": self.refreshes,
+                                        "trace_increases": inc})
+
+
+def ppcg_solve(a, t=None, x0=None, opts=None, threads=1):
+    """Lowest eigenpairs of a Hermitian operator with PPCG on the GPU.
+
+    Same contract as blockeig.ppcg.ppcg_solve (ppcg.py:587-614); ``threads`` is accepted
+    for API compatibility and has no effect (results are identical for any value).
+    """
+    if opts is None:
+        raise ValueError("opts is required")
+    opts.validate()
+    s = PPCGSolver(a, t, x0, opts).start()
+    while not s.step():
+        pass
+    return s.finish()

@@ -1,0 +1,297 @@
+"""Kernel-level parity of the sm_100a kernels against the CPU oracle (numpy restatement of
+the reference's block_inner / SparseHermitian.apply / block_update / solve_pencil /
+cholesky_qr).  Tolerances are stated per test; all arithmetic is fp64."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import ppcg_oracle as O
+from util import gauss, hpd_matrix, orthonormal, sym_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, torch):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("n,m1,m2", [(1, 1, 1), (7, 3, 5), (1000, 66, 66), (4096, 523, 523), (50000, 70, 130),
+                                     (3000, 1, 200)])
+def test_gram_matches_numpy(cuda, n, m1, m2):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    x, y = gauss(n, m1, 1), gauss(n, m2, 2)
+    c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    ref = O.herm_gram(x, y)
+    # fp64 rounding: |err| <= c * n * eps * |x||y| (block_inner vs triple loop bar is 1e-14 rel)
+    scale = np.sqrt(n) * np.abs(x).max() * np.abs(y).max()
+    assert np.max(np.abs(c - ref)) <= 1e-13 * max(scale, 1.0) * np.sqrt(n)
+
+
+def test_gram_column_views_and_symmetric(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, kt = 20000, 91
+    buf = gauss(n, kt, 3)
+    tb = dev(buf, torch)
+    for lo in (0, 5, 17):
+        v = tb[:, lo:]
+        g = K.gram(v, v, symmetric=True).cpu().numpy()
+        ref = buf[:, lo:].T @ buf[:, lo:]
+        assert np.array_equal(g, g.T)
+        assert np.max(np.abs(g - ref)) <= 1e-11 * np.max(np.abs(ref))
+    # determinism: bitwise identical reruns
+    g1 = K.gram(tb[:, 3:], tb[:, 7:]).cpu().numpy()
+    g2 = K.gram(tb[:, 3:], tb[:, 7:]).cpu().numpy()
+    assert np.array_equal(g1, g2)
+
+
+def test_complex_gram(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    x, y = gauss(3000, 13, 4, True), gauss(3000, 9, 5, True)
+    c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    ref = x.conj().T @ y
+    assert np.max(np.abs(c - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("n,K_,N", [(1, 1, 1), (130, 7, 9), (10000, 66, 66), (110592, 64, 523), (5000, 200, 3)])
+def test_tsgemm_residual_rowscale(cuda, n, K_, N):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    x, g, z = gauss(n, K_, 6), gauss(K_, N, 7), gauss(n, N, 8)
+    d = 1.0 + np.random.default_rng(9).random(n)
+    y = torch.empty((n, N), dtype=torch.float64, device="cuda")
+    K.tsgemm([dev(x, torch)], [dev(g, torch)], [y], alpha=-1.0, beta=1.0, zs=[dev(z, torch)],
+             rowscale=dev(d, torch))
+    ref = d[:, None] * (z - x @ g)
+    assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref))) * np.sqrt(K_)
+
+
+def test_tsgemm_metric_split_and_upper(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m, k = 20000, 70, 64
+    x, ax = gauss(n, m, 10), gauss(n, m, 11)
+    g = x.T @ ax
+    metric = torch.zeros(1, dtype=torch.float64, device="cuda")
+    w = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    K.tsgemm([dev(x, torch)], [dev(g, torch)], [w], alpha=-1.0, beta=1.0, zs=[dev(ax, torch)], metric=metric,
+             ksplit=k, nsplit=k)
+    ref_metric = np.linalg.norm(ax[:, :k] - x[:, :k] @ g[:k, :k], "fro") ** 2
+    assert abs(metric.item() - ref_metric) <= 1e-10 * ref_metric
+    assert np.max(np.abs(w.cpu().numpy() - (ax - x @ g))) <= 1e-9
+    # upper-triangular skip
+    r = np.triu(gauss(m, m, 12))
+    y = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    K.tsgemm([dev(x, torch)], [dev(r, torch)], [y], upper=True)
+    assert np.max(np.abs(y.cpu().numpy() - x @ r)) <= 1e-11 * np.max(np.abs(x @ r))
+
+
+def test_spmm_matches_scipy(cuda):
+    from paper_1407_7506_b200 import kernels as K
+    from paper_1407_7506_b200.operators import DeviceCsr
+    from paper_1407_7506_b200.problems import config_problem
+
+    torch = cuda
+    a, _, _, _ = config_problem(2, N=20)
+    csr = a._csr
+    dc = DeviceCsr(csr)
+    for m in (1, 31, 66, 300):
+        x = gauss(csr.shape[0], m, 13)
+        y = torch.empty((csr.shape[0], m), dtype=torch.float64, device="cuda")
+        dc.apply_into(dev(x, torch), y)
+        ref = csr @ x
+        assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-13 * np.max(np.abs(ref))
+    # complex operator (Peierls structure)
+    b, _, _, _ = config_problem(5, N=8)
+    dz = DeviceCsr(b._csr)
+    x = gauss(b.n, 20, 14, True)
+    y = torch.empty((b.n, 20), dtype=torch.complex128, device="cuda")
+    dz.apply_into(dev(x, torch), y)
+    ref = b._csr @ x
+    assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("d,want", [(1, 1), (6, 2), (24, 8), (65, 17), (96, 32)])
+def test_pencil_batched_vs_oracle(cuda, d, want):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    nb = 3
+    A = np.stack([sym_matrix(d, 20 + i) for i in range(nb)])
+    B = np.stack([hpd_matrix(d, 30 + i) for i in range(nb)])
+    om = torch.zeros((nb, want), dtype=torch.float64, device="cuda")
+    C = torch.zeros((nb, d, want), dtype=torch.float64, device="cuda")
+    st = torch.zeros((nb, 4), dtype=torch.int32, device="cuda")
+    K.pencil_batched(dev(A, torch), dev(B, torch), want, om, C, st)
+    om, C, st = om.cpu().numpy(), C.cpu().numpy(), st.cpu().numpy()
+    for i in range(nb):
+        assert st[i, 2] == 0
+        w_ref, _ = O.solve_small_pencil(A[i], B[i], want)
+        assert np.allclose(om[i], w_ref, atol=1e-12 * max(1.0, np.max(np.abs(w_ref))), rtol=0)
+        # B-orthonormality and eigen-equation (core.py:167-172 contract)
+        Bs = 0.5 * (B[i] + B[i].T)
+        As = 0.5 * (A[i] + A[i].T)
+        assert np.allclose(C[i].T @ Bs @ C[i], np.eye(want), atol=1e-11)
+        assert np.allclose(As @ C[i], Bs @ C[i] * om[i][None, :], atol=1e-10 * max(1, np.abs(As).max()))
+
+
+def test_pencil_singular_detected(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    d = 6
+    v = gauss(d, 3, 40)
+    B = v @ v.T  # rank 3
+    A = sym_matrix(d, 41)
+    om = torch.zeros((1, 2), dtype=torch.float64, device="cuda")
+    C = torch.zeros((1, d, 2), dtype=torch.float64, device="cuda")
+    st = torch.zeros((1, 4), dtype=torch.int32, device="cuda")
+    K.pencil_batched(dev(A[None], torch), dev(B[None], torch), 2, om, C, st)
+    assert st.cpu().numpy()[0, 2] == 1
+    with pytest.raises(O.OracleSingularGram):
+        O.solve_small_pencil(A, B, 2)
+
+
+def _device_block_update(torch, x, w, p, ax, aw, ap, q, force_fallback=False):
+    """Run bk_subblock_grams/pencils/recombine on one set of subblocks."""
+    from paper_1407_7506_b200 import kernels as K
+
+    n, m = x.shape
+    has_p = p is not None
+    bufs = [dev(b, torch) if b is not None else torch.zeros_like(dev(x, torch)) for b in (x, w, p, ax, aw, ap)]
+    outs = [torch.zeros_like(bufs[0]) for _ in range(4)]
+    nb = (m + q - 1) // q
+    dmax = (3 if has_p else 2) * q
+    araw = torch.zeros(nb * dmax * dmax, dtype=torch.float64, device="cuda")
+    braw = torch.zeros_like(araw)
+    coef = torch.zeros(nb * dmax * q, dtype=torch.float64, device="cuda")
+    theta = torch.zeros(m, dtype=torch.float64, device="cuda")
+    info = torch.zeros(nb * 4, dtype=torch.int32, device="cuda")
+    cs = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(3, dtype=torch.int64, device="cuda")
+    ptr = [b.data_ptr() for b in bufs]
+    K.subblock_grams(n, m, q, has_p, *ptr, m, 0, araw, braw)
+    K.subblock_pencils(m, q, has_p, araw, braw, coef, theta, info, cs, force_fallback=force_fallback)
+    K.subblock_recombine(n, m, q, has_p, coef, *ptr, *[o.data_ptr() for o in outs], m, 0, flags)
+    return [o.cpu().numpy() for o in outs], theta.cpu().numpy(), info.cpu().numpy().reshape(nb, 4), cs.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,m,q,with_p", [(40, 2, 2, True), (500, 24, 8, True), (500, 24, 8, False),
+                                          (2000, 66, 8, True), (3000, 70, 32, True), (3000, 45, 32, False)])
+def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
+    torch = cuda
+    a = sym_matrix(n, 50)
+    x = orthonormal(n, m, 51)
+    w = gauss(n, m, 52)
+    w -= x @ (x.T @ w)
+    p = None
+    if with_p:
+        p = gauss(n, m, 53)
+        p -= x @ (x.T @ p)
+        p *= 1e-2
+    ax, aw = a @ x, a @ w
+    ap = a @ p if with_p else None
+    (xo, po, axo, apo), theta, info, cs = _device_block_update(torch, x, w, p, ax, aw, ap, q)
+    for lo, hi in O.partition(m, q):
+        r = O.subblock_update(x[:, lo:hi], w[:, lo:hi], None if p is None else p[:, lo:hi],
+                              ax[:, lo:hi], aw[:, lo:hi], None if ap is None else ap[:, lo:hi])
+        j = lo // q
+        assert info[j, 2] == 0 and info[j, 0] == int(r.used_fallback)
+        assert np.allclose(theta[lo:hi], r.theta, atol=1e-11 * max(1, np.abs(r.theta).max()), rtol=0)
+        # eigenvector signs are arbitrary: compare the spans column by column up to sign
+        for c in range(hi - lo):
+            s = np.sign(np.dot(xo[:, lo + c], r.x[:, c])) or 1.0
+            assert np.allclose(s * xo[:, lo + c], r.x[:, c], atol=1e-9)
+            assert np.allclose(s * po[:, lo + c], r.p[:, c], atol=1e-9)
+        aps = aw[:, lo:hi] @ r.c_w
+        if r.c_p.shape[0] and ap is not None:
+            aps = aps + ap[:, lo:hi] @ r.c_p
+        axr = ax[:, lo:hi] @ r.c_x + aps
+        for c in range(hi - lo):
+            s = np.sign(np.dot(xo[:, lo + c], r.x[:, c])) or 1.0
+            assert np.allclose(s * axo[:, lo + c], axr[:, c], atol=1e-8 * max(1, np.abs(axr).max()))
+        assert abs(cs[j] - r.coeff_scale) <= 1e-8 * r.coeff_scale
+
+
+def test_subblock_engineered_fallback(cuda):
+    """alpha = 0 case of test_ppcg.py:108-117: x an exact eigenvector, w a lower one."""
+    torch = cuda
+    a = np.diag([1.0, 2.0])
+    x = np.eye(2)[:, 1:2]
+    w = np.eye(2)[:, 0:1]
+    (xo, po, axo, apo), theta, info, cs = _device_block_update(torch, x, w, None, a @ x, a @ w, None, 1)
+    assert info[0, 0] == 1  # used_fallback
+    assert np.linalg.svd(xo, compute_uv=False)[-1] > 1e-8
+    assert abs(theta[0] - 1.0) <= 1e-14
+
+
+def test_subblock_zero_w_passthrough(cuda):
+    torch = cuda
+    a = np.diag([1.0, 2.0, 3.0])
+    x = np.eye(3)[:, :2]
+    (xo, po, axo, apo), theta, info, cs = _device_block_update(torch, x, np.zeros((3, 2)), None, a @ x,
+                                                               np.zeros((3, 2)), None, 2)
+    assert np.array_equal(xo, x)
+    assert np.allclose(theta, [1.0, 2.0])
+    assert info[0, 1] == 1 and info[0, 0] == 0
+
+
+def test_forced_fallback_matches_oracle(cuda):
+    torch = cuda
+    n, m = 300, 6
+    a = sym_matrix(n, 60)
+    x = orthonormal(n, m, 61)
+    w = 50.0 * gauss(n, m, 62)
+    w -= x @ (x.T @ w)
+    (xo, po, axo, apo), theta, info, cs = _device_block_update(torch, x, w, None, a @ x, a @ w, None, m,
+                                                               force_fallback=True)
+    r = O.steepest_fallback(x, w, a @ x, a @ w)
+    assert info[0, 0] == 1
+    assert np.allclose(theta, r.theta, atol=1e-10 * np.abs(r.theta).max())
+
+
+def test_dense_cholqr_and_rr_pencil(cuda):
+    from paper_1407_7506_b200 import kernels as K
+    from paper_1407_7506_b200.errors import RankDeficiencyError  # noqa: F401
+
+    torch = cuda
+    D = K.Dense()
+    x = gauss(4000, 40, 70)
+    g = x.T @ x
+    r = torch.from_numpy(g.copy()).cuda()
+    fail = torch.full((1,), -5, dtype=torch.int32, device="cuda")
+    D.chol_upper_floor(r, fail)
+    assert fail.item() == -1
+    r_ref = O.chol_upper_with_floor(g)
+    assert np.allclose(r.cpu().numpy(), r_ref, atol=1e-10 * np.abs(r_ref).max())
+    # rank-deficient Gram reports the failing column (test_core.py:115-120 analogue)
+    xd = x.copy()
+    xd[:, 2] = xd[:, 0] + xd[:, 1]
+    gd = xd.T @ xd
+    rd = torch.from_numpy(gd.copy()).cuda()
+    D.chol_upper_floor(rd, fail)
+    with pytest.raises(O.OracleRankDeficiency) as e:
+        O.chol_upper_with_floor(gd)
+    assert fail.item() == e.value.column == 2
+    # RR pencil vs oracle
+    d = 70
+    A, B = sym_matrix(d, 71), hpd_matrix(d, 72)
+    At, Bt = torch.from_numpy(A.copy()).cuda(), torch.from_numpy(B.copy()).cuda()
+    om = torch.zeros(d, dtype=torch.float64, device="cuda")
+    C = torch.zeros((d, d), dtype=torch.float64, device="cuda")
+    st = torch.zeros(4, dtype=torch.int32, device="cuda")
+    D.rr_pencil(At, Bt, om, C, st)
+    w_ref, c_ref = O.solve_small_pencil(A, B, d)
+    assert st[0].item() == 0
+    assert np.allclose(om.cpu().numpy(), w_ref, atol=1e-11 * np.abs(w_ref).max())
+    Cn = C.cpu().numpy()
+    assert np.allclose(Cn.T @ (0.5 * (B + B.T)) @ Cn, np.eye(d), atol=1e-10)
+    D.close()

@@ -1,0 +1,162 @@
+"""Solver-level parity of the device PPCG against the CPU oracle (numpy restatement of the
+reference ppcg_solve) and against the reference's own solver-level tests
+(test_ppcg.py::TestPpcgSolve, test_acceptance.py) replayed on the device solver."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ppcg_oracle as O
+from util import HostCsr, HostDense, HostDiag, sine_angle
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve_both(a_dev, a_host, t_dev, t_host, opts, x0=None):
+    from paper_1407_7506_b200 import ppcg_solve
+
+    rep = ppcg_solve(a_dev, t_dev, x0=x0, opts=opts)
+    ref = O.oracle_solve(a_host, t_host, x0=x0, opts=opts)
+    return rep, ref
+
+
+def test_config1_parity_vs_oracle(cuda):
+    """BASELINE config 1 (2-D 5-pt 64^2 + V, k=64, q=8, Jacobi, tol 1e-6), same seeded X0."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+
+    a, k, q, tol = config_problem(1)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=2000)
+    rep, ref = _solve_both(a, HostCsr(a._csr), t, HostDiag(t.d), opts)
+    assert rep.status == ref.status == "converged"
+    # trajectory parity: same iteration count (+-1) and lock schedule
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert rep.rr_count in (ref.rr_count, ref.rr_count + 1, ref.rr_count - 1)
+    # eigenvalues: relative 1e-10
+    assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-10
+    # subspace: max principal angle (sine form) <= 1e-6 vs the oracle's converged subspace
+    assert sine_angle(ref.vectors, rep.vectors) <= 1e-6
+    # residual criterion in the reference's own metric
+    assert rep.trace[-1].rel_resid > opts.tol
+    assert max(rep.diagnostics["proj_defect"]) <= 1e-10
+    n = min(len(rep.trace), len(ref.trace), 40)
+    for r1, r2 in zip(rep.trace[:n], ref.trace[:n]):
+        assert r1.n_locked == r2.n_locked
+        assert r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-12 * abs(r2.trace_value)
+
+
+def test_laplacian_analytic_spectrum(cuda):
+    from paper_1407_7506_b200 import SolverOptions, laplacian_1d, ppcg_solve
+
+    n, k = 500, 10
+    rep = ppcg_solve(laplacian_1d(n), opts=SolverOptions(k=k, tol=1e-6, seed=0, max_iter=2000))
+    analytic = 2.0 - 2.0 * np.cos(np.arange(1, k + 1) * np.pi / (n + 1))
+    assert rep.status == "converged"
+    assert np.allclose(rep.values, analytic, atol=1e-8)
+
+
+def test_jacobi_preconditioned_laplacian(cuda):
+    from paper_1407_7506_b200 import SolverOptions, jacobi_preconditioner, laplacian_1d, ppcg_solve
+
+    n, k = 300, 6
+    a = laplacian_1d(n)
+    rep = ppcg_solve(a, jacobi_preconditioner(a), opts=SolverOptions(k=k, tol=1e-7, seed=0, max_iter=1500))
+    analytic = 2.0 - 2.0 * np.cos(np.arange(1, k + 1) * np.pi / (n + 1))
+    assert rep.status == "converged"
+    assert np.allclose(rep.values, analytic, atol=1e-8)
+
+
+def test_random_sparse_matches_oracle_trajectory(cuda):
+    from paper_1407_7506_b200 import SolverOptions, random_hermitian
+
+    a = random_hermitian(90, 0.25, seed=17)
+    opts = SolverOptions(k=6, sbsize=2, tol=1e-9, seed=9, max_iter=80)
+    rep, ref = _solve_both(a, HostCsr(a._csr), None, None, opts)
+    assert rep.status == ref.status
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert np.allclose(rep.values, ref.values, rtol=1e-10, atol=1e-12)
+
+
+def test_determinism_bitwise(cuda):
+    """test_ppcg.py:325-341: reruns (and any `threads`) are bitwise identical."""
+    from paper_1407_7506_b200 import SolverOptions, ppcg_solve, random_hermitian
+
+    a = random_hermitian(90, 0.25, seed=17)
+
+    def run(threads):
+        return ppcg_solve(a, opts=SolverOptions(k=6, sbsize=2, tol=1e-9, seed=9, max_iter=80), threads=threads)
+
+    r1, r2, r4 = run(1), run(1), run(4)
+    for other in (r2, r4):
+        assert len(r1.trace) == len(other.trace)
+        for t1, t2 in zip(r1.trace, other.trace):
+            assert t1.trace_value == t2.trace_value and t1.rel_resid == t2.rel_resid
+            assert t1.n_locked == t2.n_locked and t1.n_matvec == t2.n_matvec
+        assert np.array_equal(r1.values, other.values)
+        assert np.array_equal(r1.vectors, other.vectors)
+
+
+def test_dense_diag_problem(cuda):
+    from paper_1407_7506_b200 import DenseHermitian, DiagonalOperator, SolverOptions, ppcg_solve
+
+    a = DenseHermitian(np.diag(np.arange(1.0, 101.0)))
+    opts = SolverOptions(k=5, nbuf=2, sbsize=1, rr_period=5, tol=1e-8, seed=3, max_iter=400)
+    rep = ppcg_solve(a, DiagonalOperator(np.ones(100)), opts=opts)
+    assert rep.status == "converged"
+    assert np.allclose(rep.values, [1, 2, 3, 4, 5], atol=1e-7)
+
+
+def test_exact_invariant_start(cuda):
+    from paper_1407_7506_b200 import DenseHermitian, SolverOptions, ppcg_solve
+
+    a = DenseHermitian(np.diag(np.arange(1.0, 11.0)))
+    rep = ppcg_solve(a, x0=np.eye(10)[:, :2], opts=SolverOptions(k=2, nbuf=0, tol=1e-10))
+    assert rep.status == "converged" and rep.iterations == 0 and len(rep.trace) == 0
+    assert np.allclose(rep.values, [1.0, 2.0], atol=1e-12)
+
+
+def test_max_iter_zero_and_trace_rows(cuda):
+    from paper_1407_7506_b200 import SolverOptions, ppcg_solve, random_hermitian
+
+    a = random_hermitian(30, 0.5, seed=18)
+    rep = ppcg_solve(a, opts=SolverOptions(k=3, tol=1e-12, seed=1, max_iter=0))
+    assert rep.status == "max_iter" and rep.iterations == 0 and len(rep.trace) == 0
+    assert rep.values.shape == (3,)
+    b = random_hermitian(50, 0.4, seed=15)
+    rep = ppcg_solve(b, opts=SolverOptions(k=4, tol=1e-20, seed=7, max_iter=9))
+    assert rep.status == "max_iter" and rep.iterations == 9 and len(rep.trace) == 9
+
+
+def test_rr_period_inf(cuda):
+    from paper_1407_7506_b200 import DenseHermitian, SolverOptions, ppcg_solve
+
+    a = DenseHermitian(np.diag(np.arange(1.0, 41.0)))
+    rep = ppcg_solve(a, opts=SolverOptions(k=3, nbuf=0, rr_period=math.inf, tol=1e-8, seed=2, max_iter=60))
+    assert rep.rr_count == 1 and len(rep.values_history) == 0
+
+
+def test_policies_and_taylor(cuda):
+    from paper_1407_7506_b200 import SolverOptions, ppcg_solve, random_hermitian
+
+    a = random_hermitian(80, 0.3, seed=13)
+    w_ref = np.linalg.eigvalsh(a.to_dense())[:4]
+    rep = ppcg_solve(a, opts=SolverOptions(k=4, tol=1e-8, seed=5, max_iter=300, orth_scheme="taylor-polar"))
+    assert rep.status == "converged" and np.allclose(rep.values, w_ref, atol=1e-7)
+    b = random_hermitian(80, 0.3, seed=14)
+    w_ref = np.linalg.eigvalsh(b.to_dense())[:4]
+    rep = ppcg_solve(b, opts=SolverOptions(k=4, tol=1e-8, seed=6, max_iter=400, orth_policy="adaptive"))
+    assert rep.status == "converged" and np.allclose(rep.values, w_ref, atol=1e-7)
+
+
+def test_well_problem_golden_iterations(cuda):
+    """Acceptance C3/C5 golden counts (test_acceptance.py:30-36): 14 and 21 iterations."""
+    from paper_1407_7506_b200 import SolverOptions, jacobi_preconditioner, ppcg_solve, well_problem
+
+    a = well_problem(8, 8, 8, depth=80.0, seed=3)
+    t = jacobi_preconditioner(a, shift=-90.0)
+    rep = ppcg_solve(a, t, opts=SolverOptions(k=10, nbuf=2, sbsize=5, rr_period=5, tol=1e-4, seed=1, max_iter=140))
+    assert rep.status == "converged" and rep.iterations <= 14
+    rep5 = ppcg_solve(a, t, opts=SolverOptions(k=10, nbuf=2, sbsize=5, rr_period=5, tol=1e-6, seed=1, max_iter=210))
+    assert rep5.status == "converged" and rep5.iterations <= 21
