@@ -1,0 +1,378 @@
+"""Benchmark of the B200-native PPCG hot path (one JSON line on rank 0).
+
+Workload: BASELINE.json config 2 — 3-D 7-point Laplacian 48^3 + 8 Gaussian wells
+(n = 110,592, fp64 CSR), k = 512 (k_total = 523), sbsize q = 32, Jacobi preconditioner,
+tol 1e-6; seeded synthetic inputs.  One "step" = one PPCG outer
+iteration (ppcg.py:653-758 of the reference), Rayleigh-Ritz every 5th as in the reference
+default, so K steps mix RR and non-RR iterations in the reference's proportion.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+--impl reference times the CPU oracle (numpy restatement of the reference, oracle/) on the
+host cores with all BLAS threads; under torchrun only rank 0 works.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPCG iterations/s (config 2: 48^3 7-pt + wells, n=110592, k=512, q=32, fp64)"
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    try:
+        d = json.load(open(p))
+        return float(d["fp64_peak_tflops_for_roofline"]), "measured cuBLAS DGEMM 8192^3 sustained (profiles/fp64_peak_r01.json)"
+    except Exception:
+        return 35.44, "fallback: round-1 measured cuBLAS DGEMM"
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch for `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def build_problem(cfg):
+    from paper_1407_7506_b200.problems import config_problem, jacobi_preconditioner
+
+    a, k, q, tol = config_problem(cfg)
+    return a, jacobi_preconditioner(a), k, q, tol
+
+
+def cfg_dict(cfg, n, k, q, kt, extra=None):
+    d = {"workload": f"BASELINE config {cfg}", "n": n, "k": k, "k_total": kt, "sbsize": q,
+         "operator": "CSR fp64 (7-pt 48^3 + wells)" if cfg == 2 else f"config {cfg}",
+         "preconditioner": "Jacobi", "rr_period": 5, "tol": 1e-6 if cfg <= 3 else 1e-5,
+         "l2": "inputs larger than L2 (state ~10 x n x k_total x 8 B >> 126 MB)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from threadpoolctl import threadpool_info
+
+    from oracle.ppcg_oracle import OracleRun
+    from paper_1407_7506_b200.ppcg import SolverOptions
+
+    a, t, k, q, tol = build_problem(args.config)
+
+    class HostCsr:
+        def __init__(self, csr):
+            self.csr, self.n, self.dtype = csr, csr.shape[0], csr.dtype
+
+        def apply(self, b):
+            return self.csr @ b
+
+    class HostDiag:
+        def __init__(self, d):
+            self.d = d
+
+        def apply(self, b):
+            return self.d[:, None] * b
+
+    cores = len(os.sched_getaffinity(0)) or 1
+    opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=10 ** 6)
+    run = OracleRun(HostCsr(a._csr), HostDiag(t.d), None, opts, blas_threads=cores).start()
+    for _ in range(args.warmup):
+        run.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run.step()
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    blas = [f"{i.get('internal_api')}:{i.get('num_threads')}" for i in threadpool_info()]
+    line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config 2)",
+            "config": cfg_dict(args.config, a.n, k, q, run.kt), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.warmup} untimed + {args.steps} timed PPCG iterations of config "
+                                       f"{args.config} by the numpy oracle (BLAS {blas})"},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def event_time(torch, fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def kernel_rooflines(torch, s):
+    """Time the dominant kernels on the live solver state (CUDA events, launching stream)."""
+    from paper_1407_7506_b200 import kernels as K
+
+    n, kt, L = s.n, s.kt, s.L
+    ka = kt - L
+    x, ax, w, aw = s.X(), s.AX(), s.W[:, L:], s.AW[:, L:]
+    G = s.Gm[:ka, :ka]
+    out = {}
+    ms = event_time(torch, lambda: K.gram(x, ax, G), 10)
+    out["gram"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9, "flops_per_launch": 2.0 * n * ka * ka}
+    tmp = torch.empty_like(s.W)[:, L:]
+    ms = event_time(torch, lambda: K.tsgemm([x], [G], [tmp], alpha=-1.0, beta=1.0, zs=[ax]), 10)
+    out["tsgemm"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9}
+    nnz = s.dev_a.nnz
+    ms = event_time(torch, lambda: s.dev_a.apply_into(w, aw), 10)
+    byts = 2.0 * n * ka * 8 + nnz * 12 + 4 * (n + 1)
+    out["spmm"] = {"ms": ms, "gbs": byts / ms / 1e6, "bytes_per_launch": byts}
+    q = s.opts.sbsize
+    ms = event_time(torch, lambda: K.subblock_grams(n, ka, q, True, s.XF[s.xi].data_ptr(), s.W.data_ptr(),
+                                                    s.P[s.pi].data_ptr(), s.AXF[s.xi].data_ptr(),
+                                                    s.AW.data_ptr(), s.AP[s.pi].data_ptr(), kt, L, s.araw,
+                                                    s.braw), 5)
+    nb = (ka + q - 1) // q
+    fl = 0.0
+    for j in range(nb):
+        wj = min(q, ka - j * q)
+        fl += 2 * 2.0 * n * (3 * wj) ** 2
+    out["subblock_grams"] = {"ms": ms, "tflops": fl / ms / 1e9}
+    ms = event_time(torch, lambda: K.subblock_pencils(ka, q, True, s.araw, s.braw, s.coef, s.theta, s.info,
+                                                      s.cscale), 3)
+    out["pencils"] = {"ms": ms}
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1407_7506_b200 import _lib
+    from paper_1407_7506_b200.ppcg import PPCGSolver, SolverOptions, ppcg_solve
+
+    lib = _lib.load()
+    a, t, k, q, tol = build_problem(args.config)
+    opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=10 ** 6)
+    s = PPCGSolver(a, t, None, opts).start()
+    for _ in range(args.warmup):
+        s.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    launches0 = lib.bk_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    it0 = s.it
+    for _ in range(args.steps):
+        if s.step():
+            break
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = lib.bk_launch_count() - launches0
+    clocks = clk.stop()
+    steps_done = s.it - it0
+    ms = e0.elapsed_time(e1)
+    tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    value = world * steps_done / (ms_max / 1e3)
+
+    line = None
+    if rank == 0:
+        kr = kernel_rooflines(torch, s)
+        peak, peak_src = fp64_peak()
+        hbm, hbm_src = hbm_peak()
+        g = kr["gram"]
+        roofline = {"bound": "tensor", "kernel": "gram_kernel (X^T AX, DMMA m8n8k4, split-K)",
+                    "achieved": g["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": g["tflops"] / peak,
+                    "traffic": ncu_traffic("gram_kernel"), "peak_source": peak_src,
+                    "algorithmic_flops_per_launch": g["flops_per_launch"]}
+        kernels = {name: dict(v) for name, v in kr.items()}
+        kernels["spmm"]["frac_of_hbm"] = kr["spmm"]["gbs"] / hbm
+        kernels["tsgemm"]["frac_of_fp64"] = kr["tsgemm"]["tflops"] / peak
+        kernels["subblock_grams"]["frac_of_fp64"] = kr["subblock_grams"]["tflops"] / peak
+        kernels["hbm_peak_source"] = hbm_src
+        # ---- e2e through the public API with host buffers (uploads + downloads inside)
+        from paper_1407_7506_b200.operators import SparseHermitian
+        from paper_1407_7506_b200.problems import jacobi_preconditioner
+
+        a2 = SparseHermitian(a._csr.copy(), "symmetric")
+        t2 = jacobi_preconditioner(a2)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        rep = ppcg_solve(a2, t2, opts=SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=args.steps))
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        kt = s.kt
+        h2d = a._csr.nnz * 12 + 4 * (a.n + 1) + a.n * kt * 8 + a.n * 8
+        d2h = a.n * k * 8 + k * 8 + rep.iterations * (256 + 64)
+        e2e = {"value": rep.iterations / (w1 - w0), "unit": "iterations/s",
+               "h2d_bytes_per_step": h2d // max(rep.iterations, 1), "d2h_bytes_per_step": d2h // max(rep.iterations, 1),
+               "note": f"public ppcg_solve(host CSR, Jacobi, max_iter={args.steps}) wall time incl. CSR/X0 upload, "
+                       "init CholQR+SpMM, final RR and vector download; bytes are per-job / iterations"}
+        line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": steps_done,
+                "warmup": args.warmup, "ms_per_step": ms_max / max(steps_done, 1), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config 2)",
+                "config": cfg_dict(args.config, a.n, k, q, s.kt,
+                                   {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                                    "n_locked_at_start": int(s.L)}),
+                "roofline": roofline, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks}
+        if not args.no_cpu and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(args):
+    """Oracle (numpy restatement of the reference) on a bounded sample: iterations 1-2 of
+    the same config on the host cores."""
+    from oracle.ppcg_oracle import OracleRun
+    from paper_1407_7506_b200.ppcg import SolverOptions
+
+    a, t, k, q, tol = build_problem(args.config)
+
+    class H:
+        def __init__(self, csr):
+            self.csr, self.n, self.dtype = csr, csr.shape[0], csr.dtype
+
+        def apply(self, b):
+            return self.csr @ b
+
+    class D:
+        def __init__(self, d):
+            self.d = d
+
+        def apply(self, b):
+            return self.d[:, None] * b
+
+    cores = len(os.sched_getaffinity(0)) or 1
+    run = OracleRun(H(a._csr), D(t.d), None, SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=10 ** 6),
+                    blas_threads=cores).start()
+    t0 = time.perf_counter()
+    run.step()
+    n_steps = 1
+    if time.perf_counter() - t0 < 12.0:
+        run.step()
+        n_steps = 2
+    dt = time.perf_counter() - t0
+    return {"value": n_steps / dt, "unit": "iterations/s", "cores": cores, "kind": "port",
+            "sample": f"iterations 1-{n_steps} of config {args.config} by the numpy oracle (oracle/ppcg_oracle.py), "
+                      f"OpenBLAS with {cores} threads; {dt:.1f} s"}
+
+
+def main(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

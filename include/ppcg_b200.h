@@ -25,6 +25,8 @@ extern "C" {
 #define BK_ERR_UNSUPPORTED (-4)
 
 int bk_version(void);
+/* number of kernels this library has launched (host-side counter; evidence for gpu_launches) */
+unsigned long long bk_launch_count(void);
 
 /* ---- operator apply: SparseHermitian.apply, problems.py:72-73 (scipy csr_matvecs) */
 int bk_spmm_csr_d(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, int m,

@@ -28,6 +28,7 @@ PP = ctypes.POINTER(ctypes.c_void_p)
 # name -> (restype, argtypes)
 _SIGS = {
     "bk_version": (c_int, []),
+    "bk_launch_count": (ctypes.c_ulonglong, []),
     "bk_spmm_csr_d": (c_int, [c_i64, vp, vp, vp, c_int, vp, c_i64, vp, c_i64, vp]),
     "bk_spmm_csr_z": (c_int, [c_i64, vp, vp, vp, c_int, vp, c_i64, vp, c_i64, vp]),
     "bk_scale_rows_d": (c_int, [c_i64, c_int, vp, vp, c_i64, vp, c_i64, vp]),

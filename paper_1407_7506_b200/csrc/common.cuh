@@ -12,6 +12,10 @@
 
 #define BK_DEV __device__ __forceinline__
 
+// host-side count of kernels launched by this library (exported as bk_launch_count)
+extern unsigned long long bk_launch_counter;
+#define BK_COUNT() __atomic_fetch_add(&bk_launch_counter, 1ull, __ATOMIC_RELAXED)
+
 #define BK_CHECK_LAUNCH()                                   \
   do {                                                      \
     cudaError_t _e = cudaGetLastError();                    \

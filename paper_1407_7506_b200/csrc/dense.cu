@@ -214,11 +214,13 @@ static int chol_upper_floor(DenseCtx* c, int m, double* G, int64_t ldg, int cplx
   if (ensure(c, db + diag_bytes, hb) != BK_OK) { cusolverDnDestroyParams(prm); return BK_ERR_CUDA; }
   double* gdiag = reinterpret_cast<double*>(c->dwork);
   void* work = static_cast<char*>(c->dwork) + diag_bytes;
+  BK_COUNT();
   k_save_diag<<<grid_for(m), 256, 0, c->st>>>(m, G, ldg, cplx, gdiag);
   cusolverStatus_t s = cusolverDnXpotrf(c->h, prm, CUBLAS_FILL_MODE_LOWER, m, dt, G, ldg, dt, work, db,
                                         hb ? c->hwork : nullptr, hb, c->dinfo);
   cusolverDnDestroyParams(prm);
   if (s != CUSOLVER_STATUS_SUCCESS) return BK_ERR_SOLVER;
+  BK_COUNT();
   k_chol_check<<<grid_for((int64_t)m * m), 256, 0, c->st>>>(m, G, ldg, gdiag, c->dinfo, cplx, fail_col);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -258,8 +260,11 @@ static int rr_pencil(DenseCtx* c, int d, double* A, int64_t lda, double* B, int6
                      int64_t ldc, int cplx, int* status) {
   if (d <= 0 || lda > 0x7fffffff || ldb > 0x7fffffff) return BK_ERR_ARG;
   const int w = cplx ? 2 : 1;
+  BK_COUNT();
   k_symmetrize<<<grid_for((int64_t)d * d), 256, 0, c->st>>>(d, A, lda, cplx);
+  BK_COUNT();
   k_symmetrize<<<grid_for((int64_t)d * d), 256, 0, c->st>>>(d, B, ldb, cplx);
+  BK_COUNT();
   k_fro2<<<1, 1024, 0, c->st>>>(d, B, ldb, cplx, c->dscal);
   // singular-Gram probe on a shifted copy
   int lw = 0, lwp = 0;
@@ -282,6 +287,7 @@ static int rr_pencil(DenseCtx* c, int d, double* A, int64_t lda, double* B, int6
   if (ensure(c, tmp_bytes + wbytes, 0) != BK_OK) return BK_ERR_CUDA;
   double* tmp = reinterpret_cast<double*>(c->dwork);
   double* work = reinterpret_cast<double*>(static_cast<char*>(c->dwork) + tmp_bytes);
+  BK_COUNT();
   k_copy_shift<<<grid_for((int64_t)d * d * w), 256, 0, c->st>>>(d, B, ldb, tmp, d, cplx, c->dscal);
   if (!cplx) {
     s = cusolverDnDpotrf(c->h, CUBLAS_FILL_MODE_LOWER, d, tmp, d, work, max(lw, lwp), c->dinfo);
@@ -297,7 +303,9 @@ static int rr_pencil(DenseCtx* c, int d, double* A, int64_t lda, double* B, int6
                          (int)ldb, omega, reinterpret_cast<cuDoubleComplex*>(work), max(lw, lwp), c->dinfo + 1);
   }
   if (s != CUSOLVER_STATUS_SUCCESS) return BK_ERR_SOLVER;
+  BK_COUNT();
   k_status<<<1, 1, 0, c->st>>>(c->dinfo, c->dinfo + 1, status);
+  BK_COUNT();
   k_colmajor_to_rowmajor<<<grid_for((int64_t)d * d), 256, 0, c->st>>>(d, d, A, lda, C, ldc, cplx);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -336,6 +344,7 @@ __global__ void k_cm_to_rm(int64_t n, int m, const double* T, double* X, int64_t
 static int householder_q(DenseCtx* c, int64_t n, int m, double* X, int64_t ldx, double* tmp, int cplx) {
   if (n > 0x7fffffff || m <= 0 || n < m) return BK_ERR_ARG;
   const int w = cplx ? 2 : 1;
+  BK_COUNT();
   k_rm_to_cm<<<4096, 256, 0, c->st>>>(n, m, X, ldx, tmp, cplx);
   int l1 = 0, l2 = 0;
   cusolverStatus_t s;
@@ -364,6 +373,7 @@ static int householder_q(DenseCtx* c, int64_t n, int m, double* X, int64_t ldx, 
     if (s == CUSOLVER_STATUS_SUCCESS) s = cusolverDnZungqr(c->h, (int)n, m, m, t, (int)n, tt, wk, lw, c->dinfo);
   }
   if (s != CUSOLVER_STATUS_SUCCESS) return BK_ERR_SOLVER;
+  BK_COUNT();
   k_cm_to_rm<<<4096, 256, 0, c->st>>>(n, m, tmp, X, ldx, cplx);
   BK_CHECK_LAUNCH();
   return BK_OK;

@@ -306,6 +306,7 @@ static int launch_gram(GramParams& P, int64_t total_tiles_slots, void* ws, int64
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_bytes());
     attr = true;
   }
+  BK_COUNT();
   gram_kernel<<<(unsigned)grid, G_THREADS, g_smem_bytes(), st>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;

@@ -169,6 +169,7 @@ extern "C" int bk_scale_rows_d(int64_t n, int m, const double* d, const double* 
                                int64_t ldy, void* stream) {
   if (n < 0 || m < 0) return BK_ERR_ARG;
   if (n == 0 || m == 0) return BK_OK;
+  BK_COUNT();
   k_scale_rows<<<gridn(n * m), 256, 0, (cudaStream_t)stream>>>(n, m, d, X, ldx, Y, ldy);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -183,6 +184,7 @@ extern "C" int bk_sumsq_d(int64_t n, int m, const double* X, int64_t ldx, double
   if (n == 0 || m == 0) return cudaMemsetAsync(out, 0, sizeof(double), st) == cudaSuccess ? BK_OK : BK_ERR_CUDA;
   int* ticket = reinterpret_cast<int*>(ws);
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  BK_COUNT();
   k_sumsq<<<SQ_CTAS, SQ_THREADS, 0, st>>>(n, m, X, ldx, part, ticket, out);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -191,6 +193,7 @@ extern "C" int bk_sumsq_d(int64_t n, int m, const double* X, int64_t ldx, double
 // out[0] = sum |c|^2, out[1] = sum |c - delta|^2, out[2] = Re trace (cplx: interleaved)
 extern "C" int bk_small_stats_d(int m1, int m2, const double* C, int64_t ldc, int cplx, double* out, void* stream) {
   if (m1 < 0 || m2 < 0) return BK_ERR_ARG;
+  BK_COUNT();
   k_small_stats<<<1, 1024, 0, (cudaStream_t)stream>>>(m1, m2, C, ldc, cplx, out);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -212,6 +215,7 @@ extern "C" int bk_rr_residual_d(int64_t n, int kt, int cplx, const double* V, in
   }
   int* ticket = reinterpret_cast<int*>(ws);
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  BK_COUNT();
   k_rr_residual<<<ctas, RR_THREADS, smem, (cudaStream_t)stream>>>(n, kt, cplx, V, ldv, AV, ldav, omega, rowscale, W,
                                                                   ldw, part, ticket, colnorm2);
   BK_CHECK_LAUNCH();
@@ -221,6 +225,7 @@ extern "C" int bk_rr_residual_d(int64_t n, int kt, int cplx, const double* V, in
 extern "C" int bk_cplx_expand_d(int K, int N, const double* G, int64_t ldg, double* Gr, int64_t ldr, void* stream) {
   if (K < 0 || N < 0) return BK_ERR_ARG;
   if (K == 0 || N == 0) return BK_OK;
+  BK_COUNT();
   k_cplx_expand<<<gridn((int64_t)K * N), 256, 0, (cudaStream_t)stream>>>(K, N, G, ldg, Gr, ldr);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -230,6 +235,7 @@ extern "C" int bk_cplx_gram_combine_d(int m1, int m2, const double* Cr, int64_t 
                                       void* stream) {
   if (m1 < 0 || m2 < 0) return BK_ERR_ARG;
   if (m1 == 0 || m2 == 0) return BK_OK;
+  BK_COUNT();
   k_cplx_gram_combine<<<gridn((int64_t)m1 * m2), 256, 0, (cudaStream_t)stream>>>(m1, m2, Cr, ldr, C, ldc);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -258,3 +264,6 @@ extern "C" int bk_zero_cols(int64_t n, int w, int elem_bytes, void* dst, int64_t
 }
 
 extern "C" int bk_version(void) { return 1; }
+
+unsigned long long bk_launch_counter = 0;
+extern "C" unsigned long long bk_launch_count(void) { return __atomic_load_n(&bk_launch_counter, __ATOMIC_RELAXED); }

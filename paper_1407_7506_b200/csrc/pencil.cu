@@ -570,6 +570,7 @@ extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* 
     cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes());
     attr = true;
   }
+  BK_COUNT();
   pencil_kernel<<<P.nb, P_THREADS, p_smem_bytes(), (cudaStream_t)stream>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;
@@ -598,6 +599,7 @@ extern "C" int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, cons
     cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes());
     attr = true;
   }
+  BK_COUNT();
   pencil_kernel<<<nb, P_THREADS, p_smem_bytes(), (cudaStream_t)stream>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;

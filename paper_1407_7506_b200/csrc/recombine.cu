@@ -176,6 +176,7 @@ extern "C" int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, c
   const int nb = (k_act + q - 1) / q;
   dim3 grid((unsigned)((n + R_BM - 1) / R_BM), nb, 2);
   if (nb > 65535) return BK_ERR_UNSUPPORTED;
+  BK_COUNT();
   recombine_kernel<<<grid, R_THREADS, smem, (cudaStream_t)stream>>>(R);
   BK_CHECK_LAUNCH();
   return BK_OK;

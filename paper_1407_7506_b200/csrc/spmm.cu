@@ -109,6 +109,7 @@ extern "C" int bk_spmm_csr_d(int64_t n, const int32_t* rowptr, const int32_t* co
   if (n == 0 || m == 0) return BK_OK;
   const unsigned grid = (unsigned)((n + S_THREADS / 32 - 1) / (S_THREADS / 32));
   cudaStream_t st = (cudaStream_t)stream;
+  BK_COUNT();
   if (m <= 32) spmm_csr_real<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
   else if (m <= 64) spmm_csr_real<2><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
   else if (m <= 128) spmm_csr_real<4><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
@@ -127,6 +128,7 @@ extern "C" int bk_spmm_csr_z(int64_t n, const int32_t* rowptr, const int32_t* co
   auto v2 = reinterpret_cast<const double2*>(val);
   auto x2 = reinterpret_cast<const double2*>(X);
   auto y2 = reinterpret_cast<double2*>(Y);
+  BK_COUNT();
   if (m <= 32) spmm_csr_cplx<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
   else if (m <= 64) spmm_csr_cplx<2><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
   else spmm_csr_cplx<4><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);

@@ -266,6 +266,7 @@ extern "C" int bk_tsgemm_batched_d(int nprob, int64_t n, int K, int N, double al
     cudaFuncSetAttribute(tsgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem_bytes());
     attr = true;
   }
+  BK_COUNT();
   tsgemm_kernel<<<grid, T_THREADS, t_smem_bytes(), (cudaStream_t)stream>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;
