@@ -24,7 +24,7 @@
 namespace bk {
 
 constexpr int G_BM = 64, G_BN = 64, G_BK = 16, G_STAGES = 4, G_THREADS = 128;
-constexpr int G_PAD = 8;                    // row stride 72 doubles: conflict-free fragments
+constexpr int G_PAD = 4;  // row stride 68 = 4 mod 16 doubles: half-warp fragment loads hit 4 disjoint 8-bank groups
 constexpr int G_LDS = G_BM + G_PAD;
 constexpr int G_WM = 4, G_WN = 4;           // warp tile = 32 x 32 (4 x 4 MMA tiles)
 
@@ -270,12 +270,23 @@ static void fill_tiles(GramProblem& g) {
 }
 
 static int choose_chunks(int64_t nrows, int64_t total_tiles) {
-  // aim for ~3 resident CTAs per SM over 148 SMs, each chunk >= 4 stages
-  int64_t target = 3LL * kSMs;
-  int64_t c = (target + total_tiles - 1) / lmax(total_tiles, 1);
-  int64_t maxc = lmax(1, nrows / (4 * G_BK));
-  c = lmax(1, min(c, maxc));
-  return (int)lmin(c, 256);
+  // Wave-aware split-K: 3 resident CTAs per SM -> 444 slots.  Pick the chunk count (each
+  // chunk >= 32 stages when possible) whose last wave is fullest: a 1.1-wave grid idles
+  // most of the second wave.
+  const int64_t slots = 3LL * kSMs;
+  total_tiles = lmax(total_tiles, 1);
+  const int64_t cmax = lmax(1, lmin(256, nrows / (32 * G_BK)));
+  if (total_tiles >= 8 * slots || cmax == 1) return 1;
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t c = 1; c <= cmax; ++c) {
+    const int64_t ctas = total_tiles * c;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (eff >= 0.92) return (int)c;  // smallest chunk count with a >= 92% full last wave
+    if (eff > best_eff) { best_eff = eff; best = c; }
+  }
+  return (int)best;
 }
 
 // workspace layout: [tickets: 64 KB][partials]

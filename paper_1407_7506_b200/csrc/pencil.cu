@@ -90,40 +90,90 @@ BK_DEV double block_max(double v, double* red) {
 
 // ---------------------------------------------------------------- in-place lower Cholesky
 // Returns true on success (all pivots > 0 and finite), like LAPACK potrf.
+// Work is mapped 2-D without integer division: warps over rows, lanes over columns.
+#define BK_WARP (threadIdx.x >> 5)
+#define BK_LANE (threadIdx.x & 31)
+#define BK_NWARP (blockDim.x >> 5)
+
 BK_DEV bool smem_cholesky(double* M, int ld, int d, int* flag) {
+  // right-looking, one column per step; the pivot test is uniform (all threads read the
+  // same shared value after the barrier)
   for (int j = 0; j < d; ++j) {
     __syncthreads();
     const double piv = M[j * ld + j];
-    if (!(piv > 0.0) || !isfinite(piv)) return false;  // uniform: all threads read the same value
+    if (!(piv > 0.0) || !isfinite(piv)) return false;
     const double ljj = sqrt(piv);
     const double inv = 1.0 / ljj;
+    // trailing update of rows i > j uses the scaled column: l_ij = a_ij / ljj
+    for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
+      const double lij = M[i * ld + j] * inv;
+      for (int k = j + 1 + BK_LANE; k <= i; k += 32) M[i * ld + k] = fma(-lij, M[k * ld + j] * inv, M[i * ld + k]);
+    }
     __syncthreads();
     for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) M[i * ld + j] *= inv;
     if (threadIdx.x == 0) M[j * ld + j] = ljj;
-    __syncthreads();
-    const int rem = d - j - 1;
-    const int tot = rem * rem;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) M[i * ld + k] = fma(-M[i * ld + j], M[k * ld + j], M[i * ld + k]);
-    }
   }
   __syncthreads();
   return true;
 }
 
-// Linv (lower, ld li) from L (lower, ld ll): row-sequential forward substitution
+// Linv (lower, ld li) from L (lower, ld ll): right-looking column sweep
+//   X = I; for j: X[j,:] /= l_jj; X[i,:] -= l_ij X[j,:] (i > j)
 BK_DEV void smem_lower_inverse(const double* L, int ll, double* Li, int li, int d) {
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) Li[(e / d) * li + e % d] = 0.0;
+  for (int i = BK_WARP; i < d; i += BK_NWARP)
+    for (int c = BK_LANE; c < d; c += 32) Li[i * li + c] = (i == c) ? 1.0 / L[i * ll + i] : 0.0;
   __syncthreads();
-  for (int i = 0; i < d; ++i) {
-    const double inv = 1.0 / L[i * ll + i];
-    for (int j = threadIdx.x; j <= i; j += blockDim.x) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) s = fma(-L[i * ll + k], Li[k * li + j], s);
-      Li[i * li + j] = s * inv;
+  for (int j = 0; j < d; ++j) {
+    // row j of X is final (already divided by l_jj); eliminate below
+    for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
+      const double f = L[i * ll + j] / L[i * ll + i];
+      for (int c = BK_LANE; c <= j; c += 32) Li[i * li + c] = fma(-f, Li[j * li + c], Li[i * li + c]);
     }
     __syncthreads();
+  }
+}
+
+// C (d x d, ldc) = op(A) * op(B) over shared memory, 6x3 register block per thread for
+// d <= 96 (warps -> rows w, w+16, ...; lanes -> cols l, l+32, l+64).
+//   tb = false: C[i][j] = sum_k A[i][k] B[k][j]
+//   tb = true : C[i][j] = sum_k A[i][k] B[j][k]
+template <bool TA, bool TB>
+BK_DEV void smem_gemm(const double* A, int la, const double* B, int lb, double* C, int lc, int d, int kmax,
+                      int ncols = -1) {
+  constexpr int RI = 6, RJ = 3;
+  const int nc = ncols < 0 ? d : ncols;
+  for (int i0 = BK_WARP; i0 < d; i0 += BK_NWARP * RI) {
+    double acc[RI][RJ];
+#pragma unroll
+    for (int a = 0; a < RI; ++a)
+#pragma unroll
+      for (int b = 0; b < RJ; ++b) acc[a][b] = 0.0;
+    for (int k = 0; k < kmax; ++k) {
+      double av[RI], bv[RJ];
+#pragma unroll
+      for (int a = 0; a < RI; ++a) {
+        const int i = i0 + a * BK_NWARP;
+        av[a] = i < d ? (TA ? A[k * la + i] : A[i * la + k]) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < RJ; ++b) {
+        const int j = BK_LANE + 32 * b;
+        bv[b] = j < nc ? (TB ? B[j * lb + k] : B[k * lb + j]) : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < RI; ++a)
+#pragma unroll
+        for (int b = 0; b < RJ; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < RI; ++a) {
+      const int i = i0 + a * BK_NWARP;
+#pragma unroll
+      for (int b = 0; b < RJ; ++b) {
+        const int j = BK_LANE + 32 * b;
+        if (i < d && j < nc) C[i * lc + j] = acc[a][b];
+      }
+    }
   }
 }
 
@@ -141,9 +191,21 @@ BK_DEV void rr_pair(int r, int i, int dd, int& p, int& q) {
 // Returns the number of sweeps.
 BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, PSmem& S) {
   if (withV) {
-    for (int e = threadIdx.x; e < d * d; e += blockDim.x) V[(e / d) * lv + e % d] = (e / d == e % d) ? 1.0 : 0.0;
+    for (int i = BK_WARP; i < d; i += BK_NWARP)
+      for (int c = BK_LANE; c < d; c += 32) V[i * lv + c] = (i == c) ? 1.0 : 0.0;
   }
   if (d == 1) { __syncthreads(); return 0; }
+  {
+    double f = 0.0;
+    for (int i = BK_WARP; i < d; i += BK_NWARP)
+      for (int c = BK_LANE; c < d; c += 32) {
+        const double v = A[i * la + c];
+        f = fma(v, v, f);
+      }
+    f = sqrt(block_sum(f, S.red));
+    if (threadIdx.x == 0) S.red[30] = 0.5 * DBL_EPSILON * f / (double)d;
+    __syncthreads();
+  }
   const int dd = d + (d & 1);
   const int npairs = dd / 2;
   int sweep = 0;
@@ -159,7 +221,12 @@ BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, 
         if (q < d) {
           const double apq = A[p * la + q];
           const double app = A[p * la + p], aqq = A[q * la + q];
-          if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq))) {
+          // rotate unless |a_pq| is below both the relative (Demmel-Veselic) and the
+          // absolute eps*||A||_F/d floor: an entry that small moves eigenvalues by less than
+          // the rounding already in the diagonal (avoids endless sweeps on noise when a
+          // diagonal entry is ~0)
+          if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq)) &&
+              fabs(apq) > S.red[30]) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -173,35 +240,39 @@ BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, 
         S.rs[i] = s;
       }
       __syncthreads();
-      // 2. row rotations  A <- J^T A
-      for (int e = threadIdx.x; e < npairs * d; e += blockDim.x) {
-        const int i = e / d, j = e % d;
+      // 2. row rotations  A <- J^T A   (warp per pair, lanes over columns: stride-1 rows)
+      for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
         const double s = S.rs[i];
-        if (s == 0.0) continue;
+        if (s == 0.0) continue;  // warp-uniform
         const double c = S.rc[i];
-        const int p = S.pp[i], q = S.pq[i];
-        const double ap = A[p * la + j], aq = A[q * la + j];
-        A[p * la + j] = c * ap - s * aq;
-        A[q * la + j] = s * ap + c * aq;
+        double* ap_ = A + S.pp[i] * la;
+        double* aq_ = A + S.pq[i] * la;
+        for (int j = BK_LANE; j < d; j += 32) {
+          const double ap = ap_[j], aq = aq_[j];
+          ap_[j] = c * ap - s * aq;
+          aq_[j] = s * ap + c * aq;
+        }
       }
       __syncthreads();
-      // 3. column rotations  A <- A J, V <- V J; the annihilated pair is set to exact zero
-      for (int e = threadIdx.x; e < npairs * d; e += blockDim.x) {
-        const int i = e / d, row = e % d;
+      // 3. column rotations  A <- A J, V <- V J (lanes over rows: odd stride, conflict-free);
+      //    the annihilated pair is set to exact zero
+      for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
         const double s = S.rs[i];
         if (s == 0.0) continue;
         const double c = S.rc[i];
         const int p = S.pp[i], q = S.pq[i];
-        const double ap = A[row * la + p], aq = A[row * la + q];
-        double np_ = c * ap - s * aq, nq = s * ap + c * aq;
-        if (row == p) nq = 0.0;
-        if (row == q) np_ = 0.0;
-        A[row * la + p] = np_;
-        A[row * la + q] = nq;
-        if (withV) {
-          const double vp = V[row * lv + p], vq = V[row * lv + q];
-          V[row * lv + p] = c * vp - s * vq;
-          V[row * lv + q] = s * vp + c * vq;
+        for (int row = BK_LANE; row < d; row += 32) {
+          const double ap = A[row * la + p], aq = A[row * la + q];
+          double np_ = c * ap - s * aq, nq = s * ap + c * aq;
+          if (row == p) nq = 0.0;
+          if (row == q) np_ = 0.0;
+          A[row * la + p] = np_;
+          A[row * la + q] = nq;
+          if (withV) {
+            const double vp = V[row * lv + p], vq = V[row * lv + q];
+            V[row * lv + p] = c * vp - s * vq;
+            V[row * lv + q] = s * vp + c * vq;
+          }
         }
       }
       __syncthreads();
@@ -265,7 +336,7 @@ BK_DEV void smem_svals(double* M, int lm, int rows, int cols, double* sv, PSmem&
 
 // ---------------------------------------------------------------- one pencil attempt
 // Assembled basis: idx[0:d] raw columns, sf[0:d] scale factors.  Raw Grams at (Ar, Br, ldr).
-// On success: ev[0:want] ascending eigenvalues (ord applied), C (d x want) in M0 (ld PLD).
+// On success: ev[0:want] ascending eigenvalues (ord applied), C (d x want) in M1 (ld PLD).
 // Returns 0 ok, 1 singular (either Cholesky failed).
 BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, int want, PSmem& S) {
   double* A = S.M0;
@@ -273,12 +344,15 @@ BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, in
   double* Li = S.M2;
   // assemble symmetrised, scaled B and its Frobenius norm
   double fro = 0.0;
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int a = e / d, b = e % d;
-    const int ia = S.idx[a], ib = S.idx[b];
-    const double v = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * S.sf[a] * S.sf[b];
-    B[a * PLD + b] = v;
-    fro = fma(v, v, fro);
+  for (int a = BK_WARP; a < d; a += BK_NWARP) {
+    const int ia = S.idx[a];
+    const double sa = S.sf[a];
+    for (int b = BK_LANE; b < d; b += 32) {
+      const int ib = S.idx[b];
+      const double v = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * sa * S.sf[b];
+      B[a * PLD + b] = v;
+      fro = fma(v, v, fro);
+    }
   }
   fro = sqrt(block_sum(fro, S.red));
   const double flo = kGramRtol * fmax(fro, 1e-300);
@@ -286,40 +360,30 @@ BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, in
   __syncthreads();
   if (!smem_cholesky(B, PLD, d, S.misc)) return 1;  // core.py:193-197
   // reload B (exact) and factor it for the reduction (sygvd's potrf)
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int a = e / d, b = e % d;
-    const int ia = S.idx[a], ib = S.idx[b];
-    B[a * PLD + b] = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * S.sf[a] * S.sf[b];
-    A[a * PLD + b] = 0.5 * (Ar[ia * ldr + ib] + Ar[ib * ldr + ia]) * S.sf[a] * S.sf[b];
+  for (int a = BK_WARP; a < d; a += BK_NWARP) {
+    const int ia = S.idx[a];
+    const double sa = S.sf[a];
+    for (int b = BK_LANE; b < d; b += 32) {
+      const int ib = S.idx[b];
+      const double sab = sa * S.sf[b];
+      B[a * PLD + b] = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * sab;
+      A[a * PLD + b] = 0.5 * (Ar[ia * ldr + ib] + Ar[ib * ldr + ia]) * sab;
+    }
   }
   __syncthreads();
   if (!smem_cholesky(B, PLD, d, S.misc)) return 1;  // core.py:198-201
   smem_lower_inverse(B, PLD, Li, PLD, d);
-  // T = Linv A  -> B (L no longer needed)
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int i = e / d, j = e % d;
-    double s = 0.0;
-    for (int k = 0; k <= i; ++k) s = fma(Li[i * PLD + k], A[k * PLD + j], s);
-    B[i * PLD + j] = s;
-  }
+  smem_gemm<false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A -> B (L no longer needed)
   __syncthreads();
-  // Ared = T Linv^T -> A
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int i = e / d, j = e % d;
-    double s = 0.0;
-    for (int k = 0; k <= j; ++k) s = fma(B[i * PLD + k], Li[j * PLD + k], s);
-    A[i * PLD + j] = s;
-  }
+  smem_gemm<false, true>(B, PLD, Li, PLD, A, PLD, d, d);   // Ared = T Linv^T -> A
   __syncthreads();
-  // symmetrise (reduced matrix is symmetric in exact arithmetic)
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-    const int i = e / d, j = e % d;
-    if (i < j) {
+  // symmetrise (the reduced matrix is symmetric in exact arithmetic)
+  for (int i = BK_WARP; i < d; i += BK_NWARP)
+    for (int j = i + 1 + BK_LANE; j < d; j += 32) {
       const double v = 0.5 * (A[i * PLD + j] + A[j * PLD + i]);
       A[i * PLD + j] = v;
       A[j * PLD + i] = v;
     }
-  }
   __syncthreads();
   smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
   for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = A[i * PLD + i];
@@ -335,19 +399,15 @@ BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, in
     S.ord[rank] = i;
   }
   __syncthreads();
-  // C = Linv^T V[:, ord[0:want]] -> A (ld PLD); eigenvalues -> A-independent slot ev2
-  for (int e = threadIdx.x; e < d * want; e += blockDim.x) {
-    const int i = e / want, r = e % want;
-    const int col = S.ord[r];
-    double s = 0.0;
-    for (int k = i; k < d; ++k) s = fma(Li[k * PLD + i], B[k * PLD + col], s);
-    A[i * PLD + r] = s;
-  }
+  // gather V[:, ord[0:want]] -> A, then C = Linv^T Vsel -> B (ld PLD)
+  for (int k = BK_WARP; k < d; k += BK_NWARP)
+    for (int r = BK_LANE; r < want; r += 32) A[k * PLD + r] = B[k * PLD + S.ord[r]];
   __syncthreads();
-  // sorted eigenvalues into rc scratch (size >= want)... keep them in sf-free slot: use Li row 0
-  for (int r = threadIdx.x; r < want; r += blockDim.x) Li[r] = S.ev[S.ord[r]];
+  smem_gemm<true, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+  // sorted eigenvalues
+  for (int r = threadIdx.x; r < want; r += blockDim.x) A[PD * PLD - 1 - r] = S.ev[S.ord[r]];
   __syncthreads();
-  for (int r = threadIdx.x; r < want; r += blockDim.x) S.ev[r] = Li[r];
+  for (int r = threadIdx.x; r < want; r += blockDim.x) S.ev[r] = A[PD * PLD - 1 - r];
   __syncthreads();
   return 0;
 }
@@ -384,7 +444,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     const int st = pencil_attempt(Ar, Br, ldr, d, P.want, S);
     double* cout = P.coef + (int64_t)j * P.dmax * P.want;
     if (st == 0) {
-      for (int e = tid; e < d * P.want; e += blockDim.x) cout[e] = S.M0[(e / P.want) * PLD + e % P.want];
+      for (int e = tid; e < d * P.want; e += blockDim.x) cout[e] = S.M1[(e / P.want) * PLD + e % P.want];
       for (int r = tid; r < P.want; r += blockDim.x) P.theta[(int64_t)j * P.want + r] = S.ev[r];
     }
     if (tid == 0) { P.info[4 * j + 2] = st; P.info[4 * j + 0] = 0; P.info[4 * j + 1] = 0; P.info[4 * j + 3] = 1; }
@@ -476,9 +536,9 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
       np_used = __popcll(mp);
       // rank test: sigma_min(C_X) < 1e-14 max(||C||_2, 1)  (ppcg.py:351-356)
       double* T1 = S.M2;                 // C copy (d x w, ld w)  -- Linv no longer needed
-      double* T2 = S.M1;                 // C_X copy (w x w, ld w)
-      for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M0[(e / w) * PLD + e % w];
-      for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M0[(e / w) * PLD + e % w];
+      double* T2 = S.M0;                 // C_X copy (w x w, ld w); C itself stays in M1
+      for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M1[(e / w) * PLD + e % w];
+      for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M1[(e / w) * PLD + e % w];
       __syncthreads();
       smem_svals(T1, w, d, w, S.rc, S);
       double cn = 0.0;
@@ -510,14 +570,14 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     if (!err && !(fallback && zero_res)) {
       // coefficients: X rows direct, W/P rows un-scaled onto original columns (ppcg.py:358-363)
       double m = 0.0;
-      for (int e = tid; e < d * w; e += blockDim.x) m = fmax(m, fabs(S.M0[(e / w) * PLD + e % w]));
+      for (int e = tid; e < d * w; e += blockDim.x) m = fmax(m, fabs(S.M1[(e / w) * PLD + e % w]));
       cmax = block_max(m, S.red);
       for (int e = tid; e < nparts * w * w; e += blockDim.x) cout[e] = 0.0;
       __syncthreads();
       for (int e = tid; e < d * w; e += blockDim.x) {
         const int a = e / w, c = e % w;
         const int raw = S.idx[a];
-        cout[raw * w + c] = S.M0[a * PLD + c] * S.sf[a];
+        cout[raw * w + c] = S.M1[a * PLD + c] * S.sf[a];
       }
       for (int i = tid; i < w; i += blockDim.x) P.theta[lo + i] = S.ev[i];
     }

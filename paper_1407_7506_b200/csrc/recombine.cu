@@ -28,7 +28,7 @@ struct RecombParams {
 };
 
 BK_DEV int pad_a(int w) { int l = (w + 3) & ~3; if ((l & 7) == 0) l += 4; return l; }   // l % 8 == 4
-BK_DEV int pad_b(int w) { int l = (w + 7) & ~7; if ((l & 15) == 0) l += 8; return l; }  // l % 16 == 8
+BK_DEV int pad_b(int w) { int l = (w + 7) & ~7; return l + 4; }  // l % 8 == 4: 4 rows -> 4 disjoint 8-bank groups
 
 __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_constant__ RecombParams P) {
   extern __shared__ __align__(16) double sm[];
@@ -165,8 +165,7 @@ extern "C" int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, c
   R.flags = flags;
   int la = (q + 3) & ~3;
   if ((la & 7) == 0) la += 4;
-  int lb = (q + 7) & ~7;
-  if ((lb & 15) == 0) lb += 8;
+  const int lb = ((q + 7) & ~7) + 4;
   const int smem = (3 * R_BM * la + 3 * q * lb) * (int)sizeof(double);
   static int attr_bytes = 0;
   if (smem > attr_bytes) {

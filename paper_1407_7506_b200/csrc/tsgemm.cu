@@ -19,7 +19,7 @@ namespace bk {
 
 constexpr int T_BM = 128, T_BN = 64, T_BK = 16, T_STAGES = 3, T_THREADS = 256;
 constexpr int T_XLD = T_BK + 4;    // 20 doubles: conflict-free A fragments
-constexpr int T_GLD = T_BN + 8;    // 72 doubles: conflict-free B fragments
+constexpr int T_GLD = T_BN + 4;    // 68 = 4 mod 16 doubles: conflict-free B fragments
 constexpr int T_WM = 4, T_WN = 4;  // warp tile 32 x 32, warps 4 (rows) x 2 (cols)
 
 struct TsProblem {
