@@ -210,8 +210,8 @@ def kernel_rooflines(torch, s):
     q = s.opts.sbsize
     ms = event_time(torch, lambda: K.subblock_grams(n, ka, q, True, s.XF[s.xi].data_ptr(), s.W.data_ptr(),
                                                     s.P[s.pi].data_ptr(), s.AXF[s.xi].data_ptr(),
-                                                    s.AW.data_ptr(), s.AP[s.pi].data_ptr(), kt, L, s.araw,
-                                                    s.braw), 5)
+                                                    s.AW.data_ptr(), s.AP[s.pi].data_ptr(), s.ldp, L, s.araw,
+                                                    s.braw, tmp=s.gtmp), 5)
     nb = (ka + q - 1) // q
     fl = 0.0
     for j in range(nb):

@@ -57,6 +57,11 @@ int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const double* X,
                         const double* P, const double* AX, const double* AW, const double* AP,
                         int64_t ld, int64_t c0, double* Araw, double* Braw, void* ws,
                         int64_t ws_bytes, void* stream);
+/* complex128 blocks (interleaved; ld, c0 in complex elements); tmpA/tmpB: nb*(2*dmax)^2 doubles */
+int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X, const double* W,
+                        const double* P, const double* AX, const double* AW, const double* AP,
+                        int64_t ld, int64_t c0, double* Araw, double* Braw, double* tmpA,
+                        double* tmpB, void* ws, int64_t ws_bytes, void* stream);
 
 /* ---- batched subblock update (block_update ppcg.py:278-378 incl. fallback 231-275,
  *      solve_pencil core.py:175-202) and plain batched pencils */
@@ -66,6 +71,11 @@ int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const
                           void* stream);
 int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
                         double* omega, double* C, int* status, void* stream);
+int bk_subblock_pencils_z(int k_act, int q, int has_p, const double* Araw, const double* Braw,
+                          double* coef, double* theta, int* info, double* cscale, int force_fallback,
+                          void* stream);
+int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, const double* B, int want,
+                        double* omega, double* C, int* status, void* stream);
 
 /* ---- recombination: ppcg.py:365-369 and _run_subblocks ppcg.py:521-532 (+ breakdown
  *      flags of ppcg.py:701-705) */
@@ -74,6 +84,12 @@ int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double
                             const double* AW, const double* AP, double* Xo, double* Po,
                             double* AXo, double* APo, int64_t ld, int64_t c0,
                             unsigned long long* flags, void* stream);
+/* complex128: coef complex (nb x dmax x q); coef_tmp: nb*(2*dmax)*(2*q) doubles */
+int bk_subblock_recombine_z(int64_t n, int k_act, int q, int has_p, const double* coef,
+                            const double* X, const double* W, const double* P, const double* AX,
+                            const double* AW, const double* AP, double* Xo, double* Po,
+                            double* AXo, double* APo, int64_t ld, int64_t c0,
+                            unsigned long long* flags, double* coef_tmp, void* stream);
 
 /* ---- tall update GEMM Y = s.*(alpha X G + beta Z): _apply_projection ppcg.py:443-445,
  *      residual ppcg.py:630/758 (+Jacobi ppcg.py:678 as s), CholQR core.py:99 (flags bit0:

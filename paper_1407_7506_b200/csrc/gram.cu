@@ -436,3 +436,44 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
   P.nrows = n;
   return launch_gram(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
 }
+
+namespace bk {
+// per-block combine of real Grams of interleaved views into complex X^H Y blocks
+__global__ void k_subblock_combine(int nb, int k_act, int q, int nparts, int dmax, const double* __restrict__ tr,
+                                   double* __restrict__ out) {
+  const int j = blockIdx.y;
+  const int w = min(q, k_act - j * q);
+  const int d0 = nparts * w;
+  const int ldr = 2 * dmax;
+  const double* t = tr + (int64_t)j * ldr * ldr;
+  double* o = out + (int64_t)j * dmax * dmax * 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d0 * d0; e += gridDim.x * blockDim.x) {
+    const int a = e / d0, b = e % d0;
+    const double rr = t[(2 * a) * ldr + 2 * b], ri = t[(2 * a) * ldr + 2 * b + 1];
+    const double ir = t[(2 * a + 1) * ldr + 2 * b], ii = t[(2 * a + 1) * ldr + 2 * b + 1];
+    o[2 * (a * dmax + b)] = rr + ii;
+    o[2 * (a * dmax + b) + 1] = ri - ir;
+  }
+}
+}  // namespace bk
+
+// complex128 variant: X..AP interleaved complex, ld/c0 in complex elements; Araw/Braw are
+// nb x dmax x dmax complex; tmpA/tmpB are real scratch of nb x (2 dmax)^2 doubles.
+extern "C" int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X, const double* W,
+                                   const double* P_, const double* AX, const double* AW, const double* AP,
+                                   int64_t ld, int64_t c0, double* Araw, double* Braw, double* tmpA, double* tmpB,
+                                   void* ws, int64_t ws_bytes, void* stream) {
+  int rc = bk_subblock_grams_d(n, 2 * k_act, 2 * q, has_p, X, W, P_, AX, AW, AP, 2 * ld, 2 * c0, tmpA, tmpB, ws,
+                               ws_bytes, stream);
+  if (rc != BK_OK) return rc;
+  const int nb = (k_act + q - 1) / q;
+  const int nparts = has_p ? 3 : 2;
+  const int dmax = nparts * q;
+  dim3 grid((unsigned)lmin(64, (dmax * dmax + 255) / 256), nb);
+  BK_COUNT();
+  k_subblock_combine<<<grid, 256, 0, (cudaStream_t)stream>>>(nb, k_act, q, nparts, dmax, tmpA, Araw);
+  BK_COUNT();
+  k_subblock_combine<<<grid, 256, 0, (cudaStream_t)stream>>>(nb, k_act, q, nparts, dmax, tmpB, Braw);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}

@@ -1,19 +1,21 @@
-// Batched projected eigenproblems of the PPCG subblock update, one CTA per subblock.
+// Batched projected eigenproblems of the PPCG subblock update, one CTA per subblock,
+// real (fp64) and complex Hermitian (complex128).
 //
 // Replaces, per subblock j, the host logic of block_update (blockeig ppcg.py:278-378)
 // from the raw Grams onwards, including
 //   * the direction-drop test and unit scaling     ppcg.py:198-203, 220-228, 296-299
 //   * SmallPencil symmetrisation                    core.py:143-164
 //   * solve_pencil: singular-Gram test (Cholesky of B - 1e-12||B||_F I) and the dense
-//     generalized eigensolve (LAPACK sygvd: potrf, reduce, eig)   core.py:175-202
+//     generalized eigensolve (LAPACK sygvd/hegvd: potrf, reduce, eig)   core.py:175-202
 //   * the SingularGramError retry ladder (drop P, shed weakest W)  ppcg.py:332-349
 //   * the sigma_min(C_X) rank test and fallback_steepest_descent   ppcg.py:351-356, 231-275
 //   * coefficient un-scaling and coeff_scale                       ppcg.py:358-363, 376
-// The dense eigensolve is Cholesky reduction C = L^{-1} A L^{-T} followed by a two-sided
+// The dense eigensolve is Cholesky reduction C = L^{-1} A L^{-H} followed by a two-sided
 // parallel cyclic Jacobi (round-robin ordering, d/2 disjoint rotations per round) with the
-// whole working set in shared memory.  Singular values for the rank test come from
-// one-sided (Hestenes) Jacobi.  No host round trip: every branch of the reference's retry
-// logic runs on the device and only counters/flags are returned.
+// whole working set in shared memory.  For complex Hermitian matrices each rotation is the
+// real rotation composed with the phase diag(1, e^{-i arg a_pq}).  Singular values for the
+// rank test come from one-sided (Hestenes) Jacobi.  No host round trip: every branch of the
+// reference's retry logic runs on the device and only counters/flags are returned.
 //
 // Mode 1 ("raw") solves one plain pencil per CTA: solve_pencil(SmallPencil(A, B), want).
 #include <cfloat>
@@ -21,30 +23,70 @@
 
 namespace bk {
 
-constexpr int PD = 96;            // max pencil dimension of the shared-memory path
-constexpr int PLD = PD + 1;       // odd leading dimension: conflict-free column access
+// ---------------------------------------------------------------- scalar helpers
+struct zd {
+  double re, im;
+};
+BK_DEV zd operator+(zd a, zd b) { return {a.re + b.re, a.im + b.im}; }
+BK_DEV zd operator-(zd a, zd b) { return {a.re - b.re, a.im - b.im}; }
+BK_DEV zd operator*(zd a, zd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+BK_DEV zd operator*(double s, zd a) { return {s * a.re, s * a.im}; }
+BK_DEV zd operator*(zd a, double s) { return {s * a.re, s * a.im}; }
+BK_DEV double cj(double a) { return a; }
+BK_DEV zd cj(zd a) { return {a.re, -a.im}; }
+BK_DEV double rl(double a) { return a; }
+BK_DEV double rl(zd a) { return a.re; }
+BK_DEV double ab2(double a) { return a * a; }
+BK_DEV double ab2(zd a) { return a.re * a.re + a.im * a.im; }
+BK_DEV double fmaT(double a, double b, double c) { return fma(a, b, c); }
+BK_DEV zd fmaT(zd a, zd b, zd c) {
+  return {fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
+}
+template <class T> BK_DEV T fromR(double x);
+template <> BK_DEV double fromR<double>(double x) { return x; }
+template <> BK_DEV zd fromR<zd>(double x) { return {x, 0.0}; }
+BK_DEV double im_part(double) { return 0.0; }
+BK_DEV double im_part(zd a) { return a.im; }
+template <class T> BK_DEV T make_scalar(double re, double im);
+template <> BK_DEV double make_scalar<double>(double re, double) { return re; }
+template <> BK_DEV zd make_scalar<zd>(double re, double im) { return {re, im}; }
+BK_DEV void real_diag(double&) {}
+BK_DEV void real_diag(zd& a) { a.im = 0.0; }
+// magnitude/phase split of an off-diagonal entry: real keeps the sign in `mag` (phase 1)
+BK_DEV void magph(double a, double& mag, double& ph) { mag = a; ph = 1.0; }
+BK_DEV void magph(zd a, double& mag, zd& ph) {
+  mag = sqrt(ab2(a));
+  ph = mag > 0.0 ? zd{a.re / mag, a.im / mag} : zd{1.0, 0.0};
+}
+
+template <class T> struct PD_;
+template <> struct PD_<double> { static constexpr int v = 96; };
+template <> struct PD_<zd> { static constexpr int v = 64; };
+
 constexpr int P_THREADS = 512;
 constexpr double kGramRtol = 1e-12, kDirFloor = 1e-14, kCxFloor = 1e-14;
 
 struct PencilParams {
   int nb;
   int k_act, q, has_p, dmax;
-  const double* Araw;  // nb x dmax x dmax
-  const double* Braw;
-  double* coef;        // nb x (dmax x q): block j rows [part*w + i], ld = w
-  double* theta;       // k_act (block mode) / nb x want (raw mode)
-  int* info;           // nb x 4: fallback, zero_residual, error, attempts
-  double* cscale;      // nb
-  int mode;            // 0 = block_update, 1 = raw pencil
-  int want;            // raw mode
-  int rawd;            // raw mode pencil dimension
+  const void* Araw;  // nb x dmax x dmax (scalar T)
+  const void* Braw;
+  void* coef;        // nb x (dmax x q): block j rows [part*w + i], ld = w (scalar T)
+  double* theta;     // k_act (block mode) / nb x want (raw mode)
+  int* info;         // nb x 4: fallback, zero_residual, error, attempts
+  double* cscale;    // nb
+  int mode;          // 0 = block_update, 1 = raw pencil
+  int want;          // raw mode
+  int rawd;          // raw mode pencil dimension
   int force_fallback;  // 1: fallback_steepest_descent directly (ppcg.py:456-472 redo)
 };
 
+template <class T>
 struct PSmem {
-  double* M0;  // PD x PLD : A (reduced), later temps
-  double* M1;  // PD x PLD : B -> L -> T -> V
-  double* M2;  // PD x PLD : Linv
+  T* M0;  // PD x PLD : A (reduced), later temps
+  T* M1;  // PD x PLD : B -> L -> T -> V -> C
+  T* M2;  // PD x PLD : Linv
+  T* rph;        // PD/2 rotation phases
   double* nrm;   // PD column norms of [X|W|P]
   double* sf;    // PD scale factor of the assembled basis (1 or 1/norm)
   double* ev;    // PD eigenvalues
@@ -58,112 +100,108 @@ struct PSmem {
   int* misc;     // 8 ints: [0] flag, [1] rotation count
 };
 
+#define BK_WARP (threadIdx.x >> 5)
+#define BK_LANE (threadIdx.x & 31)
+#define BK_NWARP (blockDim.x >> 5)
+
 // ---------------------------------------------------------------- block reductions
 BK_DEV double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   v = warp_sum(v);
   __syncthreads();
-  if (lane == 0) red[w] = v;
+  if (BK_LANE == 0) red[BK_WARP] = v;
   __syncthreads();
-  double t = 0.0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    double t = 0.0;
+    for (int i = 0; i < (int)BK_NWARP; ++i) t += red[i];
     red[31] = t;
   }
   __syncthreads();
   return red[31];
 }
 BK_DEV double block_max(double v, double* red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   v = warp_max(v);
   __syncthreads();
-  if (lane == 0) red[w] = v;
+  if (BK_LANE == 0) red[BK_WARP] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = red[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) t = fmax(t, red[i]);
+    for (int i = 1; i < (int)BK_NWARP; ++i) t = fmax(t, red[i]);
     red[31] = t;
   }
   __syncthreads();
   return red[31];
 }
 
-// ---------------------------------------------------------------- in-place lower Cholesky
-// Returns true on success (all pivots > 0 and finite), like LAPACK potrf.
-// Work is mapped 2-D without integer division: warps over rows, lanes over columns.
-#define BK_WARP (threadIdx.x >> 5)
-#define BK_LANE (threadIdx.x & 31)
-#define BK_NWARP (blockDim.x >> 5)
-
-BK_DEV bool smem_cholesky(double* M, int ld, int d, int* flag) {
-  // right-looking, one column per step; the pivot test is uniform (all threads read the
-  // same shared value after the barrier)
+// ---------------------------------------------------------------- Cholesky L L^H, in place
+// Right-looking, one column per step.  Returns true on success (all pivots > 0 and
+// finite), like LAPACK potrf; the test is uniform (all threads read the same value).
+template <class T>
+BK_DEV bool smem_cholesky(T* M, int ld, int d) {
   for (int j = 0; j < d; ++j) {
     __syncthreads();
-    const double piv = M[j * ld + j];
+    const double piv = rl(M[j * ld + j]);
     if (!(piv > 0.0) || !isfinite(piv)) return false;
     const double ljj = sqrt(piv);
     const double inv = 1.0 / ljj;
-    // trailing update of rows i > j uses the scaled column: l_ij = a_ij / ljj
     for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
-      const double lij = M[i * ld + j] * inv;
-      for (int k = j + 1 + BK_LANE; k <= i; k += 32) M[i * ld + k] = fma(-lij, M[k * ld + j] * inv, M[i * ld + k]);
+      const T lij = M[i * ld + j] * inv;
+      for (int k = j + 1 + BK_LANE; k <= i; k += 32)
+        M[i * ld + k] = M[i * ld + k] - lij * cj(M[k * ld + j] * inv);
     }
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) M[i * ld + j] *= inv;
-    if (threadIdx.x == 0) M[j * ld + j] = ljj;
+    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) M[i * ld + j] = M[i * ld + j] * inv;
+    if (threadIdx.x == 0) M[j * ld + j] = fromR<T>(ljj);
   }
   __syncthreads();
   return true;
 }
 
-// Linv (lower, ld li) from L (lower, ld ll): right-looking column sweep
-//   X = I; for j: X[j,:] /= l_jj; X[i,:] -= l_ij X[j,:] (i > j)
-BK_DEV void smem_lower_inverse(const double* L, int ll, double* Li, int li, int d) {
+// Linv (lower) from L (lower): X = I; for j: X[i,:] -= (l_ij / l_ii) X[j,:] (i > j)
+template <class T>
+BK_DEV void smem_lower_inverse(const T* L, int ll, T* Li, int li, int d) {
   for (int i = BK_WARP; i < d; i += BK_NWARP)
-    for (int c = BK_LANE; c < d; c += 32) Li[i * li + c] = (i == c) ? 1.0 / L[i * ll + i] : 0.0;
+    for (int c = BK_LANE; c < d; c += 32) Li[i * li + c] = fromR<T>((i == c) ? 1.0 / rl(L[i * ll + i]) : 0.0);
   __syncthreads();
   for (int j = 0; j < d; ++j) {
-    // row j of X is final (already divided by l_jj); eliminate below
     for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
-      const double f = L[i * ll + j] / L[i * ll + i];
-      for (int c = BK_LANE; c <= j; c += 32) Li[i * li + c] = fma(-f, Li[j * li + c], Li[i * li + c]);
+      const T f = L[i * ll + j] * (1.0 / rl(L[i * ll + i]));
+      for (int c = BK_LANE; c <= j; c += 32) Li[i * li + c] = Li[i * li + c] - f * Li[j * li + c];
     }
     __syncthreads();
   }
 }
 
-// C (d x d, ldc) = op(A) * op(B) over shared memory, 6x3 register block per thread for
-// d <= 96 (warps -> rows w, w+16, ...; lanes -> cols l, l+32, l+64).
-//   tb = false: C[i][j] = sum_k A[i][k] B[k][j]
-//   tb = true : C[i][j] = sum_k A[i][k] B[j][k]
-template <bool TA, bool TB>
-BK_DEV void smem_gemm(const double* A, int la, const double* B, int lb, double* C, int lc, int d, int kmax,
-                      int ncols = -1) {
+// C = op(A) op(B) in shared memory (d <= 96): 6x3 register block per thread,
+// warps -> rows w, w+16, ...; lanes -> cols l, l+32, l+64.  op = transpose (TA/TB) and/or
+// conjugate (CA/CB).
+template <class T, bool TA, bool CA, bool TB, bool CB>
+BK_DEV void smem_gemm(const T* A, int la, const T* B, int lb, T* C, int lc, int d, int kmax, int ncols = -1) {
   constexpr int RI = 6, RJ = 3;
   const int nc = ncols < 0 ? d : ncols;
   for (int i0 = BK_WARP; i0 < d; i0 += BK_NWARP * RI) {
-    double acc[RI][RJ];
+    T acc[RI][RJ];
 #pragma unroll
     for (int a = 0; a < RI; ++a)
 #pragma unroll
-      for (int b = 0; b < RJ; ++b) acc[a][b] = 0.0;
+      for (int b = 0; b < RJ; ++b) acc[a][b] = fromR<T>(0.0);
     for (int k = 0; k < kmax; ++k) {
-      double av[RI], bv[RJ];
+      T av[RI], bv[RJ];
 #pragma unroll
       for (int a = 0; a < RI; ++a) {
         const int i = i0 + a * BK_NWARP;
-        av[a] = i < d ? (TA ? A[k * la + i] : A[i * la + k]) : 0.0;
+        T v = i < d ? (TA ? A[k * la + i] : A[i * la + k]) : fromR<T>(0.0);
+        av[a] = CA ? cj(v) : v;
       }
 #pragma unroll
       for (int b = 0; b < RJ; ++b) {
         const int j = BK_LANE + 32 * b;
-        bv[b] = j < nc ? (TB ? B[j * lb + k] : B[k * lb + j]) : 0.0;
+        T v = j < nc ? (TB ? B[j * lb + k] : B[k * lb + j]) : fromR<T>(0.0);
+        bv[b] = CB ? cj(v) : v;
       }
 #pragma unroll
       for (int a = 0; a < RI; ++a)
 #pragma unroll
-        for (int b = 0; b < RJ; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < RJ; ++b) acc[a][b] = fmaT(av[a], bv[b], acc[a][b]);
     }
 #pragma unroll
     for (int a = 0; a < RI; ++a) {
@@ -187,22 +225,22 @@ BK_DEV void rr_pair(int r, int i, int dd, int& p, int& q) {
   q = max(a, b);
 }
 
-// Diagonalises symmetric A (d x d, ld la) in place; accumulates V (ld lv) if withV.
-// Returns the number of sweeps.
-BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, PSmem& S) {
+// Diagonalises Hermitian A (d x d, ld la) in place; accumulates V (ld lv) if withV.
+template <class T>
+BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& S) {
   if (withV) {
     for (int i = BK_WARP; i < d; i += BK_NWARP)
-      for (int c = BK_LANE; c < d; c += 32) V[i * lv + c] = (i == c) ? 1.0 : 0.0;
+      for (int c = BK_LANE; c < d; c += 32) V[i * lv + c] = fromR<T>((i == c) ? 1.0 : 0.0);
   }
   if (d == 1) { __syncthreads(); return 0; }
   {
     double f = 0.0;
     for (int i = BK_WARP; i < d; i += BK_NWARP)
-      for (int c = BK_LANE; c < d; c += 32) {
-        const double v = A[i * la + c];
-        f = fma(v, v, f);
-      }
+      for (int c = BK_LANE; c < d; c += 32) f += ab2(A[i * la + c]);
     f = sqrt(block_sum(f, S.red));
+    // rotate unless |a_pq| is below both the relative (Demmel-Veselic) and the absolute
+    // eps ||A||_F / d floor: entries that small move eigenvalues by less than the rounding
+    // already in the diagonal (avoids endless sweeps on noise when a diagonal is ~0)
     if (threadIdx.x == 0) S.red[30] = 0.5 * DBL_EPSILON * f / (double)d;
     __syncthreads();
   }
@@ -218,16 +256,15 @@ BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, 
         int p, q;
         rr_pair(r, i, dd, p, q);
         double c = 1.0, s = 0.0;
+        T ph = fromR<T>(1.0);
         if (q < d) {
-          const double apq = A[p * la + q];
-          const double app = A[p * la + p], aqq = A[q * la + q];
-          // rotate unless |a_pq| is below both the relative (Demmel-Veselic) and the
-          // absolute eps*||A||_F/d floor: an entry that small moves eigenvalues by less than
-          // the rounding already in the diagonal (avoids endless sweeps on noise when a
-          // diagonal entry is ~0)
-          if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq)) &&
-              fabs(apq) > S.red[30]) {
-            const double tau = (aqq - app) / (2.0 * apq);
+          const T apq = A[p * la + q];
+          const double app = rl(A[p * la + p]), aqq = rl(A[q * la + q]);
+          const double aabs = sqrt(ab2(apq));
+          if (aabs != 0.0 && aabs > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq)) && aabs > S.red[30]) {
+            double mag;
+            magph(apq, mag, ph);
+            const double tau = (aqq - app) / (2.0 * mag);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
             s = t * c;
@@ -238,38 +275,43 @@ BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, 
         S.pq[i] = q;
         S.rc[i] = c;
         S.rs[i] = s;
+        S.rph[i] = ph;
       }
       __syncthreads();
-      // 2. row rotations  A <- J^T A   (warp per pair, lanes over columns: stride-1 rows)
+      // 2. row rotations A <- J^H A  (warp per pair, lanes over columns)
       for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
         const double s = S.rs[i];
         if (s == 0.0) continue;  // warp-uniform
         const double c = S.rc[i];
-        double* ap_ = A + S.pp[i] * la;
-        double* aq_ = A + S.pq[i] * la;
+        const T ph = S.rph[i];
+        T* ap_ = A + S.pp[i] * la;
+        T* aq_ = A + S.pq[i] * la;
         for (int j = BK_LANE; j < d; j += 32) {
-          const double ap = ap_[j], aq = aq_[j];
+          const T ap = ap_[j], aq = ph * aq_[j];
           ap_[j] = c * ap - s * aq;
           aq_[j] = s * ap + c * aq;
         }
       }
       __syncthreads();
-      // 3. column rotations  A <- A J, V <- V J (lanes over rows: odd stride, conflict-free);
-      //    the annihilated pair is set to exact zero
+      // 3. column rotations A <- A J, V <- V J (lanes over rows: odd stride); the
+      //    annihilated pair is set to exact zero
       for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
         const double s = S.rs[i];
         if (s == 0.0) continue;
         const double c = S.rc[i];
+        const T phc = cj(S.rph[i]);
         const int p = S.pp[i], q = S.pq[i];
         for (int row = BK_LANE; row < d; row += 32) {
-          const double ap = A[row * la + p], aq = A[row * la + q];
-          double np_ = c * ap - s * aq, nq = s * ap + c * aq;
-          if (row == p) nq = 0.0;
-          if (row == q) np_ = 0.0;
+          const T ap = A[row * la + p], aq = phc * A[row * la + q];
+          T np_ = c * ap - s * aq, nq = s * ap + c * aq;
+          if (row == p) nq = fromR<T>(0.0);
+          if (row == q) np_ = fromR<T>(0.0);
+          if (row == p) real_diag(np_);
+          if (row == q) real_diag(nq);
           A[row * la + p] = np_;
           A[row * la + q] = nq;
           if (withV) {
-            const double vp = V[row * lv + p], vq = V[row * lv + q];
+            const T vp = V[row * lv + p], vq = phc * V[row * lv + q];
             V[row * lv + p] = c * vp - s * vq;
             V[row * lv + q] = s * vp + c * vq;
           }
@@ -284,9 +326,10 @@ BK_DEV int smem_jacobi(double* A, int la, double* V, int lv, int d, bool withV, 
   return sweep;
 }
 
-// One-sided Jacobi on M (rows x cols, ld lm), in place; returns singular values in sv[0:cols]
-BK_DEV void smem_svals(double* M, int lm, int rows, int cols, double* sv, PSmem& S) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// One-sided Jacobi on M (rows x cols, ld lm), in place; singular values into sv[0:cols]
+template <class T>
+BK_DEV void smem_svals(T* M, int lm, int rows, int cols, double* sv, PSmem<T>& S) {
+  const int lane = BK_LANE, warp = BK_WARP, nw = BK_NWARP;
   if (cols > 1) {
     const int dd = cols + (cols & 1), npairs = dd / 2;
     for (int sweep = 0; sweep < 60; ++sweep) {
@@ -297,22 +340,30 @@ BK_DEV void smem_svals(double* M, int lm, int rows, int cols, double* sv, PSmem&
           int p, q;
           rr_pair(r, i, dd, p, q);
           if (q >= cols) continue;
-          double a = 0.0, b = 0.0, g = 0.0;
+          double a = 0.0, b = 0.0, gr = 0.0, gi = 0.0;
           for (int k = lane; k < rows; k += 32) {
-            const double x = M[k * lm + p], y = M[k * lm + q];
-            a = fma(x, x, a);
-            b = fma(y, y, b);
-            g = fma(x, y, g);
+            const T x = M[k * lm + p], y = M[k * lm + q];
+            a += ab2(x);
+            b += ab2(y);
+            const T g = cj(x) * y;  // x^H y
+            gr += rl(g);
+            gi += im_part(g);
           }
           a = warp_sum(a);
           b = warp_sum(b);
-          g = warp_sum(g);
-          if (g == 0.0 || fabs(g) <= DBL_EPSILON * sqrt(a * b)) continue;
-          const double zeta = (b - a) / (2.0 * g);
+          gr = warp_sum(gr);
+          gi = warp_sum(gi);
+          const double gabs = sqrt(gr * gr + gi * gi);
+          if (gabs == 0.0 || gabs <= DBL_EPSILON * sqrt(a * b)) continue;
+          double mag;
+          T ph;
+          magph(make_scalar<T>(gr, gi), mag, ph);
+          const double zeta = (b - a) / (2.0 * mag);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          const T phc = cj(ph);
           for (int k = lane; k < rows; k += 32) {
-            const double x = M[k * lm + p], y = M[k * lm + q];
+            const T x = M[k * lm + p], y = phc * M[k * lm + q];
             M[k * lm + p] = c * x - s * y;
             M[k * lm + q] = s * x + c * y;
           }
@@ -327,7 +378,7 @@ BK_DEV void smem_svals(double* M, int lm, int rows, int cols, double* sv, PSmem&
   __syncthreads();
   for (int j = warp; j < cols; j += nw) {
     double a = 0.0;
-    for (int k = lane; k < rows; k += 32) a = fma(M[k * lm + j], M[k * lm + j], a);
+    for (int k = lane; k < rows; k += 32) a += ab2(M[k * lm + j]);
     a = warp_sum(a);
     if (lane == 0) sv[j] = sqrt(a);
   }
@@ -336,57 +387,65 @@ BK_DEV void smem_svals(double* M, int lm, int rows, int cols, double* sv, PSmem&
 
 // ---------------------------------------------------------------- one pencil attempt
 // Assembled basis: idx[0:d] raw columns, sf[0:d] scale factors.  Raw Grams at (Ar, Br, ldr).
-// On success: ev[0:want] ascending eigenvalues (ord applied), C (d x want) in M1 (ld PLD).
+// On success: ev[0:want] ascending eigenvalues, C (d x want) in M1 (ld PLD).
 // Returns 0 ok, 1 singular (either Cholesky failed).
-BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, int want, PSmem& S) {
-  double* A = S.M0;
-  double* B = S.M1;
-  double* Li = S.M2;
-  // assemble symmetrised, scaled B and its Frobenius norm
+template <class T>
+BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PSmem<T>& S) {
+  constexpr int PD = PD_<T>::v, PLD = PD + 1;
+  T* A = S.M0;
+  T* B = S.M1;
+  T* Li = S.M2;
+  // assemble (M + M^H)/2 of the scaled basis, and ||B||_F
   double fro = 0.0;
   for (int a = BK_WARP; a < d; a += BK_NWARP) {
     const int ia = S.idx[a];
     const double sa = S.sf[a];
     for (int b = BK_LANE; b < d; b += 32) {
       const int ib = S.idx[b];
-      const double v = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * sa * S.sf[b];
+      T v = (Br[ia * ldr + ib] + cj(Br[ib * ldr + ia])) * (0.5 * sa * S.sf[b]);
+      if (a == b) real_diag(v);
       B[a * PLD + b] = v;
-      fro = fma(v, v, fro);
+      fro += ab2(v);
     }
   }
   fro = sqrt(block_sum(fro, S.red));
   const double flo = kGramRtol * fmax(fro, 1e-300);
-  for (int a = threadIdx.x; a < d; a += blockDim.x) B[a * PLD + a] -= flo;
+  for (int a = threadIdx.x; a < d; a += blockDim.x) B[a * PLD + a] = B[a * PLD + a] - fromR<T>(flo);
   __syncthreads();
-  if (!smem_cholesky(B, PLD, d, S.misc)) return 1;  // core.py:193-197
+  if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:193-197
   // reload B (exact) and factor it for the reduction (sygvd's potrf)
   for (int a = BK_WARP; a < d; a += BK_NWARP) {
     const int ia = S.idx[a];
     const double sa = S.sf[a];
     for (int b = BK_LANE; b < d; b += 32) {
       const int ib = S.idx[b];
-      const double sab = sa * S.sf[b];
-      B[a * PLD + b] = 0.5 * (Br[ia * ldr + ib] + Br[ib * ldr + ia]) * sab;
-      A[a * PLD + b] = 0.5 * (Ar[ia * ldr + ib] + Ar[ib * ldr + ia]) * sab;
+      const double sab = 0.5 * sa * S.sf[b];
+      T vb = (Br[ia * ldr + ib] + cj(Br[ib * ldr + ia])) * sab;
+      T va = (Ar[ia * ldr + ib] + cj(Ar[ib * ldr + ia])) * sab;
+      if (a == b) { real_diag(vb); real_diag(va); }
+      B[a * PLD + b] = vb;
+      A[a * PLD + b] = va;
     }
   }
   __syncthreads();
-  if (!smem_cholesky(B, PLD, d, S.misc)) return 1;  // core.py:198-201
+  if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:198-201
   smem_lower_inverse(B, PLD, Li, PLD, d);
-  smem_gemm<false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A -> B (L no longer needed)
+  smem_gemm<T, false, false, false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A
   __syncthreads();
-  smem_gemm<false, true>(B, PLD, Li, PLD, A, PLD, d, d);   // Ared = T Linv^T -> A
+  smem_gemm<T, false, false, true, true>(B, PLD, Li, PLD, A, PLD, d, d);    // Ared = T Linv^H
   __syncthreads();
-  // symmetrise (the reduced matrix is symmetric in exact arithmetic)
-  for (int i = BK_WARP; i < d; i += BK_NWARP)
+  // Hermitian symmetrisation of the reduced matrix
+  for (int i = BK_WARP; i < d; i += BK_NWARP) {
     for (int j = i + 1 + BK_LANE; j < d; j += 32) {
-      const double v = 0.5 * (A[i * PLD + j] + A[j * PLD + i]);
+      const T v = (A[i * PLD + j] + cj(A[j * PLD + i])) * 0.5;
       A[i * PLD + j] = v;
-      A[j * PLD + i] = v;
+      A[j * PLD + i] = cj(v);
     }
+    if (BK_LANE == 0) real_diag(A[i * PLD + i]);
+  }
   __syncthreads();
   smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
-  for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = A[i * PLD + i];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
   __syncthreads();
   // ascending order (ties by index)
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -399,27 +458,30 @@ BK_DEV int pencil_attempt(const double* Ar, const double* Br, int ldr, int d, in
     S.ord[rank] = i;
   }
   __syncthreads();
-  // gather V[:, ord[0:want]] -> A, then C = Linv^T Vsel -> B (ld PLD)
+  // gather V[:, ord[0:want]] -> A, then C = Linv^H Vsel -> B
   for (int k = BK_WARP; k < d; k += BK_NWARP)
     for (int r = BK_LANE; r < want; r += 32) A[k * PLD + r] = B[k * PLD + S.ord[r]];
   __syncthreads();
-  smem_gemm<true, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
-  // sorted eigenvalues
-  for (int r = threadIdx.x; r < want; r += blockDim.x) A[PD * PLD - 1 - r] = S.ev[S.ord[r]];
+  smem_gemm<T, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+  double* evs = S.rc;  // rotation scratch (PD/2 >= want) is free once the Jacobi is done
+  for (int r = threadIdx.x; r < want; r += blockDim.x) evs[r] = S.ev[S.ord[r]];
   __syncthreads();
-  for (int r = threadIdx.x; r < want; r += blockDim.x) S.ev[r] = A[PD * PLD - 1 - r];
+  for (int r = threadIdx.x; r < want; r += blockDim.x) S.ev[r] = evs[r];
   __syncthreads();
   return 0;
 }
 
 // ---------------------------------------------------------------- the kernel
+template <class T>
 __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_constant__ PencilParams P) {
+  constexpr int PD = PD_<T>::v, PLD = PD + 1;
   extern __shared__ __align__(16) double sm[];
-  PSmem S;
-  S.M0 = sm;
+  PSmem<T> S;
+  S.M0 = reinterpret_cast<T*>(sm);
   S.M1 = S.M0 + PD * PLD;
   S.M2 = S.M1 + PD * PLD;
-  S.nrm = S.M2 + PD * PLD;
+  S.rph = S.M2 + PD * PLD;
+  S.nrm = reinterpret_cast<double*>(S.rph + PD / 2);
   S.sf = S.nrm + PD;
   S.ev = S.sf + PD;
   S.rc = S.ev + PD;
@@ -433,8 +495,8 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
 
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
-  const double* Ar = P.Araw + (int64_t)j * P.dmax * P.dmax;
-  const double* Br = P.Braw + (int64_t)j * P.dmax * P.dmax;
+  const T* Ar = static_cast<const T*>(P.Araw) + (int64_t)j * P.dmax * P.dmax;
+  const T* Br = static_cast<const T*>(P.Braw) + (int64_t)j * P.dmax * P.dmax;
   const int ldr = P.dmax;
 
   if (P.mode == 1) {  // plain solve_pencil(SmallPencil(A, B), want)
@@ -442,7 +504,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     for (int i = tid; i < d; i += blockDim.x) { S.idx[i] = i; S.sf[i] = 1.0; }
     __syncthreads();
     const int st = pencil_attempt(Ar, Br, ldr, d, P.want, S);
-    double* cout = P.coef + (int64_t)j * P.dmax * P.want;
+    T* cout = static_cast<T*>(P.coef) + (int64_t)j * P.dmax * P.want;
     if (st == 0) {
       for (int e = tid; e < d * P.want; e += blockDim.x) cout[e] = S.M1[(e / P.want) * PLD + e % P.want];
       for (int r = tid; r < P.want; r += blockDim.x) P.theta[(int64_t)j * P.want + r] = S.ev[r];
@@ -455,17 +517,17 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   const int w = min(P.q, P.k_act - lo);
   const int nparts = P.has_p ? 3 : 2;
   const int d0 = nparts * w;
-  double* cout = P.coef + (int64_t)j * P.dmax * P.q;  // rows part*w + i, ld w
+  T* cout = static_cast<T*>(P.coef) + (int64_t)j * P.dmax * P.q;  // rows part*w + i, ld w
 
   // column norms of the raw basis from the Gram diagonal (ppcg.py:202, 226)
-  for (int i = tid; i < d0; i += blockDim.x) S.nrm[i] = sqrt(fmax(Br[i * ldr + i], 0.0));
+  for (int i = tid; i < d0; i += blockDim.x) S.nrm[i] = sqrt(fmax(rl(Br[i * ldr + i]), 0.0));
   __syncthreads();
   double sc = 0.0;
   for (int i = 0; i < w; ++i) sc = fmax(sc, S.nrm[i]);
   sc = fmax(sc, 1e-300);
   const double floor_ = kDirFloor * sc;  // ppcg.py:198-203
 
-  // kept masks as bit sets (w <= 32 -> fits 64-bit masks for 3 parts)
+  // kept masks as bit sets (w <= 32)
   unsigned long long keptw = 0ull, keptp = 0ull;
   for (int i = 0; i < w; ++i) {
     if (S.nrm[w + i] > floor_) keptw |= 1ull << i;
@@ -475,7 +537,6 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   int fallback = 0, zero_res = 0, err = 0, attempts = 0;
   double cmax = 1.0;
   int status = 0;
-  int nw_used = 0, np_used = 0;
 
   auto assemble = [&](unsigned long long mw, unsigned long long mp) -> int {
     // basis order: X (all), kept W, kept P (ppcg.py:312-330)
@@ -498,9 +559,9 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     // x unchanged, p = 0, theta = Rayleigh quotients (ppcg.py:300-310, 255-265)
     for (int e = tid; e < nparts * w * w; e += blockDim.x) {
       const int r = e / w, c = e % w;
-      cout[e] = (r < w && r == c) ? 1.0 : 0.0;
+      cout[e] = fromR<T>((r < w && r == c) ? 1.0 : 0.0);
     }
-    for (int i = tid; i < w; i += blockDim.x) P.theta[lo + i] = Ar[i * ldr + i] / Br[i * ldr + i];
+    for (int i = tid; i < w; i += blockDim.x) P.theta[lo + i] = rl(Ar[i * ldr + i]) / rl(Br[i * ldr + i]);
     fallback = fb;
     zero_res = 1;
     cmax = 1.0;
@@ -513,44 +574,42 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     int d = 0;
     bool do_fallback = P.force_fallback != 0;
     if (!do_fallback) {
-    d = assemble(mw, mp);
-    status = pencil_attempt(Ar, Br, ldr, d, w, S);
-    ++attempts;
-    if (status != 0) {
-      mp = 0ull;  // drop P first, then shed the weakest W column (ppcg.py:335-349)
-      while (true) {
-        d = assemble(mw, mp);
-        status = pencil_attempt(Ar, Br, ldr, d, w, S);
-        ++attempts;
-        if (status == 0) break;
-        if (mw == 0ull) { err = 1; break; }
-        int worst = -1;
-        double wv = 0.0;
-        for (int i = 0; i < w; ++i)
-          if ((mw >> i & 1ull) && (worst < 0 || S.nrm[w + i] < wv)) { worst = i; wv = S.nrm[w + i]; }
-        mw &= ~(1ull << worst);
+      d = assemble(mw, mp);
+      status = pencil_attempt(Ar, Br, ldr, d, w, S);
+      ++attempts;
+      if (status != 0) {
+        mp = 0ull;  // drop P first, then shed the weakest W column (ppcg.py:335-349)
+        while (true) {
+          d = assemble(mw, mp);
+          status = pencil_attempt(Ar, Br, ldr, d, w, S);
+          ++attempts;
+          if (status == 0) break;
+          if (mw == 0ull) { err = 1; break; }
+          int worst = -1;
+          double wv = 0.0;
+          for (int i = 0; i < w; ++i)
+            if ((mw >> i & 1ull) && (worst < 0 || S.nrm[w + i] < wv)) { worst = i; wv = S.nrm[w + i]; }
+          mw &= ~(1ull << worst);
+        }
+      }
+      if (!err) {
+        // rank test: sigma_min(C_X) < 1e-14 max(||C||_2, 1)  (ppcg.py:351-356)
+        T* T1 = S.M2;  // C copy (d x w, ld w) -- Linv no longer needed
+        T* T2 = S.M0;  // C_X copy (w x w, ld w); C itself stays in M1
+        for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M1[(e / w) * PLD + e % w];
+        for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M1[(e / w) * PLD + e % w];
+        __syncthreads();
+        smem_svals(T1, w, d, w, S.rc, S);
+        double cn = 0.0;
+        for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
+        __syncthreads();
+        smem_svals(T2, w, w, w, S.rc, S);
+        double smin = S.rc[0];
+        for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
+        __syncthreads();
+        if (smin < kCxFloor * fmax(cn, 1.0)) do_fallback = true;
       }
     }
-    if (!err) {
-      nw_used = __popcll(mw);
-      np_used = __popcll(mp);
-      // rank test: sigma_min(C_X) < 1e-14 max(||C||_2, 1)  (ppcg.py:351-356)
-      double* T1 = S.M2;                 // C copy (d x w, ld w)  -- Linv no longer needed
-      double* T2 = S.M0;                 // C_X copy (w x w, ld w); C itself stays in M1
-      for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M1[(e / w) * PLD + e % w];
-      for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M1[(e / w) * PLD + e % w];
-      __syncthreads();
-      smem_svals(T1, w, d, w, S.rc, S);
-      double cn = 0.0;
-      for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
-      __syncthreads();
-      smem_svals(T2, w, w, w, S.rc, S);
-      double smin = S.rc[0];
-      for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
-      __syncthreads();
-      if (smin < kCxFloor * fmax(cn, 1.0)) do_fallback = true;
-    }
-    }  // !force_fallback
     if (do_fallback) {
       // fallback_steepest_descent: pencil over [X, kept W] (ppcg.py:231-275), no retries
       fallback = 1;
@@ -563,21 +622,18 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         status = pencil_attempt(Ar, Br, ldr, d, w, S);
         ++attempts;
         if (status != 0) err = 1;
-        nw_used = __popcll(mw);
-        np_used = 0;
       }
     }
     if (!err && !(fallback && zero_res)) {
       // coefficients: X rows direct, W/P rows un-scaled onto original columns (ppcg.py:358-363)
       double m = 0.0;
-      for (int e = tid; e < d * w; e += blockDim.x) m = fmax(m, fabs(S.M1[(e / w) * PLD + e % w]));
+      for (int e = tid; e < d * w; e += blockDim.x) m = fmax(m, sqrt(ab2(S.M1[(e / w) * PLD + e % w])));
       cmax = block_max(m, S.red);
-      for (int e = tid; e < nparts * w * w; e += blockDim.x) cout[e] = 0.0;
+      for (int e = tid; e < nparts * w * w; e += blockDim.x) cout[e] = fromR<T>(0.0);
       __syncthreads();
       for (int e = tid; e < d * w; e += blockDim.x) {
         const int a = e / w, c = e % w;
-        const int raw = S.idx[a];
-        cout[raw * w + c] = S.M1[a * PLD + c] * S.sf[a];
+        cout[S.idx[a] * w + c] = S.M1[a * PLD + c] * S.sf[a];
       }
       for (int i = tid; i < w; i += blockDim.x) P.theta[lo + i] = S.ev[i];
     }
@@ -592,25 +648,32 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   }
 }
 
+template <class T>
 static int p_smem_bytes() {
-  return (3 * PD * PLD + 3 * PD + PD + 32) * (int)sizeof(double) + (2 * PD + PD + 8) * (int)sizeof(int);
+  constexpr int PD = PD_<T>::v, PLD = PD + 1;
+  return (3 * PD * PLD + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
+         (2 * PD + PD + 8) * (int)sizeof(int);
 }
 
-}  // namespace bk
+template <class T>
+static int launch_pencils(const PencilParams& P, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pencil_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes<T>());
+    attr = true;
+  }
+  BK_COUNT();
+  pencil_kernel<T><<<P.nb, P_THREADS, p_smem_bytes<T>(), st>>>(P);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
 
-using namespace bk;
-
-extern "C" int bk_pencil_max_dim(void) { return PD; }
-
-// Device-side block_update for every subblock (see file header).  Araw/Braw from
-// bk_subblock_grams_d.  coef: nb x (dmax x q) doubles; theta: k_act; info: nb x 4 ints
-// (used_fallback, zero_residual, error, attempts); cscale: nb doubles.
-extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
-                                     double* coef, double* theta, int* info, double* cscale, int force_fallback,
-                                     void* stream) {
+template <class T>
+static int subblock_pencils(int k_act, int q, int has_p, const void* Araw, const void* Braw, void* coef,
+                            double* theta, int* info, double* cscale, int force_fallback, void* stream) {
   if (k_act <= 0 || q <= 0) return BK_ERR_ARG;
   const int dmax = (has_p ? 3 : 2) * q;
-  if (dmax > PD || q > 32) return BK_ERR_UNSUPPORTED;
+  if (dmax > PD_<T>::v || q > 32) return BK_ERR_UNSUPPORTED;
   PencilParams P{};
   P.nb = (k_act + q - 1) / q;
   P.k_act = k_act;
@@ -625,24 +688,14 @@ extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* 
   P.cscale = cscale;
   P.mode = 0;
   P.force_fallback = force_fallback ? 1 : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes());
-    attr = true;
-  }
-  BK_COUNT();
-  pencil_kernel<<<P.nb, P_THREADS, p_smem_bytes(), (cudaStream_t)stream>>>(P);
-  BK_CHECK_LAUNCH();
-  return BK_OK;
+  return launch_pencils<T>(P, (cudaStream_t)stream);
 }
 
-// Batched plain pencils: nb problems of dimension d (stride ldm*ldm, ld ldm), want smallest
-// pairs.  omega: nb x want; C: nb x (ldm x want) (ld want); status: nb x 4 ints ([2] = 1 if
-// singular).  (core.py:175-202)
-extern "C" int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
-                                   double* omega, double* C, int* status, void* stream) {
+template <class T>
+static int pencil_batched(int nb, int d, int ldm, const void* A, const void* B, int want, double* omega, void* C,
+                          int* status, void* stream) {
   if (nb <= 0 || d <= 0 || want < 1 || want > d || ldm < d) return BK_ERR_ARG;
-  if (d > PD) return BK_ERR_UNSUPPORTED;
+  if (d > PD_<T>::v) return BK_ERR_UNSUPPORTED;
   PencilParams P{};
   P.nb = nb;
   P.dmax = ldm;
@@ -654,13 +707,37 @@ extern "C" int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, cons
   P.mode = 1;
   P.want = want;
   P.rawd = d;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes());
-    attr = true;
-  }
-  BK_COUNT();
-  pencil_kernel<<<nb, P_THREADS, p_smem_bytes(), (cudaStream_t)stream>>>(P);
-  BK_CHECK_LAUNCH();
-  return BK_OK;
+  return launch_pencils<T>(P, (cudaStream_t)stream);
+}
+
+}  // namespace bk
+
+using namespace bk;
+
+extern "C" int bk_pencil_max_dim(void) { return PD_<double>::v; }
+
+// Device-side block_update for every subblock (see file header).  Araw/Braw from
+// bk_subblock_grams_*.  coef: nb x (dmax x q) scalars; theta: k_act; info: nb x 4 ints
+// (used_fallback, zero_residual, error, attempts); cscale: nb doubles.
+extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
+                                     double* coef, double* theta, int* info, double* cscale, int force_fallback,
+                                     void* stream) {
+  return subblock_pencils<double>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, stream);
+}
+extern "C" int bk_subblock_pencils_z(int k_act, int q, int has_p, const double* Araw, const double* Braw,
+                                     double* coef, double* theta, int* info, double* cscale, int force_fallback,
+                                     void* stream) {
+  return subblock_pencils<zd>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, stream);
+}
+
+// Batched plain pencils: nb problems of dimension d (stride ldm*ldm, ld ldm), want smallest
+// pairs.  omega: nb x want; C: nb x (ldm x want) (ld want); status: nb x 4 ints ([2] = 1 if
+// singular).  (core.py:175-202)
+extern "C" int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
+                                   double* omega, double* C, int* status, void* stream) {
+  return pencil_batched<double>(nb, d, ldm, A, B, want, omega, C, status, stream);
+}
+extern "C" int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, const double* B, int want,
+                                   double* omega, double* C, int* status, void* stream) {
+  return pencil_batched<zd>(nb, d, ldm, A, B, want, omega, C, status, stream);
 }

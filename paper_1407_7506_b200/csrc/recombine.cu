@@ -25,7 +25,28 @@ struct RecombParams {
   double* outX[2];          // side -> X' / AX'
   double* outP[2];          // side -> P' / AP'
   unsigned long long* flags;  // [0] nonfinite (0/1), [1] max|X'| bits, [2] max|P'| bits
+  int cplx;                   // real view of complex data: columns pair up as (re, im)
 };
+
+// complex coefficients (block j: nparts*w x w, ld w, stride dmax*q) -> real expanded
+// (2 nparts w x 2w, ld 2w, stride (2 dmax)(2 q)) so the real kernel applies X C on views
+__global__ void k_expand_coef(int k_act, int q, int nparts, const double* __restrict__ cz, double* __restrict__ cr) {
+  const int j = blockIdx.y;
+  const int w = min(q, k_act - j * q);
+  const int dmax = nparts * q;
+  const double* src = cz + (int64_t)j * dmax * q * 2;
+  double* dst = cr + (int64_t)j * (2 * dmax) * (2 * q);
+  const int rows = nparts * w;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * w; e += gridDim.x * blockDim.x) {
+    const int i = e / w, c = e % w;
+    const double gr = src[2 * (i * w + c)], gi = src[2 * (i * w + c) + 1];
+    const int ld = 2 * w;
+    dst[(2 * i) * ld + 2 * c] = gr;
+    dst[(2 * i) * ld + 2 * c + 1] = gi;
+    dst[(2 * i + 1) * ld + 2 * c] = -gi;
+    dst[(2 * i + 1) * ld + 2 * c + 1] = gr;
+  }
+}
 
 BK_DEV int pad_a(int w) { int l = (w + 3) & ~3; if ((l & 7) == 0) l += 4; return l; }   // l % 8 == 4
 BK_DEV int pad_b(int w) { int l = (w + 7) & ~7; return l + 4; }  // l % 8 == 4: 4 rows -> 4 disjoint 8-bank groups
@@ -110,6 +131,7 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
 #pragma unroll
     for (int b = 0; b < R_QMAX / 8; ++b) {
       if (b >= ntv) continue;
+      double x2 = 0.0, p2 = 0.0;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = b * 8 + 2 * fk + e;
@@ -120,8 +142,17 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
         ox[off] = xv;
         op[off] = pv;
         nonfin |= !isfinite(xv) || !isfinite(pv);
-        mx = fmax(mx, fabs(xv));
-        mp = fmax(mp, fabs(pv));
+        if (P.cplx) {  // (re, im) pair of one complex entry: modulus like np.abs
+          x2 = fma(xv, xv, x2);
+          p2 = fma(pv, pv, p2);
+        } else {
+          mx = fmax(mx, fabs(xv));
+          mp = fmax(mp, fabs(pv));
+        }
+      }
+      if (P.cplx) {
+        mx = fmax(mx, sqrt(x2));
+        mp = fmax(mp, sqrt(p2));
       }
     }
   }
@@ -141,15 +172,46 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
 
 using namespace bk;
 
+static int recombine(int64_t n, int k_act, int q, int has_p, const double* coef, const double* X, const double* W,
+                     const double* P_, const double* AX, const double* AW, const double* AP, double* Xo, double* Po,
+                     double* AXo, double* APo, int64_t ld, int64_t c0, unsigned long long* flags, int cplx,
+                     void* stream);
+
 // flags: 3 x uint64 on device, zeroed by the caller.  Outputs may not alias inputs.
 extern "C" int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double* coef,
                                        const double* X, const double* W, const double* P_, const double* AX,
                                        const double* AW, const double* AP, double* Xo, double* Po, double* AXo,
                                        double* APo, int64_t ld, int64_t c0, unsigned long long* flags,
                                        void* stream) {
+  return recombine(n, k_act, q, has_p, coef, X, W, P_, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags, 0, stream);
+}
+
+// complex128: blocks interleaved, ld/c0 in complex elements, coef complex (nb x dmax x q);
+// coef_tmp: real scratch of nb x (2 dmax)(2 q) doubles for the expanded coefficients.
+extern "C" int bk_subblock_recombine_z(int64_t n, int k_act, int q, int has_p, const double* coef,
+                                       const double* X, const double* W, const double* P_, const double* AX,
+                                       const double* AW, const double* AP, double* Xo, double* Po, double* AXo,
+                                       double* APo, int64_t ld, int64_t c0, unsigned long long* flags,
+                                       double* coef_tmp, void* stream) {
+  if (n <= 0 || k_act <= 0 || q <= 0) return BK_ERR_ARG;
+  const int nb = (k_act + q - 1) / q;
+  const int nparts = has_p ? 3 : 2;
+  dim3 grid((unsigned)lmin(64, (nparts * q * q + 255) / 256), nb);
+  BK_COUNT();
+  k_expand_coef<<<grid, 256, 0, (cudaStream_t)stream>>>(k_act, q, nparts, coef, coef_tmp);
+  BK_CHECK_LAUNCH();
+  return recombine(n, 2 * k_act, 2 * q, has_p, coef_tmp, X, W, P_, AX, AW, AP, Xo, Po, AXo, APo, 2 * ld, 2 * c0,
+                   flags, 1, stream);
+}
+
+static int recombine(int64_t n, int k_act, int q, int has_p, const double* coef, const double* X, const double* W,
+                     const double* P_, const double* AX, const double* AW, const double* AP, double* Xo, double* Po,
+                     double* AXo, double* APo, int64_t ld, int64_t c0, unsigned long long* flags, int cplx,
+                     void* stream) {
   if (n <= 0 || k_act <= 0 || q <= 0) return BK_ERR_ARG;
   if (q > R_QMAX) return BK_ERR_UNSUPPORTED;
   RecombParams R{};
+  R.cplx = cplx;
   R.n = n;
   R.k_act = k_act;
   R.q = q;

@@ -66,11 +66,14 @@ class Workspace:
 _WS = {}
 
 
-def workspace():
-    dev = torch.cuda.current_device()
-    ws = _WS.get(dev)
+def workspace(kind="gram"):
+    """One zeroed scratch buffer per reduction family and device.  Each family keeps its
+    tickets at offset 0 and resets them after use; families must not share a buffer (one
+    family's partials would overwrite another's tickets)."""
+    key = (torch.cuda.current_device(), kind)
+    ws = _WS.get(key)
     if ws is None:
-        ws = _WS[dev] = Workspace(torch.device("cuda", dev))
+        ws = _WS[key] = Workspace(torch.device("cuda", key[0]))
     return ws
 
 
@@ -165,7 +168,7 @@ def tsgemm(xs, gs, ys, alpha=1.0, beta=0.0, zs=None, rowscale=None, upper=False,
     ZP, _d = _lib.ptr_array(zp) if zp is not None else (None, None)
     if metric is not None:
         nbytes = _lib.load().bk_tsgemm_ws_bytes(n, N)
-        wp, wb = workspace().get(nbytes)
+        wp, wb = workspace("metric").get(nbytes)
         mp = metric.data_ptr()
     else:
         wp, wb, mp = None, 0, None
@@ -188,7 +191,7 @@ def sumsq(x, out):
     """out[0] = ||x||_F^2 (deterministic)."""
     px, n, mr, lx = real_view(x)
     lib = _lib.load()
-    wp, wb = workspace().get(lib.bk_sumsq_ws_bytes())
+    wp, wb = workspace("sumsq").get(lib.bk_sumsq_ws_bytes())
     _lib.call("bk_sumsq_d", n, mr, px, lx, out.data_ptr(), wp, wb, stream_ptr())
     return out
 
@@ -219,7 +222,7 @@ def rr_residual(v, av, omega, rowscale, w_out, colnorm2):
     n, kt = v.shape
     cplx = 1 if v.dtype == C128 else 0
     lib = _lib.load()
-    wp, wb = workspace().get(lib.bk_rr_residual_ws_bytes(kt))
+    wp, wb = workspace("rr").get(lib.bk_rr_residual_ws_bytes(kt))
     _lib.call("bk_rr_residual_d", n, kt, cplx, v.data_ptr(), ld_of(v), av.data_ptr(), ld_of(av),
               omega.data_ptr(), rowscale.data_ptr() if rowscale is not None else None,
               w_out.data_ptr() if w_out is not None else None,
@@ -240,29 +243,47 @@ def spmm_csr(rowptr, col, val, x, y):
 
 
 # ----------------------------------------------------------------------------- subblock path
-def subblock_grams(n, k_act, q, has_p, X, W, P, AX, AW, AP, ld, c0, araw, braw):
+def subblock_grams(n, k_act, q, has_p, X, W, P, AX, AW, AP, ld, c0, araw, braw, tmp=None):
+    """Raw pencil Grams of every subblock.  Pointers are raw device addresses of the state
+    buffers (ld, c0 in elements of the state dtype); complex needs real scratch ``tmp``
+    (two tensors of nb*(2*dmax)^2 doubles)."""
     lib = _lib.load()
-    wp, wb = workspace().get(lib.bk_subblock_grams_ws_bytes(n, k_act, q, 1 if has_p else 0))
-    _lib.call("bk_subblock_grams_d", n, k_act, q, 1 if has_p else 0, X, W, P if has_p else None, AX, AW,
+    hp = 1 if has_p else 0
+    if araw.dtype == C128:
+        wp, wb = workspace().get(lib.bk_subblock_grams_ws_bytes(n, 2 * k_act, 2 * q, hp))
+        _lib.call("bk_subblock_grams_z", n, k_act, q, hp, X, W, P if has_p else None, AX, AW,
+                  AP if has_p else None, ld, c0, araw.data_ptr(), braw.data_ptr(), tmp[0].data_ptr(),
+                  tmp[1].data_ptr(), wp, wb, stream_ptr())
+        return
+    wp, wb = workspace().get(lib.bk_subblock_grams_ws_bytes(n, k_act, q, hp))
+    _lib.call("bk_subblock_grams_d", n, k_act, q, hp, X, W, P if has_p else None, AX, AW,
               AP if has_p else None, ld, c0, araw.data_ptr(), braw.data_ptr(), wp, wb, stream_ptr())
 
 
 def subblock_pencils(k_act, q, has_p, araw, braw, coef, theta, info, cscale, force_fallback=False):
-    _lib.call("bk_subblock_pencils_d", k_act, q, 1 if has_p else 0, araw.data_ptr(), braw.data_ptr(),
+    name = "bk_subblock_pencils_z" if araw.dtype == C128 else "bk_subblock_pencils_d"
+    _lib.call(name, k_act, q, 1 if has_p else 0, araw.data_ptr(), braw.data_ptr(),
               coef.data_ptr(), theta.data_ptr(), info.data_ptr(), cscale.data_ptr(),
               1 if force_fallback else 0, stream_ptr())
 
 
-def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags):
+def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags,
+                       coef_tmp=None):
+    if coef.dtype == C128:
+        _lib.call("bk_subblock_recombine_z", n, k_act, q, 1 if has_p else 0, coef.data_ptr(), X, W,
+                  P if has_p else None, AX, AW, AP if has_p else None, Xo, Po, AXo, APo, ld, c0,
+                  flags.data_ptr(), coef_tmp.data_ptr(), stream_ptr())
+        return
     _lib.call("bk_subblock_recombine_d", n, k_act, q, 1 if has_p else 0, coef.data_ptr(), X, W,
               P if has_p else None, AX, AW, AP if has_p else None, Xo, Po, AXo, APo, ld, c0,
               flags.data_ptr(), stream_ptr())
 
 
 def pencil_batched(a, b, want, omega, c, status):
-    """a, b: (nb, ldm, ldm) float64; solves nb pencils of dimension ldm."""
+    """a, b: (nb, ldm, ldm) float64/complex128; solves nb pencils of dimension ldm."""
     nb, d, _ = a.shape
-    _lib.call("bk_pencil_batched_d", nb, d, d, a.data_ptr(), b.data_ptr(), want, omega.data_ptr(),
+    name = "bk_pencil_batched_z" if a.dtype == C128 else "bk_pencil_batched_d"
+    _lib.call(name, nb, d, d, a.data_ptr(), b.data_ptr(), want, omega.data_ptr(),
               c.data_ptr(), status.data_ptr(), stream_ptr())
 
 

@@ -160,6 +160,9 @@ class PPCGSolver:
         if opts is None:
             raise ValueError("opts is required")
         opts.validate()
+        from . import _lib
+
+        _lib.load()  # DeviceError without the library or a GPU: there is no CPU fallback
         self.torch, self.K = torch, K
         self.opts = opts
         self.a = a
@@ -200,12 +203,16 @@ class PPCGSolver:
         torch = self.torch
         n, kt = self.n, self.kt
         z = lambda *s, dt=None: torch.zeros(s, dtype=dt or self.tdt, device="cuda")  # noqa: E731
-        self.XF = [z(n, kt), z(n, kt)]
-        self.AXF = [z(n, kt), z(n, kt)]
-        self.W = z(n, kt)
-        self.AW = z(n, kt)
-        self.P = [z(n, kt), z(n, kt)]
-        self.AP = [z(n, kt), z(n, kt)]
+        # n x k_total blocks with the row stride padded to a multiple of 4 elements (16/32-byte
+        # aligned rows for vector and bulk-tensor loads); columns keep global positions
+        self.ldp = (kt + 3) // 4 * 4
+        blk = lambda: z(n, self.ldp)[:, :kt]  # noqa: E731
+        self.XF = [blk(), blk()]
+        self.AXF = [blk(), blk()]
+        self.W = blk()
+        self.AW = blk()
+        self.P = [blk(), blk()]
+        self.AP = [blk(), blk()]
         self.xi = 0   # current X/AX buffer
         self.pi = 0   # current P/AP buffer
         self.Gm = z(kt, kt)
@@ -235,6 +242,11 @@ class PPCGSolver:
         self.araw = z(nbmax * dmax * dmax)
         self.braw = z(nbmax * dmax * dmax)
         self.coef = z(nbmax * dmax * q)
+        if self.cplx:  # real scratch for Grams of interleaved views and expanded coefficients
+            self.gtmp = (z(nbmax * 4 * dmax * dmax, dt=torch.float64), z(nbmax * 4 * dmax * dmax, dt=torch.float64))
+            self.coef_tmp = z(nbmax * 4 * dmax * q, dt=torch.float64)
+        else:
+            self.gtmp, self.coef_tmp = None, None
         self.theta = z(kt, dt=torch.float64)
         self.info = torch.zeros(nbmax * 4, dtype=torch.int32, device="cuda")
         self.cscale = z(nbmax, dt=torch.float64)
@@ -504,14 +516,15 @@ class PPCGSolver:
         Ps, APs = self.P[psrc], self.AP[psrc]
         K.subblock_grams(self.n, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
                          AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
-                         self.araw, self.braw)
+                         self.araw, self.braw, tmp=self.gtmp)
         K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
                            self.cscale)
         self.flags64.zero_()
         K.subblock_recombine(self.n, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
                              Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
                              self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
-                             self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64)
+                             self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
+                             coef_tmp=self.coef_tmp)
         nb = (ka + q - 1) // q
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
@@ -596,20 +609,20 @@ class PPCGSolver:
         c0 = self._c0r(L + lo)
         XFp, AXFp = self.XF[prev_idx], self.AXF[prev_idx]
         K.subblock_grams(self.n, w, w, False, XFp.data_ptr(), self.W.data_ptr(), 0, AXFp.data_ptr(),
-                         self.AW.data_ptr(), 0, self._ldr(), c0, self.araw, self.braw)
+                         self.AW.data_ptr(), 0, self._ldr(), c0, self.araw, self.braw, tmp=self.gtmp)
         K.subblock_pencils(w, w, False, self.araw, self.braw, self.coef, self.theta, self.info, self.cscale,
                            force_fallback=True)
         self.flags64.zero_()
         K.subblock_recombine(self.n, w, w, False, self.coef, XFp.data_ptr(), self.W.data_ptr(), 0,
                              AXFp.data_ptr(), self.AW.data_ptr(), 0, self.XF[self.xi].data_ptr(),
                              self.P[self.pi].data_ptr(), self.AXF[self.xi].data_ptr(),
-                             self.AP[self.pi].data_ptr(), self._ldr(), c0, self.flags64)
+                             self.AP[self.pi].data_ptr(), self._ldr(), c0, self.flags64, coef_tmp=self.coef_tmp)
         self._fetch((self.info, self.h_info))
         if int(self.h_info.numpy()[2]) != 0:
             raise SingularGramError("Gram matrix numerically singular in fallback pencil")
 
     def _ldr(self):
-        return self.kt  # all state buffers share ld = k_total (complex: in complex elements)
+        return self.ldp  # all state buffers share the padded row stride (complex: in complex elements)
 
     def _c0r(self, c):
         return c

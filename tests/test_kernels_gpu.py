@@ -221,6 +221,52 @@ def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
         assert abs(cs[j] - r.coeff_scale) <= 1e-8 * r.coeff_scale
 
 
+@pytest.mark.parametrize("n,m,q,with_p", [(300, 6, 3, True), (400, 20, 8, True), (400, 20, 8, False)])
+def test_complex_subblock_update_vs_oracle(cuda, n, m, q, with_p):
+    """complex Hermitian subblock update: Grams of interleaved views, complex Jacobi pencils,
+    expanded-coefficient recombination vs the oracle's block_update."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    a = sym_matrix(n, 80, True)
+    x = orthonormal(n, m, 81, True)
+    w = gauss(n, m, 82, True)
+    w -= x @ (x.conj().T @ w)
+    p = None
+    if with_p:
+        p = 1e-2 * gauss(n, m, 83, True)
+        p -= x @ (x.conj().T @ p)
+    blocks = [x, w, p, a @ x, a @ w, a @ p if with_p else None]
+    bufs = [dev(b, torch) if b is not None else torch.zeros((n, m), dtype=torch.complex128, device="cuda") for b in blocks]
+    outs = [torch.zeros_like(bufs[0]) for _ in range(4)]
+    nb = (m + q - 1) // q
+    dmax = (3 if with_p else 2) * q
+    z = lambda k, dt=torch.complex128: torch.zeros(k, dtype=dt, device="cuda")  # noqa: E731
+    araw, braw, coef = z(nb * dmax * dmax), z(nb * dmax * dmax), z(nb * dmax * q)
+    tmp = (z(nb * 4 * dmax * dmax, torch.float64), z(nb * 4 * dmax * dmax, torch.float64))
+    ctmp = z(nb * 4 * dmax * q, torch.float64)
+    theta, cs = z(m, torch.float64), z(nb, torch.float64)
+    info = torch.zeros(nb * 4, dtype=torch.int32, device="cuda")
+    flags = torch.zeros(3, dtype=torch.int64, device="cuda")
+    ptr = [b.data_ptr() for b in bufs]
+    K.subblock_grams(n, m, q, with_p, *ptr, m, 0, araw, braw, tmp=tmp)
+    K.subblock_pencils(m, q, with_p, araw, braw, coef, theta, info, cs)
+    K.subblock_recombine(n, m, q, with_p, coef, *ptr, *[o.data_ptr() for o in outs], m, 0, flags, coef_tmp=ctmp)
+    xo = outs[0].cpu().numpy()
+    th = theta.cpu().numpy()
+    inf = info.cpu().numpy().reshape(nb, 4)
+    for lo, hi in O.partition(m, q):
+        r = O.subblock_update(x[:, lo:hi], w[:, lo:hi], None if p is None else p[:, lo:hi],
+                              blocks[3][:, lo:hi], blocks[4][:, lo:hi], None if p is None else blocks[5][:, lo:hi])
+        j = lo // q
+        assert inf[j, 2] == 0 and inf[j, 0] == int(r.used_fallback)
+        assert np.allclose(th[lo:hi], r.theta, atol=1e-11 * max(1, np.abs(r.theta).max()), rtol=0)
+        for c in range(hi - lo):
+            ph = np.vdot(xo[:, lo + c], r.x[:, c])
+            ph /= abs(ph)
+            assert np.allclose(xo[:, lo + c] * ph, r.x[:, c], atol=1e-9)
+
+
 def test_subblock_engineered_fallback(cuda):
     """alpha = 0 case of test_ppcg.py:108-117: x an exact eigenvector, w a lower one."""
     torch = cuda
