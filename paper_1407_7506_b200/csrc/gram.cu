@@ -3,30 +3,32 @@
 // Replaces the reference's block_inner (blockeig core.py:43-49, `x.conj().T @ y`, OpenBLAS
 // dgemm) at every call site on the PPCG hot path: the full Grams of _apply_projection
 // (ppcg.py:441-445), the orthonormality Gram (ppcg.py:448-453), the residual Gram
-// (ppcg.py:630,758) and the per-q-block pencil Grams of _solve_subblock_pencil
-// (ppcg.py:206-211).
+// (ppcg.py:630,758), proj_defect (ppcg.py:688-692) and the per-q-block pencil Grams of
+// _solve_subblock_pencil (ppcg.py:206-211).
 //
-// Design (DESIGN.md §4.2):
-//  * reduction dimension = rows n (huge); the output is small (m1 x m2).  The row range is
-//    split into `nchunks` contiguous chunks; each CTA computes one 64x64 output tile over
-//    one chunk, 16 rows per pipeline stage, 4-stage cp.async ring.
+// Design (DESIGN.md §4.1):
+//  * the reduction dimension is the row count n (huge); the output is small.  Rows are
+//    split into chunks; each CTA computes one BM x BN output tile over one chunk, 16 rows
+//    per stage through a cp.async ring (16-byte copies when offsets allow, else 8-byte).
+//  * configurations follow the shape that saturates the B200 DMMA pipe (measured: cuBLAS'
+//    64x128x16, 3-stage, 4-warp DGEMM runs the tensor pipe at 96%): 4 warps with 32x64 warp
+//    tiles, two CTAs per SM so one CTA's barrier waits are covered by the other's DMMAs.
+//    "big" = 64x128 (k_total-wide Grams), "small" = 64x64 (pencil-sized outputs).
+//  * fragments are double buffered; warps with a fully valid tile issue unpredicated DMMAs
+//    (a predicated mma.sync costs a WARPSYNC + NOP per instruction).
 //  * split-K partials go to a workspace; the LAST CTA to finish a tile (atomic ticket)
-//    sums the partials in fixed chunk order -> results are bitwise run-to-run
-//    deterministic, with a single launch.
-//  * operands are "virtual concatenations" of up to 3 column segments of row-major
-//    blocks, so S = [X_j | W_j | P_j] of a subblock is never materialised.
-//  * symmetric mode (X == Y) computes only tiles ti <= tj and mirrors; diagonal tiles
-//    write the upper triangle and mirror it, so the result is exactly symmetric.
-//  * warps skip 8x8 MMA tiles that lie entirely outside the output, so ragged widths
-//    (m = 523, 1045, ...) waste at most 7 columns of tensor work.
+//    sums the partials in fixed chunk order -> bitwise run-to-run deterministic, one launch.
+//  * operands are virtual concatenations of up to 3 column segments of row-major blocks,
+//    so S = [X_j | W_j | P_j] of a subblock is never materialised.
+//  * symmetric mode (X == Y) skips tiles below the diagonal and mirrors the upper triangle,
+//    so the result is exactly symmetric.
+//  * row strides of BM+4 / BN+4 (= 4 mod 16 doubles) make the half-warp fragment loads
+//    (4 rows x 4 doubles) conflict-free.
 #include "common.cuh"
 
 namespace bk {
 
-constexpr int G_BM = 64, G_BN = 64, G_BK = 16, G_STAGES = 4, G_THREADS = 128;
-constexpr int G_PAD = 4;  // row stride 68 = 4 mod 16 doubles: half-warp fragment loads hit 4 disjoint 8-bank groups
-constexpr int G_LDS = G_BM + G_PAD;
-constexpr int G_WM = 4, G_WN = 4;           // warp tile = 32 x 32 (4 x 4 MMA tiles)
+constexpr int G_BK = 16;
 
 struct Seg {
   const double* p;
@@ -62,16 +64,17 @@ struct GramParams {
   int k_act, q, has_p, dmax;
   double* outA;               // nb blocks of dmax x dmax (A_hat raw)
   double* outB;               // nb blocks of dmax x dmax (B_hat raw)
-  int tiles_dim;              // tiles per dim for dmax
   // common
   int64_t nrows;
   int nchunks;
   int64_t chunk_rows;
   int max_tiles;              // tiles per problem slot in the grid
-  double* ws;                 // partials: [prob][tile][chunk][64*64]
+  int vec16;                  // all segment offsets/leading dims even: 16-byte copies
+  double* ws;                 // partials: [prob][tile][chunk][BM*BN]
   int* tickets;               // [prob][tile]
 };
 
+template <int BM, int BN>
 BK_DEV void subblock_problem(const GramParams& P, int b, GramProblem& g) {
   int j = b >> 1, kind = b & 1;
   int lo = j * P.q;
@@ -88,29 +91,76 @@ BK_DEV void subblock_problem(const GramParams& P, int b, GramProblem& g) {
   g.C = (kind ? P.outB : P.outA) + (int64_t)j * P.dmax * P.dmax;
   g.ldc = P.dmax;
   g.symmetric = kind;
-  g.tiles_m = g.tiles_n = (g.M + G_BM - 1) / G_BM;
-  g.ntiles = g.symmetric ? g.tiles_m * (g.tiles_m + 1) / 2 : g.tiles_m * g.tiles_n;
+  g.tiles_m = (g.M + BM - 1) / BM;
+  g.tiles_n = (g.N + BN - 1) / BN;
+  g.ntiles = g.tiles_m * g.tiles_n;
 }
 
-BK_DEV const double* seg_col_ptr(const Seg* segs, int nseg, int c, int64_t& ld, bool& valid) {
+// pointer to virtual column c (nullptr if outside the segments); ld of its segment
+BK_DEV const double* seg_col(const Seg* segs, int nseg, int c, int64_t& ld, int& seg) {
   int off = 0;
   for (int s = 0; s < nseg; ++s) {
     if (c < off + segs[s].width) {
       ld = segs[s].ld;
-      valid = true;
+      seg = s;
       return segs[s].p + segs[s].col0 + (c - off);
     }
     off += segs[s].width;
   }
-  valid = false;
   ld = 0;
+  seg = -1;
   return nullptr;
 }
 
-__global__ void __launch_bounds__(G_THREADS, 2) gram_kernel(const __grid_constant__ GramParams P) {
+// Per-thread loader for a pair of adjacent virtual columns
+struct PairCol {
+  const double* p0;   // column c
+  const double* p1;   // column c+1
+  int64_t ld0, ld1;
+  bool v0, v1, fused; // fused: c and c+1 contiguous and 16-byte aligned -> one 16-byte copy
+};
+
+BK_DEV PairCol make_pair(const Seg* segs, int nseg, int M, int c, bool vec16) {
+  PairCol pc;
+  int s0, s1;
+  pc.p0 = seg_col(segs, nseg, c, pc.ld0, s0);
+  pc.p1 = seg_col(segs, nseg, c + 1, pc.ld1, s1);
+  pc.v0 = pc.p0 != nullptr && c < M;
+  pc.v1 = pc.p1 != nullptr && c + 1 < M;
+  pc.fused = vec16 && pc.v0 && pc.v1 && s0 == s1 && ((reinterpret_cast<uintptr_t>(pc.p0) & 15) == 0);
+  if (!pc.v0) pc.p0 = segs[0].p;
+  if (!pc.v1) pc.p1 = segs[0].p;
+  return pc;
+}
+
+BK_DEV void load_pair(double* dst, const PairCol& pc, int64_t row, bool rv) {
+  if (pc.fused) {
+    cp_async16(dst, rv ? pc.p0 + row * pc.ld0 : pc.p0, rv ? 16 : 0);
+  } else {
+    cp_async8(dst, rv && pc.v0 ? pc.p0 + row * pc.ld0 : pc.p0, rv && pc.v0);
+    cp_async8(dst + 1, rv && pc.v1 ? pc.p1 + row * pc.ld1 : pc.p1, rv && pc.v1);
+  }
+}
+
+template <int BM_, int BN_, int STAGES_, int MINB_, int SLOTS_>
+struct GCfg {
+  static constexpr int BM = BM_, BN = BN_, STAGES = STAGES_, MINB = MINB_, SLOTS_PER_SM = SLOTS_;
+  static constexpr int THREADS = 128;             // 2 x 2 warps
+  static constexpr int WM = BM / 2 / 8, WN = BN / 2 / 8;
+  static constexpr int LDX = BM + 4, LDY = BN + 4; // = 4 mod 16
+  static constexpr int XPAIRS = G_BK * BM / 2 / THREADS, YPAIRS = G_BK * BN / 2 / THREADS;
+  static constexpr int XSTAGE = G_BK * LDX, YSTAGE = G_BK * LDY;
+  static constexpr int SMEM = STAGES * (XSTAGE + YSTAGE) * (int)sizeof(double);
+};
+using Big = GCfg<64, 128, 4, 2, 2>;
+using Small = GCfg<64, 64, 4, 3, 3>;
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_constant__ GramParams P) {
+  constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN, ST = C::STAGES;
   extern __shared__ __align__(16) double smem[];
-  double* Xs = smem;                                   // [STAGES][BK][LDS]
-  double* Ys = smem + G_STAGES * G_BK * G_LDS;         // [STAGES][BK][LDS]
+  double* Xs = smem;                    // [STAGES][BK][LDX]
+  double* Ys = smem + ST * C::XSTAGE;   // [STAGES][BK][LDY]
   __shared__ int s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -120,100 +170,110 @@ __global__ void __launch_bounds__(G_THREADS, 2) gram_kernel(const __grid_constan
 
   GramProblem g;
   if (P.explicit_list) g = P.prob[pidx];
-  else subblock_problem(P, pidx, g);
+  else subblock_problem<BM, BN>(P, pidx, g);
   if (slot >= g.ntiles) return;
-
-  int ti, tj;
-  if (g.symmetric) {  // slot -> (ti, tj), ti <= tj, row-major over the upper triangle
-    int t = slot, r = 0, len = g.tiles_m;
-    while (t >= len) { t -= len; ++r; --len; }
-    ti = r; tj = r + t;
-  } else {
-    ti = slot / g.tiles_n; tj = slot % g.tiles_n;
-  }
-  const int m0 = ti * G_BM, n0 = tj * G_BN;
+  const int ti = slot / g.tiles_n, tj = slot % g.tiles_n;
+  const int m0 = ti * BM, n0 = tj * BN;
+  if (g.symmetric && n0 + BN <= m0) return;  // entirely below the diagonal: mirrored
 
   const int64_t r_begin = (int64_t)chunk * P.chunk_rows;
-  const int64_t r_end = min(P.nrows, r_begin + P.chunk_rows);
+  const int64_t r_end = lmin(P.nrows, r_begin + P.chunk_rows);
   const int nstages = (int)((r_end - r_begin + G_BK - 1) / G_BK);
 
-  // each thread loads a fixed column of each operand: col = tid % 64, rows tid/64 + 2i
-  const int lc = tid & 63, lr = tid >> 6;
-  int64_t ldx, ldy;
-  bool vx, vy;
-  const double* px = seg_col_ptr(g.xs, g.nxs, m0 + lc, ldx, vx);
-  const double* py = seg_col_ptr(g.ys, g.nys, n0 + lc, ldy, vy);
-  vx = vx && (m0 + lc < g.M);
-  vy = vy && (n0 + lc < g.N);
+  // loader: X pairs: column (tid % (BM/2)) * 2, rows tid / (BM/2) + step i; Y likewise
+  constexpr int XCPR = BM / 2, YCPR = BN / 2;
+  const int xc = (tid % XCPR) * 2, xr = tid / XCPR;
+  const int yc = (tid % YCPR) * 2, yr = tid / YCPR;
+  const PairCol px = make_pair(g.xs, g.nxs, g.M, m0 + xc, P.vec16);
+  const PairCol py = make_pair(g.ys, g.nys, g.N, n0 + yc, P.vec16);
 
   auto load_stage = [&](int s, int st) {
     const int64_t rb = r_begin + (int64_t)s * G_BK;
-    double* xd = Xs + st * G_BK * G_LDS;
-    double* yd = Ys + st * G_BK * G_LDS;
+    double* xd = Xs + st * C::XSTAGE;
+    double* yd = Ys + st * C::YSTAGE;
 #pragma unroll
-    for (int i = 0; i < G_BK / 2; ++i) {
-      const int kr = lr + 2 * i;
+    for (int i = 0; i < C::XPAIRS; ++i) {
+      const int kr = xr + (C::THREADS / XCPR) * i;
       const int64_t row = rb + kr;
-      const bool rv = row < r_end;
-      cp_async8(xd + kr * G_LDS + lc, rv && vx ? px + row * ldx : px, rv && vx);
-      cp_async8(yd + kr * G_LDS + lc, rv && vy ? py + row * ldy : py, rv && vy);
+      load_pair(xd + kr * LDX + xc, px, row, row < r_end);
+    }
+#pragma unroll
+    for (int i = 0; i < C::YPAIRS; ++i) {
+      const int kr = yr + (C::THREADS / YCPR) * i;
+      const int64_t row = rb + kr;
+      load_pair(yd + kr * LDY + yc, py, row, row < r_end);
     }
   };
 
-  // warp tile placement and valid MMA-tile counts (skip tiles entirely outside M x N)
+  // warp placement (2 x 2); valid DMMA tiles (skip tiles outside M x N / below the diagonal)
   const int wm = warp >> 1, wn = warp & 1;
-  const int wm0 = m0 + wm * 8 * G_WM, wn0 = n0 + wn * 8 * G_WN;
-  const int mtv = max(0, min(G_WM, (g.M - wm0 + 7) / 8));
-  const int ntv = max(0, min(G_WN, (g.N - wn0 + 7) / 8));
-  const bool warp_active = mtv > 0 && ntv > 0 && !(g.symmetric && ti == tj && wm > wn);
+  const int wm0 = m0 + wm * 8 * WM, wn0 = n0 + wn * 8 * WN;
+  const int mtv = max(0, min(WM, (g.M - wm0 + 7) / 8));
+  const int ntv = max(0, min(WN, (g.N - wn0 + 7) / 8));
+  const bool below = g.symmetric && (wn0 + 8 * WN <= wm0);
+  const bool warp_active = mtv > 0 && ntv > 0 && !below;
+  const bool full_tile = mtv == WM && ntv == WN;
 
-  double acc[G_WM][G_WN][2];
+  double acc[WM][WN][2];
 #pragma unroll
-  for (int a = 0; a < G_WM; ++a)
+  for (int a = 0; a < WM; ++a)
 #pragma unroll
-    for (int b = 0; b < G_WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < G_STAGES - 1; ++s) {
+  for (int s = 0; s < ST - 1; ++s) {
     if (s < nstages) load_stage(s, s);
     cp_async_commit();
   }
 
   const int fr = lane & 3, fc = lane >> 2;  // fragment: k = lane%4, m/n = lane/4
+  const int xoff = fr * LDX + wm * 8 * WM + fc, yoff = fr * LDY + wn * 8 * WN + fc;
   for (int s = 0; s < nstages; ++s) {
-    cp_async_wait<G_STAGES - 2>();
+    cp_async_wait<ST - 2>();
     __syncthreads();
     {
-      const int sn = s + G_STAGES - 1;
-      if (sn < nstages) load_stage(sn, sn % G_STAGES);
+      const int sn = s + ST - 1;
+      if (sn < nstages) load_stage(sn, sn % ST);
       cp_async_commit();
     }
     if (warp_active) {
-      const double* xs = Xs + (s % G_STAGES) * G_BK * G_LDS;
-      const double* ys = Ys + (s % G_STAGES) * G_BK * G_LDS;
+      const double* xs = Xs + (s % ST) * C::XSTAGE + xoff;
+      const double* ys = Ys + (s % ST) * C::YSTAGE + yoff;
+      double af[2][WM], bf[2][WN];
 #pragma unroll
-      for (int kk = 0; kk < G_BK; kk += 4) {
-        double af[G_WM], bf[G_WN];
+      for (int a = 0; a < WM; ++a) af[0][a] = lds64(xs + a * 8);
 #pragma unroll
-        for (int a = 0; a < G_WM; ++a) af[a] = xs[(kk + fr) * G_LDS + wm * 8 * G_WM + a * 8 + fc];
+      for (int b = 0; b < WN; ++b) bf[0][b] = lds64(ys + b * 8);
+      if (full_tile) {
 #pragma unroll
-        for (int b = 0; b < G_WN; ++b) bf[b] = ys[(kk + fr) * G_LDS + wn * 8 * G_WN + b * 8 + fc];
+        for (int kq = 0; kq < G_BK / 4; ++kq) {
+          const int cur = kq & 1;
+          dmma_step_il<WM, WN>(acc, af[cur], bf[cur], af[cur ^ 1], bf[cur ^ 1], xs + (kq + 1) * 4 * LDX, 8,
+                               ys + (kq + 1) * 4 * LDY, 8, kq + 1 < G_BK / 4);
+        }
+      } else {
 #pragma unroll
-        for (int a = 0; a < G_WM; ++a)
+        for (int kq = 0; kq < G_BK / 4; ++kq) {
+          const int cur = kq & 1;
+          if (kq + 1 < G_BK / 4) {
 #pragma unroll
-          for (int b = 0; b < G_WN; ++b)
-            if (a < mtv && b < ntv) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            for (int a = 0; a < WM; ++a) af[cur ^ 1][a] = xs[(kq + 1) * 4 * LDX + a * 8];
+#pragma unroll
+            for (int b = 0; b < WN; ++b) bf[cur ^ 1][b] = ys[(kq + 1) * 4 * LDY + b * 8];
+          }
+          dmma_block<WM, WN, false>(acc, af[cur], bf[cur], mtv, ntv);
+        }
       }
     }
   }
   cp_async_wait<0>();
 
-  // ---- epilogue: accumulator element (a,b,e) -> tile row wm*32+a*8+lane/4, col wn*32+b*8+2*(lane%4)+e
+  // ---- epilogue: (a,b,e) -> tile row wm*8WM + a*8 + lane/4, col wn*8WN + b*8 + 2*(lane%4) + e
   auto store_final = [&](int lrow, int lcol, double v) {
     const int gi = m0 + lrow, gj = n0 + lcol;
     if (gi >= g.M || gj >= g.N) return;
     if (g.symmetric) {
-      if (ti == tj && lrow > lcol) return;  // diagonal tile: upper triangle then mirror
+      if (gi > gj) return;  // upper triangle, mirrored
       g.C[(int64_t)gi * g.ldc + gj] = v;
       g.C[(int64_t)gj * g.ldc + gi] = v;
     } else {
@@ -222,58 +282,44 @@ __global__ void __launch_bounds__(G_THREADS, 2) gram_kernel(const __grid_constan
   };
 
   if (P.nchunks == 1) {
+    if (!warp_active) return;
 #pragma unroll
-    for (int a = 0; a < G_WM; ++a)
+    for (int a = 0; a < WM; ++a)
 #pragma unroll
-      for (int b = 0; b < G_WN; ++b)
+      for (int b = 0; b < WN; ++b)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          store_final(wm * 8 * G_WM + a * 8 + (lane >> 2), wn * 8 * G_WN + b * 8 + 2 * (lane & 3) + e,
-                      acc[a][b][e]);
+          store_final(wm * 8 * WM + a * 8 + (lane >> 2), wn * 8 * WN + b * 8 + 2 * (lane & 3) + e, acc[a][b][e]);
     return;
   }
 
   const int64_t tile_id = (int64_t)pidx * P.max_tiles + slot;
-  double* part = P.ws + (tile_id * P.nchunks + chunk) * (G_BM * G_BN);
+  double* part = P.ws + (tile_id * P.nchunks + chunk) * (BM * BN);
 #pragma unroll
-  for (int a = 0; a < G_WM; ++a)
+  for (int a = 0; a < WM; ++a)
 #pragma unroll
-    for (int b = 0; b < G_WN; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        part[(wm * 8 * G_WM + a * 8 + (lane >> 2)) * G_BN + wn * 8 * G_WN + b * 8 + 2 * (lane & 3) + e] =
-            acc[a][b][e];
+    for (int b = 0; b < WN; ++b)
+      *reinterpret_cast<double2*>(part + (wm * 8 * WM + a * 8 + (lane >> 2)) * BN + wn * 8 * WN + b * 8 +
+                                  2 * (lane & 3)) = make_double2(acc[a][b][0], acc[a][b][1]);
   __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    int t = atomicAdd(&P.tickets[tile_id], 1);
-    s_last = (t == P.nchunks - 1);
-  }
+  if (tid == 0) s_last = (atomicAdd(&P.tickets[tile_id], 1) == P.nchunks - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const double* base = P.ws + tile_id * P.nchunks * (G_BM * G_BN);
-  for (int e = tid; e < G_BM * G_BN; e += G_THREADS) {
+  const double* base = P.ws + tile_id * P.nchunks * (BM * BN);
+  for (int e = tid; e < BM * BN; e += C::THREADS) {
     double v = 0.0;
-    for (int c = 0; c < P.nchunks; ++c) v += __ldcg(base + (int64_t)c * (G_BM * G_BN) + e);
-    store_final(e / G_BN, e % G_BN, v);
+    for (int c = 0; c < P.nchunks; ++c) v += __ldcg(base + (int64_t)c * (BM * BN) + e);
+    store_final(e / BN, e % BN, v);
   }
   if (tid == 0) P.tickets[tile_id] = 0;  // reset for the next launch (stream-ordered)
 }
 
-static int g_smem_bytes() { return 2 * G_STAGES * G_BK * G_LDS * (int)sizeof(double); }
-
-static void fill_tiles(GramProblem& g) {
-  g.tiles_m = (g.M + G_BM - 1) / G_BM;
-  g.tiles_n = (g.N + G_BN - 1) / G_BN;
-  g.ntiles = g.symmetric ? g.tiles_m * (g.tiles_m + 1) / 2 : g.tiles_m * g.tiles_n;
-}
-
-static int choose_chunks(int64_t nrows, int64_t total_tiles) {
-  // Wave-aware split-K: 3 resident CTAs per SM -> 444 slots.  Pick the chunk count (each
-  // chunk >= 32 stages when possible) whose last wave is fullest: a 1.1-wave grid idles
-  // most of the second wave.
-  const int64_t slots = 3LL * kSMs;
+static int choose_chunks(int64_t nrows, int64_t total_tiles, int slots_per_sm) {
+  // Wave-aware split-K: the smallest chunk count whose last wave is >= 92% full (each chunk
+  // >= 32 stages when possible); a 1.1-wave grid idles most of the second wave.
+  const int64_t slots = (int64_t)slots_per_sm * kSMs;
   total_tiles = lmax(total_tiles, 1);
   const int64_t cmax = lmax(1, lmin(256, nrows / (32 * G_BK)));
   if (total_tiles >= 8 * slots || cmax == 1) return 1;
@@ -283,7 +329,7 @@ static int choose_chunks(int64_t nrows, int64_t total_tiles) {
     const int64_t ctas = total_tiles * c;
     const int64_t waves = (ctas + slots - 1) / slots;
     const double eff = (double)ctas / (double)(waves * slots);
-    if (eff >= 0.92) return (int)c;  // smallest chunk count with a >= 92% full last wave
+    if (eff >= 0.92) return (int)c;
     if (eff > best_eff) { best_eff = eff; best = c; }
   }
   return (int)best;
@@ -292,15 +338,20 @@ static int choose_chunks(int64_t nrows, int64_t total_tiles) {
 // workspace layout: [tickets: 64 KB][partials]
 constexpr int64_t kTicketBytes = 1 << 16;
 
-static int launch_gram(GramParams& P, int64_t total_tiles_slots, void* ws, int64_t ws_bytes,
-                       cudaStream_t st) {
-  P.nchunks = choose_chunks(P.nrows, total_tiles_slots);
-  int64_t part_bytes = (int64_t)total_tiles_slots * P.nchunks * G_BM * G_BN * sizeof(double);
+template <class C>
+static int64_t ws_bytes_for(int64_t nrows, int64_t tiles) {
+  const int c = choose_chunks(nrows, tiles, C::SLOTS_PER_SM);
+  return kTicketBytes + tiles * c * C::BM * C::BN * (int64_t)sizeof(double);
+}
+
+template <class C>
+static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  P.nchunks = choose_chunks(P.nrows, total_tiles_slots, C::SLOTS_PER_SM);
+  int64_t part_bytes = (int64_t)total_tiles_slots * P.nchunks * C::BM * C::BN * sizeof(double);
   if (P.nchunks > 1) {
-    // shrink chunks until the partials fit the workspace
-    while (P.nchunks > 1 && kTicketBytes + part_bytes > ws_bytes) {
+    while (P.nchunks > 1 && kTicketBytes + part_bytes > ws_bytes) {  // fit the workspace
       P.nchunks = (P.nchunks + 1) / 2;
-      part_bytes = (int64_t)total_tiles_slots * P.nchunks * G_BM * G_BN * sizeof(double);
+      part_bytes = (int64_t)total_tiles_slots * P.nchunks * C::BM * C::BN * sizeof(double);
     }
     if (P.nchunks > 1 && total_tiles_slots * (int64_t)sizeof(int) > kTicketBytes) P.nchunks = 1;
   }
@@ -309,18 +360,62 @@ static int launch_gram(GramParams& P, int64_t total_tiles_slots, void* ws, int64
   P.nchunks = (int)lmax(1, (P.nrows + P.chunk_rows - 1) / P.chunk_rows);
   P.tickets = reinterpret_cast<int*>(ws);
   P.ws = reinterpret_cast<double*>(static_cast<char*>(ws) + kTicketBytes);
-  int64_t grid = (int64_t)P.nprob * P.max_tiles * P.nchunks;
+  const int64_t grid = (int64_t)P.nprob * P.max_tiles * P.nchunks;
   if (grid <= 0) return BK_OK;
   if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_bytes());
+    cudaFuncSetAttribute(gram_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
   BK_COUNT();
-  gram_kernel<<<(unsigned)grid, G_THREADS, g_smem_bytes(), st>>>(P);
+  gram_kernel<C><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;
+}
+
+static bool even_segs(const GramProblem& g) {
+  for (int s = 0; s < g.nxs; ++s)
+    if ((g.xs[s].ld & 1) || (g.xs[s].col0 & 1) || (reinterpret_cast<uintptr_t>(g.xs[s].p) & 15)) return false;
+  for (int s = 0; s < g.nys; ++s)
+    if ((g.ys[s].ld & 1) || (g.ys[s].col0 & 1) || (reinterpret_cast<uintptr_t>(g.ys[s].p) & 15)) return false;
+  return true;
+}
+
+template <class C>
+static void fill_tiles(GramProblem& g) {
+  g.tiles_m = (g.M + C::BM - 1) / C::BM;
+  g.tiles_n = (g.N + C::BN - 1) / C::BN;
+  g.ntiles = g.tiles_m * g.tiles_n;
+}
+
+// tile choice: 64x64 at 3 CTAs/SM measured fastest at config-2 shapes (22.6 vs 17.3
+// TFLOP/s for 64x128 at 2 CTAs/SM, profiles/gemm_sweep_r01.json); PPCG_GRAM_TILE=128
+// selects the wide tile for tuning
+static bool use_big(int m2) {
+  static int force = [] {
+    const char* e = getenv("PPCG_GRAM_TILE");
+    return e ? atoi(e) : 0;
+  }();
+  return force == 128 && m2 >= 192;
+}
+
+template <class C>
+static int gram_explicit(int nprob, GramParams& P, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  int maxt = 0;
+  P.vec16 = 1;
+  for (int i = 0; i < nprob; ++i) {
+    GramProblem& g = P.prob[i];
+    fill_tiles<C>(g);
+    if (g.M == 0 || g.N == 0) g.ntiles = 0;
+    maxt = max(maxt, g.ntiles);
+    if (!even_segs(g)) P.vec16 = 0;
+  }
+  if (maxt == 0) return BK_OK;
+  P.nprob = nprob;
+  P.explicit_list = 1;
+  P.max_tiles = maxt;
+  return launch_gram_cfg<C>(P, (int64_t)maxt * nprob, ws, ws_bytes, st);
 }
 
 }  // namespace bk
@@ -328,13 +423,12 @@ static int launch_gram(GramParams& P, int64_t total_tiles_slots, void* ws, int64
 using namespace bk;
 
 extern "C" int64_t bk_gram_ws_bytes(int64_t n, int m1, int m2) {
-  int64_t tiles = (int64_t)((m1 + G_BM - 1) / G_BM) * ((m2 + G_BN - 1) / G_BN);
-  int c = choose_chunks(n, tiles);
-  return kTicketBytes + tiles * c * G_BM * G_BN * (int64_t)sizeof(double);
+  if (use_big(m2)) return ws_bytes_for<Big>(n, (int64_t)((m1 + 63) / 64) * ((m2 + 127) / 128));
+  return ws_bytes_for<Small>(n, (int64_t)((m1 + 63) / 64) * ((m2 + 63) / 64));
 }
 
 // C (m1 x m2, ldc) = X(:, 0:m1)^T Y(:, 0:m2) over n rows.  symmetric != 0 requires X == Y,
-// m1 == m2 and computes half the tiles.  (core.py:43-49)
+// m1 == m2 and computes only the tiles meeting the upper triangle.  (core.py:43-49)
 extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
                          int64_t ldy, double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes,
                          void* stream) {
@@ -347,8 +441,6 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
     return BK_OK;
   }
   GramParams P{};
-  P.nprob = 1;
-  P.explicit_list = 1;
   GramProblem& g = P.prob[0];
   g.xs[0] = {X, ldx, 0, m1};
   g.ys[0] = {Y, ldy, 0, m2};
@@ -358,10 +450,9 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
   g.C = C;
   g.ldc = ldc;
   g.symmetric = symmetric ? 1 : 0;
-  fill_tiles(g);
-  P.max_tiles = g.ntiles;
   P.nrows = n;
-  return launch_gram(P, g.ntiles, ws, ws_bytes, (cudaStream_t)stream);
+  if (use_big(m2)) return gram_explicit<Big>(1, P, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_explicit<Small>(1, P, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 // Two Grams sharing the row range in one launch: C1 = X1^T Y1, C2 = X2^T Y2 (e.g. the
@@ -372,17 +463,13 @@ extern "C" int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t
                           int64_t ws_bytes, void* stream) {
   if (n <= 0) return BK_ERR_ARG;
   GramParams P{};
-  P.nprob = 2;
-  P.explicit_list = 1;
-  GramProblem* gs[2] = {&P.prob[0], &P.prob[1]};
   const double* xs[2] = {X1, X2};
   const double* ys[2] = {Y1, Y2};
   int64_t lx[2] = {ldx1, ldx2}, ly[2] = {ldy1, ldy2}, lc[2] = {ldc1, ldc2};
   int ma[2] = {m1a, m1b}, na[2] = {m2a, m2b};
   double* cs[2] = {C1, C2};
-  int maxt = 0;
   for (int i = 0; i < 2; ++i) {
-    GramProblem& g = *gs[i];
+    GramProblem& g = P.prob[i];
     g.xs[0] = {xs[i], lx[i], 0, ma[i]};
     g.ys[0] = {ys[i], ly[i], 0, na[i]};
     g.nxs = g.nys = 1;
@@ -391,23 +478,18 @@ extern "C" int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t
     g.C = cs[i];
     g.ldc = lc[i];
     g.symmetric = 0;
-    fill_tiles(g);
-    if (ma[i] == 0 || na[i] == 0) g.ntiles = 0;
-    maxt = max(maxt, g.ntiles);
   }
-  if (maxt == 0) return BK_OK;
-  P.max_tiles = maxt;
   P.nrows = n;
-  return launch_gram(P, (int64_t)maxt * 2, ws, ws_bytes, (cudaStream_t)stream);
+  if (use_big(max(m2a, m2b))) return gram_explicit<Big>(2, P, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_explicit<Small>(2, P, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int has_p) {
-  int nb = (k_act + q - 1) / q;
-  int dmax = (has_p ? 3 : 2) * q;
-  int t = (dmax + G_BM - 1) / G_BM;
-  int64_t tiles = (int64_t)2 * nb * t * t;
-  int c = choose_chunks(n, tiles);
-  return kTicketBytes + tiles * c * G_BM * G_BN * (int64_t)sizeof(double);
+  const int nb = (k_act + q - 1) / q;
+  const int dmax = (has_p ? 3 : 2) * q;
+  if (use_big(dmax)) return ws_bytes_for<Big>(n, (int64_t)2 * nb * ((dmax + 63) / 64) * ((dmax + 127) / 128));
+  const int t = (dmax + 63) / 64;
+  return ws_bytes_for<Small>(n, (int64_t)2 * nb * t * t);
 }
 
 // Per-subblock raw pencil Grams (ppcg.py:206-211 before unit scaling, ppcg.py:220-228):
@@ -419,7 +501,7 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
                                    int64_t ws_bytes, void* stream) {
   if (n <= 0 || k_act <= 0 || q <= 0) return BK_ERR_ARG;
   GramParams P{};
-  int nb = (k_act + q - 1) / q;
+  const int nb = (k_act + q - 1) / q;
   P.explicit_list = 0;
   P.nprob = 2 * nb;
   P.sX = X; P.sW = W; P.sP = P_; P.sAX = AX; P.sAW = AW; P.sAP = AP;
@@ -431,10 +513,20 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
   P.dmax = (has_p ? 3 : 2) * q;
   P.outA = Araw;
   P.outB = Braw;
-  int t = (P.dmax + G_BM - 1) / G_BM;
-  P.max_tiles = t * t;  // non-symmetric slot count bounds the symmetric one
   P.nrows = n;
-  return launch_gram(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
+  // 16-byte copies need even offsets/ld everywhere (q even keeps every block start even)
+  const double* ptrs[6] = {X, W, P_, AX, AW, AP};
+  bool aligned = !(ld & 1) && !(c0 & 1) && !(q & 1);
+  for (int i = 0; i < 6; ++i)
+    if (ptrs[i] && (reinterpret_cast<uintptr_t>(ptrs[i]) & 15)) aligned = false;
+  P.vec16 = aligned ? 1 : 0;
+  if (use_big(P.dmax)) {
+    P.max_tiles = ((P.dmax + 63) / 64) * ((P.dmax + 127) / 128);
+    return launch_gram_cfg<Big>(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
+  }
+  const int t = (P.dmax + 63) / 64;
+  P.max_tiles = t * t;
+  return launch_gram_cfg<Small>(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 namespace bk {

@@ -13,14 +13,17 @@
 // (rayleigh_ritz.py:71-92 on the leading k columns): ||AX_k - X_k G_kk||_F^2 is the
 // partial-K accumulator snapshot after the first k columns of X, reduced deterministically
 // (never written to HBM).
+//
+// Tiles: 64 rows x BN (BN = 128 for k_total-wide outputs, 64 otherwise), 4 warps (2 x 2,
+// warp tile 32 x BN/2), two or three CTAs per SM; K in 16-column stages through a cp.async
+// ring (16-byte copies when aligned), fragments double buffered, unpredicated DMMAs for full
+// warp tiles.
 #include "common.cuh"
 
 namespace bk {
 
-constexpr int T_BM = 128, T_BN = 64, T_BK = 16, T_STAGES = 3, T_THREADS = 256;
-constexpr int T_XLD = T_BK + 4;    // 20 doubles: conflict-free A fragments
-constexpr int T_GLD = T_BN + 4;    // 68 = 4 mod 16 doubles: conflict-free B fragments
-constexpr int T_WM = 4, T_WN = 4;  // warp tile 32 x 32, warps 4 (rows) x 2 (cols)
+constexpr int T_BK = 16, T_THREADS = 128, T_BM = 64;
+constexpr int T_XLD = T_BK + 4;  // 20 doubles = 4 mod 16: conflict-free A fragments
 
 struct TsProblem {
   const double* X;
@@ -39,98 +42,136 @@ struct TsParams {
   const double* rowscale;  // may be null
   int upper_tri;           // G upper triangular: skip rows i >= col tile end
   int ksplit, nsplit;      // metric snapshot after K columns [0, ksplit) on output cols < nsplit
+  int vec_x, vec_g;        // 16-byte copies allowed for X (even k offsets) / G
   double* metric_out;      // device scalar (sum of squares); null -> no metric
   double* metric_ws;       // per-CTA partials
   int* metric_ticket;
 };
 
-__global__ void __launch_bounds__(T_THREADS, 2) tsgemm_kernel(const __grid_constant__ TsParams P) {
+BK_DEV void cp_pair(double* dst, const double* src, int nvalid, bool vec, const double* fb) {
+  if (vec) {
+    cp_async16(dst, nvalid > 0 ? src : fb, nvalid * 8);
+  } else {
+    cp_async8(dst, nvalid > 0 ? src : fb, nvalid > 0);
+    cp_async8(dst + 1, nvalid > 1 ? src + 1 : fb, nvalid > 1);
+  }
+}
+
+template <int BN_, int STAGES_, int MINB_>
+struct TCfg {
+  static constexpr int BN = BN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int GLD = BN + 4;                 // = 4 mod 16
+  static constexpr int WM = T_BM / 2 / 8, WN = BN / 2 / 8;
+  static constexpr int XROWSTEP = T_THREADS / 8;     // X: 8 pairs per 16-column row
+  static constexpr int XNLOAD = T_BM / XROWSTEP;
+  static constexpr int GCPR = BN / 2;
+  static constexpr int GROWSTEP = T_THREADS / GCPR;
+  static constexpr int GNLOAD = T_BK / GROWSTEP;
+  static constexpr int XSTAGE = T_BM * T_XLD, GSTAGE = T_BK * GLD;
+  static constexpr int SMEM = STAGES * (XSTAGE + GSTAGE) * (int)sizeof(double);
+};
+using TBig = TCfg<128, 4, 2>;
+using TSmall = TCfg<64, 4, 3>;
+
+template <class C>
+__global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid_constant__ TsParams P) {
+  constexpr int BN = C::BN, WM = C::WM, WN = C::WN, GLD = C::GLD, ST = C::STAGES;
   extern __shared__ __align__(16) double smem[];
-  double* Xs = smem;                              // [STAGES][BM][XLD]
-  double* Gs = smem + T_STAGES * T_BM * T_XLD;    // [STAGES][BK][GLD]
+  double* Xs = smem;                   // [STAGES][BM][XLD]
+  double* Gs = smem + ST * C::XSTAGE;  // [STAGES][BK][GLD]
   __shared__ double s_red[T_THREADS / 32];
   __shared__ int s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const TsProblem pr = P.prob[blockIdx.z];
-  const int n0 = blockIdx.x * T_BN;
+  const int n0 = blockIdx.x * BN;
   const int64_t r0 = (int64_t)blockIdx.y * T_BM;
+  const int kend_all = P.upper_tri ? min(P.K, n0 + BN) : P.K;
 
-  const int kend_all = P.upper_tri ? min(P.K, n0 + T_BN) : P.K;
+  const int xc = (tid & 7) * 2, xr = tid >> 3;
+  const int gc = (tid % C::GCPR) * 2, gr = tid / C::GCPR;
+  const int gnv = max(0, min(2, P.N - (n0 + gc)));
 
-  // loader geometry
-  const int xc = tid & 15, xr = tid >> 4;   // X: col fixed, rows xr + 16 i (i < 8)
-  const int gc = tid & 63, gr = tid >> 6;   // G: col fixed, rows gr + 4 i (i < 4)
-
-  auto load_stage = [&](int kb, int kstop, int st) {
-    double* xd = Xs + st * T_BM * T_XLD;
-    double* gd = Gs + st * T_BK * T_GLD;
+  auto load_stage = [&](int kb, int kstop, int st, bool vx) {
+    double* xd = Xs + st * C::XSTAGE;
+    double* gd = Gs + st * C::GSTAGE;
     const int kx = kb + xc;
-    const bool kxv = kx < kstop;
+    const int xnv = max(0, min(2, kstop - kx));
 #pragma unroll
-    for (int i = 0; i < T_BM / 16; ++i) {
-      const int lr = xr + 16 * i;
+    for (int i = 0; i < C::XNLOAD; ++i) {
+      const int lr = xr + C::XROWSTEP * i;
       const int64_t row = r0 + lr;
-      const bool v = kxv && row < P.n;
-      cp_async8(xd + lr * T_XLD + xc, v ? pr.X + row * P.ldx + kx : pr.X, v);
+      cp_pair(xd + lr * T_XLD + xc, pr.X + row * P.ldx + kx, row < P.n ? xnv : 0, vx, pr.X);
     }
-    const bool gcv = n0 + gc < P.N;
 #pragma unroll
-    for (int i = 0; i < T_BK / 4; ++i) {
-      const int lk = gr + 4 * i;
+    for (int i = 0; i < C::GNLOAD; ++i) {
+      const int lk = gr + C::GROWSTEP * i;
       const int k = kb + lk;
-      const bool v = gcv && k < kstop;
-      cp_async8(gd + lk * T_GLD + gc, v ? pr.G + (int64_t)k * P.ldg + n0 + gc : pr.G, v);
+      cp_pair(gd + lk * GLD + gc, pr.G + (int64_t)k * P.ldg + n0 + gc, k < kstop ? gnv : 0, P.vec_g != 0, pr.G);
     }
   };
 
   const int wm = warp >> 1, wn = warp & 1;
-  const int64_t wr0 = r0 + wm * 32;
-  const int wc0 = n0 + wn * 32;
-  const int mtv = (int)lmax(0, lmin(T_WM, (P.n - wr0 + 7) / 8));
-  const int ntv = max(0, min(T_WN, (P.N - wc0 + 7) / 8));
+  const int64_t wr0 = r0 + wm * 8 * WM;
+  const int wc0 = n0 + wn * 8 * WN;
+  const int mtv = (int)lmax(0, lmin(WM, (P.n - wr0 + 7) / 8));
+  const int ntv = max(0, min(WN, (P.N - wc0 + 7) / 8));
   const bool active = mtv > 0 && ntv > 0;
+  const bool full_tile = mtv == WM && ntv == WN;
 
-  double acc[T_WM][T_WN][2];
+  double acc[WM][WN][2];
 #pragma unroll
-  for (int a = 0; a < T_WM; ++a)
+  for (int a = 0; a < WM; ++a)
 #pragma unroll
-    for (int b = 0; b < T_WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int fk = lane & 3, fm = lane >> 2;
 
   // one K phase over [kbeg, kstop)
   auto run_phase = [&](int kbeg, int kstop) {
     if (kstop <= kbeg) return;
+    const bool vx = P.vec_x && !(kbeg & 1);
     const int nst = (kstop - kbeg + T_BK - 1) / T_BK;
 #pragma unroll
-    for (int s = 0; s < T_STAGES - 1; ++s) {
-      if (s < nst) load_stage(kbeg + s * T_BK, kstop, s);
+    for (int s = 0; s < ST - 1; ++s) {
+      if (s < nst) load_stage(kbeg + s * T_BK, kstop, s, vx);
       cp_async_commit();
     }
     for (int s = 0; s < nst; ++s) {
-      cp_async_wait<T_STAGES - 2>();
+      cp_async_wait<ST - 2>();
       __syncthreads();
       {
-        const int sn = s + T_STAGES - 1;
-        if (sn < nst) load_stage(kbeg + sn * T_BK, kstop, sn % T_STAGES);
+        const int sn = s + ST - 1;
+        if (sn < nst) load_stage(kbeg + sn * T_BK, kstop, sn % ST, vx);
         cp_async_commit();
       }
       if (active) {
-        const double* xs = Xs + (s % T_STAGES) * T_BM * T_XLD;
-        const double* gs = Gs + (s % T_STAGES) * T_BK * T_GLD;
+        const double* xs = Xs + (s % ST) * C::XSTAGE + (wm * 8 * WM + fm) * T_XLD + fk;
+        const double* gs = Gs + (s % ST) * C::GSTAGE + fk * GLD + wn * 8 * WN + fm;
+        double af[2][WM], bf[2][WN];
 #pragma unroll
-        for (int kk = 0; kk < T_BK; kk += 4) {
-          double af[T_WM], bf[T_WN];
+        for (int a = 0; a < WM; ++a) af[0][a] = lds64(xs + a * 8 * T_XLD);
 #pragma unroll
-          for (int a = 0; a < T_WM; ++a) af[a] = xs[(wm * 32 + a * 8 + fm) * T_XLD + kk + fk];
+        for (int b = 0; b < WN; ++b) bf[0][b] = lds64(gs + b * 8);
+        if (full_tile) {
 #pragma unroll
-          for (int b = 0; b < T_WN; ++b) bf[b] = gs[(kk + fk) * T_GLD + wn * 32 + b * 8 + fm];
+          for (int kq = 0; kq < T_BK / 4; ++kq) {
+            const int cur = kq & 1;
+            dmma_step_il<WM, WN>(acc, af[cur], bf[cur], af[cur ^ 1], bf[cur ^ 1], xs + (kq + 1) * 4, 8 * T_XLD,
+                                 gs + (kq + 1) * 4 * GLD, 8, kq + 1 < T_BK / 4);
+          }
+        } else {
 #pragma unroll
-          for (int a = 0; a < T_WM; ++a)
+          for (int kq = 0; kq < T_BK / 4; ++kq) {
+            const int cur = kq & 1;
+            if (kq + 1 < T_BK / 4) {
 #pragma unroll
-            for (int b = 0; b < T_WN; ++b)
-              if (a < mtv && b < ntv) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+              for (int a = 0; a < WM; ++a) af[cur ^ 1][a] = xs[a * 8 * T_XLD + (kq + 1) * 4];
+#pragma unroll
+              for (int b = 0; b < WN; ++b) bf[cur ^ 1][b] = gs[(kq + 1) * 4 * GLD + b * 8];
+            }
+            dmma_block<WM, WN, false>(acc, af[cur], bf[cur], mtv, ntv);
+          }
         }
       }
     }
@@ -145,17 +186,17 @@ __global__ void __launch_bounds__(T_THREADS, 2) tsgemm_kernel(const __grid_const
     double ss = 0.0;
     if (blockIdx.z == 0) {
 #pragma unroll
-      for (int a = 0; a < T_WM; ++a) {
+      for (int a = 0; a < WM; ++a) {
         const int64_t row = wr0 + a * 8 + (lane >> 2);
         if (row >= P.n) continue;
 #pragma unroll
-        for (int b = 0; b < T_WN; ++b)
+        for (int b = 0; b < WN; ++b)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = wc0 + b * 8 + 2 * (lane & 3) + e;
             if (col < P.nsplit && col < P.N) {
-              double zv = P.beta != 0.0 ? pr.Z[row * P.ldz + col] : 0.0;
-              double v = P.alpha * acc[a][b][e] + P.beta * zv;
+              const double zv = P.beta != 0.0 ? pr.Z[row * P.ldz + col] : 0.0;
+              const double v = P.alpha * acc[a][b][e] + P.beta * zv;
               ss = fma(v, v, ss);
             }
           }
@@ -171,8 +212,7 @@ __global__ void __launch_bounds__(T_THREADS, 2) tsgemm_kernel(const __grid_const
       P.metric_ws[cta] = t;
       __threadfence();
       const int64_t total = (int64_t)gridDim.x * gridDim.y * gridDim.z;
-      int tk = atomicAdd(P.metric_ticket, 1);
-      s_last = (tk == total - 1);
+      s_last = (atomicAdd(P.metric_ticket, 1) == total - 1);
       if (s_last) {
         __threadfence();
         double sum = 0.0;
@@ -189,12 +229,12 @@ __global__ void __launch_bounds__(T_THREADS, 2) tsgemm_kernel(const __grid_const
   // ---- epilogue (metric-only launches pass Y = null)
   if (pr.Y == nullptr) return;
 #pragma unroll
-  for (int a = 0; a < T_WM; ++a) {
+  for (int a = 0; a < WM; ++a) {
     const int64_t row = wr0 + a * 8 + (lane >> 2);
     if (row >= P.n) continue;
     const double sr = P.rowscale ? P.rowscale[row] : 1.0;
 #pragma unroll
-    for (int b = 0; b < T_WN; ++b) {
+    for (int b = 0; b < WN; ++b) {
       const int col = wc0 + b * 8 + 2 * (lane & 3);
       double v0 = P.alpha * acc[a][b][0];
       double v1 = P.alpha * acc[a][b][1];
@@ -208,14 +248,38 @@ __global__ void __launch_bounds__(T_THREADS, 2) tsgemm_kernel(const __grid_const
   }
 }
 
-static int t_smem_bytes() { return (T_STAGES * T_BM * T_XLD + T_STAGES * T_BK * T_GLD) * (int)sizeof(double); }
+template <class C>
+static int launch_ts(TsParams& P, cudaStream_t st) {
+  dim3 grid((P.N + C::BN - 1) / C::BN, (unsigned)((P.n + T_BM - 1) / T_BM), P.nprob);
+  if (grid.y > 65535) return BK_ERR_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tsgemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  BK_COUNT();
+  tsgemm_kernel<C><<<grid, T_THREADS, C::SMEM, st>>>(P);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+// tile choice: 64x64 at 3 CTAs/SM measured fastest at config-2 shapes (28.1 vs 21.5
+// TFLOP/s for 64x128, profiles/gemm_sweep_r01.json); PPCG_TS_TILE=128 selects the wide tile
+static bool ts_big(int N) {
+  static int force = [] {
+    const char* e = getenv("PPCG_TS_TILE");
+    return e ? atoi(e) : 0;
+  }();
+  return force == 128 && N >= 192;
+}
 
 }  // namespace bk
 
 using namespace bk;
 
 extern "C" int64_t bk_tsgemm_ws_bytes(int64_t n, int N) {
-  int64_t ctas = ((n + T_BM - 1) / T_BM) * ((N + T_BN - 1) / T_BN) * 4;
+  const int bn = ts_big(N) ? TBig::BN : TSmall::BN;
+  const int64_t ctas = ((n + T_BM - 1) / T_BM) * ((N + bn - 1) / bn) * 4;
   return 256 + ctas * (int64_t)sizeof(double);
 }
 
@@ -232,12 +296,16 @@ extern "C" int bk_tsgemm_batched_d(int nprob, int64_t n, int K, int N, double al
   if (n == 0 || N == 0) return BK_OK;
   TsParams P{};
   P.nprob = nprob;
+  P.vec_x = !(ldx & 1);
+  P.vec_g = !(ldg & 1);
   for (int b = 0; b < nprob; ++b) {
     P.prob[b].X = Xs[b];
     P.prob[b].G = Gs[b];
     P.prob[b].Z = Zs ? Zs[b] : nullptr;
     P.prob[b].Y = Ys[b];
     if (beta != 0.0 && P.prob[b].Z == nullptr) return BK_ERR_ARG;
+    if (reinterpret_cast<uintptr_t>(Xs[b]) & 15) P.vec_x = 0;
+    if (reinterpret_cast<uintptr_t>(Gs[b]) & 15) P.vec_g = 0;
   }
   P.n = n;
   P.K = K;
@@ -252,24 +320,17 @@ extern "C" int bk_tsgemm_batched_d(int nprob, int64_t n, int K, int N, double al
   P.upper_tri = flags & 1;
   P.ksplit = ksplit;
   P.nsplit = nsplit;
-  dim3 grid((N + T_BN - 1) / T_BN, (unsigned)((n + T_BM - 1) / T_BM), nprob);
-  if (grid.y > 65535) return BK_ERR_UNSUPPORTED;
+  const int bn = ts_big(N) ? TBig::BN : TSmall::BN;
   if (metric_out) {
-    int64_t need = 256 + (int64_t)grid.x * grid.y * grid.z * sizeof(double);
+    const int64_t ctas = ((n + T_BM - 1) / T_BM) * ((N + bn - 1) / bn) * nprob;
+    const int64_t need = 256 + ctas * (int64_t)sizeof(double);
     if (ws == nullptr || ws_bytes < need) return BK_ERR_ARG;
     P.metric_ticket = reinterpret_cast<int*>(ws);
     P.metric_ws = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
     P.metric_out = metric_out;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tsgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem_bytes());
-    attr = true;
-  }
-  BK_COUNT();
-  tsgemm_kernel<<<grid, T_THREADS, t_smem_bytes(), (cudaStream_t)stream>>>(P);
-  BK_CHECK_LAUNCH();
-  return BK_OK;
+  if (ts_big(N)) return launch_ts<TBig>(P, (cudaStream_t)stream);
+  return launch_ts<TSmall>(P, (cudaStream_t)stream);
 }
 
 extern "C" int bk_tsgemm_d(int64_t n, int K, int N, double alpha, const double* X, int64_t ldx, const double* G,
@@ -279,6 +340,6 @@ extern "C" int bk_tsgemm_d(int64_t n, int K, int N, double alpha, const double* 
   const double* gs[1] = {G};
   const double* zs[1] = {Z};
   double* ys[1] = {Y};
-  return bk_tsgemm_batched_d(1, n, K, N, alpha, xs, ldx, gs, ldg, beta, Z ? zs : nullptr, ldz, ys, ldy,
-                             rowscale, flags, 0, 0, nullptr, nullptr, 0, stream);
+  return bk_tsgemm_batched_d(1, n, K, N, alpha, xs, ldx, gs, ldg, beta, Z ? zs : nullptr, ldz, ys, ldy, rowscale,
+                             flags, 0, 0, nullptr, nullptr, 0, stream);
 }

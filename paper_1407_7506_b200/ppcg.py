@@ -215,15 +215,16 @@ class PPCGSolver:
         self.AP = [blk(), blk()]
         self.xi = 0   # current X/AX buffer
         self.pi = 0   # current P/AP buffer
-        self.Gm = z(kt, kt)
-        self.Gl = z(kt, kt)
-        self.Gp = z(kt, kt)
-        self.Gp2 = z(kt, kt)
-        self.Gfull = z(kt, kt)
-        self.Rm = z(kt, kt)
-        self.Ahat = z(kt, kt)
-        self.Bhat = z(kt, kt)
-        self.Cm = z(kt, kt)
+        sq = lambda: z(kt, self.ldp)[:, :kt]  # noqa: E731  (even ld: 16-byte operand loads)
+        self.Gm = sq()
+        self.Gl = sq()
+        self.Gp = sq()
+        self.Gp2 = sq()
+        self.Gfull = sq()
+        self.Rm = sq()
+        self.Ahat = sq()
+        self.Bhat = sq()
+        self.Cm = sq()
         self.omega = z(kt, dt=torch.float64)
         self.colnorm2 = z(kt, dt=torch.float64)
         self.stats = z(32, dt=torch.float64)

@@ -1,0 +1,37 @@
+"""Microbenchmark of the FP64 DMMA Gram / tall-GEMM kernels at config-2 shapes
+(n = 110,592, m = 523, row stride 524).  Tile overrides via PPCG_GRAM_TILE / PPCG_TS_TILE."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1407_7506_b200 import kernels as K  # noqa: E402
+
+
+def t(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+n, m, ld = 110592, 523, 524
+x = torch.randn(n, ld, dtype=torch.float64, device="cuda")[:, :m]
+y = torch.randn(n, ld, dtype=torch.float64, device="cuda")[:, :m]
+g = torch.zeros(m, ld, dtype=torch.float64, device="cuda")[:, :m]
+out = torch.zeros(n, ld, dtype=torch.float64, device="cuda")[:, :m]
+fl = 2.0 * n * m * m
+res = {"gram_tile": os.environ.get("PPCG_GRAM_TILE", "default"), "ts_tile": os.environ.get("PPCG_TS_TILE", "default")}
+res["gram_xy_tflops"] = fl / t(lambda: K.gram(x, y, g)) / 1e9
+res["gram_sym_tflops"] = 0.5 * fl / t(lambda: K.gram(x, x, g, symmetric=True)) / 1e9
+gg = torch.randn(m, ld, dtype=torch.float64, device="cuda")[:, :m]
+res["tsgemm_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], alpha=-1.0, beta=1.0, zs=[y])) / 1e9
+res["tsgemm_x2_tflops"] = 2 * fl / t(lambda: K.tsgemm([x, y], [gg, gg], [out, out])) / 1e9
+print(json.dumps(res))
