@@ -78,8 +78,9 @@ def workspace(kind="gram"):
 
 
 # ----------------------------------------------------------------------------- Grams
-def gram(x, y, out=None, symmetric=False):
-    """out = X^H Y (m1 x m2).  symmetric=True requires x is y (same view)."""
+def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
+    """out = X^H Y (m1 x m2).  symmetric=True requires x is y (same view).  Launches on a
+    second stream must pass their own ``ws_kind`` (split-K tickets live in the workspace)."""
     n = x.shape[0]
     if y.shape[0] != n:
         raise DeviceError(f"row dimensions differ: {n} vs {y.shape[0]}")
@@ -92,7 +93,7 @@ def gram(x, y, out=None, symmetric=False):
         px, _, _, lx = real_view(x)
         py, _, _, ly = real_view(y)
         nb = _lib.load().bk_gram_ws_bytes(n, m1, m2)
-        wp, wb = workspace().get(nb)
+        wp, wb = workspace(ws_kind).get(nb)
         _lib.call("bk_gram_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out),
                   1 if symmetric else 0, wp, wb, stream_ptr())
         return out
@@ -101,7 +102,7 @@ def gram(x, y, out=None, symmetric=False):
     py, _, r2, ly = real_view(y)
     tmp = torch.empty((r1, r2), dtype=F64, device=x.device)
     nb = _lib.load().bk_gram_ws_bytes(n, r1, r2)
-    wp, wb = workspace().get(nb)
+    wp, wb = workspace(ws_kind).get(nb)
     _lib.call("bk_gram_d", n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2,
               1 if symmetric else 0, wp, wb, stream_ptr())
     _lib.call("bk_cplx_gram_combine_d", m1, m2, tmp.data_ptr(), r2, out.data_ptr(), ld_of(out),

@@ -206,6 +206,7 @@ class PPCGSolver:
         # n x k_total blocks with the row stride padded to a multiple of 4 elements (16/32-byte
         # aligned rows for vector and bulk-tensor loads); columns keep global positions
         self.ldp = (kt + 3) // 4 * 4
+        self.side = torch.cuda.Stream()  # diagnostics that overlap the subblock pencils
         blk = lambda: z(n, self.ldp)[:, :kt]  # noqa: E731
         self.XF = [blk(), blk()]
         self.AXF = [blk(), blk()]
@@ -504,10 +505,15 @@ class PPCGSolver:
                     K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
         if not wnorm_done:
             K.sumsq(w, self.stats[4:5])
-        # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692)
+        # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692): a diagnostic that
+        # nothing downstream reads, so it runs on a side stream concurrently with the
+        # subblock pencils (one CTA per subblock leaves most SMs idle)
         Gd = self.Gp[:kt, :ka]
-        K.gram(self.XF[self.xi], w, Gd)
-        K.small_stats(Gd, self.stats[5:8])
+        main = torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        with torch.cuda.stream(self.side):
+            K.gram(self.XF[self.xi], w, Gd, ws_kind="side")
+            K.small_stats(Gd, self.stats[5:8])
 
         # subblock updates (ppcg.py:694-696) -> other buffers
         q = o.sbsize
@@ -527,6 +533,7 @@ class PPCGSolver:
                              self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
                              coef_tmp=self.coef_tmp)
         nb = (ka + q - 1) // q
+        main.wait_stream(self.side)
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
         s = self.h_stats.numpy()
