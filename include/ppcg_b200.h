@@ -66,16 +66,19 @@ int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X,
 /* ---- batched subblock update (block_update ppcg.py:278-378 incl. fallback 231-275,
  *      solve_pencil core.py:175-202) and plain batched pencils */
 int bk_pencil_max_dim(void);
+/* global workspace for nb pencils of dimension dmax (0 when d <= 96 real / 64 complex, which
+ * run entirely in shared memory); pass it as ws/ws_bytes below */
+int64_t bk_pencil_ws_bytes(int nb, int dmax, int cplx);
 int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                           double* coef, double* theta, int* info, double* cscale, int force_fallback,
-                          void* stream);
+                          void* ws, int64_t ws_bytes, void* stream);
 int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
-                        double* omega, double* C, int* status, void* stream);
+                        double* omega, double* C, int* status, void* ws, int64_t ws_bytes, void* stream);
 int bk_subblock_pencils_z(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                           double* coef, double* theta, int* info, double* cscale, int force_fallback,
-                          void* stream);
+                          void* ws, int64_t ws_bytes, void* stream);
 int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, const double* B, int want,
-                        double* omega, double* C, int* status, void* stream);
+                        double* omega, double* C, int* status, void* ws, int64_t ws_bytes, void* stream);
 
 /* ---- recombination: ppcg.py:365-369 and _run_subblocks ppcg.py:521-532 (+ breakdown
  *      flags of ppcg.py:701-705) */

@@ -43,12 +43,13 @@ _SIGS = {
     "bk_subblock_grams_z": (c_int, [c_i64, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, c_i64,
                                     vp, vp, vp, vp, vp, c_i64, vp]),
     "bk_pencil_max_dim": (c_int, []),
-    "bk_subblock_pencils_z": (c_int, [c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_int, vp]),
-    "bk_pencil_batched_z": (c_int, [c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp]),
+    "bk_pencil_ws_bytes": (c_i64, [c_int, c_int, c_int]),
+    "bk_subblock_pencils_z": (c_int, [c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_int, vp, c_i64, vp]),
+    "bk_pencil_batched_z": (c_int, [c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp, c_i64, vp]),
     "bk_subblock_recombine_z": (c_int, [c_i64, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, vp,
                                         vp, vp, vp, vp, c_i64, c_i64, vp, vp, vp]),
-    "bk_subblock_pencils_d": (c_int, [c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_int, vp]),
-    "bk_pencil_batched_d": (c_int, [c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp]),
+    "bk_subblock_pencils_d": (c_int, [c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_int, vp, c_i64, vp]),
+    "bk_pencil_batched_d": (c_int, [c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp, c_i64, vp]),
     "bk_subblock_recombine_d": (c_int, [c_i64, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, vp,
                                         vp, vp, vp, vp, c_i64, c_i64, vp, vp]),
     "bk_tsgemm_ws_bytes": (c_i64, [c_i64, c_int]),

@@ -59,9 +59,14 @@ BK_DEV void magph(zd a, double& mag, zd& ph) {
   ph = mag > 0.0 ? zd{a.re / mag, a.im / mag} : zd{1.0, 0.0};
 }
 
+// Pencil dimension caps: the shared-memory variant holds A, B/V and Linv in shared memory;
+// the large variant (d <= PD_BIG = 3 x 64, configs 3-5) keeps them in a per-CTA slice of a
+// caller-owned, L2-resident global workspace with only the vectors in shared memory.
 template <class T> struct PD_;
 template <> struct PD_<double> { static constexpr int v = 96; };
 template <> struct PD_<zd> { static constexpr int v = 64; };
+constexpr int PD_BIG = 192;
+constexpr int QMAX_BIG = 64;
 
 constexpr int P_THREADS = 512;
 constexpr double kGramRtol = 1e-12, kDirFloor = 1e-14, kCxFloor = 1e-14;
@@ -79,6 +84,7 @@ struct PencilParams {
   int want;          // raw mode
   int rawd;          // raw mode pencil dimension
   int force_fallback;  // 1: fallback_steepest_descent directly (ppcg.py:456-472 redo)
+  void* ws;          // large variant: nb x 3 x PD_BIG x (PD_BIG + 1) scalars
 };
 
 template <class T>
@@ -171,12 +177,11 @@ BK_DEV void smem_lower_inverse(const T* L, int ll, T* Li, int li, int d) {
   }
 }
 
-// C = op(A) op(B) in shared memory (d <= 96): 6x3 register block per thread,
-// warps -> rows w, w+16, ...; lanes -> cols l, l+32, l+64.  op = transpose (TA/TB) and/or
-// conjugate (CA/CB).
-template <class T, bool TA, bool CA, bool TB, bool CB>
+// C = op(A) op(B) (d <= PD): RI x RJ register block per thread, warps -> rows w, w+16, ...;
+// lanes -> cols l, l+32, ....  op = transpose (TA/TB) and/or conjugate (CA/CB).
+template <class T, int PD, bool TA, bool CA, bool TB, bool CB>
 BK_DEV void smem_gemm(const T* A, int la, const T* B, int lb, T* C, int lc, int d, int kmax, int ncols = -1) {
-  constexpr int RI = 6, RJ = 3;
+  constexpr int RJ = PD > 96 ? (PD + 31) / 32 : 3, RI = RJ > 3 ? 3 : 6;
   const int nc = ncols < 0 ? d : ncols;
   for (int i0 = BK_WARP; i0 < d; i0 += BK_NWARP * RI) {
     T acc[RI][RJ];
@@ -389,9 +394,9 @@ BK_DEV void smem_svals(T* M, int lm, int rows, int cols, double* sv, PSmem<T>& S
 // Assembled basis: idx[0:d] raw columns, sf[0:d] scale factors.  Raw Grams at (Ar, Br, ldr).
 // On success: ev[0:want] ascending eigenvalues, C (d x want) in M1 (ld PLD).
 // Returns 0 ok, 1 singular (either Cholesky failed).
-template <class T>
+template <class T, int PD>
 BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PSmem<T>& S) {
-  constexpr int PD = PD_<T>::v, PLD = PD + 1;
+  constexpr int PLD = PD + 1;
   T* A = S.M0;
   T* B = S.M1;
   T* Li = S.M2;
@@ -430,9 +435,9 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
   __syncthreads();
   if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:198-201
   smem_lower_inverse(B, PLD, Li, PLD, d);
-  smem_gemm<T, false, false, false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A
+  smem_gemm<T, PD, false, false, false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A
   __syncthreads();
-  smem_gemm<T, false, false, true, true>(B, PLD, Li, PLD, A, PLD, d, d);    // Ared = T Linv^H
+  smem_gemm<T, PD, false, false, true, true>(B, PLD, Li, PLD, A, PLD, d, d);    // Ared = T Linv^H
   __syncthreads();
   // Hermitian symmetrisation of the reduced matrix
   for (int i = BK_WARP; i < d; i += BK_NWARP) {
@@ -462,7 +467,7 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
   for (int k = BK_WARP; k < d; k += BK_NWARP)
     for (int r = BK_LANE; r < want; r += 32) A[k * PLD + r] = B[k * PLD + S.ord[r]];
   __syncthreads();
-  smem_gemm<T, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+  smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
   double* evs = S.rc;  // rotation scratch (PD/2 >= want) is free once the Jacobi is done
   for (int r = threadIdx.x; r < want; r += blockDim.x) evs[r] = S.ev[S.ord[r]];
   __syncthreads();
@@ -472,15 +477,20 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
 }
 
 // ---------------------------------------------------------------- the kernel
-template <class T>
+template <class T, int PD, bool GMEM>
 __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_constant__ PencilParams P) {
-  constexpr int PD = PD_<T>::v, PLD = PD + 1;
+  constexpr int PLD = PD + 1;
   extern __shared__ __align__(16) double sm[];
   PSmem<T> S;
-  S.M0 = reinterpret_cast<T*>(sm);
+  if constexpr (GMEM) {
+    S.M0 = static_cast<T*>(P.ws) + (int64_t)blockIdx.x * 3 * PD * PLD;
+    S.rph = reinterpret_cast<T*>(sm);
+  } else {
+    S.M0 = reinterpret_cast<T*>(sm);
+    S.rph = S.M0 + 3 * PD * PLD;
+  }
   S.M1 = S.M0 + PD * PLD;
   S.M2 = S.M1 + PD * PLD;
-  S.rph = S.M2 + PD * PLD;
   S.nrm = reinterpret_cast<double*>(S.rph + PD / 2);
   S.sf = S.nrm + PD;
   S.ev = S.sf + PD;
@@ -503,7 +513,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     const int d = P.rawd;
     for (int i = tid; i < d; i += blockDim.x) { S.idx[i] = i; S.sf[i] = 1.0; }
     __syncthreads();
-    const int st = pencil_attempt(Ar, Br, ldr, d, P.want, S);
+    const int st = pencil_attempt<T, PD>(Ar, Br, ldr, d, P.want, S);
     T* cout = static_cast<T*>(P.coef) + (int64_t)j * P.dmax * P.want;
     if (st == 0) {
       for (int e = tid; e < d * P.want; e += blockDim.x) cout[e] = S.M1[(e / P.want) * PLD + e % P.want];
@@ -527,7 +537,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   sc = fmax(sc, 1e-300);
   const double floor_ = kDirFloor * sc;  // ppcg.py:198-203
 
-  // kept masks as bit sets (w <= 32)
+  // kept masks as bit sets (w <= 64)
   unsigned long long keptw = 0ull, keptp = 0ull;
   for (int i = 0; i < w; ++i) {
     if (S.nrm[w + i] > floor_) keptw |= 1ull << i;
@@ -575,13 +585,13 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     bool do_fallback = P.force_fallback != 0;
     if (!do_fallback) {
       d = assemble(mw, mp);
-      status = pencil_attempt(Ar, Br, ldr, d, w, S);
+      status = pencil_attempt<T, PD>(Ar, Br, ldr, d, w, S);
       ++attempts;
       if (status != 0) {
         mp = 0ull;  // drop P first, then shed the weakest W column (ppcg.py:335-349)
         while (true) {
           d = assemble(mw, mp);
-          status = pencil_attempt(Ar, Br, ldr, d, w, S);
+          status = pencil_attempt<T, PD>(Ar, Br, ldr, d, w, S);
           ++attempts;
           if (status == 0) break;
           if (mw == 0ull) { err = 1; break; }
@@ -619,7 +629,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         write_passthrough(true);
       } else {
         d = assemble(mw, mp);
-        status = pencil_attempt(Ar, Br, ldr, d, w, S);
+        status = pencil_attempt<T, PD>(Ar, Br, ldr, d, w, S);
         ++attempts;
         if (status != 0) err = 1;
       }
@@ -648,32 +658,54 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   }
 }
 
-template <class T>
+template <class T, int PD, bool GMEM>
 static int p_smem_bytes() {
-  constexpr int PD = PD_<T>::v, PLD = PD + 1;
-  return (3 * PD * PLD + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
+  constexpr int PLD = PD + 1;
+  return ((GMEM ? 0 : 3 * PD * PLD) + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
          (2 * PD + PD + 8) * (int)sizeof(int);
 }
 
+// global workspace of the large variant (0 when the shared-memory variant applies)
 template <class T>
-static int launch_pencils(const PencilParams& P, cudaStream_t st) {
+static int64_t p_ws_bytes(int nb, int dmax) {
+  if (dmax <= PD_<T>::v) return 0;
+  return (int64_t)nb * 3 * PD_BIG * (PD_BIG + 1) * (int64_t)sizeof(T);
+}
+
+template <class T, int PD, bool GMEM>
+static void launch_variant(const PencilParams& P, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pencil_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes<T>());
+    cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         p_smem_bytes<T, PD, GMEM>());
+    // the large variant streams its matrices through L1: keep the carveout small
+    if (GMEM) cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     attr = true;
   }
-  BK_COUNT();
-  pencil_kernel<T><<<P.nb, P_THREADS, p_smem_bytes<T>(), st>>>(P);
+  pencil_kernel<T, PD, GMEM><<<P.nb, P_THREADS, p_smem_bytes<T, PD, GMEM>(), st>>>(P);
+}
+
+template <class T>
+static int launch_pencils(const PencilParams& P, int dim, int64_t ws_bytes, cudaStream_t st) {
+  if (dim <= PD_<T>::v) {
+    BK_COUNT();
+    launch_variant<T, PD_<T>::v, false>(P, st);
+  } else {
+    if (P.ws == nullptr || ws_bytes < p_ws_bytes<T>(P.nb, dim)) return BK_ERR_ARG;
+    BK_COUNT();
+    launch_variant<T, PD_BIG, true>(P, st);
+  }
   BK_CHECK_LAUNCH();
   return BK_OK;
 }
 
 template <class T>
 static int subblock_pencils(int k_act, int q, int has_p, const void* Araw, const void* Braw, void* coef,
-                            double* theta, int* info, double* cscale, int force_fallback, void* stream) {
+                            double* theta, int* info, double* cscale, int force_fallback, void* ws,
+                            int64_t ws_bytes, void* stream) {
   if (k_act <= 0 || q <= 0) return BK_ERR_ARG;
   const int dmax = (has_p ? 3 : 2) * q;
-  if (dmax > PD_<T>::v || q > 32) return BK_ERR_UNSUPPORTED;
+  if (dmax > PD_BIG || q > QMAX_BIG) return BK_ERR_UNSUPPORTED;
   PencilParams P{};
   P.nb = (k_act + q - 1) / q;
   P.k_act = k_act;
@@ -688,14 +720,15 @@ static int subblock_pencils(int k_act, int q, int has_p, const void* Araw, const
   P.cscale = cscale;
   P.mode = 0;
   P.force_fallback = force_fallback ? 1 : 0;
-  return launch_pencils<T>(P, (cudaStream_t)stream);
+  P.ws = ws;
+  return launch_pencils<T>(P, dmax, ws_bytes, (cudaStream_t)stream);
 }
 
 template <class T>
 static int pencil_batched(int nb, int d, int ldm, const void* A, const void* B, int want, double* omega, void* C,
-                          int* status, void* stream) {
+                          int* status, void* ws, int64_t ws_bytes, void* stream) {
   if (nb <= 0 || d <= 0 || want < 1 || want > d || ldm < d) return BK_ERR_ARG;
-  if (d > PD_<T>::v) return BK_ERR_UNSUPPORTED;
+  if (d > PD_BIG) return BK_ERR_UNSUPPORTED;
   PencilParams P{};
   P.nb = nb;
   P.dmax = ldm;
@@ -707,37 +740,50 @@ static int pencil_batched(int nb, int d, int ldm, const void* A, const void* B, 
   P.mode = 1;
   P.want = want;
   P.rawd = d;
-  return launch_pencils<T>(P, (cudaStream_t)stream);
+  P.ws = ws;
+  // the variant follows the pencil dimension, not the (possibly padded) storage stride
+  return launch_pencils<T>(P, d, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // namespace bk
 
 using namespace bk;
 
-extern "C" int bk_pencil_max_dim(void) { return PD_<double>::v; }
+extern "C" int bk_pencil_max_dim(void) { return PD_BIG; }
+
+// Global workspace bytes the pencil solves need for nb problems of dimension dmax (0 when
+// they fit the shared-memory variant: d <= 96 real, d <= 64 complex).
+extern "C" int64_t bk_pencil_ws_bytes(int nb, int dmax, int cplx) {
+  if (nb <= 0 || dmax <= 0) return 0;
+  return cplx ? p_ws_bytes<zd>(nb, dmax) : p_ws_bytes<double>(nb, dmax);
+}
 
 // Device-side block_update for every subblock (see file header).  Araw/Braw from
 // bk_subblock_grams_*.  coef: nb x (dmax x q) scalars; theta: k_act; info: nb x 4 ints
 // (used_fallback, zero_residual, error, attempts); cscale: nb doubles.
 extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                                      double* coef, double* theta, int* info, double* cscale, int force_fallback,
-                                     void* stream) {
-  return subblock_pencils<double>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, stream);
+                                     void* ws, int64_t ws_bytes, void* stream) {
+  return subblock_pencils<double>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, ws,
+                                  ws_bytes, stream);
 }
 extern "C" int bk_subblock_pencils_z(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                                      double* coef, double* theta, int* info, double* cscale, int force_fallback,
-                                     void* stream) {
-  return subblock_pencils<zd>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, stream);
+                                     void* ws, int64_t ws_bytes, void* stream) {
+  return subblock_pencils<zd>(k_act, q, has_p, Araw, Braw, coef, theta, info, cscale, force_fallback, ws,
+                              ws_bytes, stream);
 }
 
 // Batched plain pencils: nb problems of dimension d (stride ldm*ldm, ld ldm), want smallest
 // pairs.  omega: nb x want; C: nb x (ldm x want) (ld want); status: nb x 4 ints ([2] = 1 if
 // singular).  (core.py:175-202)
 extern "C" int bk_pencil_batched_d(int nb, int d, int ldm, const double* A, const double* B, int want,
-                                   double* omega, double* C, int* status, void* stream) {
-  return pencil_batched<double>(nb, d, ldm, A, B, want, omega, C, status, stream);
+                                   double* omega, double* C, int* status, void* ws, int64_t ws_bytes,
+                                   void* stream) {
+  return pencil_batched<double>(nb, d, ldm, A, B, want, omega, C, status, ws, ws_bytes, stream);
 }
 extern "C" int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, const double* B, int want,
-                                   double* omega, double* C, int* status, void* stream) {
-  return pencil_batched<zd>(nb, d, ldm, A, B, want, omega, C, status, stream);
+                                   double* omega, double* C, int* status, void* ws, int64_t ws_bytes,
+                                   void* stream) {
+  return pencil_batched<zd>(nb, d, ldm, A, B, want, omega, C, status, ws, ws_bytes, stream);
 }

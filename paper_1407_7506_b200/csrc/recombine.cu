@@ -13,7 +13,7 @@
 namespace bk {
 
 constexpr int R_BM = 64, R_THREADS = 128;  // 4 warps x 16 rows
-constexpr int R_QMAX = 64;
+constexpr int R_QMAX = 128;  // real-view width (complex q <= 64)
 
 struct RecombParams {
   int64_t n;
@@ -48,76 +48,106 @@ __global__ void k_expand_coef(int k_act, int q, int nparts, const double* __rest
   }
 }
 
-BK_DEV int pad_a(int w) { int l = (w + 3) & ~3; if ((l & 7) == 0) l += 4; return l; }   // l % 8 == 4
-BK_DEV int pad_b(int w) { int l = (w + 7) & ~7; return l + 4; }  // l % 8 == 4: 4 rows -> 4 disjoint 8-bank groups
+// Tiling: a CTA owns 64 rows x NT output columns of one subblock and one side; it streams
+// the concatenated basis [X_j | W_j | P_j] (3w columns) through a 3-stage cp.async ring in
+// chunks of 16 columns together with the matching 16 x NT coefficient rows, and accumulates
+// X_j C_X and W_j C_W + P_j C_P in separate DMMA accumulators (the first part is X).  A
+// CTA therefore reads its rows once per column tile (NT covers w for real q <= 64) and the
+// coefficients stream from L2.  Strides of 20 / NT+4 doubles (== 4 mod 16) keep the
+// fragment loads conflict-free.
+constexpr int R_KC = 16, R_STAGES = 3, R_LA = R_KC + 4;
 
+template <int NT>
 __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_constant__ RecombParams P) {
+  constexpr int LB = NT + 4, WN = NT / 8;
+  constexpr int IN_STAGE = R_BM * R_LA, CF_STAGE = R_KC * LB;
   extern __shared__ __align__(16) double sm[];
+  double* In = sm;                          // [stage][R_BM][R_LA]
+  double* Cf = sm + R_STAGES * IN_STAGE;    // [stage][R_KC][LB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int j = blockIdx.y, side = blockIdx.z;
+  const int j = blockIdx.y;
+  const int side = blockIdx.z & 1;
+  const int ct0 = (blockIdx.z >> 1) * NT;   // first output column of this tile
   const int64_t r0 = (int64_t)blockIdx.x * R_BM;
   const int lo = j * P.q;
   const int w = min(P.q, P.k_act - lo);
+  if (ct0 >= w) return;
   const int nparts = P.has_p ? 3 : 2;
-  const int la = pad_a(w), lb = pad_b(w);
-  double* In = sm;                                  // [part][R_BM][la]
-  double* Cf = sm + 3 * R_BM * la;                  // [nparts*w][lb]
+  const int cpp = (w + R_KC - 1) / R_KC;    // chunks per part
+  const int nchunks = nparts * cpp;
   const double* cg = P.coef + (int64_t)j * P.dmax * P.q;
+  const bool al16 = ((P.ld | (P.c0 + lo)) & 1) == 0;  // 16-byte aligned row segments
 
-  // stage inputs (rows r0..r0+63, cols c0+lo .. +w of each part) and coefficients
-  for (int part = 0; part < nparts; ++part) {
-    const double* src = P.in[side][part];
-    for (int e = tid; e < R_BM * w; e += R_THREADS) {
-      const int r = e / w, c = e % w;
-      const int64_t row = r0 + r;
-      const bool v = row < P.n;
-      cp_async8(In + (part * R_BM + r) * la + c, v ? src + row * P.ld + P.c0 + lo + c : src, v);
+  auto load_chunk = [&](int c, int stage) {
+    const int part = c / cpp, k0 = (c % cpp) * R_KC;
+    const int kw = min(R_KC, w - k0);
+    const double* src = P.in[side][part] + P.c0 + lo + k0;
+    double* in = In + stage * IN_STAGE;
+    if (al16) {
+      for (int e = tid; e < R_BM * (R_KC / 2); e += R_THREADS) {
+        const int r = e / (R_KC / 2), c2 = 2 * (e % (R_KC / 2));
+        const int64_t row = r0 + r;
+        const int nbytes = (row < P.n) ? 8 * max(0, min(2, kw - c2)) : 0;
+        cp_async16(in + r * R_LA + c2, nbytes ? src + row * P.ld + c2 : src, nbytes);
+      }
+    } else {
+      for (int e = tid; e < R_BM * R_KC; e += R_THREADS) {
+        const int r = e / R_KC, cc = e % R_KC;
+        const int64_t row = r0 + r;
+        const bool v = row < P.n && cc < kw;
+        cp_async8(in + r * R_LA + cc, v ? src + row * P.ld + cc : src, v);
+      }
     }
-  }
-  for (int e = tid; e < nparts * w * w; e += R_THREADS) {
-    const int r = e / w, c = e % w;
-    cp_async8(Cf + r * lb + c, cg + e, true);
-  }
-  cp_async_commit();
-  // zero the MMA padding: columns w..(w rounded to 8) of inputs and coefficient rows
-  const int w8 = (w + 7) & ~7, k4 = (w + 3) & ~3;
-  for (int e = tid; e < nparts * R_BM * (k4 - w); e += R_THREADS) {
-    const int part = e / (R_BM * (k4 - w)), rem = e % (R_BM * (k4 - w));
-    In[(part * R_BM + rem / (k4 - w)) * la + w + rem % (k4 - w)] = 0.0;
-  }
-  for (int e = tid; e < nparts * w * (w8 - w); e += R_THREADS) Cf[(e / (w8 - w)) * lb + w + e % (w8 - w)] = 0.0;
-  cp_async_wait<0>();
-  __syncthreads();
+    double* cf = Cf + stage * CF_STAGE;
+    const double* csrc = cg + (int64_t)(part * w + k0) * w + ct0;
+    for (int e = tid; e < R_KC * NT; e += R_THREADS) {
+      const int r = e / NT, cc = e % NT;
+      const bool v = r < kw && ct0 + cc < w;
+      cp_async8(cf + r * LB + cc, v ? csrc + r * w + cc : cg, v);
+    }
+  };
 
-  // warp: rows warp*16 .. +16 (2 MMA rows), cols 0..w8 (<= 8 MMA cols)
-  double accX[2][R_QMAX / 8][2], accP[2][R_QMAX / 8][2];
+  double accX[2][WN][2], accP[2][WN][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < R_QMAX / 8; ++b) accX[a][b][0] = accX[a][b][1] = accP[a][b][0] = accP[a][b][1] = 0.0;
-  const int ntv = w8 / 8;
+    for (int b = 0; b < WN; ++b) accX[a][b][0] = accX[a][b][1] = accP[a][b][0] = accP[a][b][1] = 0.0;
   const int fk = lane & 3, fm = lane >> 2;
-  for (int part = 0; part < nparts; ++part) {
-    const double* ia = In + part * R_BM * la;
-    for (int kk = 0; kk < k4; kk += 4) {
-      double af[2], bf[R_QMAX / 8];
+
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = ia[(warp * 16 + a * 8 + fm) * la + kk + fk];
-      const int crow = part * w + kk + fk;
-      const bool kv = kk + fk < w;
+  for (int s = 0; s < R_STAGES - 1; ++s) {
+    if (s < nchunks) load_chunk(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<R_STAGES - 2>();
+    __syncthreads();
+    if (c + R_STAGES - 1 < nchunks) load_chunk(c + R_STAGES - 1, (c + R_STAGES - 1) % R_STAGES);
+    cp_async_commit();
+    const double* ia = In + (c % R_STAGES) * IN_STAGE + (warp * 16 + fm) * R_LA + fk;
+    const double* cb = Cf + (c % R_STAGES) * CF_STAGE + fk * LB + fm;
+    const bool xpart = c < cpp;
 #pragma unroll
-      for (int b = 0; b < R_QMAX / 8; ++b)
-        if (b < ntv) bf[b] = kv ? Cf[crow * lb + b * 8 + fm] : 0.0;
+    for (int kk = 0; kk < R_KC; kk += 4) {
+      double af[2], bf[WN];
+      af[0] = ia[kk];
+      af[1] = ia[8 * R_LA + kk];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < WN; ++b) bf[b] = cb[kk * LB + b * 8];
+      if (xpart) {
 #pragma unroll
-        for (int b = 0; b < R_QMAX / 8; ++b)
-          if (b < ntv) {
-            if (part == 0) dmma_8x8x4(accX[a][b][0], accX[a][b][1], af[a], bf[b]);
-            else dmma_8x8x4(accP[a][b][0], accP[a][b][1], af[a], bf[b]);
-          }
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < WN; ++b) dmma_8x8x4(accX[a][b][0], accX[a][b][1], af[a], bf[b]);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < WN; ++b) dmma_8x8x4(accP[a][b][0], accP[a][b][1], af[a], bf[b]);
+      }
     }
   }
+  cp_async_wait<0>();
 
   // epilogue: P' = accP, X' = accX + accP; breakdown statistics
   bool nonfin = false;
@@ -129,30 +159,34 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
     const int64_t row = r0 + warp * 16 + a * 8 + fm;
     if (row >= P.n) continue;
 #pragma unroll
-    for (int b = 0; b < R_QMAX / 8; ++b) {
-      if (b >= ntv) continue;
-      double x2 = 0.0, p2 = 0.0;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = b * 8 + 2 * fk + e;
-        if (c >= w) continue;
-        const double pv = accP[a][b][e];
-        const double xv = accX[a][b][e] + pv;
-        const int64_t off = row * P.ld + P.c0 + lo + c;
-        ox[off] = xv;
-        op[off] = pv;
-        nonfin |= !isfinite(xv) || !isfinite(pv);
-        if (P.cplx) {  // (re, im) pair of one complex entry: modulus like np.abs
-          x2 = fma(xv, xv, x2);
-          p2 = fma(pv, pv, p2);
+    for (int b = 0; b < WN; ++b) {
+      const int c = ct0 + b * 8 + 2 * fk;  // this lane's two adjacent columns c, c+1
+      if (c >= w) continue;
+      const double p0 = accP[a][b][0], p1 = accP[a][b][1];
+      const double x0 = accX[a][b][0] + p0, x1 = accX[a][b][1] + p1;
+      const int64_t off = row * P.ld + P.c0 + lo + c;
+      if (c + 1 < w) {
+        if ((off & 1) == 0) {
+          *reinterpret_cast<double2*>(ox + off) = make_double2(x0, x1);
+          *reinterpret_cast<double2*>(op + off) = make_double2(p0, p1);
         } else {
-          mx = fmax(mx, fabs(xv));
-          mp = fmax(mp, fabs(pv));
+          ox[off] = x0; ox[off + 1] = x1;
+          op[off] = p0; op[off + 1] = p1;
         }
-      }
-      if (P.cplx) {
-        mx = fmax(mx, sqrt(x2));
-        mp = fmax(mp, sqrt(p2));
+        nonfin |= !isfinite(x0) || !isfinite(x1) || !isfinite(p0) || !isfinite(p1);
+        if (P.cplx) {  // (re, im) of one complex entry: modulus like np.abs
+          mx = fmax(mx, sqrt(fma(x0, x0, x1 * x1)));
+          mp = fmax(mp, sqrt(fma(p0, p0, p1 * p1)));
+        } else {
+          mx = fmax(mx, fmax(fabs(x0), fabs(x1)));
+          mp = fmax(mp, fmax(fabs(p0), fabs(p1)));
+        }
+      } else {  // odd real width: last column alone
+        ox[off] = x0;
+        op[off] = p0;
+        nonfin |= !isfinite(x0) || !isfinite(p0);
+        mx = fmax(mx, fabs(x0));
+        mp = fmax(mp, fabs(p0));
       }
     }
   }
@@ -166,6 +200,17 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
       if (mp > 0.0) atomicMax(&P.flags[2], dbits(mp));
     }
   }
+}
+
+template <int NT>
+static void launch_recombine(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
+  constexpr int smem = R_STAGES * (R_BM * R_LA + R_KC * (NT + 4)) * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(recombine_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  recombine_kernel<NT><<<dim3(nrt, nb, 2 * nct), R_THREADS, smem, st>>>(R);
 }
 
 }  // namespace bk
@@ -225,20 +270,14 @@ static int recombine(int64_t n, int k_act, int q, int has_p, const double* coef,
   R.outX[0] = Xo; R.outX[1] = AXo;
   R.outP[0] = Po; R.outP[1] = APo;
   R.flags = flags;
-  int la = (q + 3) & ~3;
-  if ((la & 7) == 0) la += 4;
-  const int lb = ((q + 7) & ~7) + 4;
-  const int smem = (3 * R_BM * la + 3 * q * lb) * (int)sizeof(double);
-  static int attr_bytes = 0;
-  if (smem > attr_bytes) {
-    cudaFuncSetAttribute(recombine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_bytes = smem;
-  }
   const int nb = (k_act + q - 1) / q;
-  dim3 grid((unsigned)((n + R_BM - 1) / R_BM), nb, 2);
   if (nb > 65535) return BK_ERR_UNSUPPORTED;
+  const unsigned nrt = (unsigned)((n + R_BM - 1) / R_BM);
+  cudaStream_t st = (cudaStream_t)stream;
   BK_COUNT();
-  recombine_kernel<<<grid, R_THREADS, smem, (cudaStream_t)stream>>>(R);
+  if (q <= 16) launch_recombine<16>(R, nrt, nb, 1, st);
+  else if (q <= 32) launch_recombine<32>(R, nrt, nb, 1, st);
+  else launch_recombine<64>(R, nrt, nb, (q + 63) / 64, st);
   BK_CHECK_LAUNCH();
   return BK_OK;
 }

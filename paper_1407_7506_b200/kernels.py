@@ -261,11 +261,19 @@ def subblock_grams(n, k_act, q, has_p, X, W, P, AX, AW, AP, ld, c0, araw, braw, 
               AP if has_p else None, ld, c0, araw.data_ptr(), braw.data_ptr(), wp, wb, stream_ptr())
 
 
+def _pencil_ws(nb, d, cplx):
+    """Global scratch of the large (d > 96 real / 64 complex) pencil variant, else (None, 0)."""
+    nbytes = _lib.load().bk_pencil_ws_bytes(nb, d, 1 if cplx else 0)
+    return workspace("pencil").get(nbytes) if nbytes else (None, 0)
+
+
 def subblock_pencils(k_act, q, has_p, araw, braw, coef, theta, info, cscale, force_fallback=False):
-    name = "bk_subblock_pencils_z" if araw.dtype == C128 else "bk_subblock_pencils_d"
+    cplx = araw.dtype == C128
+    name = "bk_subblock_pencils_z" if cplx else "bk_subblock_pencils_d"
+    wp, wb = _pencil_ws((k_act + q - 1) // q, (3 if has_p else 2) * q, cplx)
     _lib.call(name, k_act, q, 1 if has_p else 0, araw.data_ptr(), braw.data_ptr(),
               coef.data_ptr(), theta.data_ptr(), info.data_ptr(), cscale.data_ptr(),
-              1 if force_fallback else 0, stream_ptr())
+              1 if force_fallback else 0, wp, wb, stream_ptr())
 
 
 def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags,
@@ -283,9 +291,11 @@ def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AX
 def pencil_batched(a, b, want, omega, c, status):
     """a, b: (nb, ldm, ldm) float64/complex128; solves nb pencils of dimension ldm."""
     nb, d, _ = a.shape
-    name = "bk_pencil_batched_z" if a.dtype == C128 else "bk_pencil_batched_d"
+    cplx = a.dtype == C128
+    name = "bk_pencil_batched_z" if cplx else "bk_pencil_batched_d"
+    wp, wb = _pencil_ws(nb, d, cplx)
     _lib.call(name, nb, d, d, a.data_ptr(), b.data_ptr(), want, omega.data_ptr(),
-              c.data_ptr(), status.data_ptr(), stream_ptr())
+              c.data_ptr(), status.data_ptr(), wp, wb, stream_ptr())
 
 
 # ----------------------------------------------------------------------------- dense (cuSOLVER)

@@ -119,8 +119,10 @@ def test_spmm_matches_scipy(cuda):
     assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-13 * np.max(np.abs(ref))
 
 
-@pytest.mark.parametrize("d,want", [(1, 1), (6, 2), (24, 8), (65, 17), (96, 32)])
+@pytest.mark.parametrize("d,want", [(1, 1), (6, 2), (24, 8), (65, 17), (96, 32), (97, 32), (150, 40), (192, 64)])
 def test_pencil_batched_vs_oracle(cuda, d, want):
+    """d <= 96 runs in shared memory, 96 < d <= 192 (q = 64 at configs 3-5) in the
+    global-workspace variant."""
     from paper_1407_7506_b200 import kernels as K
 
     torch = cuda
@@ -140,6 +142,29 @@ def test_pencil_batched_vs_oracle(cuda, d, want):
         Bs = 0.5 * (B[i] + B[i].T)
         As = 0.5 * (A[i] + A[i].T)
         assert np.allclose(C[i].T @ Bs @ C[i], np.eye(want), atol=1e-11)
+        assert np.allclose(As @ C[i], Bs @ C[i] * om[i][None, :], atol=1e-10 * max(1, np.abs(As).max()))
+
+
+@pytest.mark.parametrize("d,want", [(5, 2), (64, 20), (96, 32), (192, 64)])
+def test_complex_pencil_batched_vs_oracle(cuda, d, want):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    nb = 2
+    A = np.stack([sym_matrix(d, 70 + i, True) for i in range(nb)])
+    B = np.stack([hpd_matrix(d, 75 + i, True) for i in range(nb)])
+    om = torch.zeros((nb, want), dtype=torch.float64, device="cuda")
+    C = torch.zeros((nb, d, want), dtype=torch.complex128, device="cuda")
+    st = torch.zeros((nb, 4), dtype=torch.int32, device="cuda")
+    K.pencil_batched(dev(A, torch), dev(B, torch), want, om, C, st)
+    om, C, st = om.cpu().numpy(), C.cpu().numpy(), st.cpu().numpy()
+    for i in range(nb):
+        assert st[i, 2] == 0
+        w_ref, _ = O.solve_small_pencil(A[i], B[i], want)
+        assert np.allclose(om[i], w_ref, atol=1e-12 * max(1.0, np.max(np.abs(w_ref))), rtol=0)
+        Bs = 0.5 * (B[i] + B[i].conj().T)
+        As = 0.5 * (A[i] + A[i].conj().T)
+        assert np.allclose(C[i].conj().T @ Bs @ C[i], np.eye(want), atol=1e-11)
         assert np.allclose(As @ C[i], Bs @ C[i] * om[i][None, :], atol=1e-10 * max(1, np.abs(As).max()))
 
 
@@ -185,7 +210,9 @@ def _device_block_update(torch, x, w, p, ax, aw, ap, q, force_fallback=False):
 
 
 @pytest.mark.parametrize("n,m,q,with_p", [(40, 2, 2, True), (500, 24, 8, True), (500, 24, 8, False),
-                                          (2000, 66, 8, True), (3000, 70, 32, True), (3000, 45, 32, False)])
+                                          (2000, 66, 8, True), (3000, 70, 32, True), (3000, 45, 32, False),
+                                          (3000, 37, 16, True), (4000, 150, 64, True), (4000, 100, 64, False),
+                                          (3000, 41, 48, True)])
 def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
     torch = cuda
     a = sym_matrix(n, 50)
@@ -221,7 +248,8 @@ def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
         assert abs(cs[j] - r.coeff_scale) <= 1e-8 * r.coeff_scale
 
 
-@pytest.mark.parametrize("n,m,q,with_p", [(300, 6, 3, True), (400, 20, 8, True), (400, 20, 8, False)])
+@pytest.mark.parametrize("n,m,q,with_p", [(300, 6, 3, True), (400, 20, 8, True), (400, 20, 8, False),
+                                          (1500, 40, 32, True), (2500, 100, 64, True)])
 def test_complex_subblock_update_vs_oracle(cuda, n, m, q, with_p):
     """complex Hermitian subblock update: Grams of interleaved views, complex Jacobi pencils,
     expanded-coefficient recombination vs the oracle's block_update."""

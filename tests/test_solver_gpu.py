@@ -160,3 +160,24 @@ def test_well_problem_golden_iterations(cuda):
     assert rep.status == "converged" and rep.iterations <= 14
     rep5 = ppcg_solve(a, t, opts=SolverOptions(k=10, nbuf=2, sbsize=5, rr_period=5, tol=1e-6, seed=1, max_iter=210))
     assert rep5.status == "converged" and rep5.iterations <= 21
+
+
+@pytest.mark.parametrize("cfg,N,k,iters", [(3, 14, 128, 12), (4, 8, 128, 10), (5, 8, 124, 10)])
+def test_q64_scaled_configs_match_oracle_trajectory(cuda, cfg, N, k, iters):
+    """Configs 3-5 run with sbsize 64 (pencils of dimension 192, the global-workspace pencil
+    variant; complex at cfg5): scaled-down instances of the same operators, first iterations
+    of the trace vs the oracle from the same seeded X0."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+
+    a, _, q, tol = config_problem(cfg, N=N)
+    assert q == 64
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=iters)
+    rep, ref = _solve_both(a, HostCsr(a._csr), t, HostDiag(t.d), opts)
+    assert rep.iterations == ref.iterations == iters
+    for r1, r2 in zip(rep.trace, ref.trace):
+        assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-11 * abs(r2.trace_value)
+        assert abs(r1.rel_resid - r2.rel_resid) <= 1e-6 * r2.rel_resid
+    assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-9
+    assert max(rep.diagnostics["proj_defect"]) <= 1e-10
