@@ -19,6 +19,7 @@
 //
 // Mode 1 ("raw") solves one plain pencil per CTA: solve_pencil(SmallPencil(A, B), want).
 #include <cfloat>
+#include <type_traits>
 #include "common.cuh"
 
 namespace bk {
@@ -104,6 +105,11 @@ struct PSmem {
   int* pp;       // PD/2
   int* pq;       // PD/2
   int* misc;     // 8 ints: [0] flag, [1] rotation count
+  // packed variant (real, d > 96): upper triangle of the reduced matrix in shared memory,
+  // row offsets, and the per-CTA rotation log in global memory
+  double* pk;
+  int* ro;
+  double2* rlog;
 };
 
 #define BK_WARP (threadIdx.x >> 5)
@@ -390,6 +396,144 @@ BK_DEV void smem_svals(T* M, int lm, int rows, int cols, double* sv, PSmem<T>& S
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- packed two-sided Jacobi
+// Real symmetric d <= 192 (sbsize 64): the matrix does not fit shared memory as a square, so
+// only its upper triangle is kept (packed, entry (a <= b) at ro[a] + b, ~148 KB).  One
+// round applies d/2 disjoint rotations; A' = J^T A J decomposes into independent 2x2 blocks
+// (pair i rows) x (pair j columns), so a round is ONE pass over the triangle of pair
+// blocks (one barrier for the rotation parameters, one after the update) instead of a row
+// pass then a column pass.  Rotations follow smem_jacobi's convention and threshold exactly.
+// The eigenvector matrix is not accumulated: every round's (c, s) goes to a global log and
+// only the wanted columns are rebuilt afterwards (replay_rotations).
+constexpr int LOG_SWEEPS = 40;
+template <class T, int PD>
+constexpr bool kPacked = PD > 96 && std::is_same<T, double>::value;
+
+// per-CTA global workspace of the large variant: A, B/C, Linv (+ the rotation log)
+template <class T, int PD>
+__host__ __device__ constexpr int64_t p_ws_block_bytes() {
+  return (int64_t)3 * PD * (PD + 1) * (int64_t)sizeof(T) +
+         (kPacked<T, PD> ? (int64_t)LOG_SWEEPS * (PD - 1) * (PD / 2) * 16 : 0);
+}
+
+BK_DEV int packed_jacobi(int d, PSmem<double>& S) {
+  double* pk = S.pk;
+  const int* ro = S.ro;
+  {
+    double f = 0.0;
+    for (int a = BK_WARP; a < d; a += BK_NWARP)
+      for (int b = a + BK_LANE; b < d; b += 32) {
+        const double v = pk[ro[a] + b];
+        f += (a == b ? 1.0 : 2.0) * v * v;
+      }
+    f = sqrt(block_sum(f, S.red));
+    if (threadIdx.x == 0) S.red[30] = 0.5 * DBL_EPSILON * f / (double)d;
+    __syncthreads();
+  }
+  if (d == 1) return 0;
+  const int dd = d + (d & 1), npairs = dd / 2, nr = dd - 1;
+  int sweep = 0;
+  for (; sweep < LOG_SWEEPS; ++sweep) {
+    if (threadIdx.x == 0) S.misc[1] = 0;
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
+        int p, q;
+        rr_pair(r, i, dd, p, q);
+        double c = 1.0, sn = 0.0;
+        if (q < d) {
+          const double apq = pk[ro[p] + q], app = pk[ro[p] + p], aqq = pk[ro[q] + q];
+          const double aabs = fabs(apq);
+          if (aabs != 0.0 && aabs > DBL_EPSILON * 0.5 * sqrt(fabs(app) * fabs(aqq)) && aabs > S.red[30]) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sn = t * c;
+            atomicAdd(&S.misc[1], 1);
+          }
+        }
+        S.pp[i] = p;
+        S.pq[i] = q;
+        S.rc[i] = c;
+        S.rs[i] = sn;
+        S.rlog[((int64_t)sweep * nr + r) * npairs + i] = make_double2(c, sn);
+      }
+      __syncthreads();
+      for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
+        const int pi = S.pp[i], qi = S.pq[i];
+        const double ci = S.rc[i], si = S.rs[i];
+        const bool qiv = qi < d;
+        for (int j = i + BK_LANE; j < npairs; j += 32) {
+          const double sj = S.rs[j];
+          if (si == 0.0 && sj == 0.0) continue;
+          const double cj_ = S.rc[j];
+          if (j == i) {  // diagonal block: annihilate a_pq
+            const int ipp = ro[pi] + pi, iqq = ro[qi] + qi, ipq = ro[pi] + qi;
+            const double app = pk[ipp], aqq = pk[iqq], apq = pk[ipq];
+            const double cs2 = 2.0 * ci * si * apq;
+            pk[ipp] = ci * ci * app - cs2 + si * si * aqq;
+            pk[iqq] = si * si * app + cs2 + ci * ci * aqq;
+            pk[ipq] = 0.0;
+            continue;
+          }
+          const int pj = S.pp[j], qj = S.pq[j];
+          const bool qjv = qj < d;
+          // entries (pi,pj) (pi,qj) (qi,pj) (qi,qj) of the symmetric matrix, stored at (min,max)
+          const int e00 = pi < pj ? ro[pi] + pj : ro[pj] + pi;
+          const int e01 = qjv ? (pi < qj ? ro[pi] + qj : ro[qj] + pi) : 0;
+          const int e10 = qiv ? (qi < pj ? ro[qi] + pj : ro[pj] + qi) : 0;
+          const int e11 = (qiv && qjv) ? (qi < qj ? ro[qi] + qj : ro[qj] + qi) : 0;
+          const double m00 = pk[e00];
+          const double m01 = qjv ? pk[e01] : 0.0;
+          const double m10 = qiv ? pk[e10] : 0.0;
+          const double m11 = (qiv && qjv) ? pk[e11] : 0.0;
+          // rows of pair i, then columns of pair j (smem_jacobi's row / column rotations)
+          const double t00 = ci * m00 - si * m10, t01 = ci * m01 - si * m11;
+          const double t10 = si * m00 + ci * m10, t11 = si * m01 + ci * m11;
+          pk[e00] = cj_ * t00 - sj * t01;
+          if (qjv) pk[e01] = sj * t00 + cj_ * t01;
+          if (qiv) pk[e10] = cj_ * t10 - sj * t11;
+          if (qiv && qjv) pk[e11] = sj * t10 + cj_ * t11;
+        }
+      }
+      __syncthreads();
+    }
+    if (S.misc[1] == 0) break;
+    __syncthreads();
+  }
+  __syncthreads();
+  return min(sweep + 1, LOG_SWEEPS);  // logged sweeps (the last one may be all identities)
+}
+
+// Rebuild the wanted eigenvector columns V[:, ord[0:want]] = G_1 ... G_R E from the log:
+// E (d x want, ld le, shared) starts as the selected identity columns and the rounds are
+// applied in reverse.  Each warp owns whole columns, so no block barrier is needed between
+// rounds (pairs within a round are disjoint; lanes sync per round with __syncwarp).
+BK_DEV void replay_rotations(double* E, int le, int d, const int* sel, int want, int sweeps, PSmem<double>& S) {
+  const int dd = d + (d & 1), npairs = dd / 2, nr = dd - 1;
+  for (int k = BK_WARP; k < d; k += BK_NWARP)
+    for (int r = BK_LANE; r < want; r += 32) E[k * le + r] = (k == sel[r]) ? 1.0 : 0.0;
+  __syncthreads();
+  if (d == 1) return;
+  for (int64_t rr = (int64_t)sweeps * nr - 1; rr >= 0; --rr) {
+    const int r = (int)(rr % nr);
+    const double2* lg = S.rlog + rr * npairs;
+    for (int i = BK_LANE; i < npairs; i += 32) {
+      const double2 cs = lg[i];
+      if (cs.y == 0.0) continue;
+      int p, q;
+      rr_pair(r, i, dd, p, q);
+      for (int c = BK_WARP; c < want; c += BK_NWARP) {
+        const double mp = E[p * le + c], mq = E[q * le + c];
+        E[p * le + c] = cs.x * mp + cs.y * mq;
+        E[q * le + c] = cs.x * mq - cs.y * mp;
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- one pencil attempt
 // Assembled basis: idx[0:d] raw columns, sf[0:d] scale factors.  Raw Grams at (Ar, Br, ldr).
 // On success: ev[0:want] ascending eigenvalues, C (d x want) in M1 (ld PLD).
@@ -449,8 +593,20 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
     if (BK_LANE == 0) real_diag(A[i * PLD + i]);
   }
   __syncthreads();
-  smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
-  for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
+  constexpr bool PACKED = kPacked<T, PD>;
+  int sweeps = 0;
+  if constexpr (PACKED) {
+    for (int a = threadIdx.x; a < d; a += blockDim.x) S.ro[a] = a * (2 * d - a + 1) / 2 - a;
+    __syncthreads();
+    for (int a = BK_WARP; a < d; a += BK_NWARP)
+      for (int b = a + BK_LANE; b < d; b += 32) S.pk[S.ro[a] + b] = A[a * PLD + b];
+    __syncthreads();
+    sweeps = packed_jacobi(d, reinterpret_cast<PSmem<double>&>(S));
+    for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = S.pk[S.ro[i] + i];
+  } else {
+    smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
+    for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
+  }
   __syncthreads();
   // ascending order (ties by index)
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -463,11 +619,24 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
     S.ord[rank] = i;
   }
   __syncthreads();
-  // gather V[:, ord[0:want]] -> A, then C = Linv^H Vsel -> B
-  for (int k = BK_WARP; k < d; k += BK_NWARP)
-    for (int r = BK_LANE; r < want; r += 32) A[k * PLD + r] = B[k * PLD + S.ord[r]];
-  __syncthreads();
-  smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+  if constexpr (PACKED) {
+    // rebuild V[:, ord[0:want]] in shared memory (the packed triangle is dead), C -> B, in
+    // column chunks that fit the triangle's space (one chunk for want <= 64)
+    constexpr int CW = ((PD * (PD + 1) / 2) / PD - 1) | 1;
+    for (int c0 = 0; c0 < want; c0 += CW) {
+      const int cw = min(CW, want - c0), le = cw | 1;
+      replay_rotations(reinterpret_cast<double*>(S.pk), le, d, S.ord + c0, cw, sweeps,
+                       reinterpret_cast<PSmem<double>&>(S));
+      smem_gemm<T, PD, true, true, false, false>(Li, PLD, reinterpret_cast<T*>(S.pk), le, B + c0, PLD, d, d, cw);
+      __syncthreads();
+    }
+  } else {
+    // gather V[:, ord[0:want]] -> A, then C = Linv^H Vsel -> B
+    for (int k = BK_WARP; k < d; k += BK_NWARP)
+      for (int r = BK_LANE; r < want; r += 32) A[k * PLD + r] = B[k * PLD + S.ord[r]];
+    __syncthreads();
+    smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+  }
   double* evs = S.rc;  // rotation scratch (PD/2 >= want) is free once the Jacobi is done
   for (int r = threadIdx.x; r < want; r += blockDim.x) evs[r] = S.ev[S.ord[r]];
   __syncthreads();
@@ -483,7 +652,8 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   extern __shared__ __align__(16) double sm[];
   PSmem<T> S;
   if constexpr (GMEM) {
-    S.M0 = static_cast<T*>(P.ws) + (int64_t)blockIdx.x * 3 * PD * PLD;
+    S.M0 = reinterpret_cast<T*>(static_cast<char*>(P.ws) + (int64_t)blockIdx.x * p_ws_block_bytes<T, PD>());
+    S.rlog = reinterpret_cast<double2*>(S.M0 + 3 * PD * PLD);
     S.rph = reinterpret_cast<T*>(sm);
   } else {
     S.M0 = reinterpret_cast<T*>(sm);
@@ -502,6 +672,8 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   S.pp = S.ord + PD;
   S.pq = S.pp + PD / 2;
   S.misc = S.pq + PD / 2;
+  S.ro = S.misc + 8;
+  S.pk = reinterpret_cast<double*>(S.ro + ((PD + 3) & ~3));
 
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
@@ -604,8 +776,10 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
       }
       if (!err) {
         // rank test: sigma_min(C_X) < 1e-14 max(||C||_2, 1)  (ppcg.py:351-356)
-        T* T1 = S.M2;  // C copy (d x w, ld w) -- Linv no longer needed
-        T* T2 = S.M0;  // C_X copy (w x w, ld w); C itself stays in M1
+        // C copy (d x w, ld w) and C_X copy (w x w, ld w); C itself stays in M1.  The packed
+        // variant's shared triangle is free by now; otherwise Linv and A are dead
+        T* T1 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) : S.M2;
+        T* T2 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) + d * w : S.M0;
         for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M1[(e / w) * PLD + e % w];
         for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M1[(e / w) * PLD + e % w];
         __syncthreads();
@@ -661,15 +835,17 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
 template <class T, int PD, bool GMEM>
 static int p_smem_bytes() {
   constexpr int PLD = PD + 1;
-  return ((GMEM ? 0 : 3 * PD * PLD) + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
-         (2 * PD + PD + 8) * (int)sizeof(int);
+  int b = ((GMEM ? 0 : 3 * PD * PLD) + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
+          (2 * PD + PD + 8 + ((PD + 3) & ~3)) * (int)sizeof(int);
+  if (kPacked<T, PD>) b += PD * (PD + 1) / 2 * (int)sizeof(double);
+  return b;
 }
 
 // global workspace of the large variant (0 when the shared-memory variant applies)
 template <class T>
 static int64_t p_ws_bytes(int nb, int dmax) {
   if (dmax <= PD_<T>::v) return 0;
-  return (int64_t)nb * 3 * PD_BIG * (PD_BIG + 1) * (int64_t)sizeof(T);
+  return (int64_t)nb * p_ws_block_bytes<T, PD_BIG>();
 }
 
 template <class T, int PD, bool GMEM>
@@ -678,8 +854,9 @@ static void launch_variant(const PencilParams& P, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p_smem_bytes<T, PD, GMEM>());
-    // the large variant streams its matrices through L1: keep the carveout small
-    if (GMEM) cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    // the complex large variant streams its matrices through L1: keep the carveout small
+    if (GMEM && !kPacked<T, PD>)
+      cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     attr = true;
   }
   pencil_kernel<T, PD, GMEM><<<P.nb, P_THREADS, p_smem_bytes<T, PD, GMEM>(), st>>>(P);
