@@ -778,16 +778,18 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         // rank test: sigma_min(C_X) < 1e-14 max(||C||_2, 1)  (ppcg.py:351-356)
         // C copy (d x w, ld w) and C_X copy (w x w, ld w); C itself stays in M1.  The packed
         // variant's shared triangle is free by now; otherwise Linv and A are dead
+        // (odd row stride lw: the one-sided sweeps walk columns, lanes over rows)
+        const int lw = w | 1;
         T* T1 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) : S.M2;
-        T* T2 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) + d * w : S.M0;
-        for (int e = tid; e < d * w; e += blockDim.x) T1[e] = S.M1[(e / w) * PLD + e % w];
-        for (int e = tid; e < w * w; e += blockDim.x) T2[e] = S.M1[(e / w) * PLD + e % w];
+        T* T2 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) + d * lw : S.M0;
+        for (int e = tid; e < d * w; e += blockDim.x) T1[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
+        for (int e = tid; e < w * w; e += blockDim.x) T2[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
         __syncthreads();
-        smem_svals(T1, w, d, w, S.rc, S);
+        smem_svals(T1, lw, d, w, S.rc, S);
         double cn = 0.0;
         for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
         __syncthreads();
-        smem_svals(T2, w, w, w, S.rc, S);
+        smem_svals(T2, lw, w, w, S.rc, S);
         double smin = S.rc[0];
         for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
         __syncthreads();
