@@ -166,7 +166,7 @@ def run_reference(args):
     blas = [f"{i.get('internal_api')}:{i.get('num_threads')}" for i in threadpool_info()]
     line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config 2)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config 2)",
             "config": cfg_dict(args.config, a.n, k, q, run.kt), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": cores, "kind": "port",
                              "sample": f"{args.warmup} untimed + {args.steps} timed PPCG iterations of config "
@@ -193,9 +193,13 @@ def kernel_rooflines(torch, s):
     """Time the dominant kernels on the live solver state (CUDA events, launching stream)."""
     from paper_1407_7506_b200 import kernels as K
 
-    n, kt, L = s.n, s.kt, s.L
+    n, kt, L = s.nl, s.kt, s.L  # rows of this rank (all rows on one GPU)
     ka = kt - L
     x, ax, w, aw = s.X(), s.AX(), s.W[:, L:], s.AW[:, L:]
+    win = w
+    if s.plan is not None:  # row partition: the local CSR reads W's extended (ghost) buffer
+        base, _ = s._ext_of(w)
+        win = base[:, L:L + ka]
     G = s.Gm[:ka, :ka]
     out = {}
     ms = event_time(torch, lambda: K.gram(x, ax, G), 10)
@@ -204,7 +208,7 @@ def kernel_rooflines(torch, s):
     ms = event_time(torch, lambda: K.tsgemm([x], [G], [tmp], alpha=-1.0, beta=1.0, zs=[ax]), 10)
     out["tsgemm"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9}
     nnz = s.dev_a.nnz
-    ms = event_time(torch, lambda: s.dev_a.apply_into(w, aw), 10)
+    ms = event_time(torch, lambda: s.dev_a.apply_into(win, aw), 10)
     byts = 2.0 * n * ka * 8 + nnz * 12 + 4 * (n + 1)
     out["spmm"] = {"ms": ms, "gbs": byts / ms / 1e6, "bytes_per_launch": byts}
     q = s.opts.sbsize
@@ -232,15 +236,19 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1407_7506_b200 import _lib
+    from paper_1407_7506_b200.distributed import TorchComm, dist_ppcg_solve
     from paper_1407_7506_b200.ppcg import PPCGSolver, SolverOptions, ppcg_solve
 
+    if world > 1:
+        comm = TorchComm()  # row partition of the one problem: strong scaling
     lib = _lib.load()
     a, t, k, q, tol = build_problem(args.config)
     opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=10 ** 6)
-    s = PPCGSolver(a, t, None, opts).start()
+    s = PPCGSolver(a, t, None, opts, comm=comm).start()
     for _ in range(args.warmup):
         s.step()
     torch.cuda.synchronize()
@@ -269,7 +277,29 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
-    value = world * steps_done / (ms_max / 1e3)
+    value = steps_done / (ms_max / 1e3)  # every rank works on the same iterations
+
+    # ---- e2e through the public API with host buffers (uploads + downloads inside); with
+    # a row partition every rank takes part (the solve is collective)
+    from paper_1407_7506_b200.operators import SparseHermitian
+    from paper_1407_7506_b200.problems import jacobi_preconditioner
+
+    a2 = SparseHermitian(a._csr.copy(), "symmetric")
+    t2 = jacobi_preconditioner(a2)
+    e2e_opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=args.steps)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    w0 = time.perf_counter()
+    if world > 1:
+        rep = dist_ppcg_solve(a2, t2, None, e2e_opts, comm=comm)
+    else:
+        rep = ppcg_solve(a2, t2, opts=e2e_opts)
+    torch.cuda.synchronize()
+    wt = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+    e2e_s = float(wt.item())
 
     line = None
     if rank == 0:
@@ -286,29 +316,24 @@ def run_ours(args):
         kernels["tsgemm"]["frac_of_fp64"] = kr["tsgemm"]["tflops"] / peak
         kernels["subblock_grams"]["frac_of_fp64"] = kr["subblock_grams"]["tflops"] / peak
         kernels["hbm_peak_source"] = hbm_src
-        # ---- e2e through the public API with host buffers (uploads + downloads inside)
-        from paper_1407_7506_b200.operators import SparseHermitian
-        from paper_1407_7506_b200.problems import jacobi_preconditioner
-
-        a2 = SparseHermitian(a._csr.copy(), "symmetric")
-        t2 = jacobi_preconditioner(a2)
-        torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        rep = ppcg_solve(a2, t2, opts=SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=args.steps))
-        torch.cuda.synchronize()
-        w1 = time.perf_counter()
         kt = s.kt
-        h2d = a._csr.nnz * 12 + 4 * (a.n + 1) + a.n * kt * 8 + a.n * 8
+        nl = s.nl
+        nnz_l = int(s.dev_a.nnz)
+        h2d = nnz_l * 12 + 4 * (nl + 1) + nl * kt * 8 + nl * 8
         d2h = a.n * k * 8 + k * 8 + rep.iterations * (256 + 64)
-        e2e = {"value": rep.iterations / (w1 - w0), "unit": "iterations/s",
+        api = "dist_ppcg_solve (row partition, NCCL)" if world > 1 else "ppcg_solve"
+        e2e = {"value": rep.iterations / e2e_s, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d // max(rep.iterations, 1), "d2h_bytes_per_step": d2h // max(rep.iterations, 1),
-               "note": f"public ppcg_solve(host CSR, Jacobi, max_iter={args.steps}) wall time incl. CSR/X0 upload, "
-                       "init CholQR+SpMM, final RR and vector download; bytes are per-job / iterations"}
+               "note": f"public {api}(host CSR, Jacobi, max_iter={args.steps}) wall time (max over ranks) incl. "
+                       "CSR/X0 upload, init CholQR+SpMM, final RR and vector download; bytes are per-job (rank 0) / "
+                       "iterations"}
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": steps_done,
                 "warmup": args.warmup, "ms_per_step": ms_max / max(steps_done, 1), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config 2)",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": f"synthetic (seeded config {args.config})",
                 "config": cfg_dict(args.config, a.n, k, q, s.kt,
-                                   {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                                   {"parallelism": (f"row partition x{world} (NCCL allreduce per Gram, halo P2P per "
+                                                    "SpMM)") if world > 1 else "single GPU",
                                     "n_locked_at_start": int(s.L)}),
                 "roofline": roofline, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}

@@ -67,10 +67,10 @@ _WS = {}
 
 
 def workspace(kind="gram"):
-    """One zeroed scratch buffer per reduction family and device.  Each family keeps its
-    tickets at offset 0 and resets them after use; families must not share a buffer (one
-    family's partials would overwrite another's tickets)."""
-    key = (torch.cuda.current_device(), kind)
+    """One zeroed scratch buffer per reduction family, device and stream.  Each family keeps
+    its tickets at offset 0 and resets them after use; families must not share a buffer (one
+    family's partials would overwrite another's tickets), and neither may two streams."""
+    key = (torch.cuda.current_device(), kind, torch.cuda.current_stream().cuda_stream)
     ws = _WS.get(key)
     if ws is None:
         ws = _WS[key] = Workspace(torch.device("cuda", key[0]))

@@ -166,26 +166,78 @@ class PPCGSolver:
         self.torch, self.K = torch, K
         self.opts = opts
         self.a = a
-        self.dev_a = as_device_operator(a)
-        self.prec = as_device_preconditioner(t)
-        self.rowscale = self.prec[1] if self.prec is not None and self.prec[0] == "diag" else None
         self.n = int(a.n)
-        self.cplx = bool(np.issubdtype(np.dtype(a.dtype), np.complexfloating)) or self.dev_a.complex
+        # row partition (distributed.py): comm with size > 1 -> this rank owns rows [lo, hi)
+        self.comm = comm if comm is not None and comm.size > 1 else None
+        self.plan = None
+        if self.comm is not None:
+            from .distributed import HaloPlan, host_csr_of, local_rows_csr, partition_rows
+            from .operators import DeviceCsr
+
+            csr = host_csr_of(a)
+            self.bounds = partition_rows(self.n, self.comm.size, csr.indptr)
+            self.plan = p = HaloPlan(csr, self.bounds, self.comm.rank)
+            self.dev_a = DeviceCsr(local_rows_csr(csr, p.lo, p.hi, p.g_lo, p.n_ext))
+            self.prec = as_device_preconditioner(t)
+            if self.prec is not None and self.prec[0] != "diag":
+                raise NotImplementedError("row-partitioned runs support diagonal preconditioners only")
+            self.rowscale = self.prec[1][p.lo:p.hi] if self.prec is not None else None
+            self.nl = p.hi - p.lo
+            self.cplx = bool(np.iscomplexobj(csr.data)) or bool(
+                np.issubdtype(np.dtype(a.dtype), np.complexfloating))
+        else:
+            self.dev_a = as_device_operator(a)
+            self.prec = as_device_preconditioner(t)
+            self.rowscale = self.prec[1] if self.prec is not None and self.prec[0] == "diag" else None
+            self.nl = self.n
+            self.cplx = bool(np.issubdtype(np.dtype(a.dtype), np.complexfloating)) or self.dev_a.complex
         self.tdt = torch.complex128 if self.cplx else torch.float64
         self.k = opts.k
         self.kt = opts.k + opts.resolved_nbuf()
         if self.kt > self.n:
             raise DimensionError(f"k + nbuf = {self.kt} exceeds operator dimension {self.n}")
         self.x0 = x0
-        self.comm = comm
         self.matvecs = 0
 
     # ------------------------------------------------------------------ helpers
     def _A(self, x, y):
         """y = A x on device, counted in matvec units (operators.py:122-124)."""
         self.matvecs += x.shape[1]
-        if x.shape[1]:
+        if not x.shape[1]:
+            return
+        if self.plan is None:
             self.dev_a.apply_into(x, y)
+            return
+        # row partition: fill the ghost rows of x's extended buffer, then the local CSR
+        # (columns relative to the extended buffer's first row) multiplies it
+        base, owned = self._ext_of(x)
+        p = self.plan
+        self.comm.exchange([(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.send],
+                           [(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.recv])
+        es = x.element_size()
+        c0 = (x.data_ptr() - owned.data_ptr()) // es
+        self.dev_a.apply_into(base[:, c0:c0 + x.shape[1]], y)
+
+    def _ext_of(self, x):
+        for base, owned in self._ext:
+            lo = base.data_ptr()
+            if lo <= x.data_ptr() < lo + base.numel() * base.element_size():
+                return base, owned
+        raise DimensionError("operator applied to a block without ghost rows")
+
+    def _red(self, *ts):
+        """Sum the row-partial results of a Gram / norm over the ranks (no-op on one GPU)."""
+        if self.comm is None:
+            return
+        for t in ts:
+            if t.numel() == 0:
+                continue
+            if t.is_contiguous():
+                self.comm.allreduce_sum(t)
+            else:
+                tmp = t.contiguous()
+                self.comm.allreduce_sum(tmp)
+                t.copy_(tmp)
 
     def _precond_general(self, w):
         if self.prec is not None and self.prec[0] == "op":
@@ -201,18 +253,31 @@ class PPCGSolver:
 
     def _alloc(self):
         torch = self.torch
-        n, kt = self.n, self.kt
+        kt = self.kt
         z = lambda *s, dt=None: torch.zeros(s, dtype=dt or self.tdt, device="cuda")  # noqa: E731
         # n x k_total blocks with the row stride padded to a multiple of 4 elements (16/32-byte
         # aligned rows for vector and bulk-tensor loads); columns keep global positions
         self.ldp = (kt + 3) // 4 * 4
         self.side = torch.cuda.Stream()  # diagnostics that overlap the subblock pencils
-        blk = lambda: z(n, self.ldp)[:, :kt]  # noqa: E731
-        self.XF = [blk(), blk()]
+        nl = self.nl
+        blk = lambda: z(nl, self.ldp)[:, :kt]  # noqa: E731
+        self._ext = []
+
+        def xblk():
+            # blocks the operator is applied to (X, W, P): with a row partition they carry
+            # the ghost rows above and below the owned slab in one contiguous buffer
+            if self.plan is None:
+                return blk()
+            base = z(self.plan.n_ext, self.ldp)
+            owned = base[self.plan.top:self.plan.top + nl, :kt]
+            self._ext.append((base, owned))
+            return owned
+
+        self.XF = [xblk(), xblk()]
         self.AXF = [blk(), blk()]
-        self.W = blk()
+        self.W = xblk()
         self.AW = blk()
-        self.P = [blk(), blk()]
+        self.P = [xblk(), xblk()]
         self.AP = [blk(), blk()]
         self.xi = 0   # current X/AX buffer
         self.pi = 0   # current P/AP buffer
@@ -321,10 +386,12 @@ class PPCGSolver:
         x, ax = self.X(), self.AX()
         G = self.Gm[:ka, :ka]
         K.gram(x, ax, G)
+        self._red(G)
         w = self.W[:, L:]
         if L == 0:
             K.tsgemm([x], [G], [w], alpha=-1.0, beta=1.0, zs=[ax], rowscale=self.rowscale,
                      metric=self.stats[0:1], ksplit=k, nsplit=k)
+            self._red(self.stats[0:1])
             K.small_stats(G[:k, :k], self.stats[1:4])
             self.metric_cached = True
         else:
@@ -336,7 +403,12 @@ class PPCGSolver:
         """X <- qr(X)[0], AX <- A X (ppcg.py:712-713, 756-757)."""
         L = self.L
         x = self.X()
-        self.dense.householder_q(x, self.AW)
+        if self.comm is None:
+            self.dense.householder_q(x, self.AW)
+        else:  # tall QR of the whole block: gather, factor redundantly, keep own rows
+            full = self.comm.allgather_rows(x.contiguous(), self.bounds)
+            self.dense.householder_q(full, self.torch.empty_like(full))
+            x.copy_(full[self.plan.lo:self.plan.hi])
         self._A(x, self.AX())
 
     # ------------------------------------------------------------------ Rayleigh-Ritz
@@ -349,6 +421,7 @@ class PPCGSolver:
             S, AS = self.XF[self.xi], self.AXF[self.xi]
             K.gram(S, AS, self.Ahat)
             K.gram(S, S, self.Bhat, symmetric=True)
+            self._red(self.Ahat, self.Bhat)
             self.dense.rr_pencil(self.Ahat, self.Bhat, self.omega, self.Cm, self.rr_status)
             self._fetch((self.rr_status, self.h_rr_status))
             if int(self.h_rr_status[0]) == 0:
@@ -359,6 +432,7 @@ class PPCGSolver:
             ka = kt - self.L
             G = self.Gm[:ka, :ka]
             K.gram(self.X(), self.X(), G, symmetric=True)
+            self._red(G)
             try:
                 self._cholqr_inplace_swap(G, self.xi)
             except RankDeficiencyError:
@@ -379,6 +453,7 @@ class PPCGSolver:
         src, dst = self._ritz(fresh=True)
         V, AV = self.XF[dst], self.AXF[dst]
         K.rr_residual(V, AV, self.omega, self.rowscale, self.W, self.colnorm2)
+        self._red(self.colnorm2)
         self._fetch((self.omega, self.h_omega), (self.colnorm2, self.h_colnorm2))
         omega = self.h_omega.numpy().copy()
         rn = np.sqrt(self.h_colnorm2.numpy())
@@ -410,9 +485,12 @@ class PPCGSolver:
         x_host = draw_initial_block(self.n, self.kt, self.cplx, self.opts.seed, self.x0)
         # cholesky_qr of the initial block (ppcg.py:437-438)
         raw = self.XF[1]
+        if self.plan is not None:
+            x_host = x_host[self.plan.lo:self.plan.hi]
         raw.copy_(torch.from_numpy(np.ascontiguousarray(x_host)).to("cuda", non_blocking=False))
         G = self.Gm
         K.gram(raw, raw, G, symmetric=True)
+        self._red(G)
         self.xi = 1
         self._cholqr_inplace_swap(G, 1)
         self._A(self.X(), self.AX())
@@ -435,9 +513,11 @@ class PPCGSolver:
             xl, axl = self.XF[self.xi][:, :k], self.AXF[self.xi][:, :k]
             Gk = self.Gl[:k, :k]
             K.gram(xl, axl, Gk)
+            self._red(Gk)
             K.small_stats(Gk, self.stats[1:4])
             K.tsgemm([xl], [Gk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[0:1],
                      ksplit=k, nsplit=k)
+            self._red(self.stats[0:1])
         self._fetch((self.stats, self.h_stats))
         s = self.h_stats.numpy()
         rel = math.sqrt(max(s[0], 0.0)) / max(math.sqrt(max(s[1], 0.0)), 1e-300)
@@ -475,15 +555,18 @@ class PPCGSolver:
             last_w = o.project_w and L == 0
             if o.project_w and proj_p:
                 K.gram2(x, w, G1, x, p, G3)
+                self._red(G1, G3)
                 K.tsgemm([x, self.AX(), x, self.AX()], [G1, G1, G3, G3], [w, aw, p, ap], alpha=-1.0,
                          beta=1.0, zs=[w, aw, p, ap], metric=self.stats[4:5] if last_w else None,
                          ksplit=ka, nsplit=ka)
             elif o.project_w:
                 K.gram(x, w, G1)
+                self._red(G1)
                 K.tsgemm([x, ax], [G1, G1], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
                          metric=self.stats[4:5] if last_w else None, ksplit=ka, nsplit=ka)
             else:
                 K.gram(x, p, G3)
+                self._red(G3)
                 K.tsgemm([x, ax], [G3, G3], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
             wnorm_done = last_w
             if L:
@@ -492,27 +575,36 @@ class PPCGSolver:
                 G4 = self.Gp[:L, :ka]
                 if o.project_w and proj_p:
                     K.gram2(xl, w, G2, xl, p, G4)
+                    self._red(G2, G4)
                     K.tsgemm([xl, axl, xl, axl], [G2, G2, G4, G4], [w, aw, p, ap], alpha=-1.0, beta=1.0,
                              zs=[w, aw, p, ap], metric=self.stats[4:5], ksplit=L, nsplit=ka)
                     wnorm_done = True
                 elif o.project_w:
                     K.gram(xl, w, G2)
+                    self._red(G2)
                     K.tsgemm([xl, axl], [G2, G2], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
                              metric=self.stats[4:5], ksplit=L, nsplit=ka)
                     wnorm_done = True
                 else:
                     K.gram(xl, p, G4)
+                    self._red(G4)
                     K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
         if not wnorm_done:
             K.sumsq(w, self.stats[4:5])
+        self._red(self.stats[4:5])
         # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692): a diagnostic that
         # nothing downstream reads, so it runs on a side stream concurrently with the
         # subblock pencils (one CTA per subblock leaves most SMs idle)
         Gd = self.Gp[:kt, :ka]
         main = torch.cuda.current_stream()
-        self.side.wait_stream(main)
-        with torch.cuda.stream(self.side):
-            K.gram(self.XF[self.xi], w, Gd, ws_kind="side")
+        if self.comm is None:
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                K.gram(self.XF[self.xi], w, Gd, ws_kind="side")
+                K.small_stats(Gd, self.stats[5:8])
+        else:  # collectives stay on one stream, in the same order on every rank
+            K.gram(self.XF[self.xi], w, Gd)
+            self._red(Gd)
             K.small_stats(Gd, self.stats[5:8])
 
         # subblock updates (ppcg.py:694-696) -> other buffers
@@ -521,18 +613,21 @@ class PPCGSolver:
         psrc, pdst = self.pi, 1 - self.pi
         XFs, AXFs = self.XF[src], self.AXF[src]
         Ps, APs = self.P[psrc], self.AP[psrc]
-        K.subblock_grams(self.n, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
+        K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
                          AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
                          self.araw, self.braw, tmp=self.gtmp)
+        self._red(self.araw, self.braw)
         K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
                            self.cscale)
         self.flags64.zero_()
-        K.subblock_recombine(self.n, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
+        K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
                              Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
                              self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
                              self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
                              coef_tmp=self.coef_tmp)
         nb = (ka + q - 1) // q
+        if self.comm is not None:
+            self.comm.allreduce_max(self.flags64)
         main.wait_stream(self.side)
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
@@ -568,6 +663,7 @@ class PPCGSolver:
             self._A(self.Pa(), self.APa())
         # orthonormality loss of [X_lock, X] (ppcg.py:726-729)
         K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
+        self._red(self.Gfull)
         K.small_stats(self.Gfull, self.stats[8:11])
         self._fetch((self.stats, self.h_stats))
         loss = float(math.sqrt(max(self.h_stats.numpy()[9], 0.0)))
@@ -587,6 +683,7 @@ class PPCGSolver:
                     self._redo_without_p(prev_idx, prev_pidx, err.column)
                     try:
                         K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
+                        self._red(self.Gfull)
                         self._orth(self.Gfull[L:, L:], loss)
                     except RankDeficiencyError:
                         self._householder_refresh()
@@ -616,12 +713,13 @@ class PPCGSolver:
         w = hi - lo
         c0 = self._c0r(L + lo)
         XFp, AXFp = self.XF[prev_idx], self.AXF[prev_idx]
-        K.subblock_grams(self.n, w, w, False, XFp.data_ptr(), self.W.data_ptr(), 0, AXFp.data_ptr(),
+        K.subblock_grams(self.nl, w, w, False, XFp.data_ptr(), self.W.data_ptr(), 0, AXFp.data_ptr(),
                          self.AW.data_ptr(), 0, self._ldr(), c0, self.araw, self.braw, tmp=self.gtmp)
+        self._red(self.araw, self.braw)
         K.subblock_pencils(w, w, False, self.araw, self.braw, self.coef, self.theta, self.info, self.cscale,
                            force_fallback=True)
         self.flags64.zero_()
-        K.subblock_recombine(self.n, w, w, False, self.coef, XFp.data_ptr(), self.W.data_ptr(), 0,
+        K.subblock_recombine(self.nl, w, w, False, self.coef, XFp.data_ptr(), self.W.data_ptr(), 0,
                              AXFp.data_ptr(), self.AW.data_ptr(), 0, self.XF[self.xi].data_ptr(),
                              self.P[self.pi].data_ptr(), self.AXF[self.xi].data_ptr(),
                              self.AP[self.pi].data_ptr(), self._ldr(), c0, self.flags64, coef_tmp=self.coef_tmp)
@@ -647,10 +745,13 @@ class PPCGSolver:
         src, dst = self._ritz(fresh=False)
         V, AV = self.XF[dst][:, :k], self.AXF[dst][:, :k]
         K.rr_residual(V, AV, self.omega, None, None, self.colnorm2)
+        self._red(self.colnorm2)
         self.rr_count += 1
         self._fetch((self.omega, self.h_omega), (self.colnorm2, self.h_colnorm2))
         values = self.h_omega.numpy()[:k].copy()
         rn = np.sqrt(self.h_colnorm2.numpy()[:k]).tolist()
+        if self.comm is not None:
+            V = self.comm.allgather_rows(V.contiguous(), self.bounds)
         vectors = V.cpu().numpy()
         self.xi = dst
         inc = [b.iteration for a_, b in zip(self.trace, self.trace[1:]) if b.trace_value > a_.trace_value]

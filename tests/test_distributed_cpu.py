@@ -1,0 +1,131 @@
+"""Host side of the row-partitioned solver on CPU: the partition, the halo
+plan and local CSR, and the torch.distributed communicator over gloo with world_size 2
+(allreduce sum/max, the halo exchange feeding a sharded SpMM, gathered rows)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_1407_7506_b200.distributed import HaloPlan, local_rows_csr, partition_rows
+
+
+def _problems():
+    from paper_1407_7506_b200 import config_problem, random_hermitian
+
+    return [("cfg1", config_problem(1, N=16)[0]._csr), ("cfg4", config_problem(4, N=6)[0]._csr),
+            ("cfg5", config_problem(5, N=6)[0]._csr), ("rand", random_hermitian(90, 0.25, seed=17)._csr)]
+
+
+def test_partition_rows_covers_and_balances():
+    rp = np.arange(0, 7 * 1001, 7)
+    for size in (1, 2, 3, 7, 8):
+        for b in (partition_rows(1000, size), partition_rows(1000, size, rp)):
+            assert b[0][0] == 0 and b[-1][1] == 1000
+            assert all(lo < hi for lo, hi in b)
+            assert all(b[i][1] == b[i + 1][0] for i in range(size - 1))
+            sizes = [hi - lo for lo, hi in b]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        partition_rows(3, 4)
+
+
+@pytest.mark.parametrize("size", [1, 2, 3, 4])
+def test_halo_plan_local_spmm_equals_global(size):
+    rng = np.random.default_rng(0)
+    for name, csr in _problems():
+        n = csr.shape[0]
+        bounds = partition_rows(n, size, csr.indptr)
+        x = rng.standard_normal((n, 5))
+        if np.iscomplexobj(csr.data):
+            x = x + 1j * rng.standard_normal((n, 5))
+        y = csr @ x
+        plans = [HaloPlan(csr, bounds, r) for r in range(size)]
+        for r, p in enumerate(plans):
+            loc = local_rows_csr(csr, p.lo, p.hi, p.g_lo, p.n_ext)
+            assert loc.shape == (p.hi - p.lo, p.n_ext)
+            # the extended block = owned rows + received ghost rows, nothing else is read
+            ext = np.zeros((p.n_ext, 5), dtype=x.dtype)
+            ext[p.top:p.top + p.hi - p.lo] = x[p.lo:p.hi]
+            for peer, a, b in p.recv:
+                assert bounds[peer][0] <= a < b <= bounds[peer][1]
+                ext[a - p.g_lo:b - p.g_lo] = x[a:b]
+            np.testing.assert_allclose(loc @ ext, y[p.lo:p.hi], rtol=1e-13, atol=1e-13)
+            # what r receives from s is exactly what s sends to r, in the same order
+            for s_ in range(size):
+                got = [(a, b) for peer, a, b in p.recv if peer == s_]
+                sent = [(a, b) for peer, a, b in plans[s_].send if peer == r]
+                assert got == sent, (name, r, s_)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, size, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1407_7506_b200 import config_problem
+    from paper_1407_7506_b200.distributed import HaloPlan, TorchComm, local_rows_csr, partition_rows
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        comm = TorchComm()
+        res = {}
+        # sums / max exactly as the solver uses them
+        t = torch.arange(6, dtype=torch.float64) * (rank + 1)
+        comm.allreduce_sum(t)
+        res["sum"] = t.tolist()
+        z = torch.tensor([1 + 2j, rank - 1j], dtype=torch.complex128)
+        comm.allreduce_sum(z)
+        res["zsum"] = z.tolist()
+        f = torch.tensor([rank, 10 - rank, 0], dtype=torch.int64)
+        comm.allreduce_max(f)
+        res["max"] = f.tolist()
+        # sharded SpMM through the halo exchange
+        csr = config_problem(4, N=6)[0]._csr
+        n = csr.shape[0]
+        bounds = partition_rows(n, size, csr.indptr)
+        p = HaloPlan(csr, bounds, rank)
+        x = np.random.default_rng(3).standard_normal((n, 4))
+        base = torch.zeros((p.n_ext, 4), dtype=torch.float64)
+        base[p.top:p.top + p.hi - p.lo] = torch.from_numpy(x[p.lo:p.hi])
+        comm.exchange([(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.send],
+                      [(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.recv])
+        loc = local_rows_csr(csr, p.lo, p.hi, p.g_lo, p.n_ext)
+        y = loc @ base.numpy()
+        res["spmm_err"] = float(np.max(np.abs(y - (csr @ x)[p.lo:p.hi])))
+        full = comm.allgather_rows(torch.from_numpy(y), bounds)
+        res["gather_err"] = float(np.max(np.abs(full.numpy() - csr @ x)))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_gloo_world2():
+    import torch.multiprocessing as mp
+
+    size = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, size, port, q)) for r in range(size)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in range(size))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for r in range(size):
+        res = out[r]
+        assert res["sum"] == [3.0 * i for i in range(6)]
+        assert res["zsum"] == [2 + 4j, 1 - 2j]
+        assert res["max"] == [1, 10, 0]
+        assert res["spmm_err"] <= 1e-12 and res["gather_err"] <= 1e-12
