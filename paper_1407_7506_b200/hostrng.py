@@ -1,0 +1,99 @@
+"""Multi-threaded host draw of ``numpy.random.default_rng(seed).standard_normal(count)``,
+bit-identical to the sequential draw.
+
+The reference draws the initial block X0 with numpy's PCG64 generator (ppcg.py:414-438) and
+parity requires the same X0, so it cannot come from a device RNG.  At
+config 2 the sequential draw (110,592 x 523 normals) takes ~0.7 s on one core, longer than
+20 solver iterations on the GPU.  It parallelises because PCG64 can jump ahead:
+
+  * numpy's normal sampler (a ziggurat) consumes one 64-bit draw per normal on its fast
+    path and a few more on its rare slow paths, so chunk c of the output starts at an
+    unknown stream position near c*M;
+  * every chunk is therefore drawn speculatively from stream position c*M (PCG64.advance);
+    that chain coincides with the true sequence from the first stream position where both
+    start a normal -- within a few normals, since almost every normal is a one-draw fast
+    path;
+  * the chains are spliced where a run of ``_RUN`` consecutive values of chunk c appears in
+    chunk c-1's overlap (32 identical doubles cannot occur by accident), and any shortfall
+    at the end is drawn sequentially from the last chunk's generator, which by then sits on
+    the true stream.
+If a splice point is not found the function falls back to the sequential draw, so the
+result is always exactly the sequential one.
+"""
+
+from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_RUN = 32
+_MIN_PARALLEL = 1 << 21
+
+
+def _threads():
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return max(1, os.cpu_count() or 1)
+
+
+def _find_splice(prev, prev_from, nxt):
+    """(t, j): prev[t:t+_RUN] == nxt[j:j+_RUN] with t >= prev_from and the smallest j, or None."""
+    lo = max(prev_from, len(prev) - len(prev) // 8 - 4 * _RUN)
+    win = prev[lo:len(prev) - _RUN]
+    for j in range(0, min(256, len(nxt) - _RUN)):
+        for t in np.flatnonzero(win == nxt[j]):
+            t = int(t) + lo
+            if np.array_equal(prev[t:t + _RUN], nxt[j:j + _RUN]):
+                return t, j
+    return None
+
+
+def standard_normal(seed, count, threads=None):
+    """Flat float64 array equal to ``np.random.default_rng(seed).standard_normal(count)``."""
+    threads = threads or _threads()
+    if count < _MIN_PARALLEL or threads < 2:
+        return np.random.default_rng(seed).standard_normal(count)
+    nchunk = min(threads, max(2, count // (_MIN_PARALLEL // 2)))
+    M = -(-count // nchunk)           # nominal stream draws per chunk
+    extra = M // 16 + 4096            # overlap covering the slow-path surplus of a chunk
+
+    def draw(c):
+        bg = np.random.PCG64(seed)
+        if c:
+            bg.advance(c * M)
+        g = np.random.Generator(bg)
+        return g, g.standard_normal(M + extra)
+
+    with ThreadPoolExecutor(max_workers=nchunk) as ex:
+        parts = list(ex.map(draw, range(nchunk)))
+    # splice: chunk c contributes from index j_c onwards, at output index i_c
+    starts = [(0, 0)]
+    for c in range(1, nchunk):
+        i_prev, j_prev = starts[-1]
+        sp = _find_splice(parts[c - 1][1], j_prev, parts[c][1])
+        if sp is None:
+            return np.random.default_rng(seed).standard_normal(count)
+        t, j = sp
+        starts.append((i_prev + (t - j_prev), j))
+    out = np.empty(count)
+    bounds = [s[0] for s in starts] + [None]
+
+    def copy(c):
+        i, j = starts[c]
+        arr = parts[c][1]
+        end = bounds[c + 1] if c + 1 < nchunk else min(count, i + len(arr) - j)
+        end = min(end, count)
+        if end > i:
+            out[i:end] = arr[j:j + (end - i)]
+        return end
+
+    with ThreadPoolExecutor(max_workers=nchunk) as ex:
+        ends = list(ex.map(copy, range(nchunk)))
+    filled = ends[-1]
+    if filled < count:  # the last chain is on the true stream: continue it sequentially
+        g, arr = parts[-1]
+        out[filled:] = g.standard_normal(count - filled)
+    return out

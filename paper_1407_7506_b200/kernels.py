@@ -8,6 +8,8 @@ tensor-core kernel is real; complex products are assembled by small expand/combi
 
 from __future__ import annotations
 
+import threading
+
 import torch
 
 from . import _lib
@@ -299,6 +301,83 @@ def pencil_batched(a, b, want, omega, c, status):
 
 
 # ----------------------------------------------------------------------------- dense (cuSOLVER)
+_DENSE = threading.local()
+
+
+def dense_context():
+    """The calling thread's cached Dense context for the current device (creating a
+    cuSOLVER handle costs tens of ms; a handle must not be shared between host threads)."""
+    cache = getattr(_DENSE, "by_dev", None)
+    if cache is None:
+        cache = _DENSE.by_dev = {}
+    dev = torch.cuda.current_device()
+    ctx = cache.get(dev)
+    if ctx is None or ctx.h is None:
+        ctx = cache[dev] = Dense()
+    return ctx
+
+
+_STAGE = threading.local()
+
+
+def to_host(x, chunk_bytes=32 << 20):
+    """numpy copy of a (possibly row-strided) 2-D device block through two pinned staging
+    buffers: the device->pinned copy of one row chunk overlaps the pinned->numpy copy of
+    the previous one (a pageable .cpu() of a large block runs at a few GB/s)."""
+    import numpy as np
+
+    n, m = x.shape
+    out = np.empty((n, m), dtype=np.complex128 if x.dtype == C128 else np.float64)
+    if n == 0 or m == 0:
+        return out
+    rows = max(1, chunk_bytes // (m * x.element_size()))
+    key = (x.dtype, m, rows)
+    st = getattr(_STAGE, "bufs", None)
+    if st is None or st[0] != key:
+        bufs = [torch.empty((rows, m), dtype=x.dtype, pin_memory=True) for _ in range(2)]
+        st = _STAGE.bufs = (key, bufs, [torch.cuda.Event(), torch.cuda.Event()])
+    _, bufs, evs = st
+    pend = None
+    for k, r0 in enumerate(range(0, n, rows)):
+        r1 = min(n, r0 + rows)
+        b = k & 1
+        bufs[b][: r1 - r0].copy_(x[r0:r1], non_blocking=True)
+        evs[b].record()
+        if pend is not None:
+            pb, p0, p1 = pend
+            evs[pb].synchronize()
+            out[p0:p1] = bufs[pb][: p1 - p0].numpy()
+        pend = (b, r0, r1)
+    pb, p0, p1 = pend
+    evs[pb].synchronize()
+    out[p0:p1] = bufs[pb][: p1 - p0].numpy()
+    return out
+
+
+def from_host(arr, x, chunk_bytes=32 << 20):
+    """x[:, :] = arr (numpy, C-contiguous rows) through two pinned staging buffers: the
+    pinned->device copy of one row chunk overlaps the numpy->pinned copy of the next."""
+    n, m = x.shape
+    if n == 0 or m == 0:
+        return x
+    rows = max(1, chunk_bytes // (m * x.element_size()))
+    bufs = [torch.empty((rows, m), dtype=x.dtype, pin_memory=True) for _ in range(2)]
+    evs = [None, None]
+    for k, r0 in enumerate(range(0, n, rows)):
+        r1 = min(n, r0 + rows)
+        b = k & 1
+        if evs[b] is not None:
+            evs[b].synchronize()
+        bufs[b][: r1 - r0].numpy()[...] = arr[r0:r1]
+        x[r0:r1].copy_(bufs[b][: r1 - r0], non_blocking=True)
+        evs[b] = torch.cuda.Event()
+        evs[b].record()
+    for e in evs:
+        if e is not None:
+            e.synchronize()
+    return x
+
+
 class Dense:
     """Owns a bk_dense context (cuSOLVER handle + workspace) bound to the current stream."""
 

@@ -125,13 +125,17 @@ def lock_count(values, rnorms, tol):
 def draw_initial_block(n, kt, complex_field, seed, x0=None):
     """Host draw of X0 exactly as _initial_block (ppcg.py:414-438) before orthonormalisation:
     numpy PCG64 normals (real block then imaginary block), x0 padded on the right."""
+    from .hostrng import standard_normal
+
     dtype = np.complex128 if complex_field else np.float64
-    rng = np.random.default_rng(seed)
 
     def draw(cols):
-        blk = rng.standard_normal((n, cols))
+        # one stream: n*cols real parts, then n*cols imaginary parts (multi-threaded,
+        # bit-identical to rng.standard_normal((n, cols)) twice; hostrng.py)
+        flat = standard_normal(seed, n * cols * (2 if complex_field else 1))
+        blk = flat[: n * cols].reshape(n, cols)
         if complex_field:
-            blk = blk + 1j * rng.standard_normal((n, cols))
+            blk = blk + 1j * flat[n * cols:].reshape(n, cols)
         return blk
 
     if x0 is None:
@@ -320,9 +324,9 @@ class PPCGSolver:
         self.h_info = torch.zeros(nbmax * 4, dtype=torch.int32).pin_memory()
         self.h_cscale = torch.zeros(nbmax, dtype=torch.float64).pin_memory()
         self.eye = torch.eye(kt, dtype=self.tdt, device="cuda")
-        from .kernels import Dense
+        from .kernels import dense_context
 
-        self.dense = Dense()
+        self.dense = dense_context()
 
     # views
     def X(self):
@@ -487,7 +491,7 @@ class PPCGSolver:
         raw = self.XF[1]
         if self.plan is not None:
             x_host = x_host[self.plan.lo:self.plan.hi]
-        raw.copy_(torch.from_numpy(np.ascontiguousarray(x_host)).to("cuda", non_blocking=False))
+        K.from_host(np.ascontiguousarray(x_host), raw)
         G = self.Gm
         K.gram(raw, raw, G, symmetric=True)
         self._red(G)
@@ -752,10 +756,9 @@ class PPCGSolver:
         rn = np.sqrt(self.h_colnorm2.numpy()[:k]).tolist()
         if self.comm is not None:
             V = self.comm.allgather_rows(V.contiguous(), self.bounds)
-        vectors = V.cpu().numpy()
+        vectors = K.to_host(V)
         self.xi = dst
         inc = [b.iteration for a_, b in zip(self.trace, self.trace[1:]) if b.trace_value > a_.trace_value]
-        self.dense.close()
         return SolveReport(values=values, vectors=vectors, trace=self.trace, status=self.status,
                            iterations=self.iterations, matvecs=self.matvecs, rr_count=self.rr_count,
                            breakdown_recoveries=self.recoveries, wall_ms=wall,

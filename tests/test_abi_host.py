@@ -136,3 +136,24 @@ def test_oracle_is_not_imported_by_the_product():
             "print(any(m.startswith('oracle') for m in sys.modules))")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert out.stdout.strip() == "False", out.stderr
+
+
+def test_parallel_host_normals_bit_identical():
+    """X0 draw (ppcg.py:414-438): the multi-threaded PCG64 draw equals numpy's sequential one."""
+    from paper_1407_7506_b200.hostrng import standard_normal
+
+    for seed, count, th in [(0, 3_000_000, 4), (7, 2_200_001, 3), (11, 4_500_000, 8), (2, 1000, 4)]:
+        assert np.array_equal(standard_normal(seed, count, th), np.random.default_rng(seed).standard_normal(count))
+
+
+def test_initial_block_matches_reference_draw():
+    from paper_1407_7506_b200.ppcg import draw_initial_block
+
+    for cplx in (False, True):
+        n, kt = 20000, 120
+        x = draw_initial_block(n, kt, cplx, 3)
+        rng = np.random.default_rng(3)
+        ref = rng.standard_normal((n, kt))
+        if cplx:
+            ref = ref + 1j * rng.standard_normal((n, kt))
+        assert np.array_equal(x, ref)
