@@ -142,11 +142,12 @@ BK_DEV void load_pair(double* dst, const PairCol& pc, int64_t row, bool rv) {
   }
 }
 
-template <int BM_, int BN_, int STAGES_, int MINB_, int SLOTS_>
+template <int BM_, int BN_, int STAGES_, int MINB_, int SLOTS_, int WARPS_M_ = 2, int WARPS_N_ = 2>
 struct GCfg {
   static constexpr int BM = BM_, BN = BN_, STAGES = STAGES_, MINB = MINB_, SLOTS_PER_SM = SLOTS_;
-  static constexpr int THREADS = 128;             // 2 x 2 warps
-  static constexpr int WM = BM / 2 / 8, WN = BN / 2 / 8;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int WM = BM / WARPS_M / 8, WN = BN / WARPS_N / 8;
   static constexpr int LDX = BM + 4, LDY = BN + 4; // = 4 mod 16
   static constexpr int XPAIRS = G_BK * BM / 2 / THREADS, YPAIRS = G_BK * BN / 2 / THREADS;
   static constexpr int XSTAGE = G_BK * LDX, YSTAGE = G_BK * LDY;
@@ -154,6 +155,9 @@ struct GCfg {
 };
 using Big = GCfg<64, 128, 4, 2, 2>;
 using Small = GCfg<64, 64, 4, 3, 3>;
+// subblock pencil Grams of width 3q = 96 (q = 32, config 2): one 96 x 96 tile, 3 x 2 warps
+// of 32 x 48 -- 64 x 64 tiles would leave 44% of the DMMA work on padding (4 tiles for 96^2)
+using Sb96 = GCfg<96, 96, 4, 2, 2, 3, 2>;
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_constant__ GramParams P) {
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
   };
 
   // warp placement (2 x 2); valid DMMA tiles (skip tiles outside M x N / below the diagonal)
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int wm0 = m0 + wm * 8 * WM, wn0 = n0 + wn * 8 * WN;
   const int mtv = max(0, min(WM, (g.M - wm0 + 7) / 8));
   const int ntv = max(0, min(WN, (g.N - wn0 + 7) / 8));
@@ -488,6 +492,7 @@ extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int h
   const int nb = (k_act + q - 1) / q;
   const int dmax = (has_p ? 3 : 2) * q;
   if (use_big(dmax)) return ws_bytes_for<Big>(n, (int64_t)2 * nb * ((dmax + 63) / 64) * ((dmax + 127) / 128));
+  if (dmax > 64 && dmax <= 96) return ws_bytes_for<Sb96>(n, (int64_t)2 * nb);
   const int t = (dmax + 63) / 64;
   return ws_bytes_for<Small>(n, (int64_t)2 * nb * t * t);
 }
@@ -523,6 +528,10 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
   if (use_big(P.dmax)) {
     P.max_tiles = ((P.dmax + 63) / 64) * ((P.dmax + 127) / 128);
     return launch_gram_cfg<Big>(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
+  }
+  if (P.dmax > 64 && P.dmax <= 96) {
+    P.max_tiles = 1;
+    return launch_gram_cfg<Sb96>(P, (int64_t)P.nprob, ws, ws_bytes, (cudaStream_t)stream);
   }
   const int t = (P.dmax + 63) / 64;
   P.max_tiles = t * t;

@@ -205,19 +205,27 @@ __global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid
     ss = warp_sum(ss);
     if (lane == 0) s_red[warp] = ss;
     __syncthreads();
+    const int64_t total = (int64_t)gridDim.x * gridDim.y * gridDim.z;
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < T_THREADS / 32; ++w) t += s_red[w];
       const int64_t cta = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
       P.metric_ws[cta] = t;
       __threadfence();
-      const int64_t total = (int64_t)gridDim.x * gridDim.y * gridDim.z;
       s_last = (atomicAdd(P.metric_ticket, 1) == total - 1);
-      if (s_last) {
-        __threadfence();
-        double sum = 0.0;
-        for (int64_t c = 0; c < total; ++c) sum += __ldcg(P.metric_ws + c);
-        *P.metric_out = sum;
+    }
+    __syncthreads();
+    if (s_last) {  // block-uniform: the last CTA sums the partials with all its threads,
+      __threadfence();  // each over a fixed strided subset, then a fixed-order tree
+      double sum = 0.0;
+      for (int64_t c = tid; c < total; c += T_THREADS) sum += __ldcg(P.metric_ws + c);
+      sum = warp_sum(sum);
+      if (lane == 0) s_red[warp] = sum;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < T_THREADS / 32; ++w) t += s_red[w];
+        *P.metric_out = t;
         *P.metric_ticket = 0;
       }
     }

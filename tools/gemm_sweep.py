@@ -34,4 +34,18 @@ res["gram_sym_tflops"] = 0.5 * fl / t(lambda: K.gram(x, x, g, symmetric=True)) /
 gg = torch.randn(m, ld, dtype=torch.float64, device="cuda")[:, :m]
 res["tsgemm_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], alpha=-1.0, beta=1.0, zs=[y])) / 1e9
 res["tsgemm_x2_tflops"] = 2 * fl / t(lambda: K.tsgemm([x, y], [gg, gg], [out, out])) / 1e9
+# the solver's call shapes: projection (4 in-place updates, +- metric), residual (row scale + metric)
+bufs = [torch.randn(n, ld, dtype=torch.float64, device="cuda")[:, :m] for _ in range(4)]
+xs = [x, y, x, y]
+gs = [gg, gg, gg, gg]
+st = torch.zeros(4, dtype=torch.float64, device="cuda")
+res["proj4_inplace_tflops"] = 4 * fl / t(lambda: K.tsgemm(xs, gs, bufs, alpha=-1.0, beta=1.0, zs=bufs)) / 1e9
+res["proj4_inplace_metric_tflops"] = 4 * fl / t(lambda: K.tsgemm(xs, gs, bufs, alpha=-1.0, beta=1.0, zs=bufs,
+                                                                  metric=st[0:1], ksplit=m, nsplit=m)) / 1e9
+rs = torch.rand(n, dtype=torch.float64, device="cuda")
+res["resid_rowscale_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], alpha=-1.0, beta=1.0, zs=[y], rowscale=rs)) / 1e9
+res["resid_rowscale_metric_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], alpha=-1.0, beta=1.0, zs=[y], rowscale=rs,
+                                                               metric=st[0:1], ksplit=512, nsplit=512)) / 1e9
+res["cholqr_upper_tflops"] = 0.5 * 2 * fl / t(lambda: K.tsgemm([x, y], [gg, gg], [out, bufs[0]], upper=True)) / 1e9
+res["gram2_tflops"] = 2 * fl / t(lambda: K.gram2(x, y, g, x, bufs[1], gg)) / 1e9
 print(json.dumps(res))
