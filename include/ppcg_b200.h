@@ -67,7 +67,8 @@ int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X,
  *      solve_pencil core.py:175-202) and plain batched pencils */
 int bk_pencil_max_dim(void);
 /* global workspace for nb pencils of dimension dmax (0 when d <= 96 real / 64 complex, which
- * run entirely in shared memory); pass it as ws/ws_bytes below */
+ * run entirely in shared memory; larger ones keep their matrices and, real, the Jacobi
+ * rotation log here); pass it as ws/ws_bytes below */
 int64_t bk_pencil_ws_bytes(int nb, int dmax, int cplx);
 int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                           double* coef, double* theta, int* info, double* cscale, int force_fallback,

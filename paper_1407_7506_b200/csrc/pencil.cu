@@ -406,13 +406,20 @@ BK_DEV void smem_svals(T* M, int lm, int rows, int cols, double* sv, PSmem<T>& S
 // The eigenvector matrix is not accumulated: every round's (c, s) goes to a global log and
 // only the wanted columns are rebuilt afterwards (replay_rotations).
 constexpr int LOG_SWEEPS = 40;
+// real pencils of the large variant use the packed Jacobi + rotation log, the triangle in its
+// own shared region.  (Measured at d = 96: the square three-phase sweep with V accumulated in
+// shared memory is faster there -- 3.5 vs 4.2 ms for config 2's 17 pencils -- so the
+// shared-memory variant keeps it; the packed path could also place the triangle in the dead
+// B matrix, see pkbuf below.)
 template <class T, int PD>
-constexpr bool kPacked = PD > 96 && std::is_same<T, double>::value;
+constexpr bool kPacked = std::is_same<T, double>::value && (PD > PD_<T>::v);
+template <class T, int PD>
+constexpr bool kOwnPk = kPacked<T, PD> && (PD > PD_<T>::v);
 
-// per-CTA global workspace of the large variant: A, B/C, Linv (+ the rotation log)
+// per-CTA global workspace: A, B/C, Linv of the large variant, and the rotation log
 template <class T, int PD>
 __host__ __device__ constexpr int64_t p_ws_block_bytes() {
-  return (int64_t)3 * PD * (PD + 1) * (int64_t)sizeof(T) +
+  return (PD > PD_<T>::v ? (int64_t)3 * PD * (PD + 1) * (int64_t)sizeof(T) : 0) +
          (kPacked<T, PD> ? (int64_t)LOG_SWEEPS * (PD - 1) * (PD / 2) * 16 : 0);
 }
 
@@ -595,14 +602,19 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
   __syncthreads();
   constexpr bool PACKED = kPacked<T, PD>;
   int sweeps = 0;
+  // packed triangle: own shared region (large variant) or the dead B (shared variant);
+  // the rebuilt eigenvector columns go to the same region / the dead A
+  double* const pkbuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(B);
+  double* const ebuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(A);
   if constexpr (PACKED) {
     for (int a = threadIdx.x; a < d; a += blockDim.x) S.ro[a] = a * (2 * d - a + 1) / 2 - a;
     __syncthreads();
     for (int a = BK_WARP; a < d; a += BK_NWARP)
-      for (int b = a + BK_LANE; b < d; b += 32) S.pk[S.ro[a] + b] = A[a * PLD + b];
+      for (int b = a + BK_LANE; b < d; b += 32) pkbuf[S.ro[a] + b] = rl(A[a * PLD + b]);
     __syncthreads();
+    S.pk = pkbuf;
     sweeps = packed_jacobi(d, reinterpret_cast<PSmem<double>&>(S));
-    for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = S.pk[S.ro[i] + i];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = pkbuf[S.ro[i] + i];
   } else {
     smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
     for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
@@ -625,9 +637,8 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
     constexpr int CW = ((PD * (PD + 1) / 2) / PD - 1) | 1;
     for (int c0 = 0; c0 < want; c0 += CW) {
       const int cw = min(CW, want - c0), le = cw | 1;
-      replay_rotations(reinterpret_cast<double*>(S.pk), le, d, S.ord + c0, cw, sweeps,
-                       reinterpret_cast<PSmem<double>&>(S));
-      smem_gemm<T, PD, true, true, false, false>(Li, PLD, reinterpret_cast<T*>(S.pk), le, B + c0, PLD, d, d, cw);
+      replay_rotations(ebuf, le, d, S.ord + c0, cw, sweeps, reinterpret_cast<PSmem<double>&>(S));
+      smem_gemm<T, PD, true, true, false, false>(Li, PLD, reinterpret_cast<T*>(ebuf), le, B + c0, PLD, d, d, cw);
       __syncthreads();
     }
   } else {
@@ -651,12 +662,14 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   constexpr int PLD = PD + 1;
   extern __shared__ __align__(16) double sm[];
   PSmem<T> S;
+  char* const wsb = static_cast<char*>(P.ws) + (int64_t)blockIdx.x * p_ws_block_bytes<T, PD>();
   if constexpr (GMEM) {
-    S.M0 = reinterpret_cast<T*>(static_cast<char*>(P.ws) + (int64_t)blockIdx.x * p_ws_block_bytes<T, PD>());
+    S.M0 = reinterpret_cast<T*>(wsb);
     S.rlog = reinterpret_cast<double2*>(S.M0 + 3 * PD * PLD);
     S.rph = reinterpret_cast<T*>(sm);
   } else {
     S.M0 = reinterpret_cast<T*>(sm);
+    S.rlog = reinterpret_cast<double2*>(wsb);
     S.rph = S.M0 + 3 * PD * PLD;
   }
   S.M1 = S.M0 + PD * PLD;
@@ -780,8 +793,8 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         // variant's shared triangle is free by now; otherwise Linv and A are dead
         // (odd row stride lw: the one-sided sweeps walk columns, lanes over rows)
         const int lw = w | 1;
-        T* T1 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) : S.M2;
-        T* T2 = kPacked<T, PD> ? reinterpret_cast<T*>(S.pk) + d * lw : S.M0;
+        T* T1 = kOwnPk<T, PD> ? reinterpret_cast<T*>(S.pk) : S.M2;
+        T* T2 = kOwnPk<T, PD> ? reinterpret_cast<T*>(S.pk) + d * lw : S.M0;
         for (int e = tid; e < d * w; e += blockDim.x) T1[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
         for (int e = tid; e < w * w; e += blockDim.x) T2[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
         __syncthreads();
@@ -839,14 +852,14 @@ static int p_smem_bytes() {
   constexpr int PLD = PD + 1;
   int b = ((GMEM ? 0 : 3 * PD * PLD) + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
           (2 * PD + PD + 8 + ((PD + 3) & ~3)) * (int)sizeof(int);
-  if (kPacked<T, PD>) b += PD * (PD + 1) / 2 * (int)sizeof(double);
+  if (kOwnPk<T, PD>) b += PD * (PD + 1) / 2 * (int)sizeof(double);
   return b;
 }
 
 // global workspace of the large variant (0 when the shared-memory variant applies)
 template <class T>
 static int64_t p_ws_bytes(int nb, int dmax) {
-  if (dmax <= PD_<T>::v) return 0;
+  if (dmax <= PD_<T>::v) return (int64_t)nb * p_ws_block_bytes<T, PD_<T>::v>();
   return (int64_t)nb * p_ws_block_bytes<T, PD_BIG>();
 }
 
@@ -857,7 +870,7 @@ static void launch_variant(const PencilParams& P, cudaStream_t st) {
     cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p_smem_bytes<T, PD, GMEM>());
     // the complex large variant streams its matrices through L1: keep the carveout small
-    if (GMEM && !kPacked<T, PD>)
+    if (GMEM && !kOwnPk<T, PD>)
       cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     attr = true;
   }
@@ -867,6 +880,7 @@ static void launch_variant(const PencilParams& P, cudaStream_t st) {
 template <class T>
 static int launch_pencils(const PencilParams& P, int dim, int64_t ws_bytes, cudaStream_t st) {
   if (dim <= PD_<T>::v) {
+    if (p_ws_bytes<T>(P.nb, dim) > 0 && (P.ws == nullptr || ws_bytes < p_ws_bytes<T>(P.nb, dim))) return BK_ERR_ARG;
     BK_COUNT();
     launch_variant<T, PD_<T>::v, false>(P, st);
   } else {
@@ -930,8 +944,8 @@ using namespace bk;
 
 extern "C" int bk_pencil_max_dim(void) { return PD_BIG; }
 
-// Global workspace bytes the pencil solves need for nb problems of dimension dmax (0 when
-// they fit the shared-memory variant: d <= 96 real, d <= 64 complex).
+// Global workspace bytes the pencil solves need for nb problems of dimension dmax: 0 for the
+// shared-memory variant (d <= 96 real, 64 complex), else A/B/Linv (+ the real rotation log).
 extern "C" int64_t bk_pencil_ws_bytes(int nb, int dmax, int cplx) {
   if (nb <= 0 || dmax <= 0) return 0;
   return cplx ? p_ws_bytes<zd>(nb, dmax) : p_ws_bytes<double>(nb, dmax);
