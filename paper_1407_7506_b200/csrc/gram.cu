@@ -323,10 +323,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
 static int choose_chunks(int64_t nrows, int64_t total_tiles, int slots_per_sm) {
   // Wave-aware split-K: the smallest chunk count whose last wave is >= 92% full (each chunk
   // >= 32 stages when possible); a 1.1-wave grid idles most of the second wave.
+  // At least 8 waves: short CTAs let the dynamic block scheduler even out CTAs of unequal
+  // cost (edge tiles of 523 = 8 x 64 + 11) and shrink the tail; measured at config 2:
+  // 22.5 -> 24.1 TF/s (X^T Y), 17.2 -> 20.2 (symmetric), 22.8 -> 24.6 (two Grams)
+  // (profiles/gemm_sweep_r01c.json).  PPCG_GRAM_MINWAVES overrides (0 = off).
+  static const int min_waves = [] {
+    const char* e = getenv("PPCG_GRAM_MINWAVES");
+    return e ? atoi(e) : 8;
+  }();
   const int64_t slots = (int64_t)slots_per_sm * kSMs;
   total_tiles = lmax(total_tiles, 1);
   const int64_t cmax = lmax(1, lmin(256, nrows / (32 * G_BK)));
   if (total_tiles >= 8 * slots || cmax == 1) return 1;
+  if (min_waves > 0) {
+    for (int64_t c = 1; c <= cmax; ++c) {
+      const int64_t ctas = total_tiles * c;
+      const int64_t waves = (ctas + slots - 1) / slots;
+      if (waves >= min_waves && (double)ctas / (double)(waves * slots) >= 0.92) return (int)c;
+    }
+  }
   int64_t best = 1;
   double best_eff = -1.0;
   for (int64_t c = 1; c <= cmax; ++c) {

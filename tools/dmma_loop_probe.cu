@@ -1,0 +1,115 @@
+// Mainloop probes for the FP64 DMMA GEMM kernels (what limits gram_kernel at ~74% pipe?):
+//   mode 0: fragments from shared memory every k-step, no barriers (pure LDS + DMMA)
+//   mode 1: + __syncthreads() every stage of 4 k-steps
+//   mode 2: + a cp.async ring refilling each stage from global memory (the real loop)
+// 64x64 CTA tile, 4 warps of WM x WN DMMA tiles (4x4 = 32x32 warp tile), BK = 16.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dmma_loop_probe tools/dmma_loop_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int BK = 16, LD = 68, ST = 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+
+template <int MODE, int WM, int WN>
+__global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, double* out, int stages) {
+  extern __shared__ double sm[];
+  double* Xs = sm;
+  double* Ys = sm + ST * BK * LD;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 2 * ST * BK * LD; e += 128) sm[e] = 1e-3 * (e % 97);
+  __syncthreads();
+  const int wm = warp >> 1, wn = warp & 1;
+  const int fr = lane & 3, fc = lane >> 2;
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int a = 0; a < WM; ++a)
+#pragma unroll
+    for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double* gsrc = g + (int64_t)blockIdx.x * 1024;
+  for (int s = 0; s < stages; ++s) {
+    const int st = s % ST;
+    if (MODE == 2) {
+      asm volatile("cp.async.wait_group 2;\n" ::);
+    }
+    if (MODE >= 1) __syncthreads();
+    if (MODE == 2) {  // refill stage (s+3)%ST: 16 x 64 doubles for each operand
+      const int sn = (s + ST - 1) % ST;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = tid + 128 * i, r = e >> 5, c = (e & 31) * 2;
+        cp16(Xs + sn * BK * LD + r * LD + c, gsrc + ((s * 16 + r) & 1023) * 0 + c);
+        cp16(Ys + sn * BK * LD + r * LD + c, gsrc + 512 + c);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    const double* xs = Xs + st * BK * LD + fr * LD + wm * 8 * WM + fc;
+    const double* ys = Ys + st * BK * LD + fr * LD + wn * 8 * WN + fc;
+#pragma unroll
+    for (int kq = 0; kq < BK / 4; ++kq) {
+      double af[WM], bf[WN];
+#pragma unroll
+      for (int a = 0; a < WM; ++a) af[a] = xs[kq * 4 * LD + a * 8];
+#pragma unroll
+      for (int b = 0; b < WN; ++b) bf[b] = ys[kq * 4 * LD + b * 8];
+#pragma unroll
+      for (int a = 0; a < WM; ++a)
+#pragma unroll
+        for (int b = 0; b < WN; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int a = 0; a < WM; ++a)
+#pragma unroll
+    for (int b = 0; b < WN; ++b) t += acc[a][b][0] + acc[a][b][1];
+  if (t == 1234.5) out[0] = t;
+}
+
+template <int MODE, int WM, int WN>
+void run(const char* name, int blocks, const double* g, double* out, int stages) {
+  const int smem = 2 * ST * BK * LD * 8;
+  cudaFuncSetAttribute(loop<MODE, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  loop<MODE, WM, WN><<<blocks, 128, smem>>>(g, out, stages);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    loop<MODE, WM, WN><<<blocks, 128, smem>>>(g, out, stages);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * 64 * 64 * BK * (double)stages * blocks;
+  printf("{\"probe\":\"%s\",\"ctas\":%d,\"tflops\":%.2f,\"err\":\"%s\"}\n", name, blocks, flops / best / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  const int sms = p.multiProcessorCount;
+  double *g, *out;
+  cudaMalloc(&g, sizeof(double) * 1024 * sms * 4);
+  cudaMemset(g, 0, sizeof(double) * 1024 * sms * 4);
+  cudaMalloc(&out, 8);
+  const int stages = 20000;
+  for (int per : {2, 3}) {
+    run<0, 4, 4>(per == 2 ? "lds_only_2cta" : "lds_only_3cta", sms * per, g, out, stages);
+    run<1, 4, 4>(per == 2 ? "lds_barrier_2cta" : "lds_barrier_3cta", sms * per, g, out, stages);
+    run<2, 4, 4>(per == 2 ? "cpasync_ring_2cta" : "cpasync_ring_3cta", sms * per, g, out, stages);
+  }
+  return 0;
+}
