@@ -79,7 +79,7 @@ struct PencilParams {
   const void* Braw;
   void* coef;        // nb x (dmax x q): block j rows [part*w + i], ld = w (scalar T)
   double* theta;     // k_act (block mode) / nb x want (raw mode)
-  int* info;         // nb x 4: fallback, zero_residual, error, attempts
+  int* info;         // nb x 4: fallback, zero_residual, error, attempts | Jacobi sweeps << 8
   double* cscale;    // nb
   int mode;          // 0 = block_update, 1 = raw pencil
   int want;          // raw mode
@@ -334,6 +334,7 @@ BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& 
     __syncthreads();
   }
   __syncthreads();
+  if (threadIdx.x == 0) S.misc[2] += min(sweep + 1, 60);  // sweeps, reported in info[3] >> 8
   return sweep;
 }
 
@@ -509,6 +510,7 @@ BK_DEV int packed_jacobi(int d, PSmem<double>& S) {
     __syncthreads();
   }
   __syncthreads();
+  if (threadIdx.x == 0) S.misc[2] += min(sweep + 1, LOG_SWEEPS);
   return min(sweep + 1, LOG_SWEEPS);  // logged sweeps (the last one may be all identities)
 }
 
@@ -685,6 +687,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   S.pp = S.ord + PD;
   S.pq = S.pp + PD / 2;
   S.misc = S.pq + PD / 2;
+  if (threadIdx.x == 0) S.misc[2] = 0;
   S.ro = S.misc + 8;
   S.pk = reinterpret_cast<double*>(S.ro + ((PD + 3) & ~3));
 
@@ -704,7 +707,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
       for (int e = tid; e < d * P.want; e += blockDim.x) cout[e] = S.M1[(e / P.want) * PLD + e % P.want];
       for (int r = tid; r < P.want; r += blockDim.x) P.theta[(int64_t)j * P.want + r] = S.ev[r];
     }
-    if (tid == 0) { P.info[4 * j + 2] = st; P.info[4 * j + 0] = 0; P.info[4 * j + 1] = 0; P.info[4 * j + 3] = 1; }
+    if (tid == 0) { P.info[4 * j + 2] = st; P.info[4 * j + 0] = 0; P.info[4 * j + 1] = 0; P.info[4 * j + 3] = 1 | (S.misc[2] << 8); }
     return;
   }
 
@@ -842,7 +845,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     P.info[4 * j + 0] = fallback;
     P.info[4 * j + 1] = zero_res;
     P.info[4 * j + 2] = err;
-    P.info[4 * j + 3] = attempts;
+    P.info[4 * j + 3] = attempts | (S.misc[2] << 8);  // attempts, Jacobi sweeps (all attempts)
     P.cscale[j] = cmax;
   }
 }
@@ -953,7 +956,7 @@ extern "C" int64_t bk_pencil_ws_bytes(int nb, int dmax, int cplx) {
 
 // Device-side block_update for every subblock (see file header).  Araw/Braw from
 // bk_subblock_grams_*.  coef: nb x (dmax x q) scalars; theta: k_act; info: nb x 4 ints
-// (used_fallback, zero_residual, error, attempts); cscale: nb doubles.
+// (used_fallback, zero_residual, error, attempts | total Jacobi sweeps << 8); cscale: nb doubles.
 extern "C" int bk_subblock_pencils_d(int k_act, int q, int has_p, const double* Araw, const double* Braw,
                                      double* coef, double* theta, int* info, double* cscale, int force_fallback,
                                      void* ws, int64_t ws_bytes, void* stream) {
