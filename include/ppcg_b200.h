@@ -81,6 +81,25 @@ int bk_subblock_pencils_z(int k_act, int q, int has_p, const double* Araw, const
 int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, const double* B, int want,
                         double* omega, double* C, int* status, void* ws, int64_t ws_bytes, void* stream);
 
+/* ---- large subblock updates (pencil dimension > bk_pencil_max_dim(): whole-block PPCG,
+ *      LOBPCG): block_update ppcg.py:278-378 with the branch logic on the host
+ *      (bigblock.py); cplx selects interleaved complex128 data */
+/* A, B (d x d, ld) = scaled symmetrised pencil of the kept basis columns idx[0:d] with
+ * scales sf[0:d] from raw Grams Ar/Br (ld ldr)  (ppcg.py:312-330, core.py:143-164) */
+int bk_block_assemble(int d, int cplx, const int* idx, const double* sf, const double* Ar,
+                      const double* Br, int64_t ldr, double* A, double* B, int64_t ld, void* stream);
+/* coef (nrows x w, ld w) = C[:, :w] rows scattered to raw columns idx and un-scaled by sf;
+ * cmax = max |C[:, :w]| (coeff_scale, ppcg.py:358-363, 376) */
+int bk_block_coef(int d, int w, int nrows, int cplx, const int* idx, const double* sf, const double* C,
+                  int64_t ldc, double* coef, double* cmax, void* stream);
+/* breakdown statistics of an n x m block (ppcg.py:701-705): flags[0] |= non-finite,
+ * flags[slot] = max(flags[slot], bits(max |x|)), slot 1 = X, 2 = P, 0 = non-finite test only */
+int bk_block_stats(int64_t n, int m, int cplx, const double* X, int64_t ldx, unsigned long long* flags,
+                   int slot, void* stream);
+/* singular values (descending) of a row-major m x n matrix (gesvd); rank test ppcg.py:351-356 */
+int bk_svals_d(void* ctx, int m, int n, const double* M, int64_t ldm, double* s);
+int bk_svals_z(void* ctx, int m, int n, const double* M, int64_t ldm, double* s);
+
 /* ---- recombination: ppcg.py:365-369 and _run_subblocks ppcg.py:521-532 (+ breakdown
  *      flags of ppcg.py:701-705) */
 int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double* coef,

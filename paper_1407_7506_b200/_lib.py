@@ -44,6 +44,11 @@ _SIGS = {
                                     vp, vp, vp, vp, vp, c_i64, vp]),
     "bk_pencil_max_dim": (c_int, []),
     "bk_pencil_ws_bytes": (c_i64, [c_int, c_int, c_int]),
+    "bk_block_assemble": (c_int, [c_int, c_int, vp, vp, vp, vp, c_i64, vp, vp, c_i64, vp]),
+    "bk_block_coef": (c_int, [c_int, c_int, c_int, c_int, vp, vp, vp, c_i64, vp, vp, vp]),
+    "bk_block_stats": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_int, vp]),
+    "bk_svals_d": (c_int, [vp, c_int, c_int, vp, c_i64, vp]),
+    "bk_svals_z": (c_int, [vp, c_int, c_int, vp, c_i64, vp]),
     "bk_subblock_pencils_z": (c_int, [c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_int, vp, c_i64, vp]),
     "bk_pencil_batched_z": (c_int, [c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp, c_i64, vp]),
     "bk_subblock_recombine_z": (c_int, [c_i64, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, vp,

@@ -385,3 +385,54 @@ extern "C" int bk_householder_q_d(void* ctx, int64_t n, int m, double* X, int64_
 extern "C" int bk_householder_q_z(void* ctx, int64_t n, int m, double* X, int64_t ldx, double* tmp) {
   return householder_q(static_cast<DenseCtx*>(ctx), n, m, X, ldx, tmp, 1);
 }
+
+// Singular values of a row-major m x n matrix M (ld ldm, scalars of the field) into s
+// (min(m, n) device doubles, descending), via gesvd on a column-major copy (m >= n arranged
+// by transposing when needed: singular values are transpose-invariant).  Used by the large
+// subblock path for the rank test sigma_min(C_X) < 1e-14 max(||C||_2, 1) (ppcg.py:351-356).
+namespace bk {
+__global__ void k_to_colmajor(int rows, int cols, const double* M, int64_t ldm, int trans, double* T, int cplx) {
+  // trans == 0: T (rows x cols, col-major, ld rows) = M;  trans == 1: T (cols x rows) = M^T
+  const int64_t tot = (int64_t)rows * cols;
+  const int w = cplx ? 2 : 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    const int64_t dst = trans ? ((int64_t)i * cols + j) : ((int64_t)j * rows + i);
+    for (int t = 0; t < w; ++t) T[dst * w + t] = M[(i * ldm + j) * w + t];
+  }
+}
+}  // namespace bk
+
+static int svals(DenseCtx* c, int m, int n, const double* M, int64_t ldm, double* s, int cplx) {
+  if (m <= 0 || n <= 0) return BK_ERR_ARG;
+  const int w = cplx ? 2 : 1;
+  const int trans = m < n ? 1 : 0;
+  const int mm = trans ? n : m, nn = trans ? m : n;  // column-major mm x nn with mm >= nn
+  int lw = 0;
+  cusolverStatus_t st = cplx ? cusolverDnZgesvd_bufferSize(c->h, mm, nn, &lw) : cusolverDnDgesvd_bufferSize(c->h, mm, nn, &lw);
+  if (st != CUSOLVER_STATUS_SUCCESS) return BK_ERR_SOLVER;
+  const size_t abytes = (((size_t)mm * nn * w * sizeof(double)) + 255) & ~(size_t)255;
+  const size_t rbytes = (((size_t)nn * 5 * sizeof(double)) + 255) & ~(size_t)255;
+  if (ensure(c, abytes + rbytes + (size_t)lw * w * sizeof(double), 0) != BK_OK) return BK_ERR_CUDA;
+  double* T = reinterpret_cast<double*>(c->dwork);
+  double* rwork = reinterpret_cast<double*>(static_cast<char*>(c->dwork) + abytes);
+  double* work = reinterpret_cast<double*>(static_cast<char*>(c->dwork) + abytes + rbytes);
+  BK_COUNT();
+  k_to_colmajor<<<grid_for((int64_t)m * n), 256, 0, c->st>>>(m, n, M, ldm, trans, T, cplx);
+  if (!cplx) {
+    st = cusolverDnDgesvd(c->h, 'N', 'N', mm, nn, T, mm, s, nullptr, 1, nullptr, 1, work, lw, rwork, c->dinfo);
+  } else {
+    st = cusolverDnZgesvd(c->h, 'N', 'N', mm, nn, reinterpret_cast<cuDoubleComplex*>(T), mm, s, nullptr, 1, nullptr,
+                          1, reinterpret_cast<cuDoubleComplex*>(work), lw, rwork, c->dinfo);
+  }
+  if (st != CUSOLVER_STATUS_SUCCESS) return BK_ERR_SOLVER;
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+extern "C" int bk_svals_d(void* ctx, int m, int n, const double* M, int64_t ldm, double* s) {
+  return svals(static_cast<DenseCtx*>(ctx), m, n, M, ldm, s, 0);
+}
+extern "C" int bk_svals_z(void* ctx, int m, int n, const double* M, int64_t ldm, double* s) {
+  return svals(static_cast<DenseCtx*>(ctx), m, n, M, ldm, s, 1);
+}

@@ -290,6 +290,31 @@ def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AX
               flags.data_ptr(), stream_ptr())
 
 
+# ----------------------------------------------------------------------------- large subblocks
+def pencil_max_dim():
+    """Largest pencil dimension the batched device pencils solve (larger: bigblock.py)."""
+    return int(_lib.load().bk_pencil_max_dim())
+
+
+def block_assemble(d, idx, sf, araw, braw, ldr, a, b):
+    """a, b (d x d) = scaled symmetrised pencil of the kept raw columns idx (int32) / scales sf."""
+    cplx = 1 if a.dtype == C128 else 0
+    _lib.call("bk_block_assemble", d, cplx, idx.data_ptr(), sf.data_ptr(), araw.data_ptr(), braw.data_ptr(), ldr,
+              a.data_ptr(), b.data_ptr(), ld_of(a), stream_ptr())
+
+
+def block_coef(d, w, nrows, idx, sf, c, coef, cmax):
+    cplx = 1 if c.dtype == C128 else 0
+    _lib.call("bk_block_coef", d, w, nrows, cplx, idx.data_ptr(), sf.data_ptr(), c.data_ptr(), ld_of(c),
+              coef.data_ptr(), cmax.data_ptr(), stream_ptr())
+
+
+def block_stats(x, flags, slot):
+    cplx = 1 if x.dtype == C128 else 0
+    _lib.call("bk_block_stats", x.shape[0], x.shape[1], cplx, x.data_ptr(), ld_of(x), flags.data_ptr(), slot,
+              stream_ptr())
+
+
 def pencil_batched(a, b, want, omega, c, status):
     """a, b: (nb, ldm, ldm) float64/complex128; solves nb pencils of dimension ldm."""
     nb, d, _ = a.shape
@@ -419,6 +444,12 @@ class Dense:
         name = "bk_rr_pencil_z" if a.dtype == C128 else "bk_rr_pencil_d"
         _lib.call(name, self.h, a.shape[0], a.data_ptr(), ld_of(a), b.data_ptr(), ld_of(b),
                   omega.data_ptr(), c.data_ptr(), ld_of(c), status.data_ptr())
+
+    def svals(self, m, s):
+        """s[:min(m.shape)] = singular values of the (row-major view) m, descending."""
+        self._sync_stream()
+        name = "bk_svals_z" if m.dtype == C128 else "bk_svals_d"
+        _lib.call(name, self.h, m.shape[0], m.shape[1], m.data_ptr(), ld_of(m), s.data_ptr())
 
     def householder_q(self, x, tmp):
         self._sync_stream()

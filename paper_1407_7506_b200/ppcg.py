@@ -202,6 +202,7 @@ class PPCGSolver:
             raise DimensionError(f"k + nbuf = {self.kt} exceeds operator dimension {self.n}")
         self.x0 = x0
         self.matvecs = 0
+        self._pmax = None
 
     # ------------------------------------------------------------------ helpers
     def _A(self, x, y):
@@ -324,9 +325,11 @@ class PPCGSolver:
         self.h_info = torch.zeros(nbmax * 4, dtype=torch.int32).pin_memory()
         self.h_cscale = torch.zeros(nbmax, dtype=torch.float64).pin_memory()
         self.eye = torch.eye(kt, dtype=self.tdt, device="cuda")
+        from .bigblock import LargeBlocks
         from .kernels import dense_context
 
         self.dense = dense_context()
+        self.large = LargeBlocks(self)
 
     # views
     def X(self):
@@ -617,18 +620,23 @@ class PPCGSolver:
         psrc, pdst = self.pi, 1 - self.pi
         XFs, AXFs = self.XF[src], self.AXF[src]
         Ps, APs = self.P[psrc], self.AP[psrc]
-        K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
-                         AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
-                         self.araw, self.braw, tmp=self.gtmp)
-        self._red(self.araw, self.braw)
-        K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
-                           self.cscale)
-        self.flags64.zero_()
-        K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
-                             Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
-                             self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
-                             self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
-                             coef_tmp=self.coef_tmp)
+        if self._large((3 if self.has_p else 2) * q, q):
+            # pencils beyond the batched kernel (whole-block mode, sbsize >= 65): bigblock.py
+            self.flags64.zero_()
+            self.large.update(ka, q, self.has_p, src, psrc, dst, pdst)
+        else:
+            K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
+                             AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
+                             self.araw, self.braw, tmp=self.gtmp)
+            self._red(self.araw, self.braw)
+            K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
+                               self.cscale)
+            self.flags64.zero_()
+            K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
+                                 Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
+                                 self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
+                                 self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
+                                 coef_tmp=self.coef_tmp)
         nb = (ka + q - 1) // q
         if self.comm is not None:
             self.comm.allreduce_max(self.flags64)
@@ -717,6 +725,14 @@ class PPCGSolver:
         w = hi - lo
         c0 = self._c0r(L + lo)
         XFp, AXFp = self.XF[prev_idx], self.AXF[prev_idx]
+        if self._large(2 * w, w):
+            self.flags64.zero_()
+            self.large.update(ka, q, False, prev_idx, self.pi, self.xi, self.pi, force_fallback=True,
+                              blocks=[(lo, hi)])
+            self._fetch((self.info, self.h_info))
+            if int(self.h_info.numpy()[2]) != 0:
+                raise SingularGramError("Gram matrix numerically singular in fallback pencil")
+            return
         K.subblock_grams(self.nl, w, w, False, XFp.data_ptr(), self.W.data_ptr(), 0, AXFp.data_ptr(),
                          self.AW.data_ptr(), 0, self._ldr(), c0, self.araw, self.braw, tmp=self.gtmp)
         self._red(self.araw, self.braw)
@@ -730,6 +746,13 @@ class PPCGSolver:
         self._fetch((self.info, self.h_info))
         if int(self.h_info.numpy()[2]) != 0:
             raise SingularGramError("Gram matrix numerically singular in fallback pencil")
+
+    def _large(self, dmax, q):
+        """Pencils beyond the batched kernels (dimension > 192 or subblocks wider than 64)
+        go through bigblock.py."""
+        if self._pmax is None:
+            self._pmax = self.K.pencil_max_dim()
+        return dmax > self._pmax or q > 64
 
     def _ldr(self):
         return self.ldp  # all state buffers share the padded row stride (complex: in complex elements)

@@ -181,3 +181,23 @@ def test_q64_scaled_configs_match_oracle_trajectory(cuda, cfg, N, k, iters):
         assert abs(r1.rel_resid - r2.rel_resid) <= 1e-6 * r2.rel_resid
     assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-9
     assert max(rep.diagnostics["proj_defect"]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,N,k,sb,iters", [(1, 24, 64, 66, 14), (5, 8, 64, 66, 10), (3, 9, 80, 41, 8)])
+def test_large_pencils_whole_block_vs_oracle(cuda, cfg, N, k, sb, iters):
+    """Subblocks whose pencil exceeds the batched kernels (3q > 192: whole-block PPCG, the
+    LOBPCG-equivalent mode of test_acceptance.py:90-106) go through bigblock.py: host-side
+    block_update branches, device Grams/cuSOLVER/tsgemm.  Real and complex, vs the oracle
+    trajectory from the same X0 (iteration 1 has no P and still uses the batched pencils)."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+
+    a, _, _, tol = config_problem(cfg, N=N)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=k, sbsize=sb, tol=1e-9, seed=0, max_iter=iters)
+    rep, ref = _solve_both(a, HostCsr(a._csr), t, HostDiag(t.d), opts)
+    assert rep.iterations == ref.iterations
+    for r1, r2 in zip(rep.trace, ref.trace):
+        assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-11 * abs(r2.trace_value)
+    assert rep.breakdown_recoveries == ref.breakdown_recoveries
+    assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-9
