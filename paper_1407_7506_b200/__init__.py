@@ -14,6 +14,7 @@ from .operators import (  # noqa: F401
     CountingOperator, DenseHermitian, DiagonalOperator, DiagonalPreconditioner, IdentityPreconditioner,
     MatrixFreeOperator, SparseHermitian,
 )
+from .baselines import BaselineOptions, davidson_solve, lobpcg_solve  # noqa: F401
 from .ppcg import PPCGSolver, SolveReport, SolverOptions, ppcg_solve, split_blocks  # noqa: F401
 from .problems import (  # noqa: F401
     config_problem, jacobi_preconditioner, laplacian_1d, laplacian_2d, laplacian_3d,

@@ -548,57 +548,10 @@ class PPCGSolver:
         self.trace.append(TraceRecord(iteration=it, trace_value=tr, rel_resid=rel, n_locked=L,
                                       n_matvec=self.matvecs,
                                       wall_ms=(time.perf_counter() - self.t0) * 1e3))
-        x, ax = self.X(), self.AX()
         w, aw = self.W[:, L:], self.AW[:, L:]
         # W = T(W) is already applied (fused into the producer); AW = A W  (ppcg.py:678-679)
         self._A(w, aw)
-        # projections (ppcg.py:680-687), W and P batched, X then X_lock sequentially
-        wnorm_done = False
-        p, ap = (self.Pa(), self.APa()) if self.has_p else (None, None)
-        proj_p = self.has_p and o.project_p
-        G1 = self.Gm[:ka, :ka]
-        G3 = self.Gp2[:ka, :ka]
-        if o.project_w or proj_p:
-            last_w = o.project_w and L == 0
-            if o.project_w and proj_p:
-                K.gram2(x, w, G1, x, p, G3)
-                self._red(G1, G3)
-                K.tsgemm([x, self.AX(), x, self.AX()], [G1, G1, G3, G3], [w, aw, p, ap], alpha=-1.0,
-                         beta=1.0, zs=[w, aw, p, ap], metric=self.stats[4:5] if last_w else None,
-                         ksplit=ka, nsplit=ka)
-            elif o.project_w:
-                K.gram(x, w, G1)
-                self._red(G1)
-                K.tsgemm([x, ax], [G1, G1], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
-                         metric=self.stats[4:5] if last_w else None, ksplit=ka, nsplit=ka)
-            else:
-                K.gram(x, p, G3)
-                self._red(G3)
-                K.tsgemm([x, ax], [G3, G3], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
-            wnorm_done = last_w
-            if L:
-                xl, axl = self.XF[self.xi][:, :L], self.AXF[self.xi][:, :L]
-                G2 = self.Gl[:L, :ka]
-                G4 = self.Gp[:L, :ka]
-                if o.project_w and proj_p:
-                    K.gram2(xl, w, G2, xl, p, G4)
-                    self._red(G2, G4)
-                    K.tsgemm([xl, axl, xl, axl], [G2, G2, G4, G4], [w, aw, p, ap], alpha=-1.0, beta=1.0,
-                             zs=[w, aw, p, ap], metric=self.stats[4:5], ksplit=L, nsplit=ka)
-                    wnorm_done = True
-                elif o.project_w:
-                    K.gram(xl, w, G2)
-                    self._red(G2)
-                    K.tsgemm([xl, axl], [G2, G2], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
-                             metric=self.stats[4:5], ksplit=L, nsplit=ka)
-                    wnorm_done = True
-                else:
-                    K.gram(xl, p, G4)
-                    self._red(G4)
-                    K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
-        if not wnorm_done:
-            K.sumsq(w, self.stats[4:5])
-        self._red(self.stats[4:5])
+        self._project(L, ka, w, aw)
         # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692): a diagnostic that
         # nothing downstream reads, so it runs on a side stream concurrently with the
         # subblock pencils (one CTA per subblock leaves most SMs idle)
@@ -618,28 +571,8 @@ class PPCGSolver:
         q = o.sbsize
         src, dst = self.xi, 1 - self.xi
         psrc, pdst = self.pi, 1 - self.pi
-        XFs, AXFs = self.XF[src], self.AXF[src]
-        Ps, APs = self.P[psrc], self.AP[psrc]
-        if self._large((3 if self.has_p else 2) * q, q):
-            # pencils beyond the batched kernel (whole-block mode, sbsize >= 65): bigblock.py
-            self.flags64.zero_()
-            self.large.update(ka, q, self.has_p, src, psrc, dst, pdst)
-        else:
-            K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
-                             AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
-                             self.araw, self.braw, tmp=self.gtmp)
-            self._red(self.araw, self.braw)
-            K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
-                               self.cscale)
-            self.flags64.zero_()
-            K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
-                                 Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
-                                 self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
-                                 self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
-                                 coef_tmp=self.coef_tmp)
+        self._subblock_update(ka, q, src, psrc, dst, pdst)
         nb = (ka + q - 1) // q
-        if self.comm is not None:
-            self.comm.allreduce_max(self.flags64)
         main.wait_stream(self.side)
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
@@ -702,6 +635,86 @@ class PPCGSolver:
             self._residual_w()
         self._check_max_iter()
         return self.done
+
+    def _project(self, L, ka, w, aw):
+        """Projections of W and P against X, then X_lock (ppcg.py:680-687; the same sequence
+        as LOBPCG's, baselines.py:265-274), W and P batched per basis; ||W||_F^2 into
+        stats[4] (fused into the last W update when possible)."""
+        K, o = self.K, self.opts
+        x, ax = self.X(), self.AX()
+        wnorm_done = False
+        p, ap = (self.Pa(), self.APa()) if self.has_p else (None, None)
+        proj_p = self.has_p and o.project_p
+        G1 = self.Gm[:ka, :ka]
+        G3 = self.Gp2[:ka, :ka]
+        if o.project_w or proj_p:
+            last_w = o.project_w and L == 0
+            if o.project_w and proj_p:
+                K.gram2(x, w, G1, x, p, G3)
+                self._red(G1, G3)
+                K.tsgemm([x, self.AX(), x, self.AX()], [G1, G1, G3, G3], [w, aw, p, ap], alpha=-1.0,
+                         beta=1.0, zs=[w, aw, p, ap], metric=self.stats[4:5] if last_w else None,
+                         ksplit=ka, nsplit=ka)
+            elif o.project_w:
+                K.gram(x, w, G1)
+                self._red(G1)
+                K.tsgemm([x, ax], [G1, G1], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
+                         metric=self.stats[4:5] if last_w else None, ksplit=ka, nsplit=ka)
+            else:
+                K.gram(x, p, G3)
+                self._red(G3)
+                K.tsgemm([x, ax], [G3, G3], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+            wnorm_done = last_w
+            if L:
+                xl, axl = self.XF[self.xi][:, :L], self.AXF[self.xi][:, :L]
+                G2 = self.Gl[:L, :ka]
+                G4 = self.Gp[:L, :ka]
+                if o.project_w and proj_p:
+                    K.gram2(xl, w, G2, xl, p, G4)
+                    self._red(G2, G4)
+                    K.tsgemm([xl, axl, xl, axl], [G2, G2, G4, G4], [w, aw, p, ap], alpha=-1.0, beta=1.0,
+                             zs=[w, aw, p, ap], metric=self.stats[4:5], ksplit=L, nsplit=ka)
+                    wnorm_done = True
+                elif o.project_w:
+                    K.gram(xl, w, G2)
+                    self._red(G2)
+                    K.tsgemm([xl, axl], [G2, G2], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
+                             metric=self.stats[4:5], ksplit=L, nsplit=ka)
+                    wnorm_done = True
+                else:
+                    K.gram(xl, p, G4)
+                    self._red(G4)
+                    K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+        if not wnorm_done:
+            K.sumsq(w, self.stats[4:5])
+        self._red(self.stats[4:5])
+
+    def _subblock_update(self, ka, q, src, psrc, dst, pdst):
+        """block_update of every q-wide subblock of the active block (ppcg.py:487-533):
+        batched device pencils, or bigblock.py beyond their limits; writes XF[dst], P[pdst],
+        AXF[dst], AP[pdst], theta, info, cscale and the breakdown flags."""
+        K, L = self.K, self.L
+        XFs, AXFs = self.XF[src], self.AXF[src]
+        Ps, APs = self.P[psrc], self.AP[psrc]
+        if self._large((3 if self.has_p else 2) * q, q):
+            # pencils beyond the batched kernel (whole-block mode, sbsize >= 65): bigblock.py
+            self.flags64.zero_()
+            self.large.update(ka, q, self.has_p, src, psrc, dst, pdst)
+        else:
+            K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
+                             AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
+                             self.araw, self.braw, tmp=self.gtmp)
+            self._red(self.araw, self.braw)
+            K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
+                               self.cscale)
+            self.flags64.zero_()
+            K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
+                                 Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
+                                 self.XF[dst].data_ptr(), self.P[pdst].data_ptr(), self.AXF[dst].data_ptr(),
+                                 self.AP[pdst].data_ptr(), self._ldr(), self._c0r(L), self.flags64,
+                                 coef_tmp=self.coef_tmp)
+        if self.comm is not None:
+            self.comm.allreduce_max(self.flags64)
 
     def _orth(self, gact, loss):
         """_orth_active (ppcg.py:475-484)."""

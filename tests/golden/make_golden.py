@@ -170,6 +170,47 @@ def solves():
     np.savez_compressed(os.path.join(HERE, "solves.npz"), **out)
 
 
+def baselines():
+    """Reference lobpcg_solve / davidson_solve (baselines.py:72-315) on the reference's test
+    problems and scaled BASELINE structures (real and complex), plus the whole-block PPCG /
+    LOBPCG equivalence case of test_acceptance.py:90-106."""
+    out = {}
+    o1, _, _, _ = P.config_problem(1, N=24)
+    a1 = B.SparseHermitian(o1._csr, "symmetric")
+    o5, _, _, _ = P.config_problem(5, N=8)
+    a5 = B.SparseHermitian(o5._csr, "hermitian")
+    runs = {
+        "rand90": (B.random_hermitian(90, 0.25, seed=17), None, dict(k=6, tol=1e-9, seed=9, max_iter=200)),
+        "lap1d": (B.laplacian_1d(300), "jacobi", dict(k=8, tol=1e-7, seed=0, max_iter=1500)),
+        "cfg1s": (a1, "jacobi", dict(k=16, tol=1e-7, seed=0, max_iter=600)),
+        "randz60": (B.random_hermitian(60, 0.5, seed=4, complex_field=True), None, dict(k=4, tol=1e-9, seed=1,
+                                                                                        max_iter=400)),
+        "cfg5s": (a5, "jacobi", dict(k=16, tol=1e-6, seed=0, max_iter=600)),
+    }
+    for name, (a, t, kw) in runs.items():
+        tt = B.jacobi_preconditioner(a) if t == "jacobi" else None
+        for solver, tag in ((B.lobpcg_solve, "lob"), (B.davidson_solve, "dav")):
+            t0 = time.time()
+            rep = solver(a, tt, opts=B.BaselineOptions(**kw))
+            print(f"{tag}_{name}: {rep.status} {rep.iterations} it {rep.matvecs} mv in {time.time() - t0:.1f}s")
+            pre = f"{tag}_{name}"
+            out[f"{pre}_values"] = rep.values
+            out[f"{pre}_trace"] = np.array([[r.iteration, r.trace_value, r.rel_resid, r.n_locked, r.n_matvec]
+                                            for r in rep.trace]).reshape(-1, 5)
+            out[f"{pre}_meta"] = np.array([rep.iterations, rep.matvecs, rep.rr_count, rep.breakdown_recoveries,
+                                           1 if rep.status == "converged" else 0])
+            out[f"{pre}_final_rn"] = np.array(rep.diagnostics["final_residual_norms"])
+            if a.n <= 600:
+                out[f"{pre}_vectors"] = rep.vectors
+    # test_acceptance.py:90-106: whole-block PPCG (rr_period 1) vs LOBPCG from the same x0
+    a = B.random_hermitian(100, 0.2, seed=12)
+    x0 = np.random.default_rng(5).standard_normal((100, 8))
+    rl = B.lobpcg_solve(a, x0=x0, opts=B.BaselineOptions(k=8, nbuf=0, tol=1e-14, seed=5, max_iter=10))
+    out["equiv_x0"] = x0
+    out["equiv_lob_vhist"] = np.array(rl.values_history[:10])
+    np.savez_compressed(os.path.join(HERE, "baselines.npz"), **out)
+
+
 def cfg2(iters):
     ours, k, q, tol = P.config_problem(2)
     a = B.SparseHermitian(ours._csr, "symmetric")
@@ -185,7 +226,11 @@ def cfg2(iters):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--baselines", action="store_true")
     args = ap.parse_args()
+    if args.baselines:
+        baselines()
+        sys.exit(0)
     kernels()
     generators()
     if args.cfg2:
