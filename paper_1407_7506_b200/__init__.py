@@ -15,6 +15,7 @@ from .operators import (  # noqa: F401
     MatrixFreeOperator, SparseHermitian,
 )
 from .baselines import BaselineOptions, davidson_solve, lobpcg_solve  # noqa: F401
+from .mmio import read_matrix_market, write_matrix_market  # noqa: F401
 from .ppcg import PPCGSolver, SolveReport, SolverOptions, ppcg_solve, split_blocks  # noqa: F401
 from .problems import (  # noqa: F401
     config_problem, jacobi_preconditioner, laplacian_1d, laplacian_2d, laplacian_3d,
