@@ -101,8 +101,7 @@ class LOBPCGSolver(PPCGSolver):
         self.trace.append(TraceRecord(iteration=it, trace_value=tr, rel_resid=rel, n_locked=L, n_matvec=self.matvecs,
                                       wall_ms=(time.perf_counter() - self.t0) * 1e3))
         w, aw = self.W[:, L:], self.AW[:, L:]
-        self._A(w, aw)                      # baselines.py:259
-        self._project(L, ka, w, aw)         # baselines.py:260-268
+        self._project(L, ka, w, aw)         # AW = A W + projections, baselines.py:259-268
         src, dst = self.xi, 1 - self.xi
         psrc, pdst = self.pi, 1 - self.pi
         self._subblock_update(ka, ka, src, psrc, dst, pdst)   # whole-block block_update

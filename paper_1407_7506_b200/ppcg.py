@@ -549,8 +549,8 @@ class PPCGSolver:
                                       n_matvec=self.matvecs,
                                       wall_ms=(time.perf_counter() - self.t0) * 1e3))
         w, aw = self.W[:, L:], self.AW[:, L:]
-        # W = T(W) is already applied (fused into the producer); AW = A W  (ppcg.py:678-679)
-        self._A(w, aw)
+        # W = T(W) is already applied (fused into the producer); AW = A W and the
+        # projections (ppcg.py:678-687)
         self._project(L, ka, w, aw)
         # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692): a diagnostic that
         # nothing downstream reads, so it runs on a side stream concurrently with the
@@ -636,58 +636,67 @@ class PPCGSolver:
         self._check_max_iter()
         return self.done
 
+    # AW = A W after the projections instead of updating A W with AX G: the same operator
+    # applications (one per iteration on W, so matvec counts and traces match), one fewer
+    # n x k_total x k_total GEMM per iteration, and an AW that is exact for the projected W
+    # rather than carrying the drift of the cached AX (ppcg.py:679-687 apply first and update).
+    FRESH_AW = True
+
     def _project(self, L, ka, w, aw):
-        """Projections of W and P against X, then X_lock (ppcg.py:680-687; the same sequence
-        as LOBPCG's, baselines.py:265-274), W and P batched per basis; ||W||_F^2 into
-        stats[4] (fused into the last W update when possible)."""
+        """W = T(R) arrives preconditioned; projections of W and P against X, then X_lock
+        (ppcg.py:680-687; the same sequence as LOBPCG's, baselines.py:259-268), W and P
+        batched per basis; AW = A W (ppcg.py:679, see FRESH_AW); ||W||_F^2 into stats[4]
+        (fused into the last W update when possible)."""
         K, o = self.K, self.opts
-        x, ax = self.X(), self.AX()
-        wnorm_done = False
+        fresh = self.FRESH_AW and o.project_w
+        if not fresh:
+            self._A(w, aw)
         p, ap = (self.Pa(), self.APa()) if self.has_p else (None, None)
         proj_p = self.has_p and o.project_p
-        G1 = self.Gm[:ka, :ka]
-        G3 = self.Gp2[:ka, :ka]
+
+        def update(xb, axb, gw, gp, ks, metric):
+            xs, gs, ys = [], [], []
+            if o.project_w:
+                xs.append(xb), gs.append(gw), ys.append(w)
+                if not fresh:
+                    xs.append(axb), gs.append(gw), ys.append(aw)
+            if proj_p:
+                xs += [xb, axb]
+                gs += [gp, gp]
+                ys += [p, ap]
+            K.tsgemm(xs, gs, ys, alpha=-1.0, beta=1.0, zs=ys, metric=metric if o.project_w else None,
+                     ksplit=ks, nsplit=ka)
+
+        def grams(xb, gw, gp):
+            if o.project_w and proj_p:
+                K.gram2(xb, w, gw, xb, p, gp)
+                self._red(gw, gp)
+            elif o.project_w:
+                K.gram(xb, w, gw)
+                self._red(gw)
+            else:
+                K.gram(xb, p, gp)
+                self._red(gp)
+
+        wnorm_done = False
         if o.project_w or proj_p:
             last_w = o.project_w and L == 0
-            if o.project_w and proj_p:
-                K.gram2(x, w, G1, x, p, G3)
-                self._red(G1, G3)
-                K.tsgemm([x, self.AX(), x, self.AX()], [G1, G1, G3, G3], [w, aw, p, ap], alpha=-1.0,
-                         beta=1.0, zs=[w, aw, p, ap], metric=self.stats[4:5] if last_w else None,
-                         ksplit=ka, nsplit=ka)
-            elif o.project_w:
-                K.gram(x, w, G1)
-                self._red(G1)
-                K.tsgemm([x, ax], [G1, G1], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
-                         metric=self.stats[4:5] if last_w else None, ksplit=ka, nsplit=ka)
-            else:
-                K.gram(x, p, G3)
-                self._red(G3)
-                K.tsgemm([x, ax], [G3, G3], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+            x, ax = self.X(), self.AX()
+            G1, G3 = self.Gm[:ka, :ka], self.Gp2[:ka, :ka]
+            grams(x, G1, G3)
+            update(x, ax, G1, G3, ka, self.stats[4:5] if last_w else None)
             wnorm_done = last_w
             if L:
                 xl, axl = self.XF[self.xi][:, :L], self.AXF[self.xi][:, :L]
-                G2 = self.Gl[:L, :ka]
-                G4 = self.Gp[:L, :ka]
-                if o.project_w and proj_p:
-                    K.gram2(xl, w, G2, xl, p, G4)
-                    self._red(G2, G4)
-                    K.tsgemm([xl, axl, xl, axl], [G2, G2, G4, G4], [w, aw, p, ap], alpha=-1.0, beta=1.0,
-                             zs=[w, aw, p, ap], metric=self.stats[4:5], ksplit=L, nsplit=ka)
-                    wnorm_done = True
-                elif o.project_w:
-                    K.gram(xl, w, G2)
-                    self._red(G2)
-                    K.tsgemm([xl, axl], [G2, G2], [w, aw], alpha=-1.0, beta=1.0, zs=[w, aw],
-                             metric=self.stats[4:5], ksplit=L, nsplit=ka)
-                    wnorm_done = True
-                else:
-                    K.gram(xl, p, G4)
-                    self._red(G4)
-                    K.tsgemm([xl, axl], [G4, G4], [p, ap], alpha=-1.0, beta=1.0, zs=[p, ap])
+                G2, G4 = self.Gl[:L, :ka], self.Gp[:L, :ka]
+                grams(xl, G2, G4)
+                update(xl, axl, G2, G4, L, self.stats[4:5])
+                wnorm_done = o.project_w
         if not wnorm_done:
             K.sumsq(w, self.stats[4:5])
         self._red(self.stats[4:5])
+        if fresh:
+            self._A(w, aw)
 
     def _subblock_update(self, ka, q, src, psrc, dst, pdst):
         """block_update of every q-wide subblock of the active block (ppcg.py:487-533):
