@@ -292,6 +292,7 @@ class PPCGSolver:
         self.Gp = sq()
         self.Gp2 = sq()
         self.Gfull = sq()
+        self.Gstack = sq()
         self.Rm = sq()
         self.Ahat = sq()
         self.Bhat = sq()
@@ -401,9 +402,45 @@ class PPCGSolver:
             self._red(self.stats[0:1])
             K.small_stats(G[:k, :k], self.stats[1:4])
             self.metric_cached = True
+        elif L < k:
+            self._residual_w_locked(x, ax, w)
+            return
         else:
             K.tsgemm([x], [G], [w], alpha=-1.0, beta=1.0, zs=[ax], rowscale=self.rowscale)
             self.metric_cached = False
+        self._precond_general(w)
+
+    def _residual_w_locked(self, x, ax, w):
+        """0 < L < k: the residual of the active block AND the next stopping metric over the
+        leading k columns of [X_lock X] (ppcg.py:655-664) without the separate k x k Gram
+        and metric GEMM (2 n k^2 flops each):
+          Gs = [X_lock X]^H AX                  one Gram; its lower ka rows are X^H AX
+          Y  = AX - [X_lock X] Gs               snapshot after K = k: ||AX_lead - X_lead G_lead||^2
+                                                on the active lead columns
+          W  = T(Y + X_lock Gs[:L])             = T(AX - X (X^H AX)), ppcg.py:630/758
+          Glk = X_lead^H AX_lock, ||AX_lock - X_lead Glk||^2 for the locked lead columns,
+          ||G_lead||_F^2 and Re tr G_lead from the blocks [Glk | Gs[:k, :k-L]]."""
+        K = self.K
+        L, k, ka = self.L, self.k, self.kt - self.L
+        ma = k - L
+        XFc, AXFc = self.XF[self.xi], self.AXF[self.xi]
+        xl, axl = XFc[:, :L], AXFc[:, :L]
+        Gs = self.Gstack[:, :ka]
+        K.gram(XFc, ax, Gs)
+        self._red(Gs)
+        K.tsgemm([XFc], [Gs], [w], alpha=-1.0, beta=1.0, zs=[ax], metric=self.stats[0:1], ksplit=k, nsplit=ma)
+        K.tsgemm([xl], [Gs[:L]], [w], alpha=1.0, beta=1.0, zs=[w], rowscale=self.rowscale)
+        Glk = self.Gl[:k, :L]
+        K.gram(XFc[:, :k], axl, Glk)
+        self._red(Glk)
+        K.tsgemm([XFc[:, :k]], [Glk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[11:12], ksplit=k,
+                 nsplit=L)
+        self._red(self.stats[0:1], self.stats[11:12])
+        K.sumsq(Glk, self.stats[12:13])
+        K.sumsq(Gs[:k, :ma], self.stats[13:14])
+        K.small_stats(Glk[:L], self.stats[14:17])
+        K.small_stats(Gs[L:k, :ma], self.stats[17:20])
+        self.metric_cached = "locked"
         self._precond_general(w)
 
     def _householder_refresh(self):
@@ -527,6 +564,9 @@ class PPCGSolver:
             self._red(self.stats[0:1])
         self._fetch((self.stats, self.h_stats))
         s = self.h_stats.numpy()
+        if self.metric_cached == "locked":  # assembled from the locked/active blocks
+            rel = math.sqrt(max(s[0] + s[11], 0.0)) / max(math.sqrt(max(s[12] + s[13], 0.0)), 1e-300)
+            return float(rel), float(s[16] + s[19])
         rel = math.sqrt(max(s[0], 0.0)) / max(math.sqrt(max(s[1], 0.0)), 1e-300)
         return float(rel), float(s[3])
 
