@@ -133,6 +133,43 @@ BK_DEV PairCol make_pair(const Seg* segs, int nseg, int M, int c, bool vec16) {
   return pc;
 }
 
+// Fast-path source of a column pair: a 16-byte aligned address readable on every row.
+//  * both columns valid and contiguous                -> the pair itself;
+//  * last valid column c with c + 1 past the operand  -> the pair if c + 1 is still inside the
+//    row stride (the padding column: read, never used);
+//  * both columns past the operand                    -> the tile's first pair (read, never used).
+// Values of columns >= M only reach accumulator rows/columns that are never stored, so edge
+// tiles can run the unpredicated full-tile loop.  ok = false: this tile takes the general path.
+BK_DEV const double* fast_pair(const Seg* segs, int nseg, int M, int c, int c_tile0, bool vec16, int64_t& ld,
+                               bool& ok) {
+  ok = false;
+  ld = 0;
+  if (!vec16) return nullptr;
+  int64_t ld0, ld1;
+  int s0, s1;
+  const double* p0 = seg_col(segs, nseg, c, ld0, s0);
+  const double* p1 = seg_col(segs, nseg, c + 1, ld1, s1);
+  const bool v0 = p0 != nullptr && c < M, v1 = p1 != nullptr && c + 1 < M;
+  if (v0 && v1) {
+    ok = s0 == s1 && (reinterpret_cast<uintptr_t>(p0) & 15) == 0;
+    ld = ld0;
+    return p0;
+  }
+  if (v0) {  // c + 1 past the operand: inside the row stride?
+    int off = 0;
+    for (int s = 0; s < s0; ++s) off += segs[s].width;
+    const int64_t phys = segs[s0].col0 + (c - off) + 1;
+    ok = phys < segs[s0].ld && (reinterpret_cast<uintptr_t>(p0) & 15) == 0;
+    ld = ld0;
+    return p0;
+  }
+  const double* pt = seg_col(segs, nseg, c_tile0, ld0, s0);
+  const double* pt1 = seg_col(segs, nseg, c_tile0 + 1, ld1, s1);
+  ok = pt != nullptr && pt1 != nullptr && s0 == s1 && c_tile0 + 1 < M && (reinterpret_cast<uintptr_t>(pt) & 15) == 0;
+  ld = ld0;
+  return pt;
+}
+
 BK_DEV void load_pair(double* dst, const PairCol& pc, int64_t row, bool rv) {
   if (pc.fused) {
     cp_async16(dst, rv ? pc.p0 + row * pc.ld0 : pc.p0, rv ? 16 : 0);
@@ -191,6 +228,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
   const PairCol px = make_pair(g.xs, g.nxs, g.M, m0 + xc, P.vec16);
   const PairCol py = make_pair(g.ys, g.nys, g.N, n0 + yc, P.vec16);
 
+  // Fast path (CTA-uniform): every column pair of the tile is one aligned 16-byte copy and
+  // the chunk is whole stages -> unpredicated cp.async with per-thread running pointers and
+  // full warp tiles only.  Edge tiles, odd offsets and ragged chunks take the general path.
+  int64_t fldx, fldy;
+  bool okx, oky;
+  const double* fpx = fast_pair(g.xs, g.nxs, g.M, m0 + xc, m0, P.vec16, fldx, okx);
+  const double* fpy = fast_pair(g.ys, g.nys, g.N, n0 + yc, n0, P.vec16, fldy, oky);
+  const bool fast = __syncthreads_and(okx && oky) && ((r_end - r_begin) % G_BK) == 0;
+
   auto load_stage = [&](int s, int st) {
     const int64_t rb = r_begin + (int64_t)s * G_BK;
     double* xd = Xs + st * C::XSTAGE;
@@ -208,6 +254,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
       load_pair(yd + kr * LDY + yc, py, row, row < r_end);
     }
   };
+  const double* fx = fpx + (r_begin + xr) * fldx;
+  const double* fy = fpy + (r_begin + yr) * fldy;
+  const int64_t fxs = (int64_t)(C::THREADS / XCPR) * fldx, fys = (int64_t)(C::THREADS / YCPR) * fldy;
+  auto load_stage_fast = [&](int s, int st) {
+    double* xd = Xs + st * C::XSTAGE + xr * LDX + xc;
+    double* yd = Ys + st * C::YSTAGE + yr * LDY + yc;
+    const double* gx = fx + (int64_t)s * G_BK * fldx;
+    const double* gy = fy + (int64_t)s * G_BK * fldy;
+#pragma unroll
+    for (int i = 0; i < C::XPAIRS; ++i) cp_async16(xd + (C::THREADS / XCPR) * i * LDX, gx + i * fxs, 16);
+#pragma unroll
+    for (int i = 0; i < C::YPAIRS; ++i) cp_async16(yd + (C::THREADS / YCPR) * i * LDY, gy + i * fys, 16);
+  };
 
   // warp placement (2 x 2); valid DMMA tiles (skip tiles outside M x N / below the diagonal)
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
@@ -224,14 +283,44 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
 #pragma unroll
     for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  const int fr = lane & 3, fc = lane >> 2;  // fragment: k = lane%4, m/n = lane/4
+  const int xoff = fr * LDX + wm * 8 * WM + fc, yoff = fr * LDY + wn * 8 * WN + fc;
+  if (fast) {
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+      if (s < nstages) load_stage_fast(s, s);
+      cp_async_commit();
+    }
+    for (int s = 0; s < nstages; ++s) {
+      cp_async_wait<ST - 2>();
+      __syncthreads();
+      {
+        const int sn = s + ST - 1;
+        if (sn < nstages) load_stage_fast(sn, sn % ST);
+        cp_async_commit();
+      }
+      if (warp_active) {  // partially valid warps run the full tile (extra entries are never stored)
+        const double* xs = Xs + (s % ST) * C::XSTAGE + xoff;
+        const double* ys = Ys + (s % ST) * C::YSTAGE + yoff;
+        double af[2][WM], bf[2][WN];
+#pragma unroll
+        for (int a = 0; a < WM; ++a) af[0][a] = lds64(xs + a * 8);
+#pragma unroll
+        for (int b = 0; b < WN; ++b) bf[0][b] = lds64(ys + b * 8);
+#pragma unroll
+        for (int kq = 0; kq < G_BK / 4; ++kq) {
+          const int cur = kq & 1;
+          dmma_step_il<WM, WN>(acc, af[cur], bf[cur], af[cur ^ 1], bf[cur ^ 1], xs + (kq + 1) * 4 * LDX, 8,
+                               ys + (kq + 1) * 4 * LDY, 8, kq + 1 < G_BK / 4);
+        }
+      }
+    }
+  } else {
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
     if (s < nstages) load_stage(s, s);
     cp_async_commit();
   }
-
-  const int fr = lane & 3, fc = lane >> 2;  // fragment: k = lane%4, m/n = lane/4
-  const int xoff = fr * LDX + wm * 8 * WM + fc, yoff = fr * LDY + wn * 8 * WN + fc;
   for (int s = 0; s < nstages; ++s) {
     cp_async_wait<ST - 2>();
     __syncthreads();
@@ -269,6 +358,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
         }
       }
     }
+  }
   }
   cp_async_wait<0>();
 

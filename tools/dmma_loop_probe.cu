@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, dou
   const double* gsrc = g + (int64_t)blockIdx.x * 1024;
   for (int s = 0; s < stages; ++s) {
     const int st = s % ST;
-    if (MODE == 2) {
+    if (MODE >= 2) {
       asm volatile("cp.async.wait_group 2;\n" ::);
     }
     if (MODE >= 1) __syncthreads();
@@ -47,6 +47,21 @@ __global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, dou
         const int e = tid + 128 * i, r = e >> 5, c = (e & 31) * 2;
         cp16(Xs + sn * BK * LD + r * LD + c, gsrc + ((s * 16 + r) & 1023) * 0 + c);
         cp16(Ys + sn * BK * LD + r * LD + c, gsrc + 512 + c);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    if (MODE == 3) {  // the Gram's real stream: rows of a tall row-major matrix (ld 524),
+      // CTA = (tile, chunk): X cols tile*64 mod 512, Y cols (tile*7)*64 mod 512, chunk rows
+      const int sn = (s + ST - 1) % ST;
+      const int tile = blockIdx.x % 81, chunk = blockIdx.x / 81;
+      const int xc0 = (tile % 9) * 56, yc0 = (tile / 9) * 56;
+      const int64_t row0 = (int64_t)chunk * stages * 16 + (int64_t)(s + ST - 1) * 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = tid + 128 * i, r = e >> 5, c = (e & 31) * 2;
+        const int64_t row = (row0 + r) % 110592;
+        cp16(Xs + sn * BK * LD + r * LD + c, g + row * 524 + xc0 + c);
+        cp16(Ys + sn * BK * LD + r * LD + c, g + row * 524 + yc0 + c);
       }
       asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -102,8 +117,9 @@ int main() {
   cudaGetDeviceProperties(&p, 0);
   const int sms = p.multiProcessorCount;
   double *g, *out;
-  cudaMalloc(&g, sizeof(double) * 1024 * sms * 4);
-  cudaMemset(g, 0, sizeof(double) * 1024 * sms * 4);
+  const size_t gbytes = sizeof(double) * 110592 * 524;
+  cudaMalloc(&g, gbytes);
+  cudaMemset(g, 0, gbytes);
   cudaMalloc(&out, 8);
   const int stages = 20000;
   for (int per : {2, 3}) {
@@ -111,5 +127,8 @@ int main() {
     run<1, 4, 4>(per == 2 ? "lds_barrier_2cta" : "lds_barrier_3cta", sms * per, g, out, stages);
     run<2, 4, 4>(per == 2 ? "cpasync_ring_2cta" : "cpasync_ring_3cta", sms * per, g, out, stages);
   }
+  // the config-2 Gram's stream: 81 tiles x 16 chunks of 432 stages, 3 CTAs/SM
+  run<3, 4, 4>("hbm_stream_gram_shape", 81 * 16, g, out, 432);
+  run<3, 4, 4>("hbm_stream_gram_shape_8waves", 81 * 44, g, out, 157);
   return 0;
 }

@@ -48,4 +48,11 @@ res["resid_rowscale_metric_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], 
                                                                metric=st[0:1], ksplit=512, nsplit=512)) / 1e9
 res["cholqr_upper_tflops"] = 0.5 * 2 * fl / t(lambda: K.tsgemm([x, y], [gg, gg], [out, bufs[0]], upper=True)) / 1e9
 res["gram2_tflops"] = 2 * fl / t(lambda: K.gram2(x, y, g, x, bufs[1], gg)) / 1e9
+# edge-tile effect: widths that are / are not multiples of the 64-wide tile
+for mm in (512, 576, 520):
+    xx = torch.randn(n, 580, dtype=torch.float64, device="cuda")[:, :mm]
+    gg2 = torch.zeros(mm, 580, dtype=torch.float64, device="cuda")[:, :mm]
+    res[f"gram_m{mm}_tflops"] = 2.0 * n * mm * mm / t(lambda: K.gram(xx, xx, gg2)) / 1e9
+    oo = torch.zeros(n, 580, dtype=torch.float64, device="cuda")[:, :mm]
+    res[f"tsgemm_m{mm}_tflops"] = 2.0 * n * mm * mm / t(lambda: K.tsgemm([xx], [gg2], [oo])) / 1e9
 print(json.dumps(res))
