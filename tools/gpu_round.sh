@@ -15,7 +15,8 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_sma
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu \
     > gpurun_out/ncu_launch_$tag.log 2>&1
-python tools/profile_iter.py 2 2 > gpurun_out/plain.log 2>&1 && for k in gram_kernel tsgemm_kernel pencil_kernel recombine_kernel spmm_csr; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+python tools/profile_iter.py 2 2 > gpurun_out/plain.log 2>&1 && for ks in gram_kernel:3 tsgemm_kernel:3 pencil_kernel:1 recombine_kernel:1 spmm_csr:2; do
+    k=${ks%%:*}; skip=${ks##*:}
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
         -o gpurun_out/prof_${tag}_$k python tools/profile_iter.py 2 2 > gpurun_out/ncu_${tag}_$k.log 2>&1
 done
