@@ -34,6 +34,7 @@ except Exception:  # pragma: no cover
 # --- thresholds (ppcg.py:39-45, core.py:64, core.py:175, rayleigh_ritz.py:22, problems.py:276)
 CX_RANK_FLOOR = 1e-14
 COEFF_REFRESH = 100.0
+BREAKDOWN_MAX = 1e8   # ppcg.py:705
 DIRECTION_FLOOR = 1e-14
 PIVOT_FLOOR = 1e-14
 GRAM_RTOL = 1e-12
@@ -548,7 +549,7 @@ class OracleRun:
             self.recoveries += nfb
             broken = not all(np.isfinite(b).all() for b in (self.x, self.p, self.ax, self.ap))
             if not broken:
-                broken = max(float(np.max(np.abs(self.x))), float(np.max(np.abs(self.p)))) > 1e8
+                broken = max(float(np.max(np.abs(self.x))), float(np.max(np.abs(self.p)))) > BREAKDOWN_MAX
             if broken:
                 self.recoveries += 1
                 self.orth_loss.append(math.inf)

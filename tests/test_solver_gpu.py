@@ -201,3 +201,34 @@ def test_large_pencils_whole_block_vs_oracle(cuda, cfg, N, k, sb, iters):
         assert abs(r1.trace_value - r2.trace_value) <= 1e-11 * abs(r2.trace_value)
     assert rep.breakdown_recoveries == ref.breakdown_recoveries
     assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-9
+
+
+@pytest.mark.parametrize("which", ["refresh", "breakdown"])
+def test_guard_branches_match_oracle(cuda, monkeypatch, which):
+    """The cache-refresh (coeff_scale > threshold: two extra operator applies, ppcg.py:718-724)
+    and breakdown-recovery (max |X|,|P| > threshold: Householder QR of the pre-update X, P
+    dropped, ppcg.py:698-717) branches, forced by lowering their thresholds in both the device
+    solver and the oracle: same recoveries/refresh counts, matvec counts and trajectory."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+    from paper_1407_7506_b200 import ppcg as PP
+
+    if which == "refresh":
+        monkeypatch.setattr(PP, "_COEFF_REFRESH", 0.99)   # coeff_scale >= 1: refresh every iteration
+        monkeypatch.setattr(O, "COEFF_REFRESH", 0.99)
+    else:
+        monkeypatch.setattr(PP, "_BREAKDOWN_MAX", 0.27)   # one recovery in the oracle's run
+        monkeypatch.setattr(O, "BREAKDOWN_MAX", 0.27)
+    a, _, _, _ = config_problem(1, N=16)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=12, sbsize=4, tol=1e-8, seed=0, max_iter=25)
+    rep, ref = _solve_both(a, HostCsr(a._csr), t, HostDiag(t.d), opts)
+    assert rep.iterations == ref.iterations
+    assert rep.breakdown_recoveries == ref.breakdown_recoveries
+    assert rep.diagnostics["cache_refreshes"] == ref.diagnostics["cache_refreshes"]
+    if which == "refresh":
+        assert ref.diagnostics["cache_refreshes"] > 0
+    else:
+        assert ref.breakdown_recoveries > 0
+    for r1, r2 in zip(rep.trace, ref.trace):
+        assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-10 * abs(r2.trace_value)
