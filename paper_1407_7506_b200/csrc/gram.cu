@@ -46,6 +46,10 @@ struct GramProblem {
   int64_t ldc;
   int symmetric;
   int tiles_m, tiles_n, ntiles;
+  // strip problems of a split Gram: entry (i, j) lands at C[(i + row_off)][(j + col_off)],
+  // transposed if trans; mirror also writes the transpose position when it lies outside
+  // the strip (global row < col_off)
+  int row_off, col_off, trans, mirror;
 };
 
 struct GramParams {
@@ -70,12 +74,14 @@ struct GramParams {
   int64_t chunk_rows;
   int max_tiles;              // tiles per problem slot in the grid
   int vec16;                  // all segment offsets/leading dims even: 16-byte copies
+  int allow_fast;             // fast-path switch (PPCG_GRAM_FAST=0 disables, for A/B checks)
   double* ws;                 // partials: [prob][tile][chunk][BM*BN]
   int* tickets;               // [prob][tile]
 };
 
 template <int BM, int BN>
 BK_DEV void subblock_problem(const GramParams& P, int b, GramProblem& g) {
+  g = GramProblem{};  // no strip offsets / transposition / mirroring in subblock mode
   int j = b >> 1, kind = b & 1;
   int lo = j * P.q;
   int w = min(P.q, P.k_act - lo);
@@ -195,6 +201,9 @@ using Small = GCfg<64, 64, 4, 3, 3>;
 // subblock pencil Grams of width 3q = 96 (q = 32, config 2): one 96 x 96 tile, 3 x 2 warps
 // of 32 x 48 -- 64 x 64 tiles would leave 44% of the DMMA work on padding (4 tiles for 96^2)
 using Sb96 = GCfg<96, 96, 4, 2, 2, 3, 2>;
+// narrow strips left over when a Gram's width is not a multiple of 64 (523 = 8 x 64 + 11):
+// 64 x 16 tiles, 4 warps of 16 x 16, small enough for 4 CTAs per SM
+using Strip = GCfg<64, 16, 4, 4, 4, 4, 1>;
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_constant__ GramParams P) {
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
   bool okx, oky;
   const double* fpx = fast_pair(g.xs, g.nxs, g.M, m0 + xc, m0, P.vec16, fldx, okx);
   const double* fpy = fast_pair(g.ys, g.nys, g.N, n0 + yc, n0, P.vec16, fldy, oky);
-  const bool fast = __syncthreads_and(okx && oky) && ((r_end - r_begin) % G_BK) == 0;
+  const bool fast = __syncthreads_and(okx && oky) && ((r_end - r_begin) % G_BK) == 0 && P.allow_fast;
 
   auto load_stage = [&](int s, int st) {
     const int64_t rb = r_begin + (int64_t)s * G_BK;
@@ -371,7 +380,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
       g.C[(int64_t)gi * g.ldc + gj] = v;
       g.C[(int64_t)gj * g.ldc + gi] = v;
     } else {
-      g.C[(int64_t)gi * g.ldc + gj] = v;
+      int r = gi + g.row_off, c = gj + g.col_off;
+      if (g.trans) { const int t = r; r = c; c = t; }
+      g.C[(int64_t)r * g.ldc + c] = v;
+      if (g.mirror && r < g.col_off) g.C[(int64_t)c * g.ldc + r] = v;
     }
   };
 
@@ -455,6 +467,11 @@ static int64_t ws_bytes_for(int64_t nrows, int64_t tiles) {
 
 template <class C>
 static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  static const int fast_on = [] {
+    const char* e = getenv("PPCG_GRAM_FAST");
+    return e ? atoi(e) : 1;
+  }();
+  P.allow_fast = fast_on;
   P.nchunks = choose_chunks(P.nrows, total_tiles_slots, C::SLOTS_PER_SM);
   int64_t part_bytes = (int64_t)total_tiles_slots * P.nchunks * C::BM * C::BN * sizeof(double);
   if (P.nchunks > 1) {
@@ -527,13 +544,88 @@ static int gram_explicit(int nprob, GramParams& P, void* ws, int64_t ws_bytes, c
   return launch_gram_cfg<C>(P, (int64_t)maxt * nprob, ws, ws_bytes, st);
 }
 
+// Split of a Gram whose width is not a multiple of 64 (k_total = 523 = 8 x 64 + 11): the
+// 64-aligned main block runs full 64 x 64 tiles (30+ TF/s, vs ~24 when a ninth, mostly empty
+// tile row/column rides along -- such edge CTAs stream as many rows as full ones), the
+// remainder strips run 64 x 16 tiles in a second launch.  The right strip covers all rows
+// (incl. the corner); the bottom strip is computed transposed (Y^T X) so it also has a
+// 64-aligned long side; a symmetric Gram needs only the right strip, mirrored.
+static int env_flag(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static bool split_worth(const GramProblem& g) {
+  static const int on = env_flag("PPCG_GRAM_SPLIT", 1);
+  return on && g.M >= 128 && g.N >= 128 && (g.M % 64 != 0 || g.N % 64 != 0) && g.nxs == 1 && g.nys == 1 && !use_big(g.N);
+}
+
+static int split_parts(const GramProblem& g, GramProblem& main, GramProblem* strips) {
+  const int M1 = g.M / 64 * 64, N1 = g.N / 64 * 64;
+  main = g;
+  main.M = M1;
+  main.N = N1;
+  main.xs[0].width = M1;
+  main.ys[0].width = N1;
+  int ns = 0;
+  if (g.N > N1) {  // right strip: rows [0, M) x cols [N1, N)
+    GramProblem r = g;
+    r.symmetric = 0;
+    r.ys[0].col0 += N1;
+    r.ys[0].width = g.N - N1;
+    r.N = g.N - N1;
+    r.col_off = N1;
+    r.mirror = g.symmetric;
+    strips[ns++] = r;
+  }
+  if (!g.symmetric && g.M > M1) {  // bottom strip rows [M1, M) x cols [0, N1), as (Y^T X)^T
+    GramProblem b = g;
+    b.symmetric = 0;
+    b.xs[0] = g.ys[0];
+    b.xs[0].width = N1;
+    b.ys[0] = g.xs[0];
+    b.ys[0].col0 += M1;
+    b.ys[0].width = g.M - M1;
+    b.M = N1;
+    b.N = g.M - M1;
+    b.col_off = M1;
+    b.trans = 1;
+    strips[ns++] = b;
+  }
+  return ns;
+}
+
+static int gram_problems(int nprob, const GramProblem* probs, int64_t n, void* ws, int64_t ws_bytes,
+                         cudaStream_t st) {
+  bool split = true;
+  for (int i = 0; i < nprob; ++i) split = split && split_worth(probs[i]);
+  GramParams A{};
+  A.nrows = n;
+  if (!split) {
+    for (int i = 0; i < nprob; ++i) A.prob[i] = probs[i];
+    if (use_big(probs[0].N)) return gram_explicit<Big>(nprob, A, ws, ws_bytes, st);
+    return gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
+  }
+  GramParams B{};
+  B.nrows = n;
+  int nb = 0;
+  for (int i = 0; i < nprob; ++i) nb += split_parts(probs[i], A.prob[i], B.prob + nb);
+  int rc = gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
+  if (rc != BK_OK || nb == 0) return rc;
+  return gram_explicit<Strip>(nb, B, ws, ws_bytes, st);
+}
+
 }  // namespace bk
 
 using namespace bk;
 
 extern "C" int64_t bk_gram_ws_bytes(int64_t n, int m1, int m2) {
   if (use_big(m2)) return ws_bytes_for<Big>(n, (int64_t)((m1 + 63) / 64) * ((m2 + 127) / 128));
-  return ws_bytes_for<Small>(n, (int64_t)((m1 + 63) / 64) * ((m2 + 63) / 64));
+  const int64_t full = ws_bytes_for<Small>(n, (int64_t)((m1 + 63) / 64) * ((m2 + 63) / 64));
+  // split launches (sequential, sharing the buffer): up to two strip problems per Gram
+  const int64_t right = (int64_t)((m1 + 63) / 64) * (((m2 % 64) + 15) / 16);
+  const int64_t bottom = (int64_t)(m2 / 64) * (((m1 % 64) + 15) / 16);
+  return lmax(full, ws_bytes_for<Strip>(n, 2 * lmax(right, bottom)));
 }
 
 // C (m1 x m2, ldc) = X(:, 0:m1)^T Y(:, 0:m2) over n rows.  symmetric != 0 requires X == Y,
@@ -559,9 +651,7 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
   g.C = C;
   g.ldc = ldc;
   g.symmetric = symmetric ? 1 : 0;
-  P.nrows = n;
-  if (use_big(m2)) return gram_explicit<Big>(1, P, ws, ws_bytes, (cudaStream_t)stream);
-  return gram_explicit<Small>(1, P, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_problems(1, &g, n, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 // Two Grams sharing the row range in one launch: C1 = X1^T Y1, C2 = X2^T Y2 (e.g. the
@@ -588,9 +678,7 @@ extern "C" int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t
     g.ldc = lc[i];
     g.symmetric = 0;
   }
-  P.nrows = n;
-  if (use_big(max(m2a, m2b))) return gram_explicit<Big>(2, P, ws, ws_bytes, (cudaStream_t)stream);
-  return gram_explicit<Small>(2, P, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_problems(2, P.prob, n, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int has_p) {
