@@ -73,6 +73,13 @@ BK_DEV void dmma_step_il(double (&acc)[WM][WN][2], const double* af, const doubl
         else if (i < WM + WN) bfn[i - WM] = lds64(yn + (i - WM) * ys);
       }
     }
+  // thin warp tiles (WM * WN < WM + WN, e.g. 4 x 1): the fragments left over
+#pragma unroll
+  for (int i = WM * WN; i < WM + WN; ++i)
+    if (has_next) {
+      if (i < WM) afn[i] = lds64(xn + i * xs);
+      else bfn[i - WM] = lds64(yn + (i - WM) * ys);
+    }
 }
 
 // ---- cp.async (LDGSTS) with zero-fill: copies src_bytes (0..cp) and zero-fills the rest
