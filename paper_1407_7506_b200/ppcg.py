@@ -203,6 +203,7 @@ class PPCGSolver:
         self.x0 = x0
         self.matvecs = 0
         self._pmax = None
+        self._overlap = None
 
     # ------------------------------------------------------------------ helpers
     def _A(self, x, y):
@@ -597,13 +598,16 @@ class PPCGSolver:
         # subblock pencils (one CTA per subblock leaves most SMs idle)
         Gd = self.Gp[:kt, :ka]
         main = torch.cuda.current_stream()
+        xfull = self.XF[self.xi]
         if self.comm is None:
-            self.side.wait_stream(main)
-            with torch.cuda.stream(self.side):
-                K.gram(self.XF[self.xi], w, Gd, ws_kind="side")
-                K.small_stats(Gd, self.stats[5:8])
+            def overlap():  # issued once the pencil Grams are queued: runs beside the pencils
+                self.side.wait_stream(main)
+                with torch.cuda.stream(self.side):
+                    K.gram(xfull, w, Gd, ws_kind="side")
+                    K.small_stats(Gd, self.stats[5:8])
+            self._overlap = overlap
         else:  # collectives stay on one stream, in the same order on every rank
-            K.gram(self.XF[self.xi], w, Gd)
+            K.gram(xfull, w, Gd)
             self._red(Gd)
             K.small_stats(Gd, self.stats[5:8])
 
@@ -745,8 +749,11 @@ class PPCGSolver:
         K, L = self.K, self.L
         XFs, AXFs = self.XF[src], self.AXF[src]
         Ps, APs = self.P[psrc], self.AP[psrc]
+        overlap, self._overlap = self._overlap, None
         if self._large((3 if self.has_p else 2) * q, q):
             # pencils beyond the batched kernel (whole-block mode, sbsize >= 65): bigblock.py
+            if overlap:
+                overlap()
             self.flags64.zero_()
             self.large.update(ka, q, self.has_p, src, psrc, dst, pdst)
         else:
@@ -754,6 +761,8 @@ class PPCGSolver:
                              AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
                              self.araw, self.braw, tmp=self.gtmp)
             self._red(self.araw, self.braw)
+            if overlap:
+                overlap()
             K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
                                self.cscale)
             self.flags64.zero_()
