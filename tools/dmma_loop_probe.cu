@@ -7,7 +7,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-constexpr int BK = 16, LD = 68, ST = 4;
+constexpr int BK = 16, LD = 68;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -18,8 +18,8 @@ __device__ __forceinline__ void cp16(void* s, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
 }
 
-template <int MODE, int WM, int WN>
-__global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, double* out, int stages) {
+template <int MODE, int WM, int WN, int ST = 4, int MINB = 3>
+__global__ void __launch_bounds__(128, MINB) loop(const double* __restrict__ g, double* out, int stages) {
   extern __shared__ double sm[];
   double* Xs = sm;
   double* Ys = sm + ST * BK * LD;
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, dou
   for (int s = 0; s < stages; ++s) {
     const int st = s % ST;
     if (MODE >= 2) {
-      asm volatile("cp.async.wait_group 2;\n" ::);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
     }
     if (MODE >= 1) __syncthreads();
     if (MODE == 2) {  // refill stage (s+3)%ST: 16 x 64 doubles for each operand
@@ -88,19 +88,19 @@ __global__ void __launch_bounds__(128, 3) loop(const double* __restrict__ g, dou
   if (t == 1234.5) out[0] = t;
 }
 
-template <int MODE, int WM, int WN>
+template <int MODE, int WM, int WN, int ST = 4, int MINB = 3>
 void run(const char* name, int blocks, const double* g, double* out, int stages) {
   const int smem = 2 * ST * BK * LD * 8;
-  cudaFuncSetAttribute(loop<MODE, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(loop<MODE, WM, WN, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  loop<MODE, WM, WN><<<blocks, 128, smem>>>(g, out, stages);
+  loop<MODE, WM, WN, ST, MINB><<<blocks, 128, smem>>>(g, out, stages);
   cudaDeviceSynchronize();
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(e0);
-    loop<MODE, WM, WN><<<blocks, 128, smem>>>(g, out, stages);
+    loop<MODE, WM, WN, ST, MINB><<<blocks, 128, smem>>>(g, out, stages);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -130,5 +130,11 @@ int main() {
   // the config-2 Gram's stream: 81 tiles x 16 chunks of 432 stages, 3 CTAs/SM
   run<3, 4, 4>("hbm_stream_gram_shape", 81 * 16, g, out, 432);
   run<3, 4, 4>("hbm_stream_gram_shape_8waves", 81 * 44, g, out, 157);
+  run<3, 4, 4, 6, 2>("hbm_stream_st6_2cta", 81 * 44, g, out, 157);
+  run<3, 4, 4, 3, 3>("hbm_stream_st3_3cta", 81 * 44, g, out, 157);
+  run<3, 4, 4, 8, 1>("hbm_stream_st8_1cta", 81 * 44, g, out, 157);
+  run<3, 4, 4, 5, 2>("hbm_stream_st5_2cta", 81 * 44, g, out, 157);
+  run<3, 4, 4, 3, 4>("hbm_stream_st3_4cta", 81 * 44, g, out, 157);
+  run<1, 4, 4, 3, 4>("lds_barrier_st3_4cta", sms * 4, g, out, 20000);
   return 0;
 }
