@@ -48,6 +48,18 @@ int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, cons
                int64_t ldy1, double* C1, int64_t ldc1, int m1b, int m2b, const double* X2,
                int64_t ldx2, const double* Y2, int64_t ldy2, double* C2, int64_t ldc2, void* ws,
                int64_t ws_bytes, void* stream);
+/* Grams whose width is not a multiple of 64 run as a 64-aligned main block plus narrow
+ * strips; bk_gram_splits says whether a width splits, and the _part variants launch one
+ * part (1 = main block, 2 = strips, 0 = both) so the strips can run on a second stream with
+ * their own workspace beside the main block */
+int bk_gram_splits(int m1, int m2);
+int bk_gram_part_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
+                   int64_t ldy, double* C, int64_t ldc, int symmetric, int part, void* ws,
+                   int64_t ws_bytes, void* stream);
+int bk_gram2_part_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1,
+                    int64_t ldy1, double* C1, int64_t ldc1, int m1b, int m2b, const double* X2,
+                    int64_t ldx2, const double* Y2, int64_t ldy2, double* C2, int64_t ldc2, int part,
+                    void* ws, int64_t ws_bytes, void* stream);
 int bk_cplx_gram_combine_d(int m1, int m2, const double* Cr, int64_t ldr, double* C, int64_t ldc,
                            void* stream);
 

@@ -34,6 +34,11 @@ _SIGS = {
     "bk_scale_rows_d": (c_int, [c_i64, c_int, vp, vp, c_i64, vp, c_i64, vp]),
     "bk_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int]),
     "bk_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
+    "bk_gram_splits": (c_int, [c_int, c_int]),
+    "bk_gram_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,
+                               vp]),
+    "bk_gram2_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,
+                                vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
     "bk_gram2_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64,
                            c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, vp, c_i64, vp]),
     "bk_cplx_gram_combine_d": (c_int, [c_int, c_int, vp, c_i64, vp, c_i64, vp]),

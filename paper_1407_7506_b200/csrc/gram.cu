@@ -595,13 +595,17 @@ static int split_parts(const GramProblem& g, GramProblem& main, GramProblem* str
   return ns;
 }
 
+// part: 0 = whole Gram (main then strips on `st`), 1 = main block only, 2 = strips only
+// (parts 1/2 let the caller run the memory-bound strips on a second stream beside the
+// compute-bound main launch; an unsplit Gram is all "main").
 static int gram_problems(int nprob, const GramProblem* probs, int64_t n, void* ws, int64_t ws_bytes,
-                         cudaStream_t st) {
+                         cudaStream_t st, int part = 0) {
   bool split = true;
   for (int i = 0; i < nprob; ++i) split = split && split_worth(probs[i]);
   GramParams A{};
   A.nrows = n;
   if (!split) {
+    if (part == 2) return BK_OK;
     for (int i = 0; i < nprob; ++i) A.prob[i] = probs[i];
     if (use_big(probs[0].N)) return gram_explicit<Big>(nprob, A, ws, ws_bytes, st);
     return gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
@@ -610,8 +614,11 @@ static int gram_problems(int nprob, const GramProblem* probs, int64_t n, void* w
   B.nrows = n;
   int nb = 0;
   for (int i = 0; i < nprob; ++i) nb += split_parts(probs[i], A.prob[i], B.prob + nb);
-  int rc = gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
-  if (rc != BK_OK || nb == 0) return rc;
+  if (part != 2) {
+    int rc = gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
+    if (rc != BK_OK) return rc;
+  }
+  if (part == 1 || nb == 0) return BK_OK;
   return gram_explicit<Strip>(nb, B, ws, ws_bytes, st);
 }
 
@@ -630,9 +637,35 @@ extern "C" int64_t bk_gram_ws_bytes(int64_t n, int m1, int m2) {
 
 // C (m1 x m2, ldc) = X(:, 0:m1)^T Y(:, 0:m2) over n rows.  symmetric != 0 requires X == Y,
 // m1 == m2 and computes only the tiles meeting the upper triangle.  (core.py:43-49)
+static int gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy, double* C,
+                  int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream, int part);
+
 extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
                          int64_t ldy, double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes,
                          void* stream) {
+  return gram_d(n, m1, m2, X, ldx, Y, ldy, C, ldc, symmetric, ws, ws_bytes, stream, 0);
+}
+
+// 1 if bk_gram_d / bk_gram2_d split this width into a main block and strips (see gram_problems)
+extern "C" int bk_gram_splits(int m1, int m2) {
+  GramProblem g{};
+  g.M = m1;
+  g.N = m2;
+  g.nxs = g.nys = 1;
+  return split_worth(g) ? 1 : 0;
+}
+
+// One part of a Gram (part 1 = main block, 2 = strips; 0 = all): callers run part 2 on a
+// second stream with its own workspace, fenced by events, beside part 1.
+extern "C" int bk_gram_part_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
+                              int64_t ldy, double* C, int64_t ldc, int symmetric, int part, void* ws,
+                              int64_t ws_bytes, void* stream) {
+  if (part < 0 || part > 2) return BK_ERR_ARG;
+  return gram_d(n, m1, m2, X, ldx, Y, ldy, C, ldc, symmetric, ws, ws_bytes, stream, part);
+}
+
+static int gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy, double* C,
+                  int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream, int part) {
   if (n < 0 || m1 < 0 || m2 < 0 || (symmetric && m1 != m2)) return BK_ERR_ARG;
   if (m1 == 0 || m2 == 0) return BK_OK;
   if (n == 0) {
@@ -651,15 +684,35 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
   g.C = C;
   g.ldc = ldc;
   g.symmetric = symmetric ? 1 : 0;
-  return gram_problems(1, &g, n, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_problems(1, &g, n, ws, ws_bytes, (cudaStream_t)stream, part);
 }
 
 // Two Grams sharing the row range in one launch: C1 = X1^T Y1, C2 = X2^T Y2 (e.g. the
 // projection Grams X^T W and X^T P of ppcg.py:680-687).
+static int gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1, int64_t ldy1,
+                   double* C1, int64_t ldc1, int m1b, int m2b, const double* X2, int64_t ldx2, const double* Y2,
+                   int64_t ldy2, double* C2, int64_t ldc2, void* ws, int64_t ws_bytes, void* stream, int part);
+
 extern "C" int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1,
                           int64_t ldy1, double* C1, int64_t ldc1, int m1b, int m2b, const double* X2,
                           int64_t ldx2, const double* Y2, int64_t ldy2, double* C2, int64_t ldc2, void* ws,
                           int64_t ws_bytes, void* stream) {
+  return gram2_d(n, m1a, m2a, X1, ldx1, Y1, ldy1, C1, ldc1, m1b, m2b, X2, ldx2, Y2, ldy2, C2, ldc2, ws, ws_bytes,
+                 stream, 0);
+}
+
+extern "C" int bk_gram2_part_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1,
+                               int64_t ldy1, double* C1, int64_t ldc1, int m1b, int m2b, const double* X2,
+                               int64_t ldx2, const double* Y2, int64_t ldy2, double* C2, int64_t ldc2, int part,
+                               void* ws, int64_t ws_bytes, void* stream) {
+  if (part < 0 || part > 2) return BK_ERR_ARG;
+  return gram2_d(n, m1a, m2a, X1, ldx1, Y1, ldy1, C1, ldc1, m1b, m2b, X2, ldx2, Y2, ldy2, C2, ldc2, ws, ws_bytes,
+                 stream, part);
+}
+
+static int gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, const double* Y1, int64_t ldy1,
+                   double* C1, int64_t ldc1, int m1b, int m2b, const double* X2, int64_t ldx2, const double* Y2,
+                   int64_t ldy2, double* C2, int64_t ldc2, void* ws, int64_t ws_bytes, void* stream, int part) {
   if (n <= 0) return BK_ERR_ARG;
   GramParams P{};
   const double* xs[2] = {X1, X2};
@@ -678,7 +731,7 @@ extern "C" int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t
     g.ldc = lc[i];
     g.symmetric = 0;
   }
-  return gram_problems(2, P.prob, n, ws, ws_bytes, (cudaStream_t)stream);
+  return gram_problems(2, P.prob, n, ws, ws_bytes, (cudaStream_t)stream, part);
 }
 
 extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int has_p) {

@@ -80,6 +80,35 @@ def workspace(kind="gram"):
 
 
 # ----------------------------------------------------------------------------- Grams
+_STRIP = threading.local()
+
+
+def set_strip_stream(stream):
+    """Second stream for the narrow strip launches of split Grams (None: same stream).  The
+    compute-bound 64-aligned main launch and the memory-bound strips then overlap."""
+    _STRIP.stream = stream
+
+
+def _split_launch(splits, call_part, ws_kind, nbytes):
+    """call_part(part, ws_ptr, ws_bytes, stream): whole Gram on the current stream, or the
+    main block there and the strips on the strip stream (own workspace), fenced by events."""
+    side = getattr(_STRIP, "stream", None)
+    main = torch.cuda.current_stream()
+    if side is None or not splits or side == main:
+        wp, wb = workspace(ws_kind).get(nbytes)
+        call_part(0, wp, wb, stream_ptr())
+        return
+    ev = torch.cuda.Event()
+    ev.record(main)
+    wp, wb = workspace(ws_kind).get(nbytes)
+    call_part(1, wp, wb, stream_ptr())
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        sp, sb = workspace("strip").get(nbytes)
+        call_part(2, sp, sb, stream_ptr())
+    main.wait_stream(side)
+
+
 def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
     """out = X^H Y (m1 x m2).  symmetric=True requires x is y (same view).  Launches on a
     second stream must pass their own ``ws_kind`` (split-K tickets live in the workspace)."""
@@ -91,22 +120,21 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
         out = torch.empty((m1, m2), dtype=x.dtype, device=x.device)
     if m1 == 0 or m2 == 0:
         return out
+    lib = _lib.load()
     if x.dtype == F64:
         px, _, _, lx = real_view(x)
         py, _, _, ly = real_view(y)
-        nb = _lib.load().bk_gram_ws_bytes(n, m1, m2)
-        wp, wb = workspace(ws_kind).get(nb)
-        _lib.call("bk_gram_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out),
-                  1 if symmetric else 0, wp, wb, stream_ptr())
+        _split_launch(lib.bk_gram_splits(m1, m2), lambda part, wp, wb, st: _lib.call(
+            "bk_gram_part_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), 1 if symmetric else 0, part,
+            wp, wb, st), ws_kind, lib.bk_gram_ws_bytes(n, m1, m2))
         return out
     # complex: real Gram of the interleaved views, then combine
     px, _, r1, lx = real_view(x)
     py, _, r2, ly = real_view(y)
     tmp = torch.empty((r1, r2), dtype=F64, device=x.device)
-    nb = _lib.load().bk_gram_ws_bytes(n, r1, r2)
-    wp, wb = workspace(ws_kind).get(nb)
-    _lib.call("bk_gram_d", n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2,
-              1 if symmetric else 0, wp, wb, stream_ptr())
+    _split_launch(lib.bk_gram_splits(r1, r2), lambda part, wp, wb, st: _lib.call(
+        "bk_gram_part_d", n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2, 1 if symmetric else 0, part, wp, wb, st),
+        ws_kind, lib.bk_gram_ws_bytes(n, r1, r2))
     _lib.call("bk_cplx_gram_combine_d", m1, m2, tmp.data_ptr(), r2, out.data_ptr(), ld_of(out),
               stream_ptr())
     return out
@@ -125,9 +153,10 @@ def gram2(x1, y1, out1, x2, y2, out2):
     q2, _, _, k2 = real_view(y2)
     lib = _lib.load()
     nb = 2 * max(lib.bk_gram_ws_bytes(n, x1.shape[1], y1.shape[1]), lib.bk_gram_ws_bytes(n, x2.shape[1], y2.shape[1]))
-    wp, wb = workspace().get(nb)
-    _lib.call("bk_gram2_d", n, x1.shape[1], y1.shape[1], p1, l1, q1, k1, out1.data_ptr(), ld_of(out1),
-              x2.shape[1], y2.shape[1], p2, l2, q2, k2, out2.data_ptr(), ld_of(out2), wp, wb, stream_ptr())
+    splits = lib.bk_gram_splits(x1.shape[1], y1.shape[1]) and lib.bk_gram_splits(x2.shape[1], y2.shape[1])
+    _split_launch(splits, lambda part, wp, wb, st: _lib.call(
+        "bk_gram2_part_d", n, x1.shape[1], y1.shape[1], p1, l1, q1, k1, out1.data_ptr(), ld_of(out1), x2.shape[1],
+        y2.shape[1], p2, l2, q2, k2, out2.data_ptr(), ld_of(out2), part, wp, wb, st), "gram", nb)
 
 
 # ----------------------------------------------------------------------------- tall GEMM

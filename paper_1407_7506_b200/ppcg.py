@@ -265,6 +265,9 @@ class PPCGSolver:
         # aligned rows for vector and bulk-tensor loads); columns keep global positions
         self.ldp = (kt + 3) // 4 * 4
         self.side = torch.cuda.Stream()  # diagnostics that overlap the subblock pencils
+        # (kernels.set_strip_stream can run the narrow strips of split Grams on a second
+        # stream beside the main launch; measured slower end to end at config 2 -- the strip
+        # CTAs only start as main CTAs retire and the fences add host work -- so it is off)
         nl = self.nl
         blk = lambda: z(nl, self.ldp)[:, :kt]  # noqa: E731
         self._ext = []
