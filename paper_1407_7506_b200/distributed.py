@@ -171,33 +171,53 @@ class TorchComm(Comm):
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        # gloo moves CPU tensors: device tensors are staged through host copies (used to
+        # exercise the multi-rank path where only one GPU is available; NCCL is the product)
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _staged(self, t, fn):
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            fn(h)
+            t.copy_(h)
+        else:
+            fn(t)
 
     def allreduce_sum(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        self._staged(t, lambda x: self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group))
 
     def allreduce_max(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        self._staged(t, lambda x: self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX, group=self.group))
 
     def _global(self, peer):
         return peer if self.group is None else self.dist.get_global_rank(self.group, peer)
 
     def exchange(self, sends, recvs):
         dist = self.dist
+        if self.stage:
+            sends = [(p, t.cpu()) for p, t in sends]
+            hrecv = [(p, t, t.new_empty(t.shape, device="cpu")) for p, t in recvs]
+            recvs = [(p, h) for p, _, h in hrecv]
         ops = [dist.P2POp(dist.isend, t, self._global(p), self.group) for p, t in sends]
         ops += [dist.P2POp(dist.irecv, t, self._global(p), self.group) for p, t in recvs]
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if self.stage:
+            for _, t, h in hrecv:
+                t.copy_(h)
 
     def allgather_rows(self, local, bounds):
         import torch
 
+        dev = "cpu" if self.stage else local.device
         rows = max(b - a for a, b in bounds)
-        pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
         pad[: local.shape[0]] = local
-        out = torch.empty((self.size * rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        out = torch.empty((self.size * rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
         self.dist.all_gather_into_tensor(out, pad, group=self.group)
-        return torch.cat([out[r * rows: r * rows + (b - a)] for r, (a, b) in enumerate(bounds)])
+        full = torch.cat([out[r * rows: r * rows + (b - a)] for r, (a, b) in enumerate(bounds)])
+        return full.to(local.device)
 
     def barrier(self):
         self.dist.barrier(group=self.group)
