@@ -81,3 +81,31 @@ def test_row_partition_complex_and_q64_vs_oracle(cuda):
             assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
             assert abs(r1.trace_value - r2.trace_value) <= 1e-11 * abs(r2.trace_value)
         assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-9
+
+
+def test_torchrun_two_ranks_cli(cuda, tmp_path):
+    """Real processes: `torchrun --nproc-per-node 2 -m paper_1407_7506_b200 solve --ngpus 2`
+    (TorchComm; gloo with host staging so both ranks fit one GPU -- NCCL needs one GPU per
+    rank) gives the single-GPU eigenvalues."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = ["solve", "--solver", "ppcg", "--problem", "config:1,16", "--k", "12", "--sbsize", "4",
+            "--precond", "jacobi", "--tol", "1e-8", "--max-iter", "300"]
+    env = dict(os.environ, PPCG_DIST_BACKEND="gloo", PYTHONPATH=root)
+    one = subprocess.run([sys.executable, "-m", "paper_1407_7506_b200"] + args, cwd=root, env=env,
+                         capture_output=True, text=True, timeout=300)
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29571", "-m", "paper_1407_7506_b200"]
+                         + args + ["--ngpus", "2"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0 and two.returncode == 0, two.stderr[-2000:]
+
+    def values(out):
+        lines = out.splitlines()
+        i = lines.index("eigenvalues:")
+        return np.array([float(v) for v in lines[i + 1:i + 13]])
+
+    v1, v2 = values(one.stdout), values(two.stdout)
+    assert np.max(np.abs(v1 - v2) / np.abs(v1)) <= 1e-10
