@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import DimensionError, RankDeficiencyError, SingularGramError
-from .ppcg import PPCGSolver, SolveReport, SolverOptions, draw_initial_block, lock_count
+from .ppcg import PPCGSolver, SolveReport, SolverOptions, initial_block_source, lock_count
 from .trace import TraceRecord
 
 __all__ = ["BaselineOptions", "lobpcg_solve", "davidson_solve", "LOBPCGSolver"]
@@ -287,7 +287,7 @@ class _Davidson:
         self.abasis = z(n, self.cap)
         # X0 = cholesky_qr(draw) (ppcg.py:414-438), AX = A X
         x = z(n, kt)
-        K.from_host(np.ascontiguousarray(draw_initial_block(n, kt, self.cplx, opts.seed, self.x0)), x)
+        K.from_host(initial_block_source(n, kt, self.cplx, opts.seed, self.x0), x)
         g = self._gram(x, x)
         fail = torch.full((1,), -1, dtype=torch.int32, device="cuda")
         self.dense.chol_upper_floor(g, fail)

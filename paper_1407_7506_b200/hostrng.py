@@ -51,11 +51,44 @@ def _find_splice(prev, prev_from, nxt):
     return None
 
 
-def standard_normal(seed, count, threads=None):
-    """Flat float64 array equal to ``np.random.default_rng(seed).standard_normal(count)``."""
+class FlatDraw:
+    """The draw as spliced segments, never assembled unless asked: ``segs`` holds
+    (i0, i1, arr, j0) with output[i0:i1] == arr[j0:j0 + i1 - i0], covering [0, count).
+    ``copy_range`` lets an upload fill pinned staging straight from the chunk buffers
+    (one host pass over the data instead of two)."""
+
+    def __init__(self, count, segs):
+        self.count = count
+        self.segs = segs
+
+    def copy_range(self, a, b, dst):
+        """dst[:] = output[a:b] (dst: 1-D float64 view of length b - a)."""
+        for i0, i1, arr, j0 in self.segs:
+            lo, hi = max(a, i0), min(b, i1)
+            if lo < hi:
+                dst[lo - a:hi - a] = arr[j0 + lo - i0:j0 + hi - i0]
+
+    def array(self, threads=None):
+        out = np.empty(self.count)
+        if len(self.segs) == 1:
+            i0, i1, arr, j0 = self.segs[0]
+            out[:] = arr[j0:j0 + i1 - i0]
+            return out
+
+        def copy(sg):
+            i0, i1, arr, j0 = sg
+            out[i0:i1] = arr[j0:j0 + i1 - i0]
+
+        with ThreadPoolExecutor(max_workers=min(len(self.segs), threads or _threads())) as ex:
+            list(ex.map(copy, self.segs))
+        return out
+
+
+def normal_draw(seed, count, threads=None):
+    """FlatDraw of ``np.random.default_rng(seed).standard_normal(count)``."""
     threads = threads or _threads()
     if count < _MIN_PARALLEL or threads < 2:
-        return np.random.default_rng(seed).standard_normal(count)
+        return FlatDraw(count, [(0, count, np.random.default_rng(seed).standard_normal(count), 0)])
     nchunk = min(threads, max(2, count // (_MIN_PARALLEL // 2)))
     M = -(-count // nchunk)           # nominal stream draws per chunk
     extra = M // 16 + 4096            # overlap covering the slow-path surplus of a chunk
@@ -75,25 +108,24 @@ def standard_normal(seed, count, threads=None):
         i_prev, j_prev = starts[-1]
         sp = _find_splice(parts[c - 1][1], j_prev, parts[c][1])
         if sp is None:
-            return np.random.default_rng(seed).standard_normal(count)
+            return FlatDraw(count, [(0, count, np.random.default_rng(seed).standard_normal(count), 0)])
         t, j = sp
         starts.append((i_prev + (t - j_prev), j))
-    out = np.empty(count)
-    bounds = [s[0] for s in starts] + [None]
-
-    def copy(c):
+    segs = []
+    for c in range(nchunk):
         i, j = starts[c]
         arr = parts[c][1]
-        end = bounds[c + 1] if c + 1 < nchunk else min(count, i + len(arr) - j)
+        end = starts[c + 1][0] if c + 1 < nchunk else i + len(arr) - j
         end = min(end, count)
         if end > i:
-            out[i:end] = arr[j:j + (end - i)]
-        return end
-
-    with ThreadPoolExecutor(max_workers=nchunk) as ex:
-        ends = list(ex.map(copy, range(nchunk)))
-    filled = ends[-1]
+            segs.append((i, end, arr, j))
+    filled = segs[-1][1]
     if filled < count:  # the last chain is on the true stream: continue it sequentially
-        g, arr = parts[-1]
-        out[filled:] = g.standard_normal(count - filled)
-    return out
+        g, _ = parts[-1]
+        segs.append((filled, count, g.standard_normal(count - filled), 0))
+    return FlatDraw(count, segs)
+
+
+def standard_normal(seed, count, threads=None):
+    """Flat float64 array equal to ``np.random.default_rng(seed).standard_normal(count)``."""
+    return normal_draw(seed, count, threads).array(threads)

@@ -372,19 +372,47 @@ def dense_context():
 
 
 _STAGE = threading.local()
+_POOL = []
+_POOL_LOCK = threading.Lock()
+
+
+def _par_rows(fn, r0, r1, row_bytes, min_bytes=1 << 20):
+    """fn(a, b) over [r0, r1) split across a shared host thread pool (numpy copies release
+    the GIL; spreading them also spreads the page faults of a freshly allocated target)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    with _POOL_LOCK:
+        if not _POOL:
+            try:
+                nt = len(os.sched_getaffinity(0))
+            except Exception:
+                nt = os.cpu_count() or 1
+            _POOL.append((ThreadPoolExecutor(max_workers=max(1, min(16, nt))), max(1, min(16, nt))))
+    pool, nt = _POOL[0]
+    parts = max(1, min(nt, (r1 - r0) * row_bytes // min_bytes))
+    if parts == 1:
+        fn(r0, r1)
+        return
+    step = -(-(r1 - r0) // parts)
+    futs = [pool.submit(fn, a, min(r1, a + step)) for a in range(r0, r1, step)]
+    for f in futs:
+        f.result()
 
 
 def to_host(x, chunk_bytes=32 << 20):
     """numpy copy of a (possibly row-strided) 2-D device block through two pinned staging
-    buffers: the device->pinned copy of one row chunk overlaps the pinned->numpy copy of
-    the previous one (a pageable .cpu() of a large block runs at a few GB/s)."""
+    buffers: the device->pinned copy of one row chunk overlaps the (multi-threaded)
+    pinned->numpy copy of the previous one (a pageable .cpu() of a large block runs at a
+    few GB/s)."""
     import numpy as np
 
     n, m = x.shape
     out = np.empty((n, m), dtype=np.complex128 if x.dtype == C128 else np.float64)
     if n == 0 or m == 0:
         return out
-    rows = max(1, chunk_bytes // (m * x.element_size()))
+    rb = m * x.element_size()
+    rows = max(1, chunk_bytes // rb)
     key = (x.dtype, m, rows)
     st = getattr(_STAGE, "bufs", None)
     if st is None or st[0] != key:
@@ -392,37 +420,57 @@ def to_host(x, chunk_bytes=32 << 20):
         st = _STAGE.bufs = (key, bufs, [torch.cuda.Event(), torch.cuda.Event()])
     _, bufs, evs = st
     pend = None
+
+    def drain(pb, p0, p1):
+        evs[pb].synchronize()
+        src = bufs[pb].numpy()
+
+        def cp(a, b):
+            out[a:b] = src[a - p0:b - p0]
+        _par_rows(cp, p0, p1, rb)
+
     for k, r0 in enumerate(range(0, n, rows)):
         r1 = min(n, r0 + rows)
         b = k & 1
         bufs[b][: r1 - r0].copy_(x[r0:r1], non_blocking=True)
         evs[b].record()
         if pend is not None:
-            pb, p0, p1 = pend
-            evs[pb].synchronize()
-            out[p0:p1] = bufs[pb][: p1 - p0].numpy()
+            drain(*pend)
         pend = (b, r0, r1)
-    pb, p0, p1 = pend
-    evs[pb].synchronize()
-    out[p0:p1] = bufs[pb][: p1 - p0].numpy()
+    drain(*pend)
     return out
 
 
-def from_host(arr, x, chunk_bytes=32 << 20):
-    """x[:, :] = arr (numpy, C-contiguous rows) through two pinned staging buffers: the
-    pinned->device copy of one row chunk overlaps the numpy->pinned copy of the next."""
+def from_host(src, x, chunk_bytes=32 << 20):
+    """x[:, :] = src through two pinned staging buffers: the pinned->device copy of one row
+    chunk overlaps the (multi-threaded) fill of the next.  src is a C-contiguous numpy
+    array, or any object with ``fill_rows(r0, r1, dst)`` (dst: a contiguous
+    (r1 - r0) x m numpy view) -- the X0 draw fills staging straight from its chunks."""
     n, m = x.shape
     if n == 0 or m == 0:
         return x
-    rows = max(1, chunk_bytes // (m * x.element_size()))
-    bufs = [torch.empty((rows, m), dtype=x.dtype, pin_memory=True) for _ in range(2)]
+    rb = m * x.element_size()
+    rows = max(1, chunk_bytes // rb)
+    key = (x.dtype, m, rows)
+    st = getattr(_STAGE, "up", None)
+    if st is None or st[0] != key:
+        st = _STAGE.up = (key, [torch.empty((rows, m), dtype=x.dtype, pin_memory=True) for _ in range(2)])
+    bufs = st[1]
+    fill = getattr(src, "fill_rows", None)
     evs = [None, None]
     for k, r0 in enumerate(range(0, n, rows)):
         r1 = min(n, r0 + rows)
         b = k & 1
         if evs[b] is not None:
             evs[b].synchronize()
-        bufs[b][: r1 - r0].numpy()[...] = arr[r0:r1]
+        dst = bufs[b].numpy()
+
+        def cp(a, c, dst=dst, r0=r0):
+            if fill is not None:
+                fill(a, c, dst[a - r0:c - r0])
+            else:
+                dst[a - r0:c - r0] = src[a:c]
+        _par_rows(cp, r0, r1, rb)
         x[r0:r1].copy_(bufs[b][: r1 - r0], non_blocking=True)
         evs[b] = torch.cuda.Event()
         evs[b].record()

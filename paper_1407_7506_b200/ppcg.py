@@ -151,6 +151,27 @@ def draw_initial_block(n, kt, complex_field, seed, x0=None):
     return np.column_stack([x0, draw(pad).astype(dtype)]) if pad else x0.copy()
 
 
+class _DrawRows:
+    """Rows [lo, hi) of the real X0 draw without assembling it: from_host fills its pinned
+    staging straight from the generator chunks (hostrng.FlatDraw)."""
+
+    def __init__(self, draw, kt, lo):
+        self.d, self.kt, self.lo = draw, kt, lo
+
+    def fill_rows(self, r0, r1, dst):
+        self.d.copy_range((self.lo + r0) * self.kt, (self.lo + r1) * self.kt, dst.reshape(-1))
+
+
+def initial_block_source(n, kt, complex_field, seed, x0=None, lo=0, hi=None):
+    """Rows [lo, hi) of draw_initial_block(...) in a form K.from_host accepts."""
+    from .hostrng import normal_draw
+
+    hi = n if hi is None else hi
+    if x0 is None and not complex_field:
+        return _DrawRows(normal_draw(seed, n * kt), kt, lo)
+    return np.ascontiguousarray(draw_initial_block(n, kt, complex_field, seed, x0)[lo:hi])
+
+
 class PPCGSolver:
     """Step-wise device PPCG (``start`` / ``step`` / ``finish``), used by ``ppcg_solve`` and
     by bench.py to time single outer iterations."""
@@ -530,12 +551,10 @@ class PPCGSolver:
         self.L = 0
         self.has_p = False
         self.metric_cached = False
-        x_host = draw_initial_block(self.n, self.kt, self.cplx, self.opts.seed, self.x0)
         # cholesky_qr of the initial block (ppcg.py:437-438)
         raw = self.XF[1]
-        if self.plan is not None:
-            x_host = x_host[self.plan.lo:self.plan.hi]
-        K.from_host(np.ascontiguousarray(x_host), raw)
+        lo, hi = (self.plan.lo, self.plan.hi) if self.plan is not None else (0, self.n)
+        K.from_host(initial_block_source(self.n, self.kt, self.cplx, self.opts.seed, self.x0, lo, hi), raw)
         G = self.Gm
         K.gram(raw, raw, G, symmetric=True)
         self._red(G)

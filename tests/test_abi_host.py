@@ -157,3 +157,20 @@ def test_initial_block_matches_reference_draw():
         if cplx:
             ref = ref + 1j * rng.standard_normal((n, kt))
         assert np.array_equal(x, ref)
+
+
+def test_initial_block_source_rows_match_draw():
+    """The unassembled X0 draw (hostrng.FlatDraw) hands out exactly the rows of the draw."""
+    from paper_1407_7506_b200.ppcg import draw_initial_block, initial_block_source
+
+    n, kt = 30000, 110
+    ref = draw_initial_block(n, kt, False, 5)
+    for lo, hi in ((0, n), (1234, 20001)):
+        src = initial_block_source(n, kt, False, 5, None, lo, hi)
+        out = np.empty((hi - lo, kt))
+        for r0 in range(0, hi - lo, 7001):
+            r1 = min(hi - lo, r0 + 7001)
+            src.fill_rows(r0, r1, out[r0:r1])
+        assert np.array_equal(out, ref[lo:hi])
+    src = initial_block_source(n, kt, True, 5, None, 10, 20)
+    assert np.array_equal(src, draw_initial_block(n, kt, True, 5)[10:20])
