@@ -53,6 +53,10 @@ int bk_gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, cons
  * part (1 = main block, 2 = strips, 0 = both) so the strips can run on a second stream with
  * their own workspace beside the main block */
 int bk_gram_splits(int m1, int m2);
+/* Gram loader: 1 = warp-specialised bulk-copy pipeline (default where row strides are even),
+ * 0 = the cp.async ring of every thread; returns the previous mode (mode < 0: query only).
+ * Both give bitwise identical results; the switch exists for A/B measurement and tests. */
+int bk_gram_set_loader(int mode);
 int bk_gram_part_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
                    int64_t ldy, double* C, int64_t ldc, int symmetric, int part, void* ws,
                    int64_t ws_bytes, void* stream);
@@ -158,6 +162,10 @@ int bk_rr_residual_d(int64_t n, int kt, int cplx, const double* V, int64_t ldv, 
 /* ---- strided column-range copy / zero (P realignment, lock_and_compact ppcg.py:399-408) */
 int bk_copy_cols(int64_t n, int w, int elem_bytes, const void* src, int64_t lds, int64_t sc0,
                  void* dst, int64_t ldd, int64_t dc0, void* stream);
+/* stream-ordered delay of ns nanoseconds (one idle thread): queued ahead of a large launch
+ * on a side stream, it lets the work made runnable at the same moment on the main stream
+ * (the subblock pencils) be dispatched to the SMs first */
+int bk_delay(int64_t ns, void* stream);
 int bk_zero_cols(int64_t n, int w, int elem_bytes, void* dst, int64_t ldd, int64_t dc0,
                  void* stream);
 

@@ -35,6 +35,7 @@ _SIGS = {
     "bk_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int]),
     "bk_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
     "bk_gram_splits": (c_int, [c_int, c_int]),
+    "bk_gram_set_loader": (c_int, [c_int]),
     "bk_gram_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,
                                vp]),
     "bk_gram2_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,
@@ -76,6 +77,7 @@ _SIGS = {
                                  c_i64, vp]),
     "bk_copy_cols": (c_int, [c_i64, c_int, c_int, vp, c_i64, c_i64, vp, c_i64, c_i64, vp]),
     "bk_zero_cols": (c_int, [c_i64, c_int, c_int, vp, c_i64, c_i64, vp]),
+    "bk_delay": (c_int, [c_i64, vp]),
     "bk_dense_create": (c_int, [PP, vp]),
     "bk_dense_destroy": (c_int, [vp]),
     "bk_dense_set_stream": (c_int, [vp, vp]),

@@ -75,6 +75,7 @@ struct GramParams {
   int max_tiles;              // tiles per problem slot in the grid
   int vec16;                  // all segment offsets/leading dims even: 16-byte copies
   int allow_fast;             // fast-path switch (PPCG_GRAM_FAST=0 disables, for A/B checks)
+  int bulk;                   // host: run gram_bulk_kernel (even row strides; PPCG_GRAM_BULK=0 disables)
   double* ws;                 // partials: [prob][tile][chunk][BM*BN]
   int* tickets;               // [prob][tile]
 };
@@ -422,6 +423,262 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gram_kernel(const __grid_
   if (tid == 0) P.tickets[tile_id] = 0;  // reset for the next launch (stream-ordered)
 }
 
+// ---------------------------------------------------------------------------------------
+// Warp-specialised variant (the default wherever row strides are even): one producer warp
+// streams each stage with bulk async copies (cp.async.bulk, one per row piece, completing
+// on the stage's "full" mbarrier); the MMA warps wait on it and release the stage through an
+// "empty" mbarrier.  The MMA warps issue no copy instructions and no CTA-wide barriers:
+// the DMMA mainloop probe measured 34.2 TF/s for this scheme vs 31.2 for the cp.async ring
+// on the same HBM stream (profiles/dmma_loop_probe_r01.json).
+//  * explicit problems (one segment per operand) may start at an odd column: the copy starts
+//    one column early and the tile sits one double right in shared memory (sh = 1), so every
+//    copy is 16-byte aligned -- odd locked counts L no longer drop to 8-byte copies;
+//  * subblock problems lay segments out at even ("padded") offsets: segment s, column off at
+//    tile column s * wp + off, wp = w rounded up to even; the epilogue maps back;
+//  * rows past the chunk end in a partial last stage are zero-filled by the producer.
+// Copies never run past an even row stride (host-checked), and tile columns past the
+// operand only feed accumulator entries that are never stored.
+struct Pieces {
+  const double* src[3];  // global address of the piece's first copied column in row 0
+  int soff[3];           // shared-memory column of that column
+  int len[3];            // doubles per row (even)
+  int n;
+  int64_t ld;
+};
+
+BK_DEV int pad_map(int p, int wp, int w) {  // padded tile column -> virtual column (or -1)
+  if (wp == 0) return p;
+  const int s = p / wp, off = p - s * wp;
+  return off < w ? s * w + off : -1;
+}
+
+// pieces of a tile [c0, c0 + B) of one operand; sh = shared-memory shift of column 0
+BK_DEV void tile_pieces(const GramProblem& g, bool xop, int c0, int B, int wp, Pieces& pc, int& sh) {
+  const Seg* segs = xop ? g.xs : g.ys;
+  const int nseg = xop ? g.nxs : g.nys;
+  const int M = xop ? g.M : g.N;
+  pc.n = 0;
+  pc.ld = segs[0].ld;
+  sh = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    pc.src[i] = segs[0].p;
+    pc.soff[i] = 0;
+    pc.len[i] = 0;
+  }
+  if (wp == 0) {  // one segment, any column parity
+    const double* p0 = segs[0].p + segs[0].col0;
+    sh = (int)((reinterpret_cast<uintptr_t>(p0) >> 3) & 1);
+    const int width = min(B, M - c0);
+    pc.src[0] = p0 + c0 - sh;
+    pc.soff[0] = 0;
+    pc.len[0] = (width + sh + 1) & ~1;
+    pc.n = 1;
+    return;
+  }
+  for (int s = 0; s < nseg; ++s) {
+    const int lo = s * wp, hi = lo + wp;
+    const int a = max(c0, lo), b = min(c0 + B, hi);
+    if (a >= b) continue;
+    pc.src[pc.n] = segs[s].p + segs[s].col0 + (a - lo);
+    pc.soff[pc.n] = a - c0;
+    pc.len[pc.n] = b - a;
+    ++pc.n;
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(const __grid_constant__ GramParams P) {
+  constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN, ST = C::STAGES;
+  constexpr int NCW = C::THREADS / 32;  // MMA warps
+  extern __shared__ __align__(16) double smem[];
+  double* Xs = smem;                    // [STAGES][BK][LDX]
+  double* Ys = smem + ST * C::XSTAGE;   // [STAGES][BK][LDY]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ys + ST * C::YSTAGE);
+  uint64_t* empty = full + ST;
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = blockIdx.x % P.max_tiles;
+  const int chunk = (blockIdx.x / P.max_tiles) % P.nchunks;
+  const int pidx = blockIdx.x / (P.max_tiles * P.nchunks);
+
+  GramProblem g;
+  int wp = 0, w = 0;  // padded segment stride (subblock mode) and real segment width
+  int Mp, Np;
+  if (P.explicit_list) {
+    g = P.prob[pidx];
+    Mp = g.M;
+    Np = g.N;
+  } else {
+    subblock_problem<BM, BN>(P, pidx, g);
+    w = g.xs[0].width;
+    wp = (w + 1) & ~1;
+    Mp = Np = g.nxs * wp;
+    g.tiles_m = (Mp + BM - 1) / BM;
+    g.tiles_n = (Np + BN - 1) / BN;
+    g.ntiles = g.tiles_m * g.tiles_n;
+  }
+  if (slot >= g.ntiles) return;
+  const int ti = slot / g.tiles_n, tj = slot % g.tiles_n;
+  const int m0 = ti * BM, n0 = tj * BN;
+  if (g.symmetric && n0 + BN <= m0) return;  // entirely below the diagonal: mirrored
+
+  const int64_t r_begin = (int64_t)chunk * P.chunk_rows;
+  const int64_t r_end = lmin(P.nrows, r_begin + P.chunk_rows);
+  const int nstages = (int)((r_end - r_begin + G_BK - 1) / G_BK);
+
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NCW) {  // ---- producer warp: lane = (operand, row); pieces held in registers
+    const int r = lane & 15;
+    const bool xop = lane < 16;
+    Pieces pc;
+    int sh, bx = 0, by = 0;
+    tile_pieces(g, true, m0, BM, wp, pc, sh);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) bx += i < pc.n ? pc.len[i] : 0;
+    Pieces py;
+    tile_pieces(g, false, n0, BN, wp, py, sh);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) by += i < py.n ? py.len[i] : 0;
+    if (!xop) pc = py;
+    const uint32_t stage_row_bytes = (uint32_t)(bx + by) * 8;
+    double* dbase = xop ? Xs + r * LDX : Ys + r * LDY;
+    const int dstage = xop ? C::XSTAGE : C::YSTAGE;
+    const double* src0 = pc.src[0] + (r_begin + r) * pc.ld;
+    const double* src1 = pc.src[1] + (r_begin + r) * pc.ld;
+    const double* src2 = pc.src[2] + (r_begin + r) * pc.ld;
+    const int64_t sstep = (int64_t)G_BK * pc.ld;
+    for (int s = 0; s < nstages; ++s) {
+      const int st = s % ST;
+      if (s >= ST) mbar_wait(empty + st, ((s / ST) - 1) & 1);
+      const int64_t rb = r_begin + (int64_t)s * G_BK;
+      const int nvalid = (int)lmin(G_BK, r_end - rb);
+      double* dst = dbase + st * dstage;
+      if (r >= nvalid) {  // partial last stage: zero rows (generic stores, before the arrive)
+        const int ld = xop ? LDX : LDY;
+        for (int c = 0; c < ld; ++c) dst[c] = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(full + st, (uint32_t)nvalid * stage_row_bytes);
+      __syncwarp();
+      if (r < nvalid) {
+        const int64_t o = (int64_t)s * sstep;
+        bulk_g2s(dst + pc.soff[0], src0 + o, pc.len[0] * 8, full + st);
+        if (pc.n > 1) bulk_g2s(dst + pc.soff[1], src1 + o, pc.len[1] * 8, full + st);
+        if (pc.n > 2) bulk_g2s(dst + pc.soff[2], src2 + o, pc.len[2] * 8, full + st);
+      }
+    }
+    return;
+  }
+
+  // ---- MMA warps
+  int shx = 0, shy = 0;
+  if (wp == 0) {
+    shx = (int)((reinterpret_cast<uintptr_t>(g.xs[0].p + g.xs[0].col0) >> 3) & 1);
+    shy = (int)((reinterpret_cast<uintptr_t>(g.ys[0].p + g.ys[0].col0) >> 3) & 1);
+  }
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int wm0 = m0 + wm * 8 * WM, wn0 = n0 + wn * 8 * WN;
+  const bool below = g.symmetric && (wn0 + 8 * WN <= wm0);
+  const bool warp_active = wm0 < Mp && wn0 < Np && !below;
+
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int a = 0; a < WM; ++a)
+#pragma unroll
+    for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const int fr = lane & 3, fc = lane >> 2;
+  const int xoff = fr * LDX + wm * 8 * WM + fc + shx, yoff = fr * LDY + wn * 8 * WN + fc + shy;
+  for (int s = 0; s < nstages; ++s) {
+    const int st = s % ST;
+    mbar_wait(full + st, (s / ST) & 1);
+    if (warp_active) {
+      const double* xs = Xs + st * C::XSTAGE + xoff;
+      const double* ys = Ys + st * C::YSTAGE + yoff;
+      double af[2][WM], bf[2][WN];
+#pragma unroll
+      for (int a = 0; a < WM; ++a) af[0][a] = lds64(xs + a * 8);
+#pragma unroll
+      for (int b = 0; b < WN; ++b) bf[0][b] = lds64(ys + b * 8);
+#pragma unroll
+      for (int kq = 0; kq < G_BK / 4; ++kq) {
+        const int cur = kq & 1;
+        dmma_step_il<WM, WN>(acc, af[cur], bf[cur], af[cur ^ 1], bf[cur ^ 1], xs + (kq + 1) * 4 * LDX, 8,
+                             ys + (kq + 1) * 4 * LDY, 8, kq + 1 < G_BK / 4);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+  }
+
+  // ---- epilogue (MMA warps only): tile (lrow, lcol) -> virtual (gi, gj)
+  auto store_final = [&](int lrow, int lcol, double v) {
+    const int pi = m0 + lrow, pj = n0 + lcol;
+    if (pi >= Mp || pj >= Np) return;
+    const int gi = pad_map(pi, wp, w), gj = pad_map(pj, wp, w);
+    if (gi < 0 || gj < 0 || gi >= g.M || gj >= g.N) return;
+    if (g.symmetric) {
+      if (gi > gj) return;  // upper triangle, mirrored
+      g.C[(int64_t)gi * g.ldc + gj] = v;
+      g.C[(int64_t)gj * g.ldc + gi] = v;
+    } else {
+      int r = gi + g.row_off, c = gj + g.col_off;
+      if (g.trans) { const int t = r; r = c; c = t; }
+      g.C[(int64_t)r * g.ldc + c] = v;
+      if (g.mirror && r < g.col_off) g.C[(int64_t)c * g.ldc + r] = v;
+    }
+  };
+
+  if (P.nchunks == 1) {
+    if (!warp_active) return;
+#pragma unroll
+    for (int a = 0; a < WM; ++a)
+#pragma unroll
+      for (int b = 0; b < WN; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          store_final(wm * 8 * WM + a * 8 + (lane >> 2), wn * 8 * WN + b * 8 + 2 * (lane & 3) + e, acc[a][b][e]);
+    return;
+  }
+
+  const int64_t tile_id = (int64_t)pidx * P.max_tiles + slot;
+  double* part = P.ws + (tile_id * P.nchunks + chunk) * (BM * BN);
+#pragma unroll
+  for (int a = 0; a < WM; ++a)
+#pragma unroll
+    for (int b = 0; b < WN; ++b)
+      *reinterpret_cast<double2*>(part + (wm * 8 * WM + a * 8 + (lane >> 2)) * BN + wn * 8 * WN + b * 8 +
+                                  2 * (lane & 3)) = make_double2(acc[a][b][0], acc[a][b][1]);
+  __threadfence();
+  named_bar_sync(1, C::THREADS);
+  if (tid == 0) s_last = (atomicAdd(&P.tickets[tile_id], 1) == P.nchunks - 1);
+  named_bar_sync(1, C::THREADS);
+  if (!s_last) return;
+  __threadfence();
+  const double* base = P.ws + tile_id * P.nchunks * (BM * BN);
+  for (int e = tid; e < BM * BN; e += C::THREADS) {
+    double v = 0.0;
+    for (int c = 0; c < P.nchunks; ++c) v += __ldcg(base + (int64_t)c * (BM * BN) + e);
+    store_final(e / BN, e % BN, v);
+  }
+  if (tid == 0) P.tickets[tile_id] = 0;
+}
+
+static int g_bulk_loader = [] {
+  const char* e = getenv("PPCG_GRAM_BULK");
+  return e ? atoi(e) : 1;
+}();
+
 static int choose_chunks(int64_t nrows, int64_t total_tiles, int slots_per_sm) {
   // Wave-aware split-K: the smallest chunk count whose last wave is >= 92% full (each chunk
   // >= 32 stages when possible); a 1.1-wave grid idles most of the second wave.
@@ -492,10 +749,15 @@ static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, i
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gram_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gram_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM + 16 * C::STAGES);
     attr = true;
   }
   BK_COUNT();
-  gram_kernel<C><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
+  if (P.bulk && g_bulk_loader)
+    gram_bulk_kernel<C><<<(unsigned)grid, C::THREADS + 32, C::SMEM + 16 * C::STAGES, st>>>(P);
+  else
+    gram_kernel<C><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
   BK_CHECK_LAUNCH();
   return BK_OK;
 }
@@ -530,12 +792,17 @@ template <class C>
 static int gram_explicit(int nprob, GramParams& P, void* ws, int64_t ws_bytes, cudaStream_t st) {
   int maxt = 0;
   P.vec16 = 1;
+  P.bulk = 1;
   for (int i = 0; i < nprob; ++i) {
     GramProblem& g = P.prob[i];
     fill_tiles<C>(g);
     if (g.M == 0 || g.N == 0) g.ntiles = 0;
     maxt = max(maxt, g.ntiles);
     if (!even_segs(g)) P.vec16 = 0;
+    // bulk copies: one segment per operand, even row strides (copies end within the row)
+    if (g.nxs != 1 || g.nys != 1 || (g.xs[0].ld & 1) || (g.ys[0].ld & 1) ||
+        (reinterpret_cast<uintptr_t>(g.xs[0].p) & 7) || (reinterpret_cast<uintptr_t>(g.ys[0].p) & 7))
+      P.bulk = 0;
   }
   if (maxt == 0) return BK_OK;
   P.nprob = nprob;
@@ -644,6 +911,12 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
                          int64_t ldy, double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes,
                          void* stream) {
   return gram_d(n, m1, m2, X, ldx, Y, ldy, C, ldc, symmetric, ws, ws_bytes, stream, 0);
+}
+
+extern "C" int bk_gram_set_loader(int mode) {
+  const int prev = g_bulk_loader;
+  if (mode >= 0) g_bulk_loader = mode ? 1 : 0;
+  return prev;
 }
 
 // 1 if bk_gram_d / bk_gram2_d split this width into a main block and strips (see gram_problems)
@@ -771,7 +1044,9 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
   for (int i = 0; i < 6; ++i)
     if (ptrs[i] && (reinterpret_cast<uintptr_t>(ptrs[i]) & 15)) aligned = false;
   P.vec16 = aligned ? 1 : 0;
+  P.bulk = aligned ? 1 : 0;  // padded segment layout needs even q, offsets and stride
   if (use_big(P.dmax)) {
+    P.bulk = 0;
     P.max_tiles = ((P.dmax + 63) / 64) * ((P.dmax + 127) / 128);
     return launch_gram_cfg<Big>(P, (int64_t)P.nprob * P.max_tiles, ws, ws_bytes, (cudaStream_t)stream);
   }

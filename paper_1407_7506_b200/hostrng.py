@@ -24,6 +24,7 @@ result is always exactly the sequential one.
 from __future__ import annotations
 
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -84,8 +85,14 @@ class FlatDraw:
         return out
 
 
-def normal_draw(seed, count, threads=None):
-    """FlatDraw of ``np.random.default_rng(seed).standard_normal(count)``."""
+_SCRATCH = threading.local()
+
+
+def normal_draw(seed, count, threads=None, reuse=False):
+    """FlatDraw of ``np.random.default_rng(seed).standard_normal(count)``.  With ``reuse``
+    the chunks are drawn into this thread's scratch buffers from the previous call (no
+    fresh pages to fault in), so the result is only valid until the thread's next
+    ``reuse`` call -- for callers that consume it at once (the X0 upload)."""
     threads = threads or _threads()
     if count < _MIN_PARALLEL or threads < 2:
         return FlatDraw(count, [(0, count, np.random.default_rng(seed).standard_normal(count), 0)])
@@ -93,11 +100,19 @@ def normal_draw(seed, count, threads=None):
     M = -(-count // nchunk)           # nominal stream draws per chunk
     extra = M // 16 + 4096            # overlap covering the slow-path surplus of a chunk
 
+    bufs = None
+    if reuse:
+        bufs = getattr(_SCRATCH, "bufs", None)
+        if bufs is None or len(bufs) != nchunk or len(bufs[0]) != M + extra:
+            bufs = _SCRATCH.bufs = [np.empty(M + extra) for _ in range(nchunk)]
+
     def draw(c):
         bg = np.random.PCG64(seed)
         if c:
             bg.advance(c * M)
         g = np.random.Generator(bg)
+        if bufs is not None:
+            return g, g.standard_normal(M + extra, out=bufs[c])
         return g, g.standard_normal(M + extra)
 
     with ThreadPoolExecutor(max_workers=nchunk) as ex:

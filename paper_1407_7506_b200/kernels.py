@@ -244,6 +244,11 @@ def copy_cols(src, dst):
               dst.data_ptr(), ld_of(dst), 0, stream_ptr())
 
 
+def delay(ns):
+    """Stream-ordered idle of ns nanoseconds on the current stream (bk_delay)."""
+    _lib.call("bk_delay", int(ns), stream_ptr())
+
+
 def zero_cols(dst):
     es = 16 if dst.dtype == C128 else 8
     _lib.call("bk_zero_cols", dst.shape[0], dst.shape[1], es, dst.data_ptr(), ld_of(dst), 0, stream_ptr())

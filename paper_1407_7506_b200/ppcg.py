@@ -21,6 +21,7 @@ column keeps its global position for the whole run, so
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -31,6 +32,9 @@ from .trace import TraceRecord
 
 __all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSolver"]
 
+# host-sync trimming (bit 0: projections queued before the metric is read; bit 1: the
+# orthonormality Gram queued before the update's flags are read); PPCG_SPECULATE overrides
+_SPECULATE = int(os.environ.get("PPCG_SPECULATE", "3"))
 _COEFF_REFRESH = 100.0   # ppcg.py:41
 _BREAKDOWN_MAX = 1e8     # ppcg.py:705
 _TAYLOR_OK = 0.1         # core.py:127
@@ -168,13 +172,15 @@ def initial_block_source(n, kt, complex_field, seed, x0=None, lo=0, hi=None):
 
     hi = n if hi is None else hi
     if x0 is None and not complex_field:
-        return _DrawRows(normal_draw(seed, n * kt), kt, lo)
+        return _DrawRows(normal_draw(seed, n * kt, reuse=True), kt, lo)
     return np.ascontiguousarray(draw_initial_block(n, kt, complex_field, seed, x0)[lo:hi])
 
 
 class PPCGSolver:
     """Step-wise device PPCG (``start`` / ``step`` / ``finish``), used by ``ppcg_solve`` and
     by bench.py to time single outer iterations."""
+
+    _metric_ev = None  # event after the queued metric copy (speculative projection, step)
 
     def __init__(self, a, t=None, x0=None, opts=None, comm=None):
         import torch
@@ -565,6 +571,7 @@ class PPCGSolver:
         self.trace, self.values_history = [], []
         self.orth_loss, self.proj_defect = [], []
         self.rr_count = self.recoveries = self.refreshes = 0
+        self._metric_ev = None
         self.prev_trace = None
         self.status, self.iterations = "max_iter", self.opts.max_iter
         self.it = 0
@@ -585,7 +592,11 @@ class PPCGSolver:
             K.tsgemm([xl], [Gk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[0:1],
                      ksplit=k, nsplit=k)
             self._red(self.stats[0:1])
-        self._fetch((self.stats, self.h_stats))
+        if self._metric_ev is None:
+            self._fetch((self.stats, self.h_stats))
+        else:  # copy issued before the speculative projection launches (step)
+            self._metric_ev.synchronize()
+            self._metric_ev = None
         s = self.h_stats.numpy()
         if self.metric_cached == "locked":  # assembled from the locked/active blocks
             rel = math.sqrt(max(s[0] + s[11], 0.0)) / max(math.sqrt(max(s[12] + s[13], 0.0)), 1e-300)
@@ -599,22 +610,36 @@ class PPCGSolver:
             return True
         K, torch, o = self.K, self.torch, self.opts
         it = self.it = self.it + 1
+        L, kt = self.L, self.kt
+        ka = kt - L
+        w, aw = self.W[:, L:], self.AW[:, L:]
+        mv0 = self.matvecs
+        # The stopping metric is already on the device (fused into the last residual): queue
+        # its copy, then the projections of this iteration, then wait for the copy only -- the
+        # GPU runs the projections while the host tests convergence.  On convergence the
+        # speculative work (W, AW, stats[4] of an iteration that does not happen) is dropped:
+        # finish() reads only X and AX, and the matvec count is rolled back.
+        spec = bool(self.metric_cached) and ka > 0 and _SPECULATE & 1
+        if spec:
+            self.h_stats.copy_(self.stats, non_blocking=True)
+            self._metric_ev = self.torch.cuda.Event()
+            self._metric_ev.record()
+            # W = T(W) is already applied (fused into the producer); AW = A W and the
+            # projections (ppcg.py:678-687)
+            self._project(L, ka, w, aw)
         rel, tr = self._metrics()
         chg = math.inf if self.prev_trace is None else abs(tr - self.prev_trace) / max(abs(tr), 1e-300)
         self.prev_trace = tr
         done = rel <= o.tol or (o.trace_tol is not None and chg <= o.trace_tol)
-        L, kt = self.L, self.kt
-        ka = kt - L
         if done or ka == 0:
+            self.matvecs = mv0
             self.status, self.iterations, self.done = "converged", it - 1, True
             return True
         self.trace.append(TraceRecord(iteration=it, trace_value=tr, rel_resid=rel, n_locked=L,
-                                      n_matvec=self.matvecs,
+                                      n_matvec=mv0,
                                       wall_ms=(time.perf_counter() - self.t0) * 1e3))
-        w, aw = self.W[:, L:], self.AW[:, L:]
-        # W = T(W) is already applied (fused into the producer); AW = A W and the
-        # projections (ppcg.py:678-687)
-        self._project(L, ka, w, aw)
+        if not spec:
+            self._project(L, ka, w, aw)
         # proj_defect = ||[X_lock X]^H W||_F / ||W||_F (ppcg.py:688-692): a diagnostic that
         # nothing downstream reads, so it runs on a side stream concurrently with the
         # subblock pencils (one CTA per subblock leaves most SMs idle)
@@ -622,9 +647,14 @@ class PPCGSolver:
         main = torch.cuda.current_stream()
         xfull = self.XF[self.xi]
         if self.comm is None:
-            def overlap():  # issued once the pencil Grams are queued: runs beside the pencils
-                self.side.wait_stream(main)
+            def overlap(ready):  # after the pencil Grams (event `ready`): runs beside the pencils
+                self.side.wait_event(ready)
                 with torch.cuda.stream(self.side):
+                    # A pencil CTA needs a whole SM's shared memory, so it cannot start on an
+                    # SM holding Gram CTAs; if both become runnable together the Gram may take
+                    # every SM first (seen whenever the host runs ahead of the GPU).  A 20 us
+                    # stream-ordered delay lets the pencil CTAs be dispatched first.
+                    K.delay(20000)
                     K.gram(xfull, w, Gd, ws_kind="side")
                     K.small_stats(Gd, self.stats[5:8])
             self._overlap = overlap
@@ -640,6 +670,14 @@ class PPCGSolver:
         self._subblock_update(ka, q, src, psrc, dst, pdst)
         nb = (ka + q - 1) // q
         main.wait_stream(self.side)
+        # orthonormality Gram of the updated [X_lock, X] (ppcg.py:726-729), queued before the
+        # host reads the update's flags so one sync serves both; a breakdown (rare) restores
+        # the previous X and leaves this Gram unused, a coefficient refresh keeps X
+        early = bool(_SPECULATE & 2)
+        if early:
+            K.gram(self.XF[dst], self.XF[dst], self.Gfull, symmetric=True)
+            self._red(self.Gfull)
+            K.small_stats(self.Gfull, self.stats[8:11])
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
         s = self.h_stats.numpy()
@@ -672,12 +710,13 @@ class PPCGSolver:
             self.refreshes += 1
             self._A(self.X(), self.AX())
             self._A(self.Pa(), self.APa())
-        # orthonormality loss of [X_lock, X] (ppcg.py:726-729)
-        K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
-        self._red(self.Gfull)
-        K.small_stats(self.Gfull, self.stats[8:11])
-        self._fetch((self.stats, self.h_stats))
-        loss = float(math.sqrt(max(self.h_stats.numpy()[9], 0.0)))
+        # orthonormality loss of [X_lock, X] (ppcg.py:726-729): its Gram came with the flags
+        if not early:
+            K.gram(self.XF[self.xi], self.XF[self.xi], self.Gfull, symmetric=True)
+            self._red(self.Gfull)
+            K.small_stats(self.Gfull, self.stats[8:11])
+            self._fetch((self.stats, self.h_stats))
+        loss = float(math.sqrt(max(s[9], 0.0)))
         self.orth_loss.append(loss)
         gact = self.Gfull[L:, L:]
         if math.isfinite(o.rr_period) and it % int(o.rr_period) == 0:
@@ -775,7 +814,9 @@ class PPCGSolver:
         if self._large((3 if self.has_p else 2) * q, q):
             # pencils beyond the batched kernel (whole-block mode, sbsize >= 65): bigblock.py
             if overlap:
-                overlap()
+                ready = self.torch.cuda.Event()
+                ready.record()
+                overlap(ready)
             self.flags64.zero_()
             self.large.update(ka, q, self.has_p, src, psrc, dst, pdst)
         else:
@@ -783,10 +824,12 @@ class PPCGSolver:
                              AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
                              self.araw, self.braw, tmp=self.gtmp)
             self._red(self.araw, self.braw)
-            if overlap:
-                overlap()
+            ready = self.torch.cuda.Event()
+            ready.record()
             K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
                                self.cscale)
+            if overlap:
+                overlap(ready)
             self.flags64.zero_()
             K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
                                  Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),

@@ -369,3 +369,71 @@ def test_dense_cholqr_and_rr_pencil(cuda):
     Cn = C.cpu().numpy()
     assert np.allclose(Cn.T @ (0.5 * (B + B.T)) @ Cn, np.eye(d), atol=1e-10)
     D.close()
+
+
+def _both_loaders(f):
+    """f() under the bulk-copy Gram loader and under the cp.async ring; restores the mode."""
+    from paper_1407_7506_b200 import _lib
+
+    lib = _lib.load()
+    prev = lib.bk_gram_set_loader(1)
+    try:
+        a = f()
+        lib.bk_gram_set_loader(0)
+        b = f()
+    finally:
+        lib.bk_gram_set_loader(prev)
+    return a, b
+
+
+@pytest.mark.parametrize("n", [4096, 20011])
+def test_gram_bulk_loader_bitwise(cuda, n):
+    """Warp-specialised bulk-copy Grams (odd column starts shifted in shared memory, ragged
+    last stage zero-filled) give bitwise the cp.async ring's result, and match numpy."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    buf = gauss(n, 524, 61)
+    tb = dev(buf, torch)
+    cases = [(0, 523, 0, 523), (1, 522, 1, 522), (10, 513, 10, 513), (5, 64, 0, 11), (3, 200, 7, 130),
+             (523 - 11, 11, 0, 523), (1, 1, 2, 3)]
+    for (a0, wa, b0, wb) in cases:
+        x, y = tb[:, a0:a0 + wa], tb[:, b0:b0 + wb]
+        g1, g0 = _both_loaders(lambda: K.gram(x, y).cpu().numpy())
+        assert np.array_equal(g1, g0), (a0, wa, b0, wb)
+        ref = buf[:, a0:a0 + wa].T @ buf[:, b0:b0 + wb]
+        assert np.max(np.abs(g1 - ref)) <= 1e-12 * np.max(np.abs(ref))
+        if (a0, wa) == (b0, wb):
+            s1, s0 = _both_loaders(lambda: K.gram(x, x, symmetric=True).cpu().numpy())
+            assert np.array_equal(s1, s0) and np.array_equal(s1, s1.T)
+            assert np.max(np.abs(s1 - ref)) <= 1e-12 * np.max(np.abs(ref))
+    x1, y1, x2, y2 = tb[:, 1:524], tb[:, 0:523], tb[:, 1:524], tb[:, 3:100]
+
+    def two():
+        o1 = torch.empty((523, 523), dtype=torch.float64, device="cuda")
+        o2 = torch.empty((523, 97), dtype=torch.float64, device="cuda")
+        K.gram2(x1, y1, o1, x2, y2, o2)
+        return o1.cpu().numpy(), o2.cpu().numpy()
+    (a1, a2), (b1, b2) = _both_loaders(two)
+    assert np.array_equal(a1, b1) and np.array_equal(a2, b2)
+    assert np.max(np.abs(a2 - buf[:, 1:524].T @ buf[:, 3:100])) <= 1e-12 * np.max(np.abs(a2))
+
+
+def test_solver_bulk_loader_bitwise(cuda):
+    """Six config-2-shaped PPCG iterations (subblock Grams with an odd-width last block,
+    split Grams, side-stream Gram) are bitwise identical under both Gram loaders."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+    from paper_1407_7506_b200.ppcg import PPCGSolver
+
+    a, _, _, tol = config_problem(2, N=20)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=75, sbsize=32, tol=1e-12, seed=0, max_iter=6)
+
+    def run():
+        s = PPCGSolver(a, t, None, opts).start()
+        while not s.step():
+            pass
+        return [r.trace_value for r in s.trace], s.X().cpu().numpy()
+    (t1, x1), (t0, x0) = _both_loaders(run)
+    assert t1 == t0
+    assert np.array_equal(x1, x0)

@@ -7,7 +7,11 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_1407_7506_b200 import _lib  # noqa: E402
 from paper_1407_7506_b200 import kernels as K  # noqa: E402
+
+if "GRAM_LOADER" in os.environ:  # 1 = bulk-copy pipeline, 0 = cp.async ring
+    _lib.load().bk_gram_set_loader(int(os.environ["GRAM_LOADER"]))
 
 
 def t(fn, reps=10):
@@ -29,7 +33,10 @@ g = torch.zeros(m, ld, dtype=torch.float64, device="cuda")[:, :m]
 out = torch.zeros(n, ld, dtype=torch.float64, device="cuda")[:, :m]
 fl = 2.0 * n * m * m
 res = {"gram_tile": os.environ.get("PPCG_GRAM_TILE", "default"), "ts_tile": os.environ.get("PPCG_TS_TILE", "default")}
+res["gram_loader"] = _lib.load().bk_gram_set_loader(-1)
 res["gram_xy_tflops"] = fl / t(lambda: K.gram(x, y, g)) / 1e9
+xo = torch.randn(n, 534, dtype=torch.float64, device="cuda")[:, 11:534]  # odd column start (odd L)
+res["gram_xy_oddcol_tflops"] = fl / t(lambda: K.gram(xo, y, g)) / 1e9
 res["gram_sym_tflops"] = 0.5 * fl / t(lambda: K.gram(x, x, g, symmetric=True)) / 1e9
 gg = torch.randn(m, ld, dtype=torch.float64, device="cuda")[:, :m]
 res["tsgemm_tflops"] = fl / t(lambda: K.tsgemm([x], [gg], [out], alpha=-1.0, beta=1.0, zs=[y])) / 1e9

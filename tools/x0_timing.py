@@ -58,3 +58,7 @@ t("pinned alloc 463 MB (cached after first)", lambda: torch.empty((n, kt), dtype
 t("parallel copy into pinned, 16 threads", lambda: par_copy(pin.numpy(), x.reshape(n, kt), 16))
 t("H2D from pinned (one copy)", lambda: dev[:, :kt].copy_(pin, non_blocking=True))
 t("D2H into pinned", lambda: pin.copy_(dev[:, :kt], non_blocking=True))
+t("normal_draw (fresh chunks)", lambda: H.normal_draw(0, count))
+t("normal_draw (reused chunks)", lambda: H.normal_draw(0, count, reuse=True))
+d = H.normal_draw(0, count, reuse=True)
+assert np.array_equal(d.array(), x)
