@@ -9,6 +9,9 @@
 // once per 32-entry batch by the lanes and broadcast with shuffles.  Row-major X rows of
 // 7/27-point stencils have reuse distances of one grid plane, far inside the 126 MB L2, so
 // DRAM traffic is ~ read X once + write Y once + the CSR arrays.
+#include <cuda.h>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bk {
@@ -98,9 +101,197 @@ __global__ void __launch_bounds__(S_THREADS) spmm_csr_cplx(int64_t n, const int3
   }
 }
 
+
+// ---- one warp per row, whole row in one pass (default for blocks up to 1024 real / 512
+// complex columns).
+//
+// The row gather above is latency-bound (ncu: long-scoreboard stalls, DRAM ~35% busy): per
+// nonzero it issues one 8-byte load per lane and waits for it before the next nonzero.
+// Here every lane owns NV 16-byte pieces of the row (real: the aligned column pairs
+// (2p - off, 2p + 1 - off); complex: one element), so a warp moves a whole X row per
+// nonzero with 16-byte loads, and the loads of U nonzeros are issued before their FMAs.
+// The loop body is branch-free: padded nonzero slots and pieces outside the row reload a
+// valid piece and are discarded at the (warp-uniform) FMA predicate / the store.  Real
+// blocks whose first or last column is half of a 16-byte pair leave those (at most two)
+// columns to spmm_csr_edge.  Each warp walks RPW consecutive rows and loads the next row's
+// (col, val) batch while the current row computes.  FMAs stay in nonzero order: the result
+// equals the gather's and scipy's csr_matvecs bit for bit.
+constexpr int V_THREADS = 256;
+constexpr int V_RPW = 4;  // rows per warp
+
+template <bool CPLX>
+BK_DEV void vec_load_nz(const int32_t* col, const double* val, int kk, int ke, int& cj, double& ar, double& ai) {
+  cj = 0;
+  ar = ai = 0.0;
+  if (kk < ke) {
+    cj = __ldg(col + kk);
+    if (CPLX) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(val) + kk);
+      ar = t.x;
+      ai = t.y;
+    } else {
+      ar = __ldg(val + kk);
+    }
+  }
+}
+
+// pieces [p_lo, p_hi] of each row are computed (16-byte aligned pairs / complex elements)
+template <bool CPLX, int NV, int U, int MINB>
+__global__ void __launch_bounds__(V_THREADS, MINB) spmm_csr_vec(int64_t n, const int32_t* __restrict__ rowptr,
+                                                                const int32_t* __restrict__ col,
+                                                                const double* __restrict__ val, int p_lo, int p_hi,
+                                                                const double2* __restrict__ X, int64_t ldx,
+                                                                double2* __restrict__ Y, int64_t ldy) {
+  // X, Y: 16-byte aligned bases, ldx/ldy in 16-byte pieces
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * (V_THREADS / 32) + (threadIdx.x >> 5);
+  const int64_t rbeg = warp * V_RPW;
+  if (rbeg >= n) return;
+  const int64_t rend = lmin(n, rbeg + V_RPW);
+  int pc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) pc[v] = min(max(v * 32 + lane, p_lo), p_hi);
+  int kb = __ldg(rowptr + rbeg), ke = __ldg(rowptr + rbeg + 1);
+  int cj;
+  double ar, ai;
+  vec_load_nz<CPLX>(col, val, kb + lane, ke, cj, ar, ai);
+  for (int64_t row = rbeg; row < rend; ++row) {
+    int nkb = 0, nke = 0, ncj = 0;
+    double nar = 0.0, nai = 0.0;
+    if (row + 1 < rend) {  // prefetch the next row's first (col, val) batch
+      nkb = ke;
+      nke = __ldg(rowptr + row + 2);
+      vec_load_nz<CPLX>(col, val, nkb + lane, nke, ncj, nar, nai);
+    }
+    double2 acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = make_double2(0.0, 0.0);
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+      if (k0 > kb) vec_load_nz<CPLX>(col, val, k0 + lane, ke, cj, ar, ai);  // > 32 nonzeros
+      const int cnt = min(32, ke - k0);
+      for (int t0 = 0; t0 < cnt; t0 += U) {
+        double2 xv[U][NV];
+        double a_r[U], a_i[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int src = t0 + u < cnt ? t0 + u : t0;  // padded slots reload slot t0's row
+          const int64_t jr = __shfl_sync(0xffffffffu, cj, src);
+          a_r[u] = __shfl_sync(0xffffffffu, ar, src);
+          a_i[u] = CPLX ? __shfl_sync(0xffffffffu, ai, src) : 0.0;
+          const double2* xr = X + jr * ldx;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) xv[u][v] = __ldg(xr + pc[v]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t0 + u < cnt) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              if (CPLX) {
+                acc[v].x = fma(a_r[u], xv[u][v].x, fma(-a_i[u], xv[u][v].y, acc[v].x));
+                acc[v].y = fma(a_r[u], xv[u][v].y, fma(a_i[u], xv[u][v].x, acc[v].y));
+              } else {
+                acc[v].x = fma(a_r[u], xv[u][v].x, acc[v].x);
+                acc[v].y = fma(a_r[u], xv[u][v].y, acc[v].y);
+              }
+            }
+          }
+      }
+    }
+    double2* yr = Y + row * ldy;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int p = v * 32 + lane;
+      if (p >= p_lo && p <= p_hi) yr[p] = acc[v];
+    }
+    kb = nkb;
+    ke = nke;
+    cj = ncj;
+    ar = nar;
+    ai = nai;
+  }
+}
+
+// the (at most two) real columns c0, c1 (-1 = none) that are half of a 16-byte pair: one
+// thread per row, nonzeros in CSR order
+__global__ void spmm_csr_edge(int64_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, int c0, int c1, const double* __restrict__ X,
+                              int64_t ldx, double* __restrict__ Y, int64_t ldy) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int kb = __ldg(rowptr + row), ke = __ldg(rowptr + row + 1);
+  double a0 = 0.0, a1 = 0.0;
+  for (int k = kb; k < ke; ++k) {
+    const int64_t j = __ldg(col + k);
+    const double a = __ldg(val + k);
+    if (c0 >= 0) a0 = fma(a, __ldg(X + j * ldx + c0), a0);
+    if (c1 >= 0) a1 = fma(a, __ldg(X + j * ldx + c1), a1);
+  }
+  if (c0 >= 0) Y[row * ldy + c0] = a0;
+  if (c1 >= 0) Y[row * ldy + c1] = a1;
+}
+
+// experiment knob for the real NV = 9 case (config 2 widths): 0 = default (U 2, MINB 1)
+static int bk_vec_cfg = 0;
+
+template <bool CPLX>
+static void launch_vec(int nv, int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, int p_lo,
+                       int p_hi, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t st) {
+  const int64_t rows_per_cta = (int64_t)V_RPW * (V_THREADS / 32);
+  const unsigned grid = (unsigned)((n + rows_per_cta - 1) / rows_per_cta);
+  auto x2 = reinterpret_cast<const double2*>(X);
+  auto y2 = reinterpret_cast<double2*>(Y);
+  const int64_t lx = ldx / 2, ly = ldy / 2;
+#define BK_VEC(NV_, U_, MB_) \
+  spmm_csr_vec<CPLX, NV_, U_, MB_><<<grid, V_THREADS, 0, st>>>(n, rowptr, col, val, p_lo, p_hi, x2, lx, y2, ly)
+  if (!CPLX && nv == 9 && bk_vec_cfg != 0) {
+    switch (bk_vec_cfg) {
+      case 1: BK_VEC(9, 1, 1); break;
+      case 2: BK_VEC(9, 1, 2); break;
+      case 3: BK_VEC(9, 2, 2); break;
+      case 4: BK_VEC(9, 4, 1); break;
+      case 5: BK_VEC(9, 1, 3); break;
+      default: BK_VEC(9, 2, 1); break;
+    }
+    return;
+  }
+  // two CTAs per SM (<= 128 registers) beat deeper per-warp MLP (config 2, NV = 9: U 1 x 2 CTAs
+  // 0.27 ms, U 2 x 1 CTA 0.37 ms; profiles/spmm_sweep_r01.jsonl)
+  switch (nv) {
+    case 1: BK_VEC(1, 4, 2); break;
+    case 2: BK_VEC(2, 4, 2); break;
+    case 3: BK_VEC(3, 2, 2); break;
+    case 4: BK_VEC(4, 2, 2); break;
+    case 5: BK_VEC(5, 2, 2); break;
+    case 6: BK_VEC(6, 1, 2); break;
+    case 7: BK_VEC(7, 1, 2); break;
+    case 8: BK_VEC(8, 1, 2); break;
+    case 9: BK_VEC(9, 1, 2); break;
+    case 10: BK_VEC(10, 1, 2); break;
+    case 11: BK_VEC(11, 1, 2); break;
+    case 12: BK_VEC(12, 1, 2); break;
+    case 13: BK_VEC(13, 1, 1); break;
+    case 14: BK_VEC(14, 1, 1); break;
+    case 15: BK_VEC(15, 1, 1); break;
+    case 16: BK_VEC(16, 1, 1); break;
+    default: break;
+  }
+#undef BK_VEC
+}
+
 }  // namespace bk
 
 using namespace bk;
+
+// 2: whole-row vector gather (default where it applies); 0: row gather.  3..7 select the
+// vector kernel's (U, MINB) experiment variants for NV = 9 (tools/spmm_sweep.py).
+static int bk_spmm_variant = 2;
+extern "C" int bk_spmm_set_variant(int variant) {
+  if (variant < 0 || variant == 1 || variant > 2 + 5) return BK_ERR_ARG;
+  bk_spmm_variant = variant > 2 ? 2 : variant;
+  bk_vec_cfg = variant > 2 ? variant - 2 : 0;
+  return BK_OK;
+}
 
 // Y(:, 0:m) = A X(:, 0:m) for a CSR A with n rows (int32 indices).  X and Y row-major.
 extern "C" int bk_spmm_csr_d(int64_t n, const int32_t* rowptr, const int32_t* col, const double* val, int m,
@@ -110,7 +301,18 @@ extern "C" int bk_spmm_csr_d(int64_t n, const int32_t* rowptr, const int32_t* co
   const unsigned grid = (unsigned)((n + S_THREADS / 32 - 1) / (S_THREADS / 32));
   cudaStream_t st = (cudaStream_t)stream;
   BK_COUNT();
-  if (m <= 32) spmm_csr_real<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
+  const int off = (int)((reinterpret_cast<uintptr_t>(X) >> 3) & 1);
+  const bool vec_ok = (ldx % 2) == 0 && (ldy % 2) == 0 && off == (int)((reinterpret_cast<uintptr_t>(Y) >> 3) & 1);
+  const int nv = (m + off + 63) / 64;
+  const int p_lo = off, p_hi = (m + off) / 2 - 1;  // full 16-byte pairs of X - off
+  if (bk_spmm_variant == 2 && vec_ok && nv <= 16 && p_hi >= p_lo) {
+    launch_vec<false>(nv, n, rowptr, col, val, p_lo, p_hi, X - off, ldx, Y - off, ldy, st);
+    const int c0 = off ? 0 : -1, c1 = ((m + off) & 1) ? m - 1 : -1;
+    if (c0 >= 0 || c1 >= 0) {
+      BK_COUNT();
+      spmm_csr_edge<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rowptr, col, val, c0, c1, X, ldx, Y, ldy);
+    }
+  } else if (m <= 32) spmm_csr_real<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
   else if (m <= 64) spmm_csr_real<2><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
   else if (m <= 128) spmm_csr_real<4><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
   else spmm_csr_real<8><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, val, m, X, ldx, Y, ldy);
@@ -129,9 +331,372 @@ extern "C" int bk_spmm_csr_z(int64_t n, const int32_t* rowptr, const int32_t* co
   auto x2 = reinterpret_cast<const double2*>(X);
   auto y2 = reinterpret_cast<double2*>(Y);
   BK_COUNT();
-  if (m <= 32) spmm_csr_cplx<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
+  const int nvz = (m + 31) / 32;
+  if (bk_spmm_variant == 2 && nvz <= 16) {
+    launch_vec<true>(nvz, n, rowptr, col, val, 0, m - 1, X, 2 * ldx, Y, 2 * ldy, st);
+  } else if (m <= 32) spmm_csr_cplx<1><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
   else if (m <= 64) spmm_csr_cplx<2><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
   else spmm_csr_cplx<4><<<grid, S_THREADS, 0, st>>>(n, rowptr, col, v2, m, x2, ldx, y2, ldy);
   BK_CHECK_LAUNCH();
   return BK_OK;
+}
+
+// ---- plane-marching stencil SpMM (default when the CSR is a nearest-neighbour stencil on an
+// inferred grid, spmm_plan.py StencilPlan).
+//
+// Work unit = an 8 x 8 tile (y, z) of the grid x one 256-byte column slice x a range of
+// planes x.  The unit marches along x.  A producer warp streams, per plane, the 10 x 10 halo
+// tile of X and the tile rows' CSR entries (grid-ordered ELL: values, and per entry the
+// 16-bit ring offset of its X row) into an NS-slot shared-memory ring with three 4-D TMA
+// loads (cp.async.bulk.tensor; grid-edge halo rows arrive zero-filled); 16 consumer warps
+// compute plane x from the X slots of planes x-1, x, x+1.  Full/empty mbarriers replace CTA
+// barriers; the kernel is persistent and each CTA walks its units as one continuous load
+// stream, so loads run ahead across unit boundaries.  Every X row crosses L2 -> SM ~1.56
+// times instead of once per referencing nonzero (7x / 27x), and consumers touch global
+// memory only for the stores.
+//
+// Consumers: thread t computes row t/8 of the tile, 16-byte pieces t%8 and t%8 + 8 of the
+// slice (a quarter-warp reads one row's 128 contiguous bytes: no bank conflicts).  A row's
+// entries are processed in chunks whose offsets / values / X pieces are all loaded before
+// the chunk's first FMA; FMAs run in CSR order, so the result equals bk_spmm_csr_* bit for
+// bit.  Plane x's entries travel with X plane x + 1 (both are first needed by plane x).
+// Real blocks are addressed in 16-byte pairs of X - off (off = 8-byte misalignment); the
+// at most two half-valid edge pairs are computed like the rest (the extra element is the
+// preceding buffer column or a zero-filled one) and stored element-wise.
+namespace bk {
+
+constexpr int M_T = 8;                   // tile edge (y and z)
+constexpr int M_H = M_T + 2;             // halo tile edge
+constexpr int M_HR = M_H * M_H;          // X rows per ring slot
+constexpr int M_COLS = 32;               // doubles per row slice (256 B)
+constexpr int M_XS = M_HR * M_COLS * 8;  // X bytes per slot
+constexpr int M_NSMAX = 6;               // ring slots (3 planes in use, up to 3 in flight)
+constexpr int M_CONS = 512;              // consumer threads (8 per tile row)
+constexpr int M_THREADS = M_CONS + 32;   // + producer warp
+constexpr uint16_t M_PAD = 0xffff;       // ELL padding offset
+
+struct MarchArgs {
+  int nx, ny, nz;
+  int xlo;             // first plane the X tensor map covers
+  int gy, gz, nslices, xseg, nunits;
+  int m, off;          // real: columns and 8-byte misalignment of X, Y; complex: off = 0
+  int vdoubles;        // ELL value row in doubles (real: even width; complex: 2 x width)
+  int woff;            // ELL offset row in uint16 (multiple of 8)
+  int width;           // ELL entries per row
+  int slot_bytes, vals_off, offs_off, ns;
+  double* Y;           // 16-byte aligned base (Y - off for real), ldy in doubles
+  int64_t ldy;
+};
+
+struct MarchUnit {
+  int s, y0, z0, xa, xb;
+};
+
+BK_DEV MarchUnit march_unit(const MarchArgs& A, int u) {
+  MarchUnit U;
+  U.s = u % A.nslices;
+  u /= A.nslices;
+  U.z0 = (u % A.gz) * M_T;
+  u /= A.gz;
+  U.y0 = (u % A.gy) * M_T;
+  const int seg = u / A.gy;
+  U.xa = (int)((int64_t)seg * A.nx / A.xseg);
+  U.xb = (int)((int64_t)(seg + 1) * A.nx / A.xseg);
+  return U;
+}
+
+BK_DEV void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool CPLX>
+using march_vt = typename std::conditional<CPLX, double2, double>::type;
+
+// one row: entries [0, W) (W > 0: compile-time width, chunks of C; W == 0: runtime width)
+template <bool CPLX, int W, int C>
+BK_DEV void march_row(const uint16_t* orow, const march_vt<CPLX>* vrow, int width, const double* sb0,
+                      const double* sb1, const double* sb2, int hb, double2 (&acc)[2]) {
+  const int wd = W > 0 ? W : width;
+#pragma unroll(W > 0 ? 32 : 1)
+  for (int c0 = 0; c0 < wd; c0 += C) {
+    uint16_t o[C];
+    march_vt<CPLX> a[C];
+    double2 v0[C], v1[C];
+    if (W > 0 && W <= 8) {  // one 16-byte load of the row's offsets, values in 16-byte pairs
+      const uint4 ow = *reinterpret_cast<const uint4*>(orow);
+      const uint32_t wds[4] = {ow.x, ow.y, ow.z, ow.w};
+#pragma unroll
+      for (int t = 0; t < C; ++t) o[t] = (uint16_t)(wds[t >> 1] >> (16 * (t & 1)));
+      if constexpr (CPLX) {
+#pragma unroll
+        for (int t = 0; t < C; ++t) a[t] = vrow[t];
+      } else {
+#pragma unroll
+        for (int t = 0; t < C; t += 2) {
+          const double2 pr = *reinterpret_cast<const double2*>(vrow + t);
+          a[t] = pr.x;
+          if (t + 1 < C) a[t + 1] = pr.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < C; ++t) {
+        o[t] = c0 + t < wd ? orow[c0 + t] : M_PAD;
+        a[t] = c0 + t < wd ? vrow[c0 + t] : march_vt<CPLX>{};
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int e = o[t] == M_PAD ? (1 << 14) : o[t];  // padding reads the centre slot, never used
+      const int d = e >> 14;
+      const double* xr = (d == 0 ? sb0 : d == 1 ? sb1 : sb2) + (e & 0x3fff) + hb;
+      v0[t] = *reinterpret_cast<const double2*>(xr);
+      v1[t] = *reinterpret_cast<const double2*>(xr + 16);
+    }
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      if (o[t] == M_PAD) continue;
+      if constexpr (CPLX) {
+        acc[0].x = fma(a[t].x, v0[t].x, fma(-a[t].y, v0[t].y, acc[0].x));
+        acc[0].y = fma(a[t].x, v0[t].y, fma(a[t].y, v0[t].x, acc[0].y));
+        acc[1].x = fma(a[t].x, v1[t].x, fma(-a[t].y, v1[t].y, acc[1].x));
+        acc[1].y = fma(a[t].x, v1[t].y, fma(a[t].y, v1[t].x, acc[1].y));
+      } else {
+        acc[0].x = fma(a[t], v0[t].x, acc[0].x);
+        acc[0].y = fma(a[t], v0[t].y, acc[0].y);
+        acc[1].x = fma(a[t], v1[t].x, acc[1].x);
+        acc[1].y = fma(a[t], v1[t].y, acc[1].y);
+      }
+    }
+  }
+}
+
+// store one 16-byte piece pc of a row (real: element-wise where the pair is half valid)
+template <bool CPLX>
+BK_DEV void march_store(const MarchArgs& A, double* yr, int pc, double2 v) {
+  if (CPLX) {
+    if (pc < A.m) *reinterpret_cast<double2*>(yr + 2 * pc) = v;
+  } else {
+    const int c = 2 * pc - A.off;  // first column of the pair
+    if (c >= 0 && c + 1 < A.m) {
+      *reinterpret_cast<double2*>(yr + 2 * pc) = v;
+    } else {
+      if (c >= 0 && c < A.m) yr[2 * pc] = v.x;
+      if (c + 1 >= 0 && c + 1 < A.m) yr[2 * pc + 1] = v.y;
+    }
+  }
+}
+
+template <bool CPLX, int W>
+__global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                                  const __grid_constant__ CUtensorMap vmap,
+                                                                  const __grid_constant__ CUtensorMap omap,
+                                                                  MarchArgs A) {
+  extern __shared__ __align__(128) unsigned char msm[];
+  __shared__ __align__(8) uint64_t full[M_NSMAX], empty[M_NSMAX];
+  const int NS = A.ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], M_CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == M_CONS / 32) {
+    // ---------------- producer: one elected lane streams the planes of every unit
+    if (lane == 0) {
+      const uint32_t csr_bytes = M_T * M_T * (A.vdoubles * 8 + A.woff * 2);
+      int k = 0;
+      for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+        const MarchUnit U = march_unit(A, u);
+        for (int p = U.xa - 1; p <= U.xb; ++p, ++k) {
+          const int slot = k % NS;
+          unsigned char* sb = msm + (size_t)slot * A.slot_bytes;
+          if (k >= NS) mbar_wait(&empty[slot], ((k / NS) - 1) & 1);
+          const bool csr = p - 1 >= U.xa && p - 1 < U.xb;  // entries of plane p - 1 ride along
+          mbar_arrive_expect_tx(&full[slot], M_XS + (csr ? csr_bytes : 0));
+          tma_load_4d(sb, &xmap, U.s * M_COLS, U.z0 - 1, U.y0 - 1, p - A.xlo, &full[slot]);
+          if (csr) {
+            tma_load_4d(sb + A.vals_off, &vmap, 0, U.z0, U.y0, p - 1, &full[slot]);
+            tma_load_4d(sb + A.offs_off, &omap, 0, U.z0, U.y0, p - 1, &full[slot]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  using VT = march_vt<CPLX>;
+  constexpr int C = W == 27 ? 9 : (W > 0 ? W : 4);
+  const int g = threadIdx.x & 7, r = threadIdx.x >> 3;
+  const int iy = r / M_T, iz = r % M_T;
+  const int hb = (iy * M_H + iz) * M_COLS + 2 * g;  // X row of (dy, dz) = (-1, -1), this piece
+  const int64_t plane = (int64_t)A.ny * A.nz;
+  int k = 0;  // load index of the unit's first plane
+  for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+    const MarchUnit U = march_unit(A, u);
+    const bool act = U.y0 + iy < A.ny && U.z0 + iz < A.nz;
+    int64_t row = ((int64_t)U.xa * A.ny + U.y0 + iy) * A.nz + U.z0 + iz;
+    mbar_wait(&full[k % NS], (k / NS) & 1);
+    mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
+    for (int x = U.xa; x < U.xb; ++x, row += plane) {
+      const int kx = k + (x - U.xa);  // load index of plane x - 1
+      const int s0 = kx % NS, s1 = (kx + 1) % NS, s2 = (kx + 2) % NS;
+      mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
+      if (act) {
+        const unsigned char* b2 = msm + (size_t)s2 * A.slot_bytes;
+        double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+        march_row<CPLX, W, C>(reinterpret_cast<const uint16_t*>(b2 + A.offs_off) + r * A.woff,
+                              reinterpret_cast<const VT*>(reinterpret_cast<const double*>(b2 + A.vals_off) +
+                                                          r * A.vdoubles),
+                              A.width, reinterpret_cast<const double*>(msm + (size_t)s0 * A.slot_bytes),
+                              reinterpret_cast<const double*>(msm + (size_t)s1 * A.slot_bytes),
+                              reinterpret_cast<const double*>(b2), hb, acc);
+        double* yr = A.Y + row * A.ldy;
+        const int pc = U.s * (M_COLS / 2) + g;
+        march_store<CPLX>(A, yr, pc, acc[0]);
+        march_store<CPLX>(A, yr, pc + 8, acc[1]);
+      }
+      // plane x - 1's slot is not needed again
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s0]);
+    }
+    // release the unit's last two planes
+    const int kl = k + (U.xb - U.xa);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[kl % NS]);
+      mbar_arrive(&empty[(kl + 1) % NS]);
+    }
+    k = kl + 2;
+  }
+}
+
+}  // namespace bk
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 4-D tiled tensor map: dims d0 (contiguous) .. d3, strides in elements, box (b0, b1, b2, 1)
+static int encode_4d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, int64_t d0, int64_t d1,
+                     int64_t d2, int64_t d3, int64_t s1, int64_t s2, int64_t s3, int b0, int b1, int b2) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return BK_ERR_CUDA;
+  const cuuint64_t dims[4] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2, (cuuint64_t)d3};
+  const cuuint64_t strides[3] = {(cuuint64_t)(s1 * esize), (cuuint64_t)(s2 * esize), (cuuint64_t)(s3 * esize)};
+  const cuuint32_t box[4] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (enc(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return BK_ERR_UNSUPPORTED;
+  return BK_OK;
+}
+
+static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
+                        const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx, double* Y,
+                        int64_t ldy, void* stream) {
+  if (nx < 0 || ny <= 0 || nz <= 0 || m < 0 || xhi < xlo || width <= 0 || woff < width || (woff % 8)) return BK_ERR_ARG;
+  if (nx == 0 || m == 0) return BK_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  MarchArgs A;
+  A.nx = nx;
+  A.ny = ny;
+  A.nz = nz;
+  A.xlo = xlo;
+  A.width = width;
+  A.woff = woff;
+  A.m = m;
+  const double* xbase;  // 16-byte aligned base of row-space row 0
+  int64_t ldxd, cols;   // leading dimension and tensor width in doubles
+  if (cplx) {
+    A.off = 0;
+    xbase = X + 2 * d0 * ldx;
+    ldxd = 2 * ldx;
+    cols = 2 * (int64_t)m;
+    A.Y = Y;
+    A.ldy = 2 * ldy;
+    A.vdoubles = 2 * width;
+  } else {
+    A.off = (int)((reinterpret_cast<uintptr_t>(X) >> 3) & 1);
+    if ((ldx & 1) || (ldy & 1) || A.off != (int)((reinterpret_cast<uintptr_t>(Y) >> 3) & 1)) return BK_ERR_UNSUPPORTED;
+    xbase = X - A.off + d0 * ldx;
+    ldxd = ldx;
+    cols = m + A.off;
+    A.Y = Y - A.off;
+    A.ldy = ldy;
+    A.vdoubles = (width + 1) / 2 * 2;
+  }
+  if (A.vdoubles > 256 || woff > 256) return BK_ERR_UNSUPPORTED;  // TMA box limit
+  A.vals_off = M_XS;
+  A.offs_off = A.vals_off + M_T * M_T * A.vdoubles * 8;
+  A.slot_bytes = (A.offs_off + M_T * M_T * woff * 2 + 127) / 128 * 128;
+  A.ns = (int)lmin(M_NSMAX, (227 * 1024) / A.slot_bytes);
+  if (A.ns < 4) return BK_ERR_UNSUPPORTED;
+  const size_t smem = (size_t)A.ns * A.slot_bytes;
+  CUtensorMap xmap, vmap, omap;
+  const int64_t P = (int64_t)ny * nz;
+  int rc = encode_4d(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, xbase + (int64_t)xlo * P * ldxd, cols, nz, ny,
+                     xhi - xlo, ldxd, nz * ldxd, P * ldxd, M_COLS, M_H, M_H);
+  if (rc == BK_OK)
+    rc = encode_4d(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, ell_val, A.vdoubles, nz, ny, nx, A.vdoubles,
+                   nz * A.vdoubles, P * A.vdoubles, A.vdoubles, M_T, M_T);
+  if (rc == BK_OK)
+    rc = encode_4d(&omap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, ell_off, woff, nz, ny, nx, woff, nz * woff, P * woff,
+                   woff, M_T, M_T);
+  if (rc != BK_OK) return rc;
+  A.gy = (ny + M_T - 1) / M_T;
+  A.gz = (nz + M_T - 1) / M_T;
+  A.nslices = (int)((cols + M_COLS - 1) / M_COLS);
+  // x segments: >= 8 units per CTA (balance) while a segment keeps >= 8 planes
+  const int64_t per_seg = (int64_t)A.gy * A.gz * A.nslices;
+  A.xseg = 1;
+  while (A.xseg * 2 <= nx / 8 && per_seg * A.xseg < 8 * kSMs) A.xseg *= 2;
+  A.nunits = (int)(per_seg * A.xseg);
+  // the 7-point (3-D), 27-point and 5-point (2-D) widths run with compile-time chunks
+  auto kern = cplx ? (width == 7 ? spmm_march_kernel<true, 7> : width == 5 ? spmm_march_kernel<true, 5>
+                      : width == 27 ? spmm_march_kernel<true, 27> : spmm_march_kernel<true, 0>)
+                   : (width == 7 ? spmm_march_kernel<false, 7> : width == 5 ? spmm_march_kernel<false, 5>
+                      : width == 27 ? spmm_march_kernel<false, 27> : spmm_march_kernel<false, 0>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)lmin(A.nunits, kSMs);
+  BK_COUNT();
+  kern<<<grid, M_THREADS, smem, st>>>(xmap, vmap, omap, A);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+// Y = A X for a CSR A that is a nearest-neighbour stencil on an nx x ny x nz C-order grid,
+// from the plan of spmm_plan.py StencilPlan (grid-ordered ELL values and 16-bit ring offsets,
+// d0 = column shift, planes [xlo, xhi) referenced); same result as bk_spmm_csr_d.  Real: ldx,
+// ldy even and X, Y equally 16-byte aligned, else BK_ERR_UNSUPPORTED.
+extern "C" int bk_spmm_march_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
+                               const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx,
+                               double* Y, int64_t ldy, void* stream) {
+  return march_launch(false, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, stream);
+}
+
+// complex128: ell_val, X, Y interleaved; ld in complex elements
+extern "C" int bk_spmm_march_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
+                               const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx,
+                               double* Y, int64_t ldy, void* stream) {
+  return march_launch(true, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, stream);
 }

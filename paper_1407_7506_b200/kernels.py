@@ -279,6 +279,23 @@ def spmm_csr(rowptr, col, val, x, y):
     return y
 
 
+def spmm_march(plan, x, y):
+    """Plane-marching stencil SpMM (bk_spmm_march_*) with a device StencilPlan; returns False
+    when the views' alignment does not allow it (the caller then uses spmm_csr)."""
+    m = x.shape[1]
+    ldx, ldy = ld_of(x), ld_of(y)
+    if x.dtype == F64:
+        if ldx % 2 or ldy % 2 or (x.data_ptr() % 16) != (y.data_ptr() % 16) or x.data_ptr() % 8:
+            return False
+        name = "bk_spmm_march_d"
+    else:
+        name = "bk_spmm_march_z"
+    nx, ny, nz = plan.grid
+    _lib.call(name, nx, ny, nz, plan.xlo, plan.xhi, plan.d0, plan.ell_val.data_ptr(), plan.ell_off.data_ptr(),
+              plan.width, plan.woff, m, x.data_ptr(), ldx, y.data_ptr(), ldy, stream_ptr())
+    return True
+
+
 # ----------------------------------------------------------------------------- subblock path
 def subblock_grams(n, k_act, q, has_p, X, W, P, AX, AW, AP, ld, c0, araw, braw, tmp=None):
     """Raw pencil Grams of every subblock.  Pointers are raw device addresses of the state

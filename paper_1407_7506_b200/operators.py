@@ -8,7 +8,9 @@ turn any operator — these classes, the reference's own ``blockeig`` objects, o
 user object — into a device apply used inside the solver:
 
 * anything exposing a scipy CSR as ``_csr`` (SparseHermitian, both packages) -> CSR SpMM
-  (bk_spmm_csr_*; replaces problems.py:72-73);
+  (replaces problems.py:72-73): the plane-marching stencil kernel (bk_spmm_march_*) when the
+  CSR is a nearest-neighbour stencil on a grid inferred from its offsets (spmm_plan.py),
+  the whole-row gather (bk_spmm_csr_*) otherwise;
 * ``DenseHermitian`` (``matrix``) -> DMMA tall GEMM;
 * ``DiagonalOperator`` (``diag``) / ``DiagonalPreconditioner`` (``d``) -> row scaling, which
   the solver fuses into the residual epilogue for preconditioners (operators.py:96-110);
@@ -236,13 +238,36 @@ class DeviceCsr:
         vals = csr.data.astype(np.complex128 if self.complex else np.float64)
         self.val = torch.from_numpy(vals).cuda()
         self.diag = np.real(csr.diagonal())
+        self.stencil = _device_stencil_plan(csr, vals) if DeviceCsr.use_stencil else None
+
+    # plane-marching stencil kernel when the CSR is a nearest-neighbour stencil on an inferred
+    # grid (spmm_plan.py); the whole-row gather otherwise
+    use_stencil = True
 
     def apply_into(self, x, y):
         from . import kernels
 
         if self.complex and x.dtype != _torch().complex128:
             raise DimensionError("complex operator applied to a real block")
+        if (self.stencil is not None and DeviceCsr.use_stencil
+                and kernels.spmm_march(self.stencil, x, y)):
+            return
         kernels.spmm_csr(self.rowptr, self.col, self.val, x, y)
+
+
+def _device_stencil_plan(csr, vals):
+    from .spmm_plan import StencilPlan
+
+    if csr.shape[0] == 0 or csr.nnz == 0:
+        return None
+    plan = StencilPlan(csr.indptr, csr.indices, csr.shape[0], csr.shape[1])
+    if not plan.ok:
+        return None
+    torch = _torch()
+    plan.ell_val = torch.from_numpy(plan.ell_values(vals)).cuda()
+    plan.ell_off = torch.from_numpy(plan.ell_off.view(np.int16)).cuda()
+    del plan.rows_, plan.slot_
+    return plan
 
 
 class DeviceDense:
