@@ -238,7 +238,8 @@ class DeviceCsr:
         vals = csr.data.astype(np.complex128 if self.complex else np.float64)
         self.val = torch.from_numpy(vals).cuda()
         self.diag = np.real(csr.diagonal())
-        self.stencil = _device_stencil_plan(csr, vals) if DeviceCsr.use_stencil else None
+        self.ncols = csr.shape[1]
+        self.stencil = _device_stencil_plan(self) if DeviceCsr.use_stencil else None
 
     # plane-marching stencil kernel when the CSR is a nearest-neighbour stencil on an inferred
     # grid (spmm_plan.py); the whole-row gather otherwise
@@ -255,18 +256,17 @@ class DeviceCsr:
         kernels.spmm_csr(self.rowptr, self.col, self.val, x, y)
 
 
-def _device_stencil_plan(csr, vals):
+def _device_stencil_plan(dc):
+    """StencilPlan built on the GPU from the already uploaded CSR (spmm_plan.py)."""
     from .spmm_plan import StencilPlan
 
-    if csr.shape[0] == 0 or csr.nnz == 0:
+    if dc.n == 0 or dc.nnz == 0:
         return None
-    plan = StencilPlan(csr.indptr, csr.indices, csr.shape[0], csr.shape[1])
+    plan = StencilPlan(dc.rowptr, dc.col, dc.n, dc.ncols)
     if not plan.ok:
         return None
-    torch = _torch()
-    plan.ell_val = torch.from_numpy(plan.ell_values(vals)).cuda()
-    plan.ell_off = torch.from_numpy(plan.ell_off.view(np.int16)).cuda()
-    del plan.rows_, plan.slot_
+    plan.ell_val = plan.ell_values(dc.val)
+    plan.release_host_index()
     return plan
 
 

@@ -32,21 +32,29 @@ TY = TZ = 8         # grid tile per CTA (the kernel's compile-time tile)
 SLICE_DOUBLES = 32  # doubles per staged X row slice (the kernel's M_COLS)
 
 
+def _torch():
+    import torch
+
+    return torch
+
+
 def _row_ids(indptr):
+    torch = _torch()
     n = indptr.shape[0] - 1
-    return np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr).astype(np.int64))
+    return torch.repeat_interleave(torch.arange(n, dtype=torch.int64, device=indptr.device), indptr[1:] - indptr[:-1])
 
 
 def infer_grid(indptr, indices, n):
     """((nx, ny, nz), d0) such that every offset col - row - d0 lies in the 27-point stencil
-    set of an nx x ny x nz C-order grid, or None."""
+    set of an nx x ny x nz C-order grid, or None.  indptr / indices: int64 torch tensors."""
+    torch = _torch()
     if n == 0 or indices.shape[0] == 0:
         return None
-    rows = _row_ids(indptr)
-    off = indices.astype(np.int64) - rows
-    vals, counts = np.unique(off, return_counts=True)
+    off = indices - _row_ids(indptr)
+    vals, counts = torch.unique(off, return_counts=True)
     if vals.shape[0] > 27:
         return None
+    vals, counts = vals.cpu().numpy(), counts.cpu().numpy()
     # the diagonal's shift d0: the most frequent offsets first (ties: the one nearest the
     # middle of the offset range, e.g. interior slabs where +-P are as frequent as 0)
     mid = int(vals.min()) + int(vals.max())
@@ -83,16 +91,21 @@ def _grid_for(o, n):
 
 
 class StencilPlan:
-    """Host side of the march SpMM: grid (nx, ny, nz), shift d0, planes [xlo, xhi) the
-    columns reach, and the grid-ordered ELL arrays: ``ell_off`` (n x woff uint16, the ring
-    offset of each entry's X row, 0xffff = padding) and ``ell_values(data)``.  ``ok`` is False when the
-    CSR is not a nearest-neighbour stencil on an inferred grid."""
+    """The march SpMM's plan: grid (nx, ny, nz), shift d0, planes [xlo, xhi) the columns
+    reach, and the grid-ordered ELL arrays ``ell_off`` (n x woff int16 holding uint16 bit
+    patterns: the ring offset of each entry's X row, 0xffff = padding) and
+    ``ell_values(data)``, as torch tensors on ``indptr``'s device (built on the GPU in
+    production: a few elementwise passes over the nonzeros).  ``ok`` is False when the CSR is
+    not a nearest-neighbour stencil on an inferred grid."""
 
-    def __init__(self, indptr, indices, n, ncols=None):
+    def __init__(self, indptr, indices, n, ncols=None, device=None):
+        torch = _torch()
         self.ok = False
         ncols = n if ncols is None else ncols
-        indptr = np.asarray(indptr, dtype=np.int64)
-        indices = np.asarray(indices, dtype=np.int64)
+        indptr = torch.as_tensor(np.asarray(indptr) if not torch.is_tensor(indptr) else indptr,
+                                 device=device).to(torch.int64)
+        indices = torch.as_tensor(np.asarray(indices) if not torch.is_tensor(indices) else indices,
+                                  device=indptr.device).to(torch.int64)
         g = infer_grid(indptr, indices, n)
         if g is None:
             return
@@ -100,17 +113,17 @@ class StencilPlan:
         rows = _row_ids(indptr)
         c = indices - d0
         P = ny * nz
-        rx, ry, rz = rows // P, (rows // nz) % ny, rows % nz
-        cx = np.floor_divide(c, P)
+        cx = torch.div(c, P, rounding_mode="floor")
         rem = c - cx * P
-        cy, cz = rem // nz, rem % nz
-        dx, dy, dz = cx - rx, cy - ry, cz - rz
-        if indices.shape[0] and (np.abs(dx).max() > 1 or np.abs(dy).max() > 1 or np.abs(dz).max() > 1):
+        dx = cx - torch.div(rows, P, rounding_mode="floor")
+        dy = torch.div(rem, nz, rounding_mode="floor") - torch.div(rows, nz, rounding_mode="floor") % ny
+        dz = rem % nz - rows % nz
+        amax = torch.stack([dx.abs().max(), dy.abs().max(), dz.abs().max(), cx.min(), cx.max()]).cpu().tolist()
+        if max(amax[:3]) > 1:
             return
         # planes the column indices reach (ghost planes of a row partition: -1 and nx); the
         # kernel stages whole planes [xlo, xhi) of X rows d0 + p*P .., which must exist
-        xlo = int(cx.min()) if indices.shape[0] else 0
-        xhi = int(cx.max()) + 1 if indices.shape[0] else nx
+        xlo, xhi = int(amax[3]), int(amax[4]) + 1
         if d0 % P or d0 + xlo * P < 0 or d0 + xhi * P > ncols:
             return
         self.grid = (int(nx), int(ny), int(nz))
@@ -119,24 +132,32 @@ class StencilPlan:
         # grid-ordered ELL (row r's entries in CSR order, then padding 0xffff): the kernel stages
         # a plane tile's entries with one TMA load, like the X tile.  Per entry the kernel's
         # ring offset of its X row: (dx+1) << 14 | ((dy+1)*(TY+2) + dz+1) * SLICE_DOUBLES
-        offs = (((dx + 1) << 14) | (((dy + 1) * (TY + 2) + (dz + 1)) * SLICE_DOUBLES)).astype(np.uint16)
-        cnt = np.diff(indptr)
-        w = int(cnt.max(initial=1))
+        offs = ((dx + 1) << 14) | (((dy + 1) * (TY + 2) + (dz + 1)) * SLICE_DOUBLES)
+        cnt = indptr[1:] - indptr[:-1]
+        w = max(int(cnt.max().item()), 1)
         self.width = w
         self.woff = -(-w // 8) * 8                         # 16-byte rows of uint16
-        slot = np.arange(indices.shape[0], dtype=np.int64) - indptr[rows]
-        ell_off = np.full((n, self.woff), 0xFFFF, dtype=np.uint16)
-        ell_off[rows, slot] = offs
+        slot = torch.arange(indices.shape[0], dtype=torch.int64, device=indptr.device) - indptr[rows]
+        ell_off = torch.full((n, self.woff), -1, dtype=torch.int16, device=indptr.device)
+        ell_off[rows, slot] = offs.to(torch.int32).to(torch.int16)  # uint16 bit patterns
         self.ell_off = ell_off
-        self.rows_, self.slot_ = rows, slot
+        self._rows, self._slot = rows, slot
         self.ok = True
 
     def ell_values(self, data):
-        """Values in the grid-ordered ELL layout: real rows padded to an even width (16-byte
-        rows), complex rows of ``width`` elements; padding is zero (never read)."""
-        if np.iscomplexobj(data):
-            out = np.zeros((self.ell_off.shape[0], self.width), dtype=np.complex128)
+        """Values (torch tensor or numpy, on any device) in the grid-ordered ELL layout: real
+        rows padded to an even width (16-byte rows), complex rows of ``width`` elements;
+        padding is zero (never read)."""
+        torch = _torch()
+        data = torch.as_tensor(data).to(self.ell_off.device)
+        if data.is_complex():
+            out = torch.zeros((self.ell_off.shape[0], self.width), dtype=torch.complex128, device=data.device)
         else:
-            out = np.zeros((self.ell_off.shape[0], -(-self.width // 2) * 2), dtype=np.float64)
-        out[self.rows_, self.slot_] = data
+            out = torch.zeros((self.ell_off.shape[0], -(-self.width // 2) * 2), dtype=torch.float64,
+                              device=data.device)
+        out[self._rows, self._slot] = data.to(out.dtype)
         return out
+
+    def release_host_index(self):
+        """Drop the per-nonzero scatter indices once the values are laid out."""
+        del self._rows, self._slot

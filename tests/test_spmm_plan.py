@@ -15,12 +15,13 @@ def replay(csr, plan, x):
     """Y = A X through the plan: each ELL entry's offset decoded to (dx, dy, dz) exactly as
     the kernel maps it to a ring slot / halo row, values in ELL order."""
     nx, ny, nz = plan.grid
-    vals = plan.ell_values(csr.data)
+    vals = plan.ell_values(csr.data).numpy()
+    offs = plan.ell_off.numpy().view(np.uint16)
     y = np.zeros((csr.shape[0], x.shape[1]), dtype=np.result_type(vals, x))
     for r in range(csr.shape[0]):
         ix, iy, iz = r // (ny * nz), (r // nz) % ny, r % nz
         for t in range(plan.width):
-            o = int(plan.ell_off[r, t])
+            o = int(offs[r, t])
             if o == 0xFFFF:
                 break
             dx = (o >> 14) - 1

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_spmm_gpu.py -q -x 2>&1 | tail -15 > gpurun_out/tests_spmm_new.log
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -5 > gpurun_out/tests_spmm.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python tools/e2e_profile.py 2 20 > gpurun_out/e2e_profile.log 2>&1
