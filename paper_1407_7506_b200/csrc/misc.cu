@@ -62,18 +62,22 @@ __global__ void k_small_stats(int m1, int m2, const double* C, int64_t ldc, int 
   __shared__ double r0[32], r1[32], r2[32];
   double s = 0.0, si = 0.0, tr = 0.0;
   const int w = cplx ? 2 : 1;
-  for (int64_t e = threadIdx.x; e < (int64_t)m1 * m2; e += blockDim.x) {
-    const int i = (int)(e / m2), j = (int)(e % m2);
-    const double* p = C + (i * ldc + j) * w;
-    double a2 = p[0] * p[0];
-    if (cplx) a2 += p[1] * p[1];
-    s += a2;
-    if (i == j) {
-      const double dr = p[0] - 1.0;
-      si += dr * dr + (cplx ? p[1] * p[1] : 0.0);
-      tr += p[0];
-    } else {
-      si += a2;
+  // warps own rows, lanes columns (coalesced, no index division)
+  const int nw = blockDim.x >> 5, wq = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i = wq; i < m1; i += nw) {
+    const double* rowp = C + (int64_t)i * ldc * w;
+    for (int j = ln; j < m2; j += 32) {
+      const double* p = rowp + (int64_t)j * w;
+      double a2 = p[0] * p[0];
+      if (cplx) a2 += p[1] * p[1];
+      s += a2;
+      if (i == j) {
+        const double dr = p[0] - 1.0;
+        si += dr * dr + (cplx ? p[1] * p[1] : 0.0);
+        tr += p[0];
+      } else {
+        si += a2;
+      }
     }
   }
   s = warp_sum(s);

@@ -32,13 +32,30 @@ __all__ = ["partition_rows", "HaloPlan", "local_rows_csr", "Comm", "TorchComm", 
            "thread_comms", "host_csr_of", "dist_ppcg_solve"]
 
 
-def partition_rows(n, size, rowptr=None):
+def partition_rows(n, size, rowptr=None, plane=None):
     """Contiguous row slabs [lo, hi) for ``size`` ranks.  With CSR row pointers the cuts
-    balance nonzeros (SpMM work), otherwise rows; every slab is non-empty when n >= size."""
+    balance nonzeros (SpMM work), otherwise rows; every slab is non-empty when n >= size.
+    ``plane``: rows per grid plane of a stencil operator (spmm_plan.infer_grid); when the grid
+    has at least ``size`` planes the cuts fall on plane boundaries, so every rank's local CSR
+    is again a whole-plane stencil for the plane-marching SpMM and its halo is one plane."""
     if size < 1:
         raise ValueError("size must be >= 1")
     if n < size:
         raise ValueError(f"cannot split {n} rows over {size} ranks")
+    if plane is not None and plane > 0 and n % plane == 0 and n // plane >= size:
+        npl = n // plane
+        if rowptr is None:
+            pc = [(npl * r) // size for r in range(size + 1)]
+        else:
+            rp = np.asarray(rowptr, dtype=np.int64)
+            work = (rp + np.arange(n + 1, dtype=np.int64))[::plane]  # work at plane boundaries
+            tot = int(work[-1])
+            pc = [0]
+            for r in range(1, size):
+                c = int(np.searchsorted(work, (tot * r) // size, side="left"))
+                pc.append(min(max(c, pc[-1] + 1), npl - (size - r)))
+            pc.append(npl)
+        return [(pc[r] * plane, pc[r + 1] * plane) for r in range(size)]
     if rowptr is None:
         cuts = [(n * r) // size for r in range(size + 1)]
     else:

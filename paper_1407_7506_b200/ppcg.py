@@ -206,7 +206,7 @@ class PPCGSolver:
             from .operators import DeviceCsr
 
             csr = host_csr_of(a)
-            self.bounds = partition_rows(self.n, self.comm.size, csr.indptr)
+            self.bounds = partition_rows(self.n, self.comm.size, csr.indptr, plane=_stencil_plane(csr))
             self.plan = p = HaloPlan(csr, self.bounds, self.comm.rank)
             self.dev_a = DeviceCsr(local_rows_csr(csr, p.lo, p.hi, p.g_lo, p.n_ext))
             self.prec = as_device_preconditioner(t)
@@ -925,6 +925,17 @@ class PPCGSolver:
                            diagnostics={"orth_loss": self.orth_loss, "proj_defect": self.proj_defect,
                                         "final_residual_norms": rn, "cache_refreshes": self.refreshes,
                                         "trace_increases": inc})
+
+
+def _stencil_plane(csr):
+    """Rows per grid plane when the CSR is a nearest-neighbour stencil (spmm_plan.infer_grid)."""
+    import torch
+
+    from .spmm_plan import infer_grid
+
+    g = infer_grid(torch.from_numpy(csr.indptr.astype(np.int64)), torch.from_numpy(csr.indices.astype(np.int64)),
+                   csr.shape[0])
+    return None if g is None else g[0][1] * g[0][2]
 
 
 def ppcg_solve(a, t=None, x0=None, opts=None, threads=1):

@@ -129,3 +129,37 @@ def test_torchcomm_gloo_world2():
         assert res["zsum"] == [2 + 4j, 1 - 2j]
         assert res["max"] == [1, 10, 0]
         assert res["spmm_err"] <= 1e-12 and res["gather_err"] <= 1e-12
+
+
+def test_partition_rows_plane_aligned_for_stencils():
+    """Stencil operators are cut at grid-plane boundaries (ppcg.py uses the plane inferred
+    from the CSR), so each rank's ghost-extended local CSR is again a whole-plane stencil the
+    plane-marching SpMM can run (spmm_plan.StencilPlan), with one ghost plane per side."""
+    from paper_1407_7506_b200 import config_problem
+    from paper_1407_7506_b200.ppcg import _stencil_plane
+    from paper_1407_7506_b200.spmm_plan import StencilPlan
+    from test_spmm_plan import replay
+
+    for cfg, N in ((2, 10), (4, 7), (5, 9)):
+        csr = config_problem(cfg, N=N)[0]._csr
+        n, P = csr.shape[0], _stencil_plane(csr)
+        assert P == N * N
+        for size in (2, 3, 4):
+            bounds = partition_rows(n, size, csr.indptr, plane=P)
+            assert bounds[0][0] == 0 and bounds[-1][1] == n
+            assert all(lo % P == 0 and hi % P == 0 and lo < hi for lo, hi in bounds)
+            for r in range(size):
+                hp = HaloPlan(csr, bounds, r)
+                loc = local_rows_csr(csr, hp.lo, hp.hi, hp.g_lo, hp.n_ext)
+                sp_ = StencilPlan(loc.indptr, loc.indices, loc.shape[0], loc.shape[1])
+                assert sp_.ok and sp_.grid[1:] == (N, N)
+                # (a one-plane slab may be read as shifted by a plane: an equally exact decoding)
+                x = np.random.default_rng(r).standard_normal((hp.n_ext, 2))
+                if np.iscomplexobj(loc.data):
+                    x = x + 1j * np.random.default_rng(r + 9).standard_normal((hp.n_ext, 2))
+                np.testing.assert_allclose(replay(loc, sp_, x), loc @ x, rtol=0, atol=1e-12)
+    # fewer planes than ranks: ordinary row cuts
+    csr = config_problem(2, N=3)[0]._csr
+    b = partition_rows(27, 4, csr.indptr, plane=9)
+    assert len(b) == 4 and b[-1][1] == 27 and not all(lo % 9 == 0 for lo, _ in b)
+    assert _stencil_plane(config_problem(1, N=8)[0]._csr) == 64  # 2-D: one plane
