@@ -40,16 +40,16 @@ int bk_spmm_set_variant(int variant);
  * nearest-neighbour stencil on an nx x ny x nz C-order grid, with the plan of
  * paper_1407_7506_b200/spmm_plan.py: the CSR entries re-laid out as a grid-ordered ELL
  * (ell_val: n x width values, real rows padded to an even width; ell_off: n x woff uint16,
- * woff a multiple of 8, per entry (dx+1) << 14 | ((dy+1)*10 + dz+1) * 32, 0xffff = padding),
+ * woff a multiple of 8, per entry (dx+1) << 14 | (dy+1)*10 + dz+1, 0xffff = padding),
  * d0 = column shift of a ghost-extended local CSR, planes [xlo, xhi) referenced.  X tiles and
  * entries are staged in shared memory by TMA and reused across the stencil.  Real: ldx, ldy
  * even and X, Y equally 16-byte aligned, else BK_ERR_UNSUPPORTED (use bk_spmm_csr_d). */
 int bk_spmm_march_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                     const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx, double* Y,
-                    int64_t ldy, void* stream);
+                    int64_t ldy, int row_align, void* stream);
 int bk_spmm_march_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                     const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx, double* Y,
-                    int64_t ldy, void* stream);
+                    int64_t ldy, int row_align, void* stream);
 
 /* ---- diagonal apply: DiagonalPreconditioner.apply operators.py:110, DiagonalOperator
  *      operators.py:68-69 (real d; complex blocks as real views with 2m columns) */

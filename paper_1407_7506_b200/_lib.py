@@ -33,9 +33,9 @@ _SIGS = {
     "bk_spmm_csr_z": (c_int, [c_i64, vp, vp, vp, c_int, vp, c_i64, vp, c_i64, vp]),
     "bk_spmm_set_variant": (c_int, [c_int]),
     "bk_spmm_march_d": (c_int, [c_int, c_int, c_int, c_int, c_int, c_i64, vp, vp, c_int, c_int, c_int, vp, c_i64,
-                                vp, c_i64, vp]),
+                                vp, c_i64, c_int, vp]),
     "bk_spmm_march_z": (c_int, [c_int, c_int, c_int, c_int, c_int, c_i64, vp, vp, c_int, c_int, c_int, vp, c_i64,
-                                vp, c_i64, vp]),
+                                vp, c_i64, c_int, vp]),
     "bk_scale_rows_d": (c_int, [c_i64, c_int, vp, vp, c_i64, vp, c_i64, vp]),
     "bk_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int]),
     "bk_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),

@@ -368,8 +368,8 @@ namespace bk {
 constexpr int M_T = 8;                   // tile edge (y and z)
 constexpr int M_H = M_T + 2;             // halo tile edge
 constexpr int M_HR = M_H * M_H;          // X rows per ring slot
-constexpr int M_COLS = 32;               // doubles per row slice (256 B)
-constexpr int M_XS = M_HR * M_COLS * 8;  // X bytes per slot
+// doubles per staged row slice: 64 (512 B) for real rows of <= 8 entries, else 32 (the ring
+// must still hold 4 slots of X + ELL in 227 KB); pieces per consumer thread and row = COLS / 16
 constexpr int M_NSMAX = 6;               // ring slots (3 planes in use, up to 3 in flight)
 constexpr int M_CONS = 512;              // consumer threads (8 per tile row)
 constexpr int M_THREADS = M_CONS + 32;   // + producer warp
@@ -416,16 +416,18 @@ BK_DEV void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c
 template <bool CPLX>
 using march_vt = typename std::conditional<CPLX, double2, double>::type;
 
-// one row: entries [0, W) (W > 0: compile-time width, chunks of C; W == 0: runtime width)
-template <bool CPLX, int W, int C>
+// one row: entries [0, W) (W > 0: compile-time width, chunks of C; W == 0: runtime width);
+// this thread's pieces g + 8 k (k < COLS / 16) of the slice
+template <bool CPLX, int W, int C, int COLS>
 BK_DEV void march_row(const uint16_t* orow, const march_vt<CPLX>* vrow, int width, const double* sb0,
-                      const double* sb1, const double* sb2, int hb, double2 (&acc)[2]) {
+                      const double* sb1, const double* sb2, int hb, double2 (&acc)[COLS / 16]) {
+  constexpr int M_NP = COLS / 16;
   const int wd = W > 0 ? W : width;
 #pragma unroll(W > 0 ? 32 : 1)
   for (int c0 = 0; c0 < wd; c0 += C) {
     uint16_t o[C];
     march_vt<CPLX> a[C];
-    double2 v0[C], v1[C];
+    double2 v[C][M_NP];
     if (W > 0 && W <= 8) {  // one 16-byte load of the row's offsets, values in 16-byte pairs
       const uint4 ow = *reinterpret_cast<const uint4*>(orow);
       const uint32_t wds[4] = {ow.x, ow.y, ow.z, ow.w};
@@ -453,23 +455,22 @@ BK_DEV void march_row(const uint16_t* orow, const march_vt<CPLX>* vrow, int widt
     for (int t = 0; t < C; ++t) {
       const int e = o[t] == M_PAD ? (1 << 14) : o[t];  // padding reads the centre slot, never used
       const int d = e >> 14;
-      const double* xr = (d == 0 ? sb0 : d == 1 ? sb1 : sb2) + (e & 0x3fff) + hb;
-      v0[t] = *reinterpret_cast<const double2*>(xr);
-      v1[t] = *reinterpret_cast<const double2*>(xr + 16);
+      const double* xr = (d == 0 ? sb0 : d == 1 ? sb1 : sb2) + (e & 0x3fff) * COLS + hb;
+#pragma unroll
+      for (int k = 0; k < M_NP; ++k) v[t][k] = *reinterpret_cast<const double2*>(xr + 16 * k);
     }
 #pragma unroll
     for (int t = 0; t < C; ++t) {
       if (o[t] == M_PAD) continue;
-      if constexpr (CPLX) {
-        acc[0].x = fma(a[t].x, v0[t].x, fma(-a[t].y, v0[t].y, acc[0].x));
-        acc[0].y = fma(a[t].x, v0[t].y, fma(a[t].y, v0[t].x, acc[0].y));
-        acc[1].x = fma(a[t].x, v1[t].x, fma(-a[t].y, v1[t].y, acc[1].x));
-        acc[1].y = fma(a[t].x, v1[t].y, fma(a[t].y, v1[t].x, acc[1].y));
-      } else {
-        acc[0].x = fma(a[t], v0[t].x, acc[0].x);
-        acc[0].y = fma(a[t], v0[t].y, acc[0].y);
-        acc[1].x = fma(a[t], v1[t].x, acc[1].x);
-        acc[1].y = fma(a[t], v1[t].y, acc[1].y);
+#pragma unroll
+      for (int k = 0; k < M_NP; ++k) {
+        if constexpr (CPLX) {
+          acc[k].x = fma(a[t].x, v[t][k].x, fma(-a[t].y, v[t][k].y, acc[k].x));
+          acc[k].y = fma(a[t].x, v[t][k].y, fma(a[t].y, v[t][k].x, acc[k].y));
+        } else {
+          acc[k].x = fma(a[t], v[t][k].x, acc[k].x);
+          acc[k].y = fma(a[t], v[t][k].y, acc[k].y);
+        }
       }
     }
   }
@@ -491,7 +492,7 @@ BK_DEV void march_store(const MarchArgs& A, double* yr, int pc, double2 v) {
   }
 }
 
-template <bool CPLX, int W>
+template <bool CPLX, int W, int COLS>
 __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                   const __grid_constant__ CUtensorMap vmap,
                                                                   const __grid_constant__ CUtensorMap omap,
@@ -520,8 +521,8 @@ __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_c
           unsigned char* sb = msm + (size_t)slot * A.slot_bytes;
           if (k >= NS) mbar_wait(&empty[slot], ((k / NS) - 1) & 1);
           const bool csr = p - 1 >= U.xa && p - 1 < U.xb;  // entries of plane p - 1 ride along
-          mbar_arrive_expect_tx(&full[slot], M_XS + (csr ? csr_bytes : 0));
-          tma_load_4d(sb, &xmap, U.s * M_COLS, U.z0 - 1, U.y0 - 1, p - A.xlo, &full[slot]);
+          mbar_arrive_expect_tx(&full[slot], M_HR * COLS * 8 + (csr ? csr_bytes : 0));
+          tma_load_4d(sb, &xmap, U.s * COLS, U.z0 - 1, U.y0 - 1, p - A.xlo, &full[slot]);
           if (csr) {
             tma_load_4d(sb + A.vals_off, &vmap, 0, U.z0, U.y0, p - 1, &full[slot]);
             tma_load_4d(sb + A.offs_off, &omap, 0, U.z0, U.y0, p - 1, &full[slot]);
@@ -533,10 +534,11 @@ __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_c
   }
   // ---------------- consumers
   using VT = march_vt<CPLX>;
-  constexpr int C = W == 27 ? 9 : (W > 0 ? W : 4);
+  constexpr int M_NP = COLS / 16;
+  constexpr int C = W == 27 ? (M_NP > 2 ? 5 : 9) : (W > 0 ? W : 4);
   const int g = threadIdx.x & 7, r = threadIdx.x >> 3;
   const int iy = r / M_T, iz = r % M_T;
-  const int hb = (iy * M_H + iz) * M_COLS + 2 * g;  // X row of (dy, dz) = (-1, -1), this piece
+  const int hb = (iy * M_H + iz) * COLS + 2 * g;  // X row of (dy, dz) = (-1, -1), this piece
   const int64_t plane = (int64_t)A.ny * A.nz;
   int k = 0;  // load index of the unit's first plane
   for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
@@ -551,17 +553,19 @@ __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_c
       mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
       if (act) {
         const unsigned char* b2 = msm + (size_t)s2 * A.slot_bytes;
-        double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-        march_row<CPLX, W, C>(reinterpret_cast<const uint16_t*>(b2 + A.offs_off) + r * A.woff,
+        double2 acc[M_NP];
+#pragma unroll
+        for (int k2 = 0; k2 < M_NP; ++k2) acc[k2] = make_double2(0.0, 0.0);
+        march_row<CPLX, W, C, COLS>(reinterpret_cast<const uint16_t*>(b2 + A.offs_off) + r * A.woff,
                               reinterpret_cast<const VT*>(reinterpret_cast<const double*>(b2 + A.vals_off) +
                                                           r * A.vdoubles),
                               A.width, reinterpret_cast<const double*>(msm + (size_t)s0 * A.slot_bytes),
                               reinterpret_cast<const double*>(msm + (size_t)s1 * A.slot_bytes),
                               reinterpret_cast<const double*>(b2), hb, acc);
         double* yr = A.Y + row * A.ldy;
-        const int pc = U.s * (M_COLS / 2) + g;
-        march_store<CPLX>(A, yr, pc, acc[0]);
-        march_store<CPLX>(A, yr, pc + 8, acc[1]);
+        const int pc = U.s * (COLS / 2) + g;
+#pragma unroll
+        for (int k2 = 0; k2 < M_NP; ++k2) march_store<CPLX>(A, yr, pc + 8 * k2, acc[k2]);
       }
       // plane x - 1's slot is not needed again
       __syncwarp();
@@ -613,7 +617,7 @@ static int encode_4d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const 
 
 static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                         const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx, double* Y,
-                        int64_t ldy, void* stream) {
+                        int64_t ldy, int row_align, void* stream) {
   if (nx < 0 || ny <= 0 || nz <= 0 || m < 0 || xhi < xlo || width <= 0 || woff < width || (woff % 8)) return BK_ERR_ARG;
   if (nx == 0 || m == 0) return BK_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -638,6 +642,11 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   } else {
     A.off = (int)((reinterpret_cast<uintptr_t>(X) >> 3) & 1);
     if ((ldx & 1) || (ldy & 1) || A.off != (int)((reinterpret_cast<uintptr_t>(Y) >> 3) & 1)) return BK_ERR_UNSUPPORTED;
+    // rows that start on 128-byte boundaries (caller's row_align): start the slices on the
+    // 128-byte boundary at or before column 0, so every TMA row piece covers whole lines
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(X), ya = reinterpret_cast<uintptr_t>(Y);
+    if (row_align % 128 == 0 && ldx % 16 == 0 && ldy % 16 == 0 && xa % 128 == ya % 128)
+      A.off = (int)((xa % 128) / 8);
     xbase = X - A.off + d0 * ldx;
     ldxd = ldx;
     cols = m + A.off;
@@ -646,7 +655,8 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
     A.vdoubles = (width + 1) / 2 * 2;
   }
   if (A.vdoubles > 256 || woff > 256) return BK_ERR_UNSUPPORTED;  // TMA box limit
-  A.vals_off = M_XS;
+  const int COLS = (!cplx && width <= 8) ? 64 : 32;
+  A.vals_off = M_HR * COLS * 8;
   A.offs_off = A.vals_off + M_T * M_T * A.vdoubles * 8;
   A.slot_bytes = (A.offs_off + M_T * M_T * woff * 2 + 127) / 128 * 128;
   A.ns = (int)lmin(M_NSMAX, (227 * 1024) / A.slot_bytes);
@@ -655,7 +665,7 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   CUtensorMap xmap, vmap, omap;
   const int64_t P = (int64_t)ny * nz;
   int rc = encode_4d(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, xbase + (int64_t)xlo * P * ldxd, cols, nz, ny,
-                     xhi - xlo, ldxd, nz * ldxd, P * ldxd, M_COLS, M_H, M_H);
+                     xhi - xlo, ldxd, nz * ldxd, P * ldxd, COLS, M_H, M_H);
   if (rc == BK_OK)
     rc = encode_4d(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, ell_val, A.vdoubles, nz, ny, nx, A.vdoubles,
                    nz * A.vdoubles, P * A.vdoubles, A.vdoubles, M_T, M_T);
@@ -665,17 +675,18 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   if (rc != BK_OK) return rc;
   A.gy = (ny + M_T - 1) / M_T;
   A.gz = (nz + M_T - 1) / M_T;
-  A.nslices = (int)((cols + M_COLS - 1) / M_COLS);
+  A.nslices = (int)((cols + COLS - 1) / COLS);
   // x segments: >= 8 units per CTA (balance) while a segment keeps >= 8 planes
   const int64_t per_seg = (int64_t)A.gy * A.gz * A.nslices;
   A.xseg = 1;
   while (A.xseg * 2 <= nx / 8 && per_seg * A.xseg < 8 * kSMs) A.xseg *= 2;
   A.nunits = (int)(per_seg * A.xseg);
   // the 7-point (3-D), 27-point and 5-point (2-D) widths run with compile-time chunks
-  auto kern = cplx ? (width == 7 ? spmm_march_kernel<true, 7> : width == 5 ? spmm_march_kernel<true, 5>
-                      : width == 27 ? spmm_march_kernel<true, 27> : spmm_march_kernel<true, 0>)
-                   : (width == 7 ? spmm_march_kernel<false, 7> : width == 5 ? spmm_march_kernel<false, 5>
-                      : width == 27 ? spmm_march_kernel<false, 27> : spmm_march_kernel<false, 0>);
+  auto kern = cplx ? (width == 7 ? spmm_march_kernel<true, 7, 32> : width == 5 ? spmm_march_kernel<true, 5, 32>
+                      : width == 27 ? spmm_march_kernel<true, 27, 32> : spmm_march_kernel<true, 0, 32>)
+                   : (width == 7 ? spmm_march_kernel<false, 7, 64> : width == 5 ? spmm_march_kernel<false, 5, 64>
+                      : width == 27 ? spmm_march_kernel<false, 27, 32>
+                      : width <= 8 ? spmm_march_kernel<false, 0, 64> : spmm_march_kernel<false, 0, 32>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)lmin(A.nunits, kSMs);
   BK_COUNT();
@@ -687,16 +698,20 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
 // Y = A X for a CSR A that is a nearest-neighbour stencil on an nx x ny x nz C-order grid,
 // from the plan of spmm_plan.py StencilPlan (grid-ordered ELL values and 16-bit ring offsets,
 // d0 = column shift, planes [xlo, xhi) referenced); same result as bk_spmm_csr_d.  Real: ldx,
-// ldy even and X, Y equally 16-byte aligned, else BK_ERR_UNSUPPORTED.
+// ldy even and X, Y equally 16-byte aligned, else BK_ERR_UNSUPPORTED.  row_align: the caller's
+// guarantee that the rows of the buffers X and Y are views of start on row_align-byte
+// boundaries (128 lets the slices start on 128-byte lines).
 extern "C" int bk_spmm_march_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                                const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx,
-                               double* Y, int64_t ldy, void* stream) {
-  return march_launch(false, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, stream);
+                               double* Y, int64_t ldy, int row_align, void* stream) {
+  return march_launch(false, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, row_align,
+                      stream);
 }
 
 // complex128: ell_val, X, Y interleaved; ld in complex elements
 extern "C" int bk_spmm_march_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                                const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx,
-                               double* Y, int64_t ldy, void* stream) {
-  return march_launch(true, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, stream);
+                               double* Y, int64_t ldy, int row_align, void* stream) {
+  return march_launch(true, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, row_align,
+                      stream);
 }

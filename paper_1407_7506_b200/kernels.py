@@ -279,6 +279,13 @@ def spmm_csr(rowptr, col, val, x, y):
     return y
 
 
+def _row_align(t):
+    """Byte alignment every row start of t's underlying buffer has (128 or 16)."""
+    base = t.untyped_storage().data_ptr()
+    rowb = ld_of(t) * t.element_size()
+    return 128 if base % 128 == 0 and rowb % 128 == 0 else 16
+
+
 def spmm_march(plan, x, y):
     """Plane-marching stencil SpMM (bk_spmm_march_*) with a device StencilPlan; returns False
     when the views' alignment does not allow it (the caller then uses spmm_csr)."""
@@ -292,7 +299,8 @@ def spmm_march(plan, x, y):
         name = "bk_spmm_march_z"
     nx, ny, nz = plan.grid
     _lib.call(name, nx, ny, nz, plan.xlo, plan.xhi, plan.d0, plan.ell_val.data_ptr(), plan.ell_off.data_ptr(),
-              plan.width, plan.woff, m, x.data_ptr(), ldx, y.data_ptr(), ldy, stream_ptr())
+              plan.width, plan.woff, m, x.data_ptr(), ldx, y.data_ptr(), ldy, min(_row_align(x), _row_align(y)),
+              stream_ptr())
     return True
 
 

@@ -290,7 +290,7 @@ class PPCGSolver:
         z = lambda *s, dt=None: torch.zeros(s, dtype=dt or self.tdt, device="cuda")  # noqa: E731
         # n x k_total blocks with the row stride padded to a multiple of 4 elements (16/32-byte
         # aligned rows for vector and bulk-tensor loads); columns keep global positions
-        self.ldp = (kt + 3) // 4 * 4
+        self.ldp = (kt + 15) // 16 * 16  # 128-byte rows (real): aligned TMA / bulk-copy row pieces
         self.side = torch.cuda.Stream()  # diagnostics that overlap the subblock pencils
         # (kernels.set_strip_stream can run the narrow strips of split Grams on a second
         # stream beside the main launch; measured slower end to end at config 2 -- the strip

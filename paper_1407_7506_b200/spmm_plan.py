@@ -11,7 +11,7 @@ is then read ~(10 x 10)/(8 x 8) = 1.56 times instead of 7 or 27 times.
 The kernel computes from the CSR values in CSR order (so the result equals the gather's bit
 for bit), re-laid out as a grid-ordered ELL (each row's entries contiguous, padded to the
 widest row) together with 16 bits per entry that encode the stencil offset ``(dx, dy, dz)``
-of its column relative to its row as the kernel's shared-memory ring offset, so that a plane
+of its column relative to its row as the kernel's shared-memory ring position, so that a plane
 tile's entries arrive with one TMA load like the X tile.  The grid is inferred
 from the CSR alone, so the reference's own ``SparseHermitian`` objects qualify:
 
@@ -28,8 +28,7 @@ from __future__ import annotations
 
 import numpy as np
 
-TY = TZ = 8         # grid tile per CTA (the kernel's compile-time tile)
-SLICE_DOUBLES = 32  # doubles per staged X row slice (the kernel's M_COLS)
+TY = TZ = 8  # grid tile per CTA (the kernel's compile-time tile)
 
 
 def _torch():
@@ -93,7 +92,7 @@ def _grid_for(o, n):
 class StencilPlan:
     """The march SpMM's plan: grid (nx, ny, nz), shift d0, planes [xlo, xhi) the columns
     reach, and the grid-ordered ELL arrays ``ell_off`` (n x woff int16 holding uint16 bit
-    patterns: the ring offset of each entry's X row, 0xffff = padding) and
+    patterns: the ring position (plane slot, halo row) of each entry's X row, 0xffff = padding) and
     ``ell_values(data)``, as torch tensors on ``indptr``'s device (built on the GPU in
     production: a few elementwise passes over the nonzeros).  ``ok`` is False when the CSR is
     not a nearest-neighbour stencil on an inferred grid."""
@@ -131,8 +130,8 @@ class StencilPlan:
         self.xlo, self.xhi = xlo, xhi
         # grid-ordered ELL (row r's entries in CSR order, then padding 0xffff): the kernel stages
         # a plane tile's entries with one TMA load, like the X tile.  Per entry the kernel's
-        # ring offset of its X row: (dx+1) << 14 | ((dy+1)*(TY+2) + dz+1) * SLICE_DOUBLES
-        offs = ((dx + 1) << 14) | (((dy + 1) * (TY + 2) + (dz + 1)) * SLICE_DOUBLES)
+        # ring position of its X row: (dx+1) << 14 | (dy+1)*(TY+2) + dz+1
+        offs = ((dx + 1) << 14) | ((dy + 1) * (TY + 2) + (dz + 1))
         cnt = indptr[1:] - indptr[:-1]
         w = max(int(cnt.max().item()), 1)
         self.width = w

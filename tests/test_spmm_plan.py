@@ -7,7 +7,7 @@ import pytest
 
 from paper_1407_7506_b200.distributed import local_rows_csr
 from paper_1407_7506_b200.problems import config_problem, laplacian_1d, random_hermitian
-from paper_1407_7506_b200.spmm_plan import SLICE_DOUBLES, TY, StencilPlan
+from paper_1407_7506_b200.spmm_plan import TY, StencilPlan
 from util import gauss
 
 
@@ -25,7 +25,7 @@ def replay(csr, plan, x):
             if o == 0xFFFF:
                 break
             dx = (o >> 14) - 1
-            h = (o & 0x3FFF) // SLICE_DOUBLES
+            h = o & 0x3FFF
             dy, dz = h // (TY + 2) - 1, h % (TY + 2) - 1
             src = plan.d0 + ((ix + dx) * ny + iy + dy) * nz + iz + dz
             y[r] += vals[r, t] * x[src]

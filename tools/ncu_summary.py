@@ -88,11 +88,30 @@ if __name__ == "__main__":
         i = args.index("--launches")
         launches = args[i + 1]
         args = args[:i] + args[i + 2:]
+    # --roofline NAME=REP: all launches of REP form one roofline call (e.g. the Gram's main +
+    # strip launch); kernels[NAME.split('_')[0] + '_kernel'] then carries their summed traffic
+    roofs = []
+    while "--roofline" in args:
+        i = args.index("--roofline")
+        roofs.append(args[i + 1].split("=", 1))
+        args = args[:i] + args[i + 2:]
     summary = {"kernels": {}, "captures": []}
     for p in args:
         for d in rep_summary(p):
             summary["captures"].append(d)
-            summary["kernels"].setdefault(d["kernel"].split("::")[-1].split("<")[0], d)
+            summary["kernels"].setdefault(d["kernel"].split("::")[-1].split("<")[0].replace("void ", ""), d)
+    for name, rep in roofs:
+        ls = rep_summary(rep)
+        entry = {"launches": [{k: d.get(k) for k in ("kernel", "duration_ms", "dram_bytes_per_launch",
+                                                      "tensor_pipe_active_pct", "grid")} for d in ls],
+                 "dram_bytes_total": sum(d["dram_bytes_per_launch"] for d in ls),
+                 "duration_ms_total": sum(d.get("duration_ms", 0.0) for d in ls), "rep": rep}
+        summary["roofline_" + name] = entry
+        key = name.split("_")[0] + "_kernel"
+        base = dict(ls[0])
+        base["dram_bytes_per_launch"] = entry["dram_bytes_total"]
+        base["note"] = f"dram_bytes_per_launch = all launches of the roofline call roofline_{name}"
+        summary["kernels"][key] = base
     if launches:
         summary["launch_shares"] = launch_shares(launches)
     json.dump(summary, open(out, "w"), indent=1)

@@ -40,7 +40,7 @@ def main():
         s = 16 if cplx else 8
         kt = k + -(-k * 2 // 100)
         for m, off in ((kt, 0), (kt - 10, 10), (kt - 11, 11)):
-            ld = (kt + 3) // 4 * 4
+            ld = (kt + 15) // 16 * 16  # the solver's 128-byte rows
             g = torch.Generator(device="cuda").manual_seed(1)
             xb = torch.randn(a.n, ld, dtype=dt, device="cuda", generator=g)
             yb = torch.zeros(a.n, ld, dtype=dt, device="cuda")
