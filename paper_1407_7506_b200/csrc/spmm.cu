@@ -379,7 +379,7 @@ struct MarchArgs {
   int nx, ny, nz;
   int xlo;             // first plane the X tensor map covers
   int gy, gz, nslices, xseg, nunits;
-  int m, off;          // real: columns and 8-byte misalignment of X, Y; complex: off = 0
+  int m, off;          // columns, and leading columns of the slices before column 0 (alignment)
   int vdoubles;        // ELL value row in doubles (real: even width; complex: 2 x width)
   int woff;            // ELL offset row in uint16 (multiple of 8)
   int width;           // ELL entries per row
@@ -480,7 +480,7 @@ BK_DEV void march_row(const uint16_t* orow, const march_vt<CPLX>* vrow, int widt
 template <bool CPLX>
 BK_DEV void march_store(const MarchArgs& A, double* yr, int pc, double2 v) {
   if (CPLX) {
-    if (pc < A.m) *reinterpret_cast<double2*>(yr + 2 * pc) = v;
+    if (pc >= A.off && pc - A.off < A.m) *reinterpret_cast<double2*>(yr + 2 * pc) = v;
   } else {
     const int c = 2 * pc - A.off;  // first column of the pair
     if (c >= 0 && c + 1 < A.m) {
@@ -632,11 +632,14 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   const double* xbase;  // 16-byte aligned base of row-space row 0
   int64_t ldxd, cols;   // leading dimension and tensor width in doubles
   if (cplx) {
-    A.off = 0;
-    xbase = X + 2 * d0 * ldx;
+    // off: leading complex columns (before column 0) the slices start at, for 128-byte lines
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(X), ya = reinterpret_cast<uintptr_t>(Y);
+    A.off = (row_align % 128 == 0 && ldx % 8 == 0 && ldy % 8 == 0 && xa % 128 == ya % 128) ? (int)((xa % 128) / 16)
+                                                                                       : 0;
+    xbase = X + 2 * (d0 * ldx - A.off);
     ldxd = 2 * ldx;
-    cols = 2 * (int64_t)m;
-    A.Y = Y;
+    cols = 2 * ((int64_t)m + A.off);
+    A.Y = Y - 2 * A.off;
     A.ldy = 2 * ldy;
     A.vdoubles = 2 * width;
   } else {
@@ -678,8 +681,18 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   A.nslices = (int)((cols + COLS - 1) / COLS);
   // x segments: >= 8 units per CTA (balance) while a segment keeps >= 8 planes
   const int64_t per_seg = (int64_t)A.gy * A.gz * A.nslices;
+  // x segments: minimise waves x (planes per segment + 2 halo planes); units of one wave run
+  // the same planes of neighbouring tiles (shared halo rows and whole X rows stay in L2)
   A.xseg = 1;
-  while (A.xseg * 2 <= nx / 8 && per_seg * A.xseg < 8 * kSMs) A.xseg *= 2;
+  int64_t best = -1;
+  for (int xs = 1; xs <= lmax(1, nx / 8); ++xs) {
+    const int64_t waves = (per_seg * xs + kSMs - 1) / kSMs;
+    const int64_t cost = waves * ((nx + xs - 1) / xs + 2);
+    if (best < 0 || cost < best) {
+      best = cost;
+      A.xseg = xs;
+    }
+  }
   A.nunits = (int)(per_seg * A.xseg);
   // the 7-point (3-D), 27-point and 5-point (2-D) widths run with compile-time chunks
   auto kern = cplx ? (width == 7 ? spmm_march_kernel<true, 7, 32> : width == 5 ? spmm_march_kernel<true, 5, 32>

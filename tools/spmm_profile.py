@@ -13,7 +13,7 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 a, k, q, tol = config_problem(cfg)
 d = as_device_operator(a)
 kt = k + -(-k * 2 // 100)
-ld = (kt + 3) // 4 * 4
+ld = (kt + 15) // 16 * 16
 dt = torch.complex128 if d.complex else torch.float64
 x = torch.randn(a.n, ld, dtype=dt, device="cuda")[:, :kt]
 y = torch.zeros(a.n, ld, dtype=dt, device="cuda")[:, :kt]
