@@ -3,6 +3,7 @@ tag=${1:-r1h}
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -5 > gpurun_out/tests.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 300 python tools/iter_breakdown.py 2 5 10 > gpurun_out/breakdown2_$tag.log 2>&1
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_small.json 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -13,7 +14,7 @@ for w in gram tsgemm; do
   timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -o gpurun_out/roof_${tag}_$w python tools/roofline_capture.py $w > gpurun_out/ncu_roof_$w.log 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:march -s 2 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:march -s 1 -c 1 \
    -o gpurun_out/prof_${tag}_march python tools/spmm_profile.py 2 march > gpurun_out/ncu_march.log 2>&1
 python tools/profile_iter.py 2 2 > gpurun_out/plain.log 2>&1 && for ks in pencil_kernel:1 recombine_kernel:1; do
     k=${ks%%:*}; skip=${ks##*:}
