@@ -74,6 +74,10 @@ int bk_gram_splits(int m1, int m2);
  * 0 = the cp.async ring of every thread; returns the previous mode (mode < 0: query only).
  * Both give bitwise identical results; the switch exists for A/B measurement and tests. */
 int bk_gram_set_loader(int mode);
+/* Split Grams (bk_gram_splits): 1 = main 64-aligned block and the narrow strips in one launch,
+ * interleaved by row chunk so the strips read X / Y rows while they are in L2 (default);
+ * 0 = two launches.  Returns the previous mode (mode < 0: query only). */
+int bk_gram_set_combo(int mode);
 int bk_gram_part_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y,
                    int64_t ldy, double* C, int64_t ldc, int symmetric, int part, void* ws,
                    int64_t ws_bytes, void* stream);

@@ -41,6 +41,7 @@ _SIGS = {
     "bk_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
     "bk_gram_splits": (c_int, [c_int, c_int]),
     "bk_gram_set_loader": (c_int, [c_int]),
+    "bk_gram_set_combo": (c_int, [c_int]),
     "bk_gram_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,
                                vp]),
     "bk_gram2_part_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, c_int, vp, c_i64,

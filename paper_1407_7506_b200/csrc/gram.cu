@@ -76,6 +76,8 @@ struct GramParams {
   int vec16;                  // all segment offsets/leading dims even: 16-byte copies
   int allow_fast;             // fast-path switch (PPCG_GRAM_FAST=0 disables, for A/B checks)
   int bulk;                   // host: run gram_bulk_kernel (even row strides; PPCG_GRAM_BULK=0 disables)
+  int chunk_major;            // block order (tile, problem, chunk) instead of (tile, chunk, problem)
+  int force_chunks;           // host: split-K chunk count fixed by the caller (0 = choose)
   double* ws;                 // partials: [prob][tile][chunk][BM*BN]
   int* tickets;               // [prob][tile]
 };
@@ -487,8 +489,10 @@ BK_DEV void tile_pieces(const GramProblem& g, bool xop, int c0, int B, int wp, P
   }
 }
 
+// CTA body of the bulk-loader Gram for block `bid` of problem set P (gram_bulk_kernel runs one
+// set; gram_bulk_combo runs a main-block set and a strip set interleaved by chunk)
 template <class C>
-__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(const __grid_constant__ GramParams P) {
+BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
   constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN, ST = C::STAGES;
   constexpr int NCW = C::THREADS / 32;  // MMA warps
   extern __shared__ __align__(16) double smem[];
@@ -499,9 +503,11 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(con
   __shared__ int s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int slot = blockIdx.x % P.max_tiles;
-  const int chunk = (blockIdx.x / P.max_tiles) % P.nchunks;
-  const int pidx = blockIdx.x / (P.max_tiles * P.nchunks);
+  // block order: tile fastest, then chunk, then problem; chunk_major: then problem, then chunk
+  const int slot = (int)(bid % P.max_tiles);
+  const int chunk = P.chunk_major ? (int)(bid / ((int64_t)P.max_tiles * P.nprob))
+                                  : (int)((bid / P.max_tiles) % P.nchunks);
+  const int pidx = P.chunk_major ? (int)((bid / P.max_tiles) % P.nprob) : (int)(bid / ((int64_t)P.max_tiles * P.nchunks));
 
   GramProblem g;
   int wp = 0, w = 0;  // padded segment stride (subblock mode) and real segment width
@@ -674,6 +680,31 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(con
   if (tid == 0) P.tickets[tile_id] = 0;
 }
 
+template <class C>
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(const __grid_constant__ GramParams P) {
+  gram_bulk_body<C>(P, blockIdx.x);
+}
+
+// Main block (CA tiles) and strips (CB tiles) of split Grams in ONE launch, both chunk-major
+// with the same row chunks: the CTAs of chunk c of both sets are adjacent, so the strip CTAs
+// read the chunk's X / Y rows while the main tiles hold them in L2 -- the separate strip launch
+// re-read X and AX from DRAM (1 GB per config-2 Gram) at 4x lower tensor-pipe use.
+template <class CA, class CB>
+__global__ void __launch_bounds__(CA::THREADS + 32, CA::MINB) gram_bulk_combo(const __grid_constant__ GramParams PA,
+                                                                            const __grid_constant__ GramParams PB) {
+  static_assert(CA::THREADS == CB::THREADS, "one block size");
+  const int64_t na = (int64_t)PA.max_tiles * PA.nprob, nb = (int64_t)PB.max_tiles * PB.nprob;
+  const int64_t c = blockIdx.x / (na + nb), l = blockIdx.x % (na + nb);
+  if (l < na) gram_bulk_body<CA>(PA, c * na + l);
+  else gram_bulk_body<CB>(PB, c * nb + (l - na));
+}
+
+// 1: split Grams run main block + strips in one interleaved launch (PPCG_GRAM_COMBO=0: two)
+static int g_combo = [] {
+  const char* e = getenv("PPCG_GRAM_COMBO");
+  return e ? atoi(e) : 1;
+}();
+
 static int g_bulk_loader = [] {
   const char* e = getenv("PPCG_GRAM_BULK");
   return e ? atoi(e) : 1;
@@ -729,7 +760,7 @@ static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, i
     return e ? atoi(e) : 1;
   }();
   P.allow_fast = fast_on;
-  P.nchunks = choose_chunks(P.nrows, total_tiles_slots, C::SLOTS_PER_SM);
+  P.nchunks = P.force_chunks > 0 ? P.force_chunks : choose_chunks(P.nrows, total_tiles_slots, C::SLOTS_PER_SM);
   int64_t part_bytes = (int64_t)total_tiles_slots * P.nchunks * C::BM * C::BN * sizeof(double);
   if (P.nchunks > 1) {
     while (P.nchunks > 1 && kTicketBytes + part_bytes > ws_bytes) {  // fit the workspace
@@ -786,6 +817,78 @@ static bool use_big(int m2) {
     return e ? atoi(e) : 0;
   }();
   return force == 128 && m2 >= 192;
+}
+
+template <class C>
+static int prepare_explicit(int nprob, GramParams& P) {
+  int maxt = 0;
+  P.vec16 = 1;
+  P.bulk = 1;
+  for (int i = 0; i < nprob; ++i) {
+    GramProblem& g = P.prob[i];
+    fill_tiles<C>(g);
+    if (g.M == 0 || g.N == 0) g.ntiles = 0;
+    maxt = max(maxt, g.ntiles);
+    if (!even_segs(g)) P.vec16 = 0;
+    if (g.nxs != 1 || g.nys != 1 || (g.xs[0].ld & 1) || (g.ys[0].ld & 1) ||
+        (reinterpret_cast<uintptr_t>(g.xs[0].p) & 7) || (reinterpret_cast<uintptr_t>(g.ys[0].p) & 7))
+      P.bulk = 0;
+  }
+  P.nprob = nprob;
+  P.explicit_list = 1;
+  P.max_tiles = maxt;
+  return maxt;
+}
+
+// workspace of a combined launch: [tickets A | tickets B (one 64 KB ticket region, the only
+// place any launch keeps tickets, so they are always zero between launches)][partials A][partials B]
+template <class CA, class CB>
+static int64_t combo_ws_bytes(int64_t nrows, int64_t tiles_a, int64_t tiles_b, int nchunks) {
+  return kTicketBytes + (tiles_a * CA::BM * CA::BN + tiles_b * CB::BM * CB::BN) * nchunks * (int64_t)sizeof(double);
+}
+
+template <class CA, class CB>
+static int combo_chunks(int64_t nrows, int64_t tiles_a, int64_t tiles_b) {
+  return choose_chunks(nrows, tiles_a + tiles_b, CA::SLOTS_PER_SM);
+}
+
+// A (main blocks, CA tiles) and B (strips, CB tiles) prepared by prepare_explicit; one launch
+template <class CA, class CB>
+static int launch_combo(GramParams& A, GramParams& B, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  const int64_t ta = (int64_t)A.max_tiles * A.nprob, tb = (int64_t)B.max_tiles * B.nprob;
+  int nch = A.force_chunks;
+  if (combo_ws_bytes<CA, CB>(A.nrows, ta, tb, nch) > ws_bytes || (ta + tb) * (int64_t)sizeof(int) > kTicketBytes)
+    return BK_ERR_UNSUPPORTED;
+  int64_t rows = (A.nrows + nch - 1) / nch;
+  rows = ((rows + G_BK - 1) / G_BK) * G_BK;
+  nch = (int)lmax(1, (A.nrows + rows - 1) / rows);
+  static const int fast_on = [] {
+    const char* e = getenv("PPCG_GRAM_FAST");
+    return e ? atoi(e) : 1;
+  }();
+  char* w = static_cast<char*>(ws);
+  for (GramParams* P : {&A, &B}) {
+    P->allow_fast = fast_on;
+    P->nchunks = nch;
+    P->chunk_rows = rows;
+    P->chunk_major = 1;
+  }
+  A.tickets = reinterpret_cast<int*>(w);
+  B.tickets = A.tickets + ta;
+  A.ws = reinterpret_cast<double*>(w + kTicketBytes);
+  B.ws = A.ws + ta * nch * CA::BM * CA::BN;
+  const int64_t grid = (ta + tb) * nch;
+  if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
+  const int smem = max(CA::SMEM + 16 * CA::STAGES, CB::SMEM + 16 * CB::STAGES);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_bulk_combo<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  BK_COUNT();
+  gram_bulk_combo<CA, CB><<<(unsigned)grid, CA::THREADS + 32, smem, st>>>(A, B);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
 }
 
 template <class C>
@@ -881,6 +984,21 @@ static int gram_problems(int nprob, const GramProblem* probs, int64_t n, void* w
   B.nrows = n;
   int nb = 0;
   for (int i = 0; i < nprob; ++i) nb += split_parts(probs[i], A.prob[i], B.prob + nb);
+  {
+    // main block and strips share one split-K chunking (that of the combined launch), so
+    // the combined launch and the two-launch path (parts, cp.async loader) agree bit for bit
+    GramParams A2 = A, B2 = B;
+    const int ma = prepare_explicit<Small>(nprob, A2), mb = prepare_explicit<Strip>(nb, B2);
+    const int64_t ta = (int64_t)ma * nprob, tb = (int64_t)mb * nb;
+    int nch = combo_chunks<Small, Strip>(n, ta, tb);
+    while (nch > 1 && combo_ws_bytes<Small, Strip>(n, ta, tb, nch) > ws_bytes) nch = (nch + 1) / 2;
+    A.force_chunks = B.force_chunks = nch;
+    if (part == 0 && nb > 0 && g_combo && g_bulk_loader && ma > 0 && mb > 0 && A2.bulk && B2.bulk) {
+      A2.force_chunks = B2.force_chunks = nch;
+      const int rc = launch_combo<Small, Strip>(A2, B2, ws, ws_bytes, st);
+      if (rc != BK_ERR_UNSUPPORTED) return rc;
+    }
+  }
   if (part != 2) {
     int rc = gram_explicit<Small>(nprob, A, ws, ws_bytes, st);
     if (rc != BK_OK) return rc;
@@ -899,7 +1017,10 @@ extern "C" int64_t bk_gram_ws_bytes(int64_t n, int m1, int m2) {
   // split launches (sequential, sharing the buffer): up to two strip problems per Gram
   const int64_t right = (int64_t)((m1 + 63) / 64) * (((m2 % 64) + 15) / 16);
   const int64_t bottom = (int64_t)(m2 / 64) * (((m1 % 64) + 15) / 16);
-  return lmax(full, ws_bytes_for<Strip>(n, 2 * lmax(right, bottom)));
+  // one combined launch (main 64-aligned tiles + both strips, shared chunking)
+  const int64_t main_t = (int64_t)(m1 / 64) * (m2 / 64), strip_t = 2 * lmax(right, bottom);
+  const int64_t combo = combo_ws_bytes<Small, Strip>(n, main_t, strip_t, combo_chunks<Small, Strip>(n, main_t, strip_t));
+  return lmax(lmax(full, combo), ws_bytes_for<Strip>(n, 2 * lmax(right, bottom)));
 }
 
 // C (m1 x m2, ldc) = X(:, 0:m1)^T Y(:, 0:m2) over n rows.  symmetric != 0 requires X == Y,
@@ -911,6 +1032,13 @@ extern "C" int bk_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx
                          int64_t ldy, double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes,
                          void* stream) {
   return gram_d(n, m1, m2, X, ldx, Y, ldy, C, ldc, symmetric, ws, ws_bytes, stream, 0);
+}
+
+// 1 / 0: split Grams as one combined launch / as main + strip launches; -1: query
+extern "C" int bk_gram_set_combo(int mode) {
+  const int prev = g_combo;
+  if (mode >= 0) g_combo = mode ? 1 : 0;
+  return prev;
 }
 
 extern "C" int bk_gram_set_loader(int mode) {
