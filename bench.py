@@ -292,9 +292,18 @@ def run_ours(args):
     from paper_1407_7506_b200.operators import SparseHermitian
     from paper_1407_7506_b200.problems import jacobi_preconditioner
 
+    e2e_opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=args.steps)
+    # one untimed warm-up call (allocator pools, pinned staging, solver handles), then the
+    # timed call on fresh host inputs
     a2 = SparseHermitian(a._csr.copy(), "symmetric")
     t2 = jacobi_preconditioner(a2)
-    e2e_opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=args.steps)
+    warm_opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=2)
+    if world > 1:
+        dist_ppcg_solve(a2, t2, None, warm_opts, comm=comm)
+    else:
+        ppcg_solve(a2, t2, opts=warm_opts)
+    a2 = SparseHermitian(a._csr.copy(), "symmetric")
+    t2 = jacobi_preconditioner(a2)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -333,8 +342,8 @@ def run_ours(args):
         e2e = {"value": rep.iterations / e2e_s, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d // max(rep.iterations, 1), "d2h_bytes_per_step": d2h // max(rep.iterations, 1),
                "note": f"public {api}(host CSR, Jacobi, max_iter={args.steps}) wall time (max over ranks) incl. "
-                       "CSR/X0 upload, init CholQR+SpMM, final RR and vector download; bytes are per-job (rank 0) / "
-                       "iterations"}
+                       "CSR/X0 upload, init CholQR+SpMM, final RR and vector download, after one untimed "
+                       "2-iteration warm-up call; bytes are per-job (rank 0) / iterations"}
         line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": steps_done,
                 "warmup": args.warmup, "ms_per_step": ms_max / max(steps_done, 1), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",

@@ -259,13 +259,22 @@ BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& 
   const int npairs = dd / 2;
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
-    if (threadIdx.x == 0) S.misc[1] = 0;
-    __syncthreads();
+    int rotated = 0;  // any rotation this sweep (this thread), OR-reduced at the phase-1 barrier
+    // round-robin pairs of this thread (pair i = threadIdx.x): player a = (r + i) mod np, b =
+    // (r - i) mod np, stepped incrementally instead of two modulo operations per round
+    const int np_ = dd - 1;
+    int pa = threadIdx.x % np_, pb = (np_ - threadIdx.x % np_) % np_;
     for (int r = 0; r < dd - 1; ++r) {
       // 1. rotation parameters
       for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
         int p, q;
-        rr_pair(r, i, dd, p, q);
+        if (i == threadIdx.x) {
+          const int a = i == 0 ? r : pa, b = i == 0 ? np_ : pb;
+          p = min(a, b);
+          q = max(a, b);
+        } else {
+          rr_pair(r, i, dd, p, q);
+        }
         double c = 1.0, s = 0.0;
         T ph = fromR<T>(1.0);
         if (q < d) {
@@ -279,7 +288,7 @@ BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& 
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
             s = t * c;
-            atomicAdd(&S.misc[1], 1);
+            rotated = 1;
           }
         }
         S.pp[i] = p;
@@ -288,7 +297,9 @@ BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& 
         S.rs[i] = s;
         S.rph[i] = ph;
       }
-      __syncthreads();
+      pa = pa + 1 == np_ ? 0 : pa + 1;
+      pb = pb + 1 == np_ ? 0 : pb + 1;
+      rotated = __syncthreads_or(rotated);
       // 2. row rotations A <- J^H A  (warp per pair, lanes over columns)
       for (int i = BK_WARP; i < npairs; i += BK_NWARP) {
         const double s = S.rs[i];
@@ -330,8 +341,7 @@ BK_DEV int smem_jacobi(T* A, int la, T* V, int lv, int d, bool withV, PSmem<T>& 
       }
       __syncthreads();
     }
-    if (S.misc[1] == 0) break;
-    __syncthreads();
+    if (!rotated) break;
   }
   __syncthreads();
   if (threadIdx.x == 0) S.misc[2] += min(sweep + 1, 60);  // sweeps, reported in info[3] >> 8
