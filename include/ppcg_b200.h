@@ -102,6 +102,10 @@ int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X,
 
 /* ---- batched subblock update (block_update ppcg.py:278-378 incl. fallback 231-275,
  *      solve_pencil core.py:175-202) and plain batched pencils */
+/* Dense eigensolver of real shared-memory pencils (d <= 96, want <= 32): 0 = Householder
+ * tridiagonalisation + bisection + inverse iteration (default), 1 = two-sided Jacobi.
+ * Returns the previous mode (mode < 0: query only). */
+int bk_pencil_set_eig(int mode);
 int bk_pencil_max_dim(void);
 /* global workspace for nb pencils of dimension dmax (0 when d <= 96 real / 64 complex, which
  * run entirely in shared memory; larger ones keep their matrices and, real, the Jacobi

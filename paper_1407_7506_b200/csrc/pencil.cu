@@ -85,6 +85,7 @@ struct PencilParams {
   int want;          // raw mode
   int rawd;          // raw mode pencil dimension
   int force_fallback;  // 1: fallback_steepest_descent directly (ppcg.py:456-472 redo)
+  int eig_jacobi;      // 1: dense eigensolve by Jacobi only (no tridiagonal route)
   void* ws;          // large variant: nb x 3 x PD_BIG x (PD_BIG + 1) scalars
 };
 
@@ -553,12 +554,335 @@ BK_DEV void replay_rotations(double* E, int le, int d, const int* sel, int want,
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- tridiagonal eigensolver
+// Real reduced pencils of the shared-memory variant (d <= 96, want <= 32: config 2's q = 32)
+// need only the `want` smallest of d eigenpairs.  Instead of the full two-sided Jacobi (~95
+// rounds x ~8 sweeps x 3 CTA barriers) this is the LAPACK sytrd + stebz + stein route:
+//   1. Householder tridiagonalisation T = Q^T A Q (dsytd2 order; ~3 barriers per column),
+//   2. bisection on Sturm counts for the `want` smallest eigenvalues of T, one warp per
+//      eigenvalue, 32-point multisection per step (dstebz semantics: pivmin guard, to full
+//      relative precision),
+//   3. inverse iteration for their eigenvectors (dstein: LU of T - lambda I with partial
+//      pivoting, tiny pivots perturbed, eigenvalues closer than 1e-3 ||T||_1 form clusters whose
+//      vectors are reorthogonalised in order, in waves),
+//   4. back-transformation by the reflectors (warp per column, no barriers).
+// A (d x d full symmetric, ld la) is overwritten: on exit ev[0:want] ascending eigenvalues and
+// the eigenvectors in A[k * la + r], r < want.  Mx: scratch of >= PD x (PD + 1) doubles (the
+// pencil's dead B).  Returns 0, or 1 when inverse iteration did not settle (caller redoes the
+// attempt with the Jacobi solver).
+constexpr int TD_MAXWANT = 32, TD_BATCH = 16, TD_ZOFF = 0, TD_SCROFF = 96 * 32, TD_SCR = 4 * 96;
+constexpr int TD_VOFF = TD_SCROFF + TD_BATCH * TD_SCR;  // d doubles (tridiagonalisation v)
+
+BK_DEV int sturm_count(const double* dg, const double* e, int n, double x, double pivmin) {
+  double q = dg[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int c = q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    q = (dg[i] - x) - e[i - 1] * e[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    c += q < 0.0;
+  }
+  return c;
+}
+
+// deterministic start vector component in (-1, 1)
+BK_DEV double td_start(int j, int i) {
+  uint32_t h = (uint32_t)(j * 0x9E3779B1u) ^ (uint32_t)(i * 0x85EBCA77u) ^ 0x27d4eb2fu;
+  h ^= h >> 15;
+  h *= 0x2c1b3c6du;
+  h ^= h >> 12;
+  h *= 0x297a2d39u;
+  h ^= h >> 15;
+  return (double)(h & 0xffffff) / (double)0x800000 - 1.0;
+}
+
+template <int PD>
+BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<double>& S) {
+  const int tid = threadIdx.x, lane = BK_LANE, warp = BK_WARP, nw = BK_NWARP;
+  double* dg = S.rc;              // diagonal of T (rc and rs are contiguous: PD doubles)
+  double* e = A + (d - 1) * la;   // off-diagonal of T in the dead lower part of row d - 1
+  double* v = Mx + TD_VOFF;       // reflector of the current column
+  double* p = Mx + TD_SCROFF;     // tau A22 v
+  // ---- 1. tridiagonalisation; the scaled reflector sqrt(tau) v_k goes to row k's upper part
+  for (int k = 0; k < d - 2; ++k) {
+    const int m = d - k - 1;
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int i = 1 + lane; i < m; i += 32) {
+        const double xi = A[(k + 1 + i) * la + k];
+        s2 += xi * xi;
+      }
+      s2 = warp_sum(s2);
+      const double alpha = A[(k + 1) * la + k];
+      double beta = alpha, tau = 0.0, scal = 0.0;
+      if (s2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int i = lane; i < m; i += 32) v[i] = i == 0 ? 1.0 : A[(k + 1 + i) * la + k] * scal;
+      __syncwarp();
+      if (lane == 0) {
+        S.red[28] = tau;
+        dg[k] = A[k * la + k];
+        e[k] = beta;  // column k below the diagonal is dead from here on
+      }
+    }
+    __syncthreads();
+    const double tau = S.red[28];
+    if (tau != 0.0) {
+      double pv = 0.0;
+      for (int i = warp; i < m; i += nw) {
+        const double* row = A + (k + 1 + i) * la + (k + 1);
+        double s = 0.0;
+        for (int j = lane; j < m; j += 32) s += row[j] * v[j];
+        s = warp_sum(s) * tau;
+        if (lane == 0) p[i] = s;
+        pv += s * v[i];
+      }
+      if (lane == 0) S.red[warp] = pv;
+      __syncthreads();
+      double pvt = 0.0;
+      for (int w = 0; w < nw; ++w) pvt += S.red[w];
+      const double a2 = -0.5 * tau * pvt;
+      for (int i = warp; i < m; i += nw) {
+        const double vi = v[i], wi = p[i] + a2 * vi;
+        double* row = A + (k + 1 + i) * la + (k + 1);
+        for (int j = lane; j < m; j += 32) row[j] -= vi * (p[j] + a2 * v[j]) + wi * v[j];
+      }
+    }
+    const double st = sqrt(tau);
+    for (int i = tid; i < m; i += blockDim.x) A[k * la + k + 1 + i] = st * v[i];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (d >= 2) {
+      dg[d - 2] = A[(d - 2) * la + d - 2];
+      e[d - 2] = A[(d - 1) * la + d - 2];
+    }
+    dg[d - 1] = A[(d - 1) * la + d - 1];
+    // Gershgorin interval, 1-norm, pivmin (dstebz)
+    double gl = 1e300, gu = -1e300, onenrm = 0.0, emax2 = 1.0;
+    for (int i = 0; i < d; ++i) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < d - 1 ? fabs(e[i]) : 0.0);
+      gl = fmin(gl, dg[i] - r);
+      gu = fmax(gu, dg[i] + r);
+      onenrm = fmax(onenrm, fabs(dg[i]) + r);
+      if (i < d - 1) emax2 = fmax(emax2, e[i] * e[i]);
+    }
+    const double tnorm = fmax(fabs(gl), fabs(gu));
+    const double pivmin = DBL_MIN * emax2;
+    gl -= 2.1 * tnorm * DBL_EPSILON * d + 4.2 * pivmin;
+    gu += 2.1 * tnorm * DBL_EPSILON * d + 4.2 * pivmin;
+    S.red[24] = gl;
+    S.red[25] = gu;
+    S.red[26] = pivmin;
+    S.red[27] = onenrm;
+  }
+  __syncthreads();
+  // ---- 2. bisection, one warp per wanted eigenvalue, 32-point multisection
+  double* lam = v;  // eigenvalues (v is dead)
+  {
+    const double pivmin = S.red[26];
+    for (int j = warp; j < want; j += nw) {
+      double lo = S.red[24], hi = S.red[25];
+      for (int it = 0; it < 64; ++it) {
+        if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin) break;
+        const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+        const int c = sturm_count(dg, e, d, x, pivmin);
+        const unsigned b = __ballot_sync(0xffffffffu, c > j);
+        const int f = b ? __ffs(b) - 1 : 32;
+        const double nhi = f < 32 ? __shfl_sync(0xffffffffu, x, f & 31) : hi;
+        const double nlo = f > 0 ? __shfl_sync(0xffffffffu, x, (f - 1) & 31) : lo;
+        lo = nlo;
+        hi = nhi;
+      }
+      if (lane == 0) lam[j] = 0.5 * (lo + hi);
+    }
+  }
+  __syncthreads();
+  // dstein's perturbation of too-close shifts (distinct shifts, distinct iterates)
+  double* shift = S.ev;  // (ev is rewritten at the end)
+  if (tid == 0) {
+    double prev = -1e300;
+    for (int j = 0; j < want; ++j) {
+      double x = lam[j];
+      const double pertol = 10.0 * DBL_EPSILON * fabs(x);
+      if (j > 0 && x - prev < pertol) x = prev + pertol;
+      shift[j] = x;
+      prev = x;
+    }
+  }
+  __syncthreads();
+  // ---- 3. inverse iteration, all vectors independent (TD_BATCH threads at a time); a tight
+  //    cluster's iterates come out as independent mixtures of its eigenvectors (distinct
+  //    start vectors), which the Rayleigh-Ritz step below resolves
+  double* Z = Mx + TD_ZOFF;  // Z[i * 32 + j]
+  const double tiny = DBL_EPSILON * fmax(S.red[27], DBL_MIN);
+  int bad = 0;
+  for (int b0 = 0; b0 < want; b0 += TD_BATCH) {
+    const int j = b0 + tid;
+    if (tid < TD_BATCH && j < want) {
+      double* u0 = Mx + TD_SCROFF + tid * TD_SCR;
+      double* u1 = u0 + 96;
+      double* u2 = u1 + 96;
+      double* x = u2 + 96;
+      const double lj = shift[j];
+      for (int i = 0; i < d; ++i) x[i] = td_start(j, i);
+      for (int iter = 0; iter < 3 && !bad; ++iter) {
+        // LU with partial pivoting of T - lj I (dgttrf), fused with the forward solve
+        double cd = dg[0] - lj, cdu = d > 1 ? e[0] : 0.0;
+        for (int i = 0; i < d - 1; ++i) {
+          const double dl = e[i], nd = dg[i + 1] - lj, ndu = i + 1 < d - 1 ? e[i + 1] : 0.0;
+          if (fabs(cd) >= fabs(dl)) {
+            const double piv = fabs(cd) < tiny ? copysign(tiny, cd) : cd;
+            const double f = dl / piv;
+            u0[i] = piv;
+            u1[i] = cdu;
+            u2[i] = 0.0;
+            x[i + 1] -= f * x[i];
+            cd = nd - f * cdu;
+            cdu = ndu;
+          } else {
+            const double f = cd / dl;
+            u0[i] = dl;
+            u1[i] = nd;
+            u2[i] = ndu;
+            const double t = x[i];
+            x[i] = x[i + 1];
+            x[i + 1] = t - f * x[i];
+            cd = cdu - f * nd;
+            cdu = -f * ndu;
+          }
+        }
+        u0[d - 1] = fabs(cd) < tiny ? copysign(tiny, cd) : cd;
+        x[d - 1] /= u0[d - 1];
+        if (d >= 2) x[d - 2] = (x[d - 2] - u1[d - 2] * x[d - 1]) / u0[d - 2];
+        for (int i = d - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
+        double mx = 0.0;
+        for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(x[i]));
+        if (!(mx > 0.0) || !isfinite(mx)) {
+          bad = 1;
+          break;
+        }
+        const double sc = 1.0 / mx;
+        for (int i = 0; i < d; ++i) x[i] *= sc;
+      }
+      for (int i = 0; i < d; ++i) Z[i * 32 + j] = x[i];
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad)) return 1;
+  // ---- 3b. modified Gram-Schmidt, twice, over the columns of Z (want <= 32)
+  double* cf = Mx + TD_SCROFF;  // coefficients
+  for (int j = 0; j < want; ++j) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = warp; i < j; i += nw) {
+        double s = 0.0;
+        for (int r = lane; r < d; r += 32) s += Z[r * 32 + i] * Z[r * 32 + j];
+        s = warp_sum(s);
+        if (lane == 0) cf[i] = s;
+      }
+      __syncthreads();
+      for (int r = tid; r < d; r += blockDim.x) {
+        double z = Z[r * 32 + j];
+        for (int i = 0; i < j; ++i) z -= cf[i] * Z[r * 32 + i];
+        Z[r * 32 + j] = z;
+      }
+      __syncthreads();
+    }
+    double n2 = 0.0;
+    if (warp == 0) {
+      for (int r = lane; r < d; r += 32) n2 += Z[r * 32 + j] * Z[r * 32 + j];
+      n2 = warp_sum(n2);
+      if (lane == 0) cf[32] = n2;
+    }
+    __syncthreads();
+    n2 = cf[32];
+    if (!(n2 > 0.0) || !isfinite(n2)) return 1;  // (uniform)
+    const double sc = 1.0 / sqrt(n2);
+    for (int r = tid; r < d; r += blockDim.x) Z[r * 32 + j] *= sc;
+    __syncthreads();
+  }
+  // ---- 3c. Rayleigh-Ritz in span(Z): H = Z^T T Z (want x want), Jacobi, Z <- Z U sorted
+  {
+    double* Y = Mx + TD_SCROFF;       // T Z (d x 32)
+    double* H = Y + 96 * 32;          // want x 33
+    double* U = H + 32 * 33;          // want x 33
+    for (int t = tid; t < d * want; t += blockDim.x) {
+      const int r = t / want, j = t % want;
+      double y = dg[r] * Z[r * 32 + j];
+      if (r > 0) y += e[r - 1] * Z[(r - 1) * 32 + j];
+      if (r < d - 1) y += e[r] * Z[(r + 1) * 32 + j];
+      Y[r * 32 + j] = y;
+    }
+    __syncthreads();
+    for (int t = tid; t < want * want; t += blockDim.x) {
+      const int a = t / want, b = t % want;
+      if (b < a) continue;
+      double h = 0.0;
+      for (int r = 0; r < d; ++r) h += Z[r * 32 + a] * Y[r * 32 + b];
+      double h2 = 0.0;
+      for (int r = 0; r < d; ++r) h2 += Z[r * 32 + b] * Y[r * 32 + a];
+      h = 0.5 * (h + h2);
+      H[a * 33 + b] = h;
+      H[b * 33 + a] = h;
+    }
+    __syncthreads();
+    smem_jacobi<double>(H, 33, U, 33, want, true, S);  // (uses rc/rs/pp/pq: dg is dead now)
+    __syncthreads();
+    for (int i = tid; i < want; i += blockDim.x) {
+      const double vi = H[i * 33 + i];
+      int rk = 0;
+      for (int k2 = 0; k2 < want; ++k2) {
+        const double u = H[k2 * 33 + k2];
+        rk += (u < vi) || (u == vi && k2 < i);
+      }
+      S.ord[rk] = i;
+    }
+    __syncthreads();
+    // Z U (sorted) -> Y, then back into Z
+    for (int t = tid; t < d * want; t += blockDim.x) {
+      const int r = t / want, j = t % want, c = S.ord[j];
+      double z = 0.0;
+      for (int k2 = 0; k2 < want; ++k2) z += Z[r * 32 + k2] * U[k2 * 33 + c];
+      Y[r * 32 + j] = z;
+    }
+    for (int j = tid; j < want; j += blockDim.x) S.ev[j] = H[S.ord[j] * 33 + S.ord[j]];  // (lam overlaps U)
+    __syncthreads();
+    for (int t = tid; t < d * want; t += blockDim.x) {
+      const int r = t / want, j = t % want;
+      Z[r * 32 + j] = Y[r * 32 + j];
+    }
+    __syncthreads();
+  }
+  // ---- 4. back-transformation Z <- H_0 ... H_{d-3} Z (warp per column, reflectors read-only)
+  for (int j = warp; j < want; j += nw) {
+    for (int k = d - 3; k >= 0; --k) {
+      const int m = d - k - 1;
+      const double* wk = A + k * la + k + 1;
+      double dot = 0.0;
+      for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * 32 + j];
+      dot = warp_sum(dot);
+      for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * 32 + j] -= wk[i] * dot;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // eigenvectors -> A[:, 0:want], eigenvalues -> ev[0:want] (ascending), ord = identity
+  for (int i = warp; i < d; i += nw)
+    for (int j = lane; j < want; j += 32) A[i * la + j] = Z[i * 32 + j];
+  for (int j = tid; j < want; j += blockDim.x) S.ord[j] = j;  // ev set by the Rayleigh-Ritz step
+  __syncthreads();
+  return 0;
+}
+
 // ---------------------------------------------------------------- one pencil attempt
 // Assembled basis: idx[0:d] raw columns, sf[0:d] scale factors.  Raw Grams at (Ar, Br, ldr).
 // On success: ev[0:want] ascending eigenvalues, C (d x want) in M1 (ld PLD).
 // Returns 0 ok, 1 singular (either Cholesky failed).
 template <class T, int PD>
-BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PSmem<T>& S) {
+BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int want, PSmem<T>& S, bool td) {
   constexpr int PLD = PD + 1;
   T* A = S.M0;
   T* B = S.M1;
@@ -628,6 +952,15 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
     sweeps = packed_jacobi(d, reinterpret_cast<PSmem<double>&>(S));
     for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = pkbuf[S.ro[i] + i];
   } else {
+    if constexpr (std::is_same<T, double>::value) {
+      if (td && want <= TD_MAXWANT && d >= 4 && PD <= 96) {
+        // tridiagonal route: eigenvectors land in A[:, 0:want], ev/ord set (see tridiag_eig)
+        if (tridiag_eig<PD>(A, PLD, d, want, B, S) != 0) return 2;
+        smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+        __syncthreads();
+        return 0;
+      }
+    }
     smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
     for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
   }
@@ -668,6 +1001,14 @@ BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PS
   return 0;
 }
 
+// One attempt: the tridiagonal route for real pencils (S.misc[3] == 0), redone with the
+// Jacobi solver if its inverse iteration did not settle
+template <class T, int PD>
+BK_DEV int pencil_attempt(const T* Ar, const T* Br, int ldr, int d, int want, PSmem<T>& S) {
+  const int rc = pencil_attempt_impl<T, PD>(Ar, Br, ldr, d, want, S, S.misc[3] == 0);
+  return rc == 2 ? pencil_attempt_impl<T, PD>(Ar, Br, ldr, d, want, S, false) : rc;
+}
+
 // ---------------------------------------------------------------- the kernel
 template <class T, int PD, bool GMEM>
 __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_constant__ PencilParams P) {
@@ -697,7 +1038,10 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
   S.pp = S.ord + PD;
   S.pq = S.pp + PD / 2;
   S.misc = S.pq + PD / 2;
-  if (threadIdx.x == 0) S.misc[2] = 0;
+  if (threadIdx.x == 0) {
+    S.misc[2] = 0;
+    S.misc[3] = P.eig_jacobi;
+  }
   S.ro = S.misc + 8;
   S.pk = reinterpret_cast<double*>(S.ro + ((PD + 3) & ~3));
 
@@ -890,8 +1234,15 @@ static void launch_variant(const PencilParams& P, cudaStream_t st) {
   pencil_kernel<T, PD, GMEM><<<P.nb, P_THREADS, p_smem_bytes<T, PD, GMEM>(), st>>>(P);
 }
 
+// dense eigensolve of real shared-memory pencils: 0 = tridiagonal route (default), 1 = Jacobi
+static int g_eig_jacobi = [] {
+  const char* e = getenv("PPCG_PENCIL_EIG");
+  return e && e[0] == 'j' ? 1 : 0;
+}();
+
 template <class T>
-static int launch_pencils(const PencilParams& P, int dim, int64_t ws_bytes, cudaStream_t st) {
+static int launch_pencils(PencilParams P, int dim, int64_t ws_bytes, cudaStream_t st) {
+  P.eig_jacobi = g_eig_jacobi;
   if (dim <= PD_<T>::v) {
     if (p_ws_bytes<T>(P.nb, dim) > 0 && (P.ws == nullptr || ws_bytes < p_ws_bytes<T>(P.nb, dim))) return BK_ERR_ARG;
     BK_COUNT();
@@ -956,6 +1307,14 @@ static int pencil_batched(int nb, int d, int ldm, const void* A, const void* B, 
 using namespace bk;
 
 extern "C" int bk_pencil_max_dim(void) { return PD_BIG; }
+
+// Dense eigensolver of the real shared-memory pencils (d <= 96, want <= 32): 0 = Householder
+// tridiagonalisation + bisection + inverse iteration (default), 1 = two-sided Jacobi; -1 = query.
+extern "C" int bk_pencil_set_eig(int mode) {
+  const int prev = g_eig_jacobi;
+  if (mode >= 0) g_eig_jacobi = mode ? 1 : 0;
+  return prev;
+}
 
 // Global workspace bytes the pencil solves need for nb problems of dimension dmax: 0 for the
 // shared-memory variant (d <= 96 real, 64 complex), else A/B/Linv (+ the real rotation log).
