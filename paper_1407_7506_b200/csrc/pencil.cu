@@ -683,11 +683,13 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<dou
   // ---- 2. bisection, one warp per wanted eigenvalue, 32-point multisection
   double* lam = v;  // eigenvalues (v is dead)
   {
-    const double pivmin = S.red[26];
+    const double pivmin = S.red[26], tnorm = fmax(fabs(S.red[24]), fabs(S.red[25]));
     for (int j = warp; j < want; j += nw) {
       double lo = S.red[24], hi = S.red[25];
       for (int it = 0; it < 64; ++it) {
-        if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin) break;
+        // shifts to 1e-11 ||T||: inverse iteration needs no more, and the Rayleigh-Ritz step
+        // supplies the eigenvalues to full accuracy
+        if (hi - lo <= 1e-11 * tnorm + 2.0 * pivmin) break;
         const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
         const int c = sturm_count(dg, e, d, x, pivmin);
         const unsigned b = __ballot_sync(0xffffffffu, c > j);
@@ -729,7 +731,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<dou
       double* x = u2 + 96;
       const double lj = shift[j];
       for (int i = 0; i < d; ++i) x[i] = td_start(j, i);
-      for (int iter = 0; iter < 3 && !bad; ++iter) {
+      for (int iter = 0; iter < 2 && !bad; ++iter) {
         // LU with partial pivoting of T - lj I (dgttrf), fused with the forward solve
         double cd = dg[0] - lj, cdu = d > 1 ? e[0] : 0.0;
         for (int i = 0; i < d - 1; ++i) {
@@ -1155,15 +1157,23 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         for (int e = tid; e < d * w; e += blockDim.x) T1[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
         for (int e = tid; e < w * w; e += blockDim.x) T2[(e / w) * lw + e % w] = S.M1[(e / w) * PLD + e % w];
         __syncthreads();
-        smem_svals(T1, lw, d, w, S.rc, S);
-        double cn = 0.0;
-        for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
-        __syncthreads();
+        // sigma_min(C_X) first; ||C||_2 <= ||C||_F, so sigma_min >= 1e-14 max(||C||_F, 1) already
+        // decides "no fallback" exactly as the reference would -- only below that bound is the
+        // exact ||C||_2 (one-sided Jacobi of the d x w C) needed
+        double fro2 = 0.0;
+        for (int e2 = tid; e2 < d * w; e2 += blockDim.x) fro2 += ab2(T1[(e2 / w) * lw + e2 % w]);
+        const double cfro = sqrt(block_sum(fro2, S.red));
         smem_svals(T2, lw, w, w, S.rc, S);
         double smin = S.rc[0];
         for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
         __syncthreads();
-        if (smin < kCxFloor * fmax(cn, 1.0)) do_fallback = true;
+        if (smin < kCxFloor * fmax(cfro, 1.0)) {
+          smem_svals(T1, lw, d, w, S.rc, S);
+          double cn = 0.0;
+          for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
+          __syncthreads();
+          if (smin < kCxFloor * fmax(cn, 1.0)) do_fallback = true;
+        }
       }
     }
     if (do_fallback) {
