@@ -437,3 +437,51 @@ def test_solver_bulk_loader_bitwise(cuda):
     (t1, x1), (t0, x0) = _both_loaders(run)
     assert t1 == t0
     assert np.array_equal(x1, x0)
+
+
+@pytest.mark.parametrize("kind", ["degenerate", "clustered", "graded"])
+@pytest.mark.parametrize("eig", [0, 1])
+def test_pencil_tridiagonal_route_hard_spectra(cuda, kind, eig):
+    """The d <= 96 real pencils' tridiagonal route (bisection + inverse iteration + Rayleigh-
+    Ritz, eig=0) and the Jacobi (eig=1) on spectra that stress inverse iteration: exactly
+    repeated eigenvalues inside the wanted set, tight clusters (gaps 1e-9), and a graded
+    spectrum spanning 12 orders of magnitude -- same contract as solve_small_pencil
+    (core.py:167-202): ascending eigenvalues, C^T B C = I, A C = B C diag(omega)."""
+    from paper_1407_7506_b200 import _lib
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    lib = _lib.load()
+    d, want, nb = 96, 32, 2
+    rng = np.random.default_rng(5)
+    if kind == "degenerate":
+        lam = np.sort(np.concatenate([np.repeat([0.5, 1.0, 2.0], 6), rng.uniform(3, 9, d - 18)]))
+    elif kind == "clustered":
+        lam = np.sort(np.concatenate([1.0 + 1e-9 * np.arange(12), 2.0 + 1e-9 * np.arange(12), rng.uniform(3, 9, d - 24)]))
+    else:
+        lam = np.sort(np.logspace(-6, 6, d) * rng.choice([-1.0, 1.0], d))
+    A, B = [], []
+    for i in range(nb):
+        Q = np.linalg.qr(rng.standard_normal((d, d)))[0]
+        A.append((Q * lam) @ Q.T)
+        B.append(hpd_matrix(d, 90 + i) if i else np.eye(d))
+    A, B = np.stack(A), np.stack(B)
+    om = torch.zeros((nb, want), dtype=torch.float64, device="cuda")
+    C = torch.zeros((nb, d, want), dtype=torch.float64, device="cuda")
+    st = torch.zeros((nb, 4), dtype=torch.int32, device="cuda")
+    prev = lib.bk_pencil_set_eig(eig)
+    try:
+        K.pencil_batched(dev(A, torch), dev(B, torch), want, om, C, st)
+    finally:
+        lib.bk_pencil_set_eig(prev)
+    om, C, st = om.cpu().numpy(), C.cpu().numpy(), st.cpu().numpy()
+    for i in range(nb):
+        assert st[i, 2] == 0
+        Bs, As = 0.5 * (B[i] + B[i].T), 0.5 * (A[i] + A[i].T)
+        w_ref, _ = O.solve_small_pencil(A[i], B[i], want)
+        scale = max(1.0, np.max(np.abs(np.linalg.eigvalsh(As))))
+        assert np.allclose(om[i], w_ref, atol=1e-12 * scale, rtol=0), np.max(np.abs(om[i] - w_ref))
+        assert np.all(np.diff(om[i]) >= 0)
+        assert np.allclose(C[i].T @ Bs @ C[i], np.eye(want), atol=1e-11)
+        r = As @ C[i] - Bs @ C[i] * om[i][None, :]
+        assert np.max(np.abs(r)) <= 1e-10 * scale
