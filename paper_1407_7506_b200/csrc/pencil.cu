@@ -560,18 +560,20 @@ BK_DEV void replay_rotations(double* E, int le, int d, const int* sel, int want,
 // rounds x ~8 sweeps x 3 CTA barriers) this is the LAPACK sytrd + stebz + stein route:
 //   1. Householder tridiagonalisation T = Q^T A Q (dsytd2 order; ~3 barriers per column),
 //   2. bisection on Sturm counts for the `want` smallest eigenvalues of T, one warp per
-//      eigenvalue, 32-point multisection per step (dstebz semantics: pivmin guard, to full
-//      relative precision),
-//   3. inverse iteration for their eigenvectors (dstein: LU of T - lambda I with partial
-//      pivoting, tiny pivots perturbed, eigenvalues closer than 1e-3 ||T||_1 form clusters whose
-//      vectors are reorthogonalised in order, in waves),
+//      eigenvalue, 32-point multisection per step (dstebz's pivmin guard), to 1e-11 ||T||,
+//   3. inverse iteration, two steps per eigenvalue, all vectors independent (dgttrf LU of
+//      T - lambda I with partial pivoting, tiny pivots perturbed, dstein's separation of too-close
+//      shifts), modified Gram-Schmidt twice, and a Rayleigh-Ritz step in their span (Jacobi of
+//      Z^T T Z) that resolves clusters and gives the eigenvalues to full accuracy,
 //   4. back-transformation by the reflectors (warp per column, no barriers).
 // A (d x d full symmetric, ld la) is overwritten: on exit ev[0:want] ascending eigenvalues and
-// the eigenvectors in A[k * la + r], r < want.  Mx: scratch of >= PD x (PD + 1) doubles (the
-// pencil's dead B).  Returns 0, or 1 when inverse iteration did not settle (caller redoes the
-// attempt with the Jacobi solver).
-constexpr int TD_MAXWANT = 32, TD_BATCH = 16, TD_ZOFF = 0, TD_SCROFF = 96 * 32, TD_SCR = 4 * 96;
-constexpr int TD_VOFF = TD_SCROFF + TD_BATCH * TD_SCR;  // d doubles (tridiagonalisation v)
+// the eigenvectors in A[k * la + r], r < want.  Returns 0, or 1 when inverse iteration broke
+// down (caller redoes the attempt with the Jacobi solver).
+// ZW = most wanted eigenpairs (32 for d <= 96, 64 for the d <= 192 large variant).  Buffers:
+// Z (PD x ZW), H and U (ZW x (ZW + 1)) in shared memory; scr (TD_BATCH x 4 PD) and v (PD) may
+// alias H / U (inverse iteration finishes before the Rayleigh-Ritz step).
+constexpr int TD_BATCH = 16;
+template <int PD> constexpr int td_zw() { return PD <= 96 ? 32 : 64; }
 
 BK_DEV int sturm_count(const double* dg, const double* e, int n, double x, double pivmin) {
   double q = dg[0] - x;
@@ -597,12 +599,13 @@ BK_DEV double td_start(int j, int i) {
 }
 
 template <int PD>
-BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<double>& S) {
+BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H, double* U, double* scr, double* v,
+                       PSmem<double>& S) {
+  constexpr int ZW = td_zw<PD>(), HL = ZW + 1;
   const int tid = threadIdx.x, lane = BK_LANE, warp = BK_WARP, nw = BK_NWARP;
   double* dg = S.rc;              // diagonal of T (rc and rs are contiguous: PD doubles)
   double* e = A + (d - 1) * la;   // off-diagonal of T in the dead lower part of row d - 1
-  double* v = Mx + TD_VOFF;       // reflector of the current column
-  double* p = Mx + TD_SCROFF;     // tau A22 v
+  double* p = scr;                // tau A22 v (v: reflector of the current column)
   // ---- 1. tridiagonalisation; the scaled reflector sqrt(tau) v_k goes to row k's upper part
   for (int k = 0; k < d - 2; ++k) {
     const int m = d - k - 1;
@@ -719,16 +722,15 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<dou
   // ---- 3. inverse iteration, all vectors independent (TD_BATCH threads at a time); a tight
   //    cluster's iterates come out as independent mixtures of its eigenvectors (distinct
   //    start vectors), which the Rayleigh-Ritz step below resolves
-  double* Z = Mx + TD_ZOFF;  // Z[i * 32 + j]
   const double tiny = DBL_EPSILON * fmax(S.red[27], DBL_MIN);
   int bad = 0;
   for (int b0 = 0; b0 < want; b0 += TD_BATCH) {
     const int j = b0 + tid;
     if (tid < TD_BATCH && j < want) {
-      double* u0 = Mx + TD_SCROFF + tid * TD_SCR;
-      double* u1 = u0 + 96;
-      double* u2 = u1 + 96;
-      double* x = u2 + 96;
+      double* u0 = scr + tid * 4 * PD;
+      double* u1 = u0 + PD;
+      double* u2 = u1 + PD;
+      double* x = u2 + PD;
       const double lj = shift[j];
       for (int i = 0; i < d; ++i) x[i] = td_start(j, i);
       for (int iter = 0; iter < 2 && !bad; ++iter) {
@@ -770,91 +772,99 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<dou
         const double sc = 1.0 / mx;
         for (int i = 0; i < d; ++i) x[i] *= sc;
       }
-      for (int i = 0; i < d; ++i) Z[i * 32 + j] = x[i];
+      for (int i = 0; i < d; ++i) Z[i * ZW + j] = x[i];
     }
     __syncthreads();
   }
   if (__syncthreads_or(bad)) return 1;
-  // ---- 3b. modified Gram-Schmidt, twice, over the columns of Z (want <= 32)
-  double* cf = Mx + TD_SCROFF;  // coefficients
+  // ---- 3b. modified Gram-Schmidt, twice, over the columns of Z (want <= ZW)
+  double* cf = scr;  // coefficients
   for (int j = 0; j < want; ++j) {
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = warp; i < j; i += nw) {
         double s = 0.0;
-        for (int r = lane; r < d; r += 32) s += Z[r * 32 + i] * Z[r * 32 + j];
+        for (int r = lane; r < d; r += 32) s += Z[r * ZW + i] * Z[r * ZW + j];
         s = warp_sum(s);
         if (lane == 0) cf[i] = s;
       }
       __syncthreads();
       for (int r = tid; r < d; r += blockDim.x) {
-        double z = Z[r * 32 + j];
-        for (int i = 0; i < j; ++i) z -= cf[i] * Z[r * 32 + i];
-        Z[r * 32 + j] = z;
+        double z = Z[r * ZW + j];
+        for (int i = 0; i < j; ++i) z -= cf[i] * Z[r * ZW + i];
+        Z[r * ZW + j] = z;
       }
       __syncthreads();
     }
     double n2 = 0.0;
     if (warp == 0) {
-      for (int r = lane; r < d; r += 32) n2 += Z[r * 32 + j] * Z[r * 32 + j];
+      for (int r = lane; r < d; r += 32) n2 += Z[r * ZW + j] * Z[r * ZW + j];
       n2 = warp_sum(n2);
-      if (lane == 0) cf[32] = n2;
+      if (lane == 0) cf[ZW] = n2;
     }
     __syncthreads();
-    n2 = cf[32];
+    n2 = cf[ZW];
     if (!(n2 > 0.0) || !isfinite(n2)) return 1;  // (uniform)
     const double sc = 1.0 / sqrt(n2);
-    for (int r = tid; r < d; r += blockDim.x) Z[r * 32 + j] *= sc;
+    for (int r = tid; r < d; r += blockDim.x) Z[r * ZW + j] *= sc;
     __syncthreads();
   }
-  // ---- 3c. Rayleigh-Ritz in span(Z): H = Z^T T Z (want x want), Jacobi, Z <- Z U sorted
+  // ---- 3c. Rayleigh-Ritz in span(Z): H = Z^T T Z (T Z formed on the fly), Jacobi, Z <- Z U
   {
-    double* Y = Mx + TD_SCROFF;       // T Z (d x 32)
-    double* H = Y + 96 * 32;          // want x 33
-    double* U = H + 32 * 33;          // want x 33
-    for (int t = tid; t < d * want; t += blockDim.x) {
-      const int r = t / want, j = t % want;
-      double y = dg[r] * Z[r * 32 + j];
-      if (r > 0) y += e[r - 1] * Z[(r - 1) * 32 + j];
-      if (r < d - 1) y += e[r] * Z[(r + 1) * 32 + j];
-      Y[r * 32 + j] = y;
-    }
-    __syncthreads();
     for (int t = tid; t < want * want; t += blockDim.x) {
       const int a = t / want, b = t % want;
       if (b < a) continue;
-      double h = 0.0;
-      for (int r = 0; r < d; ++r) h += Z[r * 32 + a] * Y[r * 32 + b];
-      double h2 = 0.0;
-      for (int r = 0; r < d; ++r) h2 += Z[r * 32 + b] * Y[r * 32 + a];
+      double h = 0.0, h2 = 0.0;
+      for (int r = 0; r < d; ++r) {
+        double tb = dg[r] * Z[r * ZW + b], ta = dg[r] * Z[r * ZW + a];
+        if (r > 0) {
+          tb += e[r - 1] * Z[(r - 1) * ZW + b];
+          ta += e[r - 1] * Z[(r - 1) * ZW + a];
+        }
+        if (r < d - 1) {
+          tb += e[r] * Z[(r + 1) * ZW + b];
+          ta += e[r] * Z[(r + 1) * ZW + a];
+        }
+        h += Z[r * ZW + a] * tb;
+        h2 += Z[r * ZW + b] * ta;
+      }
       h = 0.5 * (h + h2);
-      H[a * 33 + b] = h;
-      H[b * 33 + a] = h;
+      H[a * HL + b] = h;
+      H[b * HL + a] = h;
     }
     __syncthreads();
-    smem_jacobi<double>(H, 33, U, 33, want, true, S);  // (uses rc/rs/pp/pq: dg is dead now)
+    smem_jacobi<double>(H, HL, U, HL, want, true, S);  // (uses rc/rs/pp/pq: dg is dead now)
     __syncthreads();
     for (int i = tid; i < want; i += blockDim.x) {
-      const double vi = H[i * 33 + i];
+      const double vi = H[i * HL + i];
       int rk = 0;
       for (int k2 = 0; k2 < want; ++k2) {
-        const double u = H[k2 * 33 + k2];
+        const double u = H[k2 * HL + k2];
         rk += (u < vi) || (u == vi && k2 < i);
       }
       S.ord[rk] = i;
     }
     __syncthreads();
-    // Z U (sorted) -> Y, then back into Z
-    for (int t = tid; t < d * want; t += blockDim.x) {
-      const int r = t / want, j = t % want, c = S.ord[j];
-      double z = 0.0;
-      for (int k2 = 0; k2 < want; ++k2) z += Z[r * 32 + k2] * U[k2 * 33 + c];
-      Y[r * 32 + j] = z;
-    }
-    for (int j = tid; j < want; j += blockDim.x) S.ev[j] = H[S.ord[j] * 33 + S.ord[j]];  // (lam overlaps U)
-    __syncthreads();
-    for (int t = tid; t < d * want; t += blockDim.x) {
-      const int r = t / want, j = t % want;
-      Z[r * 32 + j] = Y[r * 32 + j];
+    for (int j = tid; j < want; j += blockDim.x) S.ev[j] = H[S.ord[j] * HL + S.ord[j]];
+    // Z <- Z U[:, ord] in place, a warp per row (the row in registers first)
+    for (int r = warp; r < d; r += nw) {
+      double zr[ZW / 32];
+#pragma unroll
+      for (int c = 0; c < ZW / 32; ++c) zr[c] = c * 32 + lane < want ? Z[r * ZW + c * 32 + lane] : 0.0;
+      double out[ZW / 32];
+#pragma unroll
+      for (int c = 0; c < ZW / 32; ++c) out[c] = 0.0;
+      for (int k2 = 0; k2 < want; ++k2) {
+        const double zk = __shfl_sync(0xffffffffu, zr[k2 / 32], k2 & 31);
+#pragma unroll
+        for (int c = 0; c < ZW / 32; ++c) {
+          const int j = c * 32 + lane;
+          if (j < want) out[c] = fma(zk, U[k2 * HL + S.ord[j]], out[c]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < ZW / 32; ++c)
+        if (c * 32 + lane < want) Z[r * ZW + c * 32 + lane] = out[c];
     }
     __syncthreads();
   }
@@ -864,16 +874,16 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Mx, PSmem<dou
       const int m = d - k - 1;
       const double* wk = A + k * la + k + 1;
       double dot = 0.0;
-      for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * 32 + j];
+      for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * ZW + j];
       dot = warp_sum(dot);
-      for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * 32 + j] -= wk[i] * dot;
+      for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * ZW + j] -= wk[i] * dot;
       __syncwarp();
     }
   }
   __syncthreads();
   // eigenvectors -> A[:, 0:want], eigenvalues -> ev[0:want] (ascending), ord = identity
   for (int i = warp; i < d; i += nw)
-    for (int j = lane; j < want; j += 32) A[i * la + j] = Z[i * 32 + j];
+    for (int j = lane; j < want; j += 32) A[i * la + j] = Z[i * ZW + j];
   for (int j = tid; j < want; j += blockDim.x) S.ord[j] = j;  // ev set by the Rayleigh-Ritz step
   __syncthreads();
   return 0;
@@ -944,6 +954,25 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   // the rebuilt eigenvector columns go to the same region / the dead A
   double* const pkbuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(B);
   double* const ebuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(A);
+  if constexpr (std::is_same<T, double>::value) {
+    if (td && want <= td_zw<PD>() && d >= 4) {
+      // tridiagonal route: eigenvectors land in A[:, 0:want], ev/ord set (see tridiag_eig)
+      constexpr int ZW = td_zw<PD>(), HL = ZW + 1;
+      double* Bd = reinterpret_cast<double*>(B);
+      // Z, H, U in shared memory: the dead B (shared variant) or the packed-triangle region
+      // (large variant); inverse-iteration scratch aliases H / U there, or lives in B (global)
+      double* Z = kOwnPk<T, PD> ? S.pk : Bd;
+      double* H = Z + PD * ZW;
+      double* U = H + ZW * HL;
+      double* scr = kOwnPk<T, PD> ? Bd : H;
+      double* v = scr + TD_BATCH * 4 * PD;
+      static_assert(kOwnPk<T, PD> || PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1), "td scratch");
+      if (tridiag_eig<PD>(reinterpret_cast<double*>(A), PLD, d, want, Z, H, U, scr, v, S) != 0) return 2;
+      smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
+      __syncthreads();
+      return 0;
+    }
+  }
   if constexpr (PACKED) {
     for (int a = threadIdx.x; a < d; a += blockDim.x) S.ro[a] = a * (2 * d - a + 1) / 2 - a;
     __syncthreads();
@@ -954,15 +983,6 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
     sweeps = packed_jacobi(d, reinterpret_cast<PSmem<double>&>(S));
     for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = pkbuf[S.ro[i] + i];
   } else {
-    if constexpr (std::is_same<T, double>::value) {
-      if (td && want <= TD_MAXWANT && d >= 4 && PD <= 96) {
-        // tridiagonal route: eigenvectors land in A[:, 0:want], ev/ord set (see tridiag_eig)
-        if (tridiag_eig<PD>(A, PLD, d, want, B, S) != 0) return 2;
-        smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
-        __syncthreads();
-        return 0;
-      }
-    }
     smem_jacobi(A, PLD, B, PLD, d, true, S);  // V in B
     for (int i = threadIdx.x; i < d; i += blockDim.x) S.ev[i] = rl(A[i * PLD + i]);
   }
@@ -1219,7 +1239,8 @@ static int p_smem_bytes() {
   constexpr int PLD = PD + 1;
   int b = ((GMEM ? 0 : 3 * PD * PLD) + PD / 2) * (int)sizeof(T) + (3 * PD + PD + 32) * (int)sizeof(double) +
           (2 * PD + PD + 8 + ((PD + 3) & ~3)) * (int)sizeof(int);
-  if (kOwnPk<T, PD>) b += PD * (PD + 1) / 2 * (int)sizeof(double);
+  // the packed-triangle region (large real variant) also holds the tridiagonal route's Z, H, U
+  if (kOwnPk<T, PD>) b += max(PD * (PD + 1) / 2, PD * td_zw<PD>() + 2 * td_zw<PD>() * (td_zw<PD>() + 1)) * (int)sizeof(double);
   return b;
 }
 
