@@ -868,16 +868,47 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     }
     __syncthreads();
   }
-  // ---- 4. back-transformation Z <- H_0 ... H_{d-3} Z (warp per column, reflectors read-only)
-  for (int j = warp; j < want; j += nw) {
+  // ---- 4. back-transformation Z <- H_0 ... H_{d-3} Z: a warp owns columns warp + c nw, all of
+  //    them updated in one pass over each reflector (read once; no block barriers)
+  {
+    constexpr int CPW = (ZW + 15) / 16;  // columns per warp at 16 warps
     for (int k = d - 3; k >= 0; --k) {
       const int m = d - k - 1;
       const double* wk = A + k * la + k + 1;
-      double dot = 0.0;
-      for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * ZW + j];
-      dot = warp_sum(dot);
-      for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * ZW + j] -= wk[i] * dot;
+      double dot[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) dot[c] = 0.0;
+      for (int i = lane; i < m; i += 32) {
+        const double w = wk[i];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          const int j = warp + c * nw;
+          if (j < want) dot[c] += w * Z[(k + 1 + i) * ZW + j];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) dot[c] = warp_sum(dot[c]);
+      for (int i = lane; i < m; i += 32) {
+        const double w = wk[i];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          const int j = warp + c * nw;
+          if (j < want) Z[(k + 1 + i) * ZW + j] -= w * dot[c];
+        }
+      }
       __syncwarp();
+    }
+    // columns beyond CPW * nw (fewer warps than 16): one at a time
+    for (int j = warp + CPW * nw; j < want; j += nw) {
+      for (int k = d - 3; k >= 0; --k) {
+        const int m = d - k - 1;
+        const double* wk = A + k * la + k + 1;
+        double dot = 0.0;
+        for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * ZW + j];
+        dot = warp_sum(dot);
+        for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * ZW + j] -= wk[i] * dot;
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
