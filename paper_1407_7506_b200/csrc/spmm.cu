@@ -380,6 +380,7 @@ struct MarchArgs {
   int xlo;             // first plane the X tensor map covers
   int gy, gz, nslices, xseg, nunits;
   int m, off;          // columns, and leading columns of the slices before column 0 (alignment)
+  int npieces;         // 16-byte pieces of a row from the slices' origin to the block's end
   int vdoubles;        // ELL value row in doubles (real: even width; complex: 2 x width)
   int woff;            // ELL offset row in uint16 (multiple of 8)
   int width;           // ELL entries per row
@@ -551,7 +552,9 @@ __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_c
       const int kx = k + (x - U.xa);  // load index of plane x - 1
       const int s0 = kx % NS, s1 = (kx + 1) % NS, s2 = (kx + 2) % NS;
       mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
-      if (act) {
+      // rows whose pieces all lie past the block (the last slice) skip the work
+      const int pc = U.s * (COLS / 2) + g;
+      if (act && pc < A.npieces) {
         const unsigned char* b2 = msm + (size_t)s2 * A.slot_bytes;
         double2 acc[M_NP];
 #pragma unroll
@@ -563,7 +566,6 @@ __global__ void __launch_bounds__(M_THREADS, 1) spmm_march_kernel(const __grid_c
                               reinterpret_cast<const double*>(msm + (size_t)s1 * A.slot_bytes),
                               reinterpret_cast<const double*>(b2), hb, acc);
         double* yr = A.Y + row * A.ldy;
-        const int pc = U.s * (COLS / 2) + g;
 #pragma unroll
         for (int k2 = 0; k2 < M_NP; ++k2) march_store<CPLX>(A, yr, pc + 8 * k2, acc[k2]);
       }
@@ -679,6 +681,7 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   A.gy = (ny + M_T - 1) / M_T;
   A.gz = (nz + M_T - 1) / M_T;
   A.nslices = (int)((cols + COLS - 1) / COLS);
+  A.npieces = (int)((cols + 1) / 2);
   // x segments: >= 8 units per CTA (balance) while a segment keeps >= 8 planes
   const int64_t per_seg = (int64_t)A.gy * A.gz * A.nslices;
   // x segments: minimise waves x (planes per segment + 2 halo planes); units of one wave run

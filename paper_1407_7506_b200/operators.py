@@ -239,11 +239,15 @@ class DeviceCsr:
         self.val = torch.from_numpy(vals).cuda()
         self.diag = np.real(csr.diagonal())
         self.ncols = csr.shape[1]
-        self.stencil = _device_stencil_plan(self) if DeviceCsr.use_stencil else None
+        # small operators (config 1: n = 4096) stay on the gather: the march pipeline does not pay
+        # at that size, and the plan's first torch ops would dominate a sub-second solve
+        self.stencil = (_device_stencil_plan(self)
+                        if DeviceCsr.use_stencil and self.n >= DeviceCsr.min_stencil_rows else None)
 
     # plane-marching stencil kernel when the CSR is a nearest-neighbour stencil on an inferred
     # grid (spmm_plan.py); the whole-row gather otherwise
     use_stencil = True
+    min_stencil_rows = 1 << 15
 
     def apply_into(self, x, y):
         from . import kernels
