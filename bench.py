@@ -304,8 +304,13 @@ def run_ours(args):
         ppcg_solve(a2, t2, opts=warm_opts)
     # three timed calls, each on fresh host inputs (operator, preconditioner, X0 draw); the
     # median is reported (host-side jitter of the X0 draw / downloads is ~10%)
+    import gc
+
     e2e_runs = []
+    rep = None
     for _ in range(3):
+        rep = None  # the previous call's report (its host vectors) is freed outside the timed region
+        gc.collect()
         a2 = SparseHermitian(a._csr.copy(), "symmetric")
         t2 = jacobi_preconditioner(a2)
         torch.cuda.synchronize()
