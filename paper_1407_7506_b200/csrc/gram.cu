@@ -545,6 +545,10 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
   }
   __syncthreads();
 
+  // a diagonal tile of a symmetric Gram (X == Y, m0 == n0): both operands are the same rows and
+  // columns, so only the X stage is copied and the MMA warps read Y fragments from it
+  const bool same = BM == BN && g.symmetric && m0 == n0;
+
   if (warp == NCW) {  // ---- producer warp: lane = (operand, row); pieces held in registers
     const int r = lane & 15;
     const bool xop = lane < 16;
@@ -558,7 +562,8 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) by += i < py.n ? py.len[i] : 0;
     if (!xop) pc = py;
-    const uint32_t stage_row_bytes = (uint32_t)(bx + by) * 8;
+    const uint32_t stage_row_bytes = (uint32_t)(bx + (same ? 0 : by)) * 8;
+    const bool copies = xop || !same;
     double* dbase = xop ? Xs + r * LDX : Ys + r * LDY;
     const int dstage = xop ? C::XSTAGE : C::YSTAGE;
     const double* src0 = pc.src[0] + (r_begin + r) * pc.ld;
@@ -571,14 +576,14 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
       const int64_t rb = r_begin + (int64_t)s * G_BK;
       const int nvalid = (int)lmin(G_BK, r_end - rb);
       double* dst = dbase + st * dstage;
-      if (r >= nvalid) {  // partial last stage: zero rows (generic stores, before the arrive)
+      if (copies && r >= nvalid) {  // partial last stage: zero rows (generic stores, before the arrive)
         const int ld = xop ? LDX : LDY;
         for (int c = 0; c < ld; ++c) dst[c] = 0.0;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(full + st, (uint32_t)nvalid * stage_row_bytes);
       __syncwarp();
-      if (r < nvalid) {
+      if (copies && r < nvalid) {
         const int64_t o = (int64_t)s * sstep;
         bulk_g2s(dst + pc.soff[0], src0 + o, pc.len[0] * 8, full + st);
         if (pc.n > 1) bulk_g2s(dst + pc.soff[1], src1 + o, pc.len[1] * 8, full + st);
@@ -612,7 +617,7 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
     mbar_wait(full + st, (s / ST) & 1);
     if (warp_active) {
       const double* xs = Xs + st * C::XSTAGE + xoff;
-      const double* ys = Ys + st * C::YSTAGE + yoff;
+      const double* ys = (same ? Xs : Ys) + st * C::YSTAGE + yoff;  // (BM == BN: same stage shape)
       double af[2][WM], bf[2][WN];
 #pragma unroll
       for (int a = 0; a < WM; ++a) af[0][a] = lds64(xs + a * 8);
