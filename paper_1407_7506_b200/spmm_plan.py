@@ -3,10 +3,11 @@
 A row gather reads each X row once per nonzero that references it (7x for a 7-point
 stencil, 27x for a 27-point one).  Even at full memory-level parallelism that traffic runs
 into the L2 throughput cap long before HBM (profiles/spmm_sweep_r01.jsonl).  The march
-kernel instead stages X tiles in shared memory and reuses them: a CTA owns an 8 x 8 tile of
-a grid plane and a 256-byte column slice and marches along the slowest grid axis, keeping
-planes x-1, x, x+1 of the tile (with its one-row y/z halo) in a 4-slot ring.  Every X row
-is then read ~(10 x 10)/(8 x 8) = 1.56 times instead of 7 or 27 times.
+kernel instead stages X tiles in shared memory and reuses them: a work unit is an 8 x 8 tile
+of a grid plane and a column slice (512 bytes for real rows of <= 8 entries, else 256), and it
+marches along the slowest grid axis, keeping planes x-1, x, x+1 of the tile (with its one-row
+y/z halo) in a 4-6 slot ring fed by TMA.  Every X row is then read ~(10 x 10)/(8 x 8) = 1.56
+times instead of 7 or 27 times.
 
 The kernel computes from the CSR values in CSR order (so the result equals the gather's bit
 for bit), re-laid out as a grid-ordered ELL (each row's entries contiguous, padded to the
@@ -21,7 +22,7 @@ from the CSR alone, so the reference's own ``SparseHermitian`` objects qualify:
 * decoding row and column to grid coordinates must give ``|dx|, |dy|, |dz| <= 1`` for
   every nonzero (this rejects periodic wrap-around, which would need a wider halo).
 
-Anything else keeps the gather kernels.
+Anything else keeps the gather kernels; so do operators under 32,768 rows (operators.py).
 """
 
 from __future__ import annotations
