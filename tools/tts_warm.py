@@ -6,7 +6,6 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1407_7506_b200 import SolverOptions, ppcg_solve  # noqa: E402
