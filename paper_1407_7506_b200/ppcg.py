@@ -34,7 +34,7 @@ __all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSo
 
 # host-sync trimming (bit 0: projections queued before the metric is read; bit 1: the
 # orthonormality Gram queued before the update's flags are read); PPCG_SPECULATE overrides
-_SPECULATE = int(os.environ.get("PPCG_SPECULATE", "3"))
+_SPECULATE = int(os.environ.get("PPCG_SPECULATE", "7"))
 _COEFF_REFRESH = 100.0   # ppcg.py:41
 _BREAKDOWN_MAX = 1e8     # ppcg.py:705
 _TAYLOR_OK = 0.1         # core.py:127
@@ -384,17 +384,29 @@ class PPCGSolver:
         K = self.K
         L, ka = self.L, self.kt - self.L
         R = self.Rm[:ka, :ka]
-        R.copy_(gram_act)
-        self.dense.chol_upper_floor(R, self.iflags[0:1])
+        spec = self._spec_R == L and gram_act.data_ptr() == self.Gfull[L:, L:].data_ptr()
+        self._spec_R = None
+        if not spec:
+            self._cholqr_factor(gram_act)
         self._fetch((self.iflags, self.h_iflags))
         col = int(self.h_iflags[0])
         if col >= 0:
             raise RankDeficiencyError(col)
-        self.dense.tri_inv_upper(R)
         src, dst = x_src_idx, 1 - x_src_idx
         K.tsgemm([self.XF[src][:, L:], self.AXF[src][:, L:]], [R, R],
                  [self.XF[dst][:, L:], self.AXF[dst][:, L:]], upper=True)
         self.xi = dst
+
+    _spec_R = None  # L of a CholQR factor already queued from Gfull (step)
+
+    def _cholqr_factor(self, gram_act):
+        """R^{-1} (upper) of the Gram with _cholesky_upper's pivot floor (core.py:67-83); the
+        failing column (or -1) goes to iflags[0] -- read by the caller."""
+        ka = gram_act.shape[0]
+        R = self.Rm[:ka, :ka]
+        R.copy_(gram_act)
+        self.dense.chol_upper_floor(R, self.iflags[0:1])
+        self.dense.tri_inv_upper(R)  # garbage when the factor failed; never used then
 
     def _taylor_swap(self, gram_act):
         """Taylor-polar correction X <- X p(G - I) (core.py:106-124, ppcg.py:477-481)."""
@@ -674,10 +686,19 @@ class PPCGSolver:
         # host reads the update's flags so one sync serves both; a breakdown (rare) restores
         # the previous X and leaves this Gram unused, a coefficient refresh keeps X
         early = bool(_SPECULATE & 2)
+        self._spec_R = None
         if early:
             K.gram(self.XF[dst], self.XF[dst], self.Gfull, symmetric=True)
             self._red(self.Gfull)
             K.small_stats(self.Gfull, self.stats[8:11])
+            # the CholQR factor of the coming orthonormalisation (ppcg.py:483-484) depends only on
+            # this Gram: factor and invert it before the host reads the flags, so the GPU is not
+            # idle across two host round trips (unused when the iteration ends otherwise)
+            rr_now = math.isfinite(o.rr_period) and it % int(o.rr_period) == 0
+            if (_SPECULATE & 4 and not rr_now and o.orth_scheme == "cholesky-qr"
+                    and o.orth_policy in ("every", "adaptive", "periodic")):
+                self._cholqr_factor(self.Gfull[L:, L:])
+                self._spec_R = L
         self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
                     (self.stats, self.h_stats))
         s = self.h_stats.numpy()
