@@ -24,6 +24,7 @@
 //    so the result is exactly symmetric.
 //  * row strides of BM+4 / BN+4 (= 4 mod 16 doubles) make the half-warp fragment loads
 //    (4 rows x 4 doubles) conflict-free.
+#include <cuda.h>
 #include "common.cuh"
 
 namespace bk {
@@ -493,14 +494,45 @@ BK_DEV void tile_pieces(const GramProblem& g, bool xop, int c0, int B, int wp, P
 
 // CTA body of the bulk-loader Gram for block `bid` of problem set P (gram_bulk_kernel runs one
 // set; gram_bulk_combo runs a main-block set and a strip set interleaved by chunk)
-template <class C>
-BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
+// TMA subblock variant (TMA = true, subblock mode with q <= 32, 3 segments): each segment of a
+// stage arrives as two 16 x 16 boxes (128-byte rows, 128-byte swizzle) of a 2-D tensor map
+// over its block -- 12 copies per stage instead of 96 row copies of 256 bytes, which kept the
+// MMA warps waiting on the single producer warp.  Segment s occupies tile columns
+// [32 s, 32 s + 32); element (row k, tile column p) of a stage sits at
+//   (p >> 4) * 256 + k * 16 + (((p >> 1) & 7) ^ (k & 7)) * 2 + (p & 1).
+// The 4-row k slices of the DMMA fragments take rows {0,4,1,5}, {2,6,3,7}, {8,12,9,13},
+// {10,14,11,15}: under the swizzle the two row pairs of a slice hit disjoint bank halves, so
+// a fragment load is two wavefronts (conflict-free).  The k order inside a stage only permutes
+// the summation of the Gram.
+constexpr int SB_TMA_BOX = 16 * 16;      // doubles per box
+constexpr int SB_TMA_STAGE = 6 * SB_TMA_BOX;  // 3 segments x 2 boxes per operand stage
+struct SbMaps {
+  CUtensorMap m[6];  // X, W, P, AX, AW, AP: dims (ld, n), box (16, 16), 128-byte swizzle
+};
+
+BK_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+BK_DEV int sb_tma_row(int kq, int fr) { return (kq >> 1) * 8 + (kq & 1) * 2 + (fr & 1) * 4 + (fr >> 1); }
+
+template <class C, bool TMA = false>
+BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* maps = nullptr) {
   constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN, ST = C::STAGES;
   constexpr int NCW = C::THREADS / 32;  // MMA warps
-  extern __shared__ __align__(16) double smem[];
+  constexpr int XSTG = TMA ? SB_TMA_STAGE : C::XSTAGE, YSTG = TMA ? SB_TMA_STAGE : C::YSTAGE;
+  static_assert(!TMA || (BM == 96 && BN == 96), "TMA subblock variant: one 96 x 96 tile");
+  extern __shared__ __align__(16) double smem_raw[];
+  // 128-byte swizzled boxes need 1024-byte aligned destinations (1 KB of slack allocated)
+  double* smem = TMA ? reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                     : smem_raw;
   double* Xs = smem;                    // [STAGES][BK][LDX]
-  double* Ys = smem + ST * C::XSTAGE;   // [STAGES][BK][LDY]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ys + ST * C::YSTAGE);
+  double* Ys = smem + ST * XSTG;        // [STAGES][BK][LDY]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ys + ST * YSTG);
   uint64_t* empty = full + ST;
   __shared__ int s_last;
 
@@ -521,7 +553,7 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
   } else {
     subblock_problem<BM, BN>(P, pidx, g);
     w = g.xs[0].width;
-    wp = (w + 1) & ~1;
+    wp = TMA ? 32 : (w + 1) & ~1;
     Mp = Np = g.nxs * wp;
     g.tiles_m = (Mp + BM - 1) / BM;
     g.tiles_n = (Np + BN - 1) / BN;
@@ -549,7 +581,26 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
   // columns, so only the X stage is copied and the MMA warps read Y fragments from it
   const bool same = BM == BN && g.symmetric && m0 == n0;
 
-  if (warp == NCW) {  // ---- producer warp: lane = (operand, row); pieces held in registers
+  if (TMA && warp == NCW) {  // ---- producer (TMA): one lane, 6 or 12 boxes per stage
+    if (lane == 0) {
+      const int kind = pidx & 1, col = (int)(P.sc0 + (int64_t)(pidx >> 1) * P.q);
+      const uint32_t bytes = (same ? 6u : 12u) * SB_TMA_BOX * 8u;
+      for (int s = 0; s < nstages; ++s) {
+        const int st = s % ST;
+        if (s >= ST) mbar_wait(empty + st, ((s / ST) - 1) & 1);
+        const int rb = (int)(r_begin + (int64_t)s * G_BK);
+        mbar_arrive_expect_tx(full + st, bytes);
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          const int sg = b >> 1, c = col + (b & 1) * 16;
+          tma_load_2d(Xs + st * XSTG + b * SB_TMA_BOX, maps + sg, c, rb, full + st);
+          if (!same) tma_load_2d(Ys + st * YSTG + b * SB_TMA_BOX, maps + (kind ? sg : 3 + sg), c, rb, full + st);
+        }
+      }
+    }
+    return;
+  }
+  if (!TMA && warp == NCW) {  // ---- producer warp: lane = (operand, row); pieces held in registers
     const int r = lane & 15;
     const bool xop = lane < 16;
     Pieces pc;
@@ -612,9 +663,42 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid) {
 
   const int fr = lane & 3, fc = lane >> 2;
   const int xoff = fr * LDX + wm * 8 * WM + fc + shx, yoff = fr * LDY + wn * 8 * WN + fc + shy;
+  // TMA layout: the warp's first fragment column starts a box (8 WM, 8 WN multiples of 16), so a
+  // fragment's box is (first box) + a / 2 and its 16-byte chunk ((a & 1) << 2 | fc >> 1)
+  static_assert(!TMA || ((8 * WM) % 16 == 0 && (8 * WN) % 16 == 0), "warp tiles start on boxes");
+  const int tbx = (wm * 8 * WM >> 4) * SB_TMA_BOX + (fc & 1), tby = (wn * 8 * WN >> 4) * SB_TMA_BOX + (fc & 1);
   for (int s = 0; s < nstages; ++s) {
     const int st = s % ST;
     mbar_wait(full + st, (s / ST) & 1);
+    if constexpr (TMA) {
+      if (warp_active) {
+        const double* xs = Xs + st * XSTG;
+        const double* ys = (same ? Xs : Ys) + st * YSTG;
+        double af[2][WM], bf[2][WN];
+        auto load = [&](int kq, double* fa, double* fb) {
+          const int k = sb_tma_row(kq, fr), t = ((fc >> 1) ^ k) & 7;
+          const double* xr = xs + tbx + k * 16;
+          const double* yr = ys + tby + k * 16;
+#pragma unroll
+          for (int a = 0; a < WM; ++a) fa[a] = lds64(xr + (a >> 1) * SB_TMA_BOX + ((t ^ ((a & 1) << 2)) << 1));
+#pragma unroll
+          for (int b = 0; b < WN; ++b) fb[b] = lds64(yr + (b >> 1) * SB_TMA_BOX + ((t ^ ((b & 1) << 2)) << 1));
+        };
+        load(0, af[0], bf[0]);
+#pragma unroll
+        for (int kq = 0; kq < G_BK / 4; ++kq) {
+          const int cur = kq & 1;
+          if (kq + 1 < G_BK / 4) load(kq + 1, af[cur ^ 1], bf[cur ^ 1]);
+#pragma unroll
+          for (int a = 0; a < WM; ++a)
+#pragma unroll
+            for (int b = 0; b < WN; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[cur][a], bf[cur][b]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      continue;
+    }
     if (warp_active) {
       const double* xs = Xs + st * C::XSTAGE + xoff;
       const double* ys = (same ? Xs : Ys) + st * C::YSTAGE + yoff;  // (BM == BN: same stage shape)
@@ -692,6 +776,12 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) gram_bulk_kernel(con
   gram_bulk_body<C>(P, blockIdx.x);
 }
 
+template <class C>
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
+    gram_sb_tma_kernel(const __grid_constant__ GramParams P, const __grid_constant__ SbMaps M) {
+  gram_bulk_body<C, true>(P, blockIdx.x, M.m);
+}
+
 // Main block (CA tiles) and strips (CB tiles) of split Grams in ONE launch, both chunk-major
 // with the same row chunks: the CTAs of chunk c of both sets are adjacent, so the strip CTAs
 // read the chunk's X / Y rows while the main tiles hold them in L2 -- the separate strip launch
@@ -761,7 +851,8 @@ static int64_t ws_bytes_for(int64_t nrows, int64_t tiles) {
 }
 
 template <class C>
-static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, int64_t ws_bytes, cudaStream_t st) {
+static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, int64_t ws_bytes, cudaStream_t st,
+                           const SbMaps* maps = nullptr) {
   static const int fast_on = [] {
     const char* e = getenv("PPCG_GRAM_FAST");
     return e ? atoi(e) : 1;
@@ -792,6 +883,17 @@ static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, i
     attr = true;
   }
   BK_COUNT();
+  if constexpr (C::BM == 96 && C::BN == 96) if (maps) {
+    constexpr int tsmem = C::STAGES * 2 * SB_TMA_STAGE * (int)sizeof(double) + 16 * C::STAGES + 1024;
+    static bool tattr = false;
+    if (!tattr) {
+      cudaFuncSetAttribute(gram_sb_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+      tattr = true;
+    }
+    gram_sb_tma_kernel<C><<<(unsigned)grid, C::THREADS + 32, tsmem, st>>>(P, *maps);
+    BK_CHECK_LAUNCH();
+    return BK_OK;
+  }
   if (P.bulk && g_bulk_loader)
     gram_bulk_kernel<C><<<(unsigned)grid, C::THREADS + 32, C::SMEM + 16 * C::STAGES, st>>>(P);
   else
@@ -1151,6 +1253,31 @@ extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int h
   return ws_bytes_for<Small>(n, (int64_t)2 * nb * t * t);
 }
 
+typedef CUresult (*SbEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D map over an n x ld row-major block: box 16 columns x 16 rows, 128-byte swizzle; rows past n
+// arrive zero-filled
+static bool encode_sb_map(CUtensorMap* map, const double* base, int64_t ld, int64_t n) {
+  static SbEncodeFn enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (SbEncodeFn) nullptr;
+    return reinterpret_cast<SbEncodeFn>(p);
+  }();
+  if (!enc || !base) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  const cuuint32_t box[2] = {16, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Per-subblock raw pencil Grams (ppcg.py:206-211 before unit scaling, ppcg.py:220-228):
 // for block j (columns c0 + [j*q, min((j+1)*q, k_act))), S_j = [X_j | W_j | P_j] and
 // A_j = S_j^T [AX_j | AW_j | AP_j], B_j = S_j^T S_j, each stored dmax x dmax (ld dmax).
@@ -1195,6 +1322,17 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
   }
   if (P.dmax > 64 && P.dmax <= 96) {
     P.max_tiles = 1;
+    // TMA boxes: 3 segments of <= 32 columns, 16-byte aligned bases and row strides
+    static const int sb_tma = [] {
+      const char* e = getenv("PPCG_GRAM_SBTMA");
+      return e ? atoi(e) : 1;
+    }();
+    if (sb_tma && P.has_p && q <= 32 && P.bulk && n < 0x7fffffff && c0 + (int64_t)k_act <= ld) {
+      SbMaps M;
+      bool ok = true;
+      for (int i = 0; i < 6 && ok; ++i) ok = encode_sb_map(&M.m[i], ptrs[i], ld, n);
+      if (ok) return launch_gram_cfg<Sb96>(P, (int64_t)P.nprob, ws, ws_bytes, (cudaStream_t)stream, &M);
+    }
     return launch_gram_cfg<Sb96>(P, (int64_t)P.nprob, ws, ws_bytes, (cudaStream_t)stream);
   }
   const int t = (P.dmax + 63) / 64;

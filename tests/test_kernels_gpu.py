@@ -248,8 +248,37 @@ def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
         assert abs(cs[j] - r.coeff_scale) <= 1e-8 * r.coeff_scale
 
 
+@pytest.mark.parametrize("n,m,q,c0,extra", [(5003, 109, 32, 2, 6), (4099, 96, 32, 0, 0), (777, 70, 24, 4, 2),
+                                            (20000, 40, 32, 6, 0)])
+def test_subblock_grams_raw(cuda, n, m, q, c0, extra):
+    """Raw pencil Grams A_j = S_j^T [AX AW AP]_j, B_j = S_j^T S_j (q <= 32 with P: the TMA-box
+    loader) against numpy, with column offsets, padded rows and a ragged last subblock."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    ld = c0 + m + extra
+    rng = np.random.default_rng(n + m)
+    host = [rng.standard_normal((n, ld)) for _ in range(6)]
+    bufs = [dev(h, torch) for h in host]
+    nb = (m + q - 1) // q
+    dmax = 3 * q
+    araw = torch.zeros(nb * dmax * dmax, dtype=torch.float64, device="cuda")
+    braw = torch.zeros_like(araw)
+    K.subblock_grams(n, m, q, True, *[b.data_ptr() for b in bufs], ld, c0, araw, braw)
+    A = araw.cpu().numpy().reshape(nb, dmax, dmax)
+    B = braw.cpu().numpy().reshape(nb, dmax, dmax)
+    for j in range(nb):
+        lo, hi = c0 + j * q, c0 + min(m, (j + 1) * q)
+        S = np.hstack([h[:, lo:hi] for h in host[:3]])
+        AS = np.hstack([h[:, lo:hi] for h in host[3:]])
+        d = S.shape[1]
+        ea, eb = S.T @ AS, S.T @ S
+        assert np.allclose(A[j, :d, :d], ea, atol=1e-11 * np.abs(ea).max(), rtol=0)
+        assert np.allclose(B[j, :d, :d], eb, atol=1e-11 * np.abs(eb).max(), rtol=0)
+
+
 @pytest.mark.parametrize("n,m,q,with_p", [(300, 6, 3, True), (400, 20, 8, True), (400, 20, 8, False),
-                                          (1500, 40, 32, True), (2500, 100, 64, True)])
+                                          (1500, 40, 32, True), (2500, 100, 64, True), (1200, 40, 16, True)])
 def test_complex_subblock_update_vs_oracle(cuda, n, m, q, with_p):
     """complex Hermitian subblock update: Grams of interleaved views, complex Jacobi pencils,
     expanded-coefficient recombination vs the oracle's block_update."""
