@@ -500,10 +500,11 @@ BK_DEV void tile_pieces(const GramProblem& g, bool xop, int c0, int B, int wp, P
 // MMA warps waiting on the single producer warp.  Segment s occupies tile columns
 // [32 s, 32 s + 32); element (row k, tile column p) of a stage sits at
 //   (p >> 4) * 256 + k * 16 + (((p >> 1) & 7) ^ (k & 7)) * 2 + (p & 1).
-// The 4-row k slices of the DMMA fragments take rows {0,4,1,5}, {2,6,3,7}, {8,12,9,13},
-// {10,14,11,15}: under the swizzle the two row pairs of a slice hit disjoint bank halves, so
-// a fragment load is two wavefronts (conflict-free).  The k order inside a stage only permutes
-// the summation of the Gram.
+// The 4-row k slices of the DMMA fragments take rows {0,2,4,6}, {1,3,5,7}, {8,..,14}, {9,..,15}:
+// a 64-bit fragment load is served per half-warp (4 rows x 4 columns = 2 chunks per row), and
+// under the swizzle rows 0, 2, 4, 6 put those chunk pairs in four disjoint 32-byte bank groups,
+// so each load is two conflict-free wavefronts (rows {0,4,1,5} measured 2-way conflicted).  The
+// k order inside a stage only permutes the summation of the Gram.
 constexpr int SB_TMA_BOX = 16 * 16;      // doubles per box
 constexpr int SB_TMA_STAGE = 6 * SB_TMA_BOX;  // 3 segments x 2 boxes per operand stage
 struct SbMaps {
@@ -518,7 +519,7 @@ BK_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint6
       : "memory");
 }
 
-BK_DEV int sb_tma_row(int kq, int fr) { return (kq >> 1) * 8 + (kq & 1) * 2 + (fr & 1) * 4 + (fr >> 1); }
+BK_DEV int sb_tma_row(int kq, int fr) { return (kq >> 1) * 8 + (kq & 1) + fr * 2; }
 
 template <class C, bool TMA = false>
 BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* maps = nullptr) {
