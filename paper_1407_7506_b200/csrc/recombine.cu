@@ -57,8 +57,8 @@ __global__ void k_expand_coef(int k_act, int q, int nparts, const double* __rest
 // fragment loads conflict-free.
 constexpr int R_KC = 16, R_STAGES = 3, R_LA = R_KC + 4;
 
-template <int NT>
-__global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_constant__ RecombParams P) {
+template <int NT, int MINB = 1>
+__global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid_constant__ RecombParams P) {
   constexpr int LB = NT + 4, WN = NT / 8;
   constexpr int IN_STAGE = R_BM * R_LA, CF_STAGE = R_KC * LB;
   extern __shared__ __align__(16) double sm[];
@@ -202,15 +202,28 @@ __global__ void __launch_bounds__(R_THREADS) recombine_kernel(const __grid_const
   }
 }
 
-template <int NT>
-static void launch_recombine(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
+template <int NT, int MINB>
+static void launch_recombine_m(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
   constexpr int smem = R_STAGES * (R_BM * R_LA + R_KC * (NT + 4)) * (int)sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(recombine_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(recombine_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  recombine_kernel<NT><<<dim3(nrt, nb, 2 * nct), R_THREADS, smem, st>>>(R);
+  recombine_kernel<NT, MINB><<<dim3(nrt, nb, 2 * nct), R_THREADS, smem, st>>>(R);
+}
+
+template <int NT>
+static void launch_recombine(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
+  // 5 CTAs per SM (94 registers, no spills): the short 6-chunk pipelines of a CTA need the
+  // extra resident CTAs to keep bytes in flight (config 2: 1.30 -> 1.25 ms); 6 spills
+  static const int minb = [] {
+    const char* e = getenv("PPCG_RECOMB_MINB");
+    return e ? atoi(e) : 5;
+  }();
+  if (minb == 5) launch_recombine_m<NT, 5>(R, nrt, nb, nct, st);
+  else if (minb == 6) launch_recombine_m<NT, 6>(R, nrt, nb, nct, st);
+  else launch_recombine_m<NT, 1>(R, nrt, nb, nct, st);
 }
 
 }  // namespace bk
