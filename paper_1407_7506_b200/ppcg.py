@@ -388,7 +388,7 @@ class PPCGSolver:
         self._spec_R = None
         if not spec:
             self._cholqr_factor(gram_act)
-        self._fetch((self.iflags, self.h_iflags))
+            self._fetch((self.iflags, self.h_iflags))  # (speculated: fetched with the step's flags)
         col = int(self.h_iflags[0])
         if col >= 0:
             raise RankDeficiencyError(col)
@@ -699,8 +699,11 @@ class PPCGSolver:
                     and o.orth_policy in ("every", "adaptive", "periodic")):
                 self._cholqr_factor(self.Gfull[L:, L:])
                 self._spec_R = L
-        self._fetch((self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
-                    (self.stats, self.h_stats))
+        fetch = [(self.info, self.h_info), (self.cscale, self.h_cscale), (self.flags64, self.h_flags64),
+                 (self.stats, self.h_stats)]
+        if self._spec_R is not None:
+            fetch.append((self.iflags, self.h_iflags))  # the speculated factor's pivot flag: same sync
+        self._fetch(*fetch)
         s = self.h_stats.numpy()
         wn = math.sqrt(max(s[4], 0.0))
         self.proj_defect.append(float(math.sqrt(max(s[5], 0.0)) / max(wn, 1e-300)))
@@ -716,6 +719,7 @@ class PPCGSolver:
         prev_idx, prev_pidx = src, psrc
         if broken:
             # ppcg.py:706-717: restore pre-update X, Householder QR, drop P
+            self._spec_R = None
             self.recoveries += 1
             self.orth_loss.append(math.inf)
             self.xi = prev_idx
