@@ -507,6 +507,7 @@ BK_DEV void tile_pieces(const GramProblem& g, bool xop, int c0, int B, int wp, P
 // k order inside a stage only permutes the summation of the Gram.
 constexpr int SB_TMA_BOX = 16 * 16;      // doubles per box
 constexpr int SB_TMA_STAGE = 6 * SB_TMA_BOX;  // 3 segments x 2 boxes per operand stage
+constexpr int SB_PAIR_STAGES = 8;
 struct SbMaps {
   CUtensorMap m[6];  // X, W, P, AX, AW, AP: dims (ld, n), box (16, 16), 128-byte swizzle
 };
@@ -521,10 +522,18 @@ BK_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint6
 
 BK_DEV int sb_tma_row(int kq, int fr) { return (kq >> 1) * 8 + (kq & 1) + fr * 2; }
 
-template <class C, bool TMA = false>
+// PAIR (TMA subblock mode only): one CTA computes both Grams of a subblock -- warps of group 0
+// S^T (AS), group 1 S^T S -- from one staged copy of S and AS per stage (2 operand loads per
+// stage for the two Grams instead of 3), one CTA per SM with an 8-deep ring.  13 warps put 4
+// on one SM sub-partition, whose 16K registers cap the kernel at 128 per thread.  Config 2:
+// 2.60 -> 2.28 ms for the 16 subblocks (PPCG_GRAM_SBPAIR=0: two CTAs, one per Gram).
+template <class C, bool TMA = false, bool PAIR = false>
 BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* maps = nullptr) {
-  constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN, ST = C::STAGES;
-  constexpr int NCW = C::THREADS / 32;  // MMA warps
+  static_assert(!PAIR || TMA, "pair mode loads through TMA boxes");
+  constexpr int BM = C::BM, BN = C::BN, LDX = C::LDX, LDY = C::LDY, WM = C::WM, WN = C::WN;
+  constexpr int ST = PAIR ? SB_PAIR_STAGES : C::STAGES;
+  constexpr int GW = C::THREADS / 32;          // MMA warps per group
+  constexpr int NCW = (PAIR ? 2 : 1) * GW;     // MMA warps
   constexpr int XSTG = TMA ? SB_TMA_STAGE : C::XSTAGE, YSTG = TMA ? SB_TMA_STAGE : C::YSTAGE;
   static_assert(!TMA || (BM == 96 && BN == 96), "TMA subblock variant: one 96 x 96 tile");
   extern __shared__ __align__(16) double smem_raw[];
@@ -535,14 +544,21 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* 
   double* Ys = smem + ST * XSTG;        // [STAGES][BK][LDY]
   uint64_t* full = reinterpret_cast<uint64_t*>(Ys + ST * YSTG);
   uint64_t* empty = full + ST;
-  __shared__ int s_last;
+  __shared__ int s_last_g[2];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = (PAIR && warp < NCW) ? warp / GW : 0;  // pair mode: Gram of this warp group
+  const int gwarp = warp - grp * GW, gtid = tid - grp * C::THREADS;
+  int& s_last = s_last_g[grp];
   // block order: tile fastest, then chunk, then problem; chunk_major: then problem, then chunk
-  const int slot = (int)(bid % P.max_tiles);
-  const int chunk = P.chunk_major ? (int)(bid / ((int64_t)P.max_tiles * P.nprob))
-                                  : (int)((bid / P.max_tiles) % P.nchunks);
-  const int pidx = P.chunk_major ? (int)((bid / P.max_tiles) % P.nprob) : (int)(bid / ((int64_t)P.max_tiles * P.nchunks));
+  // (pair mode: chunk fastest, then subblock; problem 2 j + group)
+  const int slot = PAIR ? 0 : (int)(bid % P.max_tiles);
+  const int chunk = PAIR ? (int)(bid % P.nchunks)
+                         : P.chunk_major ? (int)(bid / ((int64_t)P.max_tiles * P.nprob))
+                                         : (int)((bid / P.max_tiles) % P.nchunks);
+  const int pidx = PAIR ? (int)(2 * (bid / P.nchunks) + grp)
+                        : P.chunk_major ? (int)((bid / P.max_tiles) % P.nprob)
+                                        : (int)(bid / ((int64_t)P.max_tiles * P.nchunks));
 
   GramProblem g;
   int wp = 0, w = 0;  // padded segment stride (subblock mode) and real segment width
@@ -651,7 +667,7 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* 
     shx = (int)((reinterpret_cast<uintptr_t>(g.xs[0].p + g.xs[0].col0) >> 3) & 1);
     shy = (int)((reinterpret_cast<uintptr_t>(g.ys[0].p + g.ys[0].col0) >> 3) & 1);
   }
-  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int wm = gwarp / C::WARPS_N, wn = gwarp % C::WARPS_N;
   const int wm0 = m0 + wm * 8 * WM, wn0 = n0 + wn * 8 * WN;
   const bool below = g.symmetric && (wn0 + 8 * WN <= wm0);
   const bool warp_active = wm0 < Mp && wn0 < Np && !below;
@@ -685,11 +701,14 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* 
 #pragma unroll
           for (int b = 0; b < WN; ++b) fb[b] = lds64(yr + (b >> 1) * SB_TMA_BOX + ((t ^ ((b & 1) << 2)) << 1));
         };
-        load(0, af[0], bf[0]);
+        // pair mode (13 warps: 4 on one SM sub-partition, so <= 128 registers): no fragment
+        // double buffering -- the other MMA warps of the sub-partition cover the load latency
+        if (!PAIR) load(0, af[0], bf[0]);
 #pragma unroll
         for (int kq = 0; kq < G_BK / 4; ++kq) {
-          const int cur = kq & 1;
-          if (kq + 1 < G_BK / 4) load(kq + 1, af[cur ^ 1], bf[cur ^ 1]);
+          const int cur = PAIR ? 0 : kq & 1;
+          if (PAIR) load(kq, af[0], bf[0]);
+          else if (kq + 1 < G_BK / 4) load(kq + 1, af[cur ^ 1], bf[cur ^ 1]);
 #pragma unroll
           for (int a = 0; a < WM; ++a)
 #pragma unroll
@@ -758,18 +777,18 @@ BK_DEV void gram_bulk_body(const GramParams& P, int64_t bid, const CUtensorMap* 
       *reinterpret_cast<double2*>(part + (wm * 8 * WM + a * 8 + (lane >> 2)) * BN + wn * 8 * WN + b * 8 +
                                   2 * (lane & 3)) = make_double2(acc[a][b][0], acc[a][b][1]);
   __threadfence();
-  named_bar_sync(1, C::THREADS);
-  if (tid == 0) s_last = (atomicAdd(&P.tickets[tile_id], 1) == P.nchunks - 1);
-  named_bar_sync(1, C::THREADS);
+  named_bar_sync(1 + grp, C::THREADS);
+  if (gtid == 0) s_last = (atomicAdd(&P.tickets[tile_id], 1) == P.nchunks - 1);
+  named_bar_sync(1 + grp, C::THREADS);
   if (!s_last) return;
   __threadfence();
   const double* base = P.ws + tile_id * P.nchunks * (BM * BN);
-  for (int e = tid; e < BM * BN; e += C::THREADS) {
+  for (int e = gtid; e < BM * BN; e += C::THREADS) {
     double v = 0.0;
     for (int c = 0; c < P.nchunks; ++c) v += __ldcg(base + (int64_t)c * (BM * BN) + e);
     store_final(e / BN, e % BN, v);
   }
-  if (tid == 0) P.tickets[tile_id] = 0;
+  if (gtid == 0) P.tickets[tile_id] = 0;
 }
 
 template <class C>
@@ -781,6 +800,12 @@ template <class C>
 __global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
     gram_sb_tma_kernel(const __grid_constant__ GramParams P, const __grid_constant__ SbMaps M) {
   gram_bulk_body<C, true>(P, blockIdx.x, M.m);
+}
+
+template <class C>
+__global__ void __launch_bounds__(2 * C::THREADS + 32, 1)
+    gram_sb_pair_kernel(const __grid_constant__ GramParams P, const __grid_constant__ SbMaps M) {
+  gram_bulk_body<C, true, true>(P, blockIdx.x, M.m);
 }
 
 // Main block (CA tiles) and strips (CB tiles) of split Grams in ONE launch, both chunk-major
@@ -1254,6 +1279,35 @@ extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int h
   return ws_bytes_for<Small>(n, (int64_t)2 * nb * t * t);
 }
 
+// both Grams of each subblock in one CTA (gram_sb_pair_kernel): grid nb x chunks, one CTA per SM
+template <class C>
+static int launch_sb_pair(GramParams& P, int nb, void* ws, int64_t ws_bytes, cudaStream_t st, const SbMaps& M) {
+  P.nchunks = P.force_chunks > 0 ? P.force_chunks : choose_chunks(P.nrows, nb, 1);
+  auto part_bytes = [&] { return (int64_t)P.nprob * P.nchunks * C::BM * C::BN * (int64_t)sizeof(double); };
+  if (P.nchunks > 1) {
+    while (P.nchunks > 1 && kTicketBytes + part_bytes() > ws_bytes) P.nchunks = (P.nchunks + 1) / 2;
+    if (P.nchunks > 1 && (int64_t)P.nprob * (int64_t)sizeof(int) > kTicketBytes) P.nchunks = 1;
+  }
+  P.chunk_rows = (P.nrows + P.nchunks - 1) / P.nchunks;
+  P.chunk_rows = ((P.chunk_rows + G_BK - 1) / G_BK) * G_BK;
+  P.nchunks = (int)lmax(1, (P.nrows + P.chunk_rows - 1) / P.chunk_rows);
+  P.tickets = reinterpret_cast<int*>(ws);
+  P.ws = reinterpret_cast<double*>(static_cast<char*>(ws) + kTicketBytes);
+  const int64_t grid = (int64_t)nb * P.nchunks;
+  if (grid <= 0) return BK_OK;
+  if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
+  constexpr int smem = SB_PAIR_STAGES * 2 * SB_TMA_STAGE * (int)sizeof(double) + 16 * SB_PAIR_STAGES + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_sb_pair_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  BK_COUNT();
+  gram_sb_pair_kernel<C><<<(unsigned)grid, 2 * C::THREADS + 32, smem, st>>>(P, M);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
 typedef CUresult (*SbEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1332,6 +1386,11 @@ extern "C" int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const
       SbMaps M;
       bool ok = true;
       for (int i = 0; i < 6 && ok; ++i) ok = encode_sb_map(&M.m[i], ptrs[i], ld, n);
+      static const int sb_pair = [] {
+        const char* e = getenv("PPCG_GRAM_SBPAIR");
+        return e ? atoi(e) : 1;
+      }();
+      if (ok && sb_pair) return launch_sb_pair<Sb96>(P, nb, ws, ws_bytes, (cudaStream_t)stream, M);
       if (ok) return launch_gram_cfg<Sb96>(P, (int64_t)P.nprob, ws, ws_bytes, (cudaStream_t)stream, &M);
     }
     return launch_gram_cfg<Sb96>(P, (int64_t)P.nprob, ws, ws_bytes, (cudaStream_t)stream);
