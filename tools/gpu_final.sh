@@ -24,5 +24,5 @@ python tools/profile_iter.py 2 2 > gpurun_out/plain.log 2>&1 && for ks in pencil
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
         -o gpurun_out/prof_${tag}_$k python tools/profile_iter.py 2 2 > gpurun_out/ncu_${tag}_$k.log 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gram_sb_tma -s 0 -c 1 \
-    -o gpurun_out/prof_${tag}_gram_sb_tma python tools/profile_iter.py 2 3 > gpurun_out/ncu_${tag}_sbtma.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gram_sb_ -s 0 -c 1 \
+    -o gpurun_out/prof_${tag}_gram_sb_pair python tools/profile_iter.py 2 3 > gpurun_out/ncu_${tag}_sbtma.log 2>&1
