@@ -1282,7 +1282,16 @@ extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int h
 // both Grams of each subblock in one CTA (gram_sb_pair_kernel): grid nb x chunks, one CTA per SM
 template <class C>
 static int launch_sb_pair(GramParams& P, int nb, void* ws, int64_t ws_bytes, cudaStream_t st, const SbMaps& M) {
-  P.nchunks = P.force_chunks > 0 ? P.force_chunks : choose_chunks(P.nrows, nb, 1);
+  // split-K grid of 2 CTA waves (one CTA per SM): fewer, longer chunks than choose_chunks' 8
+  // waves halve the partial-sum traffic and the last-CTA reductions; config 2 measured 36.9 (8
+  // waves), 36.9 (4), 37.1 (2), 36.9 (1) it/s.  PPCG_SBPAIR_WAVES overrides (0 = choose_chunks)
+  static const int waves = [] {
+    const char* e = getenv("PPCG_SBPAIR_WAVES");
+    return e ? atoi(e) : 2;
+  }();
+  P.nchunks = P.force_chunks > 0 ? P.force_chunks
+              : waves > 0        ? (int)lmax(1, lmin(256, (int64_t)waves * kSMs / lmax(1, nb)))
+                                 : choose_chunks(P.nrows, nb, 1);
   auto part_bytes = [&] { return (int64_t)P.nprob * P.nchunks * C::BM * C::BN * (int64_t)sizeof(double); };
   if (P.nchunks > 1) {
     while (P.nchunks > 1 && kTicketBytes + part_bytes() > ws_bytes) P.nchunks = (P.nchunks + 1) / 2;
