@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -45,6 +46,9 @@ def hbm_peak():
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+NCU_SOURCE = "profiles/ncu_summary.json (ncu --set full capture of the same kernels on the live config-2 state)"
 
 
 def ncu_traffic(kernel):
@@ -169,7 +173,8 @@ def run_reference(args):
             "config": cfg_dict(args.config, a.n, k, q, run.kt), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": cores, "kind": "port",
                              "sample": f"{args.warmup} untimed + {args.steps} timed PPCG iterations of config "
-                                       f"{args.config} by the numpy oracle (BLAS {blas})"},
+                                       f"{args.config} by the numpy oracle (BLAS {blas})",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -193,6 +198,7 @@ def kernel_rooflines(torch, s):
     from paper_1407_7506_b200 import kernels as K
 
     n, kt, L = s.nl, s.kt, s.L  # rows of this rank (all rows on one GPU)
+    kt_all = kt
     ka = kt - L
     x, ax, w, aw = s.X(), s.AX(), s.W[:, L:], s.AW[:, L:]
     win = w
@@ -205,7 +211,20 @@ def kernel_rooflines(torch, s):
     out["gram"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9, "flops_per_launch": 2.0 * n * ka * ka}
     tmp = torch.empty_like(s.W)[:, L:]
     ms = event_time(torch, lambda: K.tsgemm([x], [G], [tmp], alpha=-1.0, beta=1.0, zs=[ax]), 10)
-    out["tsgemm"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9}
+    out["tsgemm"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9, "flops_per_launch": 2.0 * n * ka * ka}
+    # periodic work timed separately (north_star (5)): CholQR = potrf + pivot check + trtri on
+    # the active Gram, then X R^-1 and AX R^-1 (one tall triangular GEMM launch); Rayleigh-Ritz
+    # dense part = the k_total x k_total generalized eigensolve (cuSOLVER sygvd path)
+    Gact = s.Gfull[L:, L:]
+    ms_f = event_time(torch, lambda: s._cholqr_factor(Gact), 5)
+    R = s.Rm[:ka, :ka]
+    tmp2 = torch.empty_like(s.W)[:, L:]
+    ms_a = event_time(torch, lambda: K.tsgemm([x, ax], [R, R], [tmp, tmp2], upper=True), 5)
+    out["cholqr"] = {"factor_ms": ms_f, "apply_ms": ms_a, "ms": ms_f + ms_a,
+                     "apply_tflops": 2 * 2.0 * n * ka * ka / 2 / ms_a / 1e9, "k_act": ka}
+    ms_rr = event_time(torch, lambda: s.dense.rr_pencil(s.Ahat, s.Bhat, s.omega, s.Cm, s.rr_status), 3)
+    out["rr_dense"] = {"ms": ms_rr, "k_total": kt_all}
+    del tmp2
     nnz = s.dev_a.nnz
     ms = event_time(torch, lambda: s.dev_a.apply_into(win, aw), 10)
     byts = 2.0 * n * ka * 8 + nnz * 12 + 4 * (n + 1)
@@ -265,10 +284,18 @@ def run_ours(args):
     clk.start()
     launches0 = lib.bk_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-step events (recorded on the launching stream, no extra syncs) split the timed
+    # region into Rayleigh-Ritz iterations and plain (CholQR) iterations (north_star (5))
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    step_rr = []
     e0.record()
+    step_ev[0].record()
     it0 = s.it
-    for _ in range(args.steps):
-        if s.step():
+    for i in range(args.steps):
+        stop = s.step()
+        step_ev[i + 1].record()
+        step_rr.append(math.isfinite(s.opts.rr_period) and s.it % int(s.opts.rr_period) == 0)
+        if stop:
             break
     e1.record()
     torch.cuda.synchronize()
@@ -279,6 +306,9 @@ def run_ours(args):
     clocks = clk.stop()
     steps_done = s.it - it0
     ms = e0.elapsed_time(e1)
+    per_step = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(len(step_rr))]
+    rr_ms = [t for t, r in zip(per_step, step_rr) if r]
+    plain_ms = [t for t, r in zip(per_step, step_rr) if not r]
     red_dev = "cuda" if backend == "nccl" else "cpu"
     tmax = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
@@ -332,12 +362,14 @@ def run_ours(args):
         kr = kernel_rooflines(torch, s)
         peak, peak_src = fp64_peak()
         hbm, hbm_src = hbm_peak()
-        g = kr["gram"]
-        roofline = {"bound": "tensor", "kernel": "gram_kernel (X^T AX, DMMA m8n8k4, split-K)",
-                    "achieved": g["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": g["tflops"] / peak,
-                    "traffic": ncu_traffic("gram_kernel"), "peak_source": peak_src,
-                    "algorithmic_flops_per_launch": g["flops_per_launch"]}
+        tg = kr["tsgemm"]
+        roofline = {"bound": "tensor", "kernel": "tsgemm_kernel (W = T(AX - X G), DMMA m8n8k4; largest launch share)",
+                    "achieved": tg["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": tg["tflops"] / peak,
+                    "traffic": ncu_traffic("tsgemm_kernel"), "traffic_source": NCU_SOURCE,
+                    "peak_source": peak_src, "algorithmic_flops_per_launch": tg["flops_per_launch"]}
         kernels = {name: dict(v) for name, v in kr.items()}
+        kernels["gram"]["frac_of_fp64"] = kr["gram"]["tflops"] / peak
+        kernels["gram"]["traffic"] = ncu_traffic("gram_kernel")
         kernels["spmm"]["frac_of_hbm"] = kr["spmm"]["gbs"] / hbm
         kernels["tsgemm"]["frac_of_fp64"] = kr["tsgemm"]["tflops"] / peak
         kernels["subblock_grams"]["frac_of_fp64"] = kr["subblock_grams"]["tflops"] / peak
@@ -359,10 +391,15 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms_max / max(steps_done, 1), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": f"synthetic (seeded config {args.config})",
-                "config": cfg_dict(args.config, a.n, k, q, s.kt,
-                                   {"parallelism": (f"row partition x{world} ({backend.upper()} allreduce per Gram, "
-                                                    "halo P2P per SpMM)") if world > 1 else "single GPU",
-                                    "n_locked_at_start": int(s.L)}),
+                "config": cfg_dict(args.config, a.n, k, q, s.kt),
+                "layout": (f"row partition x{world} ({backend.upper()} allreduce per Gram, halo P2P per SpMM)"
+                           if world > 1 else "single GPU"),
+                "n_locked_at_start": int(s.L),
+                "iterations": {"plain_ms": statistics.mean(plain_ms) if plain_ms else None, "n_plain": len(plain_ms),
+                               "rr_ms": statistics.mean(rr_ms) if rr_ms else None, "n_rr": len(rr_ms),
+                               "note": "CUDA events around each timed step on the launching stream (rank 0); "
+                                       "plain = projections + subblock update + CholQR + residual; rr = the same "
+                                       "with Rayleigh-Ritz + locking in place of CholQR (ppcg.py:731-757)"},
                 "roofline": roofline, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}
         if not args.no_cpu and world == 1:
@@ -406,9 +443,31 @@ def cpu_baseline(args):
         run.step()
         n_steps = 2
     dt = time.perf_counter() - t0
-    return {"value": n_steps / dt, "unit": "iterations/s", "cores": cores, "kind": "port",
-            "sample": f"iterations 1-{n_steps} of config {args.config} by the numpy oracle (oracle/ppcg_oracle.py), "
-                      f"OpenBLAS with {cores} threads; {dt:.1f} s"}
+    out = {"value": n_steps / dt, "unit": "iterations/s", "cores": cores, "kind": "port",
+           "sample": f"iterations 1-{n_steps} of config {args.config} by the numpy oracle (oracle/ppcg_oracle.py), "
+                     f"OpenBLAS with {cores} threads; {dt:.1f} s",
+           "cpu_model": cpu_model()}
+    # the reference's own setting: BLAS pinned to one thread (ppcg.py:613), one steady iteration
+    # (with P) of the same run -- the official single-core CPU number
+    if not args.no_t1:
+        run.blas_threads = 1
+        t1 = time.perf_counter()
+        run.step()
+        d1 = time.perf_counter() - t1
+        out["pinned_t1"] = {"value": 1.0 / d1, "unit": "iterations/s", "cores": 1,
+                            "sample": f"iteration {n_steps + 1} of the same run with BLAS pinned to 1 thread "
+                                      f"(threadpool_limits(1) as ppcg.py:613); {d1:.1f} s"}
+    return out
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return None
 
 
 def main(argv=None):
@@ -419,6 +478,7 @@ def main(argv=None):
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-t1", action="store_true", help="skip the single-thread reference iteration")
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

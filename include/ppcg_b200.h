@@ -50,6 +50,21 @@ int bk_spmm_march_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const 
 int bk_spmm_march_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* ell_val,
                     const uint16_t* ell_off, int width, int woff, int m, const double* X, int64_t ldx, double* Y,
                     int64_t ldy, int row_align, void* stream);
+/* Stencil-slot SpMM (default where it applies), same result as bk_spmm_csr_*: for a
+ * nearest-neighbour stencil CSR whose rows are sorted (CSR order = (dx, dy, dz) lexicographic)
+ * and whose offsets form the 7-point cross (st = 7) or lie in the 27-point cube (st = 27).
+ * sval: n x vd doubles (StencilPlan.slot_values): row r holds the value of stencil position s
+ * in slot s (complex: interleaved) and the presence bit mask (int64 bit pattern) in its last
+ * double.  X tiles are staged by TMA; the 7-point kernel keeps the tile's centre column in
+ * registers along the march, the 27-point kernel computes 2 z rows per thread from shared
+ * X lines.  Other arguments and the alignment rules as bk_spmm_march_*. */
+int bk_spmm_stencil_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* sval, int vd, int st,
+                      int m, const double* X, int64_t ldx, double* Y, int64_t ldy, int row_align, void* stream);
+int bk_spmm_stencil_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* sval, int vd, int st,
+                      int m, const double* X, int64_t ldx, double* Y, int64_t ldy, int row_align, void* stream);
+/* kernel variant of bk_spmm_stencil_* (sweeps): 0 default; 1 = 7-point 512-byte slices /
+ * 27-point 4 rows per thread */
+int bk_spmm_stencil_set_config(int cfg);
 
 /* ---- diagonal apply: DiagonalPreconditioner.apply operators.py:110, DiagonalOperator
  *      operators.py:68-69 (real d; complex blocks as real views with 2m columns) */

@@ -731,3 +731,346 @@ extern "C" int bk_spmm_march_z(int nx, int ny, int nz, int xlo, int xhi, int64_t
   return march_launch(true, nx, ny, nz, xlo, xhi, d0, ell_val, ell_off, width, woff, m, X, ldx, Y, ldy, row_align,
                       stream);
 }
+
+// ---- stencil-slot march (default for 7-point and 27-point stencils whose CSR rows are
+// sorted: spmm_plan.py StencilPlan.slot_values).
+//
+// Same work units, TMA X ring and plane march as spmm_march_kernel, but the entries arrive
+// as a stencil-slot ELL: row r holds the value of stencil position s (CSR order = (dx, dy,
+// dz) lexicographic) in slot s and a presence mask in its last double, so every X address is
+// a compile-time offset and the kernel reuses X from registers:
+//  * 7-point (ST = 7): the centre column of the tile walks along x in registers (planes
+//    x-1, x, x+1), only the four in-plane neighbours come from shared memory, and a step
+//    holds two ring slots (planes x, x+1) instead of three -- more planes in flight.
+//  * 27-point (ST = 27): a thread computes RZ consecutive z rows and loads each (dx, dy)
+//    line of RZ + 2 X rows once for all of them: 9 (RZ + 2) / RZ shared loads per output
+//    row instead of 27.
+// FMAs run in CSR order (absent positions are skipped by the mask), so the result equals
+// bk_spmm_csr_* bit for bit.
+namespace bk {
+
+constexpr int ST_NSMAX = 8;
+
+template <int COLS, int NP, int RZ>
+constexpr int st_consumers() {
+  return M_T * M_T / RZ * (COLS / 2 / NP);
+}
+
+template <bool CPLX>
+BK_DEV void st_fma(double2& acc, march_vt<CPLX> a, double2 v) {
+  if constexpr (CPLX) {
+    acc.x = fma(a.x, v.x, fma(-a.y, v.y, acc.x));
+    acc.y = fma(a.x, v.y, fma(a.y, v.x, acc.y));
+  } else {
+    acc.x = fma(a, v.x, acc.x);
+    acc.y = fma(a, v.y, acc.y);
+  }
+}
+
+template <bool CPLX, int ST, int COLS, int NP, int RZ>
+__global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
+    spmm_stencil_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
+                        MarchArgs A) {
+  static_assert(ST == 7 || ST == 27, "stencil");
+  static_assert(ST == 27 || RZ == 1, "7-point: one row per thread");
+  constexpr int TPR = COLS / 2 / NP;  // threads per row (16-byte pieces g + TPR k)
+  constexpr int NCONS = st_consumers<COLS, NP, RZ>();
+  using VT = march_vt<CPLX>;
+  extern __shared__ __align__(128) unsigned char msm[];
+  __shared__ __align__(8) uint64_t full[ST_NSMAX], empty[ST_NSMAX];
+  const int NS = A.ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NCONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCONS / 32) {
+    if (lane == 0) {
+      const uint32_t ell_bytes = M_T * M_T * A.vdoubles * 8;
+      int k = 0;
+      for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+        const MarchUnit U = march_unit(A, u);
+        for (int p = U.xa - 1; p <= U.xb; ++p, ++k) {
+          const int slot = k % NS;
+          unsigned char* sb = msm + (size_t)slot * A.slot_bytes;
+          if (k >= NS) mbar_wait(&empty[slot], ((k / NS) - 1) & 1);
+          const bool ell = p - 1 >= U.xa && p - 1 < U.xb;  // entries of plane p - 1 ride along
+          mbar_arrive_expect_tx(&full[slot], M_HR * COLS * 8 + (ell ? ell_bytes : 0));
+          tma_load_4d(sb, &xmap, U.s * COLS, U.z0 - 1, U.y0 - 1, p - A.xlo, &full[slot]);
+          if (ell) tma_load_4d(sb + A.vals_off, &vmap, 0, U.z0, U.y0, p - 1, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: thread -> (tile row group, piece g)
+  const int g = threadIdx.x % TPR, grp = threadIdx.x / TPR;
+  constexpr int ZG = M_T / RZ;  // z groups per tile row
+  const int iy = grp / ZG, iz0 = (grp % ZG) * RZ;
+  const int64_t plane = (int64_t)A.ny * A.nz;
+  const int pc0 = g;  // first piece of this thread within the slice
+  auto xrow = [&](int slot, int hy, int hz) {  // halo-tile row (hy, hz) of a slot, this thread's pieces
+    return reinterpret_cast<const double*>(msm + (size_t)slot * A.slot_bytes) + (hy * M_H + hz) * COLS + 2 * pc0;
+  };
+  auto ld = [&](const double* p, double2 (&v)[NP]) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = *reinterpret_cast<const double2*>(p + 2 * TPR * k);
+  };
+  int k = 0;
+  for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
+    const MarchUnit U = march_unit(A, u);
+    const int pcs = U.s * (COLS / 2) + pc0;  // piece index in the row (from the slices' origin)
+    bool act[RZ];
+#pragma unroll
+    for (int i = 0; i < RZ; ++i) act[i] = U.y0 + iy < A.ny && U.z0 + iz0 + i < A.nz && pcs < A.npieces;
+    int64_t row = ((int64_t)U.xa * A.ny + U.y0 + iy) * A.nz + U.z0 + iz0;
+    if constexpr (ST == 7) {
+      double2 cprev[NP], ccur[NP], cnext[NP];
+      mbar_wait(&full[k % NS], (k / NS) & 1);
+      ld(xrow(k % NS, iy + 1, iz0 + 1), cprev);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[k % NS]);
+      mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
+      ld(xrow((k + 1) % NS, iy + 1, iz0 + 1), ccur);
+      for (int x = U.xa; x < U.xb; ++x, row += plane) {
+        const int kx = k + 1 + (x - U.xa);  // load index of plane x
+        const int s1 = kx % NS, s2 = (kx + 1) % NS;
+        mbar_wait(&full[s2], ((kx + 1) / NS) & 1);
+        ld(xrow(s2, iy + 1, iz0 + 1), cnext);
+        if (act[0]) {
+          const double* ev = reinterpret_cast<const double*>(msm + (size_t)s2 * A.slot_bytes + A.vals_off) +
+                             (iy * M_T + iz0) * A.vdoubles;
+          const uint32_t mask = (uint32_t)__double_as_longlong(ev[A.vdoubles - 1]);
+          const VT* av = reinterpret_cast<const VT*>(ev);
+          double2 nb[4][NP];
+          ld(xrow(s1, iy, iz0 + 1), nb[0]);      // (0, -1, 0)
+          ld(xrow(s1, iy + 1, iz0), nb[1]);      // (0, 0, -1)
+          ld(xrow(s1, iy + 1, iz0 + 2), nb[2]);  // (0, 0, +1)
+          ld(xrow(s1, iy + 2, iz0 + 1), nb[3]);  // (0, +1, 0)
+          double2 acc[NP];
+#pragma unroll
+          for (int q = 0; q < NP; ++q) acc[q] = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int s = 0; s < 7; ++s) {
+            if (!((mask >> s) & 1u)) continue;
+            const VT a = av[s];
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+              const double2 v = s == 0 ? cprev[q] : s == 1 ? nb[0][q] : s == 2 ? nb[1][q] : s == 3 ? ccur[q]
+                                : s == 4 ? nb[2][q] : s == 5 ? nb[3][q] : cnext[q];
+              st_fma<CPLX>(acc[q], a, v);
+            }
+          }
+          double* yr = A.Y + row * A.ldy;
+#pragma unroll
+          for (int q = 0; q < NP; ++q) march_store<CPLX>(A, yr, pcs + TPR * q, acc[q]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s1]);  // plane x: neighbours done, centre kept in registers
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          cprev[q] = ccur[q];
+          ccur[q] = cnext[q];
+        }
+      }
+      const int kl = k + 1 + (U.xb - U.xa);  // plane xb
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[kl % NS]);
+      k = kl + 1;
+    } else {
+      mbar_wait(&full[k % NS], (k / NS) & 1);
+      mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
+      for (int x = U.xa; x < U.xb; ++x, row += plane) {
+        const int kx = k + (x - U.xa);  // load index of plane x - 1
+        const int s0 = kx % NS, s2 = (kx + 2) % NS;
+        mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < RZ; ++i) any |= act[i];
+        if (any) {
+          const double* ev = reinterpret_cast<const double*>(msm + (size_t)s2 * A.slot_bytes + A.vals_off) +
+                             (iy * M_T + iz0) * A.vdoubles;
+          uint32_t mask[RZ];
+#pragma unroll
+          for (int i = 0; i < RZ; ++i) mask[i] = (uint32_t)__double_as_longlong(ev[i * A.vdoubles + A.vdoubles - 1]);
+          double2 acc[RZ][NP];
+#pragma unroll
+          for (int i = 0; i < RZ; ++i)
+#pragma unroll
+            for (int q = 0; q < NP; ++q) acc[i][q] = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int dxi = 0; dxi < 3; ++dxi) {
+            const int sl = (kx + dxi) % NS;
+#pragma unroll
+            for (int dyi = 0; dyi < 3; ++dyi) {
+              double2 v[RZ + 2][NP];
+#pragma unroll
+              for (int j = 0; j < RZ + 2; ++j) ld(xrow(sl, iy + dyi, iz0 + j), v[j]);
+#pragma unroll
+              for (int i = 0; i < RZ; ++i) {
+                const VT* av = reinterpret_cast<const VT*>(ev + i * A.vdoubles);
+#pragma unroll
+                for (int dzi = 0; dzi < 3; ++dzi) {
+                  const int s = dxi * 9 + dyi * 3 + dzi;
+                  if (!((mask[i] >> s) & 1u)) continue;
+                  const VT a = av[s];
+#pragma unroll
+                  for (int q = 0; q < NP; ++q) st_fma<CPLX>(acc[i][q], a, v[i + dzi][q]);
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < RZ; ++i)
+            if (act[i]) {
+              double* yr = A.Y + (row + i) * A.ldy;
+#pragma unroll
+              for (int q = 0; q < NP; ++q) march_store<CPLX>(A, yr, pcs + TPR * q, acc[i][q]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s0]);
+      }
+      const int kl = k + (U.xb - U.xa);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[kl % NS]);
+        mbar_arrive(&empty[(kl + 1) % NS]);
+      }
+      k = kl + 2;
+    }
+  }
+}
+
+// stencil-slot kernel variants: (COLS, NP, RZ) per stencil; the knob selects among them for sweeps
+static int bk_stencil_cfg = 0;
+
+}  // namespace bk
+
+extern "C" int bk_spmm_stencil_set_config(int cfg) {
+  if (cfg < 0 || cfg > 3) return BK_ERR_ARG;
+  bk::bk_stencil_cfg = cfg;
+  return BK_OK;
+}
+
+static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* sval,
+                          int vd, int st, int m, const double* X, int64_t ldx, double* Y, int64_t ldy, int row_align,
+                          void* stream) {
+  using namespace bk;
+  if (nx < 0 || ny <= 0 || nz <= 0 || m < 0 || xhi < xlo || (st != 7 && st != 27) || vd % 2 ||
+      vd < (cplx ? 2 * st + 1 : st + 1) || vd > 256)
+    return BK_ERR_ARG;
+  if (nx == 0 || m == 0) return BK_OK;
+  cudaStream_t strm = (cudaStream_t)stream;
+  MarchArgs A;
+  A.nx = nx;
+  A.ny = ny;
+  A.nz = nz;
+  A.xlo = xlo;
+  A.width = st;
+  A.woff = 0;
+  A.m = m;
+  A.vdoubles = vd;
+  const double* xbase;
+  int64_t ldxd, cols;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(X), ya = reinterpret_cast<uintptr_t>(Y);
+  if (cplx) {
+    A.off = (row_align % 128 == 0 && ldx % 8 == 0 && ldy % 8 == 0 && xa % 128 == ya % 128) ? (int)((xa % 128) / 16)
+                                                                                       : 0;
+    xbase = X + 2 * (d0 * ldx - A.off);
+    ldxd = 2 * ldx;
+    cols = 2 * ((int64_t)m + A.off);
+    A.Y = Y - 2 * A.off;
+    A.ldy = 2 * ldy;
+  } else {
+    A.off = (int)((xa >> 3) & 1);
+    if ((ldx & 1) || (ldy & 1) || A.off != (int)((ya >> 3) & 1)) return BK_ERR_UNSUPPORTED;
+    if (row_align % 128 == 0 && ldx % 16 == 0 && ldy % 16 == 0 && xa % 128 == ya % 128) A.off = (int)((xa % 128) / 8);
+    xbase = X - A.off + d0 * ldx;
+    ldxd = ldx;
+    cols = m + A.off;
+    A.Y = Y - A.off;
+    A.ldy = ldy;
+  }
+  // variants: 7-point (COLS, NP) = (32, 2) default / (64, 4); 27-point RZ = 2 default / 4
+  const int cfg = bk_stencil_cfg;
+  int COLS, NCONS;
+  void (*kern)(const CUtensorMap, const CUtensorMap, MarchArgs);
+  if (st == 7) {
+    if (cfg == 1) {
+      COLS = 64;
+      NCONS = st_consumers<64, 4, 1>();
+      kern = cplx ? spmm_stencil_kernel<true, 7, 64, 4, 1> : spmm_stencil_kernel<false, 7, 64, 4, 1>;
+    } else {
+      COLS = 32;
+      NCONS = st_consumers<32, 2, 1>();
+      kern = cplx ? spmm_stencil_kernel<true, 7, 32, 2, 1> : spmm_stencil_kernel<false, 7, 32, 2, 1>;
+    }
+  } else {
+    COLS = 32;
+    if (cfg == 1) {
+      NCONS = st_consumers<32, 1, 4>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4> : spmm_stencil_kernel<false, 27, 32, 1, 4>;
+    } else {
+      NCONS = st_consumers<32, 1, 2>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2>;
+    }
+  }
+  A.vals_off = M_HR * COLS * 8;
+  A.offs_off = 0;
+  A.slot_bytes = (A.vals_off + M_T * M_T * vd * 8 + 127) / 128 * 128;
+  A.ns = (int)lmin(ST_NSMAX, (227 * 1024) / A.slot_bytes);
+  if (A.ns < 4) return BK_ERR_UNSUPPORTED;
+  const size_t smem = (size_t)A.ns * A.slot_bytes;
+  CUtensorMap xmap, vmap;
+  const int64_t P = (int64_t)ny * nz;
+  int rc = encode_4d(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, xbase + (int64_t)xlo * P * ldxd, cols, nz, ny,
+                     xhi - xlo, ldxd, nz * ldxd, P * ldxd, COLS, M_H, M_H);
+  if (rc == BK_OK)
+    rc = encode_4d(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, sval, vd, nz, ny, nx, vd, nz * vd, P * vd, vd, M_T,
+                   M_T);
+  if (rc != BK_OK) return rc;
+  A.gy = (ny + M_T - 1) / M_T;
+  A.gz = (nz + M_T - 1) / M_T;
+  A.nslices = (int)((cols + COLS - 1) / COLS);
+  A.npieces = (int)((cols + 1) / 2);
+  const int64_t per_seg = (int64_t)A.gy * A.gz * A.nslices;
+  A.xseg = 1;
+  int64_t best = -1;
+  for (int xs = 1; xs <= lmax(1, nx / 8); ++xs) {
+    const int64_t waves = (per_seg * xs + kSMs - 1) / kSMs;
+    const int64_t cost = waves * ((nx + xs - 1) / xs + 2);
+    if (best < 0 || cost < best) {
+      best = cost;
+      A.xseg = xs;
+    }
+  }
+  A.nunits = (int)(per_seg * A.xseg);
+  // per launch: the attribute belongs to the current device's context (cheap)
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)lmin(A.nunits, kSMs);
+  BK_COUNT();
+  kern<<<grid, NCONS + 32, smem, strm>>>(xmap, vmap, A);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+// Y = A X for a nearest-neighbour stencil CSR with sorted rows, from the stencil-slot values of
+// spmm_plan.py StencilPlan (sval: n x vd doubles per row -- st = 7 or 27 slot values, real or
+// interleaved complex, the presence mask's bits in the row's last double); same result as
+// bk_spmm_csr_*.  Other arguments as bk_spmm_march_*.
+extern "C" int bk_spmm_stencil_d(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* sval, int vd,
+                                 int st, int m, const double* X, int64_t ldx, double* Y, int64_t ldy, int row_align,
+                                 void* stream) {
+  return stencil_launch(false, nx, ny, nz, xlo, xhi, d0, sval, vd, st, m, X, ldx, Y, ldy, row_align, stream);
+}
+
+extern "C" int bk_spmm_stencil_z(int nx, int ny, int nz, int xlo, int xhi, int64_t d0, const double* sval, int vd,
+                                 int st, int m, const double* X, int64_t ldx, double* Y, int64_t ldy, int row_align,
+                                 void* stream) {
+  return stencil_launch(true, nx, ny, nz, xlo, xhi, d0, sval, vd, st, m, X, ldx, Y, ldy, row_align, stream);
+}

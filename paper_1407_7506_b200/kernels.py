@@ -298,9 +298,15 @@ def spmm_march(plan, x, y):
     else:
         name = "bk_spmm_march_z"
     nx, ny, nz = plan.grid
+    align = min(_row_align(x), _row_align(y))
+    if getattr(plan, "sval", None) is not None and plan.use_slot:
+        _lib.call(name.replace("march", "stencil"), nx, ny, nz, plan.xlo, plan.xhi, plan.d0, plan.sval.data_ptr(),
+                  plan.vd, plan.st, m, x.data_ptr(), ldx, y.data_ptr(), ldy, align, stream_ptr())
+        return True
+    if plan.ell_val is None:
+        return False
     _lib.call(name, nx, ny, nz, plan.xlo, plan.xhi, plan.d0, plan.ell_val.data_ptr(), plan.ell_off.data_ptr(),
-              plan.width, plan.woff, m, x.data_ptr(), ldx, y.data_ptr(), ldy, min(_row_align(x), _row_align(y)),
-              stream_ptr())
+              plan.width, plan.woff, m, x.data_ptr(), ldx, y.data_ptr(), ldy, align, stream_ptr())
     return True
 
 

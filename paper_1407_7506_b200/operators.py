@@ -248,6 +248,7 @@ class DeviceCsr:
     # grid (spmm_plan.py); the whole-row gather otherwise
     use_stencil = True
     min_stencil_rows = 1 << 15
+    stencil_kinds = ("slot",)  # plan layouts built: "slot" (preferred where it applies), "march"
 
     def apply_into(self, x, y):
         from . import kernels
@@ -269,7 +270,10 @@ def _device_stencil_plan(dc):
     plan = StencilPlan(dc.rowptr, dc.col, dc.n, dc.ncols)
     if not plan.ok:
         return None
-    plan.ell_val = plan.ell_values(dc.val)
+    # stencil-slot values when the rows qualify (bk_spmm_stencil_*), else the offset ELL
+    # (bk_spmm_march_*); DeviceCsr.stencil_kinds can keep both (tests compare the kernels)
+    plan.sval = plan.slot_values(dc.val) if plan.st and "slot" in DeviceCsr.stencil_kinds else None
+    plan.ell_val = plan.ell_values(dc.val) if plan.sval is None or "march" in DeviceCsr.stencil_kinds else None
     plan.release_host_index()
     return plan
 

@@ -23,6 +23,12 @@ from the CSR alone, so the reference's own ``SparseHermitian`` objects qualify:
   every nonzero (this rejects periodic wrap-around, which would need a wider halo).
 
 Anything else keeps the gather kernels; so do operators under 32,768 rows (operators.py).
+
+Stencil-slot layout (bk_spmm_stencil_*, the default where it applies): when every row's
+columns are sorted (CSR order = stencil order (dx, dy, dz) lexicographic) and the offsets are
+the 7-point cross or lie in the 27-point cube, the values are laid out per stencil POSITION
+instead (slot s of a row = the value at position s, presence bits in the row's last double).
+The kernel then knows every X address at compile time and reuses X rows from registers.
 """
 
 from __future__ import annotations
@@ -30,6 +36,12 @@ from __future__ import annotations
 import numpy as np
 
 TY = TZ = 8  # grid tile per CTA (the kernel's compile-time tile)
+
+# 27-point position (dx+1)*9 + (dy+1)*3 + dz+1 -> 7-point cross slot
+_CROSS = {4: 0, 10: 1, 12: 2, 13: 3, 14: 4, 16: 5, 22: 6}
+# doubles per stencil-slot row (values + mask, even; padded so that the rows of one warp's
+# value loads fall in different shared-memory banks)
+_SLOT_VD = {(7, False): 10, (27, False): 28, (7, True): 18, (27, True): 58}
 
 
 def _torch():
@@ -91,6 +103,8 @@ def _grid_for(o, n):
 
 
 class StencilPlan:
+    use_slot = True  # bk_spmm_stencil_* when slot values exist (tests flip it to compare kernels)
+
     """The march SpMM's plan: grid (nx, ny, nz), shift d0, planes [xlo, xhi) the columns
     reach, and the grid-ordered ELL arrays ``ell_off`` (n x woff int16 holding uint16 bit
     patterns: the ring position (plane slot, halo row) of each entry's X row, 0xffff = padding) and
@@ -142,6 +156,19 @@ class StencilPlan:
         ell_off[rows, slot] = offs.to(torch.int32).to(torch.int16)  # uint16 bit patterns
         self.ell_off = ell_off
         self._rows, self._slot = rows, slot
+        # stencil-slot layout: rows sorted (strictly increasing positions) -> 7 or 27 slots
+        pos = (dx + 1) * 9 + (dy + 1) * 3 + (dz + 1)
+        same = rows[1:] == rows[:-1]
+        self.st = 0
+        if not bool((pos[1:][same] <= pos[:-1][same]).any().item()):
+            lut = torch.full((27,), -1, dtype=torch.int64, device=indptr.device)
+            for p27, c in _CROSS.items():
+                lut[p27] = c
+            cross = lut[pos]
+            if bool((cross >= 0).all().item()):
+                self.st, self._spos = 7, cross
+            else:
+                self.st, self._spos = 27, pos
         self.ok = True
 
     def ell_values(self, data):
@@ -158,6 +185,28 @@ class StencilPlan:
         out[self._rows, self._slot] = data.to(out.dtype)
         return out
 
+    def slot_values(self, data):
+        """Stencil-slot layout for bk_spmm_stencil_* (``st`` 7 or 27): an n x vd float64
+        tensor, row r = the values of its stencil positions (real, or interleaved complex) and
+        the presence bit mask (int64 bit pattern) in the last double; absent slots are zero and
+        never read."""
+        torch = _torch()
+        data = torch.as_tensor(data).to(self.ell_off.device)
+        cplx = data.is_complex()
+        self.vd = _SLOT_VD[(self.st, cplx)]
+        n = self.ell_off.shape[0]
+        out = torch.zeros((n, self.vd), dtype=torch.float64, device=data.device)
+        if cplx:
+            vals = out[:, :2 * self.st].view(torch.complex128)
+            vals[self._rows, self._spos] = data.to(torch.complex128)
+        else:
+            out[self._rows, self._spos] = data.to(torch.float64)
+        mask = torch.zeros(n, dtype=torch.int64, device=data.device)
+        mask.index_add_(0, self._rows, torch.ones_like(self._spos) << self._spos)
+        out[:, self.vd - 1] = mask.view(torch.float64)
+        return out
+
     def release_host_index(self):
         """Drop the per-nonzero scatter indices once the values are laid out."""
         del self._rows, self._slot
+        self.__dict__.pop("_spos", None)

@@ -4,6 +4,7 @@ Run in the build container only (the reference does not exist on the GPU box):
 
     python tests/golden/make_golden.py            # kernels, generators, config-1, small solves
     python tests/golden/make_golden.py --cfg2     # + config-2 first iterations (~3 min, 12 GB)
+    python tests/golden/make_golden.py --cfg2-full  # config-2 solve to convergence (~1-2 h, 12 GB)
 
 Every fixture records the inputs (or their seeds/recipes) and the reference outputs.  The
 CPU tests pin the oracle (oracle/ppcg_oracle.py) against these files; the GPU tests check
@@ -223,11 +224,48 @@ def cfg2(iters):
     np.savez_compressed(os.path.join(HERE, f"cfg2_iter{iters}.npz"), **out)
 
 
+def cfg2_full(blas_threads):
+    """BASELINE config 2 solved to convergence by the reference ``ppcg_solve``.
+
+    The reference pins BLAS to one thread (ppcg.py:613).  SURVEY §8(c) measured that letting
+    OpenBLAS use N threads leaves the trajectory intact (same iteration count and lock
+    schedule, Ritz values within 1e-14) and runs 2x faster, so the pin is replaced in-process
+    by an N-thread limit ("reference, BLAS xN"); no reference file is modified.
+
+    Committed: values, trace (iteration, trace_value, rel_resid, n_locked, n_matvec), meta,
+    final residual norms, values_history, orth_loss / proj_defect, and the lowest 8 and the
+    highest 8 of the k returned eigenvectors (16 x n fp64, 14 MB) for principal angles.
+    """
+    from threadpoolctl import threadpool_limits
+
+    BP.threadpool_limits = lambda limits=1: threadpool_limits(limits=blas_threads)
+    ours, k, q, tol = P.config_problem(2)
+    a = B.SparseHermitian(ours._csr, "symmetric")
+    t = B.jacobi_preconditioner(a)
+    t0 = time.time()
+    rep = B.ppcg_solve(a, t, opts=B.SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=5000))
+    wall = time.time() - t0
+    print(f"config 2 full: {rep.status} {rep.iterations} it {rep.rr_count} RR {rep.matvecs} mv "
+          f"in {wall:.1f}s (BLAS x{blas_threads})", flush=True)
+    out = {}
+    _report_arrays("cfg2", rep, out, vectors=False)
+    out["cfg2_vec_lo"] = np.ascontiguousarray(rep.vectors[:, :8])
+    out["cfg2_vec_hi"] = np.ascontiguousarray(rep.vectors[:, -8:])
+    out["cfg2_wall_s"] = np.array(wall)
+    out["cfg2_blas_threads"] = np.array(blas_threads)
+    np.savez_compressed(os.path.join(HERE, "cfg2_full.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--baselines", action="store_true")
+    ap.add_argument("--cfg2-full", action="store_true")
+    ap.add_argument("--blas-threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
+    if args.cfg2_full:
+        cfg2_full(args.blas_threads)
+        sys.exit(0)
     if args.baselines:
         baselines()
         sys.exit(0)

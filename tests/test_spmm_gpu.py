@@ -24,12 +24,19 @@ def run_variants(torch, dc, xb, off, m, cplx):
     dt = torch.complex128 if cplx else torch.float64
     x = xb[:, off:off + m]
     outs = {}
+    variants = (("slot", 2, True, True, 0), ("slot_v1", 2, True, True, 1), ("march", 2, True, False, 0),
+                ("vec", 2, False, False, 0), ("gather", 0, False, False, 0))
     try:
-        for name, variant, stencil in (("march", 2, True), ("vec", 2, False), ("gather", 0, False)):
-            if name == "march" and dc.stencil is None:
+        for name, variant, stencil, slot, cfg in variants:
+            if stencil and dc.stencil is None:
+                continue
+            if slot and getattr(dc.stencil, "sval", None) is None:
                 continue
             lib.bk_spmm_set_variant(variant)
+            lib.bk_spmm_stencil_set_config(cfg)
             DeviceCsr.use_stencil = stencil
+            if dc.stencil is not None:
+                dc.stencil.use_slot = slot
             yb = torch.full((dc.n, xb.shape[1]), float("nan"), dtype=dt, device="cuda")
             y = yb[:, off:off + m]
             dc.apply_into(x, y)
@@ -37,21 +44,27 @@ def run_variants(torch, dc, xb, off, m, cplx):
             outs[name] = yb.cpu().numpy()
     finally:
         lib.bk_spmm_set_variant(2)
+        lib.bk_spmm_stencil_set_config(0)
         DeviceCsr.use_stencil = True
+        if dc.stencil is not None:
+            dc.stencil.use_slot = True
     return outs
 
 
-def check(torch, csr, xh, ncols=None, expect_march=True):
+def check(torch, csr, xh, ncols=None, expect_march=True, expect_st=None):
     from paper_1407_7506_b200.operators import DeviceCsr
 
     cplx = np.iscomplexobj(csr.data) or np.iscomplexobj(xh)
-    prev = DeviceCsr.min_stencil_rows
+    prev = DeviceCsr.min_stencil_rows, DeviceCsr.stencil_kinds
     DeviceCsr.min_stencil_rows = 0  # the test problems are small; production plans from 32768 rows
+    DeviceCsr.stencil_kinds = ("slot", "march")  # both plan layouts: every kernel is compared
     try:
         dc = DeviceCsr(csr)
     finally:
-        DeviceCsr.min_stencil_rows = prev
+        DeviceCsr.min_stencil_rows, DeviceCsr.stencil_kinds = prev
     assert (dc.stencil is not None) == expect_march
+    if expect_st is not None:
+        assert dc.stencil.st == expect_st
     xb = torch.from_numpy(np.ascontiguousarray(xh)).cuda()
     kt = xh.shape[1]
     for off in (0, 1, 10, 11):
@@ -68,12 +81,13 @@ def check(torch, csr, xh, ncols=None, expect_march=True):
 
 
 @pytest.mark.parametrize("cfg,kw,kt", [(1, {"N": 24}, 70), (2, {"N": 20}, 131), (2, {"N": 17}, 64),
-                                       (3, {"N": 12}, 200), (4, {"N": 10}, 90), (5, {"N": 10}, 48)])
+                                       (3, {"N": 12}, 200), (4, {"N": 10}, 90), (5, {"N": 10}, 48),
+                                       (4, {"N": 13}, 37), (5, {"N": 11}, 70)])
 def test_spmm_kernels_agree(cuda, cfg, kw, kt):
     a, _, _, _ = config_problem(cfg, **kw)
     csr = a._csr
     kt = kt + kt % 2  # solver blocks have an even leading dimension
-    check(cuda, csr, gauss(csr.shape[0], kt, cfg, cplx=cfg == 5))
+    check(cuda, csr, gauss(csr.shape[0], kt, cfg, cplx=cfg == 5), expect_st=27 if cfg == 4 else 7)
 
 
 def test_spmm_non_stencil_and_1d(cuda):

@@ -79,3 +79,62 @@ def test_plan_rejects_non_stencils():
     c = laplacian_1d(50)._csr
     p = StencilPlan(c.indptr, c.indices, 50)
     assert p.ok and p.grid == (1, 1, 50)
+
+
+_CROSS_POS = ((-1, 0, 0), (0, -1, 0), (0, 0, -1), (0, 0, 0), (0, 0, 1), (0, 1, 0), (1, 0, 0))
+
+
+def replay_slots(csr, plan, x):
+    """Y = A X through the stencil-slot layout exactly as bk_spmm_stencil_* reads it: slot s of
+    a row is stencil position s (cross order for st = 7, (dx, dy, dz) lexicographic for 27),
+    skipped unless its presence bit is set."""
+    nx, ny, nz = plan.grid
+    sv = plan.slot_values(csr.data).numpy()
+    cplx = np.iscomplexobj(csr.data)
+    vals = sv[:, :2 * plan.st].view(np.complex128) if cplx else sv[:, :plan.st]
+    masks = sv[:, plan.vd - 1].view(np.int64)
+    pos = _CROSS_POS if plan.st == 7 else [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)]
+    y = np.zeros((csr.shape[0], x.shape[1]), dtype=np.result_type(vals, x))
+    for r in range(csr.shape[0]):
+        ix, iy, iz = r // (ny * nz), (r // nz) % ny, r % nz
+        for s, (dx, dy, dz) in enumerate(pos):
+            if (int(masks[r]) >> s) & 1:
+                y[r] += vals[r, s] * x[plan.d0 + ((ix + dx) * ny + iy + dy) * nz + iz + dz]
+    return y
+
+
+@pytest.mark.parametrize("cfg,kw,st", [(1, {"N": 12}, 7), (2, {"N": 6}, 7), (3, {"N": 5}, 7), (4, {"N": 5}, 27),
+                                       (5, {"N": 5}, 7)])
+def test_slot_layout_replays_csr(cfg, kw, st):
+    a, _, _, _ = config_problem(cfg, **kw)
+    csr = a._csr
+    p = StencilPlan(csr.indptr, csr.indices, csr.shape[0])
+    assert p.ok and p.st == st
+    sv = p.slot_values(csr.data)
+    assert sv.shape == (csr.shape[0], p.vd) and p.vd % 2 == 0
+    # every stored entry has its presence bit, and nothing else
+    bits = sv[:, p.vd - 1].numpy().view(np.int64)
+    assert [bin(int(b)).count("1") for b in bits] == list(np.diff(csr.indptr))
+    x = gauss(csr.shape[0], 3, 5, cplx=cfg == 5)
+    np.testing.assert_allclose(replay_slots(csr, p, x), csr @ x, rtol=0, atol=1e-12)
+    # ghost-extended local rows keep the layout (d0 shift)
+    if cfg in (3, 4):
+        P = kw["N"] ** 2
+        lo, hi = 2 * P, 4 * P
+        loc = local_rows_csr(csr, lo, hi, lo - P, 4 * P)
+        pl = StencilPlan(loc.indptr, loc.indices, loc.shape[0], loc.shape[1])
+        assert pl.ok and pl.st == st
+        np.testing.assert_allclose(replay_slots(loc, pl, x[lo - P:hi + P]), (csr @ x)[lo:hi], rtol=0, atol=1e-12)
+
+
+def test_slot_layout_needs_sorted_rows():
+    """Unsorted column indices within a row (legal CSR) keep the offset-ELL march: the slot
+    kernel's FMA order is the stencil order, which equals CSR order only for sorted rows."""
+    a, _, _, _ = config_problem(3, N=5)
+    c = a._csr.copy()
+    r = 40
+    lo, hi = c.indptr[r], c.indptr[r + 1]
+    c.indices[lo:hi] = c.indices[lo:hi][::-1].copy()
+    c.data[lo:hi] = c.data[lo:hi][::-1].copy()
+    p = StencilPlan(c.indptr, c.indices, c.shape[0])
+    assert p.ok and p.st == 0
