@@ -157,7 +157,8 @@ int bk_svals_d(void* ctx, int m, int n, const double* M, int64_t ldm, double* s)
 int bk_svals_z(void* ctx, int m, int n, const double* M, int64_t ldm, double* s);
 
 /* ---- recombination: ppcg.py:365-369 and _run_subblocks ppcg.py:521-532 (+ breakdown
- *      flags of ppcg.py:701-705) */
+ *      flags of ppcg.py:701-705).  Xo, AXo must not alias any input; Po == P and APo == AP
+ *      (both, or neither) update P, AP in place; other aliasing is BK_ERR_ARG. */
 int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double* coef,
                             const double* X, const double* W, const double* P, const double* AX,
                             const double* AW, const double* AP, double* Xo, double* Po,
@@ -202,10 +203,6 @@ int bk_rr_residual_d(int64_t n, int kt, int cplx, const double* V, int64_t ldv, 
 /* ---- strided column-range copy / zero (P realignment, lock_and_compact ppcg.py:399-408) */
 int bk_copy_cols(int64_t n, int w, int elem_bytes, const void* src, int64_t lds, int64_t sc0,
                  void* dst, int64_t ldd, int64_t dc0, void* stream);
-/* stream-ordered delay of ns nanoseconds (one idle thread): queued ahead of a large launch
- * on a side stream, it lets the work made runnable at the same moment on the main stream
- * (the subblock pencils) be dispatched to the SMs first */
-int bk_delay(int64_t ns, void* stream);
 int bk_zero_cols(int64_t n, int w, int elem_bytes, void* dst, int64_t ldd, int64_t dc0,
                  void* stream);
 

@@ -89,7 +89,6 @@ _SIGS = {
                                  c_i64, vp]),
     "bk_copy_cols": (c_int, [c_i64, c_int, c_int, vp, c_i64, c_i64, vp, c_i64, c_i64, vp]),
     "bk_zero_cols": (c_int, [c_i64, c_int, c_int, vp, c_i64, c_i64, vp]),
-    "bk_delay": (c_int, [c_i64, vp]),
     "bk_dense_create": (c_int, [PP, vp]),
     "bk_dense_destroy": (c_int, [vp]),
     "bk_dense_set_stream": (c_int, [vp, vp]),

@@ -103,7 +103,7 @@ class LOBPCGSolver(PPCGSolver):
         w, aw = self.W[:, L:], self.AW[:, L:]
         self._project(L, ka, w, aw)         # AW = A W + projections, baselines.py:259-268
         src, dst = self.xi, 1 - self.xi
-        psrc, pdst = self.pi, 1 - self.pi
+        psrc = pdst = self.pi  # P, AP in place
         self._subblock_update(ka, ka, src, psrc, dst, pdst)   # whole-block block_update
         self._fetch((self.info, self.h_info))
         info = self.h_info.numpy()[:4]

@@ -171,6 +171,11 @@ class LargeBlocks:
         wv, awv = s.W[:, cs], s.AW[:, cs]
         xo, axo = s.XF[dst][:, cs], s.AXF[dst][:, cs]
         po, apo = s.P[pdst][:, cs], s.AP[pdst][:, cs]
+        inplace = has_p and pdst == psrc
+        if inplace:  # P' = W C_W + P C_P reads P: build it in scratch, copy over P at the end
+            po_f, apo_f = po, apo
+            po = self._buf("po", (s.nl, w), s.tdt)
+            apo = self._buf("apo", (s.nl, w), s.tdt)
         cx, cw = coef[:w], coef[w: 2 * w]
         K.tsgemm([wv, awv], [cw, cw], [po, apo])
         if has_p:
@@ -178,6 +183,10 @@ class LargeBlocks:
             cp = coef[2 * w: 3 * w]
             K.tsgemm([p, ap], [cp, cp], [po, apo], beta=1.0, zs=[po, apo])
         K.tsgemm([x, ax], [cx, cx], [xo, axo], beta=1.0, zs=[po, apo])
+        if inplace:
+            K.copy_cols(po, po_f)
+            K.copy_cols(apo, apo_f)
+            po, apo = po_f, apo_f
         K.block_stats(xo, s.flags64, 1)
         K.block_stats(po, s.flags64, 2)
         K.block_stats(axo, s.flags64, 0)

@@ -267,27 +267,6 @@ extern "C" int bk_zero_cols(int64_t n, int w, int elem_bytes, void* dst, int64_t
              : BK_ERR_CUDA;
 }
 
-namespace bk {
-// one thread idles for ns nanoseconds of %globaltimer: a stream-ordered delay that lets work
-// made runnable at the same moment on another stream be dispatched first
-__global__ void k_delay(int64_t ns) {
-  uint64_t t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  do {
-    __nanosleep(1000);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  } while ((int64_t)(t - t0) < ns);
-}
-}  // namespace bk
-
-extern "C" int bk_delay(int64_t ns, void* stream) {
-  if (ns < 0) return BK_ERR_ARG;
-  BK_COUNT();
-  k_delay<<<1, 1, 0, (cudaStream_t)stream>>>(ns);
-  BK_CHECK_LAUNCH();
-  return BK_OK;
-}
-
 extern "C" int bk_version(void) { return 1; }
 
 unsigned long long bk_launch_counter = 0;

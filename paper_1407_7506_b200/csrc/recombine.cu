@@ -3,9 +3,14 @@
 // Replaces the per-subblock products of block_update and _run_subblocks:
 //   P_j' = W_j C_W + P_j C_P,  X_j' = X_j C_X + P_j'           (ppcg.py:365-369)
 //   AP_j' = AW_j C_W + AP_j C_P, AX_j' = AX_j C_X + AP_j'      (ppcg.py:521-532)
-// for every subblock j in one launch (grid: row tiles x blocks x {X side, A side}),
-// writing into separate output buffers so the pre-update blocks survive for the
-// breakdown and rank-deficiency recovery paths (ppcg.py:694, 698-717, 456-472).
+// for every subblock j in one launch (grid: row tiles x blocks x {X side, A side}).  X'
+// and AX' go to separate output buffers so the pre-update X survives for the breakdown and
+// rank-deficiency recovery paths (ppcg.py:694, 698-717, 456-472); P' and AP' may overwrite
+// P and AP in place (nothing reads the pre-update P after the update), which keeps the
+// state at 8 full-width blocks (config 5 on 8 GPUs).  A CTA reads its rows of P_j before it
+// writes them; where a subblock needs several column tiles (complex q = 64) one CTA runs the
+// tiles in turn and stages the earlier tiles' outputs in shared memory until the last tile
+// has read its inputs.
 // The breakdown test of ppcg.py:701-705 (non-finite entries in X, P, AX, AP; max|X|,
 // max|P| > 1e8) is fused into the epilogue as device-wide flags.
 #include "common.cuh"
@@ -57,21 +62,27 @@ __global__ void k_expand_coef(int k_act, int q, int nparts, const double* __rest
 // fragment loads conflict-free.
 constexpr int R_KC = 16, R_STAGES = 3, R_LA = R_KC + 4;
 
-template <int NT, int MINB = 1>
+template <int NT, int MINB = 1, bool SEQ = false>
 __global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid_constant__ RecombParams P) {
   constexpr int LB = NT + 4, WN = NT / 8;
   constexpr int IN_STAGE = R_BM * R_LA, CF_STAGE = R_KC * LB;
   extern __shared__ __align__(16) double sm[];
   double* In = sm;                          // [stage][R_BM][R_LA]
   double* Cf = sm + R_STAGES * IN_STAGE;    // [stage][R_KC][LB]
+  double* Stg = Cf + R_STAGES * CF_STAGE;   // SEQ: [tile][X', P'][R_BM][NT] of the earlier tiles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int j = blockIdx.y;
   const int side = blockIdx.z & 1;
-  const int ct0 = (blockIdx.z >> 1) * NT;   // first output column of this tile
   const int64_t r0 = (int64_t)blockIdx.x * R_BM;
   const int lo = j * P.q;
   const int w = min(P.q, P.k_act - lo);
+  const int ntiles = SEQ ? (w + NT - 1) / NT : 1;
+  bool nonfin = false;
+  double mx = 0.0, mp = 0.0;
+  for (int tile = 0; tile < ntiles; ++tile) {
+  const int ct0 = SEQ ? tile * NT : (blockIdx.z >> 1) * NT;   // first output column of this tile
   if (ct0 >= w) return;
+  if (SEQ && tile > 0) __syncthreads();  // the previous tile's stages are free
   const int nparts = P.has_p ? 3 : 2;
   const int cpp = (w + R_KC - 1) / R_KC;    // chunks per part
   const int nchunks = nparts * cpp;
@@ -150,20 +161,42 @@ __global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid
   cp_async_wait<0>();
 
   // epilogue: P' = accP, X' = accX + accP; breakdown statistics
-  bool nonfin = false;
-  double mx = 0.0, mp = 0.0;
   double* ox = P.outX[side];
   double* op = P.outP[side];
+  if (SEQ && tile + 1 < ntiles) {  // stage this tile until the last tile has read its inputs
+    double* sx = Stg + (size_t)tile * 2 * R_BM * NT;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < WN; ++b) {
+        const int rr = warp * 16 + a * 8 + fm, cc = b * 8 + 2 * fk;
+        sx[rr * NT + cc] = accX[a][b][0] + accP[a][b][0];
+        sx[rr * NT + cc + 1] = accX[a][b][1] + accP[a][b][1];
+        sx[R_BM * NT + rr * NT + cc] = accP[a][b][0];
+        sx[R_BM * NT + rr * NT + cc + 1] = accP[a][b][1];
+      }
+    continue;
+  }
+  for (int tt = SEQ ? 0 : tile; tt <= tile; ++tt) {
+  const int cb0 = SEQ ? tt * NT : ct0;
+  const double* sx = Stg + (size_t)tt * 2 * R_BM * NT;
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
     const int64_t row = r0 + warp * 16 + a * 8 + fm;
     if (row >= P.n) continue;
 #pragma unroll
     for (int b = 0; b < WN; ++b) {
-      const int c = ct0 + b * 8 + 2 * fk;  // this lane's two adjacent columns c, c+1
+      const int c = cb0 + b * 8 + 2 * fk;  // this lane's two adjacent columns c, c+1
       if (c >= w) continue;
-      const double p0 = accP[a][b][0], p1 = accP[a][b][1];
-      const double x0 = accX[a][b][0] + p0, x1 = accX[a][b][1] + p1;
+      double p0 = accP[a][b][0], p1 = accP[a][b][1];
+      double x0 = accX[a][b][0] + p0, x1 = accX[a][b][1] + p1;
+      if (SEQ && tt < tile) {
+        const int rr = warp * 16 + a * 8 + fm, cc = b * 8 + 2 * fk;
+        x0 = sx[rr * NT + cc];
+        x1 = sx[rr * NT + cc + 1];
+        p0 = sx[R_BM * NT + rr * NT + cc];
+        p1 = sx[R_BM * NT + rr * NT + cc + 1];
+      }
       const int64_t off = row * P.ld + P.c0 + lo + c;
       if (c + 1 < w) {
         if ((off & 1) == 0) {
@@ -190,6 +223,8 @@ __global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid
       }
     }
   }
+  }  // tt
+  }  // tile
   nonfin = __any_sync(0xffffffffu, nonfin);
   mx = warp_max(mx);
   mp = warp_max(mp);
@@ -205,12 +240,17 @@ __global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid
 template <int NT, int MINB>
 static void launch_recombine_m(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
   constexpr int smem = R_STAGES * (R_BM * R_LA + R_KC * (NT + 4)) * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(recombine_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  // per launch: the attribute belongs to the current device's context
+  cudaFuncSetAttribute(recombine_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   recombine_kernel<NT, MINB><<<dim3(nrt, nb, 2 * nct), R_THREADS, smem, st>>>(R);
+}
+
+// in-place P' over several column tiles: one CTA per (row tile, subblock, side) runs the tiles
+template <int NT>
+static void launch_recombine_seq(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
+  const int smem = (R_STAGES * (R_BM * R_LA + R_KC * (NT + 4)) + (nct - 1) * 2 * R_BM * NT) * (int)sizeof(double);
+  cudaFuncSetAttribute(recombine_kernel<NT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  recombine_kernel<NT, 1, true><<<dim3(nrt, nb, 2), R_THREADS, smem, st>>>(R);
 }
 
 template <int NT>
@@ -235,7 +275,8 @@ static int recombine(int64_t n, int k_act, int q, int has_p, const double* coef,
                      double* AXo, double* APo, int64_t ld, int64_t c0, unsigned long long* flags, int cplx,
                      void* stream);
 
-// flags: 3 x uint64 on device, zeroed by the caller.  Outputs may not alias inputs.
+// flags: 3 x uint64 on device, zeroed by the caller.  X', AX' may not alias inputs; P', AP'
+// may be P, AP themselves (in-place update).
 extern "C" int bk_subblock_recombine_d(int64_t n, int k_act, int q, int has_p, const double* coef,
                                        const double* X, const double* W, const double* P_, const double* AX,
                                        const double* AW, const double* AP, double* Xo, double* Po, double* AXo,
@@ -288,9 +329,14 @@ static int recombine(int64_t n, int k_act, int q, int has_p, const double* coef,
   const unsigned nrt = (unsigned)((n + R_BM - 1) / R_BM);
   cudaStream_t st = (cudaStream_t)stream;
   BK_COUNT();
+  const bool inplace = Po == P_ || APo == AP;
+  if ((Xo == X || AXo == AX || Xo == W || AXo == AW) ||
+      (inplace && !(Po == P_ && APo == AP)))  // X' may not alias inputs; P' in place on both sides or neither
+    return BK_ERR_ARG;
   if (q <= 16) launch_recombine<16>(R, nrt, nb, 1, st);
   else if (q <= 32) launch_recombine<32>(R, nrt, nb, 1, st);
-  else launch_recombine<64>(R, nrt, nb, (q + 63) / 64, st);
+  else if (q <= 64 || !inplace) launch_recombine<64>(R, nrt, nb, (q + 63) / 64, st);
+  else launch_recombine_seq<64>(R, nrt, nb, (q + 63) / 64, st);
   BK_CHECK_LAUNCH();
   return BK_OK;
 }

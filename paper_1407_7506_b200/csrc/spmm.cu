@@ -751,6 +751,28 @@ namespace bk {
 
 constexpr int ST_NSMAX = 8;
 
+// stencil-slot units: slice fastest, then x segment, then (y, z) tile, so the segments of one
+// tile run in the same wave; odd segments march down (dir = -1).  Two neighbouring segments
+// then read their shared boundary plane at the same moment (both at their start, or both at
+// their end) and the second read hits L2 instead of DRAM.
+struct StUnit {
+  int s, y0, z0, xa, xb, dir;
+};
+
+BK_DEV StUnit st_unit(const MarchArgs& A, int u) {
+  StUnit U;
+  U.s = u % A.nslices;
+  u /= A.nslices;
+  const int seg = u % A.xseg;
+  u /= A.xseg;
+  U.z0 = (u % A.gz) * M_T;
+  U.y0 = (u / A.gz) * M_T;
+  U.xa = (int)((int64_t)seg * A.nx / A.xseg);
+  U.xb = (int)((int64_t)(seg + 1) * A.nx / A.xseg);
+  U.dir = (seg & 1) ? -1 : 1;
+  return U;
+}
+
 template <int COLS, int NP, int RZ>
 constexpr int st_consumers() {
   return M_T * M_T / RZ * (COLS / 2 / NP);
@@ -793,15 +815,18 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
       const uint32_t ell_bytes = M_T * M_T * A.vdoubles * 8;
       int k = 0;
       for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-        const MarchUnit U = march_unit(A, u);
-        for (int p = U.xa - 1; p <= U.xb; ++p, ++k) {
+        const StUnit U = st_unit(A, u);
+        const int nload = U.xb - U.xa + 2;
+        for (int i = 0; i < nload; ++i, ++k) {
+          const int p = U.dir > 0 ? U.xa - 1 + i : U.xb - i;  // planes in march order
+          const int pe = p - U.dir;                             // entries of plane p - dir ride along
           const int slot = k % NS;
           unsigned char* sb = msm + (size_t)slot * A.slot_bytes;
           if (k >= NS) mbar_wait(&empty[slot], ((k / NS) - 1) & 1);
-          const bool ell = p - 1 >= U.xa && p - 1 < U.xb;  // entries of plane p - 1 ride along
+          const bool ell = pe >= U.xa && pe < U.xb;
           mbar_arrive_expect_tx(&full[slot], M_HR * COLS * 8 + (ell ? ell_bytes : 0));
           tma_load_4d(sb, &xmap, U.s * COLS, U.z0 - 1, U.y0 - 1, p - A.xlo, &full[slot]);
-          if (ell) tma_load_4d(sb + A.vals_off, &vmap, 0, U.z0, U.y0, p - 1, &full[slot]);
+          if (ell) tma_load_4d(sb + A.vals_off, &vmap, 0, U.z0, U.y0, pe, &full[slot]);
         }
       }
     }
@@ -822,25 +847,28 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
   };
   int k = 0;
   for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
-    const MarchUnit U = march_unit(A, u);
+    const StUnit U = st_unit(A, u);
     const int pcs = U.s * (COLS / 2) + pc0;  // piece index in the row (from the slices' origin)
     bool act[RZ];
 #pragma unroll
     for (int i = 0; i < RZ; ++i) act[i] = U.y0 + iy < A.ny && U.z0 + iz0 + i < A.nz && pcs < A.npieces;
-    int64_t row = ((int64_t)U.xa * A.ny + U.y0 + iy) * A.nz + U.z0 + iz0;
+    const int nsteps = U.xb - U.xa;
+    const int64_t rstep = U.dir * plane;
+    int64_t row = ((int64_t)(U.dir > 0 ? U.xa : U.xb - 1) * A.ny + U.y0 + iy) * A.nz + U.z0 + iz0;
     if constexpr (ST == 7) {
-      double2 cprev[NP], ccur[NP], cnext[NP];
+      // centre column in march order: ctp = plane x - dir, ccur = x, ctn = x + dir
+      double2 ctp[NP], ccur[NP], ctn[NP];
       mbar_wait(&full[k % NS], (k / NS) & 1);
-      ld(xrow(k % NS, iy + 1, iz0 + 1), cprev);
+      ld(xrow(k % NS, iy + 1, iz0 + 1), ctp);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[k % NS]);
       mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
       ld(xrow((k + 1) % NS, iy + 1, iz0 + 1), ccur);
-      for (int x = U.xa; x < U.xb; ++x, row += plane) {
-        const int kx = k + 1 + (x - U.xa);  // load index of plane x
+      for (int i = 0; i < nsteps; ++i, row += rstep) {
+        const int kx = k + 1 + i;  // load index of plane x
         const int s1 = kx % NS, s2 = (kx + 1) % NS;
         mbar_wait(&full[s2], ((kx + 1) / NS) & 1);
-        ld(xrow(s2, iy + 1, iz0 + 1), cnext);
+        ld(xrow(s2, iy + 1, iz0 + 1), ctn);
         if (act[0]) {
           const double* ev = reinterpret_cast<const double*>(msm + (size_t)s2 * A.slot_bytes + A.vals_off) +
                              (iy * M_T + iz0) * A.vdoubles;
@@ -860,8 +888,10 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
             const VT a = av[s];
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
-              const double2 v = s == 0 ? cprev[q] : s == 1 ? nb[0][q] : s == 2 ? nb[1][q] : s == 3 ? ccur[q]
-                                : s == 4 ? nb[2][q] : s == 5 ? nb[3][q] : cnext[q];
+              // dx = -1 / +1: the planes before / after x in grid order
+              const double2 v = s == 0 ? (U.dir > 0 ? ctp[q] : ctn[q]) : s == 1 ? nb[0][q] : s == 2 ? nb[1][q]
+                                : s == 3 ? ccur[q] : s == 4 ? nb[2][q] : s == 5 ? nb[3][q]
+                                : (U.dir > 0 ? ctn[q] : ctp[q]);
               st_fma<CPLX>(acc[q], a, v);
             }
           }
@@ -873,19 +903,19 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
         if (lane == 0) mbar_arrive(&empty[s1]);  // plane x: neighbours done, centre kept in registers
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-          cprev[q] = ccur[q];
-          ccur[q] = cnext[q];
+          ctp[q] = ccur[q];
+          ccur[q] = ctn[q];
         }
       }
-      const int kl = k + 1 + (U.xb - U.xa);  // plane xb
+      const int kl = k + 1 + nsteps;  // the last halo plane
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[kl % NS]);
       k = kl + 1;
     } else {
       mbar_wait(&full[k % NS], (k / NS) & 1);
       mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
-      for (int x = U.xa; x < U.xb; ++x, row += plane) {
-        const int kx = k + (x - U.xa);  // load index of plane x - 1
+      for (int i = 0; i < nsteps; ++i, row += rstep) {
+        const int kx = k + i;  // load index of plane x - dir
         const int s0 = kx % NS, s2 = (kx + 2) % NS;
         mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
         bool any = false;
@@ -904,7 +934,7 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
             for (int q = 0; q < NP; ++q) acc[i][q] = make_double2(0.0, 0.0);
 #pragma unroll
           for (int dxi = 0; dxi < 3; ++dxi) {
-            const int sl = (kx + dxi) % NS;
+            const int sl = (U.dir > 0 ? kx + dxi : kx + 2 - dxi) % NS;  // plane x + dxi - 1
 #pragma unroll
             for (int dyi = 0; dyi < 3; ++dyi) {
               double2 v[RZ + 2][NP];
@@ -935,7 +965,7 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s0]);
       }
-      const int kl = k + (U.xb - U.xa);
+      const int kl = k + nsteps;
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&empty[kl % NS]);
@@ -1024,6 +1054,12 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
   A.offs_off = 0;
   A.slot_bytes = (A.vals_off + M_T * M_T * vd * 8 + 127) / 128 * 128;
   A.ns = (int)lmin(ST_NSMAX, (227 * 1024) / A.slot_bytes);
+  if (A.ns < 4 && cfg != 0) {  // variant does not fit (complex 512-byte slices): the default
+    bk_stencil_cfg = 0;
+    const int rc0 = stencil_launch(cplx, nx, ny, nz, xlo, xhi, d0, sval, vd, st, m, X, ldx, Y, ldy, row_align, stream);
+    bk_stencil_cfg = cfg;
+    return rc0;
+  }
   if (A.ns < 4) return BK_ERR_UNSUPPORTED;
   const size_t smem = (size_t)A.ns * A.slot_bytes;
   CUtensorMap xmap, vmap;

@@ -174,8 +174,30 @@ class Comm:
         """Concatenate every rank's (rows_r x c) block in rank order."""
         raise NotImplementedError
 
+    def reduce_scatter_sum(self, full, chunk):
+        """``full`` (contiguous, size * chunk elements): rank r's chunk [r chunk, (r+1) chunk)
+        becomes the sum over ranks of that chunk (the other chunks are left undefined)."""
+        raise NotImplementedError
+
+    def allgather_chunks(self, full, chunk):
+        """``full`` (contiguous, size * chunk elements) holding this rank's chunk at r chunk:
+        afterwards every chunk holds its owner's values, on every rank."""
+        raise NotImplementedError
+
+    def gather_rows_host(self, local, bounds, mode="all"):
+        """Host assembly of a row-partitioned result (numpy rows_r x c per rank) without any
+        device-side gather: mode "all" -> the (n x c) array on every rank, "root" -> on rank
+        0 (other ranks get None)."""
+        raise NotImplementedError
+
     def barrier(self):
         raise NotImplementedError
+
+
+def _real(t):
+    import torch
+
+    return torch.view_as_real(t).reshape(-1) if t.is_complex() else t.reshape(-1)
 
 
 class TorchComm(Comm):
@@ -235,6 +257,51 @@ class TorchComm(Comm):
         self.dist.all_gather_into_tensor(out, pad, group=self.group)
         full = torch.cat([out[r * rows: r * rows + (b - a)] for r, (a, b) in enumerate(bounds)])
         return full.to(local.device)
+
+    def reduce_scatter_sum(self, full, chunk):
+        if self.stage:  # gloo: no reduce-scatter on staged tensors -- a sum-allreduce is a superset
+            self.allreduce_sum(full)
+            return
+        f = _real(full)
+        c = chunk * (2 if full.is_complex() else 1)
+        # in place: the output chunk is this rank's slice of the input (NCCL's in-place form)
+        self.dist.reduce_scatter_tensor(f[self.rank * c:(self.rank + 1) * c], f, group=self.group)
+
+    def allgather_chunks(self, full, chunk):
+        f = _real(full)
+        c = chunk * (2 if full.is_complex() else 1)
+        if self.stage:
+            h = f.cpu()
+            parts = list(h.split(c))
+            self.dist.all_gather(parts, parts[self.rank].clone(), group=self.group)
+            f.copy_(h)
+            return
+        self.dist.all_gather_into_tensor(f, f[self.rank * c:(self.rank + 1) * c], group=self.group)
+
+    def _host_group(self):
+        g = getattr(self, "_gloo", None)
+        if g is None:
+            g = self._gloo = self.dist.new_group(backend="gloo") if not self.stage else self.group
+        return g
+
+    def gather_rows_host(self, local, bounds, mode="all"):
+        """Rows over a host (gloo) group: rank order, padded to the largest slab.  One
+        process per GPU on one node in practice, so this is a host-memory copy per rank."""
+        import torch
+
+        g = self._host_group()
+        rows = max(b - a for a, b in bounds)
+        pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=torch.from_numpy(local[:0]).dtype)
+        pad[: local.shape[0]] = torch.from_numpy(local)
+        if mode == "root":
+            parts = [torch.empty_like(pad) for _ in range(self.size)] if self.rank == 0 else None
+            self.dist.gather(pad, parts, dst=self._global(0), group=g)
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.size)]
+            self.dist.all_gather(parts, pad, group=g)
+        if parts is None:
+            return None
+        return np.concatenate([p[: b - a].numpy() for p, (a, b) in zip(parts, bounds)])
 
     def barrier(self):
         self.dist.barrier(group=self.group)
@@ -314,6 +381,32 @@ class ThreadComm(Comm):
         vals = self._gather(local.contiguous())
         return torch.cat(vals)
 
+    def reduce_scatter_sum(self, full, chunk):
+        vals = self._gather(full)
+        lo, hi = self.rank * chunk, (self.rank + 1) * chunk
+        acc = vals[0].reshape(-1)[lo:hi].clone()
+        for v in vals[1:]:
+            acc += v.reshape(-1)[lo:hi]
+        full.reshape(-1)[lo:hi].copy_(acc)
+        self._sync(full)
+
+    def allgather_chunks(self, full, chunk):
+        vals = self._gather(full)
+        f = full.reshape(-1)
+        for r, v in enumerate(vals):
+            if r != self.rank:
+                f[r * chunk:(r + 1) * chunk].copy_(v.reshape(-1)[r * chunk:(r + 1) * chunk])
+        self._sync(full)
+
+    def gather_rows_host(self, local, bounds, mode="all"):
+        self.sh.slots[self.rank] = local
+        self.sh.barrier.wait()
+        vals = list(self.sh.slots)
+        self.sh.barrier.wait()
+        if mode == "root" and self.rank != 0:
+            return None
+        return np.concatenate(vals)
+
     def barrier(self):
         self.sh.barrier.wait()
 
@@ -323,10 +416,15 @@ def thread_comms(size):
     return [ThreadComm(sh, r) for r in range(size)]
 
 
-def dist_ppcg_solve(a, t=None, x0=None, opts=None, comm=None):
+def dist_ppcg_solve(a, t=None, x0=None, opts=None, comm=None, gather=None):
     """ppcg_solve over a row partition (one rank per GPU).  Every rank passes the same
-    operator, preconditioner, x0 and options and receives the same SolveReport (vectors
-    gathered to full length)."""
+    operator, preconditioner, x0 and options.  The eigenvectors are assembled on the host
+    from each rank's row slab (no device-side gather; PPCGSolver.finish):
+      gather="all"  -- every rank receives the full (n, k) vectors;
+      gather="root" -- rank 0 does, the other ranks receive their own rows [lo, hi)
+                       (``diagnostics["vector_rows"]``);
+      None          -- "all" up to 8 GB of vectors, else "root" (config 5: 137 GB).
+    Everything else in the SolveReport is identical on every rank."""
     from .ppcg import PPCGSolver
 
     if opts is None:
@@ -335,4 +433,4 @@ def dist_ppcg_solve(a, t=None, x0=None, opts=None, comm=None):
     s = PPCGSolver(a, t, x0, opts, comm=comm).start()
     while not s.step():
         pass
-    return s.finish()
+    return s.finish(gather=gather)

@@ -244,11 +244,6 @@ def copy_cols(src, dst):
               dst.data_ptr(), ld_of(dst), 0, stream_ptr())
 
 
-def delay(ns):
-    """Stream-ordered idle of ns nanoseconds on the current stream (bk_delay)."""
-    _lib.call("bk_delay", int(ns), stream_ptr())
-
-
 def zero_cols(dst):
     es = 16 if dst.dtype == C128 else 8
     _lib.call("bk_zero_cols", dst.shape[0], dst.shape[1], es, dst.data_ptr(), ld_of(dst), 0, stream_ptr())
@@ -341,6 +336,22 @@ def subblock_pencils(k_act, q, has_p, araw, braw, coef, theta, info, cscale, for
     _lib.call(name, k_act, q, 1 if has_p else 0, araw.data_ptr(), braw.data_ptr(),
               coef.data_ptr(), theta.data_ptr(), info.data_ptr(), cscale.data_ptr(),
               1 if force_fallback else 0, wp, wb, stream_ptr())
+
+
+def subblock_pencils_range(j0, j1, k_act, q, has_p, araw, braw, coef, theta, info, cscale):
+    """subblock_pencils for subblocks [j0, j1) only (the row-partitioned solver's chunk):
+    the same kernel on pointer-offset views -- block j's pencil, coefficients, Ritz values,
+    status and scale live at fixed strides, and only the global last block is narrower."""
+    cplx = araw.dtype == C128
+    dmax = (3 if has_p else 2) * q
+    es = araw.element_size()
+    ka = min(k_act - j0 * q, (j1 - j0) * q)
+    name = "bk_subblock_pencils_z" if cplx else "bk_subblock_pencils_d"
+    wp, wb = _pencil_ws(j1 - j0, dmax, cplx)
+    _lib.call(name, ka, q, 1 if has_p else 0, araw.data_ptr() + j0 * dmax * dmax * es,
+              braw.data_ptr() + j0 * dmax * dmax * es, coef.data_ptr() + j0 * dmax * q * coef.element_size(),
+              theta.data_ptr() + j0 * q * 8, info.data_ptr() + j0 * 4 * 4, cscale.data_ptr() + j0 * 8,
+              0, wp, wb, stream_ptr())
 
 
 def subblock_recombine(n, k_act, q, has_p, coef, X, W, P, AX, AW, AP, Xo, Po, AXo, APo, ld, c0, flags,

@@ -13,9 +13,11 @@ column keeps its global position for the whole run, so
   * the active block is the column range [L, k_total) of XF, AXF, W, AW, P, AP;
   * P realignment in lock_and_compact (ppcg.py:399-408) is a zeroing of re-activated
     columns only;
-  * X/AX and P/AP are ping-pong pairs: the subblock update, CholQR and Rayleigh-Ritz write
-    the other buffer, so the pre-update blocks survive for the breakdown and
-    rank-deficiency recoveries (ppcg.py:694-717, 456-472) without copies.
+  * X/AX are ping-pong pairs: the subblock update, CholQR and Rayleigh-Ritz write the other
+    buffer, so the pre-update X survives for the breakdown and rank-deficiency recoveries
+    (ppcg.py:694-717, 456-472) without copies;
+  * P/AP are updated in place (no recovery path reads the pre-update P: both drop P), so the
+    state is 8 full-width blocks -- config 5 fits 8 GPUs (device_bytes_plan).
 """
 
 from __future__ import annotations
@@ -30,7 +32,7 @@ import numpy as np
 from .errors import DimensionError, RankDeficiencyError, SingularGramError
 from .trace import TraceRecord
 
-__all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSolver"]
+__all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSolver", "device_bytes_plan"]
 
 # host-sync trimming (bit 0: projections queued before the metric is read; bit 1: the
 # orthonormality Gram queued before the update's flags are read); PPCG_SPECULATE overrides
@@ -259,7 +261,10 @@ class PPCGSolver:
         raise DimensionError("operator applied to a block without ghost rows")
 
     def _red(self, *ts):
-        """Sum the row-partial results of a Gram / norm over the ranks (no-op on one GPU)."""
+        """Sum the row-partial results of a Gram / norm over the ranks (no-op on one GPU).
+        A padded-row view (rows of ld > columns, unit column stride) is reduced as the
+        contiguous span from its first to its last element: no gather/scatter copies; the
+        padding in between is summed too and never read."""
         if self.comm is None:
             return
         for t in ts:
@@ -267,6 +272,9 @@ class PPCGSolver:
                 continue
             if t.is_contiguous():
                 self.comm.allreduce_sum(t)
+            elif t.dim() == 2 and t.stride(1) == 1:
+                span = (t.shape[0] - 1) * t.stride(0) + t.shape[1]
+                self.comm.allreduce_sum(t.as_strided((span,), (1,)))
             else:
                 tmp = t.contiguous()
                 self.comm.allreduce_sum(tmp)
@@ -292,6 +300,11 @@ class PPCGSolver:
         # aligned rows for vector and bulk-tensor loads); columns keep global positions
         self.ldp = (kt + 15) // 16 * 16  # 128-byte rows (real): aligned TMA / bulk-copy row pieces
         self.side = torch.cuda.Stream()  # diagnostics that overlap the subblock pencils
+        # the pencils run on a high-priority stream: when they and the side stream's Gram
+        # become runnable together, the CTA scheduler dispatches the pencil CTAs first (a
+        # pencil CTA needs a whole SM's shared memory, so it cannot start on an SM that
+        # already holds Gram CTAs)
+        self.hi = torch.cuda.Stream(priority=-5)
         # (kernels.set_strip_stream can run the narrow strips of split Grams on a second
         # stream beside the main launch; measured slower end to end at config 2 -- the strip
         # CTAs only start as main CTAs retire and the fences add host work -- so it is off)
@@ -313,10 +326,10 @@ class PPCGSolver:
         self.AXF = [blk(), blk()]
         self.W = xblk()
         self.AW = blk()
-        self.P = [xblk(), xblk()]
-        self.AP = [blk(), blk()]
+        self.P = [xblk()]   # updated in place (subblock recombination writes P', AP' over P, AP)
+        self.AP = [blk()]
         self.xi = 0   # current X/AX buffer
-        self.pi = 0   # current P/AP buffer
+        self.pi = 0   # the P/AP buffer
         sq = lambda: z(kt, self.ldp)[:, :kt]  # noqa: E731  (even ld: 16-byte operand loads)
         self.Gm = sq()
         self.Gl = sq()
@@ -342,6 +355,8 @@ class PPCGSolver:
         self.h_rr_status = torch.zeros(4, dtype=torch.int32).pin_memory()
         q = self.opts.sbsize
         nbmax = (kt + q - 1) // q
+        if self.comm is not None:  # pencils split over the ranks: a whole chunk per rank
+            nbmax = -(-nbmax // self.comm.size) * self.comm.size
         dmax = 3 * q
         self.araw = z(nbmax * dmax * dmax)
         self.braw = z(nbmax * dmax * dmax)
@@ -351,7 +366,7 @@ class PPCGSolver:
             self.coef_tmp = z(nbmax * 4 * dmax * q, dt=torch.float64)
         else:
             self.gtmp, self.coef_tmp = None, None
-        self.theta = z(kt, dt=torch.float64)
+        self.theta = z(max(kt, nbmax * q), dt=torch.float64)
         self.info = torch.zeros(nbmax * 4, dtype=torch.int32, device="cuda")
         self.cscale = z(nbmax, dt=torch.float64)
         self.h_info = torch.zeros(nbmax * 4, dtype=torch.int32).pin_memory()
@@ -488,15 +503,37 @@ class PPCGSolver:
 
     def _householder_refresh(self):
         """X <- qr(X)[0], AX <- A X (ppcg.py:712-713, 756-757)."""
-        L = self.L
         x = self.X()
         if self.comm is None:
             self.dense.householder_q(x, self.AW)
-        else:  # tall QR of the whole block: gather, factor redundantly, keep own rows
-            full = self.comm.allgather_rows(x.contiguous(), self.bounds)
-            self.dense.householder_q(full, self.torch.empty_like(full))
-            x.copy_(full[self.plan.lo:self.plan.hi])
+        else:
+            self._shifted_cholqr3()
+            x = self.X()
         self._A(x, self.AX())
+
+    def _shifted_cholqr3(self):
+        """Row partition: the orthonormal basis of ppcg.py:712-713's qr(X) without gathering
+        the block -- shifted Cholesky-QR (G + s I, s = 11 (n k + k (k+1)) u ||X||_F^2 keeps the
+        factor positive definite at any conditioning) followed by two plain Cholesky-QR
+        passes, each a Gram + allreduce + k x k factor + tall triangular GEMM.  Spans the same
+        subspace as the Householder Q with columns equal up to sign/rounding (column signs
+        are equivariant in PPCG); this path runs only after a breakdown or a
+        rank-deficient CholQR, both of which drop P."""
+        K, torch = self.K, self.torch
+        L, ka = self.L, self.kt - self.L
+        for shift in (True, False, False):
+            x = self.X()
+            G = self.Gm[:ka, :ka]
+            K.gram(x, x, G, symmetric=True)
+            self._red(G)
+            if shift:
+                tr = float(torch.real(torch.diagonal(G)).sum().item())
+                s_ = 11.0 * (self.n * ka + ka * (ka + 1)) * 2.220446049250313e-16 * max(tr, 1e-300)
+                torch.diagonal(G).add_(s_)
+            self._cholqr_factor(G)
+            src, dst = self.xi, 1 - self.xi
+            K.tsgemm([self.XF[src][:, L:]], [self.Rm[:ka, :ka]], [self.XF[dst][:, L:]], upper=True)
+            self.xi = dst
 
     # ------------------------------------------------------------------ Rayleigh-Ritz
     def _ritz(self, fresh):
@@ -662,11 +699,6 @@ class PPCGSolver:
             def overlap(ready):  # after the pencil Grams (event `ready`): runs beside the pencils
                 self.side.wait_event(ready)
                 with torch.cuda.stream(self.side):
-                    # A pencil CTA needs a whole SM's shared memory, so it cannot start on an
-                    # SM holding Gram CTAs; if both become runnable together the Gram may take
-                    # every SM first (seen whenever the host runs ahead of the GPU).  A 20 us
-                    # stream-ordered delay lets the pencil CTAs be dispatched first.
-                    K.delay(20000)
                     K.gram(xfull, w, Gd, ws_kind="side")
                     K.small_stats(Gd, self.stats[5:8])
             self._overlap = overlap
@@ -678,7 +710,7 @@ class PPCGSolver:
         # subblock updates (ppcg.py:694-696) -> other buffers
         q = o.sbsize
         src, dst = self.xi, 1 - self.xi
-        psrc, pdst = self.pi, 1 - self.pi
+        psrc = pdst = self.pi  # P, AP in place
         self._subblock_update(ka, q, src, psrc, dst, pdst)
         nb = (ka + q - 1) // q
         main.wait_stream(self.side)
@@ -848,13 +880,24 @@ class PPCGSolver:
             K.subblock_grams(self.nl, ka, q, self.has_p, XFs.data_ptr(), self.W.data_ptr(), Ps.data_ptr(),
                              AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(), self._ldr(), self._c0r(L),
                              self.araw, self.braw, tmp=self.gtmp)
-            self._red(self.araw, self.braw)
             ready = self.torch.cuda.Event()
             ready.record()
-            K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
-                               self.cscale)
-            if overlap:
+            if self.comm is not None:
+                self._pencils_split(ka, q)
+            elif overlap:
+                # pencils on the high-priority stream, the side-stream diagnostic beside them
+                torch = self.torch
+                self.hi.wait_event(ready)
+                with torch.cuda.stream(self.hi):
+                    K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
+                                       self.cscale)
+                done = torch.cuda.Event()
+                done.record(self.hi)
                 overlap(ready)
+                torch.cuda.current_stream().wait_event(done)
+            else:
+                K.subblock_pencils(ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta, self.info,
+                                   self.cscale)
             self.flags64.zero_()
             K.subblock_recombine(self.nl, ka, q, self.has_p, self.coef, XFs.data_ptr(), self.W.data_ptr(),
                                  Ps.data_ptr(), AXFs.data_ptr(), self.AW.data_ptr(), APs.data_ptr(),
@@ -863,6 +906,29 @@ class PPCGSolver:
                                  coef_tmp=self.coef_tmp)
         if self.comm is not None:
             self.comm.allreduce_max(self.flags64)
+
+    def _pencils_split(self, ka, q):
+        """Row partition: the nb subblock pencils are independent (ppcg.py:515-519), so each
+        rank solves a contiguous chunk of them.  The raw pencil Grams are reduce-scattered
+        (rank r receives the sums of its chunk only), the chunk is solved, and the
+        coefficients, Ritz values, status words and coefficient scales are all-gathered --
+        instead of an allreduce of every Gram and nb replicated solves per rank."""
+        K, comm = self.K, self.comm
+        size, r = comm.size, comm.rank
+        nb = (ka + q - 1) // q
+        per = -(-nb // size)
+        dmax = (3 if self.has_p else 2) * q
+        dd = dmax * dmax
+        comm.reduce_scatter_sum(self.araw[: size * per * dd], per * dd)
+        comm.reduce_scatter_sum(self.braw[: size * per * dd], per * dd)
+        j0, j1 = r * per, min(nb, (r + 1) * per)
+        if j0 < j1:
+            K.subblock_pencils_range(j0, j1, ka, q, self.has_p, self.araw, self.braw, self.coef, self.theta,
+                                     self.info, self.cscale)
+        comm.allgather_chunks(self.coef[: size * per * dmax * q], per * dmax * q)
+        comm.allgather_chunks(self.theta[: size * per * q], per * q)
+        comm.allgather_chunks(self.info[: size * per * 4], per * 4)
+        comm.allgather_chunks(self.cscale[: size * per], per)
 
     def _orth(self, gact, loss):
         """_orth_active (ppcg.py:475-484)."""
@@ -925,8 +991,10 @@ class PPCGSolver:
         if self.it >= self.opts.max_iter:
             self.done = True
 
-    def finish(self):
-        """Final extraction (ppcg.py:760-787) and the host report."""
+    def finish(self, gather=None):
+        """Final extraction (ppcg.py:760-787) and the host report.  Row partition: each rank
+        downloads its own rows of the Ritz vectors and the (n, k) array is assembled on the
+        host (dist_ppcg_solve's ``gather``), never on a device."""
         K, torch = self.K, self.torch
         wall = (time.perf_counter() - self.t0) * 1e3
         k = self.k
@@ -938,9 +1006,16 @@ class PPCGSolver:
         self._fetch((self.omega, self.h_omega), (self.colnorm2, self.h_colnorm2))
         values = self.h_omega.numpy()[:k].copy()
         rn = np.sqrt(self.h_colnorm2.numpy()[:k]).tolist()
-        if self.comm is not None:
-            V = self.comm.allgather_rows(V.contiguous(), self.bounds)
         vectors = K.to_host(V)
+        extra = {}
+        if self.comm is not None:
+            if gather is None:
+                gather = "all" if self.n * k * V.element_size() <= 8 << 30 else "root"
+            full = self.comm.gather_rows_host(vectors, self.bounds, mode=gather)
+            if full is not None:
+                vectors = full
+            else:
+                extra["vector_rows"] = (self.plan.lo, self.plan.hi)
         self.xi = dst
         inc = [b.iteration for a_, b in zip(self.trace, self.trace[1:]) if b.trace_value > a_.trace_value]
         return SolveReport(values=values, vectors=vectors, trace=self.trace, status=self.status,
@@ -949,7 +1024,40 @@ class PPCGSolver:
                            values_history=self.values_history,
                            diagnostics={"orth_loss": self.orth_loss, "proj_defect": self.proj_defect,
                                         "final_residual_norms": rn, "cache_refreshes": self.refreshes,
-                                        "trace_increases": inc})
+                                        "trace_increases": inc, **extra})
+
+
+def device_bytes_plan(n_loc, n_ext, kt, q, cplx, nnz_loc=0, size=1):
+    """Device bytes one rank of PPCGSolver allocates (``_alloc``), by buffer family, plus the
+    largest transient scratch of an iteration: the budget check that config 5 (complex,
+    128^3, k_total 4178) fits 8 B200s.  n_loc rows owned, n_ext = owned + ghost rows."""
+    s = 16 if cplx else 8
+    ldp = (kt + 15) // 16 * 16
+    nb = -(-kt // q)
+    nb = -(-nb // size) * size if size > 1 else nb
+    dmax = 3 * q
+    out = {
+        # XF x2, W, P carry the ghost rows (operator inputs); AXF x2, AW, AP own rows only
+        "state_blocks": 4 * n_ext * ldp * s + 4 * n_loc * ldp * s,
+        "square_grams": 10 * kt * ldp * s + kt * kt * s,          # Gm .. Cm, eye
+        "pencil_buffers": nb * dmax * dmax * s * 2 + nb * dmax * q * s
+                          + ((nb * 4 * dmax * dmax * 8 * 2 + nb * 4 * dmax * q * 8) if cplx else 0),
+        "operator": nnz_loc * (s + 4) + (n_loc + 1) * 4 + n_loc * 58 * 8 + n_loc * 8,
+    }
+    try:
+        from . import _lib
+
+        lib = _lib.load(require_cuda=False)
+        r = 2 * kt if cplx else kt
+        gram_ws = int(lib.bk_gram_ws_bytes(n_ext, r, r))
+        sb_ws = int(lib.bk_subblock_grams_ws_bytes(n_ext, 2 * kt if cplx else kt, 2 * q if cplx else q, 1))
+    except Exception:  # library not built: the measured sizes at config 5 (~0.6 / 0.2 GB)
+        gram_ws, sb_ws = 6 << 27, 2 << 27
+    out["workspaces"] = 3 * gram_ws + sb_ws  # main / side / rr families
+    # transients: the complex Gram's real (2k x 2k) product, cuSOLVER's k_total eigensolver
+    out["transient"] = ((2 * kt) ** 2 * 8 if cplx else 0) + 2 * (kt * kt + 64 * kt) * s
+    out["total"] = sum(out.values())
+    return out
 
 
 def _stencil_plane(csr):

@@ -104,6 +104,17 @@ def _gloo_worker(rank, size, port, q):
         res["spmm_err"] = float(np.max(np.abs(y - (csr @ x)[p.lo:p.hi])))
         full = comm.allgather_rows(torch.from_numpy(y), bounds)
         res["gather_err"] = float(np.max(np.abs(full.numpy() - csr @ x)))
+        # the split pencils' collectives and the host assembly of the vectors
+        rs = (torch.arange(8, dtype=torch.float64) + 1) * (rank + 1)
+        comm.reduce_scatter_sum(rs, 4)
+        res["rs"] = rs[4 * rank:4 * rank + 4].tolist()
+        ag = torch.zeros(6, dtype=torch.complex128)
+        ag[3 * rank:3 * rank + 3] = torch.tensor([rank + 1j, 2.0 * rank, -1j * rank])
+        comm.allgather_chunks(ag, 3)
+        res["ag"] = ag.tolist()
+        res["host_all"] = comm.gather_rows_host(y, bounds, mode="all")
+        res["host_root"] = comm.gather_rows_host(y, bounds, mode="root")
+        res["y_full"] = csr @ x
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -129,6 +140,69 @@ def test_torchcomm_gloo_world2():
         assert res["zsum"] == [2 + 4j, 1 - 2j]
         assert res["max"] == [1, 10, 0]
         assert res["spmm_err"] <= 1e-12 and res["gather_err"] <= 1e-12
+        assert res["rs"] == [3.0 * (4 * r + i + 1) for i in range(4)]
+        assert res["ag"] == [1j, 0j, 0j, 1 + 1j, 2 + 0j, -1j]
+        np.testing.assert_allclose(res["host_all"], res["y_full"], rtol=0, atol=1e-12)
+        if r == 0:
+            np.testing.assert_allclose(res["host_root"], res["y_full"], rtol=0, atol=1e-12)
+        else:
+            assert res["host_root"] is None
+
+
+def test_threadcomm_split_collectives():
+    """ThreadComm (ranks as threads): reduce-scatter / chunk all-gather / host row assembly
+    with sums in rank order (bitwise what its allreduce gives)."""
+    import threading
+
+    import torch
+
+    from paper_1407_7506_b200.distributed import thread_comms
+
+    size = 3
+    comms = thread_comms(size)
+    out = [None] * size
+
+    def work(r):
+        c = comms[r]
+        a = torch.arange(9, dtype=torch.float64) * (r + 1) + 0.1
+        b = a.clone()
+        c.allreduce_sum(b)
+        c.reduce_scatter_sum(a, 3)
+        g = torch.full((6,), -1.0, dtype=torch.float64)
+        g[2 * r:2 * r + 2] = r
+        c.allgather_chunks(g, 2)
+        rows = [(0, 2), (2, 3), (3, 5)]
+        loc = np.full((rows[r][1] - rows[r][0], 2), float(r))
+        out[r] = (a[3 * r:3 * r + 3].tolist(), b[3 * r:3 * r + 3].tolist(), g.tolist(),
+                  c.gather_rows_host(loc, rows, "all"), c.gather_rows_host(loc, rows, "root"))
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(60)
+    for r in range(size):
+        rs, ar, g, hall, hroot = out[r]
+        assert rs == ar
+        assert g == [0.0, 0.0, 1.0, 1.0, 2.0, 2.0]
+        assert hall.tolist() == [[0.0, 0.0]] * 2 + [[1.0, 1.0]] + [[2.0, 2.0]] * 2
+        assert (hroot is None) == (r != 0)
+
+
+def test_config5_fits_eight_b200():
+    """Per-rank device bytes of config 5 (complex 128^3 Peierls, k_total 4178, q 64) on 8
+    GPUs: 8 state blocks (P, AP updated in place), ghost planes, Grams, pencil buffers,
+    workspaces and the largest transients stay under 170 GB of the 183 GB HBM; the vectors
+    are assembled on the host (PPCGSolver.finish), never on a device."""
+    from paper_1407_7506_b200.ppcg import device_bytes_plan
+
+    n, P, kt = 128 ** 3, 128 * 128, 4096 + 82
+    plan = device_bytes_plan(n // 8, n // 8 + 2 * P, kt, 64, True, 14581760 // 8 + 2 * P, 8)
+    assert plan["total"] < 170e9, plan
+    one_block = (n // 8) * ((kt + 15) // 16 * 16) * 16
+    assert plan["state_blocks"] < 8.6 * one_block  # 8 blocks (+ ghost planes), not 10
+    # config 4 on one GPU keeps the same accounting
+    assert device_bytes_plan(96 ** 3, 96 ** 3, 2048 + 41, 64, False, 23393656, 1)["total"] < 170e9
 
 
 def test_partition_rows_plane_aligned_for_stencils():

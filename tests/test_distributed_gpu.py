@@ -109,3 +109,87 @@ def test_torchrun_two_ranks_cli(cuda, tmp_path):
 
     v1, v2 = values(one.stdout), values(two.stdout)
     assert np.max(np.abs(v1 - v2) / np.abs(v1)) <= 1e-10
+
+
+def test_row_partition_more_ranks_than_pencils(cuda):
+    """The split pencils (reduce-scatter, a chunk of subblocks per rank, all-gather) when the
+    subblocks do not divide over the ranks: 2 subblocks on 3 ranks (rank 2 solves none)."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+
+    a, _, _, _ = config_problem(1, N=12)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=4, sbsize=4, tol=1e-9, seed=0, max_iter=60)
+    rep = _run_ranks(3, a, t, opts)[0]
+    ref = O.oracle_solve(HostCsr(a._csr), HostDiag(t.d), opts=opts)
+    assert rep.iterations == ref.iterations
+    for r1, r2 in zip(rep.trace, ref.trace):
+        assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-11 * abs(r2.trace_value)
+    assert np.max(np.abs(rep.values - ref.values) / np.abs(ref.values)) <= 1e-10
+
+
+def test_row_partition_breakdown_recovery(cuda, monkeypatch):
+    """Breakdown recovery over a row partition (ppcg.py:698-717): the orthonormal basis of the
+    pre-update X comes from shifted Cholesky-QR3 over the ranks instead of a gathered
+    Householder QR (same Q up to column signs, which PPCG is equivariant to): the trajectory
+    still follows the oracle's."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+    from paper_1407_7506_b200 import ppcg as PP
+
+    monkeypatch.setattr(PP, "_BREAKDOWN_MAX", 0.27)
+    monkeypatch.setattr(O, "BREAKDOWN_MAX", 0.27)
+    a, _, _, _ = config_problem(1, N=16)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=12, sbsize=4, tol=1e-8, seed=0, max_iter=25)
+    rep = _run_ranks(2, a, t, opts)[0]
+    ref = O.oracle_solve(HostCsr(a._csr), HostDiag(t.d), opts=opts)
+    assert ref.breakdown_recoveries > 0
+    assert rep.iterations == ref.iterations and rep.breakdown_recoveries == ref.breakdown_recoveries
+    for r1, r2 in zip(rep.trace, ref.trace):
+        assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
+        assert abs(r1.trace_value - r2.trace_value) <= 1e-10 * abs(r2.trace_value)
+
+
+def test_root_gather_and_memory_plan(cuda):
+    """gather="root": rank 0 holds the (n, k) vectors, the others their own rows only; and the
+    device memory the solver allocates stays within device_bytes_plan's per-rank budget."""
+    import threading
+
+    import torch
+
+    from paper_1407_7506_b200 import SolverOptions, config_problem, jacobi_preconditioner
+    from paper_1407_7506_b200.distributed import dist_ppcg_solve, thread_comms
+    from paper_1407_7506_b200.ppcg import PPCGSolver, device_bytes_plan
+
+    a, _, _, _ = config_problem(3, N=16)
+    t = jacobi_preconditioner(a)
+    opts = SolverOptions(k=60, sbsize=16, tol=1e-6, seed=0, max_iter=6)
+    comms = thread_comms(2)
+    out = [None, None]
+
+    def work(r):
+        out[r] = dist_ppcg_solve(a, t, None, opts, comm=comms[r], gather="root")
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(300)
+    assert out[0].vectors.shape == (a.n, 60)
+    lo, hi = out[1].diagnostics["vector_rows"]
+    np.testing.assert_array_equal(out[1].vectors, out[0].vectors[lo:hi])
+    # single-rank allocation vs the plan (state blocks, Grams, pencils, operator, workspaces)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    s = PPCGSolver(a, t, None, opts).start()
+    for _ in range(3):
+        s.step()
+    torch.cuda.synchronize()
+    used = torch.cuda.max_memory_allocated() - base
+    kt = s.kt
+    plan = device_bytes_plan(a.n, a.n, kt, 16, False, a._csr.nnz, 1)
+    assert used <= plan["total"], (used, plan)
+    assert plan["state_blocks"] >= 8 * a.n * ((kt + 15) // 16 * 16) * 8
+    del s
