@@ -603,6 +603,10 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
                        PSmem<double>& S) {
   constexpr int ZW = td_zw<PD>(), HL = ZW + 1;
   const int tid = threadIdx.x, lane = BK_LANE, warp = BK_WARP, nw = BK_NWARP;
+  // Z (d x ZW) with the column index XOR-swizzled by the row: a warp walking a column (lanes
+  // over rows) or a row (lanes over columns) touches every shared-memory bank evenly; rows
+  // of ZW = 32 doubles would otherwise put a whole column in one bank
+#define ZI(r, c) Z[(r) * ZW + ((c) ^ ((r) & 31))]
   double* dg = S.rc;              // diagonal of T (rc and rs are contiguous: PD doubles)
   double* e = A + (d - 1) * la;   // off-diagonal of T in the dead lower part of row d - 1
   double* p = scr;                // tau A22 v (v: reflector of the current column)
@@ -727,12 +731,11 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
   for (int b0 = 0; b0 < want; b0 += TD_BATCH) {
     const int j = b0 + tid;
     if (tid < TD_BATCH && j < want) {
-      double* u0 = scr + tid * 4 * PD;
-      double* u1 = u0 + PD;
-      double* u2 = u1 + PD;
-      double* x = u2 + PD;
+      // per-thread arrays interleaved across the batch (element i of thread t at
+      // (4 i + a) TD_BATCH + t): the batch's simultaneous accesses are consecutive words
+#define TD_U(a, i) scr[(4 * (i) + (a)) * TD_BATCH + tid]
       const double lj = shift[j];
-      for (int i = 0; i < d; ++i) x[i] = td_start(j, i);
+      for (int i = 0; i < d; ++i) TD_U(3, i) = td_start(j, i);
       for (int iter = 0; iter < 2 && !bad; ++iter) {
         // LU with partial pivoting of T - lj I (dgttrf), fused with the forward solve
         double cd = dg[0] - lj, cdu = d > 1 ? e[0] : 0.0;
@@ -741,38 +744,38 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
           if (fabs(cd) >= fabs(dl)) {
             const double piv = fabs(cd) < tiny ? copysign(tiny, cd) : cd;
             const double f = dl / piv;
-            u0[i] = piv;
-            u1[i] = cdu;
-            u2[i] = 0.0;
-            x[i + 1] -= f * x[i];
+            TD_U(0, i) = piv;
+            TD_U(1, i) = cdu;
+            TD_U(2, i) = 0.0;
+            TD_U(3, i + 1) -= f * TD_U(3, i);
             cd = nd - f * cdu;
             cdu = ndu;
           } else {
             const double f = cd / dl;
-            u0[i] = dl;
-            u1[i] = nd;
-            u2[i] = ndu;
-            const double t = x[i];
-            x[i] = x[i + 1];
-            x[i + 1] = t - f * x[i];
+            TD_U(0, i) = dl;
+            TD_U(1, i) = nd;
+            TD_U(2, i) = ndu;
+            const double t = TD_U(3, i);
+            TD_U(3, i) = TD_U(3, i + 1);
+            TD_U(3, i + 1) = t - f * TD_U(3, i);
             cd = cdu - f * nd;
             cdu = -f * ndu;
           }
         }
-        u0[d - 1] = fabs(cd) < tiny ? copysign(tiny, cd) : cd;
-        x[d - 1] /= u0[d - 1];
-        if (d >= 2) x[d - 2] = (x[d - 2] - u1[d - 2] * x[d - 1]) / u0[d - 2];
-        for (int i = d - 3; i >= 0; --i) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
+        TD_U(0, d - 1) = fabs(cd) < tiny ? copysign(tiny, cd) : cd;
+        TD_U(3, d - 1) /= TD_U(0, d - 1);
+        if (d >= 2) TD_U(3, d - 2) = (TD_U(3, d - 2) - TD_U(1, d - 2) * TD_U(3, d - 1)) / TD_U(0, d - 2);
+        for (int i = d - 3; i >= 0; --i) TD_U(3, i) = (TD_U(3, i) - TD_U(1, i) * TD_U(3, i + 1) - TD_U(2, i) * TD_U(3, i + 2)) / TD_U(0, i);
         double mx = 0.0;
-        for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(x[i]));
+        for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(TD_U(3, i)));
         if (!(mx > 0.0) || !isfinite(mx)) {
           bad = 1;
           break;
         }
         const double sc = 1.0 / mx;
-        for (int i = 0; i < d; ++i) x[i] *= sc;
+        for (int i = 0; i < d; ++i) TD_U(3, i) *= sc;
       }
-      for (int i = 0; i < d; ++i) Z[i * ZW + j] = x[i];
+      for (int i = 0; i < d; ++i) ZI(i, j) = TD_U(3, i);
     }
     __syncthreads();
   }
@@ -783,21 +786,21 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = warp; i < j; i += nw) {
         double s = 0.0;
-        for (int r = lane; r < d; r += 32) s += Z[r * ZW + i] * Z[r * ZW + j];
+        for (int r = lane; r < d; r += 32) s += ZI(r, i) * ZI(r, j);
         s = warp_sum(s);
         if (lane == 0) cf[i] = s;
       }
       __syncthreads();
       for (int r = tid; r < d; r += blockDim.x) {
-        double z = Z[r * ZW + j];
-        for (int i = 0; i < j; ++i) z -= cf[i] * Z[r * ZW + i];
-        Z[r * ZW + j] = z;
+        double z = ZI(r, j);
+        for (int i = 0; i < j; ++i) z -= cf[i] * ZI(r, i);
+        ZI(r, j) = z;
       }
       __syncthreads();
     }
     double n2 = 0.0;
     if (warp == 0) {
-      for (int r = lane; r < d; r += 32) n2 += Z[r * ZW + j] * Z[r * ZW + j];
+      for (int r = lane; r < d; r += 32) n2 += ZI(r, j) * ZI(r, j);
       n2 = warp_sum(n2);
       if (lane == 0) cf[ZW] = n2;
     }
@@ -805,7 +808,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     n2 = cf[ZW];
     if (!(n2 > 0.0) || !isfinite(n2)) return 1;  // (uniform)
     const double sc = 1.0 / sqrt(n2);
-    for (int r = tid; r < d; r += blockDim.x) Z[r * ZW + j] *= sc;
+    for (int r = tid; r < d; r += blockDim.x) ZI(r, j) *= sc;
     __syncthreads();
   }
   // ---- 3c. Rayleigh-Ritz in span(Z): H = Z^T T Z (T Z formed on the fly), Jacobi, Z <- Z U
@@ -815,17 +818,17 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
       if (b < a) continue;
       double h = 0.0, h2 = 0.0;
       for (int r = 0; r < d; ++r) {
-        double tb = dg[r] * Z[r * ZW + b], ta = dg[r] * Z[r * ZW + a];
+        double tb = dg[r] * ZI(r, b), ta = dg[r] * ZI(r, a);
         if (r > 0) {
-          tb += e[r - 1] * Z[(r - 1) * ZW + b];
-          ta += e[r - 1] * Z[(r - 1) * ZW + a];
+          tb += e[r - 1] * ZI(r - 1, b);
+          ta += e[r - 1] * ZI(r - 1, a);
         }
         if (r < d - 1) {
-          tb += e[r] * Z[(r + 1) * ZW + b];
-          ta += e[r] * Z[(r + 1) * ZW + a];
+          tb += e[r] * ZI(r + 1, b);
+          ta += e[r] * ZI(r + 1, a);
         }
-        h += Z[r * ZW + a] * tb;
-        h2 += Z[r * ZW + b] * ta;
+        h += ZI(r, a) * tb;
+        h2 += ZI(r, b) * ta;
       }
       h = 0.5 * (h + h2);
       H[a * HL + b] = h;
@@ -849,7 +852,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     for (int r = warp; r < d; r += nw) {
       double zr[ZW / 32];
 #pragma unroll
-      for (int c = 0; c < ZW / 32; ++c) zr[c] = c * 32 + lane < want ? Z[r * ZW + c * 32 + lane] : 0.0;
+      for (int c = 0; c < ZW / 32; ++c) zr[c] = c * 32 + lane < want ? ZI(r, c * 32 + lane) : 0.0;
       double out[ZW / 32];
 #pragma unroll
       for (int c = 0; c < ZW / 32; ++c) out[c] = 0.0;
@@ -864,7 +867,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
       __syncwarp();
 #pragma unroll
       for (int c = 0; c < ZW / 32; ++c)
-        if (c * 32 + lane < want) Z[r * ZW + c * 32 + lane] = out[c];
+        if (c * 32 + lane < want) ZI(r, c * 32 + lane) = out[c];
     }
     __syncthreads();
   }
@@ -883,7 +886,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
           const int j = warp + c * nw;
-          if (j < want) dot[c] += w * Z[(k + 1 + i) * ZW + j];
+          if (j < want) dot[c] += w * ZI(k + 1 + i, j);
         }
       }
 #pragma unroll
@@ -893,7 +896,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
 #pragma unroll
         for (int c = 0; c < CPW; ++c) {
           const int j = warp + c * nw;
-          if (j < want) Z[(k + 1 + i) * ZW + j] -= w * dot[c];
+          if (j < want) ZI(k + 1 + i, j) -= w * dot[c];
         }
       }
       __syncwarp();
@@ -904,9 +907,9 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
         const int m = d - k - 1;
         const double* wk = A + k * la + k + 1;
         double dot = 0.0;
-        for (int i = lane; i < m; i += 32) dot += wk[i] * Z[(k + 1 + i) * ZW + j];
+        for (int i = lane; i < m; i += 32) dot += wk[i] * ZI(k + 1 + i, j);
         dot = warp_sum(dot);
-        for (int i = lane; i < m; i += 32) Z[(k + 1 + i) * ZW + j] -= wk[i] * dot;
+        for (int i = lane; i < m; i += 32) ZI(k + 1 + i, j) -= wk[i] * dot;
         __syncwarp();
       }
     }
@@ -914,10 +917,12 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
   __syncthreads();
   // eigenvectors -> A[:, 0:want], eigenvalues -> ev[0:want] (ascending), ord = identity
   for (int i = warp; i < d; i += nw)
-    for (int j = lane; j < want; j += 32) A[i * la + j] = Z[i * ZW + j];
+    for (int j = lane; j < want; j += 32) A[i * la + j] = ZI(i, j);
   for (int j = tid; j < want; j += blockDim.x) S.ord[j] = j;  // ev set by the Rayleigh-Ritz step
   __syncthreads();
   return 0;
+#undef TD_U
+#undef ZI
 }
 
 // ---------------------------------------------------------------- one pencil attempt

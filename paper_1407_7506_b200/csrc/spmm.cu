@@ -380,6 +380,7 @@ struct MarchArgs {
   int xlo;             // first plane the X tensor map covers
   int gy, gz, nslices, xseg, nunits;
   int m, off;          // columns, and leading columns of the slices before column 0 (alignment)
+  int order;           // stencil-slot unit order: 0 = slice fastest, 1 = (y, z) tile fastest
   int npieces;         // 16-byte pieces of a row from the slices' origin to the block's end
   int vdoubles;        // ELL value row in doubles (real: even width; complex: 2 x width)
   int woff;            // ELL offset row in uint16 (multiple of 8)
@@ -761,12 +762,28 @@ struct StUnit {
 
 BK_DEV StUnit st_unit(const MarchArgs& A, int u) {
   StUnit U;
-  U.s = u % A.nslices;
-  u /= A.nslices;
-  const int seg = u % A.xseg;
-  u /= A.xseg;
-  U.z0 = (u % A.gz) * M_T;
-  U.y0 = (u / A.gz) * M_T;
+  int seg, tile;
+  if (A.order == 0) {  // slice fastest: the slices of a tile share its entries (27-point: > L2)
+    U.s = u % A.nslices;
+    u /= A.nslices;
+    seg = u % A.xseg;
+    tile = u / A.xseg;
+  } else if (A.order == 2) {  // slice, then tile, x segment slowest
+    U.s = u % A.nslices;
+    u /= A.nslices;
+    const int ntiles = A.gy * A.gz;
+    tile = u % ntiles;
+    seg = u / ntiles;
+  } else {  // tile fastest: a wave covers whole planes of one slice, so every halo row is read
+            // by all tiles needing it at the same time (7-point: entries of all slices fit L2)
+    const int ntiles = A.gy * A.gz;
+    tile = u % ntiles;
+    u /= ntiles;
+    seg = u % A.xseg;
+    U.s = u / A.xseg;
+  }
+  U.z0 = (tile % A.gz) * M_T;
+  U.y0 = (tile / A.gz) * M_T;
   U.xa = (int)((int64_t)seg * A.nx / A.xseg);
   U.xb = (int)((int64_t)(seg + 1) * A.nx / A.xseg);
   U.dir = (seg & 1) ? -1 : 1;
@@ -978,12 +995,18 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
 
 // stencil-slot kernel variants: (COLS, NP, RZ) per stencil; the knob selects among them for sweeps
 static int bk_stencil_cfg = 0;
+static int bk_stencil_order = -1;  // unit order override (sweeps): -1 = per stencil default
+static int bk_stencil_xseg = 0;    // x segment count override (sweeps): 0 = cost model
 
 }  // namespace bk
 
+// cfg = variant + 10 (order + 1) + 100 xseg: variant 0/1; order 0 slice-(segment)-tile, 1 tile
+// fastest, 2 slice-tile-segment; xseg forces the x segment count (0: cost model)
 extern "C" int bk_spmm_stencil_set_config(int cfg) {
-  if (cfg < 0 || cfg > 3) return BK_ERR_ARG;
-  bk::bk_stencil_cfg = cfg;
+  if (cfg < 0 || cfg % 100 > 39) return BK_ERR_ARG;
+  bk::bk_stencil_cfg = cfg % 10;
+  bk::bk_stencil_order = (cfg / 10) % 10 - 1;
+  bk::bk_stencil_xseg = cfg / 100;
   return BK_OK;
 }
 
@@ -1085,7 +1108,14 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
       A.xseg = xs;
     }
   }
+  // 7-point: segments of ~12 planes, segment slowest (every wave marches one segment in
+  // lockstep over all slices of a band of tiles), odd segments downward: measured best over
+  // xseg 1..16 x three unit orders at configs 2, 3 and 5 (profiles/stencil_sweep_r02.jsonl:
+  // config 2 0.212 -> 0.175 ms, 0.68 -> 0.82 of HBM)
+  if (st == 7) A.xseg = (int)lmax(1, (nx + 6) / 12);
+  if (bk_stencil_xseg > 0) A.xseg = (int)lmin(bk_stencil_xseg, nx);
   A.nunits = (int)(per_seg * A.xseg);
+  A.order = st == 7 ? (bk_stencil_order >= 0 ? bk_stencil_order : 2) : (bk_stencil_order >= 0 ? bk_stencil_order : 0);
   // per launch: the attribute belongs to the current device's context (cheap)
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)lmin(A.nunits, kSMs);

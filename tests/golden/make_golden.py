@@ -4,7 +4,8 @@ Run in the build container only (the reference does not exist on the GPU box):
 
     python tests/golden/make_golden.py            # kernels, generators, config-1, small solves
     python tests/golden/make_golden.py --cfg2     # + config-2 first iterations (~3 min, 12 GB)
-    python tests/golden/make_golden.py --cfg2-full  # config-2 solve to convergence (~1-2 h, 12 GB)
+    python tests/golden/make_golden.py --cfg2-full  # config-2 solve to convergence (~40 min, 12 GB)
+    python tests/golden/make_golden.py --scaled     # configs 3-5 on scaled grids, q = 64
 
 Every fixture records the inputs (or their seeds/recipes) and the reference outputs.  The
 CPU tests pin the oracle (oracle/ppcg_oracle.py) against these files; the GPU tests check
@@ -256,15 +257,47 @@ def cfg2_full(blas_threads):
     np.savez_compressed(os.path.join(HERE, "cfg2_full.npz"), **out)
 
 
+SCALED = {  # BASELINE configs 3-5 at the largest size the reference solves in minutes here
+    "cfg3_n32": (3, 32, dict(k=256, sbsize=64, tol=1e-6)),
+    "cfg4_n24": (4, 24, dict(k=256, sbsize=64, tol=1e-5)),
+    "cfg5_n24": (5, 24, dict(k=256, sbsize=64, tol=1e-5)),
+}
+
+
+def scaled(blas_threads):
+    """Configs 3, 4 and 5 on scaled grids with the production block shape (q = 64: the
+    d = 192 pencils, the 7-/27-point and complex stencil SpMMs in their production mode),
+    solved to convergence by the reference (BLAS xN as in cfg2_full)."""
+    from threadpoolctl import threadpool_limits
+
+    BP.threadpool_limits = lambda limits=1: threadpool_limits(limits=blas_threads)
+    out = {}
+    for name, (cfg, N, kw) in SCALED.items():
+        ours, _, _, _ = P.config_problem(cfg, N=N)
+        a = B.SparseHermitian(ours._csr, "hermitian" if cfg == 5 else "symmetric")
+        t = B.jacobi_preconditioner(a)
+        t0 = time.time()
+        rep = B.ppcg_solve(a, t, opts=B.SolverOptions(seed=0, max_iter=3000, **kw))
+        print(f"{name}: {rep.status} {rep.iterations} it {rep.rr_count} RR in {time.time() - t0:.1f}s", flush=True)
+        _report_arrays(name, rep, out, vectors=False)
+        out[f"{name}_vec_lo"] = np.ascontiguousarray(rep.vectors[:, :4])
+        out[f"{name}_vec_hi"] = np.ascontiguousarray(rep.vectors[:, -4:])
+    np.savez_compressed(os.path.join(HERE, "scaled.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--baselines", action="store_true")
     ap.add_argument("--cfg2-full", action="store_true")
+    ap.add_argument("--scaled", action="store_true")
     ap.add_argument("--blas-threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     if args.cfg2_full:
         cfg2_full(args.blas_threads)
+        sys.exit(0)
+    if args.scaled:
+        scaled(args.blas_threads)
         sys.exit(0)
     if args.baselines:
         baselines()

@@ -33,4 +33,20 @@ for name, slot in (("march", False), ("slot", True)):
 for _ in range(3):
     y.copy_(x)
 torch.cuda.synchronize()
-print("ok", cfg, a.n, kt - off)
+# CUDA-event times (not under ncu these are the numbers to quote): each kernel and the copy
+res = {}
+for name, fn in (("march", lambda: (setattr(d.stencil, "use_slot", False), d.apply_into(x, y))),
+                 ("slot", lambda: (setattr(d.stencil, "use_slot", True), d.apply_into(x, y))),
+                 ("copy", lambda: y.copy_(x))):
+    fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        fn()
+    e1.record()
+    e1.synchronize()
+    res[name] = e0.elapsed_time(e1) / 20
+m = kt - off
+s = 16 if d.complex else 8
+byts = 2.0 * a.n * m * s + d.nnz * (s + 4) + 4 * (a.n + 1)
+print({k: (round(v, 4), round(byts / v / 1e6, 1)) for k, v in res.items()}, "bytes", byts)

@@ -24,6 +24,11 @@ def hbm_peak():
         return 6554.6
 
 
+# stencil-slot configurations (bk_spmm_stencil_set_config): v (variant), 10 + v (slice-fastest
+# unit order), 20 + v (tile-fastest unit order)
+SLOT_CFGS = [int(c) for c in os.environ.get("SLOT_CFGS", "0,1,10,20,21").split(",")]
+
+
 def main():
     cfgs = [int(c) for c in sys.argv[1:]] or [2, 3, 4, 5]
     lib = _lib.load()
@@ -46,8 +51,9 @@ def main():
             x, y = xb[:, off:off + m], yb[:, off:off + m]
             byts = 2.0 * a.n * m * s + d.nnz * (s + 4) + 4 * (a.n + 1)
             ref = None
-            for name, stencil, slot, cfgv in (("vec", False, False, 0), ("march", True, False, 0),
-                                             ("slot0", True, True, 0), ("slot1", True, True, 1)):
+            variants = [("vec", False, False, 0), ("march", True, False, 0)]
+            variants += [(f"slot{c}", True, True, c) for c in SLOT_CFGS]
+            for name, stencil, slot, cfgv in variants:
                 DeviceCsr.use_stencil = stencil
                 plan.use_slot = slot
                 lib.bk_spmm_stencil_set_config(cfgv)
@@ -69,6 +75,17 @@ def main():
                                   "kernel": name, "ms": round(ms, 4), "gbs": round(byts / ms / 1e6, 1),
                                   "frac_hbm": round(byts / ms / 1e6 / peak, 3),
                                   "bitwise_equal_to_gather": bool(torch.equal(out, ref))}), flush=True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            y.copy_(x)
+            e0.record()
+            for _ in range(20):
+                y.copy_(x)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / 20
+            print(json.dumps({"cfg": cfg, "m": m, "col_offset": off, "kernel": "copy (same block, torch)",
+                              "ms": round(ms, 4), "gbs_spmm_bytes": round(byts / ms / 1e6, 1),
+                              "frac_hbm": round(byts / ms / 1e6 / peak, 3)}), flush=True)
             del ref, out
         lib.bk_spmm_stencil_set_config(0)
         DeviceCsr.use_stencil = True
