@@ -109,6 +109,9 @@ int bk_subblock_grams_d(int64_t n, int k_act, int q, int has_p, const double* X,
                         const double* P, const double* AX, const double* AW, const double* AP,
                         int64_t ld, int64_t c0, double* Araw, double* Braw, void* ws,
                         int64_t ws_bytes, void* stream);
+/* split-K waves of the paired (q = 32) subblock Grams (default 2; 0 = choose_chunks; -1 =
+ * query); returns the previous value */
+int bk_subblock_grams_set_waves(int waves);
 /* complex128 blocks (interleaved; ld, c0 in complex elements); tmpA/tmpB: nb*(2*dmax)^2 doubles */
 int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X, const double* W,
                         const double* P, const double* AX, const double* AW, const double* AP,

@@ -41,6 +41,7 @@ _SIGS = {
     "bk_spmm_stencil_z": (c_int, [c_int, c_int, c_int, c_int, c_int, c_i64, vp, c_int, c_int, c_int, vp, c_i64,
                                   vp, c_i64, c_int, vp]),
     "bk_spmm_stencil_set_config": (c_int, [c_int]),
+    "bk_subblock_grams_set_waves": (c_int, [c_int]),
     "bk_scale_rows_d": (c_int, [c_i64, c_int, vp, vp, c_i64, vp, c_i64, vp]),
     "bk_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int]),
     "bk_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),

@@ -901,13 +901,10 @@ static int launch_gram_cfg(GramParams& P, int64_t total_tiles_slots, void* ws, i
   const int64_t grid = (int64_t)P.nprob * P.max_tiles * P.nchunks;
   if (grid <= 0) return BK_OK;
   if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    cudaFuncSetAttribute(gram_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM + 16 * C::STAGES);
-    attr = true;
-  }
+  // per launch (cheap): the attribute belongs to the current device's context
+  cudaFuncSetAttribute(gram_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaFuncSetAttribute(gram_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       C::SMEM + 16 * C::STAGES);
   BK_COUNT();
   if constexpr (C::BM == 96 && C::BN == 96) if (maps) {
     constexpr int tsmem = C::STAGES * 2 * SB_TMA_STAGE * (int)sizeof(double) + 16 * C::STAGES + 1024;
@@ -1015,11 +1012,8 @@ static int launch_combo(GramParams& A, GramParams& B, void* ws, int64_t ws_bytes
   const int64_t grid = (ta + tb) * nch;
   if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
   const int smem = max(CA::SMEM + 16 * CA::STAGES, CB::SMEM + 16 * CB::STAGES);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_bulk_combo<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  // per launch (cheap): the attribute belongs to the current device's context
+  cudaFuncSetAttribute(gram_bulk_combo<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   BK_COUNT();
   gram_bulk_combo<CA, CB><<<(unsigned)grid, CA::THREADS + 32, smem, st>>>(A, B);
   BK_CHECK_LAUNCH();
@@ -1270,11 +1264,39 @@ static int gram2_d(int64_t n, int m1a, int m2a, const double* X1, int64_t ldx1, 
   return gram_problems(2, P.prob, n, ws, ws_bytes, (cudaStream_t)stream, part);
 }
 
+// split-K grid of the paired subblock Grams: `waves` CTA waves (one CTA per SM): fewer, longer
+// chunks than choose_chunks' 8 waves halve the partial-sum traffic and the last-CTA
+// reductions; config 2 measured 36.9 (8 waves), 36.9 (4), 37.1 (2), 36.9 (1) it/s -- within
+// the ~1% run-to-run spread, so 2 is kept for the traffic.  0 = choose_chunks.  A chunk keeps
+// >= 32 stages (the choose_chunks floor), and the count depends on n and nb only, never on the
+// workspace a caller happens to hold (bk_subblock_grams_ws_bytes sizes it exactly).
+static int g_sbpair_waves = [] {
+  const char* e = getenv("PPCG_SBPAIR_WAVES");
+  return e ? atoi(e) : 2;
+}();
+
+static int sb_pair_chunks(int64_t n, int nb) {
+  const int64_t cmax = lmax(1, lmin(256, n / (32 * G_BK)));
+  if (g_sbpair_waves <= 0) return choose_chunks(n, nb, 1);
+  return (int)lmax(1, lmin(cmax, (int64_t)g_sbpair_waves * kSMs / lmax(1, nb)));
+}
+
+extern "C" int bk_subblock_grams_set_waves(int waves) {
+  if (waves < -1 || waves > 64) return BK_ERR_ARG;
+  const int prev = g_sbpair_waves;
+  if (waves >= 0) g_sbpair_waves = waves;
+  return prev;
+}
+
 extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int has_p) {
   const int nb = (k_act + q - 1) / q;
   const int dmax = (has_p ? 3 : 2) * q;
   if (use_big(dmax)) return ws_bytes_for<Big>(n, (int64_t)2 * nb * ((dmax + 63) / 64) * ((dmax + 127) / 128));
-  if (dmax > 64 && dmax <= 96) return ws_bytes_for<Sb96>(n, (int64_t)2 * nb);
+  if (dmax > 64 && dmax <= 96) {
+    // the paired launch (exactly its chunk count) or the per-Gram fallback, whichever is larger
+    const int64_t pair = kTicketBytes + (int64_t)2 * nb * sb_pair_chunks(n, nb) * Sb96::BM * Sb96::BN * 8;
+    return lmax(pair, ws_bytes_for<Sb96>(n, (int64_t)2 * nb));
+  }
   const int t = (dmax + 63) / 64;
   return ws_bytes_for<Small>(n, (int64_t)2 * nb * t * t);
 }
@@ -1282,16 +1304,7 @@ extern "C" int64_t bk_subblock_grams_ws_bytes(int64_t n, int k_act, int q, int h
 // both Grams of each subblock in one CTA (gram_sb_pair_kernel): grid nb x chunks, one CTA per SM
 template <class C>
 static int launch_sb_pair(GramParams& P, int nb, void* ws, int64_t ws_bytes, cudaStream_t st, const SbMaps& M) {
-  // split-K grid of 2 CTA waves (one CTA per SM): fewer, longer chunks than choose_chunks' 8
-  // waves halve the partial-sum traffic and the last-CTA reductions; config 2 measured 36.9 (8
-  // waves), 36.9 (4), 37.1 (2), 36.9 (1) it/s.  PPCG_SBPAIR_WAVES overrides (0 = choose_chunks)
-  static const int waves = [] {
-    const char* e = getenv("PPCG_SBPAIR_WAVES");
-    return e ? atoi(e) : 2;
-  }();
-  P.nchunks = P.force_chunks > 0 ? P.force_chunks
-              : waves > 0        ? (int)lmax(1, lmin(256, (int64_t)waves * kSMs / lmax(1, nb)))
-                                 : choose_chunks(P.nrows, nb, 1);
+  P.nchunks = P.force_chunks > 0 ? P.force_chunks : sb_pair_chunks(P.nrows, nb);
   auto part_bytes = [&] { return (int64_t)P.nprob * P.nchunks * C::BM * C::BN * (int64_t)sizeof(double); };
   if (P.nchunks > 1) {
     while (P.nchunks > 1 && kTicketBytes + part_bytes() > ws_bytes) P.nchunks = (P.nchunks + 1) / 2;
@@ -1306,11 +1319,8 @@ static int launch_sb_pair(GramParams& P, int nb, void* ws, int64_t ws_bytes, cud
   if (grid <= 0) return BK_OK;
   if (grid > 0x7fffffff) return BK_ERR_UNSUPPORTED;
   constexpr int smem = SB_PAIR_STAGES * 2 * SB_TMA_STAGE * (int)sizeof(double) + 16 * SB_PAIR_STAGES + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_sb_pair_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  // per launch (cheap): the attribute belongs to the current device's context
+  cudaFuncSetAttribute(gram_sb_pair_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   BK_COUNT();
   gram_sb_pair_kernel<C><<<(unsigned)grid, 2 * C::THREADS + 32, smem, st>>>(P, M);
   BK_CHECK_LAUNCH();

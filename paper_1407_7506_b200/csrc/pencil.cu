@@ -1289,15 +1289,12 @@ static int64_t p_ws_bytes(int nb, int dmax) {
 
 template <class T, int PD, bool GMEM>
 static void launch_variant(const PencilParams& P, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         p_smem_bytes<T, PD, GMEM>());
-    // the complex large variant streams its matrices through L1: keep the carveout small
-    if (GMEM && !kOwnPk<T, PD>)
-      cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    attr = true;
-  }
+  // per launch (cheap): the attribute belongs to the current device's context
+  cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       p_smem_bytes<T, PD, GMEM>());
+  // the complex large variant streams its matrices through L1: keep the carveout small
+  if (GMEM && !kOwnPk<T, PD>)
+    cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
   pencil_kernel<T, PD, GMEM><<<P.nb, P_THREADS, p_smem_bytes<T, PD, GMEM>(), st>>>(P);
 }
 

@@ -266,11 +266,8 @@ template <class C>
 static int launch_ts(TsParams& P, cudaStream_t st) {
   dim3 grid((P.N + C::BN - 1) / C::BN, (unsigned)((P.n + T_BM - 1) / T_BM), P.nprob);
   if (grid.y > 65535) return BK_ERR_UNSUPPORTED;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tsgemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  // per launch (cheap): the attribute belongs to the current device's context
+  cudaFuncSetAttribute(tsgemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   BK_COUNT();
   tsgemm_kernel<C><<<grid, T_THREADS, C::SMEM, st>>>(P);
   BK_CHECK_LAUNCH();

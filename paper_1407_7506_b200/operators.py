@@ -341,10 +341,35 @@ class DeviceCallback:
             np.complex128 if y.dtype == torch.complex128 else np.float64)))
 
 
+def _source_key(op):
+    """What the device copy was made from: the identity and shape of the host arrays plus a
+    sampled fingerprint of their values, so replacing (or editing) an operator's arrays after a
+    solve rebuilds the device form instead of silently reusing a stale one (the reference reads
+    the operator on every apply)."""
+    def fp(a):
+        a = np.asarray(a)
+        if a.size == 0:
+            return (id(a), 0)
+        step = max(1, a.size // 4096)
+        flat = a.reshape(-1)[::step]
+        return (id(a), a.shape, a.dtype.str, complex(np.sum(flat * (1.0 + np.arange(flat.size) % 7))))
+
+    if hasattr(op, "_csr"):
+        c = op._csr
+        return ("csr", fp(c.data), fp(c.indices), fp(c.indptr), c.shape)
+    for attr in ("matrix", "diag", "d"):
+        if hasattr(op, attr):
+            return (attr, fp(getattr(op, attr)))
+    return ("callback", id(op))
+
+
 def as_device_operator(op):
-    """Device form of an operator (cached on the object when possible)."""
+    """Device form of an operator (cached on the object, keyed by its source arrays)."""
+    if isinstance(op, CountingOperator):
+        return as_device_operator(op.inner)
+    key = _source_key(op)
     cached = getattr(op, "_dev", None)
-    if cached is not None:
+    if cached is not None and getattr(op, "_dev_key", None) == key:
         return cached
     if hasattr(op, "_csr"):
         dev = DeviceCsr(op._csr)
@@ -354,12 +379,10 @@ def as_device_operator(op):
         dev = DeviceDiag(op.diag)
     elif hasattr(op, "d") and type(op).__name__ == "DiagonalPreconditioner":
         dev = DeviceDiag(op.d)
-    elif isinstance(op, CountingOperator):
-        return as_device_operator(op.inner)
     else:
         dev = DeviceCallback(op)
     try:
-        op._dev = dev
+        op._dev, op._dev_key = dev, key
     except Exception:
         pass
     return dev

@@ -248,14 +248,25 @@ def test_subblock_update_vs_oracle(cuda, n, m, q, with_p):
         assert abs(cs[j] - r.coeff_scale) <= 1e-8 * r.coeff_scale
 
 
-@pytest.mark.parametrize("n,m,q,c0,extra", [(5003, 109, 32, 2, 6), (4099, 96, 32, 0, 0), (777, 70, 24, 4, 2),
-                                            (20000, 40, 32, 6, 0)])
-def test_subblock_grams_raw(cuda, n, m, q, c0, extra):
+@pytest.mark.parametrize("n,m,q,c0,extra,waves", [(5003, 109, 32, 2, 6, None), (4099, 96, 32, 0, 0, None),
+                                                  (777, 70, 24, 4, 2, None), (20000, 40, 32, 6, 0, None),
+                                                  (300, 75, 32, 3, 1, None), (9000, 107, 32, 1, 3, 0),
+                                                  (9000, 107, 32, 1, 3, 8)])
+def test_subblock_grams_raw(cuda, n, m, q, c0, extra, waves):
     """Raw pencil Grams A_j = S_j^T [AX AW AP]_j, B_j = S_j^T S_j (q <= 32 with P: the TMA-box
-    loader) against numpy, with column offsets, padded rows and a ragged last subblock."""
+    loader) against numpy, with column offsets, padded rows and a ragged last subblock; the
+    paired kernel's single-chunk direct store (n = 300) and its split-K wave settings."""
+    from paper_1407_7506_b200 import _lib
     from paper_1407_7506_b200 import kernels as K
 
     torch = cuda
+    if waves is not None:
+        prev = _lib.load().bk_subblock_grams_set_waves(waves)
+        try:
+            test_subblock_grams_raw(cuda, n, m, q, c0, extra, None)
+        finally:
+            _lib.load().bk_subblock_grams_set_waves(prev)
+        return
     ld = c0 + m + extra
     rng = np.random.default_rng(n + m)
     host = [rng.standard_normal((n, ld)) for _ in range(6)]

@@ -232,3 +232,17 @@ def test_guard_branches_match_oracle(cuda, monkeypatch, which):
     for r1, r2 in zip(rep.trace, ref.trace):
         assert r1.n_locked == r2.n_locked and r1.n_matvec == r2.n_matvec
         assert abs(r1.trace_value - r2.trace_value) <= 1e-10 * abs(r2.trace_value)
+
+
+def test_operator_arrays_replaced_after_solve(cuda):
+    """The device copy of an operator follows its host arrays: replacing the CSR values after
+    a solve (here A -> 2A) gives the new spectrum, not the cached one (operators.py
+    as_device_operator, keyed by the source arrays)."""
+    from paper_1407_7506_b200 import SolverOptions, config_problem, ppcg_solve
+
+    a, _, _, _ = config_problem(1, N=12)
+    opts = SolverOptions(k=4, sbsize=4, tol=1e-9, seed=0, max_iter=400)
+    v1 = ppcg_solve(a, opts=opts).values
+    a._csr.data = a._csr.data * 2.0
+    v2 = ppcg_solve(a, opts=opts).values
+    np.testing.assert_allclose(v2, 2.0 * v1, rtol=1e-9)
