@@ -155,3 +155,8 @@ BK_DEV cplx cfma(cplx a, cplx b, cplx c) {  // a*b + c
 }
 
 }  // namespace bk
+
+namespace bk {
+// hint a 128-byte line into L2 (no register result, no ordering)
+BK_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
+}  // namespace bk

@@ -133,8 +133,24 @@ __global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid
 
   const int fk = lane & 3, fm = lane >> 2;
 
-  // one K phase over [kbeg, kstop)
-  auto run_phase = [&](int kbeg, int kstop) {
+  // the epilogue's Z tile (and row scales) are known now: pull them into L2 while the K loop
+  // runs, so the epilogue loads do not expose an HBM round trip at the end of every CTA
+  if (P.beta != 0.0 && pr.Z != nullptr && pr.Y != nullptr) {
+    constexpr int LINES = BN * 8 / 128 > 0 ? BN * 8 / 128 : 1;  // 128-byte lines per tile row
+    for (int e = tid; e < T_BM * LINES; e += T_THREADS) {
+      const int64_t row = r0 + e / LINES;
+      const int col = n0 + (e % LINES) * 16;
+      if (row < P.n && col < P.N) prefetch_l2(pr.Z + row * P.ldz + col);
+    }
+  }
+  if (P.rowscale != nullptr && pr.Y != nullptr && tid < T_BM / 16) {
+    const int64_t row = r0 + tid * 16;
+    if (row < P.n) prefetch_l2(P.rowscale + row);
+  }
+
+  // one K phase over [kbeg, kstop); after stage `snap` (if >= 0) runs snap_fn() on the
+  // partial accumulators without draining the cp.async pipeline
+  auto run_phase = [&](int kbeg, int kstop, int snap, auto&& snap_fn) {
     if (kstop <= kbeg) return;
     const bool vx = P.vec_x && !(kbeg & 1);
     const int nst = (kstop - kbeg + T_BK - 1) / T_BK;
@@ -180,15 +196,15 @@ __global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid
           }
         }
       }
+      if (s == snap) snap_fn();
     }
     cp_async_wait<0>();
     __syncthreads();
   };
+  auto no_snap = [] {};
 
   // element (a,b,e) -> row wr0 + a*8 + lane/4, col wc0 + b*8 + 2*(lane%4) + e
-  if (P.metric_out != nullptr) {
-    const int ks = min(P.ksplit, kend_all);
-    run_phase(0, ks);
+  auto metric = [&] {
     double ss = 0.0;
     if (blockIdx.z == 0) {
 #pragma unroll
@@ -235,9 +251,19 @@ __global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid
         *P.metric_ticket = 0;
       }
     }
-    run_phase(ks, kend_all);
+  };
+  if (P.metric_out != nullptr) {
+    const int ks = min(P.ksplit, kend_all);
+    if (ks > 0 && ks % T_BK == 0) {
+      // snapshot at a stage boundary inside one pipelined K loop (same summation order)
+      run_phase(0, kend_all, ks / T_BK - 1, metric);
+    } else {
+      run_phase(0, ks, -1, no_snap);
+      metric();
+      run_phase(ks, kend_all, -1, no_snap);
+    }
   } else {
-    run_phase(0, kend_all);
+    run_phase(0, kend_all, -1, no_snap);
   }
 
   // ---- epilogue (metric-only launches pass Y = null)
@@ -252,12 +278,25 @@ __global__ void __launch_bounds__(T_THREADS, C::MINB) tsgemm_kernel(const __grid
       const int col = wc0 + b * 8 + 2 * (lane & 3);
       double v0 = P.alpha * acc[a][b][0];
       double v1 = P.alpha * acc[a][b][1];
-      if (P.beta != 0.0) {
-        if (col < P.N) v0 = fma(P.beta, pr.Z[row * P.ldz + col], v0);
-        if (col + 1 < P.N) v1 = fma(P.beta, pr.Z[row * P.ldz + col + 1], v1);
+      const int64_t zo = row * P.ldz + col, yo = row * P.ldy + col;
+      // 16-byte accesses when both columns exist and the pair is aligned (the usual case)
+      const bool pair = col + 1 < P.N && ((reinterpret_cast<uintptr_t>(pr.Y + yo) & 15) == 0) &&
+                        (P.beta == 0.0 || (reinterpret_cast<uintptr_t>(pr.Z + zo) & 15) == 0);
+      if (pair) {
+        if (P.beta != 0.0) {
+          const double2 z = *reinterpret_cast<const double2*>(pr.Z + zo);
+          v0 = fma(P.beta, z.x, v0);
+          v1 = fma(P.beta, z.y, v1);
+        }
+        *reinterpret_cast<double2*>(pr.Y + yo) = make_double2(sr * v0, sr * v1);
+        continue;
       }
-      if (col < P.N) pr.Y[row * P.ldy + col] = sr * v0;
-      if (col + 1 < P.N) pr.Y[row * P.ldy + col + 1] = sr * v1;
+      if (P.beta != 0.0) {
+        if (col < P.N) v0 = fma(P.beta, pr.Z[zo], v0);
+        if (col + 1 < P.N) v1 = fma(P.beta, pr.Z[zo + 1], v1);
+      }
+      if (col < P.N) pr.Y[yo] = sr * v0;
+      if (col + 1 < P.N) pr.Y[yo + 1] = sr * v1;
     }
   }
 }
