@@ -190,6 +190,27 @@ int bk_tsgemm_batched_d(int nprob, int64_t n, int K, int N, double alpha, const 
 int bk_cplx_expand_d(int K, int N, const double* G, int64_t ldg, double* Gr, int64_t ldr,
                      void* stream);
 
+/* ---- FP64 products on the int8 tensor cores (tcgen05 kind::i8, Ozaki scheme: 8 signed 8-bit
+ *      digits per element against per-row / per-column power-of-two scales, 36 digit products
+ *      accumulated exactly in int32 TMEM, combined in fp64; error within DGEMM's bound class).
+ *      Same results contract as bk_gram_d / bk_tsgemm_batched_d (the products of block_inner,
+ *      core.py:43-49, and of the tall updates listed above); deterministic; Inf/NaN in a
+ *      row / column make that row / column of the product NaN.  bk_fp64_emu_set(0/1) selects
+ *      the DMMA or the emulated kernels in the host layer (default: PPCG_FP64_EMU, else on). */
+int bk_fp64_emu_set(int mode);
+int bk_fp64_emu_enabled(void);
+/* ws bytes for one call (same: X and Y are one block; symmetric requires same).  A smaller ws
+ * (>= the size for one row chunk) is accepted: rows are then sliced in super-chunks. */
+int64_t bk_ozaki_gram_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric);
+int bk_ozaki_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                    double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream);
+/* K <= 16320; flags bit0: G upper triangular (k stages below a column tile are skipped) */
+int64_t bk_ozaki_tsgemm_ws_bytes(int nprob, int64_t n, int K, int N, int ksplit);
+int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alpha, const double* const* Xs, int64_t ldx,
+                      const double* const* Gs, int64_t ldg, double beta, const double* const* Zs, int64_t ldz,
+                      double* const* Ys, int64_t ldy, const double* rowscale, int flags, int ksplit,
+                      int nsplit, double* metric_out, void* ws, int64_t ws_bytes, void* stream);
+
 /* ---- reductions: norms of ppcg.py:689-691, rayleigh_ritz.py:83-85, ppcg.py:452 */
 int64_t bk_sumsq_ws_bytes(void);
 int bk_sumsq_d(int64_t n, int m, const double* X, int64_t ldx, double* out, void* ws,

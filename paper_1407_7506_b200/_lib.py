@@ -82,6 +82,13 @@ _SIGS = {
     "bk_tsgemm_batched_d": (c_int, [c_int, c_i64, c_int, c_int, c_dbl, PP, c_i64, PP, c_i64, c_dbl,
                                     PP, c_i64, PP, c_i64, vp, c_int, c_int, c_int, vp, vp, c_i64, vp]),
     "bk_cplx_expand_d": (c_int, [c_int, c_int, vp, c_i64, vp, c_i64, vp]),
+    "bk_fp64_emu_set": (c_int, [c_int]),
+    "bk_fp64_emu_enabled": (c_int, []),
+    "bk_ozaki_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int, c_int]),
+    "bk_ozaki_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
+    "bk_ozaki_tsgemm_ws_bytes": (c_i64, [c_int, c_i64, c_int, c_int, c_int]),
+    "bk_ozaki_tsgemm_d": (c_int, [c_int, c_i64, c_int, c_int, c_dbl, PP, c_i64, PP, c_i64, c_dbl, PP, c_i64, PP,
+                                  c_i64, vp, c_int, c_int, c_int, vp, vp, c_i64, vp]),
     "bk_sumsq_ws_bytes": (c_i64, []),
     "bk_sumsq_d": (c_int, [c_i64, c_int, vp, c_i64, vp, vp, c_i64, vp]),
     "bk_small_stats_d": (c_int, [c_int, c_int, vp, c_i64, c_int, vp, vp]),

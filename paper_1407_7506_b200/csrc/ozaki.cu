@@ -1,0 +1,885 @@
+// FP64 products on the int8 tensor cores (tcgen05.mma kind::i8, TMEM accumulators): the Ozaki
+// scheme.  sm_100a has no FP64 tcgen05 kind; its FP64 tensor path (DMMA, mma.sync) peaks at
+// 37 TFLOP/s, while the int8 tensor cores run at ~4.5 POPS.  Every FP64 operand element is
+// split into S = 8 signed 8-bit digits against a per-row / per-column power-of-two scale:
+//
+//     x = 2^(E - 6) * sum_{i<S} d_i 2^(-8 i) + O(2^(E - 8S + 2)),   d_i in [-128, 127],
+//
+// (Z = trunc(x 2^(8S-2-E)), |Z| < 2^(8S-2); the lower digits are the bytes of Z + 0x80..80
+// minus 128, the top digit its arithmetic high byte), so a dot product of two such vectors is
+// sum_{i,j} 2^(EA+EB-12-8(i+j)) <dA_i, dB_j>, each <dA_i, dB_j> an exact int32 sum
+// (|d_i d_j| <= 2^14, at most S pairs per accumulator, chunks of <= 16,320 rows).  The pairs
+// with i + j <= S - 1 are kept (36 products); the digit truncation (2^-62 of max|x|) and the
+// dropped tail (~2^-59 of max|x| max|y| per term) sit far below fp64 rounding, so the result is
+// within DGEMM's error bound class (u |X|^T |Y|) even for rows / columns whose entries span many
+// binades.  (7 digits with i + j <= 6, 28 products, measured 2^-52.5 of max|x| max|y| per term --
+// above DGEMM's bound for short sums -- tools/ozaki_probe.cu.)
+//
+// The pairs of one group t = i + j share a scale, so they accumulate in one TMEM block; B's
+// digit blocks are consecutive 64-row blocks of shared memory and the groups consecutive
+// 64-column blocks of TMEM, so A_i x [B_j0 .. B_j0+3] is ONE tcgen05.mma with N = 256 writing
+// groups i+j0 .. i+j0+3 (12 MMAs per 32-deep k step instead of 36: fewer shared-memory re-reads
+// of A, the limiter of this kernel -- ncu: tensor-core shared-memory path 80% busy).
+//
+// Kernels: digit slicing (column-wise with a transpose for Grams, row-wise for the tall GEMM),
+// the tcgen05 mainloop (TMA producer warp, single-thread MMA issue, 4 epilogue warps reading
+// TMEM), a fixed-order split-K reduction.  Results are deterministic (fixed summation orders).
+// Replaces the FP64 products of block_inner (core.py:43-49) and the tall updates
+// (ppcg.py:443-445, 630, 758; core.py:99; ppcg.py:574-577).
+#include <cuda.h>
+#include "common.cuh"
+
+namespace bk {
+namespace oz {
+
+constexpr int S = 8;            // digits per element (and digit groups t = i + j <= S - 1 kept)
+constexpr int BM = 128;         // output rows per CTA (TMEM lanes)
+constexpr int BN = 64;          // output columns per digit group (TMEM columns per group)
+constexpr int KB = 64;          // k bytes (= k elements) per pipeline stage (64-byte swizzle)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = S * BM * KB, B_BYTES = S * BN * KB;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int THREADS = 192;    // warp 0 TMA, warp 1 MMA (+TMEM alloc), warps 2-5 epilogue
+constexpr int MAX_CHUNK = 16320;  // rows per int32 accumulation: S pairs * 2^14 * 16320 < 2^31
+constexpr int KPAD = 64;
+
+BK_DEV void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 64-byte swizzle, SBO = 8 rows x 64 B, LBO = 1 (unused
+// for swizzled K-major), version 1 (sm_100)
+BK_DEV uint64_t umma_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * KB) >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+// instruction descriptor kind::i8: s32 accumulate, signed A and B, K-major both, N, M = 128
+BK_DEV uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+BK_DEV void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+// 16 accumulator columns [cc, cc+16) of this thread's TMEM lane, digit groups combined in fp64
+// (smallest group first): sum_t 2^(-12-8t) acc_t
+BK_DEV void combine16(uint32_t tmem_lane, int cc, double (&acc)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+#pragma unroll
+  for (int t = S - 1; t >= 0; --t) {
+    uint32_t v[16];
+    tmem_ld16(tmem_lane + t * BN + cc, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const double w = ldexp(1.0, -12 - 8 * t);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = fma((double)(int)v[e], w, acc[e]);
+  }
+}
+
+// signed base-256 digits of x 2^sh, sh = 8S-2-E (|x 2^sh| < 2^(8S-2)): packs digit s of 4 consecutive
+// elements into w[s] (byte e of the word = element e)
+BK_DEV void digits4(const double (&v)[4], int sh, uint32_t (&w)[S]) {
+  unsigned long long B = 0;
+#pragma unroll
+  for (int q = 0; q < S - 1; ++q) B |= 0x80ull << (8 * q);
+#pragma unroll
+  for (int s = 0; s < S; ++s) w[s] = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const long long U = (long long)ldexp(v[e], sh) + (long long)B;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int d = (s == 0) ? (int)(U >> (8 * (S - 1))) : (int)((U >> (8 * (S - 1 - s))) & 255) - 128;
+      w[s] |= ((uint32_t)(d & 255)) << (8 * e);
+    }
+  }
+}
+
+// exponent E with max|x| < 2^E; NON_FINITE marks a column / row holding Inf or NaN: its products
+// come out NaN (the breakdown guards of ppcg.py:698-724 then see them, as with DGEMM)
+constexpr int NON_FINITE = 0x40000000;
+BK_DEV int exp_of(double mx) { return !isfinite(mx) ? NON_FINITE : mx > 0 ? ilogb(mx) + 1 : 0; }
+BK_DEV int shift_of(int E) { return E == NON_FINITE ? -2000 : 8 * S - 2 - E; }
+BK_DEV double scaled(double acc, int e1, int e2) {
+  return (e1 == NON_FINITE || e2 == NON_FINITE) ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(acc, e1 + e2);
+}
+
+// ---------------------------------------------------------------------------------------- slicing
+// column maxima (|x| bit patterns, atomicMax; zeroed by the caller) of an n x m row-major block;
+// CTA = 64 rows x 256 columns
+__global__ void __launch_bounds__(256) k_colmax(int64_t n, int m, const double* __restrict__ X, int64_t ld,
+                                                unsigned long long* colmax) {
+  const int c = blockIdx.y * 256 + threadIdx.x;
+  if (c >= m) return;
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int nr = (int)lmin(64, n - r0);
+  const double* p = X + r0 * ld + c;
+  double mx = 0;
+  bool bad = false;
+  if (nr == 64) {
+#pragma unroll 16
+    for (int r = 0; r < 64; ++r) {
+      const double v = fabs(__ldg(p + r * ld));
+      mx = fmax(mx, v);
+      bad |= !(v <= 1.7976931348623157e308);
+    }
+  } else {
+    for (int r = 0; r < nr; ++r) {
+      const double v = fabs(__ldg(p + r * ld));
+      mx = fmax(mx, v);
+      bad |= !(v <= 1.7976931348623157e308);
+    }
+  }
+  // NaN bits order above every finite / infinite magnitude
+  atomicMax(colmax + c, bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mx));
+}
+
+__global__ void k_exponents(int m, const unsigned long long* colmax, int* E) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < m) E[c] = exp_of(__longlong_as_double((long long)colmax[c]));
+}
+
+// column digits, transposed: out[s][c][k - r_base] for rows k in [r0, r0 + 128) of the n x m block
+// (rows >= n -> 0; k offsets >= klim not written).  CTA = 128 rows x 32 columns, 256 threads: thread (column, 16 rows).
+__global__ void __launch_bounds__(256) k_slice_cols(int64_t n, int m, const double* __restrict__ X, int64_t ld,
+                                                    const int* E, int64_t r_base, int8_t* out, int64_t kld,
+                                                    int64_t slice_stride, int64_t klim) {
+  __shared__ __align__(16) int8_t t[S][32][128 + 16];
+  const int64_t r0 = r_base + (int64_t)blockIdx.x * 128;
+  const int c0 = blockIdx.y * 32;
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = c0 + cl;
+  const int sh = c < m ? shift_of(E[c]) : 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    double v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t r = r0 + g * 16 + h * 4 + e;
+      v[e] = (c < m && r < n) ? __ldg(X + r * ld + c) : 0.0;
+    }
+    uint32_t w[S];
+    digits4(v, sh, w);
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(&t[s][cl][g * 16 + h * 4]) = w[s];
+  }
+  __syncthreads();
+  const int64_t kofs = r0 - r_base;
+  for (int i = threadIdx.x; i < S * 32 * 8; i += blockDim.x) {
+    const int p = i & 7, cc = (i >> 3) & 31, s = i >> 8;
+    if (c0 + cc < m && kofs + p * 16 < klim)
+      *reinterpret_cast<int4*>(out + s * slice_stride + (int64_t)(c0 + cc) * kld + kofs + p * 16) =
+          *reinterpret_cast<const int4*>(&t[s][cc][p * 16]);
+  }
+}
+
+// row digits (no transpose): out[s][r - r_base][kk] for row r of the n x K block, exponent over
+// the row; k layout split at ksplit: columns [0, ksplit) -> [0, ksplit), columns [ksplit, K) ->
+// [kp1, kp1 + K - ksplit), zeros elsewhere up to kp.  One warp per row; lane = 4 columns.
+__global__ void __launch_bounds__(256) k_slice_rows(int64_t r_base, int64_t nrows, int K, const double* __restrict__ X,
+                                                    int64_t ld, int ksplit, int kp1, int kp, int8_t* out,
+                                                    int64_t slice_stride, int* E) {
+  const int64_t rl = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (rl >= nrows) return;
+  const double* x = X + (r_base + rl) * ld;
+  double mx = 0;
+  bool bad = false;
+  for (int c = lane; c < K; c += 32) {
+    const double v = fabs(__ldg(x + c));
+    mx = fmax(mx, v);
+    bad |= !(v <= 1.7976931348623157e308);
+  }
+  mx = warp_max(mx);
+  bad = __any_sync(0xffffffffu, bad);
+  const int e = bad ? NON_FINITE : exp_of(mx);
+  if (lane == 0) E[r_base + rl] = e;
+  const int sh = shift_of(e);
+  int8_t* o = out + rl * kp;
+  for (int p0 = lane * 4; p0 < kp; p0 += 128) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = p0 + q;
+      const int c = p < kp1 ? (p < ksplit ? p : -1) : (p - kp1 + ksplit < K ? p - kp1 + ksplit : -1);
+      v[q] = c >= 0 ? __ldg(x + c) : 0.0;
+    }
+    uint32_t w[S];
+    digits4(v, sh, w);
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + s * slice_stride + p0) = w[s];
+  }
+}
+
+// ---------------------------------------------------------------------------------------- mainloop
+struct GramEpi {
+  int m1, m2;
+  int ta, tb;         // tile grid (rows of 128, columns of 64)
+  int sym;            // upper tiles only
+  int64_t chunk_rows;  // rows per CTA (multiple of KB)
+  int64_t nrows;      // rows in this launch
+  const int* EA;
+  const int* EB;
+  double* part;       // [chunk][tile][128][64]
+};
+
+struct TsEpi {
+  int64_t nrows;      // rows in this launch (from row r_base)
+  int64_t r_base;
+  int N;
+  int nk;             // k stages (kp / KB)
+  int snap_stage;     // metric snapshot after this stage (-1: none)
+  int upper;          // G upper triangular (no metric): skip k stages below the tile
+  int nsplit;
+  double alpha, beta;
+  const int* ER[4];   // row exponents (indexed by global row)
+  const int* EG[4];   // G column exponents
+  const double* Z[4];
+  double* Y[4];
+  int64_t ldz, ldy;
+  const double* rowscale;  // indexed by global row
+  double* metric_ws;  // per-CTA partial sums of squares (problem 0)
+};
+
+template <int MODE>
+struct OzArgs;
+template <>
+struct OzArgs<0> {
+  using Epi = GramEpi;
+};
+template <>
+struct OzArgs<1> {
+  using Epi = TsEpi;
+};
+
+BK_DEV void sym_tile(int idx, int ta, int tb, int& a, int& b) {
+  // upper tiles (b*BN + BN - 1 >= a*BM), enumerated row by row
+  for (a = 0; a < ta; ++a) {
+    int bmin = (a * BM - (BN - 1) + BN - 1) / BN;
+    if (bmin < 0) bmin = 0;
+    const int cnt = tb - bmin;
+    if (idx < cnt) {
+      b = bmin + idx;
+      return;
+    }
+    idx -= cnt;
+  }
+  a = ta - 1;
+  b = tb - 1;
+}
+
+// MODE 0: Gram partial of one (tile, row chunk); grid (tiles, chunks).
+// MODE 1: tall GEMM tile; grid (row tiles, column tiles, problems); maps A[b], B[b] per problem.
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_oz_mma(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+             const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
+             const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
+             const __grid_constant__ CUtensorMap mapB2, const __grid_constant__ CUtensorMap mapB3,
+             const typename OzArgs<MODE>::Epi P) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint64_t* snap_full = done + 1;
+  uint64_t* snap_free = done + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 3);
+  __shared__ double s_red[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work item
+  int rowA = 0, rowB = 0, kc0 = 0, nk = 0, snap = -1, prob = 0;
+  const CUtensorMap* mA = &mapA0;
+  const CUtensorMap* mB = &mapB0;
+  if constexpr (MODE == 0) {
+    int a, b;
+    if (P.sym) {
+      sym_tile(blockIdx.x, P.ta, P.tb, a, b);
+    } else {
+      a = blockIdx.x / P.tb;
+      b = blockIdx.x % P.tb;
+    }
+    rowA = a * BM;
+    rowB = b * BN;
+    kc0 = (int)(blockIdx.y * P.chunk_rows);
+    const int64_t k1 = lmin(P.nrows, (int64_t)kc0 + P.chunk_rows);
+    nk = (int)((k1 - kc0 + KB - 1) / KB);
+  } else {
+    prob = blockIdx.z;
+    mA = prob == 0 ? &mapA0 : prob == 1 ? &mapA1 : prob == 2 ? &mapA2 : &mapA3;
+    mB = prob == 0 ? &mapB0 : prob == 1 ? &mapB1 : prob == 2 ? &mapB2 : &mapB3;
+    // column tiles fastest: the tiles of one row block run together and share its X digits in L2
+    rowA = blockIdx.y * BM;
+    rowB = blockIdx.x * BN;
+    nk = P.nk;
+    // G upper triangular: rows k >= the tile's last column are zero
+    if (P.upper) nk = min(nk, (rowB + BN + KB - 1) / KB);
+    if (prob == 0 && P.snap_stage >= 0 && rowB < P.nsplit) snap = P.snap_stage;
+  }
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(snap_full, 1);
+    mbar_init(snap_free, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(mA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(mB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % STAGES;
+        mbar_wait(empty + st, ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa = sm + st * STAGE_BYTES;
+        mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+        const int kc = kc0 + kb * KB;
+        tma3d(sa, mA, kc, rowA, 0, full + st);
+        tma3d(sa + A_BYTES, mB, kc, rowB, 0, full + st);
+      }
+    }
+  } else if (warp == 1) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % STAGES;
+      mbar_wait(full + st, (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t sa = smem_u32(sm + st * STAGE_BYTES);
+        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < KB / 32; ++ks) {
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+#pragma unroll
+            for (int j0 = 0; j0 < S - i; j0 += 4) {
+              const int nj = (S - i - j0) < 4 ? (S - i - j0) : 4;
+              const uint64_t da = umma_desc(sa + i * BM * KB + ks * 32);
+              const uint64_t db = umma_desc(sb + j0 * BN * KB + ks * 32);
+              const uint32_t accf = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (i + j0) * BN),
+                  "l"(da), "l"(db), "r"(idesc_i8(nj * BN)), "r"(accf));
+            }
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(empty + st))
+                     : "memory");
+        if (kb == snap)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(snap_full))
+                       : "memory");
+        if (kb == nk - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(done))
+                       : "memory");
+      }
+      __syncwarp();
+      if (kb == snap && kb != nk - 1) mbar_wait(snap_free, 0);  // epilogue has read the snapshot
+    }
+  } else {
+    // ---- epilogue warps: TMEM lane quadrant = warp % 4 (hardware rule), lane = row of the tile
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    if constexpr (MODE == 0) {
+      mbar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int gr = rowA + r;
+      const int ea = gr < P.m1 ? P.EA[gr] : 0;
+      double* out = P.part + (((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BM + r) * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 16) {
+        double acc[16];
+        combine16(tl, cc, acc);
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const int gc = rowB + cc + e;
+          const int e0 = gc < P.m2 ? P.EB[gc] : 0;
+          const int e1 = gc + 1 < P.m2 ? P.EB[gc + 1] : 0;
+          *reinterpret_cast<double2*>(out + cc + e) = make_double2(scaled(acc[e], ea, e0), scaled(acc[e + 1], ea, e1));
+        }
+      }
+    } else {
+      const int64_t lrow = rowA + r;  // row within this launch
+      const bool live = lrow < P.nrows;
+      const int64_t grow = P.r_base + lrow;
+      const int er = live ? P.ER[prob][grow] : 0;
+      const int* EG = P.EG[prob];
+      const double* Z = P.Z[prob];
+      double* Y = P.Y[prob];
+      if (snap >= 0) {
+        // metric: sum over cols < nsplit of (alpha X[:, :ksplit] G[:ksplit] + beta Z)^2
+        mbar_wait(snap_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        double ss = 0;
+        for (int cc = 0; cc < BN && rowB + cc < P.nsplit; cc += 16) {
+          double acc[16];
+          combine16(tl, cc, acc);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int gc = rowB + cc + e;
+            if (live && gc < P.nsplit && gc < P.N) {
+              double v = P.alpha * scaled(acc[e], er, EG[gc]);
+              if (P.beta != 0.0) v = fma(P.beta, Z[grow * P.ldz + gc], v);
+              ss = fma(v, v, ss);
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(snap_free);
+        ss = warp_sum(ss);
+        if (lane == 0) s_red[q] = ss;
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) {
+          const double t = s_red[0] + s_red[1] + s_red[2] + s_red[3];
+          P.metric_ws[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+        }
+      }
+      if (snap < 0 && prob == 0 && P.snap_stage >= 0 && threadIdx.x == 64)
+        P.metric_ws[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = 0.0;  // tile right of nsplit
+      mbar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (Y != nullptr) {
+        const double sr = (live && P.rowscale) ? P.rowscale[grow] : 1.0;
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 16) {
+          if (rowB + cc >= P.N) break;
+          double acc[16];
+          combine16(tl, cc, acc);
+          if (!live) continue;
+          const int64_t zo = grow * P.ldz + rowB + cc, yo = grow * P.ldy + rowB + cc;
+          const bool vec = ((reinterpret_cast<uintptr_t>(Y + yo) & 15) == 0) &&
+                           (P.beta == 0.0 || (reinterpret_cast<uintptr_t>(Z + zo) & 15) == 0);
+          if (vec && rowB + cc + 16 <= P.N) {
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const int gc = rowB + cc + e;
+              double v0 = P.alpha * scaled(acc[e], er, EG[gc]);
+              double v1 = P.alpha * scaled(acc[e + 1], er, EG[gc + 1]);
+              if (P.beta != 0.0) {
+                const double2 z = *reinterpret_cast<const double2*>(Z + zo + e);
+                v0 = fma(P.beta, z.x, v0);
+                v1 = fma(P.beta, z.y, v1);
+              }
+              *reinterpret_cast<double2*>(Y + yo + e) = make_double2(sr * v0, sr * v1);
+            }
+          } else {
+            for (int e = 0; e < 16; ++e) {
+              const int gc = rowB + cc + e;
+              if (gc >= P.N) break;
+              double v = P.alpha * scaled(acc[e], er, EG[gc]);
+              if (P.beta != 0.0) v = fma(P.beta, Z[zo + e], v);
+              Y[yo + e] = sr * v;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+// C (+)= sum over chunks of the partials, fixed chunk order, compensated; symmetric: upper tiles
+// mirrored.
+// grid (tiles, 16): 8 rows x 64 columns per CTA
+__global__ void k_gram_reduce(GramEpi P, int nch, double* C, int64_t ldc, int accumulate) {
+  int a, b;
+  if (P.sym) {
+    sym_tile(blockIdx.x, P.ta, P.tb, a, b);
+  } else {
+    a = blockIdx.x / P.tb;
+    b = blockIdx.x % P.tb;
+  }
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 6), c = threadIdx.x & 63;
+  const int gr = a * BM + r, gc = b * BN + c;
+  if (gr >= P.m1 || gc >= P.m2) return;
+  if (P.sym && gc < gr) return;
+  // compensated (Neumaier) sum: the chunk partials are each rounded once, so the total error stays
+  // ~u sum_chunks |partial| <= u |X|^T |Y| whatever the chunk count
+  double s = accumulate ? C[(int64_t)gr * ldc + gc] : 0.0, comp = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const double v = __ldcg(P.part + (((int64_t)ch * gridDim.x + blockIdx.x) * BM + r) * BN + c);
+    const double t = s + v;
+    comp += fabs(s) >= fabs(v) ? (s - t) + v : (v - t) + s;
+    s = t;
+  }
+  s += comp;
+  C[(int64_t)gr * ldc + gc] = s;
+  if (P.sym && gc > gr) C[(int64_t)gc * ldc + gr] = s;
+}
+
+// metric: fixed-order sum of the per-CTA partials (one thread block)
+__global__ void k_metric_sum(const double* ws, int64_t cnt, double* out, int accumulate) {
+  __shared__ double red[32];
+  double s = 0;
+  for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) s += ws[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = accumulate ? *out + t : t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------- host
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// digit array [S][rows][kld] (int8, K contiguous): box 64 k x box_rows rows x S digits, 64-byte
+// swizzle; rows >= `rows` and k >= kdim arrive zero-filled
+static bool encode_digits(CUtensorMap* map, const int8_t* base, int64_t kld, int64_t kdim, int64_t rows,
+                          int box_rows, int64_t slice_stride) {
+  static EncodeFn enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeFn) nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)kdim, (cuuint64_t)rows, (cuuint64_t)S};
+  const cuuint64_t strides[2] = {(cuuint64_t)kld, (cuuint64_t)slice_stride};
+  const cuuint32_t box[3] = {(cuuint32_t)KB, (cuuint32_t)box_rows, (cuuint32_t)S};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_emu_mode = -1;  // -1: from PPCG_FP64_EMU (default on), 0 off, 1 on
+
+static int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+static int n_tiles(int m1, int m2, int sym) {
+  const int ta = (m1 + BM - 1) / BM, tb = (m2 + BN - 1) / BN;
+  if (!sym) return ta * tb;
+  int cnt = 0;
+  for (int a = 0; a < ta; ++a) {
+    int bmin = (a * BM) / BN;
+    if (a * BM - (bmin * BN + BN - 1) > 0) ++bmin;
+    cnt += tb - (bmin < 0 ? 0 : bmin);
+  }
+  return cnt;
+}
+
+// rows per chunk: <= MAX_CHUNK, a multiple of KB, chosen for whole waves of 148 CTAs
+static int64_t gram_chunk_rows(int64_t n, int ntiles) {
+  const int64_t cmin = (n + MAX_CHUNK - 1) / MAX_CHUNK;
+  int64_t best = cmin;
+  double best_eff = -1;
+  for (int64_t c = cmin; c <= cmin * 8 + 8; ++c) {
+    const int64_t rows = align_up((n + c - 1) / c, KB);
+    const int64_t nch = (n + rows - 1) / rows;
+    const int64_t ctas = nch * ntiles;
+    const int64_t waves = (ctas + kSMs - 1) / kSMs;
+    const double eff = (double)ctas / (double)(waves * kSMs) - 0.004 * (double)nch / (double)cmin;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = c;
+    }
+  }
+  return align_up((n + best - 1) / best, KB);
+}
+
+struct GramLayout {
+  int ntiles;
+  int64_t chunk_rows, sc_rows;  // rows per chunk, rows per super-chunk (slices held at once)
+  int64_t off_cmA, off_cmB, off_EA, off_EB, off_part, off_sA, off_sB, total;
+};
+
+static GramLayout gram_layout(int64_t n, int m1, int m2, int same, int sym, int64_t ws_cap) {
+  GramLayout L{};
+  L.ntiles = n_tiles(m1, m2, sym);
+  L.chunk_rows = gram_chunk_rows(n, L.ntiles);
+  const int64_t per_row = (int64_t)S * (m1 + (same ? 0 : m2));
+  // slices of at most ~1.5 GB at once (or what the caller's workspace holds)
+  int64_t sc_chunks = (n + L.chunk_rows - 1) / L.chunk_rows;
+  const int64_t cap = ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
+  auto size_for = [&](int64_t chunks) {
+    const int64_t rows = chunks * L.chunk_rows;
+    int64_t o = 0;
+    o += align_up(8 * (int64_t)m1, 256);
+    o += align_up(8 * (int64_t)m2, 256);
+    o += align_up(4 * (int64_t)m1, 256);
+    o += align_up(4 * (int64_t)m2, 256);
+    o += align_up(chunks * L.ntiles * (int64_t)BM * BN * 8, 1024);
+    o += align_up(per_row * rows, 1024) + 1024;
+    return o;
+  };
+  while (sc_chunks > 1 && size_for(sc_chunks) > cap) sc_chunks = (sc_chunks + 1) / 2;
+  L.sc_rows = sc_chunks * L.chunk_rows;
+  int64_t o = 0;
+  L.off_cmA = o; o += align_up(8 * (int64_t)m1, 256);
+  L.off_cmB = o; o += align_up(8 * (int64_t)m2, 256);
+  L.off_EA = o;  o += align_up(4 * (int64_t)m1, 256);
+  L.off_EB = o;  o += align_up(4 * (int64_t)m2, 256);
+  L.off_part = o; o += align_up(sc_chunks * L.ntiles * (int64_t)BM * BN * 8, 1024);
+  L.off_sA = o;  o += align_up((int64_t)S * m1 * L.sc_rows, 1024);
+  L.off_sB = o;  o += same ? 0 : align_up((int64_t)S * m2 * L.sc_rows, 1024);
+  L.total = o;
+  return L;
+}
+
+}  // namespace oz
+}  // namespace bk
+
+using namespace bk;
+using namespace bk::oz;
+
+extern "C" int bk_fp64_emu_set(int mode) {
+  g_emu_mode = mode;
+  return BK_OK;
+}
+
+extern "C" int bk_fp64_emu_enabled(void) {
+  if (g_emu_mode < 0) {
+    const char* e = getenv("PPCG_FP64_EMU");
+    g_emu_mode = e ? atoi(e) : 1;
+  }
+  return g_emu_mode;
+}
+
+extern "C" int64_t bk_ozaki_gram_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric) {
+  if (n <= 0 || m1 <= 0 || m2 <= 0) return 0;
+  return gram_layout(n, m1, m2, same, symmetric, 0).total;
+}
+
+// C = X^T Y (m1 x m2) with the Ozaki scheme; same = X and Y are the same block (one slicing);
+// symmetric (requires same): upper tiles computed, mirrored.
+extern "C" int bk_ozaki_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                               double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream) {
+  if (n <= 0 || m1 <= 0 || m2 <= 0 || !X || !Y || !C) return BK_ERR_ARG;
+  const int same = (X == Y && ldx == ldy && m1 == m2) ? 1 : 0;
+  if (symmetric && !same) return BK_ERR_ARG;
+  const GramLayout L = gram_layout(n, m1, m2, same, symmetric, ws_bytes);
+  if (!ws || ws_bytes < L.total) return BK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  auto* cmA = reinterpret_cast<unsigned long long*>(w + L.off_cmA);
+  auto* cmB = reinterpret_cast<unsigned long long*>(w + L.off_cmB);
+  int* EA = reinterpret_cast<int*>(w + L.off_EA);
+  int* EB = same ? EA : reinterpret_cast<int*>(w + L.off_EB);
+  double* part = reinterpret_cast<double*>(w + L.off_part);
+  int8_t* sA = reinterpret_cast<int8_t*>(w + L.off_sA);
+  int8_t* sB = same ? sA : reinterpret_cast<int8_t*>(w + L.off_sB);
+  // exponents over all rows
+  cudaMemsetAsync(cmA, 0, 8 * (size_t)m1, st);
+  BK_COUNT();
+  k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
+  BK_COUNT();
+  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA);
+  if (!same) {
+    cudaMemsetAsync(cmB, 0, 8 * (size_t)m2, st);
+    BK_COUNT();
+    k_colmax<<<dim3((unsigned)((n + 63) / 64), (m2 + 255) / 256), 256, 0, st>>>(n, m2, Y, ldy, cmB);
+    BK_COUNT();
+    k_exponents<<<(m2 + 255) / 256, 256, 0, st>>>(m2, cmB, EB);
+  }
+  cudaFuncSetAttribute(k_oz_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  GramEpi P{};
+  P.m1 = m1;
+  P.m2 = m2;
+  P.ta = (m1 + BM - 1) / BM;
+  P.tb = (m2 + BN - 1) / BN;
+  P.sym = symmetric ? 1 : 0;
+  P.chunk_rows = L.chunk_rows;
+  P.EA = EA;
+  P.EB = EB;
+  P.part = part;
+  for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
+    const int64_t rows = lmin(L.sc_rows, n - r0);
+    const int64_t kld = align_up(rows, KPAD);
+    const dim3 gs((unsigned)((rows + 127) / 128), 1);
+    BK_COUNT();
+    k_slice_cols<<<dim3(gs.x, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
+                                                             kld * (int64_t)m1, kld);
+    if (!same) {
+      BK_COUNT();
+      k_slice_cols<<<dim3(gs.x, (m2 + 31) / 32), 256, 0, st>>>(r0 + rows, m2, Y, ldy, EB, r0, sB, kld,
+                                                               kld * (int64_t)m2, kld);
+    }
+    CUtensorMap mA, mB;
+    if (!encode_digits(&mA, sA, kld, rows, m1, BM, kld * (int64_t)m1) ||
+        !encode_digits(&mB, sB, kld, rows, m2, BN, kld * (int64_t)m2))
+      return BK_ERR_UNSUPPORTED;
+    P.nrows = rows;
+    const int nch = (int)((rows + L.chunk_rows - 1) / L.chunk_rows);
+    BK_COUNT();
+    k_oz_mma<0><<<dim3(L.ntiles, nch), THREADS, SMEM, st>>>(mA, mA, mA, mA, mB, mB, mB, mB, P);
+    BK_CHECK_LAUNCH();
+    BK_COUNT();
+    k_gram_reduce<<<dim3(L.ntiles, 16), 512, 0, st>>>(P, nch, C, ldc, r0 > 0 ? 1 : 0);
+  }
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+// ---- tall GEMM: Y_b = s (.) (alpha X_b G_b + beta Z_b), b < nprob <= 4 (semantics of
+// bk_tsgemm_batched_d; flags bit0 = G upper triangular: k stages below a tile are skipped)
+namespace bk {
+namespace oz {
+struct TsLayout {
+  int kp1, kp;
+  int64_t sc_rows;
+  int64_t off_ER, off_EG, off_cmG, off_sG, off_mws, off_sX, total;
+};
+static TsLayout ts_layout(int nprob, int64_t n, int K, int N, int ksplit, int64_t ws_cap) {
+  TsLayout L{};
+  const bool split = ksplit > 0 && ksplit < K;
+  L.kp1 = split ? (int)align_up(ksplit, KB) : (int)align_up(K, KB);
+  L.kp = split ? L.kp1 + (int)align_up(K - ksplit, KB) : L.kp1;
+  const int64_t cap = ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
+  int64_t o = 0;
+  L.off_ER = o;  o += align_up(4 * (int64_t)nprob * n, 256);
+  L.off_EG = o;  o += align_up(4 * (int64_t)nprob * N, 256);
+  L.off_cmG = o; o += align_up(8 * (int64_t)nprob * N, 256);
+  L.off_sG = o;  o += align_up((int64_t)nprob * S * N * L.kp, 1024);
+  const int64_t ctas_max = ((n + BM - 1) / BM) * ((N + BN - 1) / BN);
+  L.off_mws = o; o += align_up(8 * ctas_max, 256);
+  L.off_sX = o;
+  const int64_t per_row = (int64_t)nprob * S * L.kp;
+  int64_t rows = align_up(n, BM);
+  while (rows > BM && o + per_row * rows > cap) rows = align_up(rows / 2, BM);
+  L.sc_rows = rows;
+  L.total = o + align_up(per_row * rows, 1024);
+  return L;
+}
+}  // namespace oz
+}  // namespace bk
+
+extern "C" int64_t bk_ozaki_tsgemm_ws_bytes(int nprob, int64_t n, int K, int N, int ksplit) {
+  if (nprob < 1 || nprob > 4 || n <= 0 || K <= 0 || N <= 0) return 0;
+  return ts_layout(nprob, n, K, N, ksplit, 0).total;
+}
+
+extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alpha, const double* const* Xs,
+                                 int64_t ldx, const double* const* Gs, int64_t ldg, double beta,
+                                 const double* const* Zs, int64_t ldz, double* const* Ys, int64_t ldy,
+                                 const double* rowscale, int flags, int ksplit, int nsplit, double* metric_out,
+                                 void* ws, int64_t ws_bytes, void* stream) {
+  if (nprob < 1 || nprob > 4 || n < 0 || K <= 0 || N < 0) return BK_ERR_ARG;
+  if (n == 0 || N == 0) return BK_OK;
+  if (K > MAX_CHUNK) return BK_ERR_UNSUPPORTED;  // int32 accumulation bound
+  const int ks = metric_out ? ksplit : 0;
+  const TsLayout L = ts_layout(nprob, n, K, N, ks, ws_bytes);
+  if (!ws || ws_bytes < L.total) return BK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  int* ER = reinterpret_cast<int*>(w + L.off_ER);
+  int* EG = reinterpret_cast<int*>(w + L.off_EG);
+  auto* cmG = reinterpret_cast<unsigned long long*>(w + L.off_cmG);
+  int8_t* sG = reinterpret_cast<int8_t*>(w + L.off_sG);
+  double* mws = reinterpret_cast<double*>(w + L.off_mws);
+  int8_t* sX = reinterpret_cast<int8_t*>(w + L.off_sX);
+  const bool split = metric_out && ksplit > 0 && ksplit < K;
+  TsEpi P{};
+  P.N = N;
+  P.nk = L.kp / KB;
+  P.snap_stage = -1;
+  P.nsplit = nsplit;
+  P.alpha = alpha;
+  P.beta = beta;
+  P.ldz = ldz;
+  P.ldy = ldy;
+  P.rowscale = rowscale;
+  P.upper = (flags & 1) && !metric_out;
+  P.metric_ws = mws;
+  if (metric_out) P.snap_stage = split ? L.kp1 / KB - 1 : P.nk - 1;
+  bool any = metric_out != nullptr;
+  // G^T digits per problem: column exponents over the K rows of G; k layout split like X's
+  CUtensorMap mA[4], mB[4];
+  cudaMemsetAsync(cmG, 0, 8 * (size_t)nprob * N, st);
+  for (int b = 0; b < nprob; ++b) {
+    if (beta != 0.0 && (!Zs || !Zs[b])) return BK_ERR_ARG;
+    P.Z[b] = Zs ? Zs[b] : nullptr;
+    P.Y[b] = Ys[b];
+    any = any || Ys[b] != nullptr;
+    P.ER[b] = ER + (int64_t)b * n;
+    P.EG[b] = EG + (int64_t)b * N;
+    BK_COUNT();
+    k_colmax<<<dim3((unsigned)((K + 63) / 64), (N + 255) / 256), 256, 0, st>>>(K, N, Gs[b], ldg, cmG + (int64_t)b * N);
+    BK_COUNT();
+    k_exponents<<<(N + 255) / 256, 256, 0, st>>>(N, cmG + (int64_t)b * N, EG + (int64_t)b * N);
+    int8_t* g = sG + (int64_t)b * S * N * L.kp;
+    const int64_t sstr = (int64_t)N * L.kp;
+    cudaMemsetAsync(g, 0, (size_t)S * N * L.kp, st);
+    // rows [0, ksplit) of G -> k [0, ksplit); rows [ksplit, K) -> k [kp1, ...)
+    const int k1 = split ? ksplit : K;
+    BK_COUNT();
+    k_slice_cols<<<dim3((unsigned)((k1 + 127) / 128), (N + 31) / 32), 256, 0, st>>>(k1, N, Gs[b], ldg,
+                                                                                   EG + (int64_t)b * N, 0, g,
+                                                                                   L.kp, sstr, L.kp1);
+    if (split) {
+      // second k range: rows [ksplit, K) of G written at k offset kp1 (k_slice_cols writes
+      // out[(c * kld) + (r - r_base)], so shift the output base by kp1 - ksplit)
+      BK_COUNT();
+      k_slice_cols<<<dim3((unsigned)((K - ksplit + 127) / 128), (N + 31) / 32), 256, 0, st>>>(
+          K, N, Gs[b], ldg, EG + (int64_t)b * N, ksplit, g + L.kp1, L.kp, sstr, L.kp - L.kp1);
+    }
+    if (!encode_digits(&mB[b], g, L.kp, L.kp, N, BN, sstr)) return BK_ERR_UNSUPPORTED;
+  }
+  if (!any) return BK_OK;
+  for (int b = nprob; b < 4; ++b) mB[b] = mB[0];
+  cudaFuncSetAttribute(k_oz_mma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  const int ctn = (N + BN - 1) / BN;
+  int64_t metric_ctas = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
+    const int64_t rows = lmin(L.sc_rows, n - r0);
+    for (int b = 0; b < nprob; ++b) {
+      int8_t* x = sX + (int64_t)b * S * L.sc_rows * L.kp;
+      BK_COUNT();
+      k_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(r0, rows, K, Xs[b], ldx, split ? ksplit : K, L.kp1,
+                                                              L.kp, x, L.sc_rows * L.kp, ER + (int64_t)b * n);
+      if (!encode_digits(&mA[b], x, L.kp, L.kp, rows, BM, L.sc_rows * L.kp)) return BK_ERR_UNSUPPORTED;
+    }
+    for (int b = nprob; b < 4; ++b) mA[b] = mA[0];
+    P.nrows = rows;
+    P.r_base = r0;
+    P.metric_ws = mws + metric_ctas;
+    const dim3 grid(ctn, (unsigned)((rows + BM - 1) / BM), nprob);
+    BK_COUNT();
+    k_oz_mma<1><<<grid, THREADS, SMEM, st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P);
+    BK_CHECK_LAUNCH();
+    metric_ctas += (int64_t)grid.x * grid.y;
+  }
+  if (metric_out) {
+    BK_COUNT();
+    k_metric_sum<<<1, 512, 0, st>>>(mws, metric_ctas, metric_out, 0);
+  }
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}

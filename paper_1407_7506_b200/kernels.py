@@ -79,6 +79,45 @@ def workspace(kind="gram"):
     return ws
 
 
+# ----------------------------------------------------------------------------- FP64 emulation
+# FP64 products of at least EMU_MIN_ROWS rows and EMU_MIN_COLS columns on each side run on the
+# int8 tensor cores (Ozaki scheme, csrc/ozaki.cu); smaller ones on the FP64 DMMA kernels.
+EMU_MIN_ROWS = 16384
+EMU_MIN_COLS = 64
+
+
+def fp64_emulation_enabled():
+    return bool(_lib.load().bk_fp64_emu_enabled())
+
+
+class fp64_emulation:
+    """Context manager (and setter): ``with fp64_emulation(False): ...`` pins the DMMA kernels."""
+
+    def __init__(self, on):
+        lib = _lib.load()
+        self.prev = lib.bk_fp64_emu_enabled()
+        lib.bk_fp64_emu_set(1 if on else 0)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        _lib.load().bk_fp64_emu_set(self.prev)
+        return False
+
+
+def _emu(n, m1, m2):
+    return n >= EMU_MIN_ROWS and min(m1, m2) >= EMU_MIN_COLS and _lib.load().bk_fp64_emu_enabled()
+
+
+def _ozaki_gram(n, m1, m2, px, lx, py, ly, out_ptr, ldo, symmetric, ws_kind):
+    lib = _lib.load()
+    same = 1 if (px == py and lx == ly and m1 == m2) else 0
+    sym = 1 if (symmetric and same) else 0
+    wp, wb = workspace(ws_kind + "/oz").get(lib.bk_ozaki_gram_ws_bytes(n, m1, m2, same, sym))
+    _lib.call("bk_ozaki_gram_d", n, m1, m2, px, lx, py, ly, out_ptr, ldo, sym, wp, wb, stream_ptr())
+
+
 # ----------------------------------------------------------------------------- Grams
 _STRIP = threading.local()
 
@@ -124,6 +163,9 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
     if x.dtype == F64:
         px, _, _, lx = real_view(x)
         py, _, _, ly = real_view(y)
+        if _emu(n, m1, m2):
+            _ozaki_gram(n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), symmetric, ws_kind)
+            return out
         _split_launch(lib.bk_gram_splits(m1, m2), lambda part, wp, wb, st: _lib.call(
             "bk_gram_part_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), 1 if symmetric else 0, part,
             wp, wb, st), ws_kind, lib.bk_gram_ws_bytes(n, m1, m2))
@@ -132,6 +174,11 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
     px, _, r1, lx = real_view(x)
     py, _, r2, ly = real_view(y)
     tmp = torch.empty((r1, r2), dtype=F64, device=x.device)
+    if _emu(n, r1, r2):
+        _ozaki_gram(n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2, symmetric, ws_kind)
+        _lib.call("bk_cplx_gram_combine_d", m1, m2, tmp.data_ptr(), r2, out.data_ptr(), ld_of(out),
+                  stream_ptr())
+        return out
     _split_launch(lib.bk_gram_splits(r1, r2), lambda part, wp, wb, st: _lib.call(
         "bk_gram_part_d", n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2, 1 if symmetric else 0, part, wp, wb, st),
         ws_kind, lib.bk_gram_ws_bytes(n, r1, r2))
@@ -142,7 +189,7 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
 
 def gram2(x1, y1, out1, x2, y2, out2):
     """Two independent Grams in one launch (real only; complex falls back to two launches)."""
-    if x1.dtype != F64:
+    if x1.dtype != F64 or _emu(x1.shape[0], min(x1.shape[1], x2.shape[1]), min(y1.shape[1], y2.shape[1])):
         gram(x1, y1, out1)
         gram(x2, y2, out2)
         return
@@ -206,6 +253,15 @@ def tsgemm(xs, gs, ys, alpha=1.0, beta=0.0, zs=None, rowscale=None, upper=False,
         wp, wb, mp = None, 0, None
     if rowscale is not None and cplx:
         pass  # rowscale is per row: identical on the real view
+    if _emu(n, K, N) and K <= 16320:
+        lib = _lib.load()
+        nbytes = lib.bk_ozaki_tsgemm_ws_bytes(nprob, n, K, N, int(ksplit) if metric is not None else 0)
+        wp, wb = workspace("tsgemm/oz").get(nbytes)
+        _lib.call("bk_ozaki_tsgemm_d", nprob, n, K, N, float(alpha), XP, ldx, GP, ldg, float(beta), ZP, ldz, YP,
+                  ldy, rowscale.data_ptr() if rowscale is not None else None, 1 if upper else 0, int(ksplit),
+                  int(nsplit),
+                  metric.data_ptr() if metric is not None else None, wp, wb, stream_ptr())
+        return
     _lib.call("bk_tsgemm_batched_d", nprob, n, K, N, float(alpha), XP, ldx, GP, ldg, float(beta), ZP,
               ldz, YP, ldy, rowscale.data_ptr() if rowscale is not None else None,
               1 if upper else 0, int(ksplit), int(nsplit), mp, wp, wb, stream_ptr())

@@ -1,0 +1,211 @@
+"""FP64 products emulated on the int8 tensor cores (csrc/ozaki.cu, Ozaki scheme with 8 signed
+8-bit digits) against exact references.
+
+The bar is DGEMM's error bound class: every sampled entry within 4 * 2^-53 * (|X|^T |Y|) of the
+product computed in extended precision (np.longdouble).  Also: non-finite inputs propagate as NaN (the solver's
+breakdown guards rely on it, ppcg.py:698-724), zero columns / rows, wide dynamic range,
+super-chunked slicing, the fused stopping-metric snapshot, bitwise determinism."""
+
+import numpy as np
+import pytest
+
+from util import gauss
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def dev(x, torch):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def exact_gram(x, y, cols1=None, cols2=None):
+    """X^T Y in extended precision (np.longdouble: 64-bit significand, i.e. 11 bits beyond fp64),
+    optionally only on sampled columns; returns (reference, |X|^T |Y|)."""
+    if cols1 is not None:
+        x, y = x[:, cols1], y[:, cols2]
+    xl = x.astype(np.longdouble)
+    yl = y.astype(np.longdouble)
+    return (xl.T @ yl).astype(np.float64), (np.abs(x).T @ np.abs(y))
+
+
+def sample(m, k, seed):
+    return np.sort(np.random.default_rng(seed).choice(m, size=min(m, k), replace=False))
+
+
+def emu(torch, on=True):
+    from paper_1407_7506_b200 import kernels as K
+
+    return K.fp64_emulation(on)
+
+
+@pytest.mark.parametrize("n,m1,m2", [(20000, 64, 64), (40000, 200, 130), (110592, 523, 523), (70001, 97, 333)])
+def test_ozaki_gram_within_dgemm_bound(cuda, n, m1, m2):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    rng = np.random.default_rng(n + m1)
+    x = gauss(n, m1, 1) * np.exp(rng.uniform(-6, 6, m1))[None, :]
+    y = gauss(n, m2, 2) * np.exp(rng.uniform(-6, 6, m2))[None, :]
+    x[:, 3] = 0.0  # an all-zero column
+    with emu(torch):
+        c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    c1, c2 = sample(m1, 24, 1), sample(m2, 24, 2)
+    c1[0] = 3
+    ref, absprod = exact_gram(x, y, c1, c2)
+    err = np.abs(c[np.ix_(c1, c2)] - ref)
+    assert np.all(err <= 4 * U * absprod + 1e-300), (err / (absprod + 1e-300)).max()
+    assert np.all(c[3] == 0.0)
+
+
+def test_ozaki_gram_symmetric_and_views(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m = 50000, 300
+    big = dev(gauss(n, m + 20, 3), torch)
+    v = big[:, 11 : 11 + m]
+    x = v.cpu().numpy()
+    cs = sample(m, 40, 3)
+    ref, absprod = exact_gram(x, x, cs, cs)
+    with emu(torch):
+        g = K.gram(v, v, symmetric=True).cpu().numpy()
+        g2 = K.gram(v, v, symmetric=True).cpu().numpy()
+        gn = K.gram(v, v).cpu().numpy()
+    assert np.array_equal(g, g.T)
+    assert np.array_equal(g, g2)  # deterministic
+    assert np.all(np.abs(g[np.ix_(cs, cs)] - ref) <= 4 * U * absprod)
+    assert np.all(np.abs(gn[np.ix_(cs, cs)] - ref) <= 4 * U * absprod)
+
+
+def test_ozaki_gram_complex(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m1, m2 = 30000, 70, 90
+    x = gauss(n, m1, 4) + 1j * gauss(n, m1, 5)
+    y = gauss(n, m2, 6) + 1j * gauss(n, m2, 7)
+    with emu(torch):
+        c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    c1, c2 = sample(m1, 20, 6), sample(m2, 20, 7)
+    xs, ys = x[:, c1], y[:, c2]
+    ref = (xs.conj().T.astype(np.clongdouble) @ ys.astype(np.clongdouble)).astype(np.complex128)
+    bound = 8 * U * (np.abs(xs).T @ np.abs(ys))
+    assert np.all(np.abs(c[np.ix_(c1, c2)] - ref) <= bound)
+
+
+def test_ozaki_gram_nonfinite_propagates(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m = 20000, 80
+    x = gauss(n, m, 8)
+    y = gauss(n, m, 9)
+    x[123, 5] = np.nan
+    y[77, 9] = np.inf
+    with emu(torch):
+        c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    assert np.all(np.isnan(c[5, :]))
+    assert np.all(np.isnan(c[:, 9]))
+    ok = np.ones_like(c, dtype=bool)
+    ok[5, :] = False
+    ok[:, 9] = False
+    assert np.all(np.isfinite(c[ok]))
+
+
+def test_ozaki_gram_superchunks_match(cuda):
+    """A workspace that holds a third of the digits: rows are sliced in super-chunks and the
+    partial Grams accumulate in order; same bound (and same chunk partials) as one pass."""
+    from paper_1407_7506_b200 import _lib
+    from paper_1407_7506_b200.kernels import stream_ptr
+
+    torch = cuda
+    lib = _lib.load()
+    n, m = 100000, 128
+    x = dev(gauss(n, m, 10), torch)
+    y = dev(gauss(n, m, 11), torch)
+    full = lib.bk_ozaki_gram_ws_bytes(n, m, m, 0, 0)
+    outs = []
+    for frac in (1.0, 0.34):
+        nb = int(full * frac)
+        ws = torch.zeros(max(nb, full), dtype=torch.uint8, device="cuda")
+        c = torch.empty((m, m), dtype=torch.float64, device="cuda")
+        _lib.call("bk_ozaki_gram_d", n, m, m, x.data_ptr(), m, y.data_ptr(), m, c.data_ptr(), m, 0, ws.data_ptr(),
+                  nb if frac < 1 else full, stream_ptr())
+        outs.append(c.cpu().numpy())
+    xn, yn = x.cpu().numpy(), y.cpu().numpy()
+    cs = sample(m, 32, 4)
+    ref, absprod = exact_gram(xn, yn, cs, cs)
+    for c in outs:
+        assert np.all(np.abs(c[np.ix_(cs, cs)] - ref) <= 4 * U * absprod)
+
+
+@pytest.mark.parametrize("n,K_,N,nprob", [(40000, 523, 523, 2), (16384, 64, 200, 1), (30001, 300, 77, 4)])
+def test_ozaki_tsgemm(cuda, n, K_, N, nprob):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    rng = np.random.default_rng(K_)
+    xs = [gauss(n, K_, 20 + b) * np.exp(rng.uniform(-5, 5, n))[:, None] for b in range(nprob)]
+    gs = [gauss(K_, N, 30 + b) * np.exp(rng.uniform(-5, 5, N))[None, :] for b in range(nprob)]
+    zs = [gauss(n, N, 40 + b) for b in range(nprob)]
+    s = np.abs(gauss(n, 1, 50))[:, 0] + 0.5
+    ys = [torch.empty((n, N), dtype=torch.float64, device="cuda") for _ in range(nprob)]
+    with emu(torch):
+        K.tsgemm([dev(x, torch) for x in xs], [dev(g, torch) for g in gs], ys, alpha=-1.0, beta=1.0,
+                 zs=[dev(z, torch) for z in zs], rowscale=dev(s, torch))
+    rows = sample(n, 300, 5)
+    for b in range(nprob):
+        xr, zr, sr = xs[b][rows], zs[b][rows], s[rows, None]
+        prod = xr.astype(np.longdouble) @ gs[b].astype(np.longdouble)
+        ref = (sr * (zr - prod)).astype(np.float64)
+        bound = sr * (4 * U * (np.abs(xr) @ np.abs(gs[b])) + 2 * U * np.abs(zr - prod.astype(np.float64)))
+        assert np.all(np.abs(ys[b].cpu().numpy()[rows] - ref) <= bound + 1e-300), b
+
+
+def test_ozaki_tsgemm_metric_snapshot_and_inplace(cuda):
+    """The fused stopping metric: sum over cols < nsplit of (alpha X[:, :ksplit] G[:ksplit] + beta Z)^2,
+    with Z aliasing Y (in-place update) and a metric-only launch (Y = None)."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, Kt, N, ks, ns = 50000, 523, 523, 513, 500
+    x, g, ax = gauss(n, Kt, 60), gauss(Kt, N, 61) * 0.1, gauss(n, N, 62)
+    ref_metric = np.sum((ax[:, :ns] - x[:, :ks] @ g[:ks, :ns]) ** 2)
+    ref_w = ax - x @ g
+    with emu(torch):
+        w = dev(ax, torch)
+        metric = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [w], alpha=-1.0, beta=1.0, zs=[w], metric=metric, ksplit=ks,
+                 nsplit=ns)
+        m2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [None], alpha=-1.0, beta=1.0, zs=[dev(ax, torch)], metric=m2,
+                 ksplit=ks, nsplit=ns)
+        m3 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [None], alpha=-1.0, beta=1.0, zs=[dev(ax, torch)], metric=m3,
+                 ksplit=Kt, nsplit=N)
+    assert abs(metric.item() - ref_metric) <= 1e-12 * ref_metric
+    assert metric.item() == m2.item()
+    assert abs(m3.item() - np.sum(ref_w ** 2)) <= 1e-12 * np.sum(ref_w ** 2)
+    assert np.max(np.abs(w.cpu().numpy() - ref_w)) <= 1e-13 * np.abs(ref_w).max() * 10
+
+
+def test_ozaki_tsgemm_nonfinite_row(cuda):
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, Kt, N = 20000, 100, 100
+    x, g = gauss(n, Kt, 70), gauss(Kt, N, 71)
+    x[9, 4] = np.nan
+    g[3, 7] = np.inf
+    y = torch.empty((n, N), dtype=torch.float64, device="cuda")
+    with emu(torch):
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [y])
+    yn = y.cpu().numpy()
+    assert np.all(np.isnan(yn[9]))
+    assert np.all(np.isnan(yn[:, 7]))
+    ok = np.ones_like(yn, dtype=bool)
+    ok[9] = False
+    ok[:, 7] = False
+    assert np.all(np.isfinite(yn[ok]))

@@ -28,48 +28,89 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, int c0,
 }
 
 // ---------------------------------------------------------------- prepass
-// column max |x| as monotone uint64 bit patterns (colmax zeroed by the caller)
-__global__ void oz_colmax(int64_t n, int m, const double* X, int64_t ld, unsigned long long* colmax, int rows_per_cta) {
-  int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min((int64_t)n, r0 + rows_per_cta);
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
-    double mx = 0;
-    for (int64_t r = r0; r < r1; ++r) mx = fmax(mx, fabs(X[r * ld + c]));
-    atomicMax(colmax + c, (unsigned long long)__double_as_longlong(mx));
+// column max |x| as monotone uint64 bit patterns (colmax zeroed by the caller); CTA = 64 rows x
+// 256 columns, 16 loads in flight per thread
+__global__ void __launch_bounds__(256) oz_colmax(int64_t n, int m, const double* X, int64_t ld, unsigned long long* colmax) {
+  const int c = blockIdx.y * 256 + threadIdx.x;
+  if (c >= m) return;
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int nr = (int)min((int64_t)64, n - r0);
+  const double* p = X + r0 * ld + c;
+  double mx = 0;
+  if (nr == 64) {
+#pragma unroll 16
+    for (int r = 0; r < 64; ++r) mx = fmax(mx, fabs(__ldg(p + r * ld)));
+  } else {
+    for (int r = 0; r < nr; ++r) mx = fmax(mx, fabs(__ldg(p + r * ld)));
   }
+  atomicMax(colmax + c, (unsigned long long)__double_as_longlong(mx));
 }
 
-// slices: out[s][c][k] (k = row index, Kld bytes per column row), exponent E[c] with max|x_c| < 2^E
-// tile 128 rows x 32 columns per CTA, 256 threads
-template <int S>
-__global__ void oz_slice_cols(int64_t n, int m, const double* X, int64_t ld, const unsigned long long* colmax,
-                              int8_t* out, int64_t Kld, int64_t slice_stride) {
+// slices: out[s][c][k] (k = row index, Kld bytes per column), exponent E[c] with max|x_c| < 2^E.
+// CTA = 128 rows x 32 columns, 256 threads; thread (column cl, rows 16 g .. 16 g + 15) builds one
+// 16-byte vector per slice
+template <int S, bool DIG8>
+__global__ void __launch_bounds__(256) oz_slice_cols(int64_t n, int m, const double* X, int64_t ld,
+                                                     const unsigned long long* colmax, int8_t* out, int64_t Kld,
+                                                     int64_t slice_stride) {
   __shared__ __align__(16) int8_t t[S][32][128 + 16];
   const int64_t r0 = (int64_t)blockIdx.x * 128;
   const int c0 = blockIdx.y * 32;
-  const int cl = threadIdx.x & 31, rq = threadIdx.x >> 5;  // 8 row groups
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = c0 + cl;
   double scale = 0;
   if (c < m) {
-    double mx = __longlong_as_double((long long)colmax[c]);
-    int E = (mx > 0) ? ilogb(mx) + 1 : 0;
-    scale = ldexp(1.0, 7 * S - E);  // |x| 2^-E 2^(7S)
+    const double mx = __longlong_as_double((long long)colmax[c]);
+    const int E = (mx > 0) ? ilogb(mx) + 1 : 0;
+    scale = DIG8 ? ldexp(1.0, 8 * S - 2 - E) : ldexp(1.0, 7 * S - E);  // |x| 2^-E 2^(7S) < 2^(7S)
   }
-  for (int rr = rq; rr < 128; rr += 8) {
-    int64_t r = r0 + rr;
-    double x = (c < m && r < n) ? X[r * ld + c] : 0.0;
-    unsigned long long Y = (unsigned long long)(fabs(x) * scale);
-    int sg = x < 0 ? -1 : 1;
+  double v[16];
 #pragma unroll
-    for (int s = 0; s < S; ++s) t[s][cl][rr] = (int8_t)(sg * (int)((Y >> (7 * (S - 1 - s))) & 127));
+  for (int e = 0; e < 16; ++e) {
+    const int64_t r = r0 + g * 16 + e;
+    v[e] = (c < m && r < n) ? __ldg(X + r * ld + c) : 0.0;
   }
+  uint32_t w[S][4];
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[s][q] = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    if (DIG8) {
+      // signed base-256 digits: Z = trunc(x 2^(8S-2-E)), |Z| < 2^(8S-2); Z + B (B = 0x80 in every lower
+      // byte) has unsigned lower bytes u_i, digit_i = u_i - 128, top digit = (Z + B) >> 8(S-1)
+      const long long Z = (long long)(v[e] * scale);
+      unsigned long long B = 0;
+#pragma unroll
+      for (int q = 0; q < S - 1; ++q) B |= 0x80ull << (8 * q);
+      const long long U = Z + (long long)B;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        int d = (s == 0) ? (int)(U >> (8 * (S - 1))) : (int)((U >> (8 * (S - 1 - s))) & 255) - 128;
+        w[s][e >> 2] |= ((uint32_t)(d & 255)) << (8 * (e & 3));
+      }
+    } else {
+      const unsigned long long Y = (unsigned long long)(fabs(v[e]) * scale);
+      const bool neg = v[e] < 0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        int d = (int)((Y >> (7 * (S - 1 - s))) & 127);
+        d = neg ? -d : d;
+        w[s][e >> 2] |= ((uint32_t)(d & 255)) << (8 * (e & 3));
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    *reinterpret_cast<uint4*>(&t[s][cl][g * 16]) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
   __syncthreads();
   // write: per (s, col) 128 bytes = 8 x 16-byte pieces
   for (int i = threadIdx.x; i < S * 32 * 8; i += blockDim.x) {
-    int p = i & 7, cc = (i >> 3) & 31, s = i >> 8;
-    if (c0 + cc < m && r0 + p * 16 < Kld) {
+    const int p = i & 7, cc = (i >> 3) & 31, s = i >> 8;
+    if (c0 + cc < m && r0 + p * 16 < Kld)
       *reinterpret_cast<int4*>(out + s * slice_stride + (int64_t)(c0 + cc) * Kld + r0 + p * 16) =
           *reinterpret_cast<const int4*>(&t[s][cc][p * 16]);
-    }
   }
 }
 
@@ -104,7 +145,7 @@ struct OzCfg {
 };
 
 // grid: (tiles, chunks); C partial[chunk][tile][128][64] in fp64 (scaled by 2^(E1+E2))
-template <int S, int KB, int STAGES>
+template <int S, int KB, int STAGES, bool DIG8>
 __global__ void __launch_bounds__(192, 1)
 oz_gram_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m1, int m2,
                int64_t n, int64_t rows_per_chunk, const int* EA, const int* EB, const int2* tiles, double* part) {
@@ -154,7 +195,6 @@ oz_gram_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   } else if (warp == 1) {
     // instruction descriptor: S32 accum (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1), K-major,
     // N >> 3 at bit 17, M >> 4 at bit 24
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     for (int kb = 0; kb < nk; ++kb) {
       const int st = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
@@ -165,15 +205,19 @@ oz_gram_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < KB / 32; ++ks) {
+          // A_i x [B_j0 .. B_j0+nj-1] in one MMA (B slices are consecutive 64-row blocks in shared
+          // memory; accumulators acc[t] are consecutive 64-column blocks of TMEM, t = i + j)
 #pragma unroll
-          for (int t = 0; t < S; ++t) {
+          for (int i = 0; i < S; ++i) {
 #pragma unroll
-            for (int i = 0; i <= t; ++i) {
-              const int j = t - i;
+            for (int j0 = 0; j0 < S - i; j0 += 4) {
+              const int nj = (S - i - j0) < 4 ? (S - i - j0) : 4;
+              const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((nj * BN) >> 3) << 17) |
+                                     ((uint32_t)(BM >> 4) << 24);
               const uint64_t da = make_desc(sa + i * BM * KB + ks * 32, KB);
-              const uint64_t db = make_desc(sb + j * BN * KB + ks * 32, KB);
+              const uint64_t db = make_desc(sb + j0 * BN * KB + ks * 32, KB);
               const uint32_t acc = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;
-              const uint32_t dt = tmem + t * BN;
+              const uint32_t dt = tmem + (i + j0) * BN;
               asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
                            ::"r"(dt), "l"(da), "l"(db), "r"(idesc), "r"(acc));
@@ -209,7 +253,7 @@ oz_gram_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                      : "r"(ta));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const double w = ldexp(1.0, -7 * (t + 2));
+        const double w = DIG8 ? ldexp(1.0, -12 - 8 * t) : ldexp(1.0, -7 * (t + 2));
 #pragma unroll
         for (int e = 0; e < 16; ++e) acc[e] = fma((double)(int)v[e], w, acc[e]);
       }
@@ -226,17 +270,18 @@ oz_gram_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
-__global__ void oz_reduce(int m1, int m2, int ntiles, int nchunks, const int2* tiles, const double* part, double* Cm, int64_t ldc) {
+// C = sum over chunks of the partials (fixed order); grid (tiles, 16 row groups of 8 rows)
+__global__ void oz_reduce(int m1, int m2, int ntiles, int nchunks, const int2* tiles, const double* part, double* Cm,
+                          int64_t ldc, int sym) {
   const int tix = blockIdx.x;
   const int2 tile = tiles[tix];
-  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
-    const int r = e / BN, c = e % BN;
-    const int gr = tile.x * BM + r, gc = tile.y * BN + c;
-    if (gr >= m1 || gc >= m2) continue;
-    double s = 0;
-    for (int ch = 0; ch < nchunks; ++ch) s += part[(((int64_t)ch * ntiles + tix) * BM + r) * BN + c];
-    Cm[(int64_t)gr * ldc + gc] = s;
-  }
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 6), c = threadIdx.x & 63;
+  const int gr = tile.x * BM + r, gc = tile.y * BN + c;
+  if (gr >= m1 || gc >= m2) return;
+  double s = 0;
+  for (int ch = 0; ch < nchunks; ++ch) s += part[(((int64_t)ch * ntiles + tix) * BM + r) * BN + c];
+  if (!sym || gc >= gr) Cm[(int64_t)gr * ldc + gc] = s;
+  if (sym && gc > gr) Cm[(int64_t)gc * ldc + gr] = s;
 }
 
 typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -260,10 +305,10 @@ static void make_map(CUtensorMap* map, const int8_t* base, int64_t Kld, int m, i
   if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); exit(1); }
 }
 
-template <int S, int KB, int STAGES>
+template <int S, int KB, int STAGES, bool DIG8 = false>
 static void run(int64_t n, int m, int nchunks_req, bool sym, int reps) {
   using Cfg = OzCfg<S, KB, STAGES>;
-  printf("== S=%d KB=%d STAGES=%d n=%lld m=%d sym=%d smem=%d\n", S, KB, STAGES, (long long)n, m, (int)sym, Cfg::SMEM);
+  printf("== S=%d dig8=%d KB=%d STAGES=%d n=%lld m=%d sym=%d smem=%d\n", S, (int)DIG8, KB, STAGES, (long long)n, m, (int)sym, Cfg::SMEM);
   const int64_t ld = (m + 15) / 16 * 16;
   std::vector<double> hX(n * ld), hY(n * ld);
   std::mt19937_64 g(7);
@@ -304,7 +349,7 @@ static void run(int64_t n, int m, int nchunks_req, bool sym, int reps) {
   CUtensorMap mA, mB;
   make_map(&mA, SA, Kld, m, S, BM, KB);
   make_map(&mB, SB, Kld, m, S, BN, KB);
-  CK(cudaFuncSetAttribute(oz_gram_kernel<S, KB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  CK(cudaFuncSetAttribute(oz_gram_kernel<S, KB, STAGES, DIG8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
 
   cublasHandle_t hb;
   cublasCreate(&hb);
@@ -313,22 +358,22 @@ static void run(int64_t n, int m, int nchunks_req, bool sym, int reps) {
   for (auto& x : e) cudaEventCreate(&x);
   auto prepass = [&]() {
     cudaMemsetAsync(cmA, 0, m * 8); cudaMemsetAsync(cmB, 0, m * 8);
-    const int rpc2 = 1024;
-    oz_colmax<<<(unsigned)((n + rpc2 - 1) / rpc2), 256>>>(n, m, X, ld, cmA, rpc2);
-    oz_colmax<<<(unsigned)((n + rpc2 - 1) / rpc2), 256>>>(n, m, Y, ld, cmB, rpc2);
+    dim3 gc((unsigned)((n + 63) / 64), (m + 255) / 256);
+    oz_colmax<<<gc, 256>>>(n, m, X, ld, cmA);
+    oz_colmax<<<gc, 256>>>(n, m, Y, ld, cmB);
     oz_exponents<<<(m + 255) / 256, 256>>>(m, cmA, EA);
     oz_exponents<<<(m + 255) / 256, 256>>>(m, cmB, EB);
   };
   auto slice = [&]() {
     dim3 gs((unsigned)((n + 127) / 128), (m + 31) / 32);
-    oz_slice_cols<S><<<gs, 256>>>(n, m, X, ld, cmA, SA, Kld, Kld * m);
-    oz_slice_cols<S><<<gs, 256>>>(n, m, Y, ld, cmB, SB, Kld, Kld * m);
+    oz_slice_cols<S, DIG8><<<gs, 256>>>(n, m, X, ld, cmA, SA, Kld, Kld * m);
+    oz_slice_cols<S, DIG8><<<gs, 256>>>(n, m, Y, ld, cmB, SB, Kld, Kld * m);
   };
   auto gemm = [&]() {
     dim3 gg(ntiles, nchunks);
-    oz_gram_kernel<S, KB, STAGES><<<gg, 192, Cfg::SMEM>>>(mA, mB, m, m, n, rpc, EA, EB, dt, part);
+    oz_gram_kernel<S, KB, STAGES, DIG8><<<gg, 192, Cfg::SMEM>>>(mA, mB, m, m, n, rpc, EA, EB, dt, part);
   };
-  auto red = [&]() { oz_reduce<<<ntiles, 256>>>(m, m, ntiles, nchunks, dt, part, Co, m); };
+  auto red = [&]() { oz_reduce<<<dim3(ntiles, 16), 512>>>(m, m, ntiles, nchunks, dt, part, Co, m, 0); };
   CK(cudaMemset(Co, 0, (int64_t)m * m * 8));
   prepass(); slice(); gemm(); red();
   CK(cudaGetLastError());
@@ -400,11 +445,11 @@ int main(int argc, char** argv) {
   int m = argc > 2 ? atoi(argv[2]) : 523;
   int chunks = argc > 3 ? atoi(argv[3]) : 17;
   int reps = 5;
-  run<1, 64, 2>(4096, 192, 1, false, 2);   // plain int8 GEMM sanity (S = 1)
-  run<8, 64, 2>(8192, 200, 1, false, 2);
+  if (argc > 4) { run<7, 64, 2, true>(n, m, chunks, false, 1); return 0; }
   run<8, 64, 2>(n, m, chunks, true, reps);
-  run<8, 32, 4>(n, m, chunks, true, reps);
-  run<7, 64, 2>(n, m, chunks, true, reps);
-  run<8, 64, 2>(n, m, chunks, false, reps);
+  run<7, 64, 2, true>(8192, 200, 1, false, 2);
+  run<7, 64, 2, true>(n, m, chunks, true, reps);
+  run<7, 64, 2, true>(n, m, chunks, false, reps);
+  run<6, 64, 3, true>(n, m, chunks, true, reps);
   return 0;
 }
