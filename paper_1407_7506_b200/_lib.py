@@ -14,7 +14,7 @@ import threading
 from .errors import DeviceError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libppcg_b200.so")
+LIB_PATH = os.environ.get("PPCG_B200_LIB") or os.path.join(_HERE, "libppcg_b200.so")  # override: A/B builds
 
 _lock = threading.Lock()
 _lib = None

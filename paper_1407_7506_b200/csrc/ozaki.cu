@@ -35,12 +35,19 @@ namespace oz {
 constexpr int S = 8;            // digits per element (and digit groups t = i + j <= S - 1 kept)
 constexpr int BM = 128;         // output rows per CTA (TMEM lanes)
 constexpr int BN = 64;          // output columns per digit group (TMEM columns per group)
-constexpr int KB = 64;          // k bytes (= k elements) per pipeline stage (64-byte swizzle)
-constexpr int STAGES = 2;
+#ifndef OZ_KB
+#define OZ_KB 64
+#define OZ_STAGES 2
+#endif
+constexpr int KB = OZ_KB;       // k bytes (= k elements) per pipeline stage (swizzle width)
+constexpr int STAGES = OZ_STAGES;
 constexpr int A_BYTES = S * BM * KB, B_BYTES = S * BN * KB;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TS_STAGE_OUT = 8 * 32 * 16 * 8;  // tall GEMM: per epilogue warp a 32 x 16 fp64 staging tile
+constexpr int TS_SMEM = SMEM + TS_STAGE_OUT;
 constexpr int THREADS = 192;    // warp 0 TMA, warp 1 MMA (+TMEM alloc), warps 2-5 epilogue
+constexpr int TS_THREADS = 320; // tall GEMM: 8 epilogue warps (lane quadrant x column half)
 constexpr int MAX_CHUNK = 16320;  // rows per int32 accumulation: S pairs * 2^14 * 16320 < 2^31
 constexpr int KPAD = 64;
 
@@ -55,8 +62,9 @@ BK_DEV void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uin
 // UMMA shared-memory descriptor: K-major, 64-byte swizzle, SBO = 8 rows x 64 B, LBO = 1 (unused
 // for swizzled K-major), version 1 (sm_100)
 BK_DEV uint64_t umma_desc(uint32_t saddr) {
+  constexpr uint64_t layout = KB == 128 ? 2 : KB == 64 ? 4 : 6;  // SWIZZLE_128B / 64B / 32B
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * KB) >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+         ((uint64_t)1 << 46) | (layout << 61);
 }
 
 // instruction descriptor kind::i8: s32 accumulate, signed A and B, K-major both, N, M = 128
@@ -88,6 +96,41 @@ BK_DEV void combine16(uint32_t tmem_lane, int cc, double (&acc)[16]) {
   }
 }
 
+// Same as combine16 but exact in integers first: H = sum_{t<4} acc_t 2^(8(3-t)), L likewise for
+// t >= 4 (|H|, |L| < 2^56 fit int64), result = 2^-36 (H + 2^-32 L): two int64 -> fp64
+// conversions per column instead of eight.  Caller applies the 2^-36 (folded into the exponent).
+BK_DEV void combine16_i64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
+  static_assert(S == 8, "two halves of four digit groups");
+  long long h[16];
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + t * BN + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      long long x = (long long)(int)v[0][e];
+      x = (x << 8) + (long long)(int)v[1][e];
+      x = (x << 8) + (long long)(int)v[2][e];
+      h[e] = (x << 8) + (long long)(int)v[3][e];
+    }
+  }
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * BN + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      long long x = (long long)(int)v[0][e];
+      x = (x << 8) + (long long)(int)v[1][e];
+      x = (x << 8) + (long long)(int)v[2][e];
+      x = (x << 8) + (long long)(int)v[3][e];
+      acc[e] = fma((double)x, 0x1p-32, (double)h[e]);
+    }
+  }
+}
+
 // signed base-256 digits of x 2^sh, sh = 8S-2-E (|x 2^sh| < 2^(8S-2)): packs digit s of 4 consecutive
 // elements into w[s] (byte e of the word = element e)
 BK_DEV void digits4(const double (&v)[4], int sh, uint32_t (&w)[S]) {
@@ -113,7 +156,11 @@ constexpr int NON_FINITE = 0x40000000;
 BK_DEV int exp_of(double mx) { return !isfinite(mx) ? NON_FINITE : mx > 0 ? ilogb(mx) + 1 : 0; }
 BK_DEV int shift_of(int E) { return E == NON_FINITE ? -2000 : 8 * S - 2 - E; }
 BK_DEV double scaled(double acc, int e1, int e2) {
-  return (e1 == NON_FINITE || e2 == NON_FINITE) ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(acc, e1 + e2);
+  if (e1 == NON_FINITE || e2 == NON_FINITE) return __longlong_as_double(0x7ff8000000000000ll);
+  const int e = e1 + e2;
+  // 2^e as a normal double from its bits (one multiply); ldexp only outside the normal range
+  if (e >= -1022 && e <= 1023) return acc * __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(acc, e);
 }
 
 // ---------------------------------------------------------------------------------------- slicing
@@ -146,9 +193,16 @@ __global__ void __launch_bounds__(256) k_colmax(int64_t n, int m, const double* 
   atomicMax(colmax + c, bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(mx));
 }
 
-__global__ void k_exponents(int m, const unsigned long long* colmax, int* E) {
+__global__ void k_exponents(int m, const unsigned long long* colmax, int* E, double* pow2) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < m) E[c] = exp_of(__longlong_as_double((long long)colmax[c]));
+  if (c < m) {
+    const int e = exp_of(__longlong_as_double((long long)colmax[c]));
+    E[c] = e;
+    if (pow2)
+      pow2[c] = e == NON_FINITE ? __longlong_as_double(0x7ff8000000000000ll)
+                : (e >= -1000 && e <= 1000) ? __longlong_as_double((long long)(e + 1023) << 52)
+                                            : 0.0;
+  }
 }
 
 // column digits, transposed: out[s][c][k - r_base] for rows k in [r0, r0 + 128) of the n x m block
@@ -246,11 +300,13 @@ struct TsEpi {
   double alpha, beta;
   const int* ER[4];   // row exponents (indexed by global row)
   const int* EG[4];   // G column exponents
+  const double* EGf[4];  // 2^EG when |EG| <= 1000, NaN for non-finite columns, else 0 (exact path)
   const double* Z[4];
   double* Y[4];
   int64_t ldz, ldy;
   const double* rowscale;  // indexed by global row
   double* metric_ws;  // per-CTA partial sums of squares (problem 0)
+  int dbg;            // experiments (PPCG_OZ_DBG): 1 = no MMAs, 2 = no epilogue stores, 4 = no TMA
 };
 
 template <int MODE>
@@ -509,6 +565,287 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
+// Tall GEMM, persistent: one CTA per SM walks the tiles tau = blockIdx.x + i * gridDim.x (column
+// tiles fastest, so the column tiles of a row block run side by side and share its X digits in
+// L2).  The producer runs ahead across tile boundaries; the epilogue drains TMEM into registers
+// (digit groups combined in fp64), releases TMEM to the MMA warp, and only then scales, reads Z
+// and writes Y -- the stores of tile i overlap the MMAs of tile i + 1.  Metric tiles (problem 0,
+// columns < nsplit) pause the MMA warp after the snapshot stage until the epilogue has read it.
+__global__ void __launch_bounds__(TS_THREADS, 1)
+    k_oz_ts(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+            const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
+            const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
+            const __grid_constant__ CUtensorMap mapB2, const __grid_constant__ CUtensorMap mapB3, const TsEpi P,
+            int ctn, int rtn, int nprob) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint64_t* tmem_free = done + 1;
+  uint64_t* snap_full = done + 2;
+  uint64_t* snap_free = done + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 4);
+  double* stage_out = reinterpret_cast<double*>(sm + STAGES * STAGE_BYTES + 256);
+  __shared__ double s_red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = ctn * rtn * nprob;
+
+  struct Tile {
+    int prob, rowA, rowB, nk, snap;
+  };
+  auto tile_of = [&](int tau) {
+    Tile t;
+    t.prob = tau / (ctn * rtn);
+    const int r = tau - t.prob * ctn * rtn;
+    t.rowA = (r / ctn) * BM;
+    t.rowB = (r % ctn) * BN;
+    t.nk = P.nk;
+    if (P.upper) t.nk = min(t.nk, (t.rowB + BN + KB - 1) / KB);
+    t.snap = (t.prob == 0 && P.snap_stage >= 0 && t.rowB < P.nsplit) ? P.snap_stage : -1;
+    return t;
+  };
+  auto mapA = [&](int b) { return b == 0 ? &mapA0 : b == 1 ? &mapA1 : b == 2 ? &mapA2 : &mapA3; };
+  auto mapB = [&](int b) { return b == 0 ? &mapB0 : b == 1 ? &mapB1 : b == 2 ? &mapB2 : &mapB3; };
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(tmem_free, 256);
+    mbar_init(snap_full, 1);
+    mbar_init(snap_free, 256);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int b = 0; b < nprob; ++b) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(mapA(b)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(mapB(b)) : "memory");
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;  // global stage counter
+      for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
+        const Tile t = tile_of(tau);
+        const CUtensorMap* mA = mapA(t.prob);
+        const CUtensorMap* mB = mapB(t.prob);
+        for (int kb = 0; kb < t.nk; ++kb, ++it) {
+          const int st = it % STAGES;
+          mbar_wait(empty + st, ((it / STAGES) & 1) ^ 1);
+          uint8_t* sa = sm + st * STAGE_BYTES;
+          if (P.dbg & 4) {
+            mbar_arrive(full + st);
+            continue;
+          }
+          mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+          tma3d(sa, mA, kb * KB, t.rowA, 0, full + st);
+          tma3d(sa + A_BYTES, mB, kb * KB, t.rowB, 0, full + st);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int it = 0, ti = 0, si = 0;
+    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++ti) {
+      const Tile t = tile_of(tau);
+      mbar_wait(tmem_free, (ti & 1) ^ 1);  // epilogue has drained the previous tile
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < t.nk; ++kb, ++it) {
+        const int st = it % STAGES;
+        mbar_wait(full + st, (it / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(sm + st * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < KB / 32; ++ks) {
+            if (P.dbg & 1) break;
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+#pragma unroll
+              for (int j0 = 0; j0 < S - i; j0 += 4) {
+                const int nj = (S - i - j0) < 4 ? (S - i - j0) : 4;
+                const uint64_t da = umma_desc(sa + i * BM * KB + ks * 32);
+                const uint64_t db = umma_desc(sb + j0 * BN * KB + ks * 32);
+                const uint32_t accf = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (i + j0) * BN),
+                    "l"(da), "l"(db), "r"(idesc_i8(nj * BN)), "r"(accf));
+              }
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(empty + st))
+                       : "memory");
+          if (kb == t.snap)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(snap_full))
+                         : "memory");
+          if (kb == t.nk - 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(done))
+                         : "memory");
+        }
+        __syncwarp();
+        if (kb == t.snap) {
+          if (kb != t.nk - 1) mbar_wait(snap_free, si & 1);  // epilogue has read the snapshot
+          ++si;
+        }
+      }
+    }
+  } else {
+    // 8 epilogue warps: TMEM lane quadrant q = warp % 4 (hardware rule), column half h
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int c0 = h * 32;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    double ss = 0;  // metric partial (problem 0 tiles with columns < nsplit)
+    int ti = 0, si = 0;
+    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++ti) {
+      const Tile t = tile_of(tau);
+      const int64_t lrow = t.rowA + r;
+      const bool live = lrow < P.nrows;
+      const int64_t grow = P.r_base + lrow;
+      const int er0 = live ? P.ER[t.prob][grow] : 0;
+      const int er = er0 == NON_FINITE ? NON_FINITE : er0 - 36;  // combine16_i64 leaves 2^-36
+      const int* EG = P.EG[t.prob];
+      const double* Z = P.Z[t.prob];
+      double* Y = P.Y[t.prob];
+      const int ncol = min(32, P.N - (t.rowB + c0));  // valid columns of this warp's half (may be <= 0)
+      if (t.snap >= 0) {
+        mbar_wait(snap_full, si & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 16) {
+          if (t.rowB + c0 + cc < P.nsplit && cc < ncol) {
+            double acc[16];
+            combine16_i64(tl, c0 + cc, acc);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int gc = t.rowB + c0 + cc + e;
+              if (live && gc < P.nsplit && gc < P.N) {
+                double v = P.alpha * scaled(acc[e], er, EG[gc]);
+                if (P.beta != 0.0) v = fma(P.beta, Z[grow * P.ldz + gc], v);
+                ss = fma(v, v, ss);
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(snap_free);
+        ++si;
+      }
+      // this row's Z segment (32 doubles) into L2 while the tile's MMAs run
+      if (live && ncol > 0 && Z != nullptr && P.beta != 0.0 && Y != nullptr) {
+        const double* zr = Z + grow * P.ldz + t.rowB + c0;
+        prefetch_l2(zr);
+        prefetch_l2(zr + 16);
+      }
+      mbar_wait(done, ti & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double acc[32];
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 16) {
+        if (cc < ncol) {
+          double a16[16];
+          combine16_i64(tl, c0 + cc, a16);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[cc + e] = a16[e];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(tmem_free);
+      if (Y == nullptr || ncol <= 0 || (P.dbg & 2)) continue;
+      const bool vec = ncol == 32 && !(P.ldy & 1) && (P.beta == 0.0 || !(P.ldz & 1)) &&
+                       ((reinterpret_cast<uintptr_t>(Y + t.rowB + c0) & 15) == 0) &&
+                       (P.beta == 0.0 || (reinterpret_cast<uintptr_t>(Z + t.rowB + c0) & 15) == 0);
+      if (vec) {
+        // rows -> shared (16-byte pairs, XOR-swizzled by row), then 8 lanes per 128-byte row
+        // segment: Z loads and Y stores move whole lines
+        double* wb = stage_out + (warp - 2) * 512;
+        // row factor 2^er (exact power of two when er is in the normal range; otherwise, and for
+        // NaN markers, the exact per-element path)
+        const bool rfast = live && er >= -1000 && er <= 1000;
+        const double fr = rfast ? P.alpha * __longlong_as_double((long long)(er + 1023) << 52) : 0.0;
+        const double* EGf = P.EGf[t.prob];
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 16) {
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const int gc = t.rowB + c0 + cc + 2 * p;
+            const double2 fc = *reinterpret_cast<const double2*>(EGf + gc);
+            double u0, u1;
+            if (rfast && fc.x != 0.0 && fc.y != 0.0) {
+              u0 = acc[cc + 2 * p] * fc.x * fr;
+              u1 = acc[cc + 2 * p + 1] * fc.y * fr;
+            } else {
+              u0 = live ? P.alpha * scaled(acc[cc + 2 * p], er, EG[gc]) : 0.0;
+              u1 = live ? P.alpha * scaled(acc[cc + 2 * p + 1], er, EG[gc + 1]) : 0.0;
+            }
+            *reinterpret_cast<double2*>(wb + lane * 16 + ((p ^ (lane & 7)) * 2)) = make_double2(u0, u1);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3), p = lane & 7;
+            const int64_t lr = t.rowA + q * 32 + rr;
+            if (lr < P.nrows) {
+              const int64_t gr = P.r_base + lr;
+              const double2 u = *reinterpret_cast<const double2*>(wb + rr * 16 + ((p ^ (rr & 7)) * 2));
+              const int gc = t.rowB + c0 + cc + 2 * p;
+              double v0 = u.x, v1 = u.y;
+              if (P.beta != 0.0) {
+                const double2 z = *reinterpret_cast<const double2*>(Z + gr * P.ldz + gc);
+                v0 = fma(P.beta, z.x, v0);
+                v1 = fma(P.beta, z.y, v1);
+              }
+              const double srr = P.rowscale ? P.rowscale[gr] : 1.0;
+              *reinterpret_cast<double2*>(Y + gr * P.ldy + gc) = make_double2(srr * v0, srr * v1);
+            }
+          }
+          __syncwarp();
+        }
+      } else if (live) {
+        const double sr = P.rowscale ? P.rowscale[grow] : 1.0;
+        const int64_t zo = grow * P.ldz + t.rowB + c0, yo = grow * P.ldy + t.rowB + c0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (e < ncol) {
+            const int gc = t.rowB + c0 + e;
+            double v = P.alpha * scaled(acc[e], er, EG[gc]);
+            if (P.beta != 0.0) v = fma(P.beta, Z[zo + e], v);
+            Y[yo + e] = sr * v;
+          }
+        }
+      }
+    }
+    if (P.snap_stage >= 0) {
+      ss = warp_sum(ss);
+      if (lane == 0) s_red[warp - 2] = ss;
+      named_bar_sync(1, 256);
+      if (threadIdx.x == 64) {
+        double tsum = 0;
+        for (int w = 0; w < 8; ++w) tsum += s_red[w];
+        P.metric_ws[blockIdx.x] = tsum;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
 // C (+)= sum over chunks of the partials, fixed chunk order, compensated; symmetric: upper tiles
 // mirrored.
 // grid (tiles, 16): 8 rows x 64 columns per CTA
@@ -576,7 +913,11 @@ static bool encode_digits(CUtensorMap* map, const int8_t* base, int64_t kld, int
   const cuuint32_t box[3] = {(cuuint32_t)KB, (cuuint32_t)box_rows, (cuuint32_t)S};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             KB == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+             : KB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                        : CU_TENSOR_MAP_SWIZZLE_32B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -701,13 +1042,13 @@ extern "C" int bk_ozaki_gram_d(int64_t n, int m1, int m2, const double* X, int64
   BK_COUNT();
   k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
   BK_COUNT();
-  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA);
+  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA, nullptr);
   if (!same) {
     cudaMemsetAsync(cmB, 0, 8 * (size_t)m2, st);
     BK_COUNT();
     k_colmax<<<dim3((unsigned)((n + 63) / 64), (m2 + 255) / 256), 256, 0, st>>>(n, m2, Y, ldy, cmB);
     BK_COUNT();
-    k_exponents<<<(m2 + 255) / 256, 256, 0, st>>>(m2, cmB, EB);
+    k_exponents<<<(m2 + 255) / 256, 256, 0, st>>>(m2, cmB, EB, nullptr);
   }
   cudaFuncSetAttribute(k_oz_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   GramEpi P{};
@@ -755,7 +1096,7 @@ namespace oz {
 struct TsLayout {
   int kp1, kp;
   int64_t sc_rows;
-  int64_t off_ER, off_EG, off_cmG, off_sG, off_mws, off_sX, total;
+  int64_t off_ER, off_EG, off_EGf, off_cmG, off_sG, off_mws, off_sX, total;
 };
 static TsLayout ts_layout(int nprob, int64_t n, int K, int N, int ksplit, int64_t ws_cap) {
   TsLayout L{};
@@ -766,6 +1107,7 @@ static TsLayout ts_layout(int nprob, int64_t n, int K, int N, int ksplit, int64_
   int64_t o = 0;
   L.off_ER = o;  o += align_up(4 * (int64_t)nprob * n, 256);
   L.off_EG = o;  o += align_up(4 * (int64_t)nprob * N, 256);
+  L.off_EGf = o; o += align_up(8 * (int64_t)nprob * (N + 1), 256);
   L.off_cmG = o; o += align_up(8 * (int64_t)nprob * N, 256);
   L.off_sG = o;  o += align_up((int64_t)nprob * S * N * L.kp, 1024);
   const int64_t ctas_max = ((n + BM - 1) / BM) * ((N + BN - 1) / BN);
@@ -801,6 +1143,7 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   char* w = static_cast<char*>(ws);
   int* ER = reinterpret_cast<int*>(w + L.off_ER);
   int* EG = reinterpret_cast<int*>(w + L.off_EG);
+  double* EGf = reinterpret_cast<double*>(w + L.off_EGf);
   auto* cmG = reinterpret_cast<unsigned long long*>(w + L.off_cmG);
   int8_t* sG = reinterpret_cast<int8_t*>(w + L.off_sG);
   double* mws = reinterpret_cast<double*>(w + L.off_mws);
@@ -817,6 +1160,11 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   P.ldy = ldy;
   P.rowscale = rowscale;
   P.upper = (flags & 1) && !metric_out;
+  static const int dbg = [] {
+    const char* e = getenv("PPCG_OZ_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  P.dbg = dbg;
   P.metric_ws = mws;
   if (metric_out) P.snap_stage = split ? L.kp1 / KB - 1 : P.nk - 1;
   bool any = metric_out != nullptr;
@@ -830,10 +1178,12 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
     any = any || Ys[b] != nullptr;
     P.ER[b] = ER + (int64_t)b * n;
     P.EG[b] = EG + (int64_t)b * N;
+    P.EGf[b] = EGf + (int64_t)b * ((N + 1) & ~1);  // 16-byte aligned per problem
     BK_COUNT();
     k_colmax<<<dim3((unsigned)((K + 63) / 64), (N + 255) / 256), 256, 0, st>>>(K, N, Gs[b], ldg, cmG + (int64_t)b * N);
     BK_COUNT();
-    k_exponents<<<(N + 255) / 256, 256, 0, st>>>(N, cmG + (int64_t)b * N, EG + (int64_t)b * N);
+    k_exponents<<<(N + 255) / 256, 256, 0, st>>>(N, cmG + (int64_t)b * N, EG + (int64_t)b * N,
+                                                 EGf + (int64_t)b * ((N + 1) & ~1));
     int8_t* g = sG + (int64_t)b * S * N * L.kp;
     const int64_t sstr = (int64_t)N * L.kp;
     cudaMemsetAsync(g, 0, (size_t)S * N * L.kp, st);
@@ -854,7 +1204,7 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   }
   if (!any) return BK_OK;
   for (int b = nprob; b < 4; ++b) mB[b] = mB[0];
-  cudaFuncSetAttribute(k_oz_mma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(k_oz_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, TS_SMEM);
   const int ctn = (N + BN - 1) / BN;
   int64_t metric_ctas = 0;
   for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
@@ -870,11 +1220,13 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
     P.nrows = rows;
     P.r_base = r0;
     P.metric_ws = mws + metric_ctas;
-    const dim3 grid(ctn, (unsigned)((rows + BM - 1) / BM), nprob);
+    const int rtn = (int)((rows + BM - 1) / BM);
+    const int64_t tiles = (int64_t)ctn * rtn * nprob;
+    const int grid = (int)lmin(tiles, kSMs);
     BK_COUNT();
-    k_oz_mma<1><<<grid, THREADS, SMEM, st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P);
+    k_oz_ts<<<grid, TS_THREADS, TS_SMEM, st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P, ctn, rtn, nprob);
     BK_CHECK_LAUNCH();
-    metric_ctas += (int64_t)grid.x * grid.y;
+    metric_ctas += grid;
   }
   if (metric_out) {
     BK_COUNT();
