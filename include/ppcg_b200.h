@@ -204,6 +204,11 @@ int bk_fp64_emu_enabled(void);
 int64_t bk_ozaki_gram_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric);
 int bk_ozaki_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                     double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream);
+/* C1 = X^T Y1, C2 = X^T Y2 with X's digits computed once (the W / P projections) */
+int64_t bk_ozaki_gram2_ws_bytes(int64_t n, int m1, int m2a, int m2b);
+int bk_ozaki_gram2_d(int64_t n, int m1, const double* X, int64_t ldx, int m2a, const double* Ya, int64_t ldya,
+                     double* Ca, int64_t ldca, int m2b, const double* Yb, int64_t ldyb, double* Cb, int64_t ldcb,
+                     void* ws, int64_t ws_bytes, void* stream);
 /* K <= 16320; flags bit0: G upper triangular (k stages below a column tile are skipped) */
 int64_t bk_ozaki_tsgemm_ws_bytes(int nprob, int64_t n, int K, int N, int ksplit);
 int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alpha, const double* const* Xs, int64_t ldx,

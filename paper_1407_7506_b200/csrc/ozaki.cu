@@ -27,6 +27,7 @@
 // Replaces the FP64 products of block_inner (core.py:43-49) and the tall updates
 // (ppcg.py:443-445, 630, 758; core.py:99; ppcg.py:574-577).
 #include <cuda.h>
+#include <cstdio>
 #include "common.cuh"
 
 namespace bk {
@@ -287,6 +288,7 @@ struct GramEpi {
   const int* EA;
   const int* EB;
   double* part;       // [chunk][tile][128][64]
+  int dbg;            // experiments (PPCG_OZ_DBG): 1 = no MMAs, 4 = no TMA
 };
 
 struct TsEpi {
@@ -414,6 +416,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = kb % STAGES;
         mbar_wait(empty + st, ((kb / STAGES) & 1) ^ 1);
         uint8_t* sa = sm + st * STAGE_BYTES;
+        if (P.dbg & 4) {
+          mbar_arrive(full + st);
+          continue;
+        }
         mbar_arrive_expect_tx(full + st, STAGE_BYTES);
         const int kc = kc0 + kb * KB;
         tma3d(sa, mA, kc, rowA, 0, full + st);
@@ -430,6 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t sb = sa + A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < KB / 32; ++ks) {
+          if (P.dbg & 1) break;
 #pragma unroll
           for (int i = 0; i < S; ++i) {
 #pragma unroll
@@ -571,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // (digit groups combined in fp64), releases TMEM to the MMA warp, and only then scales, reads Z
 // and writes Y -- the stores of tile i overlap the MMAs of tile i + 1.  Metric tiles (problem 0,
 // columns < nsplit) pause the MMA warp after the snapshot stage until the epilogue has read it.
-__global__ void __launch_bounds__(TS_THREADS, 1)
+__global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-partition -> <= 168 registers
     k_oz_ts(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
             const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
             const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
@@ -723,6 +730,12 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       const double* Z = P.Z[t.prob];
       double* Y = P.Y[t.prob];
       const int ncol = min(32, P.N - (t.rowB + c0));  // valid columns of this warp's half (may be <= 0)
+      if (live && ncol > 0 && Z != nullptr && P.beta != 0.0) {
+        // this row's Z segment (32 doubles) into L2 while the tile's MMAs run (metric and stores)
+        const double* zr = Z + grow * P.ldz + t.rowB + c0;
+        prefetch_l2(zr);
+        prefetch_l2(zr + 16);
+      }
       if (t.snap >= 0) {
         mbar_wait(snap_full, si & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -731,12 +744,17 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           if (t.rowB + c0 + cc < P.nsplit && cc < ncol) {
             double acc[16];
             combine16_i64(tl, c0 + cc, acc);
+            double z[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int gc = t.rowB + c0 + cc + e;
-              if (live && gc < P.nsplit && gc < P.N) {
-                double v = P.alpha * scaled(acc[e], er, EG[gc]);
-                if (P.beta != 0.0) v = fma(P.beta, Z[grow * P.ldz + gc], v);
+              z[e] = (live && P.beta != 0.0 && e + cc < ncol) ? Z[grow * P.ldz + gc] : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int gc = t.rowB + c0 + cc + e;
+              if (live && gc < P.nsplit && e + cc < ncol) {
+                const double v = fma(P.beta, z[e], P.alpha * scaled(acc[e], er, EG[gc]));
                 ss = fma(v, v, ss);
               }
             }
@@ -745,12 +763,6 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(snap_free);
         ++si;
-      }
-      // this row's Z segment (32 doubles) into L2 while the tile's MMAs run
-      if (live && ncol > 0 && Z != nullptr && P.beta != 0.0 && Y != nullptr) {
-        const double* zr = Z + grow * P.ldz + t.rowB + c0;
-        prefetch_l2(zr);
-        prefetch_l2(zr + 16);
       }
       mbar_wait(done, ti & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -957,42 +969,131 @@ static int64_t gram_chunk_rows(int64_t n, int ntiles) {
 }
 
 struct GramLayout {
-  int ntiles;
-  int64_t chunk_rows, sc_rows;  // rows per chunk, rows per super-chunk (slices held at once)
-  int64_t off_cmA, off_cmB, off_EA, off_EB, off_part, off_sA, off_sB, total;
+  int nq;                      // B operands sharing the A digits (1 or 2)
+  int ntiles[2];
+  int64_t chunk_rows, sc_rows;  // rows per chunk, rows per super-chunk (digits held at once)
+  int64_t off_cmA, off_EA, off_sA, off_cmB[2], off_EB[2], off_part[2], off_sB[2], total;
 };
 
-static GramLayout gram_layout(int64_t n, int m1, int m2, int same, int sym, int64_t ws_cap) {
+// same: B operand q is A itself (one set of digits); sym (requires same): upper tiles only
+static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const int* same, int sym, int64_t ws_cap) {
   GramLayout L{};
-  L.ntiles = n_tiles(m1, m2, sym);
-  L.chunk_rows = gram_chunk_rows(n, L.ntiles);
-  const int64_t per_row = (int64_t)S * (m1 + (same ? 0 : m2));
-  // slices of at most ~1.5 GB at once (or what the caller's workspace holds)
+  L.nq = nq;
+  int tt = 0;
+  for (int q = 0; q < nq; ++q) tt += L.ntiles[q] = n_tiles(m1, m2[q], sym);
+  L.chunk_rows = gram_chunk_rows(n, tt);
+  int64_t per_row = (int64_t)S * m1;
+  for (int q = 0; q < nq; ++q) per_row += same[q] ? 0 : (int64_t)S * m2[q];
+  // digits of at most ~1.5 GB at once (or what the caller's workspace holds)
   int64_t sc_chunks = (n + L.chunk_rows - 1) / L.chunk_rows;
   const int64_t cap = ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
-  auto size_for = [&](int64_t chunks) {
+  auto layout = [&](int64_t chunks) {
     const int64_t rows = chunks * L.chunk_rows;
     int64_t o = 0;
-    o += align_up(8 * (int64_t)m1, 256);
-    o += align_up(8 * (int64_t)m2, 256);
-    o += align_up(4 * (int64_t)m1, 256);
-    o += align_up(4 * (int64_t)m2, 256);
-    o += align_up(chunks * L.ntiles * (int64_t)BM * BN * 8, 1024);
-    o += align_up(per_row * rows, 1024) + 1024;
+    L.off_cmA = o; o += align_up(8 * (int64_t)m1, 256);
+    L.off_EA = o;  o += align_up(4 * (int64_t)m1, 256);
+    for (int q = 0; q < nq; ++q) {
+      L.off_cmB[q] = o; o += align_up(8 * (int64_t)m2[q], 256);
+      L.off_EB[q] = o;  o += align_up(4 * (int64_t)m2[q], 256);
+      L.off_part[q] = o; o += align_up(chunks * L.ntiles[q] * (int64_t)BM * BN * 8, 1024);
+    }
+    L.off_sA = o; o += align_up((int64_t)S * m1 * rows, 1024);
+    for (int q = 0; q < nq; ++q) {
+      L.off_sB[q] = o;
+      o += same[q] ? 0 : align_up((int64_t)S * m2[q] * rows, 1024);
+    }
     return o;
   };
-  while (sc_chunks > 1 && size_for(sc_chunks) > cap) sc_chunks = (sc_chunks + 1) / 2;
+  while (sc_chunks > 1 && layout(sc_chunks) > cap) sc_chunks = (sc_chunks + 1) / 2;
   L.sc_rows = sc_chunks * L.chunk_rows;
-  int64_t o = 0;
-  L.off_cmA = o; o += align_up(8 * (int64_t)m1, 256);
-  L.off_cmB = o; o += align_up(8 * (int64_t)m2, 256);
-  L.off_EA = o;  o += align_up(4 * (int64_t)m1, 256);
-  L.off_EB = o;  o += align_up(4 * (int64_t)m2, 256);
-  L.off_part = o; o += align_up(sc_chunks * L.ntiles * (int64_t)BM * BN * 8, 1024);
-  L.off_sA = o;  o += align_up((int64_t)S * m1 * L.sc_rows, 1024);
-  L.off_sB = o;  o += same ? 0 : align_up((int64_t)S * m2 * L.sc_rows, 1024);
-  L.total = o;
+  L.total = layout(sc_chunks);
+  (void)per_row;
   return L;
+}
+
+// C_q = X^T Y_q for nq <= 2 operands Y_q that share X's digits
+static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int nq, const int* m2,
+                            const double* const* Y, const int64_t* ldy, double* const* C, const int64_t* ldc,
+                            int symmetric, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if (n <= 0 || m1 <= 0 || !X) return BK_ERR_ARG;
+  int same[2] = {0, 0};
+  for (int q = 0; q < nq; ++q) {
+    if (m2[q] <= 0 || !Y[q] || !C[q]) return BK_ERR_ARG;
+    same[q] = (X == Y[q] && ldx == ldy[q] && m1 == m2[q]) ? 1 : 0;
+    if (symmetric && !same[q]) return BK_ERR_ARG;
+  }
+  const GramLayout L = gram_layout(n, m1, nq, m2, same, symmetric, ws_bytes);
+  if (!ws || ws_bytes < L.total) return BK_ERR_ARG;
+  char* w = static_cast<char*>(ws);
+  auto* cmA = reinterpret_cast<unsigned long long*>(w + L.off_cmA);
+  int* EA = reinterpret_cast<int*>(w + L.off_EA);
+  int8_t* sA = reinterpret_cast<int8_t*>(w + L.off_sA);
+  int* EB[2];
+  int8_t* sB[2];
+  // exponents over all rows
+  cudaMemsetAsync(cmA, 0, 8 * (size_t)m1, st);
+  BK_COUNT();
+  k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
+  BK_COUNT();
+  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA, nullptr);
+  for (int q = 0; q < nq; ++q) {
+    EB[q] = same[q] ? EA : reinterpret_cast<int*>(w + L.off_EB[q]);
+    sB[q] = same[q] ? sA : reinterpret_cast<int8_t*>(w + L.off_sB[q]);
+    if (same[q]) continue;
+    auto* cmB = reinterpret_cast<unsigned long long*>(w + L.off_cmB[q]);
+    cudaMemsetAsync(cmB, 0, 8 * (size_t)m2[q], st);
+    BK_COUNT();
+    k_colmax<<<dim3((unsigned)((n + 63) / 64), (m2[q] + 255) / 256), 256, 0, st>>>(n, m2[q], Y[q], ldy[q], cmB);
+    BK_COUNT();
+    k_exponents<<<(m2[q] + 255) / 256, 256, 0, st>>>(m2[q], cmB, EB[q], nullptr);
+  }
+  cudaFuncSetAttribute(k_oz_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  static const int dbg = [] {
+    const char* e = getenv("PPCG_OZ_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  GramEpi P[2];
+  for (int q = 0; q < nq; ++q) {
+    P[q] = GramEpi{};
+    P[q].m1 = m1;
+    P[q].m2 = m2[q];
+    P[q].ta = (m1 + BM - 1) / BM;
+    P[q].tb = (m2[q] + BN - 1) / BN;
+    P[q].sym = symmetric ? 1 : 0;
+    P[q].chunk_rows = L.chunk_rows;
+    P[q].EA = EA;
+    P[q].EB = EB[q];
+    P[q].part = reinterpret_cast<double*>(w + L.off_part[q]);
+    P[q].dbg = dbg;
+  }
+  for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
+    const int64_t rows = lmin(L.sc_rows, n - r0);
+    const int64_t kld = align_up(rows, KPAD);
+    const unsigned gx = (unsigned)((rows + 127) / 128);
+    BK_COUNT();
+    k_slice_cols<<<dim3(gx, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
+                                                           kld * (int64_t)m1, kld);
+    CUtensorMap mA;
+    if (!encode_digits(&mA, sA, kld, rows, m1, BM, kld * (int64_t)m1)) return BK_ERR_UNSUPPORTED;
+    const int nch = (int)((rows + L.chunk_rows - 1) / L.chunk_rows);
+    for (int q = 0; q < nq; ++q) {
+      if (!same[q]) {
+        BK_COUNT();
+        k_slice_cols<<<dim3(gx, (m2[q] + 31) / 32), 256, 0, st>>>(r0 + rows, m2[q], Y[q], ldy[q], EB[q], r0, sB[q],
+                                                                 kld, kld * (int64_t)m2[q], kld);
+      }
+      CUtensorMap mB;
+      if (!encode_digits(&mB, sB[q], kld, rows, m2[q], BN, kld * (int64_t)m2[q])) return BK_ERR_UNSUPPORTED;
+      P[q].nrows = rows;
+      BK_COUNT();
+      k_oz_mma<0><<<dim3(L.ntiles[q], nch), THREADS, SMEM, st>>>(mA, mA, mA, mA, mB, mB, mB, mB, P[q]);
+      BK_CHECK_LAUNCH();
+      BK_COUNT();
+      k_gram_reduce<<<dim3(L.ntiles[q], 16), 512, 0, st>>>(P[q], nch, C[q], ldc[q], r0 > 0 ? 1 : 0);
+    }
+  }
+  BK_CHECK_LAUNCH();
+  return BK_OK;
 }
 
 }  // namespace oz
@@ -1016,77 +1117,37 @@ extern "C" int bk_fp64_emu_enabled(void) {
 
 extern "C" int64_t bk_ozaki_gram_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric) {
   if (n <= 0 || m1 <= 0 || m2 <= 0) return 0;
-  return gram_layout(n, m1, m2, same, symmetric, 0).total;
+  const int m2s[1] = {m2}, sm[1] = {same};
+  return gram_layout(n, m1, 1, m2s, sm, symmetric, 0).total;
 }
 
-// C = X^T Y (m1 x m2) with the Ozaki scheme; same = X and Y are the same block (one slicing);
-// symmetric (requires same): upper tiles computed, mirrored.
+// C = X^T Y (m1 x m2) with the Ozaki scheme; X and Y the same block -> one set of digits;
+// symmetric (requires that): upper tiles computed, mirrored.
 extern "C" int bk_ozaki_gram_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                                double* C, int64_t ldc, int symmetric, void* ws, int64_t ws_bytes, void* stream) {
-  if (n <= 0 || m1 <= 0 || m2 <= 0 || !X || !Y || !C) return BK_ERR_ARG;
-  const int same = (X == Y && ldx == ldy && m1 == m2) ? 1 : 0;
-  if (symmetric && !same) return BK_ERR_ARG;
-  const GramLayout L = gram_layout(n, m1, m2, same, symmetric, ws_bytes);
-  if (!ws || ws_bytes < L.total) return BK_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  char* w = static_cast<char*>(ws);
-  auto* cmA = reinterpret_cast<unsigned long long*>(w + L.off_cmA);
-  auto* cmB = reinterpret_cast<unsigned long long*>(w + L.off_cmB);
-  int* EA = reinterpret_cast<int*>(w + L.off_EA);
-  int* EB = same ? EA : reinterpret_cast<int*>(w + L.off_EB);
-  double* part = reinterpret_cast<double*>(w + L.off_part);
-  int8_t* sA = reinterpret_cast<int8_t*>(w + L.off_sA);
-  int8_t* sB = same ? sA : reinterpret_cast<int8_t*>(w + L.off_sB);
-  // exponents over all rows
-  cudaMemsetAsync(cmA, 0, 8 * (size_t)m1, st);
-  BK_COUNT();
-  k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
-  BK_COUNT();
-  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA, nullptr);
-  if (!same) {
-    cudaMemsetAsync(cmB, 0, 8 * (size_t)m2, st);
-    BK_COUNT();
-    k_colmax<<<dim3((unsigned)((n + 63) / 64), (m2 + 255) / 256), 256, 0, st>>>(n, m2, Y, ldy, cmB);
-    BK_COUNT();
-    k_exponents<<<(m2 + 255) / 256, 256, 0, st>>>(m2, cmB, EB, nullptr);
-  }
-  cudaFuncSetAttribute(k_oz_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  GramEpi P{};
-  P.m1 = m1;
-  P.m2 = m2;
-  P.ta = (m1 + BM - 1) / BM;
-  P.tb = (m2 + BN - 1) / BN;
-  P.sym = symmetric ? 1 : 0;
-  P.chunk_rows = L.chunk_rows;
-  P.EA = EA;
-  P.EB = EB;
-  P.part = part;
-  for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
-    const int64_t rows = lmin(L.sc_rows, n - r0);
-    const int64_t kld = align_up(rows, KPAD);
-    const dim3 gs((unsigned)((rows + 127) / 128), 1);
-    BK_COUNT();
-    k_slice_cols<<<dim3(gs.x, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
-                                                             kld * (int64_t)m1, kld);
-    if (!same) {
-      BK_COUNT();
-      k_slice_cols<<<dim3(gs.x, (m2 + 31) / 32), 256, 0, st>>>(r0 + rows, m2, Y, ldy, EB, r0, sB, kld,
-                                                               kld * (int64_t)m2, kld);
-    }
-    CUtensorMap mA, mB;
-    if (!encode_digits(&mA, sA, kld, rows, m1, BM, kld * (int64_t)m1) ||
-        !encode_digits(&mB, sB, kld, rows, m2, BN, kld * (int64_t)m2))
-      return BK_ERR_UNSUPPORTED;
-    P.nrows = rows;
-    const int nch = (int)((rows + L.chunk_rows - 1) / L.chunk_rows);
-    BK_COUNT();
-    k_oz_mma<0><<<dim3(L.ntiles, nch), THREADS, SMEM, st>>>(mA, mA, mA, mA, mB, mB, mB, mB, P);
-    BK_CHECK_LAUNCH();
-    BK_COUNT();
-    k_gram_reduce<<<dim3(L.ntiles, 16), 512, 0, st>>>(P, nch, C, ldc, r0 > 0 ? 1 : 0);
-  }
-  BK_CHECK_LAUNCH();
-  return BK_OK;
+  const int m2s[1] = {m2};
+  const double* Ys[1] = {Y};
+  const int64_t lds[1] = {ldy}, ldcs[1] = {ldc};
+  double* Cs[1] = {C};
+  return ozaki_gram_multi(n, m1, X, ldx, 1, m2s, Ys, lds, Cs, ldcs, symmetric, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// C1 = X^T Y1, C2 = X^T Y2 (the projections of W and P against one basis, ppcg.py:680-687):
+// X is sliced once
+extern "C" int64_t bk_ozaki_gram2_ws_bytes(int64_t n, int m1, int m2a, int m2b) {
+  if (n <= 0 || m1 <= 0 || m2a <= 0 || m2b <= 0) return 0;
+  const int m2s[2] = {m2a, m2b}, sm[2] = {0, 0};
+  return gram_layout(n, m1, 2, m2s, sm, 0, 0).total;
+}
+
+extern "C" int bk_ozaki_gram2_d(int64_t n, int m1, const double* X, int64_t ldx, int m2a, const double* Ya,
+                                int64_t ldya, double* Ca, int64_t ldca, int m2b, const double* Yb, int64_t ldyb,
+                                double* Cb, int64_t ldcb, void* ws, int64_t ws_bytes, void* stream) {
+  const int m2s[2] = {m2a, m2b};
+  const double* Ys[2] = {Ya, Yb};
+  const int64_t lds[2] = {ldya, ldyb}, ldcs[2] = {ldca, ldcb};
+  double* Cs[2] = {Ca, Cb};
+  return ozaki_gram_multi(n, m1, X, ldx, 2, m2s, Ys, lds, Cs, ldcs, 0, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 // ---- tall GEMM: Y_b = s (.) (alpha X_b G_b + beta Z_b), b < nprob <= 4 (semantics of
@@ -1170,15 +1231,28 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   bool any = metric_out != nullptr;
   // G^T digits per problem: column exponents over the K rows of G; k layout split like X's
   CUtensorMap mA[4], mB[4];
+  // problems that share X (or G) share its digits: xa[b] / ga[b] = first problem with the same block
+  int xa[4], ga[4];
+  for (int b = 0; b < nprob; ++b) {
+    xa[b] = ga[b] = b;
+    for (int c = 0; c < b; ++c) {
+      if (xa[b] == b && Xs[c] == Xs[b]) xa[b] = c;
+      if (ga[b] == b && Gs[c] == Gs[b]) ga[b] = c;
+    }
+  }
   cudaMemsetAsync(cmG, 0, 8 * (size_t)nprob * N, st);
   for (int b = 0; b < nprob; ++b) {
     if (beta != 0.0 && (!Zs || !Zs[b])) return BK_ERR_ARG;
     P.Z[b] = Zs ? Zs[b] : nullptr;
     P.Y[b] = Ys[b];
     any = any || Ys[b] != nullptr;
-    P.ER[b] = ER + (int64_t)b * n;
-    P.EG[b] = EG + (int64_t)b * N;
-    P.EGf[b] = EGf + (int64_t)b * ((N + 1) & ~1);  // 16-byte aligned per problem
+    P.ER[b] = ER + (int64_t)xa[b] * n;
+    P.EG[b] = EG + (int64_t)ga[b] * N;
+    P.EGf[b] = EGf + (int64_t)ga[b] * ((N + 1) & ~1);  // 16-byte aligned per problem
+    if (ga[b] != b) {
+      mB[b] = mB[ga[b]];
+      continue;
+    }
     BK_COUNT();
     k_colmax<<<dim3((unsigned)((K + 63) / 64), (N + 255) / 256), 256, 0, st>>>(K, N, Gs[b], ldg, cmG + (int64_t)b * N);
     BK_COUNT();
@@ -1210,6 +1284,10 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
     const int64_t rows = lmin(L.sc_rows, n - r0);
     for (int b = 0; b < nprob; ++b) {
+      if (xa[b] != b) {
+        mA[b] = mA[xa[b]];
+        continue;
+      }
       int8_t* x = sX + (int64_t)b * S * L.sc_rows * L.kp;
       BK_COUNT();
       k_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(r0, rows, K, Xs[b], ldx, split ? ksplit : K, L.kp1,
@@ -1225,7 +1303,13 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
     const int grid = (int)lmin(tiles, kSMs);
     BK_COUNT();
     k_oz_ts<<<grid, TS_THREADS, TS_SMEM, st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P, ctn, rtn, nprob);
-    BK_CHECK_LAUNCH();
+    {
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        fprintf(stderr, "bk_ozaki_tsgemm_d: launch failed: %s\n", cudaGetErrorString(e));
+        return BK_ERR_CUDA;
+      }
+    }
     metric_ctas += grid;
   }
   if (metric_out) {

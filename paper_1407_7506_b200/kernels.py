@@ -188,7 +188,19 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
 
 
 def gram2(x1, y1, out1, x2, y2, out2):
-    """Two independent Grams in one launch (real only; complex falls back to two launches)."""
+    """Two independent Grams in one launch (real only; complex falls back to two launches).
+    Emulated: X^T Y1 and X^T Y2 of one basis X share its digits."""
+    n = x1.shape[0]
+    if (x1.dtype == F64 and x1.data_ptr() == x2.data_ptr() and x1.shape == x2.shape and x1.stride() == x2.stride()
+            and _emu(n, x1.shape[1], min(y1.shape[1], y2.shape[1]))):
+        lib = _lib.load()
+        px, _, _, lx = real_view(x1)
+        pa, _, _, la = real_view(y1)
+        pb, _, _, lb = real_view(y2)
+        wp, wb = workspace("gram/oz").get(lib.bk_ozaki_gram2_ws_bytes(n, x1.shape[1], y1.shape[1], y2.shape[1]))
+        _lib.call("bk_ozaki_gram2_d", n, x1.shape[1], px, lx, y1.shape[1], pa, la, out1.data_ptr(), ld_of(out1),
+                  y2.shape[1], pb, lb, out2.data_ptr(), ld_of(out2), wp, wb, stream_ptr())
+        return
     if x1.dtype != F64 or _emu(x1.shape[0], min(x1.shape[1], x2.shape[1]), min(y1.shape[1], y2.shape[1])):
         gram(x1, y1, out1)
         gram(x2, y2, out2)

@@ -209,3 +209,32 @@ def test_ozaki_tsgemm_nonfinite_row(cuda):
     ok[9] = False
     ok[:, 7] = False
     assert np.all(np.isfinite(yn[ok]))
+
+
+def test_ozaki_gram2_shares_x_and_batched_tsgemm_shares_digits(cuda):
+    """gram2 with one basis (X sliced once) agrees with two single Grams to the DGEMM-class bound
+    (its split-K chunking follows both products' tile counts, so the chunk sums round
+    differently); a batched tall GEMM whose problems repeat X / G (the projection update
+    [X, X, AX] x [G1, G3, G3]) equals the unbatched products bitwise."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m = 30000, 150
+    x, w, p = (dev(gauss(n, m, 80 + i), torch) for i in range(3))
+    with emu(torch):
+        a1 = torch.empty((m, m), dtype=torch.float64, device="cuda")
+        a2 = torch.empty_like(a1)
+        K.gram2(x, w, a1, x, p, a2)
+        b1, b2 = K.gram(x, w), K.gram(x, p)
+        xa = x.abs()
+        for a, b, y in [(a1, b1, w), (a2, b2, p)]:
+            bound = 8 * U * (xa.T @ y.abs())
+            assert bool(((a - b).abs() <= bound).all())
+        ax = dev(gauss(n, m, 90), torch)
+        g1, g3 = dev(gauss(m, m, 91), torch), dev(gauss(m, m, 92), torch)
+        ys = [torch.zeros((n, m), dtype=torch.float64, device="cuda") for _ in range(3)]
+        K.tsgemm([x, x, ax], [g1, g3, g3], ys, alpha=-1.0, beta=0.0)
+        for y, (xx, gg) in zip(ys, [(x, g1), (x, g3), (ax, g3)]):
+            r = torch.zeros_like(y)
+            K.tsgemm([xx], [gg], [r], alpha=-1.0, beta=0.0)
+            assert torch.equal(y, r)
