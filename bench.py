@@ -49,6 +49,10 @@ def hbm_peak():
 
 
 NCU_SOURCE = "profiles/ncu_summary.json (ncu --set full capture of the same kernels on the live config-2 state)"
+NCU_OZ_SOURCE = ("profiles/ncu_ozaki_r02.json (ncu --set full --clock-control none of the emulated products on "
+                 "config-2 shapes, tools/oz_one.py)")
+# digit products per FP64 multiply-add in the emulation (csrc/ozaki.cu: 8 digits, pairs i + j <= 7)
+OZ_PRODUCTS = 36
 
 
 def ncu_traffic(kernel):
@@ -59,6 +63,26 @@ def ncu_traffic(kernel):
         return d["kernels"][kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
+
+
+def ncu_oz(kernel, key="dram_bytes_per_launch"):
+    """A per-launch figure of an emulated-FP64 kernel from profiles/ncu_ozaki_r02.json."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_ozaki_r02.json")))
+        return d["kernels"][kernel][0][key]
+    except Exception:
+        return None
+
+
+def int8_peak():
+    """Dense int8 tensor rate: twice the bf16 rate on the tcgen05 datapath (B200: 4.5 POPS vs
+    2.25 PFLOP/s nominal), applied to the MEASURED bf16 peak (burst: these kernels are timed
+    alone) -- MEASURED_PEAKS.json has no int8 entry."""
+    try:
+        bf = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        return 2.0 * bf, "2 x measured bf16 dense (MEASURED_PEAKS.json bf16_tflops, burst)"
+    except Exception:
+        return 4500.0, "fallback: nominal int8 dense 4.5 POPS (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -206,7 +230,7 @@ def kernel_rooflines(torch, s):
         base, _ = s._ext_of(w)
         win = base[:, L:L + ka]
     G = s.Gm[:ka, :ka]
-    out = {}
+    out = {"emulated": bool(K._emu(n, ka, ka))}
     ms = event_time(torch, lambda: K.gram(x, ax, G), 10)
     out["gram"] = {"ms": ms, "tflops": 2.0 * n * ka * ka / ms / 1e9, "flops_per_launch": 2.0 * n * ka * ka}
     tmp = torch.empty_like(s.W)[:, L:]
@@ -363,13 +387,34 @@ def run_ours(args):
         peak, peak_src = fp64_peak()
         hbm, hbm_src = hbm_peak()
         tg = kr["tsgemm"]
-        roofline = {"bound": "tensor", "kernel": "tsgemm_kernel (W = T(AX - X G), DMMA m8n8k4; largest launch share)",
-                    "achieved": tg["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": tg["tflops"] / peak,
-                    "traffic": ncu_traffic("tsgemm_kernel"), "traffic_source": NCU_SOURCE,
-                    "peak_source": peak_src, "algorithmic_flops_per_launch": tg["flops_per_launch"]}
-        kernels = {name: dict(v) for name, v in kr.items()}
+        if kr.get("emulated"):
+            # the FP64 products run on the int8 tensor cores (csrc/ozaki.cu): the roofline of the
+            # dominant launch (the tall GEMM, digit slicing included in the timed call) is int8
+            # tensor throughput; the FP64-equivalent rate is reported beside it
+            i8, i8_src = int8_peak()
+            tops = OZ_PRODUCTS * tg["flops_per_launch"] / tg["ms"] / 1e9
+            roofline = {"bound": "tensor",
+                        "kernel": "k_oz_ts (W = T(AX - X G): 8-digit Ozaki scheme on tcgen05 kind::i8, 36 digit "
+                                  "products per FP64 multiply-add; timed call incl. digit slicing; largest launch share)",
+                        "achieved": tops, "peak": i8, "unit": "TOPS (int8)", "frac": tops / i8,
+                        "traffic": ncu_oz("k_oz_ts"), "traffic_source": NCU_OZ_SOURCE, "peak_source": i8_src,
+                        "algorithmic_ops_per_launch": OZ_PRODUCTS * tg["flops_per_launch"],
+                        "fp64_equivalent_tflops": tg["tflops"], "fp64_equivalent_frac_of_dgemm": tg["tflops"] / peak,
+                        "fp64_peak_source": peak_src}
+        else:
+            roofline = {"bound": "tensor",
+                        "kernel": "tsgemm_kernel (W = T(AX - X G), DMMA m8n8k4; largest launch share)",
+                        "achieved": tg["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": tg["tflops"] / peak,
+                        "traffic": ncu_traffic("tsgemm_kernel"), "traffic_source": NCU_SOURCE,
+                        "peak_source": peak_src, "algorithmic_flops_per_launch": tg["flops_per_launch"]}
+        kernels = {name: dict(v) if isinstance(v, dict) else v for name, v in kr.items()}
         kernels["gram"]["frac_of_fp64"] = kr["gram"]["tflops"] / peak
-        kernels["gram"]["traffic"] = ncu_traffic("gram_kernel")
+        kernels["gram"]["traffic"] = ncu_oz("k_oz_mma<0>") if kr.get("emulated") else ncu_traffic("gram_kernel")
+        if kr.get("emulated"):
+            i8, _ = int8_peak()
+            for nm in ("gram", "tsgemm"):
+                kernels[nm]["int8_tops"] = OZ_PRODUCTS * kr[nm]["flops_per_launch"] / kr[nm]["ms"] / 1e9
+                kernels[nm]["frac_of_int8"] = kernels[nm]["int8_tops"] / i8
         kernels["spmm"]["frac_of_hbm"] = kr["spmm"]["gbs"] / hbm
         kernels["tsgemm"]["frac_of_fp64"] = kr["tsgemm"]["tflops"] / peak
         kernels["subblock_grams"]["frac_of_fp64"] = kr["subblock_grams"]["tflops"] / peak

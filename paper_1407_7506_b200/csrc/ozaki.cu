@@ -100,13 +100,14 @@ BK_DEV void combine16(uint32_t tmem_lane, int cc, double (&acc)[16]) {
 // Same as combine16 but exact in integers first: H = sum_{t<4} acc_t 2^(8(3-t)), L likewise for
 // t >= 4 (|H|, |L| < 2^56 fit int64), result = 2^-36 (H + 2^-32 L): two int64 -> fp64
 // conversions per column instead of eight.  Caller applies the 2^-36 (folded into the exponent).
+template <int GS = BN>  // TMEM columns between digit groups
 BK_DEV void combine16_i64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
   static_assert(S == 8, "two halves of four digit groups");
   long long h[16];
   {
     uint32_t v[4][16];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + t * BN + cc, v[t]);
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + t * GS + cc, v[t]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -119,7 +120,7 @@ BK_DEV void combine16_i64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
   {
     uint32_t v[4][16];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * BN + cc, v[t]);
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * GS + cc, v[t]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -574,26 +575,35 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 // Tall GEMM, persistent: one CTA per SM walks the tiles tau = blockIdx.x + i * gridDim.x (column
 // tiles fastest, so the column tiles of a row block run side by side and share its X digits in
-// L2).  The producer runs ahead across tile boundaries; the epilogue drains TMEM into registers
-// (digit groups combined in fp64), releases TMEM to the MMA warp, and only then scales, reads Z
-// and writes Y -- the stores of tile i overlap the MMAs of tile i + 1.  Metric tiles (problem 0,
-// columns < nsplit) pause the MMA warp after the snapshot stage until the epilogue has read it.
+// L2).  Tiles are 128 rows x TBN columns; with TBN = 32 the 8 digit groups take 256 TMEM columns
+// and two accumulators alternate: the MMA warp fills one while the epilogue drains the other.
+// The producer runs ahead across tile boundaries; the epilogue drains TMEM into registers
+// (digit groups combined exactly in int64, then fp64), releases the accumulator, and only then
+// scales, reads Z and writes Y through a swizzled shared staging tile (whole-line traffic).
+// Metric tiles (problem 0, columns < nsplit) pause the MMA warp after the snapshot stage until
+// the epilogue has read the snapshot.
+template <int TBN>
 __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-partition -> <= 168 registers
     k_oz_ts(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
             const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
             const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
             const __grid_constant__ CUtensorMap mapB2, const __grid_constant__ CUtensorMap mapB3, const TsEpi P,
             int ctn, int rtn, int nprob) {
+  constexpr int NACC = TBN == 32 ? 2 : 1;               // TMEM accumulators (S * TBN columns each)
+  constexpr int B_BYTES_T = S * TBN * KB;
+  constexpr int STAGE_T = A_BYTES + B_BYTES_T;
+  constexpr int CPW = TBN / 2;                          // columns per epilogue warp (2 column halves)
+  constexpr int NJ = 256 / TBN;                          // digit blocks of B per MMA (N <= 256)
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_T);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint64_t* tmem_free = done + 1;
-  uint64_t* snap_full = done + 2;
-  uint64_t* snap_free = done + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 4);
-  double* stage_out = reinterpret_cast<double*>(sm + STAGES * STAGE_BYTES + 256);
+  uint64_t* done = empty + STAGES;     // [NACC]
+  uint64_t* tmem_free = done + 2;      // [NACC]
+  uint64_t* snap_full = done + 4;
+  uint64_t* snap_free = done + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 6);
+  double* stage_out = reinterpret_cast<double*>(sm + STAGES * STAGE_T + 256);
   __shared__ double s_red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = ctn * rtn * nprob;
@@ -606,9 +616,9 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
     t.prob = tau / (ctn * rtn);
     const int r = tau - t.prob * ctn * rtn;
     t.rowA = (r / ctn) * BM;
-    t.rowB = (r % ctn) * BN;
+    t.rowB = (r % ctn) * TBN;
     t.nk = P.nk;
-    if (P.upper) t.nk = min(t.nk, (t.rowB + BN + KB - 1) / KB);
+    if (P.upper) t.nk = min(t.nk, (t.rowB + TBN + KB - 1) / KB);
     t.snap = (t.prob == 0 && P.snap_stage >= 0 && t.rowB < P.nsplit) ? P.snap_stage : -1;
     return t;
   };
@@ -620,8 +630,10 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
       mbar_init(full + i, 1);
       mbar_init(empty + i, 1);
     }
-    mbar_init(done, 1);
-    mbar_init(tmem_free, 256);
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(done + i, 1);
+      mbar_init(tmem_free + i, 256);
+    }
     mbar_init(snap_full, 1);
     mbar_init(snap_free, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -650,12 +662,12 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
         for (int kb = 0; kb < t.nk; ++kb, ++it) {
           const int st = it % STAGES;
           mbar_wait(empty + st, ((it / STAGES) & 1) ^ 1);
-          uint8_t* sa = sm + st * STAGE_BYTES;
+          uint8_t* sa = sm + st * STAGE_T;
           if (P.dbg & 4) {
             mbar_arrive(full + st);
             continue;
           }
-          mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+          mbar_arrive_expect_tx(full + st, STAGE_T);
           tma3d(sa, mA, kb * KB, t.rowA, 0, full + st);
           tma3d(sa + A_BYTES, mB, kb * KB, t.rowB, 0, full + st);
         }
@@ -665,14 +677,16 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
     int it = 0, ti = 0, si = 0;
     for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++ti) {
       const Tile t = tile_of(tau);
-      mbar_wait(tmem_free, (ti & 1) ^ 1);  // epilogue has drained the previous tile
+      const int ab = ti % NACC;                     // accumulator of this tile
+      const uint32_t acc_base = tmem + ab * S * TBN;
+      mbar_wait(tmem_free + ab, ((ti / NACC) & 1) ^ 1);  // epilogue has drained this accumulator
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int kb = 0; kb < t.nk; ++kb, ++it) {
         const int st = it % STAGES;
         mbar_wait(full + st, (it / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t sa = smem_u32(sm + st * STAGE_BYTES);
+          const uint32_t sa = smem_u32(sm + st * STAGE_T);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
           for (int ks = 0; ks < KB / 32; ++ks) {
@@ -680,15 +694,15 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
 #pragma unroll
             for (int i = 0; i < S; ++i) {
 #pragma unroll
-              for (int j0 = 0; j0 < S - i; j0 += 4) {
-                const int nj = (S - i - j0) < 4 ? (S - i - j0) : 4;
+              for (int j0 = 0; j0 < S - i; j0 += NJ) {
+                const int nj = (S - i - j0) < NJ ? (S - i - j0) : NJ;
                 const uint64_t da = umma_desc(sa + i * BM * KB + ks * 32);
-                const uint64_t db = umma_desc(sb + j0 * BN * KB + ks * 32);
+                const uint64_t db = umma_desc(sb + j0 * TBN * KB + ks * 32);
                 const uint32_t accf = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (i + j0) * BN),
-                    "l"(da), "l"(db), "r"(idesc_i8(nj * BN)), "r"(accf));
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_base + (i + j0) * TBN),
+                    "l"(da), "l"(db), "r"(idesc_i8(nj * TBN)), "r"(accf));
               }
             }
           }
@@ -701,12 +715,14 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
                          : "memory");
           if (kb == t.nk - 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(done))
+                             smem_u32(done + ab))
                          : "memory");
         }
         __syncwarp();
         if (kb == t.snap) {
-          if (kb != t.nk - 1) mbar_wait(snap_free, si & 1);  // epilogue has read the snapshot
+          // epilogue has read the snapshot -- also after a last-stage snapshot: with two
+          // accumulators the next tile's snapshot commit must not run a second phase ahead
+          mbar_wait(snap_free, si & 1);
           ++si;
         }
       }
@@ -715,35 +731,36 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
     // 8 epilogue warps: TMEM lane quadrant q = warp % 4 (hardware rule), column half h
     const int q = warp & 3, h = (warp - 2) >> 2;
     const int r = q * 32 + lane;
-    const int c0 = h * 32;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const int c0 = h * CPW;
     double ss = 0;  // metric partial (problem 0 tiles with columns < nsplit)
     int ti = 0, si = 0;
     for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++ti) {
       const Tile t = tile_of(tau);
+      const int ab = ti % NACC;
+      const uint32_t tl = tmem + ab * S * TBN + ((uint32_t)(q * 32) << 16);
       const int64_t lrow = t.rowA + r;
       const bool live = lrow < P.nrows;
       const int64_t grow = P.r_base + lrow;
       const int er0 = live ? P.ER[t.prob][grow] : 0;
-      const int er = er0 == NON_FINITE ? NON_FINITE : er0 - 36;  // combine16_i64 leaves 2^-36
+      const int er = er0 == NON_FINITE ? NON_FINITE : er0 - 36;  // combine leaves 2^-36
       const int* EG = P.EG[t.prob];
       const double* Z = P.Z[t.prob];
       double* Y = P.Y[t.prob];
-      const int ncol = min(32, P.N - (t.rowB + c0));  // valid columns of this warp's half (may be <= 0)
+      const int ncol = min(CPW, P.N - (t.rowB + c0));  // valid columns of this warp (may be <= 0)
       if (live && ncol > 0 && Z != nullptr && P.beta != 0.0) {
-        // this row's Z segment (32 doubles) into L2 while the tile's MMAs run (metric and stores)
+        // this row's Z segment into L2 while the tile's MMAs run (metric and stores)
         const double* zr = Z + grow * P.ldz + t.rowB + c0;
-        prefetch_l2(zr);
-        prefetch_l2(zr + 16);
+#pragma unroll
+        for (int c = 0; c < CPW; c += 16) prefetch_l2(zr + c);
       }
       if (t.snap >= 0) {
         mbar_wait(snap_full, si & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int cc = 0; cc < 32; cc += 16) {
+        for (int cc = 0; cc < CPW; cc += 16) {
           if (t.rowB + c0 + cc < P.nsplit && cc < ncol) {
             double acc[16];
-            combine16_i64(tl, c0 + cc, acc);
+            combine16_i64<TBN>(tl, c0 + cc, acc);
             double z[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -764,22 +781,22 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
         mbar_arrive(snap_free);
         ++si;
       }
-      mbar_wait(done, ti & 1);
+      mbar_wait(done + ab, (ti / NACC) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      double acc[32];
+      double acc[CPW];
 #pragma unroll
-      for (int cc = 0; cc < 32; cc += 16) {
+      for (int cc = 0; cc < CPW; cc += 16) {
         if (cc < ncol) {
           double a16[16];
-          combine16_i64(tl, c0 + cc, a16);
+          combine16_i64<TBN>(tl, c0 + cc, a16);
 #pragma unroll
           for (int e = 0; e < 16; ++e) acc[cc + e] = a16[e];
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(tmem_free);
+      mbar_arrive(tmem_free + ab);
       if (Y == nullptr || ncol <= 0 || (P.dbg & 2)) continue;
-      const bool vec = ncol == 32 && !(P.ldy & 1) && (P.beta == 0.0 || !(P.ldz & 1)) &&
+      const bool vec = ncol == CPW && !(P.ldy & 1) && (P.beta == 0.0 || !(P.ldz & 1)) &&
                        ((reinterpret_cast<uintptr_t>(Y + t.rowB + c0) & 15) == 0) &&
                        (P.beta == 0.0 || (reinterpret_cast<uintptr_t>(Z + t.rowB + c0) & 15) == 0);
       if (vec) {
@@ -792,7 +809,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
         const double fr = rfast ? P.alpha * __longlong_as_double((long long)(er + 1023) << 52) : 0.0;
         const double* EGf = P.EGf[t.prob];
 #pragma unroll
-        for (int cc = 0; cc < 32; cc += 16) {
+        for (int cc = 0; cc < CPW; cc += 16) {
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
             const int gc = t.rowB + c0 + cc + 2 * p;
@@ -832,7 +849,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
         const double sr = P.rowscale ? P.rowscale[grow] : 1.0;
         const int64_t zo = grow * P.ldz + t.rowB + c0, yo = grow * P.ldy + t.rowB + c0;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CPW; ++e) {
           if (e < ncol) {
             const int gc = t.rowB + c0 + e;
             double v = P.alpha * scaled(acc[e], er, EG[gc]);
@@ -856,6 +873,21 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+// 32-column tall-GEMM tiles with two TMEM accumulators (epilogue overlapped with the MMAs);
+// 64-column tiles (PPCG_OZ_TBN=64) read the X digits half as often but drain TMEM between tiles
+static int ts_tbn() {
+  static const int tbn = [] {
+    const char* e = getenv("PPCG_OZ_TBN");
+    return (e && atoi(e) == 64) ? 64 : 32;
+  }();
+  return tbn;
+}
+
+template <int TBN>
+constexpr int ts_smem() {
+  return STAGES * (A_BYTES + S * TBN * KB) + 1024 + 256 + TS_STAGE_OUT;
 }
 
 // C (+)= sum over chunks of the partials, fixed chunk order, compensated; symmetric: upper tiles
@@ -1274,12 +1306,16 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
       k_slice_cols<<<dim3((unsigned)((K - ksplit + 127) / 128), (N + 31) / 32), 256, 0, st>>>(
           K, N, Gs[b], ldg, EG + (int64_t)b * N, ksplit, g + L.kp1, L.kp, sstr, L.kp - L.kp1);
     }
-    if (!encode_digits(&mB[b], g, L.kp, L.kp, N, BN, sstr)) return BK_ERR_UNSUPPORTED;
+    if (!encode_digits(&mB[b], g, L.kp, L.kp, N, ts_tbn(), sstr)) return BK_ERR_UNSUPPORTED;
   }
   if (!any) return BK_OK;
   for (int b = nprob; b < 4; ++b) mB[b] = mB[0];
-  cudaFuncSetAttribute(k_oz_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, TS_SMEM);
-  const int ctn = (N + BN - 1) / BN;
+  const int tbn = ts_tbn();
+  if (tbn == 32)
+    cudaFuncSetAttribute(k_oz_ts<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem<32>());
+  else
+    cudaFuncSetAttribute(k_oz_ts<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem<64>());
+  const int ctn = (N + tbn - 1) / tbn;
   int64_t metric_ctas = 0;
   for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
     const int64_t rows = lmin(L.sc_rows, n - r0);
@@ -1302,7 +1338,12 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
     const int64_t tiles = (int64_t)ctn * rtn * nprob;
     const int grid = (int)lmin(tiles, kSMs);
     BK_COUNT();
-    k_oz_ts<<<grid, TS_THREADS, TS_SMEM, st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P, ctn, rtn, nprob);
+    if (tbn == 32)
+      k_oz_ts<32><<<grid, TS_THREADS, ts_smem<32>(), st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P,
+                                                          ctn, rtn, nprob);
+    else
+      k_oz_ts<64><<<grid, TS_THREADS, ts_smem<64>(), st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P,
+                                                          ctn, rtn, nprob);
     {
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {

@@ -238,3 +238,21 @@ def test_ozaki_gram2_shares_x_and_batched_tsgemm_shares_digits(cuda):
             r = torch.zeros_like(y)
             K.tsgemm([xx], [gg], [r], alpha=-1.0, beta=0.0)
             assert torch.equal(y, r)
+
+
+def test_ozaki_tsgemm_last_stage_snapshots_back_to_back(cuda):
+    """Metric launches whose snapshot is the last k stage (ksplit = K) on many consecutive
+    tiles: the MMA warp must not run a second snapshot phase ahead of the epilogue (a hang, not
+    a wrong number, if it does)."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, Kt, N = 60000, 96, 300
+    x, g, z = gauss(n, Kt, 100), gauss(Kt, N, 101), gauss(n, N, 102)
+    with emu(torch):
+        m = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [None], alpha=-1.0, beta=1.0, zs=[dev(z, torch)], metric=m,
+                 ksplit=Kt, nsplit=N)
+        torch.cuda.synchronize()
+    ref = np.sum((z - x @ g) ** 2)
+    assert abs(m.item() - ref) <= 1e-12 * ref
