@@ -299,6 +299,8 @@ struct TsEpi {
   int nk;             // k stages (kp / KB)
   int snap_stage;     // metric snapshot after this stage (-1: none)
   int upper;          // G upper triangular (no metric): skip k stages below the tile
+  int kp1, kv1, kv2;  // k layout: [0, kv1) valid, zeros to kp1, [kp1, kp1 + kv2) valid (32-deep steps
+                      // wholly in the zero padding are skipped)
   int nsplit;
   double alpha, beta;
   const int* ER[4];   // row exponents (indexed by global row)
@@ -691,6 +693,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
 #pragma unroll
           for (int ks = 0; ks < KB / 32; ++ks) {
             if (P.dbg & 1) break;
+            const int k0 = kb * KB + ks * 32;  // skip 32-deep steps that lie in the zero padding
+            if (ks > 0 && ((k0 >= P.kv1 && k0 < P.kp1) || k0 >= P.kp1 + P.kv2)) break;
 #pragma unroll
             for (int i = 0; i < S; ++i) {
 #pragma unroll
@@ -825,22 +829,30 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
             *reinterpret_cast<double2*>(wb + lane * 16 + ((p ^ (lane & 7)) * 2)) = make_double2(u0, u1);
           }
           __syncwarp();
+          // all eight Z pairs (and row scales) first: Y may alias Z, so the compiler would keep
+          // each load behind the previous store; every lane reads and writes only its own
+          // elements, so hoisting is safe and the load latencies overlap
+          const int p = lane & 7;
+          const int gc = t.rowB + c0 + cc + 2 * p;
+          double2 z[8];
+          double srr[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int rr = 4 * i + (lane >> 3), p = lane & 7;
+            const int rr = 4 * i + (lane >> 3);
+            const int64_t lr = t.rowA + q * 32 + rr;
+            const int64_t gr = P.r_base + (lr < P.nrows ? lr : 0);
+            z[i] = P.beta != 0.0 ? __ldcg(reinterpret_cast<const double2*>(Z + gr * P.ldz + gc)) : make_double2(0.0, 0.0);
+            srr[i] = P.rowscale ? __ldg(P.rowscale + gr) : 1.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3);
             const int64_t lr = t.rowA + q * 32 + rr;
             if (lr < P.nrows) {
               const int64_t gr = P.r_base + lr;
               const double2 u = *reinterpret_cast<const double2*>(wb + rr * 16 + ((p ^ (rr & 7)) * 2));
-              const int gc = t.rowB + c0 + cc + 2 * p;
-              double v0 = u.x, v1 = u.y;
-              if (P.beta != 0.0) {
-                const double2 z = *reinterpret_cast<const double2*>(Z + gr * P.ldz + gc);
-                v0 = fma(P.beta, z.x, v0);
-                v1 = fma(P.beta, z.y, v1);
-              }
-              const double srr = P.rowscale ? P.rowscale[gr] : 1.0;
-              *reinterpret_cast<double2*>(Y + gr * P.ldy + gc) = make_double2(srr * v0, srr * v1);
+              const double v0 = fma(P.beta, z[i].x, u.x), v1 = fma(P.beta, z[i].y, u.y);
+              *reinterpret_cast<double2*>(Y + gr * P.ldy + gc) = make_double2(srr[i] * v0, srr[i] * v1);
             }
           }
           __syncwarp();
@@ -1253,6 +1265,9 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   P.ldy = ldy;
   P.rowscale = rowscale;
   P.upper = (flags & 1) && !metric_out;
+  P.kp1 = L.kp1;
+  P.kv1 = split ? ksplit : K;
+  P.kv2 = split ? K - ksplit : 0;
   static const int dbg = [] {
     const char* e = getenv("PPCG_OZ_DBG");
     return e ? atoi(e) : 0;

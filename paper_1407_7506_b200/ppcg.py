@@ -1051,9 +1051,13 @@ def device_bytes_plan(n_loc, n_ext, kt, q, cplx, nnz_loc=0, size=1):
         r = 2 * kt if cplx else kt
         gram_ws = int(lib.bk_gram_ws_bytes(n_ext, r, r))
         sb_ws = int(lib.bk_subblock_grams_ws_bytes(n_ext, 2 * kt if cplx else kt, 2 * q if cplx else q, 1))
-    except Exception:  # library not built: the measured sizes at config 5 (~0.6 / 0.2 GB)
-        gram_ws, sb_ws = 6 << 27, 2 << 27
+        # emulated FP64 products (csrc/ozaki.cu): digits + split-K partials, capped per call
+        oz = int(lib.bk_ozaki_gram_ws_bytes(n_ext, r, r, 0, 0)) + int(lib.bk_ozaki_tsgemm_ws_bytes(4, n_loc, r, r, r))
+    except Exception:  # library not built: the measured sizes at config 5 (~0.6 / 0.2 / 4.6 GB)
+        gram_ws, sb_ws, oz = 6 << 27, 2 << 27, 37 << 27
     out["workspaces"] = 3 * gram_ws + sb_ws  # main / side / rr families
+    # main and side-stream emulated Grams + the tall GEMM (small products keep the DMMA kernels)
+    out["fp64_emulation_workspaces"] = 2 * oz
     # transients: the complex Gram's real (2k x 2k) product, cuSOLVER's k_total eigensolver
     out["transient"] = ((2 * kt) ** 2 * 8 if cplx else 0) + 2 * (kt * kt + 64 * kt) * s
     out["total"] = sum(out.values())
