@@ -30,6 +30,8 @@
 #include <cstdio>
 #include "common.cuh"
 
+#define BK_HD __host__ __device__ __forceinline__
+
 namespace bk {
 namespace oz {
 
@@ -121,6 +123,37 @@ BK_DEV void combine16_i64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
     uint32_t v[4][16];
 #pragma unroll
     for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * GS + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      long long x = (long long)(int)v[0][e];
+      x = (x << 8) + (long long)(int)v[1][e];
+      x = (x << 8) + (long long)(int)v[2][e];
+      x = (x << 8) + (long long)(int)v[3][e];
+      acc[e] = fma((double)x, 0x1p-32, (double)h[e]);
+    }
+  }
+}
+
+BK_DEV void combine16_i64_rt(uint32_t tmem_lane, int gs, int cc, double (&acc)[16]) {
+  long long h[16];
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + t * gs + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      long long x = (long long)(int)v[0][e];
+      x = (x << 8) + (long long)(int)v[1][e];
+      x = (x << 8) + (long long)(int)v[2][e];
+      h[e] = (x << 8) + (long long)(int)v[3][e];
+    }
+  }
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * gs + cc, v[t]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -280,15 +313,33 @@ __global__ void __launch_bounds__(256) k_slice_rows(int64_t r_base, int64_t nrow
 }
 
 // ---------------------------------------------------------------------------------------- mainloop
+// A Gram is cut into up to three segments, all in one launch (one tile list): the main block in
+// 128 x 64 tiles without padding, a narrow right strip (tiles of 16 / 32 / 64 columns), and the
+// bottom rows computed transposed (C[m1a:, :]^T = Y^T X[:, m1a:], the remainder on the N side
+// where the granularity is 16 instead of 128) -- or, for a symmetric Gram, the bottom-right
+// corner.  A segment reads A's digits (box 128 rows) and B's (box tbn rows) from its own maps.
+struct GramSeg {
+  int rowA0, rowB0;   // first operand column of the A / B side
+  int ta, tb;         // tile grid (128 A columns x tbn B columns per tile)
+  int tbn;            // 16, 32 or 64
+  int sym;            // upper tiles only (main block / corner of a symmetric Gram; equal origins)
+  int mirror;         // symmetric Gram: write the upper part (B col >= A col) and its mirror
+  int trans;          // writes C[B col][A col]
+  int limA, limB;     // operand column limits (exclusive)
+  int mapA, mapB;     // tensor map index of each side
+  int tile0;          // first tile of the segment in the launch's tile list
+  const int* EA;      // exponents of the A side's columns (indexed by operand column)
+  const int* EB;
+  int64_t part_off;   // this segment's partial sums, doubles: [chunk][tile][128][tbn]
+};
+
 struct GramEpi {
-  int m1, m2;
-  int ta, tb;         // tile grid (rows of 128, columns of 64)
-  int sym;            // upper tiles only
+  GramSeg seg[3];
+  int nseg;
+  int ntiles;         // tiles of all segments
   int64_t chunk_rows;  // rows per CTA (multiple of KB)
   int64_t nrows;      // rows in this launch
-  const int* EA;
-  const int* EB;
-  double* part;       // [chunk][tile][128][64]
+  double* part;
   int dbg;            // experiments (PPCG_OZ_DBG): 1 = no MMAs, 4 = no TMA
 };
 
@@ -314,82 +365,69 @@ struct TsEpi {
   int dbg;            // experiments (PPCG_OZ_DBG): 1 = no MMAs, 2 = no epilogue stores, 4 = no TMA
 };
 
-template <int MODE>
-struct OzArgs;
-template <>
-struct OzArgs<0> {
-  using Epi = GramEpi;
-};
-template <>
-struct OzArgs<1> {
-  using Epi = TsEpi;
-};
-
-BK_DEV void sym_tile(int idx, int ta, int tb, int& a, int& b) {
-  // upper tiles (b*BN + BN - 1 >= a*BM), enumerated row by row
+// upper tiles (b*tbn + tbn - 1 >= a*BM) of a ta x tb grid, enumerated row by row
+BK_HD int sym_bmin(int a, int tbn) {
+  const int v = a * BM - (tbn - 1);
+  return v <= 0 ? 0 : (v + tbn - 1) / tbn;
+}
+BK_DEV void sym_tile(int idx, int ta, int tb, int tbn, int& a, int& b) {
   for (a = 0; a < ta; ++a) {
-    int bmin = (a * BM - (BN - 1) + BN - 1) / BN;
-    if (bmin < 0) bmin = 0;
-    const int cnt = tb - bmin;
-    if (idx < cnt) {
-      b = bmin + idx;
+    const int cnt = tb - sym_bmin(a, tbn);
+    if (cnt > 0 && idx < cnt) {
+      b = sym_bmin(a, tbn) + idx;
       return;
     }
-    idx -= cnt;
+    if (cnt > 0) idx -= cnt;
   }
   a = ta - 1;
   b = tb - 1;
 }
 
-// MODE 0: Gram partial of one (tile, row chunk); grid (tiles, chunks).
-// MODE 1: tall GEMM tile; grid (row tiles, column tiles, problems); maps A[b], B[b] per problem.
-template <int MODE>
+BK_DEV const GramSeg& seg_of(const GramEpi& P, int tile, int& local) {
+  int i = 0;
+  while (i + 1 < P.nseg && tile >= P.seg[i + 1].tile0) ++i;
+  local = tile - P.seg[i].tile0;
+  return P.seg[i];
+}
+
+BK_DEV void seg_tile(const GramSeg& g, int local, int& a, int& b) {
+  if (g.sym) {
+    sym_tile(local, g.ta, g.tb, g.tbn, a, b);
+  } else {
+    a = local / g.tb;
+    b = local % g.tb;
+  }
+}
+
+// Gram partial of one (tile, row chunk); grid (tiles of all segments, chunks).  The B tile
+// width is per segment (16 / 32 / 64): the digit groups sit tbn TMEM columns apart, and one MMA
+// covers up to 256 / tbn digit blocks of B.
 __global__ void __launch_bounds__(THREADS, 1)
-    k_oz_mma(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
-             const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
-             const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
-             const __grid_constant__ CUtensorMap mapB2, const __grid_constant__ CUtensorMap mapB3,
-             const typename OzArgs<MODE>::Epi P) {
+    k_oz_gram(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+              const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapA3,
+              const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
+              const __grid_constant__ CUtensorMap mapB2, const __grid_constant__ CUtensorMap mapB3,
+              const GramEpi P) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
-  uint64_t* snap_full = done + 1;
-  uint64_t* snap_free = done + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 3);
-  __shared__ double s_red[4];
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- work item
-  int rowA = 0, rowB = 0, kc0 = 0, nk = 0, snap = -1, prob = 0;
-  const CUtensorMap* mA = &mapA0;
-  const CUtensorMap* mB = &mapB0;
-  if constexpr (MODE == 0) {
-    int a, b;
-    if (P.sym) {
-      sym_tile(blockIdx.x, P.ta, P.tb, a, b);
-    } else {
-      a = blockIdx.x / P.tb;
-      b = blockIdx.x % P.tb;
-    }
-    rowA = a * BM;
-    rowB = b * BN;
-    kc0 = (int)(blockIdx.y * P.chunk_rows);
-    const int64_t k1 = lmin(P.nrows, (int64_t)kc0 + P.chunk_rows);
-    nk = (int)((k1 - kc0 + KB - 1) / KB);
-  } else {
-    prob = blockIdx.z;
-    mA = prob == 0 ? &mapA0 : prob == 1 ? &mapA1 : prob == 2 ? &mapA2 : &mapA3;
-    mB = prob == 0 ? &mapB0 : prob == 1 ? &mapB1 : prob == 2 ? &mapB2 : &mapB3;
-    // column tiles fastest: the tiles of one row block run together and share its X digits in L2
-    rowA = blockIdx.y * BM;
-    rowB = blockIdx.x * BN;
-    nk = P.nk;
-    // G upper triangular: rows k >= the tile's last column are zero
-    if (P.upper) nk = min(nk, (rowB + BN + KB - 1) / KB);
-    if (prob == 0 && P.snap_stage >= 0 && rowB < P.nsplit) snap = P.snap_stage;
-  }
+  int local;
+  const GramSeg& g = seg_of(P, blockIdx.x, local);
+  int ta_, tb_;
+  seg_tile(g, local, ta_, tb_);
+  const int tbn = g.tbn;
+  const int rowA = g.rowA0 + ta_ * BM, rowB = g.rowB0 + tb_ * tbn;
+  const int kc0 = (int)(blockIdx.y * P.chunk_rows);
+  const int64_t k1 = lmin(P.nrows, (int64_t)kc0 + P.chunk_rows);
+  const int nk = (int)((k1 - kc0 + KB - 1) / KB);
+  const CUtensorMap* mA = g.mapA == 0 ? &mapA0 : g.mapA == 1 ? &mapA1 : g.mapA == 2 ? &mapA2 : &mapA3;
+  const CUtensorMap* mB = g.mapB == 0 ? &mapB0 : g.mapB == 1 ? &mapB1 : g.mapB == 2 ? &mapB2 : &mapB3;
+  const uint32_t stage_bytes = A_BYTES + S * tbn * KB;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -397,8 +435,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(empty + i, 1);
     }
     mbar_init(done, 1);
-    mbar_init(snap_full, 1);
-    mbar_init(snap_free, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(mA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(mB) : "memory");
@@ -423,150 +459,70 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_arrive(full + st);
           continue;
         }
-        mbar_arrive_expect_tx(full + st, STAGE_BYTES);
+        mbar_arrive_expect_tx(full + st, stage_bytes);
         const int kc = kc0 + kb * KB;
         tma3d(sa, mA, kc, rowA, 0, full + st);
         tma3d(sa + A_BYTES, mB, kc, rowB, 0, full + st);
       }
     }
   } else if (warp == 1) {
+    const int nj_max = 256 / tbn;
     for (int kb = 0; kb < nk; ++kb) {
       const int st = kb % STAGES;
       mbar_wait(full + st, (kb / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
+      if (lane == 0 && !(P.dbg & 1)) {
         const uint32_t sa = smem_u32(sm + st * STAGE_BYTES);
         const uint32_t sb = sa + A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < KB / 32; ++ks) {
-          if (P.dbg & 1) break;
 #pragma unroll
           for (int i = 0; i < S; ++i) {
-#pragma unroll
-            for (int j0 = 0; j0 < S - i; j0 += 4) {
-              const int nj = (S - i - j0) < 4 ? (S - i - j0) : 4;
+            for (int j0 = 0; j0 < S - i; j0 += nj_max) {
+              const int nj = (S - i - j0) < nj_max ? (S - i - j0) : nj_max;
               const uint64_t da = umma_desc(sa + i * BM * KB + ks * 32);
-              const uint64_t db = umma_desc(sb + j0 * BN * KB + ks * 32);
+              const uint64_t db = umma_desc(sb + j0 * tbn * KB + ks * 32);
               const uint32_t accf = (kb > 0 || ks > 0 || i > 0) ? 1u : 0u;
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (i + j0) * BN),
-                  "l"(da), "l"(db), "r"(idesc_i8(nj * BN)), "r"(accf));
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + (i + j0) * tbn),
+                  "l"(da), "l"(db), "r"(idesc_i8(nj * tbn)), "r"(accf));
             }
           }
         }
+      }
+      if (lane == 0) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(empty + st))
                      : "memory");
-        if (kb == snap)
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(snap_full))
-                       : "memory");
         if (kb == nk - 1)
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_u32(done))
                        : "memory");
       }
       __syncwarp();
-      if (kb == snap && kb != nk - 1) mbar_wait(snap_free, 0);  // epilogue has read the snapshot
     }
   } else {
-    // ---- epilogue warps: TMEM lane quadrant = warp % 4 (hardware rule), lane = row of the tile
+    // epilogue warps: TMEM lane quadrant = warp % 4 (hardware rule), lane = A column of the tile
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    if constexpr (MODE == 0) {
-      mbar_wait(done, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int gr = rowA + r;
-      const int ea = gr < P.m1 ? P.EA[gr] : 0;
-      double* out = P.part + (((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BM + r) * BN;
-#pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 16) {
-        double acc[16];
-        combine16(tl, cc, acc);
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int ga = rowA + r;
+    const int ea0 = ga < g.limA ? g.EA[ga] : 0;
+    const int ea = ea0 == NON_FINITE ? NON_FINITE : ea0 - 36;  // combine16_i64 leaves 2^-36
+    const int seg_tiles = g.ta * g.tb;  // partial slots per chunk (sym: the full grid, sparse)
+    double* out = P.part + g.part_off + (((int64_t)blockIdx.y * seg_tiles + ta_ * g.tb + tb_) * BM + r) * tbn;
+    for (int cc = 0; cc < tbn; cc += 16) {
+      double acc[16];
+      combine16_i64_rt(tl, tbn, cc, acc);
 #pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          const int gc = rowB + cc + e;
-          const int e0 = gc < P.m2 ? P.EB[gc] : 0;
-          const int e1 = gc + 1 < P.m2 ? P.EB[gc + 1] : 0;
-          *reinterpret_cast<double2*>(out + cc + e) = make_double2(scaled(acc[e], ea, e0), scaled(acc[e + 1], ea, e1));
-        }
-      }
-    } else {
-      const int64_t lrow = rowA + r;  // row within this launch
-      const bool live = lrow < P.nrows;
-      const int64_t grow = P.r_base + lrow;
-      const int er = live ? P.ER[prob][grow] : 0;
-      const int* EG = P.EG[prob];
-      const double* Z = P.Z[prob];
-      double* Y = P.Y[prob];
-      if (snap >= 0) {
-        // metric: sum over cols < nsplit of (alpha X[:, :ksplit] G[:ksplit] + beta Z)^2
-        mbar_wait(snap_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        double ss = 0;
-        for (int cc = 0; cc < BN && rowB + cc < P.nsplit; cc += 16) {
-          double acc[16];
-          combine16(tl, cc, acc);
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int gc = rowB + cc + e;
-            if (live && gc < P.nsplit && gc < P.N) {
-              double v = P.alpha * scaled(acc[e], er, EG[gc]);
-              if (P.beta != 0.0) v = fma(P.beta, Z[grow * P.ldz + gc], v);
-              ss = fma(v, v, ss);
-            }
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(snap_free);
-        ss = warp_sum(ss);
-        if (lane == 0) s_red[q] = ss;
-        named_bar_sync(1, 128);
-        if (threadIdx.x == 64) {
-          const double t = s_red[0] + s_red[1] + s_red[2] + s_red[3];
-          P.metric_ws[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
-        }
-      }
-      if (snap < 0 && prob == 0 && P.snap_stage >= 0 && threadIdx.x == 64)
-        P.metric_ws[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = 0.0;  // tile right of nsplit
-      mbar_wait(done, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (Y != nullptr) {
-        const double sr = (live && P.rowscale) ? P.rowscale[grow] : 1.0;
-#pragma unroll 1
-        for (int cc = 0; cc < BN; cc += 16) {
-          if (rowB + cc >= P.N) break;
-          double acc[16];
-          combine16(tl, cc, acc);
-          if (!live) continue;
-          const int64_t zo = grow * P.ldz + rowB + cc, yo = grow * P.ldy + rowB + cc;
-          const bool vec = ((reinterpret_cast<uintptr_t>(Y + yo) & 15) == 0) &&
-                           (P.beta == 0.0 || (reinterpret_cast<uintptr_t>(Z + zo) & 15) == 0);
-          if (vec && rowB + cc + 16 <= P.N) {
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const int gc = rowB + cc + e;
-              double v0 = P.alpha * scaled(acc[e], er, EG[gc]);
-              double v1 = P.alpha * scaled(acc[e + 1], er, EG[gc + 1]);
-              if (P.beta != 0.0) {
-                const double2 z = *reinterpret_cast<const double2*>(Z + zo + e);
-                v0 = fma(P.beta, z.x, v0);
-                v1 = fma(P.beta, z.y, v1);
-              }
-              *reinterpret_cast<double2*>(Y + yo + e) = make_double2(sr * v0, sr * v1);
-            }
-          } else {
-            for (int e = 0; e < 16; ++e) {
-              const int gc = rowB + cc + e;
-              if (gc >= P.N) break;
-              double v = P.alpha * scaled(acc[e], er, EG[gc]);
-              if (P.beta != 0.0) v = fma(P.beta, Z[zo + e], v);
-              Y[yo + e] = sr * v;
-            }
-          }
-        }
+      for (int e = 0; e < 16; e += 2) {
+        const int gb = rowB + cc + e;
+        const int e0 = gb < g.limB ? g.EB[gb] : 0;
+        const int e1 = gb + 1 < g.limB ? g.EB[gb + 1] : 0;
+        *reinterpret_cast<double2*>(out + cc + e) = make_double2(scaled(acc[e], ea, e0), scaled(acc[e + 1], ea, e1));
       }
     }
   }
@@ -902,33 +858,34 @@ constexpr int ts_smem() {
   return STAGES * (A_BYTES + S * TBN * KB) + 1024 + 256 + TS_STAGE_OUT;
 }
 
-// C (+)= sum over chunks of the partials, fixed chunk order, compensated; symmetric: upper tiles
-// mirrored.
-// grid (tiles, 16): 8 rows x 64 columns per CTA
+// C (+)= sum over chunks of the partials, fixed chunk order, compensated; symmetric segments
+// write their upper part and its mirror, transposed segments C[B col][A col].
+// grid (tiles of all segments, 16): 8 A columns x tbn B columns per CTA
 __global__ void k_gram_reduce(GramEpi P, int nch, double* C, int64_t ldc, int accumulate) {
+  int local;
+  const GramSeg& g = seg_of(P, blockIdx.x, local);
   int a, b;
-  if (P.sym) {
-    sym_tile(blockIdx.x, P.ta, P.tb, a, b);
-  } else {
-    a = blockIdx.x / P.tb;
-    b = blockIdx.x % P.tb;
-  }
+  seg_tile(g, local, a, b);
   const int r = blockIdx.y * 8 + (threadIdx.x >> 6), c = threadIdx.x & 63;
-  const int gr = a * BM + r, gc = b * BN + c;
-  if (gr >= P.m1 || gc >= P.m2) return;
-  if (P.sym && gc < gr) return;
+  if (c >= g.tbn) return;
+  const int gA = g.rowA0 + a * BM + r, gB = g.rowB0 + b * g.tbn + c;
+  if (gA >= g.limA || gB >= g.limB) return;
+  if (g.mirror && gB < gA) return;
+  double* dst = g.trans ? C + (int64_t)gB * ldc + gA : C + (int64_t)gA * ldc + gB;
   // compensated (Neumaier) sum: the chunk partials are each rounded once, so the total error stays
   // ~u sum_chunks |partial| <= u |X|^T |Y| whatever the chunk count
-  double s = accumulate ? C[(int64_t)gr * ldc + gc] : 0.0, comp = 0.0;
+  double s = accumulate ? *dst : 0.0, comp = 0.0;
+  const int64_t per_chunk = (int64_t)g.ta * g.tb * BM * g.tbn;
+  const double* src = P.part + g.part_off + ((int64_t)(a * g.tb + b) * BM + r) * g.tbn + c;
   for (int ch = 0; ch < nch; ++ch) {
-    const double v = __ldcg(P.part + (((int64_t)ch * gridDim.x + blockIdx.x) * BM + r) * BN + c);
+    const double v = __ldcg(src + ch * per_chunk);
     const double t = s + v;
     comp += fabs(s) >= fabs(v) ? (s - t) + v : (v - t) + s;
     s = t;
   }
   s += comp;
-  C[(int64_t)gr * ldc + gc] = s;
-  if (P.sym && gc > gr) C[(int64_t)gc * ldc + gr] = s;
+  *dst = s;
+  if (g.mirror && gB > gA) C[(int64_t)gB * ldc + gA] = s;
 }
 
 // metric: fixed-order sum of the per-CTA partials (one thread block)
@@ -981,18 +938,6 @@ static int g_emu_mode = -1;  // -1: from PPCG_FP64_EMU (default on), 0 off, 1 on
 
 static int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
-static int n_tiles(int m1, int m2, int sym) {
-  const int ta = (m1 + BM - 1) / BM, tb = (m2 + BN - 1) / BN;
-  if (!sym) return ta * tb;
-  int cnt = 0;
-  for (int a = 0; a < ta; ++a) {
-    int bmin = (a * BM) / BN;
-    if (a * BM - (bmin * BN + BN - 1) > 0) ++bmin;
-    cnt += tb - (bmin < 0 ? 0 : bmin);
-  }
-  return cnt;
-}
-
 // rows per chunk: <= MAX_CHUNK, a multiple of KB, chosen for whole waves of 148 CTAs
 static int64_t gram_chunk_rows(int64_t n, int ntiles) {
   const int64_t cmin = (n + MAX_CHUNK - 1) / MAX_CHUNK;
@@ -1012,22 +957,77 @@ static int64_t gram_chunk_rows(int64_t n, int ntiles) {
   return align_up((n + best - 1) / best, KB);
 }
 
+static int narrow_tbn(int w) { return w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+
+static int sym_count(int ta, int tb, int tbn) {
+  int cnt = 0;
+  for (int a = 0; a < ta; ++a) cnt += tb - sym_bmin(a, tbn) > 0 ? tb - sym_bmin(a, tbn) : 0;
+  return cnt;
+}
+
+// segments of C = X^T Y (operand 0 = X, 1 = Y), see GramSeg
+struct GramPlan {
+  GramSeg seg[3];
+  int opA[3], opB[3];
+  int nseg, ntiles;
+  int64_t part_per_chunk;  // doubles
+};
+
+static GramPlan gram_plan(int m1, int m2, int sym) {
+  GramPlan G{};
+  auto add = [&](int opA, int rowA0, int limA, int opB, int rowB0, int limB, int tbn, int symf, int mirror,
+                 int trans) {
+    if (limA <= rowA0 || limB <= rowB0) return;
+    GramSeg& g = G.seg[G.nseg];
+    g = GramSeg{};
+    g.rowA0 = rowA0;
+    g.limA = limA;
+    g.rowB0 = rowB0;
+    g.limB = limB;
+    g.tbn = tbn;
+    g.ta = (limA - rowA0 + BM - 1) / BM;
+    g.tb = (limB - rowB0 + tbn - 1) / tbn;
+    g.sym = symf;
+    g.mirror = mirror;
+    g.trans = trans;
+    g.tile0 = G.ntiles;
+    g.part_off = G.part_per_chunk;  // scaled by the chunk count when the launch is set up
+    G.ntiles += symf ? sym_count(g.ta, g.tb, tbn) : g.ta * g.tb;
+    G.part_per_chunk += (int64_t)g.ta * g.tb * BM * tbn;
+    G.opA[G.nseg] = opA;
+    G.opB[G.nseg] = opB;
+    ++G.nseg;
+  };
+  const int m1a = m1 / BM * BM, m2a = m2 / BN * BN;
+  if (sym) {  // X^T X: upper main tiles, the right strip (all above the diagonal), the corner
+    add(0, 0, m1a, 0, 0, m2a, BN, 1, 1, 0);
+    add(0, 0, m1a, 0, m2a, m2, narrow_tbn(m2 - m2a), 0, 1, 0);
+    add(0, m1a, m1, 0, m1a, m2, narrow_tbn(m2 - m1a), 1, 1, 0);
+  } else {
+    add(0, 0, m1a, 1, 0, m2a, BN, 0, 0, 0);
+    add(0, 0, m1a, 1, m2a, m2, narrow_tbn(m2 - m2a), 0, 0, 0);
+    add(1, 0, m2, 0, m1a, m1, narrow_tbn(m1 - m1a), 0, 0, 1);  // bottom rows, transposed
+  }
+  return G;
+}
+
 struct GramLayout {
   int nq;                      // B operands sharing the A digits (1 or 2)
-  int ntiles[2];
+  GramPlan plan[2];
   int64_t chunk_rows, sc_rows;  // rows per chunk, rows per super-chunk (digits held at once)
   int64_t off_cmA, off_EA, off_sA, off_cmB[2], off_EB[2], off_part[2], off_sB[2], total;
 };
 
-// same: B operand q is A itself (one set of digits); sym (requires same): upper tiles only
+// same: B operand q is X itself (one set of digits); sym (requires same): symmetric segments
 static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const int* same, int sym, int64_t ws_cap) {
   GramLayout L{};
   L.nq = nq;
   int tt = 0;
-  for (int q = 0; q < nq; ++q) tt += L.ntiles[q] = n_tiles(m1, m2[q], sym);
+  for (int q = 0; q < nq; ++q) {
+    L.plan[q] = gram_plan(m1, m2[q], sym);
+    tt = tt > L.plan[q].ntiles ? tt : L.plan[q].ntiles;
+  }
   L.chunk_rows = gram_chunk_rows(n, tt);
-  int64_t per_row = (int64_t)S * m1;
-  for (int q = 0; q < nq; ++q) per_row += same[q] ? 0 : (int64_t)S * m2[q];
   // digits of at most ~1.5 GB at once (or what the caller's workspace holds)
   int64_t sc_chunks = (n + L.chunk_rows - 1) / L.chunk_rows;
   const int64_t cap = ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
@@ -1039,7 +1039,7 @@ static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const in
     for (int q = 0; q < nq; ++q) {
       L.off_cmB[q] = o; o += align_up(8 * (int64_t)m2[q], 256);
       L.off_EB[q] = o;  o += align_up(4 * (int64_t)m2[q], 256);
-      L.off_part[q] = o; o += align_up(chunks * L.ntiles[q] * (int64_t)BM * BN * 8, 1024);
+      L.off_part[q] = o; o += align_up(chunks * L.plan[q].part_per_chunk * 8, 1024);
     }
     L.off_sA = o; o += align_up((int64_t)S * m1 * rows, 1024);
     for (int q = 0; q < nq; ++q) {
@@ -1051,7 +1051,6 @@ static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const in
   while (sc_chunks > 1 && layout(sc_chunks) > cap) sc_chunks = (sc_chunks + 1) / 2;
   L.sc_rows = sc_chunks * L.chunk_rows;
   L.total = layout(sc_chunks);
-  (void)per_row;
   return L;
 }
 
@@ -1091,25 +1090,11 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
     BK_COUNT();
     k_exponents<<<(m2[q] + 255) / 256, 256, 0, st>>>(m2[q], cmB, EB[q], nullptr);
   }
-  cudaFuncSetAttribute(k_oz_mma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(k_oz_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   static const int dbg = [] {
     const char* e = getenv("PPCG_OZ_DBG");
     return e ? atoi(e) : 0;
   }();
-  GramEpi P[2];
-  for (int q = 0; q < nq; ++q) {
-    P[q] = GramEpi{};
-    P[q].m1 = m1;
-    P[q].m2 = m2[q];
-    P[q].ta = (m1 + BM - 1) / BM;
-    P[q].tb = (m2[q] + BN - 1) / BN;
-    P[q].sym = symmetric ? 1 : 0;
-    P[q].chunk_rows = L.chunk_rows;
-    P[q].EA = EA;
-    P[q].EB = EB[q];
-    P[q].part = reinterpret_cast<double*>(w + L.off_part[q]);
-    P[q].dbg = dbg;
-  }
   for (int64_t r0 = 0; r0 < n; r0 += L.sc_rows) {
     const int64_t rows = lmin(L.sc_rows, n - r0);
     const int64_t kld = align_up(rows, KPAD);
@@ -1117,8 +1102,6 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
     BK_COUNT();
     k_slice_cols<<<dim3(gx, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
                                                            kld * (int64_t)m1, kld);
-    CUtensorMap mA;
-    if (!encode_digits(&mA, sA, kld, rows, m1, BM, kld * (int64_t)m1)) return BK_ERR_UNSUPPORTED;
     const int nch = (int)((rows + L.chunk_rows - 1) / L.chunk_rows);
     for (int q = 0; q < nq; ++q) {
       if (!same[q]) {
@@ -1126,14 +1109,55 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
         k_slice_cols<<<dim3(gx, (m2[q] + 31) / 32), 256, 0, st>>>(r0 + rows, m2[q], Y[q], ldy[q], EB[q], r0, sB[q],
                                                                  kld, kld * (int64_t)m2[q], kld);
       }
-      CUtensorMap mB;
-      if (!encode_digits(&mB, sB[q], kld, rows, m2[q], BN, kld * (int64_t)m2[q])) return BK_ERR_UNSUPPORTED;
-      P[q].nrows = rows;
+      // tensor maps: one per (operand, box rows) pair the segments use
+      const GramPlan& G = L.plan[q];
+      const int8_t* dig[2] = {sA, sB[q]};
+      const int mcols[2] = {m1, m2[q]};
+      const int* ex[2] = {EA, EB[q]};
+      CUtensorMap mapsA[4], mapsB[4];
+      int keyA[4], keyB[4], na = 0, nb = 0;
+      GramEpi P{};
+      P.nseg = G.nseg;
+      P.ntiles = G.ntiles;
+      P.chunk_rows = L.chunk_rows;
+      P.nrows = rows;
+      P.part = reinterpret_cast<double*>(w + L.off_part[q]);
+      P.dbg = dbg;
+      for (int i = 0; i < G.nseg; ++i) {
+        P.seg[i] = G.seg[i];
+        P.seg[i].part_off = G.seg[i].part_off * nch;
+        P.seg[i].EA = ex[G.opA[i]];
+        P.seg[i].EB = ex[G.opB[i]];
+        const int ka = G.opA[i], kbk = G.opB[i] * 1000 + G.seg[i].tbn;
+        int ia = -1, ib = -1;
+        for (int j = 0; j < na; ++j)
+          if (keyA[j] == ka) ia = j;
+        for (int j = 0; j < nb; ++j)
+          if (keyB[j] == kbk) ib = j;
+        if (ia < 0) {
+          ia = na++;
+          keyA[ia] = ka;
+          if (!encode_digits(&mapsA[ia], dig[ka], kld, rows, mcols[ka], BM, kld * (int64_t)mcols[ka]))
+            return BK_ERR_UNSUPPORTED;
+        }
+        if (ib < 0) {
+          ib = nb++;
+          keyB[ib] = kbk;
+          const int ob = G.opB[i];
+          if (!encode_digits(&mapsB[ib], dig[ob], kld, rows, mcols[ob], G.seg[i].tbn, kld * (int64_t)mcols[ob]))
+            return BK_ERR_UNSUPPORTED;
+        }
+        P.seg[i].mapA = ia;
+        P.seg[i].mapB = ib;
+      }
+      for (int j = na; j < 4; ++j) mapsA[j] = mapsA[0];
+      for (int j = nb; j < 4; ++j) mapsB[j] = mapsB[0];
       BK_COUNT();
-      k_oz_mma<0><<<dim3(L.ntiles[q], nch), THREADS, SMEM, st>>>(mA, mA, mA, mA, mB, mB, mB, mB, P[q]);
+      k_oz_gram<<<dim3(G.ntiles, nch), THREADS, SMEM, st>>>(mapsA[0], mapsA[1], mapsA[2], mapsA[3], mapsB[0],
+                                                            mapsB[1], mapsB[2], mapsB[3], P);
       BK_CHECK_LAUNCH();
       BK_COUNT();
-      k_gram_reduce<<<dim3(L.ntiles[q], 16), 512, 0, st>>>(P[q], nch, C[q], ldc[q], r0 > 0 ? 1 : 0);
+      k_gram_reduce<<<dim3(G.ntiles, 16), 512, 0, st>>>(P, nch, C[q], ldc[q], r0 > 0 ? 1 : 0);
     }
   }
   BK_CHECK_LAUNCH();
