@@ -247,10 +247,20 @@ class PPCGSolver:
         # (columns relative to the extended buffer's first row) multiplies it
         base, owned = self._ext_of(x)
         p = self.plan
-        self.comm.exchange([(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.send],
-                           [(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.recv])
         es = x.element_size()
         c0 = (x.data_ptr() - owned.data_ptr()) // es
+        w = x.shape[1]
+        if 4 * w <= 3 * base.shape[1]:
+            # narrow active block (locked columns, padding): exchange only its columns, packed
+            # into contiguous buffers, instead of whole ld-wide rows
+            sends = [(peer, base[a - p.g_lo:b - p.g_lo, c0:c0 + w].contiguous()) for peer, a, b in p.send]
+            recvs = [(peer, a, b, torch_empty_like_rows(base, b - a, w)) for peer, a, b in p.recv]
+            self.comm.exchange(sends, [(peer, t) for peer, _, _, t in recvs])
+            for _, a, b, t in recvs:
+                base[a - p.g_lo:b - p.g_lo, c0:c0 + w].copy_(t)
+        else:
+            self.comm.exchange([(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.send],
+                               [(peer, base[a - p.g_lo:b - p.g_lo]) for peer, a, b in p.recv])
         self.dev_a.apply_into(base[:, c0:c0 + x.shape[1]], y)
 
     def _ext_of(self, x):
@@ -1062,6 +1072,13 @@ def device_bytes_plan(n_loc, n_ext, kt, q, cplx, nnz_loc=0, size=1):
     out["transient"] = ((2 * kt) ** 2 * 8 if cplx else 0) + 2 * (kt * kt + 64 * kt) * s
     out["total"] = sum(out.values())
     return out
+
+
+def torch_empty_like_rows(base, rows, cols):
+    """Contiguous (rows, cols) receive buffer of base's dtype and device (packed halo)."""
+    import torch
+
+    return torch.empty((rows, cols), dtype=base.dtype, device=base.device)
 
 
 def _stencil_plane(csr):
