@@ -256,3 +256,36 @@ def test_ozaki_tsgemm_last_stage_snapshots_back_to_back(cuda):
         torch.cuda.synchronize()
     ref = np.sum((z - x @ g) ** 2)
     assert abs(m.item() - ref) <= 1e-12 * ref
+
+
+def test_ozaki_tsgemm_superchunks_bitwise(cuda):
+    """A workspace that holds the row digits of a fraction of the rows: the tall GEMM runs in
+    row super-chunks (the 4-problem projection update at config 2 does); rows are independent,
+    so Y is bitwise the one-pass result and the metric agrees to rounding of its partial sums."""
+    from paper_1407_7506_b200 import _lib
+    from paper_1407_7506_b200.kernels import stream_ptr
+
+    torch = cuda
+    lib = _lib.load()
+    n, Kt, N, ks = 70000, 200, 150, 190
+    x, g, z = dev(gauss(n, Kt, 110), torch), dev(gauss(Kt, N, 111), torch), dev(gauss(n, N, 112), torch)
+    s = dev(np.abs(gauss(n, 1, 113))[:, 0] + 0.5, torch)
+    full = lib.bk_ozaki_tsgemm_ws_bytes(1, n, Kt, N, ks)
+    outs = []
+    for frac in (1.0, 0.3):
+        nb = int(full * frac)
+        ws = torch.empty(full, dtype=torch.uint8, device="cuda")
+        y = torch.empty((n, N), dtype=torch.float64, device="cuda")
+        m = torch.zeros(1, dtype=torch.float64, device="cuda")
+        XP, _a = _lib.ptr_array([x.data_ptr()])
+        GP, _b = _lib.ptr_array([g.data_ptr()])
+        ZP, _c = _lib.ptr_array([z.data_ptr()])
+        YP, _d = _lib.ptr_array([y.data_ptr()])
+        _lib.call("bk_ozaki_tsgemm_d", 1, n, Kt, N, -1.0, XP, Kt, GP, N, 1.0, ZP, N, YP, N, s.data_ptr(), 0, ks, N,
+                  m.data_ptr(), ws.data_ptr(), nb, stream_ptr())
+        outs.append((y.cpu().numpy(), m.item()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert abs(outs[0][1] - outs[1][1]) <= 1e-14 * abs(outs[0][1])
+    xn, gn, zn = x.cpu().numpy(), g.cpu().numpy(), z.cpu().numpy()
+    ref = np.sum((zn - xn[:, :ks] @ gn[:ks]) ** 2)
+    assert abs(outs[0][1] - ref) <= 1e-12 * ref
