@@ -169,6 +169,69 @@ BK_DEV bool smem_cholesky(T* M, int ld, int d) {
   return true;
 }
 
+// The same factorisation for the large real variant, whose M lives in global (L2-resident)
+// memory: the lower triangle is staged packed in shared memory (pk, d (d+1) / 2 doubles, idle
+// at this point), column j scaled once into col[] per step, and written back.  Every element
+// sees the same operations in the same order as smem_cholesky, so L is bitwise the same.
+BK_DEV bool packed_cholesky(double* M, int ld, int d, double* pk, double* col) {
+#define PKL(i, k) pk[(i) * ((i) + 1) / 2 + (k)]
+  for (int i = BK_WARP; i < d; i += BK_NWARP)
+    for (int k = BK_LANE; k <= i; k += 32) PKL(i, k) = M[i * ld + k];
+  bool ok = true;
+  for (int j = 0; j < d; ++j) {
+    __syncthreads();
+    const double piv = PKL(j, j);
+    if (!(piv > 0.0) || !isfinite(piv)) {
+      ok = false;
+      break;
+    }
+    const double ljj = sqrt(piv);
+    const double inv = 1.0 / ljj;
+    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) col[i] = PKL(i, j) * inv;
+    __syncthreads();
+    for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
+      const double lij = col[i];
+      for (int k = j + 1 + BK_LANE; k <= i; k += 32) PKL(i, k) = PKL(i, k) - lij * col[k];
+    }
+    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) PKL(i, j) = col[i];
+    if (threadIdx.x == 0) PKL(j, j) = ljj;
+  }
+  __syncthreads();
+  if (!ok) return false;  // uniform: every thread read the same pivot
+  for (int i = BK_WARP; i < d; i += BK_NWARP)
+    for (int k = BK_LANE; k <= i; k += 32) M[i * ld + k] = PKL(i, k);
+  __syncthreads();
+#undef PKL
+  return true;
+}
+
+// smem_lower_inverse in place on the packed L that packed_cholesky leaves in pk (large real
+// variant): row i's entries c < j already hold Linv (finished by earlier steps), c = j is the
+// identity's 0 - f Linv[j][j], and L's diagonal is kept in dg until the end -- the same
+// operations per element as smem_lower_inverse, so Linv is bitwise the same.  Linv goes to
+// global memory (ld li), zeros above the diagonal.
+BK_DEV void packed_lower_inverse(double* pk, int d, double* dg, double* Li, int li) {
+#define PKL(i, k) pk[(i) * ((i) + 1) / 2 + (k)]
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dg[i] = PKL(i, i);
+  __syncthreads();
+  for (int j = 0; j < d - 1; ++j) {
+    const double ljj_inv = 1.0 / dg[j];
+    for (int i = j + 1 + BK_WARP; i < d; i += BK_NWARP) {
+      const double f = PKL(i, j) * (1.0 / dg[i]);
+      __syncwarp();
+      for (int c = BK_LANE; c < j; c += 32) PKL(i, c) = PKL(i, c) - f * PKL(j, c);
+      if (BK_LANE == 0) PKL(i, j) = 0.0 - f * ljj_inv;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) PKL(i, i) = 1.0 / dg[i];
+  __syncthreads();
+  for (int i = BK_WARP; i < d; i += BK_NWARP)
+    for (int c = BK_LANE; c < d; c += 32) Li[i * li + c] = c <= i ? PKL(i, c) : 0.0;
+  __syncthreads();
+#undef PKL
+}
+
 // Linv (lower) from L (lower): X = I; for j: X[i,:] -= (l_ij / l_ii) X[j,:] (i > j)
 template <class T>
 BK_DEV void smem_lower_inverse(const T* L, int ll, T* Li, int li, int d) {
@@ -952,7 +1015,11 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   const double flo = kGramRtol * fmax(fro, 1e-300);
   for (int a = threadIdx.x; a < d; a += blockDim.x) B[a * PLD + a] = B[a * PLD + a] - fromR<T>(flo);
   __syncthreads();
-  if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:193-197
+  if constexpr (kOwnPk<T, PD>) {
+    if (!packed_cholesky(reinterpret_cast<double*>(B), PLD, d, S.pk, S.rc)) return 1;  // core.py:193-197
+  } else {
+    if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:193-197
+  }
   // reload B (exact) and factor it for the reduction (sygvd's potrf)
   for (int a = BK_WARP; a < d; a += BK_NWARP) {
     const int ia = S.idx[a];
@@ -968,8 +1035,15 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
     }
   }
   __syncthreads();
-  if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:198-201
-  smem_lower_inverse(B, PLD, Li, PLD, d);
+  if constexpr (kOwnPk<T, PD>) {
+    if (!packed_cholesky(reinterpret_cast<double*>(B), PLD, d, S.pk, S.rc)) return 1;  // core.py:198-201
+  } else {
+    if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:198-201
+  }
+  if constexpr (kOwnPk<T, PD>)
+    packed_lower_inverse(S.pk, d, S.rc, reinterpret_cast<double*>(Li), PLD);  // L still packed in pk
+  else
+    smem_lower_inverse(B, PLD, Li, PLD, d);
   smem_gemm<T, PD, false, false, false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A
   __syncthreads();
   smem_gemm<T, PD, false, false, true, true>(B, PLD, Li, PLD, A, PLD, d, d);    // Ared = T Linv^H
