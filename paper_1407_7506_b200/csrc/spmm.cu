@@ -1068,6 +1068,14 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
     if (cfg == 1) {
       NCONS = st_consumers<32, 1, 4>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4> : spmm_stencil_kernel<false, 27, 32, 1, 4>;
+    } else if (cfg == 2) {  // two column pieces per thread: each stencil value feeds 4 FMAs
+      COLS = 64;
+      NCONS = st_consumers<64, 2, 2>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 64, 2, 2> : spmm_stencil_kernel<false, 27, 64, 2, 2>;
+    } else if (cfg == 3) {
+      COLS = 64;
+      NCONS = st_consumers<64, 2, 4>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 64, 2, 4> : spmm_stencil_kernel<false, 27, 64, 2, 4>;
     } else {
       NCONS = st_consumers<32, 1, 2>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2>;

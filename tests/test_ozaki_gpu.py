@@ -289,3 +289,33 @@ def test_ozaki_tsgemm_superchunks_bitwise(cuda):
     xn, gn, zn = x.cpu().numpy(), g.cpu().numpy(), z.cpu().numpy()
     ref = np.sum((zn - xn[:, :ks] @ gn[:ks]) ** 2)
     assert abs(outs[0][1] - ref) <= 1e-12 * ref
+
+
+def test_ozaki_extreme_scales(cuda):
+    """Columns / rows scaled to 1e-300 and 1e+150 (products down to the subnormal range and up
+    to 1e300): the power-of-two factors leave the fast path and go through exact ldexp; the
+    results stay within the DGEMM-class bound of the longdouble reference, and pure
+    subnormal inputs are represented (not flushed)."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m = 20000, 96
+    x, y = gauss(n, m, 120), gauss(n, m, 121)
+    x[:, :8] *= 1e-300
+    y[:, 8:16] *= 1e150
+    x[:, 16:24] *= 1e150
+    x[:, 24] = 5e-324 * np.sign(x[:, 24])  # subnormal column
+    with emu(torch):
+        c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+        g = gauss(m, m, 122)
+        g[:, :4] *= 1e-200
+        w = torch.empty((n, m), dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [w])
+    cs = np.arange(0, 40)
+    ref, absprod = exact_gram(x, y, cs, cs)
+    assert np.all(np.abs(c[np.ix_(cs, cs)] - ref) <= 4 * U * absprod + 1e-320)
+    assert np.count_nonzero(c[24]) > 0
+    rows = sample(n, 200, 123)
+    prod = (x[rows].astype(np.longdouble) @ g.astype(np.longdouble)).astype(np.float64)
+    bound = 4 * U * (np.abs(x[rows]) @ np.abs(g))
+    assert np.all(np.abs(w.cpu().numpy()[rows] - prod) <= bound + 1e-320)

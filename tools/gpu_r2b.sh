@@ -12,5 +12,5 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_sma
     > gpurun_out/ncu_launch_$tag.log 2>&1
 python tools/oz_one.py ts && timeout 500 ncu --set full --clock-control none --import-source on \
   -k regex:"k_oz_ts|k_slice_rows" -s 2 -c 2 -o gpurun_out/oz_ts_$tag python tools/oz_one.py ts > gpurun_out/ncu_ts_$tag.log 2>&1
-timeout 500 ncu --set full --clock-control none --import-source on -k regex:"k_oz_mma|k_slice_cols|k_colmax|k_gram_reduce" \
+timeout 500 ncu --set full --clock-control none --import-source on -k regex:"k_oz_gram|k_slice_cols|k_colmax|k_gram_reduce" \
   -s 6 -c 6 -o gpurun_out/oz_gram_$tag python tools/oz_one.py gram > gpurun_out/ncu_gram_$tag.log 2>&1
