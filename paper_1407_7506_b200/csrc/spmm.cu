@@ -794,6 +794,10 @@ template <int COLS, int NP, int RZ>
 constexpr int st_consumers() {
   return M_T * M_T / RZ * (COLS / 2 / NP);
 }
+template <int COLS, int NP, int RZ, int RY>
+constexpr int st_consumers_y() {
+  return M_T * M_T / (RZ * RY) * (COLS / 2 / NP);
+}
 
 template <bool CPLX>
 BK_DEV void st_fma(double2& acc, march_vt<CPLX> a, double2 v) {
@@ -806,14 +810,15 @@ BK_DEV void st_fma(double2& acc, march_vt<CPLX> a, double2 v) {
   }
 }
 
-template <bool CPLX, int ST, int COLS, int NP, int RZ>
-__global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
+template <bool CPLX, int ST, int COLS, int NP, int RZ, int RY = 1>
+__global__ void __launch_bounds__(st_consumers_y<COLS, NP, RZ, RY>() + 32, 1)
     spmm_stencil_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
                         MarchArgs A) {
   static_assert(ST == 7 || ST == 27, "stencil");
-  static_assert(ST == 27 || RZ == 1, "7-point: one row per thread");
+  static_assert(ST == 27 || (RZ == 1 && RY == 1), "7-point: one row per thread");
   constexpr int TPR = COLS / 2 / NP;  // threads per row (16-byte pieces g + TPR k)
-  constexpr int NCONS = st_consumers<COLS, NP, RZ>();
+  constexpr int NCONS = st_consumers_y<COLS, NP, RZ, RY>();
+  constexpr int NR = RY * RZ;         // output rows per thread: RY (y) x RZ (z) block
   using VT = march_vt<CPLX>;
   extern __shared__ __align__(128) unsigned char msm[];
   __shared__ __align__(8) uint64_t full[ST_NSMAX], empty[ST_NSMAX];
@@ -852,7 +857,7 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
   // ---------------- consumers: thread -> (tile row group, piece g)
   const int g = threadIdx.x % TPR, grp = threadIdx.x / TPR;
   constexpr int ZG = M_T / RZ;  // z groups per tile row
-  const int iy = grp / ZG, iz0 = (grp % ZG) * RZ;
+  const int iy = (grp / ZG) * RY, iz0 = (grp % ZG) * RZ;
   const int64_t plane = (int64_t)A.ny * A.nz;
   const int pc0 = g;  // first piece of this thread within the slice
   auto xrow = [&](int slot, int hy, int hz) {  // halo-tile row (hy, hz) of a slot, this thread's pieces
@@ -866,9 +871,10 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
   for (int u = blockIdx.x; u < A.nunits; u += gridDim.x) {
     const StUnit U = st_unit(A, u);
     const int pcs = U.s * (COLS / 2) + pc0;  // piece index in the row (from the slices' origin)
-    bool act[RZ];
+    bool act[NR];  // output (iy + i / RZ, iz0 + i % RZ)
 #pragma unroll
-    for (int i = 0; i < RZ; ++i) act[i] = U.y0 + iy < A.ny && U.z0 + iz0 + i < A.nz && pcs < A.npieces;
+    for (int i = 0; i < NR; ++i)
+      act[i] = U.y0 + iy + i / RZ < A.ny && U.z0 + iz0 + i % RZ < A.nz && pcs < A.npieces;
     const int nsteps = U.xb - U.xa;
     const int64_t rstep = U.dir * plane;
     int64_t row = ((int64_t)(U.dir > 0 ? U.xa : U.xb - 1) * A.ny + U.y0 + iy) * A.nz + U.z0 + iz0;
@@ -937,44 +943,71 @@ __global__ void __launch_bounds__(st_consumers<COLS, NP, RZ>() + 32, 1)
         mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
         bool any = false;
 #pragma unroll
-        for (int i = 0; i < RZ; ++i) any |= act[i];
+        for (int i = 0; i < NR; ++i) any |= act[i];
         if (any) {
           const double* ev = reinterpret_cast<const double*>(msm + (size_t)s2 * A.slot_bytes + A.vals_off) +
                              (iy * M_T + iz0) * A.vdoubles;
-          uint32_t mask[RZ];
+          // values of output i at ev + ((i / RZ) M_T + i % RZ) vdoubles
+          uint32_t mask[NR];
 #pragma unroll
-          for (int i = 0; i < RZ; ++i) mask[i] = (uint32_t)__double_as_longlong(ev[i * A.vdoubles + A.vdoubles - 1]);
-          double2 acc[RZ][NP];
+          for (int i = 0; i < NR; ++i)
+            mask[i] = (uint32_t)__double_as_longlong(ev[((i / RZ) * M_T + i % RZ) * A.vdoubles + A.vdoubles - 1]);
+          double2 acc[NR][NP];
 #pragma unroll
-          for (int i = 0; i < RZ; ++i)
+          for (int i = 0; i < NR; ++i)
 #pragma unroll
             for (int q = 0; q < NP; ++q) acc[i][q] = make_double2(0.0, 0.0);
 #pragma unroll
           for (int dxi = 0; dxi < 3; ++dxi) {
             const int sl = (U.dir > 0 ? kx + dxi : kx + 2 - dxi) % NS;  // plane x + dxi - 1
+            if constexpr (RY == 1) {
 #pragma unroll
-            for (int dyi = 0; dyi < 3; ++dyi) {
-              double2 v[RZ + 2][NP];
+              for (int dyi = 0; dyi < 3; ++dyi) {
+                double2 v[RZ + 2][NP];
 #pragma unroll
-              for (int j = 0; j < RZ + 2; ++j) ld(xrow(sl, iy + dyi, iz0 + j), v[j]);
+                for (int j = 0; j < RZ + 2; ++j) ld(xrow(sl, iy + dyi, iz0 + j), v[j]);
 #pragma unroll
-              for (int i = 0; i < RZ; ++i) {
-                const VT* av = reinterpret_cast<const VT*>(ev + i * A.vdoubles);
+                for (int i = 0; i < RZ; ++i) {
+                  const VT* av = reinterpret_cast<const VT*>(ev + i * A.vdoubles);
 #pragma unroll
-                for (int dzi = 0; dzi < 3; ++dzi) {
-                  const int s = dxi * 9 + dyi * 3 + dzi;
-                  if (!((mask[i] >> s) & 1u)) continue;
-                  const VT a = av[s];
+                  for (int dzi = 0; dzi < 3; ++dzi) {
+                    const int s = dxi * 9 + dyi * 3 + dzi;
+                    if (!((mask[i] >> s) & 1u)) continue;
+                    const VT a = av[s];
 #pragma unroll
-                  for (int q = 0; q < NP; ++q) st_fma<CPLX>(acc[i][q], a, v[i + dzi][q]);
+                    for (int q = 0; q < NP; ++q) st_fma<CPLX>(acc[i][q], a, v[i + dzi][q]);
+                  }
                 }
+              }
+            } else {
+              // the (RY + 2) x (RZ + 2) halo rows of the block once per plane: 3 (RY+2)(RZ+2) /
+              // (RY RZ) X loads per output row instead of 3 (RZ+2) (3 / RZ)
+              double2 v[RY + 2][RZ + 2][NP];
+#pragma unroll
+              for (int jy = 0; jy < RY + 2; ++jy)
+#pragma unroll
+                for (int jz = 0; jz < RZ + 2; ++jz) ld(xrow(sl, iy + jy, iz0 + jz), v[jy][jz]);
+#pragma unroll
+              for (int i = 0; i < NR; ++i) {
+                const int yi = i / RZ, zi = i % RZ;
+                const VT* av = reinterpret_cast<const VT*>(ev + (yi * M_T + zi) * A.vdoubles);
+#pragma unroll
+                for (int dyi = 0; dyi < 3; ++dyi)
+#pragma unroll
+                  for (int dzi = 0; dzi < 3; ++dzi) {
+                    const int s = dxi * 9 + dyi * 3 + dzi;
+                    if (!((mask[i] >> s) & 1u)) continue;
+                    const VT a = av[s];
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) st_fma<CPLX>(acc[i][q], a, v[yi + dyi][zi + dzi][q]);
+                  }
               }
             }
           }
 #pragma unroll
-          for (int i = 0; i < RZ; ++i)
+          for (int i = 0; i < NR; ++i)
             if (act[i]) {
-              double* yr = A.Y + (row + i) * A.ldy;
+              double* yr = A.Y + (row + (int64_t)(i / RZ) * A.nz + i % RZ) * A.ldy;
 #pragma unroll
               for (int q = 0; q < NP; ++q) march_store<CPLX>(A, yr, pcs + TPR * q, acc[i][q]);
             }
@@ -1068,14 +1101,12 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
     if (cfg == 1) {
       NCONS = st_consumers<32, 1, 4>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4> : spmm_stencil_kernel<false, 27, 32, 1, 4>;
-    } else if (cfg == 2) {  // two column pieces per thread: each stencil value feeds 4 FMAs
-      COLS = 64;
-      NCONS = st_consumers<64, 2, 2>();
-      kern = cplx ? spmm_stencil_kernel<true, 27, 64, 2, 2> : spmm_stencil_kernel<false, 27, 64, 2, 2>;
-    } else if (cfg == 3) {
-      COLS = 64;
-      NCONS = st_consumers<64, 2, 4>();
-      kern = cplx ? spmm_stencil_kernel<true, 27, 64, 2, 4> : spmm_stencil_kernel<false, 27, 64, 2, 4>;
+    } else if (cfg == 2) {  // 2 (y) x 2 (z) rows per thread
+      NCONS = st_consumers_y<32, 1, 2, 2>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2, 2>;
+    } else if (cfg == 3) {  // 2 (y) x 4 (z)
+      NCONS = st_consumers_y<32, 1, 4, 2>();
+      kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4, 2> : spmm_stencil_kernel<false, 27, 32, 1, 4, 2>;
     } else {
       NCONS = st_consumers<32, 1, 2>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2>;
