@@ -319,3 +319,40 @@ def test_ozaki_extreme_scales(cuda):
     prod = (x[rows].astype(np.longdouble) @ g.astype(np.longdouble)).astype(np.float64)
     bound = 4 * U * (np.abs(x[rows]) @ np.abs(g))
     assert np.all(np.abs(w.cpu().numpy()[rows] - prod) <= bound + 1e-320)
+
+
+@pytest.mark.parametrize("m1,m2", [(64, 64), (127, 129), (128, 64), (129, 200), (255, 65), (256, 256), (300, 64),
+                                   (65, 300)])
+def test_ozaki_gram_segments_edges(cuda, m1, m2):
+    """The Gram's segments (main 128 x 64 block, narrow right strip, bottom rows computed
+    transposed) at tile boundaries: every entry, the last rows and columns included, within
+    the DGEMM-class bound."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n = 16384
+    x, y = gauss(n, m1, 130 + m1), gauss(n, m2, 140 + m2)
+    with emu(torch):
+        c = K.gram(dev(x, torch), dev(y, torch)).cpu().numpy()
+    c1 = np.unique(np.r_[0, m1 // 2, np.arange(max(0, m1 - 12), m1)])
+    c2 = np.unique(np.r_[0, m2 // 2, np.arange(max(0, m2 - 12), m2)])
+    ref, absprod = exact_gram(x, y, c1, c2)
+    assert np.all(np.abs(c[np.ix_(c1, c2)] - ref) <= 4 * U * absprod)
+
+
+@pytest.mark.parametrize("m", [64, 127, 128, 129, 191, 192, 257])
+def test_ozaki_gram_symmetric_segments(cuda, m):
+    """Symmetric Grams: upper main tiles, the right strip and the diagonal corner, mirrored --
+    exactly symmetric, and the corner / strip entries within the bound."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n = 16384
+    xd = dev(gauss(n, m, 150 + m), torch)
+    with emu(torch):
+        g = K.gram(xd, xd, symmetric=True).cpu().numpy()
+    assert np.array_equal(g, g.T)
+    x = xd.cpu().numpy()
+    cs = np.unique(np.r_[0, m // 2, np.arange(max(0, m - 12), m)])
+    ref, absprod = exact_gram(x, x, cs, cs)
+    assert np.all(np.abs(g[np.ix_(cs, cs)] - ref) <= 4 * U * absprod)
