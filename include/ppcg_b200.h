@@ -199,6 +199,11 @@ int bk_cplx_expand_d(int K, int N, const double* G, int64_t ldg, double* Gr, int
  *      the DMMA or the emulated kernels in the host layer (default: PPCG_FP64_EMU, else on). */
 int bk_fp64_emu_set(int mode);
 int bk_fp64_emu_enabled(void);
+/* CUDA-event timing of the emulated GEMM-core launches (digit slicing excluded), for the
+ * roofline: bk_ozaki_timing(1) arms and clears, bk_ozaki_kernel_ms() syncs and returns the summed
+ * milliseconds of the launches since (up to 16), bk_ozaki_timing(0) disarms. */
+int bk_ozaki_timing(int on);
+double bk_ozaki_kernel_ms(void);
 /* ws bytes for one call (same: X and Y are one block; symmetric requires same).  A smaller ws
  * (>= the size for one row chunk) is accepted: rows are then sliced in super-chunks. */
 int64_t bk_ozaki_gram_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric);

@@ -84,6 +84,8 @@ _SIGS = {
     "bk_cplx_expand_d": (c_int, [c_int, c_int, vp, c_i64, vp, c_i64, vp]),
     "bk_fp64_emu_set": (c_int, [c_int]),
     "bk_fp64_emu_enabled": (c_int, []),
+    "bk_ozaki_timing": (c_int, [c_int]),
+    "bk_ozaki_kernel_ms": (c_dbl, []),
     "bk_ozaki_gram_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int, c_int]),
     "bk_ozaki_gram_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp]),
     "bk_ozaki_gram2_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int]),

@@ -936,6 +936,32 @@ static bool encode_digits(CUtensorMap* map, const int8_t* base, int64_t kld, int
 
 static int g_emu_mode = -1;  // -1: from PPCG_FP64_EMU (default on), 0 off, 1 on
 
+// optional CUDA-event timing of the GEMM-core launches (k_oz_gram / k_oz_ts) on their stream,
+// for bench.py's roofline (the kernel's own duration, digit slicing excluded)
+struct OzTimer {
+  int on = 0;
+  int n = 0;
+  cudaEvent_t ev[16][2];
+  bool made = false;
+  void begin(cudaStream_t st) {
+    if (!on) return;
+    if (!made) {
+      for (auto& e : ev) {
+        cudaEventCreate(&e[0]);
+        cudaEventCreate(&e[1]);
+      }
+      made = true;
+    }
+    if (n < 16) cudaEventRecord(ev[n][0], st);
+  }
+  void end(cudaStream_t st) {
+    if (!on) return;
+    if (n < 16) cudaEventRecord(ev[n][1], st);
+    ++n;
+  }
+};
+static OzTimer g_timer;
+
 static int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 // rows per chunk: <= MAX_CHUNK, a multiple of KB, chosen for whole waves of 148 CTAs
@@ -1153,8 +1179,10 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
       for (int j = na; j < 4; ++j) mapsA[j] = mapsA[0];
       for (int j = nb; j < 4; ++j) mapsB[j] = mapsB[0];
       BK_COUNT();
+      g_timer.begin(st);
       k_oz_gram<<<dim3(G.ntiles, nch), THREADS, SMEM, st>>>(mapsA[0], mapsA[1], mapsA[2], mapsA[3], mapsB[0],
                                                             mapsB[1], mapsB[2], mapsB[3], P);
+      g_timer.end(st);
       BK_CHECK_LAUNCH();
       BK_COUNT();
       k_gram_reduce<<<dim3(G.ntiles, 16), 512, 0, st>>>(P, nch, C[q], ldc[q], r0 > 0 ? 1 : 0);
@@ -1173,6 +1201,26 @@ using namespace bk::oz;
 extern "C" int bk_fp64_emu_set(int mode) {
   g_emu_mode = mode;
   return BK_OK;
+}
+
+// Kernel timing: bk_ozaki_timing(1) clears and arms the CUDA-event pairs recorded around each
+// GEMM-core launch; bk_ozaki_kernel_ms() waits for them and returns the summed milliseconds of
+// the launches since (up to 16); bk_ozaki_timing(0) disarms.
+extern "C" int bk_ozaki_timing(int on) {
+  g_timer.on = on;
+  g_timer.n = 0;
+  return BK_OK;
+}
+
+extern "C" double bk_ozaki_kernel_ms(void) {
+  double t = 0.0;
+  const int n = g_timer.n < 16 ? g_timer.n : 16;
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_timer.ev[i][1]);
+    if (cudaEventElapsedTime(&ms, g_timer.ev[i][0], g_timer.ev[i][1]) == cudaSuccess) t += ms;
+  }
+  return t;
 }
 
 extern "C" int bk_fp64_emu_enabled(void) {
@@ -1377,12 +1425,14 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
     const int64_t tiles = (int64_t)ctn * rtn * nprob;
     const int grid = (int)lmin(tiles, kSMs);
     BK_COUNT();
+    g_timer.begin(st);
     if (tbn == 32)
       k_oz_ts<32><<<grid, TS_THREADS, ts_smem<32>(), st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P,
                                                           ctn, rtn, nprob);
     else
       k_oz_ts<64><<<grid, TS_THREADS, ts_smem<64>(), st>>>(mA[0], mA[1], mA[2], mA[3], mB[0], mB[1], mB[2], mB[3], P,
                                                           ctn, rtn, nprob);
+    g_timer.end(st);
     {
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {

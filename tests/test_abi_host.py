@@ -17,7 +17,7 @@ LIB = os.path.join(ROOT, "paper_1407_7506_b200", "libppcg_b200.so")
 
 def declared_symbols():
     text = open(HDR).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|unsigned long long)\s+(bk_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|double|unsigned long long)\s+(bk_\w+)\s*\(", text, re.M)))
 
 
 @pytest.mark.skipif(not os.path.exists(LIB), reason="library not built (run make)")
