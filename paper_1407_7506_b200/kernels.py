@@ -515,15 +515,18 @@ def _par_rows(fn, r0, r1, row_bytes, min_bytes=1 << 20):
         f.result()
 
 
-def to_host(x, chunk_bytes=32 << 20):
+def to_host(x, chunk_bytes=32 << 20, out=None):
     """numpy copy of a (possibly row-strided) 2-D device block through two pinned staging
     buffers: the device->pinned copy of one row chunk overlaps the (multi-threaded)
     pinned->numpy copy of the previous one (a pageable .cpu() of a large block runs at a
-    few GB/s)."""
+    few GB/s).  ``out``: a C-contiguous destination of the right shape / dtype (e.g. one
+    whose pages were faulted in ahead of time)."""
     import numpy as np
 
     n, m = x.shape
-    out = np.empty((n, m), dtype=np.complex128 if x.dtype == C128 else np.float64)
+    dt = np.complex128 if x.dtype == C128 else np.float64
+    if out is None or out.shape != (n, m) or out.dtype != dt or not out.flags.c_contiguous:
+        out = np.empty((n, m), dtype=dt)
     if n == 0 or m == 0:
         return out
     rb = m * x.element_size()
