@@ -214,6 +214,23 @@ int64_t bk_ozaki_gram2_ws_bytes(int64_t n, int m1, int m2a, int m2b);
 int bk_ozaki_gram2_d(int64_t n, int m1, const double* X, int64_t ldx, int m2a, const double* Ya, int64_t ldya,
                      double* Ca, int64_t ldca, int m2b, const double* Yb, int64_t ldyb, double* Cb, int64_t ldcb,
                      void* ws, int64_t ws_bytes, void* stream);
+/* Column digits kept between products.  One block is the left operand of several Grams of an
+ * iteration -- X^H AX (ppcg.py:630/758), the projections X^H W / X^H P (680-687), proj_defect
+ * (688-692) -- so its exponents and digits are computed once into a caller-owned buffer
+ * (bk_ozaki_coldigits_bytes(n, m) bytes) and the *_pre_d Grams read them: X there is columns
+ * [c0, c0 + m1) of the sliced n x mdig block.  Same results as the plain entries bit for bit
+ * (the digits are the same); the pre-sliced operand is never re-sliced in row super-chunks, so
+ * ws holds the other operand's digits of all rows (*_pre_ws_bytes). */
+int64_t bk_ozaki_coldigits_bytes(int64_t n, int m);
+int bk_ozaki_coldigits_d(int64_t n, int m, const double* X, int64_t ldx, void* dig, int64_t dig_bytes, void* stream);
+int64_t bk_ozaki_gram_pre_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric);
+int bk_ozaki_gram_pre_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const void* dig, int mdig, int c0,
+                        const double* Y, int64_t ldy, double* C, int64_t ldc, int symmetric, void* ws,
+                        int64_t ws_bytes, void* stream);
+int64_t bk_ozaki_gram2_pre_ws_bytes(int64_t n, int m1, int m2a, int m2b);
+int bk_ozaki_gram2_pre_d(int64_t n, int m1, const double* X, int64_t ldx, const void* dig, int mdig, int c0, int m2a,
+                         const double* Ya, int64_t ldya, double* Ca, int64_t ldca, int m2b, const double* Yb,
+                         int64_t ldyb, double* Cb, int64_t ldcb, void* ws, int64_t ws_bytes, void* stream);
 /* K <= 16320; flags bit0: G upper triangular (k stages below a column tile are skipped) */
 int64_t bk_ozaki_tsgemm_ws_bytes(int nprob, int64_t n, int K, int N, int ksplit);
 int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alpha, const double* const* Xs, int64_t ldx,

@@ -91,6 +91,14 @@ _SIGS = {
     "bk_ozaki_gram2_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int]),
     "bk_ozaki_gram2_d": (c_int, [c_i64, c_int, vp, c_i64, c_int, vp, c_i64, vp, c_i64, c_int, vp, c_i64, vp, c_i64,
                                  vp, c_i64, vp]),
+    "bk_ozaki_coldigits_bytes": (c_i64, [c_i64, c_int]),
+    "bk_ozaki_coldigits_d": (c_int, [c_i64, c_int, vp, c_i64, vp, c_i64, vp]),
+    "bk_ozaki_gram_pre_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int, c_int]),
+    "bk_ozaki_gram_pre_d": (c_int, [c_i64, c_int, c_int, vp, c_i64, vp, c_int, c_int, vp, c_i64, vp, c_i64, c_int, vp,
+                                    c_i64, vp]),
+    "bk_ozaki_gram2_pre_ws_bytes": (c_i64, [c_i64, c_int, c_int, c_int]),
+    "bk_ozaki_gram2_pre_d": (c_int, [c_i64, c_int, vp, c_i64, vp, c_int, c_int, c_int, vp, c_i64, vp, c_i64, c_int, vp,
+                                     c_i64, vp, c_i64, vp, c_i64, vp]),
     "bk_ozaki_tsgemm_ws_bytes": (c_i64, [c_int, c_i64, c_int, c_int, c_int]),
     "bk_ozaki_tsgemm_d": (c_int, [c_int, c_i64, c_int, c_int, c_dbl, PP, c_i64, PP, c_i64, c_dbl, PP, c_i64, PP,
                                   c_i64, vp, c_int, c_int, c_int, vp, vp, c_i64, vp]),

@@ -1045,7 +1045,9 @@ struct GramLayout {
 };
 
 // same: B operand q is X itself (one set of digits); sym (requires same): symmetric segments
-static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const int* same, int sym, int64_t ws_cap) {
+// preA: X's digits come pre-sliced from the caller (all rows: one super-chunk, no cap)
+static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const int* same, int sym, int64_t ws_cap,
+                              int preA = 0) {
   GramLayout L{};
   L.nq = nq;
   int tt = 0;
@@ -1056,7 +1058,7 @@ static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const in
   L.chunk_rows = gram_chunk_rows(n, tt);
   // digits of at most ~1.5 GB at once (or what the caller's workspace holds)
   int64_t sc_chunks = (n + L.chunk_rows - 1) / L.chunk_rows;
-  const int64_t cap = ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
+  const int64_t cap = preA ? ((int64_t)1 << 62) : ws_cap > 0 ? ws_cap : ((int64_t)3 << 29);
   auto layout = [&](int64_t chunks) {
     const int64_t rows = chunks * L.chunk_rows;
     int64_t o = 0;
@@ -1067,7 +1069,7 @@ static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const in
       L.off_EB[q] = o;  o += align_up(4 * (int64_t)m2[q], 256);
       L.off_part[q] = o; o += align_up(chunks * L.plan[q].part_per_chunk * 8, 1024);
     }
-    L.off_sA = o; o += align_up((int64_t)S * m1 * rows, 1024);
+    L.off_sA = o; o += preA ? 0 : align_up((int64_t)S * m1 * rows, 1024);
     for (int q = 0; q < nq; ++q) {
       L.off_sB[q] = o;
       o += same[q] ? 0 : align_up((int64_t)S * m2[q] * rows, 1024);
@@ -1080,18 +1082,40 @@ static GramLayout gram_layout(int64_t n, int m1, int nq, const int* m2, const in
   return L;
 }
 
-// C_q = X^T Y_q for nq <= 2 operands Y_q that share X's digits
+// Column digits kept by the caller between products (bk_ozaki_coldigits_d): exponents E[m],
+// digits [S][m][kld] of all n rows, kld = align_up(n, KPAD)
+struct ColDigits {
+  const int* E;
+  const int8_t* dig;
+  int64_t kld;
+  int m;
+};
+static int64_t coldigits_hdr(int m) { return align_up(8 * (int64_t)m, 256) + align_up(4 * (int64_t)m, 256); }
+static ColDigits coldigits_view(void* buf, int64_t n, int m) {
+  char* w = static_cast<char*>(buf);
+  ColDigits d;
+  d.E = reinterpret_cast<const int*>(w + align_up(8 * (int64_t)m, 256));
+  d.dig = reinterpret_cast<const int8_t*>(w + coldigits_hdr(m));
+  d.kld = align_up(n, KPAD);
+  d.m = m;
+  return d;
+}
+
+// C_q = X^T Y_q for nq <= 2 operands Y_q that share X's digits; pre (optional): the digits of
+// the block whose columns [pre_c0, pre_c0 + m1) are X
 static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int nq, const int* m2,
                             const double* const* Y, const int64_t* ldy, double* const* C, const int64_t* ldc,
-                            int symmetric, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                            int symmetric, void* ws, int64_t ws_bytes, cudaStream_t st,
+                            const ColDigits* pre = nullptr, int pre_c0 = 0) {
   if (n <= 0 || m1 <= 0 || !X) return BK_ERR_ARG;
+  if (pre && (pre_c0 < 0 || pre_c0 + m1 > pre->m)) return BK_ERR_ARG;
   int same[2] = {0, 0};
   for (int q = 0; q < nq; ++q) {
     if (m2[q] <= 0 || !Y[q] || !C[q]) return BK_ERR_ARG;
     same[q] = (X == Y[q] && ldx == ldy[q] && m1 == m2[q]) ? 1 : 0;
     if (symmetric && !same[q]) return BK_ERR_ARG;
   }
-  const GramLayout L = gram_layout(n, m1, nq, m2, same, symmetric, ws_bytes);
+  const GramLayout L = gram_layout(n, m1, nq, m2, same, symmetric, ws_bytes, pre ? 1 : 0);
   if (!ws || ws_bytes < L.total) return BK_ERR_ARG;
   char* w = static_cast<char*>(ws);
   auto* cmA = reinterpret_cast<unsigned long long*>(w + L.off_cmA);
@@ -1099,12 +1123,17 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
   int8_t* sA = reinterpret_cast<int8_t*>(w + L.off_sA);
   int* EB[2];
   int8_t* sB[2];
-  // exponents over all rows
-  cudaMemsetAsync(cmA, 0, 8 * (size_t)m1, st);
-  BK_COUNT();
-  k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
-  BK_COUNT();
-  k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA, nullptr);
+  if (pre) {
+    EA = const_cast<int*>(pre->E) + pre_c0;
+    sA = const_cast<int8_t*>(pre->dig) + (int64_t)pre_c0 * pre->kld;
+  } else {
+    // exponents over all rows
+    cudaMemsetAsync(cmA, 0, 8 * (size_t)m1, st);
+    BK_COUNT();
+    k_colmax<<<dim3((unsigned)((n + 63) / 64), (m1 + 255) / 256), 256, 0, st>>>(n, m1, X, ldx, cmA);
+    BK_COUNT();
+    k_exponents<<<(m1 + 255) / 256, 256, 0, st>>>(m1, cmA, EA, nullptr);
+  }
   for (int q = 0; q < nq; ++q) {
     EB[q] = same[q] ? EA : reinterpret_cast<int*>(w + L.off_EB[q]);
     sB[q] = same[q] ? sA : reinterpret_cast<int8_t*>(w + L.off_sB[q]);
@@ -1125,9 +1154,12 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
     const int64_t rows = lmin(L.sc_rows, n - r0);
     const int64_t kld = align_up(rows, KPAD);
     const unsigned gx = (unsigned)((rows + 127) / 128);
-    BK_COUNT();
-    k_slice_cols<<<dim3(gx, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
-                                                           kld * (int64_t)m1, kld);
+    if (!pre) {
+      BK_COUNT();
+      k_slice_cols<<<dim3(gx, (m1 + 31) / 32), 256, 0, st>>>(r0 + rows, m1, X, ldx, EA, r0, sA, kld,
+                                                             kld * (int64_t)m1, kld);
+    }
+    const int64_t strideA = pre ? kld * (int64_t)pre->m : kld * (int64_t)m1;  // between digit planes
     const int nch = (int)((rows + L.chunk_rows - 1) / L.chunk_rows);
     for (int q = 0; q < nq; ++q) {
       if (!same[q]) {
@@ -1139,6 +1171,7 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
       const GramPlan& G = L.plan[q];
       const int8_t* dig[2] = {sA, sB[q]};
       const int mcols[2] = {m1, m2[q]};
+      const int64_t dstride[2] = {strideA, same[q] ? strideA : kld * (int64_t)m2[q]};
       const int* ex[2] = {EA, EB[q]};
       CUtensorMap mapsA[4], mapsB[4];
       int keyA[4], keyB[4], na = 0, nb = 0;
@@ -1163,14 +1196,14 @@ static int ozaki_gram_multi(int64_t n, int m1, const double* X, int64_t ldx, int
         if (ia < 0) {
           ia = na++;
           keyA[ia] = ka;
-          if (!encode_digits(&mapsA[ia], dig[ka], kld, rows, mcols[ka], BM, kld * (int64_t)mcols[ka]))
+          if (!encode_digits(&mapsA[ia], dig[ka], kld, rows, mcols[ka], BM, dstride[ka]))
             return BK_ERR_UNSUPPORTED;
         }
         if (ib < 0) {
           ib = nb++;
           keyB[ib] = kbk;
           const int ob = G.opB[i];
-          if (!encode_digits(&mapsB[ib], dig[ob], kld, rows, mcols[ob], G.seg[i].tbn, kld * (int64_t)mcols[ob]))
+          if (!encode_digits(&mapsB[ib], dig[ob], kld, rows, mcols[ob], G.seg[i].tbn, dstride[ob]))
             return BK_ERR_UNSUPPORTED;
         }
         P.seg[i].mapA = ia;
@@ -1264,6 +1297,72 @@ extern "C" int bk_ozaki_gram2_d(int64_t n, int m1, const double* X, int64_t ldx,
   const int64_t lds[2] = {ldya, ldyb}, ldcs[2] = {ldca, ldcb};
   double* Cs[2] = {Ca, Cb};
   return ozaki_gram_multi(n, m1, X, ldx, 2, m2s, Ys, lds, Cs, ldcs, 0, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// ---- column digits kept between products: the same block is the left operand of several Grams
+// of an iteration (X^H AX, the projections X^H W / X^H P, proj_defect), so its exponents and
+// digits are computed once (bk_ozaki_coldigits_d) and handed to the *_pre_d Grams together with
+// the column offset of the operand inside the sliced block.
+extern "C" int64_t bk_ozaki_coldigits_bytes(int64_t n, int m) {
+  if (n <= 0 || m <= 0) return 0;
+  return coldigits_hdr(m) + align_up((int64_t)S * m * align_up(n, KPAD), 1024);
+}
+
+extern "C" int bk_ozaki_coldigits_d(int64_t n, int m, const double* X, int64_t ldx, void* dig, int64_t dig_bytes,
+                                    void* stream) {
+  if (n <= 0 || m <= 0 || !X || !dig || dig_bytes < bk_ozaki_coldigits_bytes(n, m)) return BK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const ColDigits d = coldigits_view(dig, n, m);
+  auto* cm = reinterpret_cast<unsigned long long*>(dig);
+  cudaMemsetAsync(cm, 0, 8 * (size_t)m, st);
+  BK_COUNT();
+  k_colmax<<<dim3((unsigned)((n + 63) / 64), (m + 255) / 256), 256, 0, st>>>(n, m, X, ldx, cm);
+  BK_COUNT();
+  k_exponents<<<(m + 255) / 256, 256, 0, st>>>(m, cm, const_cast<int*>(d.E), nullptr);
+  BK_COUNT();
+  k_slice_cols<<<dim3((unsigned)((n + 127) / 128), (m + 31) / 32), 256, 0, st>>>(
+      n, m, X, ldx, d.E, 0, const_cast<int8_t*>(d.dig), d.kld, d.kld * (int64_t)m, d.kld);
+  BK_CHECK_LAUNCH();
+  return BK_OK;
+}
+
+extern "C" int64_t bk_ozaki_gram_pre_ws_bytes(int64_t n, int m1, int m2, int same, int symmetric) {
+  if (n <= 0 || m1 <= 0 || m2 <= 0) return 0;
+  const int m2s[1] = {m2}, sm[1] = {same};
+  return gram_layout(n, m1, 1, m2s, sm, symmetric, 0, 1).total;
+}
+
+// bk_ozaki_gram_d with X = columns [c0, c0 + m1) of the block (n x mdig) whose digits are `dig`
+extern "C" int bk_ozaki_gram_pre_d(int64_t n, int m1, int m2, const double* X, int64_t ldx, const void* dig, int mdig,
+                                   int c0, const double* Y, int64_t ldy, double* C, int64_t ldc, int symmetric,
+                                   void* ws, int64_t ws_bytes, void* stream) {
+  if (!dig || mdig <= 0) return BK_ERR_ARG;
+  const ColDigits d = coldigits_view(const_cast<void*>(dig), n, mdig);
+  const int m2s[1] = {m2};
+  const double* Ys[1] = {Y};
+  const int64_t lds[1] = {ldy}, ldcs[1] = {ldc};
+  double* Cs[1] = {C};
+  return ozaki_gram_multi(n, m1, X, ldx, 1, m2s, Ys, lds, Cs, ldcs, symmetric, ws, ws_bytes, (cudaStream_t)stream, &d,
+                          c0);
+}
+
+extern "C" int64_t bk_ozaki_gram2_pre_ws_bytes(int64_t n, int m1, int m2a, int m2b) {
+  if (n <= 0 || m1 <= 0 || m2a <= 0 || m2b <= 0) return 0;
+  const int m2s[2] = {m2a, m2b}, sm[2] = {0, 0};
+  return gram_layout(n, m1, 2, m2s, sm, 0, 0, 1).total;
+}
+
+extern "C" int bk_ozaki_gram2_pre_d(int64_t n, int m1, const double* X, int64_t ldx, const void* dig, int mdig, int c0,
+                                    int m2a, const double* Ya, int64_t ldya, double* Ca, int64_t ldca, int m2b,
+                                    const double* Yb, int64_t ldyb, double* Cb, int64_t ldcb, void* ws,
+                                    int64_t ws_bytes, void* stream) {
+  if (!dig || mdig <= 0) return BK_ERR_ARG;
+  const ColDigits d = coldigits_view(const_cast<void*>(dig), n, mdig);
+  const int m2s[2] = {m2a, m2b};
+  const double* Ys[2] = {Ya, Yb};
+  const int64_t lds[2] = {ldya, ldyb}, ldcs[2] = {ldca, ldcb};
+  double* Cs[2] = {Ca, Cb};
+  return ozaki_gram_multi(n, m1, X, ldx, 2, m2s, Ys, lds, Cs, ldcs, 0, ws, ws_bytes, (cudaStream_t)stream, &d, c0);
 }
 
 // ---- tall GEMM: Y_b = s (.) (alpha X_b G_b + beta Z_b), b < nprob <= 4 (semantics of

@@ -381,6 +381,7 @@ struct MarchArgs {
   int gy, gz, nslices, xseg, nunits;
   int m, off;          // columns, and leading columns of the slices before column 0 (alignment)
   int order;           // stencil-slot unit order: 0 = slice fastest, 1 = (y, z) tile fastest
+  int nodir;           // stencil-slot: every x segment marches upward (plane-holding variants)
   int npieces;         // 16-byte pieces of a row from the slices' origin to the block's end
   int vdoubles;        // ELL value row in doubles (real: even width; complex: 2 x width)
   int woff;            // ELL offset row in uint16 (multiple of 8)
@@ -625,6 +626,7 @@ static int march_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, int
   if (nx == 0 || m == 0) return BK_OK;
   cudaStream_t st = (cudaStream_t)stream;
   MarchArgs A;
+  A.nodir = 0;
   A.nx = nx;
   A.ny = ny;
   A.nz = nz;
@@ -786,7 +788,7 @@ BK_DEV StUnit st_unit(const MarchArgs& A, int u) {
   U.y0 = (tile / A.gz) * M_T;
   U.xa = (int)((int64_t)seg * A.nx / A.xseg);
   U.xb = (int)((int64_t)(seg + 1) * A.nx / A.xseg);
-  U.dir = (seg & 1) ? -1 : 1;
+  U.dir = (seg & 1) && !A.nodir ? -1 : 1;
   return U;
 }
 
@@ -810,12 +812,13 @@ BK_DEV void st_fma(double2& acc, march_vt<CPLX> a, double2 v) {
   }
 }
 
-template <bool CPLX, int ST, int COLS, int NP, int RZ, int RY = 1>
+template <bool CPLX, int ST, int COLS, int NP, int RZ, int RY = 1, int HOLD = 0>
 __global__ void __launch_bounds__(st_consumers_y<COLS, NP, RZ, RY>() + 32, 1)
     spmm_stencil_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
                         MarchArgs A) {
   static_assert(ST == 7 || ST == 27, "stencil");
   static_assert(ST == 27 || (RZ == 1 && RY == 1), "7-point: one row per thread");
+  static_assert(HOLD == 0 || (ST == 27 && RY == 1), "plane holding: 27-point, z row blocks");
   constexpr int TPR = COLS / 2 / NP;  // threads per row (16-byte pieces g + TPR k)
   constexpr int NCONS = st_consumers_y<COLS, NP, RZ, RY>();
   constexpr int NR = RY * RZ;         // output rows per thread: RY (y) x RZ (z) block
@@ -934,6 +937,142 @@ __global__ void __launch_bounds__(st_consumers_y<COLS, NP, RZ, RY>() + 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[kl % NS]);
       k = kl + 1;
+    } else if constexpr (HOLD > 0) {
+      // 27-point with X planes held in registers across the march (always upward).  HOLD = 1:
+      // plane x stays in registers from the step that loaded it as x + 1, so a step reads two
+      // planes from shared memory (x - 1 line by line, x + 1 into the held array once plane
+      // x's FMAs are done).  HOLD = 2: planes x - 1 and x are both held (two arrays swapping
+      // roles, the loop unrolled by two), a step reads only plane x + 1 -- into the array
+      // plane x - 1 has just left -- and a ring slot is released by the step that loaded it.
+      // The real values of a row are read as 16-byte pairs (14 loads for 27 slots + mask).
+      double2 pa[3][RZ + 2][NP];
+      double2 pb[HOLD == 2 ? 3 : 1][HOLD == 2 ? RZ + 2 : 1][NP];
+      auto ldline = [&](int slot, int dyi, double2 (&v)[RZ + 2][NP]) {
+#pragma unroll
+        for (int j = 0; j < RZ + 2; ++j) ld(xrow(slot, iy + dyi, iz0 + j), v[j]);
+      };
+      // the three values (dz = -1, 0, 1) of slot group s0 = 9 dx + 3 dy of one row
+      auto vals3 = [&](const double* evi, int s0, double2& carry, VT (&a)[3]) {
+        const double2* av = reinterpret_cast<const double2*>(evi);
+        if constexpr (CPLX) {
+          a[0] = av[s0];
+          a[1] = av[s0 + 1];
+          a[2] = av[s0 + 2];
+        } else if (s0 & 1) {  // (s0 - 1, s0) came with the previous group
+          const double2 t = av[(s0 + 1) >> 1];
+          a[0] = carry.y;
+          a[1] = t.x;
+          a[2] = t.y;
+        } else {
+          const double2 t = av[s0 >> 1];
+          carry = av[(s0 >> 1) + 1];
+          a[0] = t.x;
+          a[1] = t.y;
+          a[2] = carry.x;
+        }
+      };
+      auto fma_line = [&](const double* ev, const uint32_t (&mask)[RZ], double2 (&carry)[RZ], int dxi, int dyi,
+                          const double2 (&v)[RZ + 2][NP], double2 (&acc)[RZ][NP]) {
+#pragma unroll
+        for (int i = 0; i < RZ; ++i) {
+          VT a[3];
+          vals3(ev + i * A.vdoubles, dxi * 9 + dyi * 3, carry[i], a);
+#pragma unroll
+          for (int dzi = 0; dzi < 3; ++dzi) {
+            if (!((mask[i] >> (dxi * 9 + dyi * 3 + dzi)) & 1u)) continue;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) st_fma<CPLX>(acc[i][q], a[dzi], v[i + dzi][q]);
+          }
+        }
+      };
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) any |= act[i];
+      // one step: plane x - 1 = `prev` (HOLD 2) or ring slot s0 (HOLD 1), plane x = `cur`, plane
+      // x + 1 from ring slot s2 into `prev` (HOLD 2) / `cur` (HOLD 1)
+      auto step = [&](int i, double2 (&prev)[3][RZ + 2][NP], double2 (&cur)[3][RZ + 2][NP]) {
+        const int kx = k + i;  // load index of plane x - 1
+        const int s0 = kx % NS, s2 = (kx + 2) % NS;
+        mbar_wait(&full[s2], ((kx + 2) / NS) & 1);
+        if (any) {
+          const double* ev = reinterpret_cast<const double*>(msm + (size_t)s2 * A.slot_bytes + A.vals_off) +
+                             (iy * M_T + iz0) * A.vdoubles;
+          uint32_t mask[RZ];
+          double2 carry[RZ];
+          double2 acc[RZ][NP];
+#pragma unroll
+          for (int r = 0; r < RZ; ++r) {
+            mask[r] = (uint32_t)__double_as_longlong(ev[r * A.vdoubles + A.vdoubles - 1]);
+            carry[r] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < NP; ++q) acc[r][q] = make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int dyi = 0; dyi < 3; ++dyi) {
+            if constexpr (HOLD == 2) {
+              fma_line(ev, mask, carry, 0, dyi, prev[dyi], acc);
+            } else {
+              double2 v[RZ + 2][NP];
+              ldline(s0, dyi, v);
+              fma_line(ev, mask, carry, 0, dyi, v, acc);
+            }
+          }
+          if constexpr (HOLD == 2) {
+#pragma unroll
+            for (int dyi = 0; dyi < 3; ++dyi) ldline(s2, dyi, prev[dyi]);
+          }
+#pragma unroll
+          for (int dyi = 0; dyi < 3; ++dyi) fma_line(ev, mask, carry, 1, dyi, cur[dyi], acc);
+#pragma unroll
+          for (int dyi = 0; dyi < 3; ++dyi) {
+            if constexpr (HOLD == 2) {
+              fma_line(ev, mask, carry, 2, dyi, prev[dyi], acc);
+            } else {
+              ldline(s2, dyi, cur[dyi]);
+              fma_line(ev, mask, carry, 2, dyi, cur[dyi], acc);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < RZ; ++r)
+            if (act[r]) {
+              double* yr = A.Y + (row + r) * A.ldy;
+#pragma unroll
+              for (int q = 0; q < NP; ++q) march_store<CPLX>(A, yr, pcs + TPR * q, acc[r][q]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[HOLD == 2 ? s2 : s0]);
+        row += rstep;
+      };
+      mbar_wait(&full[k % NS], (k / NS) & 1);
+      mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
+      if constexpr (HOLD == 2) {
+#pragma unroll
+        for (int dyi = 0; dyi < 3; ++dyi) {
+          ldline(k % NS, dyi, pa[dyi]);
+          ldline((k + 1) % NS, dyi, pb[dyi]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[k % NS]);
+          mbar_arrive(&empty[(k + 1) % NS]);
+        }
+        for (int i = 0; i < nsteps; i += 2) {
+          step(i, pa, pb);
+          if (i + 1 < nsteps) step(i + 1, pb, pa);
+        }
+      } else {
+#pragma unroll
+        for (int dyi = 0; dyi < 3; ++dyi) ldline((k + 1) % NS, dyi, pa[dyi]);
+        for (int i = 0; i < nsteps; ++i) step(i, pa, pa);
+        const int kl = k + nsteps;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[kl % NS]);
+          mbar_arrive(&empty[(kl + 1) % NS]);
+        }
+      }
+      k += nsteps + 2;
     } else {
       mbar_wait(&full[k % NS], (k / NS) & 1);
       mbar_wait(&full[(k + 1) % NS], ((k + 1) / NS) & 1);
@@ -1059,6 +1198,7 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
   A.xlo = xlo;
   A.width = st;
   A.woff = 0;
+  A.nodir = 0;
   A.m = m;
   A.vdoubles = vd;
   const double* xbase;
@@ -1107,6 +1247,21 @@ static int stencil_launch(bool cplx, int nx, int ny, int nz, int xlo, int xhi, i
     } else if (cfg == 3) {  // 2 (y) x 4 (z)
       NCONS = st_consumers_y<32, 1, 4, 2>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4, 2> : spmm_stencil_kernel<false, 27, 32, 1, 4, 2>;
+    } else if (cfg >= 4 && cfg <= 7) {  // planes held in registers: (RZ, HOLD) = (2,1) (2,2) (4,1) (4,2)
+      A.nodir = 1;
+      if (cfg == 4) {
+        NCONS = st_consumers<32, 1, 2>();
+        kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2, 1, 1> : spmm_stencil_kernel<false, 27, 32, 1, 2, 1, 1>;
+      } else if (cfg == 5) {
+        NCONS = st_consumers<32, 1, 2>();
+        kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2, 1, 2>;
+      } else if (cfg == 6) {
+        NCONS = st_consumers<32, 1, 4>();
+        kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4, 1, 1> : spmm_stencil_kernel<false, 27, 32, 1, 4, 1, 1>;
+      } else {
+        NCONS = st_consumers<32, 1, 4>();
+        kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 4, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 4, 1, 2>;
+      }
     } else {
       NCONS = st_consumers<32, 1, 2>();
       kern = cplx ? spmm_stencil_kernel<true, 27, 32, 1, 2> : spmm_stencil_kernel<false, 27, 32, 1, 2>;

@@ -62,17 +62,21 @@ class FlatDraw:
         self.count = count
         self.segs = segs
 
+    def _resolve(self, upto):
+        return self.segs
+
     def copy_range(self, a, b, dst):
         """dst[:] = output[a:b] (dst: 1-D float64 view of length b - a)."""
-        for i0, i1, arr, j0 in self.segs:
+        for i0, i1, arr, j0 in self._resolve(b):
             lo, hi = max(a, i0), min(b, i1)
             if lo < hi:
                 dst[lo - a:hi - a] = arr[j0 + lo - i0:j0 + hi - i0]
 
     def array(self, threads=None):
         out = np.empty(self.count)
-        if len(self.segs) == 1:
-            i0, i1, arr, j0 = self.segs[0]
+        segs = self._resolve(self.count)
+        if len(segs) == 1:
+            i0, i1, arr, j0 = segs[0]
             out[:] = arr[j0:j0 + i1 - i0]
             return out
 
@@ -80,65 +84,108 @@ class FlatDraw:
             i0, i1, arr, j0 = sg
             out[i0:i1] = arr[j0:j0 + i1 - i0]
 
-        with ThreadPoolExecutor(max_workers=min(len(self.segs), threads or _threads())) as ex:
-            list(ex.map(copy, self.segs))
+        with ThreadPoolExecutor(max_workers=min(len(segs), threads or _threads())) as ex:
+            list(ex.map(copy, segs))
         return out
 
 
+class ChainedDraw(FlatDraw):
+    """FlatDraw whose chains are still being drawn: the chunks run on a thread pool in stream
+    order (several per thread), and a range of the output becomes available once the chunks
+    up to the one after it are drawn and spliced -- so an upload of the first rows overlaps
+    the draw of the later ones.  ``_resolve(upto)`` blocks until output [0, upto) is covered."""
+
+    def __init__(self, seed, count, nchunk, M, extra, bufs, threads):
+        self.count, self.seed, self.nchunk = count, seed, nchunk
+        self.segs = []
+        self._starts = [(0, 0)]   # (output index, chunk offset) where chunk c takes over
+        self._next = 0            # next chunk to splice
+        self._filled = 0
+        self._lock = threading.Lock()
+
+        def draw(c):
+            bg = np.random.PCG64(seed)
+            if c:
+                bg.advance(c * M)
+            g = np.random.Generator(bg)
+            if bufs is not None:
+                return g, g.standard_normal(M + extra, out=bufs[c])
+            return g, g.standard_normal(M + extra)
+
+        self._pool = ThreadPoolExecutor(max_workers=min(threads, nchunk))
+        self._futs = [self._pool.submit(draw, c) for c in range(nchunk)]
+        self._pool.shutdown(wait=False)
+
+    def wait(self):
+        """All chains drawn (their buffers may be reused after this)."""
+        for f in self._futs:
+            f.exception()
+
+    def _sequential(self):
+        self.segs = [(0, self.count, np.random.default_rng(self.seed).standard_normal(self.count), 0)]
+        self._filled = self.count
+        self._next = self.nchunk
+
+    def _resolve(self, upto):
+        upto = min(upto, self.count)
+        with self._lock:
+            while self._filled < upto:
+                c = self._next
+                if c >= self.nchunk:  # shortfall: the last chain sits on the true stream
+                    g, _ = self._futs[-1].result()
+                    self.segs.append((self._filled, self.count, g.standard_normal(self.count - self._filled), 0))
+                    self._filled = self.count
+                    break
+                _, arr = self._futs[c].result()
+                i, j = self._starts[c]
+                if c + 1 < self.nchunk:
+                    sp = _find_splice(arr, j, self._futs[c + 1].result()[1])
+                    if sp is None:  # never seen; the result stays exactly the sequential draw
+                        self.wait()
+                        self._sequential()
+                        break
+                    t, jn = sp
+                    end = i + (t - j)
+                    self._starts.append((end, jn))
+                else:
+                    end = i + len(arr) - j
+                end = min(end, self.count)
+                if end > i:
+                    self.segs.append((i, end, arr, j))
+                    self._filled = end
+                self._next = c + 1
+            return list(self.segs)
+
+
 _SCRATCH = threading.local()
+_CHUNKS_PER_THREAD = 4
 
 
 def normal_draw(seed, count, threads=None, reuse=False):
-    """FlatDraw of ``np.random.default_rng(seed).standard_normal(count)``.  With ``reuse``
-    the chunks are drawn into this thread's scratch buffers from the previous call (no
-    fresh pages to fault in), so the result is only valid until the thread's next
-    ``reuse`` call -- for callers that consume it at once (the X0 upload)."""
+    """FlatDraw of ``np.random.default_rng(seed).standard_normal(count)``; returns at once,
+    the chains complete in the background (ChainedDraw).  With ``reuse`` the chunks are drawn
+    into this thread's scratch buffers from the previous call (no fresh pages to fault in), so
+    the result is only valid until the thread's next ``reuse`` call -- for callers that consume
+    it at once (the X0 upload)."""
     threads = threads or _threads()
     if count < _MIN_PARALLEL or threads < 2:
         return FlatDraw(count, [(0, count, np.random.default_rng(seed).standard_normal(count), 0)])
-    nchunk = min(threads, max(2, count // (_MIN_PARALLEL // 2)))
+    nchunk = min(_CHUNKS_PER_THREAD * threads, max(2, count // (_MIN_PARALLEL // 2)))
     M = -(-count // nchunk)           # nominal stream draws per chunk
     extra = M // 16 + 4096            # overlap covering the slow-path surplus of a chunk
 
     bufs = None
     if reuse:
+        last = getattr(_SCRATCH, "last", None)
+        if last is not None:
+            last.wait()  # its chains write the scratch buffers
         bufs = getattr(_SCRATCH, "bufs", None)
         if bufs is None or len(bufs) != nchunk or len(bufs[0]) != M + extra:
             bufs = _SCRATCH.bufs = [np.empty(M + extra) for _ in range(nchunk)]
-
-    def draw(c):
-        bg = np.random.PCG64(seed)
-        if c:
-            bg.advance(c * M)
-        g = np.random.Generator(bg)
-        if bufs is not None:
-            return g, g.standard_normal(M + extra, out=bufs[c])
-        return g, g.standard_normal(M + extra)
-
-    with ThreadPoolExecutor(max_workers=nchunk) as ex:
-        parts = list(ex.map(draw, range(nchunk)))
-    # splice: chunk c contributes from index j_c onwards, at output index i_c
-    starts = [(0, 0)]
-    for c in range(1, nchunk):
-        i_prev, j_prev = starts[-1]
-        sp = _find_splice(parts[c - 1][1], j_prev, parts[c][1])
-        if sp is None:
-            return FlatDraw(count, [(0, count, np.random.default_rng(seed).standard_normal(count), 0)])
-        t, j = sp
-        starts.append((i_prev + (t - j_prev), j))
-    segs = []
-    for c in range(nchunk):
-        i, j = starts[c]
-        arr = parts[c][1]
-        end = starts[c + 1][0] if c + 1 < nchunk else i + len(arr) - j
-        end = min(end, count)
-        if end > i:
-            segs.append((i, end, arr, j))
-    filled = segs[-1][1]
-    if filled < count:  # the last chain is on the true stream: continue it sequentially
-        g, _ = parts[-1]
-        segs.append((filled, count, g.standard_normal(count - filled), 0))
-    return FlatDraw(count, segs)
+    d = ChainedDraw(seed, count, nchunk, M, extra, bufs, threads)
+    if reuse:
+        _SCRATCH.last = d
+    return d
 
 
 def standard_normal(seed, count, threads=None):

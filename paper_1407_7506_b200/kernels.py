@@ -110,10 +110,50 @@ def _emu(n, m1, m2):
     return n >= EMU_MIN_ROWS and min(m1, m2) >= EMU_MIN_COLS and _lib.load().bk_fp64_emu_enabled()
 
 
-def _ozaki_gram(n, m1, m2, px, lx, py, ly, out_ptr, ldo, symmetric, ws_kind):
+class ColDigits:
+    """Exponents and column digits of an n x m real block (view), kept between the emulated
+    Grams that have (a column range of) it as their left operand: ``coldigits(x)`` slices once,
+    ``gram(x[:, a:b], y, xdig=d)`` / ``gram2(..., xdig=d)`` skip the slicing of X.  The caller
+    keeps the block unchanged while the digits are in use."""
+
+    __slots__ = ("buf", "ptr", "ld", "n", "m")
+
+    def col0(self, px, lx, n, m1):
+        """Column offset of the operand (px, lx, n rows, m1 real columns) inside the sliced
+        block, or -1 when it is not a column range of it."""
+        d = px - self.ptr
+        if lx != self.ld or n != self.n or d < 0 or d % 8:
+            return -1
+        c0 = d // 8
+        return c0 if c0 + m1 <= self.m else -1
+
+
+def coldigits(x, buf=None):
+    """ColDigits of the block x (float64, or complex128 as its interleaved real view), into
+    ``buf`` (a uint8 CUDA tensor, grown if too small) -- or None when the emulated Grams would
+    not be used for it."""
+    px, n, mr, lx = real_view(x)
+    if not _emu(n, mr, EMU_MIN_COLS):
+        return None
+    nbytes = int(_lib.load().bk_ozaki_coldigits_bytes(n, mr))
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    d = ColDigits()
+    d.buf, d.ptr, d.ld, d.n, d.m = buf, px, lx, n, mr
+    _lib.call("bk_ozaki_coldigits_d", n, mr, px, lx, buf.data_ptr(), buf.numel(), stream_ptr())
+    return d
+
+
+def _ozaki_gram(n, m1, m2, px, lx, py, ly, out_ptr, ldo, symmetric, ws_kind, xdig=None):
     lib = _lib.load()
     same = 1 if (px == py and lx == ly and m1 == m2) else 0
     sym = 1 if (symmetric and same) else 0
+    c0 = xdig.col0(px, lx, n, m1) if xdig is not None else -1
+    if c0 >= 0:
+        wp, wb = workspace(ws_kind + "/oz").get(lib.bk_ozaki_gram_pre_ws_bytes(n, m1, m2, same, sym))
+        _lib.call("bk_ozaki_gram_pre_d", n, m1, m2, px, lx, xdig.buf.data_ptr(), xdig.m, c0, py, ly, out_ptr, ldo, sym,
+                  wp, wb, stream_ptr())
+        return
     wp, wb = workspace(ws_kind + "/oz").get(lib.bk_ozaki_gram_ws_bytes(n, m1, m2, same, sym))
     _lib.call("bk_ozaki_gram_d", n, m1, m2, px, lx, py, ly, out_ptr, ldo, sym, wp, wb, stream_ptr())
 
@@ -148,9 +188,10 @@ def _split_launch(splits, call_part, ws_kind, nbytes):
     main.wait_stream(side)
 
 
-def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
+def gram(x, y, out=None, symmetric=False, ws_kind="gram", xdig=None):
     """out = X^H Y (m1 x m2).  symmetric=True requires x is y (same view).  Launches on a
-    second stream must pass their own ``ws_kind`` (split-K tickets live in the workspace)."""
+    second stream must pass their own ``ws_kind`` (split-K tickets live in the workspace).
+    ``xdig``: ColDigits of a block that contains x as a column range (emulated Grams only)."""
     n = x.shape[0]
     if y.shape[0] != n:
         raise DeviceError(f"row dimensions differ: {n} vs {y.shape[0]}")
@@ -164,7 +205,7 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
         px, _, _, lx = real_view(x)
         py, _, _, ly = real_view(y)
         if _emu(n, m1, m2):
-            _ozaki_gram(n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), symmetric, ws_kind)
+            _ozaki_gram(n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), symmetric, ws_kind, xdig)
             return out
         _split_launch(lib.bk_gram_splits(m1, m2), lambda part, wp, wb, st: _lib.call(
             "bk_gram_part_d", n, m1, m2, px, lx, py, ly, out.data_ptr(), ld_of(out), 1 if symmetric else 0, part,
@@ -175,7 +216,7 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
     py, _, r2, ly = real_view(y)
     tmp = torch.empty((r1, r2), dtype=F64, device=x.device)
     if _emu(n, r1, r2):
-        _ozaki_gram(n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2, symmetric, ws_kind)
+        _ozaki_gram(n, r1, r2, px, lx, py, ly, tmp.data_ptr(), r2, symmetric, ws_kind, xdig)
         _lib.call("bk_cplx_gram_combine_d", m1, m2, tmp.data_ptr(), r2, out.data_ptr(), ld_of(out),
                   stream_ptr())
         return out
@@ -187,9 +228,9 @@ def gram(x, y, out=None, symmetric=False, ws_kind="gram"):
     return out
 
 
-def gram2(x1, y1, out1, x2, y2, out2):
+def gram2(x1, y1, out1, x2, y2, out2, xdig=None):
     """Two independent Grams in one launch (real only; complex falls back to two launches).
-    Emulated: X^T Y1 and X^T Y2 of one basis X share its digits."""
+    Emulated: X^T Y1 and X^T Y2 of one basis X share its digits (``xdig``: already sliced)."""
     n = x1.shape[0]
     if (x1.dtype == F64 and x1.data_ptr() == x2.data_ptr() and x1.shape == x2.shape and x1.stride() == x2.stride()
             and _emu(n, x1.shape[1], min(y1.shape[1], y2.shape[1]))):
@@ -197,13 +238,20 @@ def gram2(x1, y1, out1, x2, y2, out2):
         px, _, _, lx = real_view(x1)
         pa, _, _, la = real_view(y1)
         pb, _, _, lb = real_view(y2)
+        c0 = xdig.col0(px, lx, n, x1.shape[1]) if xdig is not None else -1
+        if c0 >= 0:
+            wp, wb = workspace("gram/oz").get(lib.bk_ozaki_gram2_pre_ws_bytes(n, x1.shape[1], y1.shape[1], y2.shape[1]))
+            _lib.call("bk_ozaki_gram2_pre_d", n, x1.shape[1], px, lx, xdig.buf.data_ptr(), xdig.m, c0, y1.shape[1], pa,
+                      la, out1.data_ptr(), ld_of(out1), y2.shape[1], pb, lb, out2.data_ptr(), ld_of(out2), wp, wb,
+                      stream_ptr())
+            return
         wp, wb = workspace("gram/oz").get(lib.bk_ozaki_gram2_ws_bytes(n, x1.shape[1], y1.shape[1], y2.shape[1]))
         _lib.call("bk_ozaki_gram2_d", n, x1.shape[1], px, lx, y1.shape[1], pa, la, out1.data_ptr(), ld_of(out1),
                   y2.shape[1], pb, lb, out2.data_ptr(), ld_of(out2), wp, wb, stream_ptr())
         return
     if x1.dtype != F64 or _emu(x1.shape[0], min(x1.shape[1], x2.shape[1]), min(y1.shape[1], y2.shape[1])):
-        gram(x1, y1, out1)
-        gram(x2, y2, out2)
+        gram(x1, y1, out1, xdig=xdig)
+        gram(x2, y2, out2, xdig=xdig)
         return
     n = x1.shape[0]
     p1, _, _, l1 = real_view(x1)
@@ -557,6 +605,18 @@ def to_host(x, chunk_bytes=32 << 20, out=None):
         pend = (b, r0, r1)
     drain(*pend)
     return out
+
+
+def to_host_pinned(x, out, chunk_bytes=128 << 20):
+    """numpy view of the page-locked tensor ``out`` after out[:, :] = x: row chunks of the
+    (row-strided) device block are packed on the device and copied straight into ``out`` --
+    no host staging pass.  The array keeps ``out`` alive (its base)."""
+    n, m = x.shape
+    rows = max(1, chunk_bytes // max(1, m * x.element_size()))
+    for r0 in range(0, n, rows):
+        out[r0:r0 + rows].copy_(x[r0:r0 + rows], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out.numpy()
 
 
 def from_host(src, x, chunk_bytes=32 << 20):

@@ -37,6 +37,10 @@ __all__ = ["SolverOptions", "SolveReport", "split_blocks", "ppcg_solve", "PPCGSo
 # host-sync trimming (bit 0: projections queued before the metric is read; bit 1: the
 # orthonormality Gram queued before the update's flags are read); PPCG_SPECULATE overrides
 _SPECULATE = int(os.environ.get("PPCG_SPECULATE", "7"))
+# column digits of X kept between the emulated Grams of an iteration (PPCGSolver._slice_x);
+# the buffer is as large as one state block, so only up to this size
+_DIGIT_CACHE = int(os.environ.get("PPCG_DIGIT_CACHE", "1"))
+_DIGIT_CACHE_MAX = 4 << 30
 _COEFF_REFRESH = 100.0   # ppcg.py:41
 _BREAKDOWN_MAX = 1e8     # ppcg.py:705
 _TAYLOR_OK = 0.1         # core.py:127
@@ -176,23 +180,69 @@ def _x0_draw_locked(n, kt, seed):
         return initial_block_source(n, kt, False, seed, None, 0, n)
 
 
-def _prefaulted(n, k, dtype):
-    """An (n, k) array whose pages are faulted in (one write per page): built on the X0
-    worker while the GPU iterates, so the final vector download copies into resident memory
-    (a fresh 453 MB array costs ~60 ms of page faults at config 2)."""
+_RESULT_POOL = []          # [page-locked (n, k) tensor, lease: weakref (dead = free)]
+_RESULT_POOL_TRIED = set()
+_RESULT_POOL_MAX = 2 << 30
+_RESULT_POOL_LOCK = __import__("threading").Lock()
+
+
+def _pinned_take(n, k, cplx, device, owner):
+    """A free page-locked (n, k) result tensor from the pool, leased to ``owner`` (a weakref),
+    or None.  The pool keeps one buffer per result shape: finish() hands the caller a numpy view
+    of it and the lease follows that array (and every view of it), so the buffer is reused
+    only after the caller has dropped the previous result -- a caller that keeps results gets
+    pageable arrays instead.  The one cold cudaHostAlloc per shape (~0.45 ms per MB, holding a
+    driver lock that stalls kernel launches) happens here, on the worker thread."""
+    import torch
+
+    dtype = torch.complex128 if cplx else torch.float64
+    nbytes = n * k * (16 if cplx else 8)
+    if nbytes > _RESULT_POOL_MAX or nbytes == 0:
+        return None
+    key = (n, k, cplx, int(device))
+    with _RESULT_POOL_LOCK:
+        for ent in _RESULT_POOL:
+            if ent[2] == key and ent[1]() is None:
+                ent[1] = owner
+                return ent
+        if key in _RESULT_POOL_TRIED:
+            return None
+        _RESULT_POOL_TRIED.add(key)
+        while _RESULT_POOL and sum(e[0].numel() * e[0].element_size() for e in _RESULT_POOL) + nbytes > _RESULT_POOL_MAX:
+            _RESULT_POOL.pop(0)
+    try:
+        with torch.cuda.device(device):
+            t = torch.empty((n, k), dtype=dtype, pin_memory=True)
+    except Exception:
+        return None
+    ent = [t, owner, key]
+    with _RESULT_POOL_LOCK:
+        _RESULT_POOL.append(ent)
+    return ent
+
+
+def _result_buffer(n, k, cplx, device, owner):
+    """The (n, k) result array, prepared on the X0 worker while the GPU iterates: a page-locked
+    pool buffer when one is free (_pinned_take), so the final vector download is one device ->
+    host copy at PCIe rate straight into the array the caller receives -- no staging copy, no
+    page faults; otherwise a pageable array with its pages faulted in (a fresh 453 MB array
+    costs ~60 ms of page faults at config 2)."""
+    ent = _pinned_take(n, k, cplx, device, owner)
+    if ent is not None:
+        return ent
     import ctypes
 
-    arr = np.empty((n, k), dtype=dtype)
+    arr = np.empty((n, k), dtype=np.complex128 if cplx else np.float64)
     # libc memset through ctypes: the GIL is released, so the thread that launches the GPU
     # work is never held up (a numpy strided write keeps the GIL)
     ctypes.memset(arr.ctypes.data, 0, arr.nbytes)
     return arr
 
 
-def _vectors_prefault(n, k, dtype):
+def _vectors_prefault(n, k, cplx, device, owner):
     if _X0["pool"] is None:
         return None
-    return _X0["pool"].submit(_prefaulted, n, k, dtype)
+    return _X0["pool"].submit(_result_buffer, n, k, cplx, device, owner)
 
 
 def _x0_prefetch(n, kt, seed):
@@ -473,11 +523,39 @@ class PPCGSolver:
         return self.AP[self.pi][:, self.L:]
 
     # ------------------------------------------------------------------ orthonormalisation
+    # Column digits of [X_lock X] for the emulated Grams (kernels.ColDigits): sliced once by
+    # _residual_w, then reused by the Grams that have the unchanged block as left operand --
+    # the next iteration's projections X^H W / X^H P and proj_defect, the final Rayleigh-Ritz.
+    # Every method that writes X drops them; the buffer index is checked on use.
+    _xdig = None
+    _xdig_buf = None
+
+    def _slice_x(self, other_cols):
+        """Slice XF[xi] for Grams whose right operands have at least ``other_cols`` columns."""
+        self._xdig = None
+        K = self.K
+        xf = self.XF[self.xi]
+        if not _DIGIT_CACHE or other_cols < K.EMU_MIN_COLS:
+            return None
+        if xf.shape[0] * xf.shape[1] * xf.element_size() > _DIGIT_CACHE_MAX:
+            return None
+        d = K.coldigits(xf, self._xdig_buf)
+        if d is None:
+            return None
+        self._xdig_buf = d.buf
+        self._xdig = (d, self.xi)
+        return d
+
+    def _xd(self):
+        t = self._xdig
+        return t[0] if t is not None and t[1] == self.xi else None
+
     def _cholqr_inplace_swap(self, gram_act, x_src_idx):
         """CholQR of the active block (core.py:86-100 / ppcg.py:483-484): R from the Gram
         with the pivot floor; X <- X R^{-1}, AX <- AX R^{-1} into the other buffer; swap.
         Raises RankDeficiencyError(column) like _cholesky_upper."""
         K = self.K
+        self._xdig = None
         L, ka = self.L, self.kt - self.L
         R = self.Rm[:ka, :ka]
         spec = self._spec_R == L and gram_act.data_ptr() == self.Gfull[L:, L:].data_ptr()
@@ -507,6 +585,7 @@ class PPCGSolver:
     def _taylor_swap(self, gram_act):
         """Taylor-polar correction X <- X p(G - I) (core.py:106-124, ppcg.py:477-481)."""
         K, torch = self.K, self.torch
+        self._xdig = None
         L, ka = self.L, self.kt - self.L
         terms = self.opts.taylor_terms
         eye = self.eye[:ka, :ka]
@@ -532,8 +611,10 @@ class PPCGSolver:
         L, ka, k = self.L, self.kt - self.L, self.k
         x, ax = self.X(), self.AX()
         G = self.Gm[:ka, :ka]
-        K.gram(x, ax, G)
-        self._red(G)
+        xd = self._slice_x(ka)
+        if not (0 < L < k):  # (the locked form builds its own stacked Gram)
+            K.gram(x, ax, G, xdig=xd)
+            self._red(G)
         w = self.W[:, L:]
         if L == 0:
             K.tsgemm([x], [G], [w], alpha=-1.0, beta=1.0, zs=[ax], rowscale=self.rowscale,
@@ -565,12 +646,13 @@ class PPCGSolver:
         XFc, AXFc = self.XF[self.xi], self.AXF[self.xi]
         xl, axl = XFc[:, :L], AXFc[:, :L]
         Gs = self.Gstack[:, :ka]
-        K.gram(XFc, ax, Gs)
+        xd = self._xd()
+        K.gram(XFc, ax, Gs, xdig=xd)
         self._red(Gs)
         K.tsgemm([XFc], [Gs], [w], alpha=-1.0, beta=1.0, zs=[ax], metric=self.stats[0:1], ksplit=k, nsplit=ma)
         K.tsgemm([xl], [Gs[:L]], [w], alpha=1.0, beta=1.0, zs=[w], rowscale=self.rowscale)
         Glk = self.Gl[:k, :L]
-        K.gram(XFc[:, :k], axl, Glk)
+        K.gram(XFc[:, :k], axl, Glk, xdig=xd)
         self._red(Glk)
         K.tsgemm([XFc[:, :k]], [Glk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[11:12], ksplit=k,
                  nsplit=L)
@@ -584,6 +666,7 @@ class PPCGSolver:
 
     def _householder_refresh(self):
         """X <- qr(X)[0], AX <- A X (ppcg.py:712-713, 756-757)."""
+        self._xdig = None
         x = self.X()
         if self.comm is None:
             self.dense.householder_q(x, self.AW)
@@ -601,6 +684,7 @@ class PPCGSolver:
         are equivariant in PPCG); this path runs only after a breakdown or a
         rank-deficient CholQR, both of which drop P."""
         K, torch = self.K, self.torch
+        self._xdig = None
         L, ka = self.L, self.kt - self.L
         for shift in (True, False, False):
             x = self.X()
@@ -624,8 +708,12 @@ class PPCGSolver:
         kt = self.kt
         for attempt in range(2):
             S, AS = self.XF[self.xi], self.AXF[self.xi]
-            K.gram(S, AS, self.Ahat)
-            K.gram(S, S, self.Bhat, symmetric=True)
+            xd = self._xd()
+            if xd is None:  # S is the left operand of both Grams: slice it once
+                xd = self._slice_x(self.kt)
+            K.gram(S, AS, self.Ahat, xdig=xd)
+            K.gram(S, S, self.Bhat, symmetric=True, xdig=xd)
+            self._xdig = None
             self._red(self.Ahat, self.Bhat)
             self.dense.rr_pencil(self.Ahat, self.Bhat, self.omega, self.Cm, self.rr_status)
             self._fetch((self.rr_status, self.h_rr_status))
@@ -697,7 +785,9 @@ class PPCGSolver:
             K.from_host(src, raw)
         self._x0_job = None
         # the result array's pages, faulted in on the worker while the GPU iterates (finish)
-        self._vec_job = (_vectors_prefault(self.n, self.k, np.complex128 if self.cplx else np.float64)
+        import weakref
+
+        self._vec_job = (_vectors_prefault(self.n, self.k, self.cplx, torch.cuda.current_device(), weakref.ref(self))
                          if self.comm is None else None)
         G = self.Gm
         K.gram(raw, raw, G, symmetric=True)
@@ -724,7 +814,7 @@ class PPCGSolver:
         if not self.metric_cached:
             xl, axl = self.XF[self.xi][:, :k], self.AXF[self.xi][:, :k]
             Gk = self.Gl[:k, :k]
-            K.gram(xl, axl, Gk)
+            K.gram(xl, axl, Gk, xdig=self._xd())
             self._red(Gk)
             K.small_stats(Gk, self.stats[1:4])
             K.tsgemm([xl], [Gk], [None], alpha=-1.0, beta=1.0, zs=[axl], metric=self.stats[0:1],
@@ -784,15 +874,17 @@ class PPCGSolver:
         Gd = self.Gp[:kt, :ka]
         main = torch.cuda.current_stream()
         xfull = self.XF[self.xi]
+        xd = self._xd()  # last use of X's digits: the subblock update writes the other buffer,
+        self._xdig = None  # the orthonormalisation after it this one
         if self.comm is None:
             def overlap(ready):  # after the pencil Grams (event `ready`): runs beside the pencils
                 self.side.wait_event(ready)
                 with torch.cuda.stream(self.side):
-                    K.gram(xfull, w, Gd, ws_kind="side")
+                    K.gram(xfull, w, Gd, ws_kind="side", xdig=xd)
                     K.small_stats(Gd, self.stats[5:8])
             self._overlap = overlap
         else:  # collectives stay on one stream, in the same order on every rank
-            K.gram(xfull, w, Gd)
+            K.gram(xfull, w, Gd, xdig=xd)
             self._red(Gd)
             K.small_stats(Gd, self.stats[5:8])
 
@@ -918,15 +1010,17 @@ class PPCGSolver:
             K.tsgemm(xs, gs, ys, alpha=-1.0, beta=1.0, zs=ys, metric=metric if o.project_w else None,
                      ksplit=ks, nsplit=ka)
 
+        xd = self._xd()
+
         def grams(xb, gw, gp):
             if o.project_w and proj_p:
-                K.gram2(xb, w, gw, xb, p, gp)
+                K.gram2(xb, w, gw, xb, p, gp, xdig=xd)
                 self._red(gw, gp)
             elif o.project_w:
-                K.gram(xb, w, gw)
+                K.gram(xb, w, gw, xdig=xd)
                 self._red(gw)
             else:
-                K.gram(xb, p, gp)
+                K.gram(xb, p, gp, xdig=xd)
                 self._red(gp)
 
         wnorm_done = False
@@ -1097,7 +1191,14 @@ class PPCGSolver:
         rn = np.sqrt(self.h_colnorm2.numpy()[:k]).tolist()
         pre = getattr(self, "_vec_job", None)
         self._vec_job = None
-        vectors = K.to_host(V, out=pre.result() if pre is not None else None)
+        buf = pre.result() if pre is not None else None
+        if isinstance(buf, list):  # pool entry: the lease passes to the array (all its views hold arr.base)
+            import weakref
+
+            vectors = K.to_host_pinned(V, buf[0])
+            buf[1] = weakref.ref(vectors.base)
+        else:
+            vectors = K.to_host(V, out=buf)
         extra = {}
         if self.comm is not None:
             if gather is None:
@@ -1146,6 +1247,8 @@ def device_bytes_plan(n_loc, n_ext, kt, q, cplx, nnz_loc=0, size=1):
         oz = int(lib.bk_ozaki_gram_ws_bytes(n_ext, r, r, 0, 0)) + int(lib.bk_ozaki_tsgemm_ws_bytes(4, n_loc, r, r, r))
     except Exception:  # library not built: the measured sizes at config 5 (~0.6 / 0.2 / 4.6 GB)
         gram_ws, sb_ws, oz = 6 << 27, 2 << 27, 37 << 27
+    dig = n_ext * ldp * s  # column digits of [X_lock X] kept between Grams (PPCGSolver._slice_x)
+    out["digit_cache"] = dig if dig <= _DIGIT_CACHE_MAX and _DIGIT_CACHE else 0
     out["workspaces"] = 3 * gram_ws + sb_ws  # main / side / rr families
     # main and side-stream emulated Grams + the tall GEMM (small products keep the DMMA kernels)
     out["fp64_emulation_workspaces"] = 2 * oz

@@ -191,6 +191,69 @@ def test_ozaki_tsgemm_metric_snapshot_and_inplace(cuda):
     assert np.max(np.abs(w.cpu().numpy() - ref_w)) <= 1e-13 * np.abs(ref_w).max() * 10
 
 
+@pytest.mark.parametrize("ks,ns", [(300, 499), (491, 523), (522, 1), (513, 33)])
+def test_ozaki_tsgemm_metric_modes(cuda, ks, ns):
+    """The three forms of the fused metric give the same number: a long K tail takes the partial-K
+    snapshot (MMA warp paused), a short one (K - ksplit <= 32) the full-K accumulator minus the
+    tail's fp64 product, ksplit = K the final accumulator; odd nsplit, row scale, edge tiles."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, Kt, N = 40000, 523, 523
+    x, g, ax = gauss(n, Kt, 160), gauss(Kt, N, 161) * 0.1, gauss(n, N, 162)
+    s = np.abs(gauss(n, 1, 163))[:, 0] + 0.5
+    ref_metric = np.sum((ax[:, :ns] - x[:, :ks] @ g[:ks, :ns]) ** 2)
+    ref_w = s[:, None] * (ax - x @ g)
+    with emu(torch):
+        w = torch.empty((n, N), dtype=torch.float64, device="cuda")
+        metric = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [w], alpha=-1.0, beta=1.0, zs=[dev(ax, torch)],
+                 rowscale=dev(s, torch), metric=metric, ksplit=ks, nsplit=ns)
+        w0 = torch.empty_like(w)
+        K.tsgemm([dev(x, torch)], [dev(g, torch)], [w0], alpha=-1.0, beta=1.0, zs=[dev(ax, torch)],
+                 rowscale=dev(s, torch))
+    assert abs(metric.item() - ref_metric) <= 1e-12 * ref_metric
+    assert np.max(np.abs(w.cpu().numpy() - ref_w)) <= 1e-12 * np.abs(ref_w).max()
+    if Kt - ks <= 32:  # no k split: the same digits as the plain product
+        assert torch.equal(w, w0)
+
+
+def test_ozaki_coldigits_reused_across_grams(cuda):
+    """Column digits sliced once (kernels.coldigits) and handed to several Grams -- full block,
+    column ranges at odd offsets (locked columns), gram2, symmetric, complex views -- give
+    bitwise the results of the Grams that slice X themselves; an operand that is not a column
+    range of the sliced block is sliced as usual."""
+    from paper_1407_7506_b200 import kernels as K
+
+    torch = cuda
+    n, m = 40000, 212
+    xb = dev(gauss(n, m + 12, 170) * np.logspace(-3, 3, m + 12)[None, :], torch)
+    x = xb[:, 5:5 + m]
+    w, p = dev(gauss(n, 150, 171), torch), dev(gauss(n, 97, 172), torch)
+    with emu(torch):
+        d = K.coldigits(x)
+        assert d is not None and d.m == m
+        for a, b in ((0, m), (11, m), (3, 140)):
+            xs = x[:, a:b]
+            assert torch.equal(K.gram(xs, w, xdig=d), K.gram(xs, w))
+            assert torch.equal(K.gram(xs, xs, symmetric=True, xdig=d), K.gram(xs, xs, symmetric=True))
+            g1, g2 = (torch.empty((b - a, 150), dtype=torch.float64, device="cuda"),
+                      torch.empty((b - a, 97), dtype=torch.float64, device="cuda"))
+            h1, h2 = torch.empty_like(g1), torch.empty_like(g2)
+            K.gram2(xs, w, g1, xs, p, g2, xdig=d)
+            K.gram2(xs, w, h1, xs, p, h2)
+            assert torch.equal(g1, h1) and torch.equal(g2, h2)
+        assert torch.equal(K.gram(w, p, xdig=d), K.gram(w, p))  # not a range of the sliced block
+        z = dev(gauss(n, 90, 173, cplx=True), torch)
+        zw = dev(gauss(n, 70, 174, cplx=True), torch)
+        dz = K.coldigits(z)
+        assert torch.equal(K.gram(z[:, 7:], zw, xdig=dz), K.gram(z[:, 7:], zw))
+        # a buffer that is too small is replaced, a large one reused
+        d2 = K.coldigits(x, d.buf)
+        assert d2.buf is d.buf
+        assert K.coldigits(x[:, :40]) is None  # below the emulation threshold: DMMA Grams
+
+
 def test_ozaki_tsgemm_nonfinite_row(cuda):
     from paper_1407_7506_b200 import kernels as K
 

@@ -24,8 +24,12 @@ def run_variants(torch, dc, xb, off, m, cplx):
     dt = torch.complex128 if cplx else torch.float64
     x = xb[:, off:off + m]
     outs = {}
-    variants = (("slot", 2, True, True, 0), ("slot_v1", 2, True, True, 1), ("march", 2, True, False, 0),
-                ("vec", 2, False, False, 0), ("gather", 0, False, False, 0))
+    # stencil-slot configurations: variant + 100 x (forced x segment count); 4..7 hold X planes in
+    # registers (27-point; the 7-point kernel ignores the variant)
+    variants = (("slot", 2, True, True, 0), ("slot_v1", 2, True, True, 1), ("slot_v4", 2, True, True, 4),
+                ("slot_v5", 2, True, True, 5), ("slot_v6", 2, True, True, 6), ("slot_v7", 2, True, True, 7),
+                ("slot_v4x2", 2, True, True, 204), ("slot_v5x3", 2, True, True, 305), ("slot_v7x2", 2, True, True, 207),
+                ("march", 2, True, False, 0), ("vec", 2, False, False, 0), ("gather", 0, False, False, 0))
     try:
         for name, variant, stencil, slot, cfg in variants:
             if stencil and dc.stencil is None:

@@ -18,7 +18,9 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 a0, k, q, tol = config_problem(cfg)
 torch.zeros(1, device="cuda")
+rep_ = None
 for rep in range(reps):
+    rep_ = None  # like bench.py: the previous result is released before the next call
     a = SparseHermitian(a0._csr.copy(), "symmetric" if a0.dtype.kind == "f" else "hermitian")
     t = jacobi_preconditioner(a)
     opts = SolverOptions(k=k, sbsize=q, tol=tol, seed=0, max_iter=iters)
