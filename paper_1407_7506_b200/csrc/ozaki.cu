@@ -135,6 +135,51 @@ BK_DEV void combine16_i64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
   }
 }
 
+// int32 -> fp64 exactly without the conversion unit: the double with high word 0x43300000 and
+// low word u is 2^52 + u, and v + 2^31 = v ^ 0x80000000 as an unsigned word
+BK_DEV double i2d(uint32_t v) {
+  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+
+// combine16_i64 in fp64 arithmetic, for short sums: with K <= TS_F64_COMBINE_K accumulated rows
+// every |acc_t| <= 8 K 2^14, so H and L (Horner in base 256 over four groups) stay below 2^53
+// and each fma is exact -- bitwise the int64 result, with half the instructions (one LOP and one
+// DADD per conversion, no 64-bit shifts / carries, no I2F.F64.S64).  An experiment
+// (PPCG_OZ_F64COMB=1): the FP64 pipe's latency makes it slightly slower than the int64 form.
+constexpr int TS_F64_COMBINE_K = 4032;
+template <int GS>
+BK_DEV void combine16_f64(uint32_t tmem_lane, int cc, double (&acc)[16]) {
+  static_assert(S == 8, "two halves of four digit groups");
+  double h[16];
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + t * GS + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      double x = i2d(v[0][e]);
+      x = fma(x, 256.0, i2d(v[1][e]));
+      x = fma(x, 256.0, i2d(v[2][e]));
+      h[e] = fma(x, 256.0, i2d(v[3][e]));
+    }
+  }
+  {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) tmem_ld16(tmem_lane + (4 + t) * GS + cc, v[t]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      double x = i2d(v[0][e]);
+      x = fma(x, 256.0, i2d(v[1][e]));
+      x = fma(x, 256.0, i2d(v[2][e]));
+      x = fma(x, 256.0, i2d(v[3][e]));
+      acc[e] = fma(x, 0x1p-32, h[e]);
+    }
+  }
+}
+
 BK_DEV void combine16_i64_rt(uint32_t tmem_lane, int gs, int cc, double (&acc)[16]) {
   long long h[16];
   {
@@ -353,6 +398,7 @@ struct TsEpi {
   int kp1, kv1, kv2;  // k layout: [0, kv1) valid, zeros to kp1, [kp1, kp1 + kv2) valid (32-deep steps
                       // wholly in the zero padding are skipped)
   int nsplit;
+  int f64comb;        // K short enough for the fp64 digit-group combine (combine16_f64)
   double alpha, beta;
   const int* ER[4];   // row exponents (indexed by global row)
   const int* EG[4];   // G column exponents
@@ -720,7 +766,10 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
         for (int cc = 0; cc < CPW; cc += 16) {
           if (t.rowB + c0 + cc < P.nsplit && cc < ncol) {
             double acc[16];
-            combine16_i64<TBN>(tl, c0 + cc, acc);
+            if (P.f64comb)
+              combine16_f64<TBN>(tl, c0 + cc, acc);
+            else
+              combine16_i64<TBN>(tl, c0 + cc, acc);
             double z[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -748,7 +797,10 @@ __global__ void __launch_bounds__(TS_THREADS, 1)  // 10 warps: 3 share a sub-par
       for (int cc = 0; cc < CPW; cc += 16) {
         if (cc < ncol) {
           double a16[16];
-          combine16_i64<TBN>(tl, c0 + cc, a16);
+          if (P.f64comb)
+            combine16_f64<TBN>(tl, c0 + cc, a16);
+          else
+            combine16_i64<TBN>(tl, c0 + cc, a16);
 #pragma unroll
           for (int e = 0; e < 16; ++e) acc[cc + e] = a16[e];
         }
@@ -1439,6 +1491,11 @@ extern "C" int bk_ozaki_tsgemm_d(int nprob, int64_t n, int K, int N, double alph
   P.kp1 = L.kp1;
   P.kv1 = split ? ksplit : K;
   P.kv2 = split ? K - ksplit : 0;
+  static const int f64c = [] {
+    const char* e = getenv("PPCG_OZ_F64COMB");
+    return e ? atoi(e) : 0;  // measured 1-4% slower than the int64 combine (profiles/ozaki_ab_r02g.txt)
+  }();
+  P.f64comb = (f64c && L.kp <= TS_F64_COMBINE_K) ? 1 : 0;
   static const int dbg = [] {
     const char* e = getenv("PPCG_OZ_DBG");
     return e ? atoi(e) : 0;
