@@ -70,6 +70,20 @@ constexpr int PD_BIG = 192;
 constexpr int QMAX_BIG = 64;
 
 constexpr int P_THREADS = 512;
+
+// phase clocks of subblock 0 (profiling builds only: make EXTRA=-DPPCG_PENCIL_PROFILE, read with
+// bk_pencil_phase_clocks; tools/pencil_phases.py)
+#ifdef PPCG_PENCIL_PROFILE
+__device__ long long g_pencil_clk[32];
+#define PMARK(id)                                                        \
+  do {                                                                   \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_pencil_clk[id] = clock64(); \
+  } while (0)
+#else
+#define PMARK(id) \
+  do {            \
+  } while (0)
+#endif
 constexpr double kGramRtol = 1e-12, kDirFloor = 1e-14, kCxFloor = 1e-14;
 
 struct PencilParams {
@@ -701,14 +715,41 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     __syncthreads();
     const double tau = S.red[28];
     if (tau != 0.0) {
+      // this warp's rows i = warp + r nw: all partial dots first, then their reductions (the
+      // shuffles of independent rows overlap; same sums in the same order as one row at a time)
+      constexpr int RMAX = (PD + P_THREADS / 32 - 1) / (P_THREADS / 32);
       double pv = 0.0;
-      for (int i = warp; i < m; i += nw) {
-        const double* row = A + (k + 1 + i) * la + (k + 1);
-        double s = 0.0;
-        for (int j = lane; j < m; j += 32) s += row[j] * v[j];
-        s = warp_sum(s) * tau;
-        if (lane == 0) p[i] = s;
-        pv += s * v[i];
+      if (nw * RMAX >= m) {
+        double sr[RMAX];
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+          const int i = warp + r * nw;
+          double s = 0.0;
+          if (i < m) {
+            const double* row = A + (k + 1 + i) * la + (k + 1);
+            for (int j = lane; j < m; j += 32) s += row[j] * v[j];
+          }
+          sr[r] = s;
+        }
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) sr[r] = warp_sum(sr[r]) * tau;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+          const int i = warp + r * nw;
+          if (i < m) {
+            if (lane == 0) p[i] = sr[r];
+            pv += sr[r] * v[i];
+          }
+        }
+      } else {
+        for (int i = warp; i < m; i += nw) {
+          const double* row = A + (k + 1 + i) * la + (k + 1);
+          double s = 0.0;
+          for (int j = lane; j < m; j += 32) s += row[j] * v[j];
+          s = warp_sum(s) * tau;
+          if (lane == 0) p[i] = s;
+          pv += s * v[i];
+        }
       }
       if (lane == 0) S.red[warp] = pv;
       __syncthreads();
@@ -750,26 +791,41 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     S.red[27] = onenrm;
   }
   __syncthreads();
+  PMARK(6);
   // ---- 2. bisection, one warp per wanted eigenvalue, 32-point multisection
   double* lam = v;  // eigenvalues (v is dead)
   {
     const double pivmin = S.red[26], tnorm = fmax(fabs(S.red[24]), fabs(S.red[25]));
-    for (int j = warp; j < want; j += nw) {
+    // 16-point multisection, a half-warp per eigenvalue (two eigenvalues per warp): the Sturm
+    // recurrences run at the SM's FP64 division rate (one SM per pencil), so fewer points per
+    // step and more steps cost less than the 32-point form (9 x 16 against 8 x 32 evaluations
+    // per eigenvalue), with all eigenvalues of a q <= 32 block refined at once
+    const double tol = 1e-11 * tnorm + 2.0 * pivmin;
+    const int half = lane >> 4, hl = lane & 15;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    for (int j0 = 2 * warp; j0 < want; j0 += 2 * nw) {
+      const int j = j0 + half;
+      const bool has = j < want;
       double lo = S.red[24], hi = S.red[25];
-      for (int it = 0; it < 64; ++it) {
+      for (int it = 0; it < 96; ++it) {
         // shifts to 1e-11 ||T||: inverse iteration needs no more, and the Rayleigh-Ritz step
         // supplies the eigenvalues to full accuracy
-        if (hi - lo <= 1e-11 * tnorm + 2.0 * pivmin) break;
-        const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-        const int c = sturm_count(dg, e, d, x, pivmin);
-        const unsigned b = __ballot_sync(0xffffffffu, c > j);
-        const int f = b ? __ffs(b) - 1 : 32;
-        const double nhi = f < 32 ? __shfl_sync(0xffffffffu, x, f & 31) : hi;
-        const double nlo = f > 0 ? __shfl_sync(0xffffffffu, x, (f - 1) & 31) : lo;
-        lo = nlo;
-        hi = nhi;
+        const bool run = has && !(hi - lo <= tol);
+        if (!__any_sync(0xffffffffu, run)) break;
+        const double x = lo + (hi - lo) * (double)(hl + 1) / 17.0;
+        const int c = run ? sturm_count(dg, e, d, x, pivmin) : 0;
+        const unsigned b = (__ballot_sync(0xffffffffu, run && c > j) & hmask) >> (16 * half);
+        const int f = b ? __ffs(b) - 1 : 16;
+        const double xh = __shfl_sync(0xffffffffu, x, 16 * half + (f & 15));
+        const double xl = __shfl_sync(0xffffffffu, x, 16 * half + ((f + 15) & 15));
+        if (run) {
+          const double nhi = f < 16 ? xh : hi;
+          const double nlo = f > 0 ? xl : lo;
+          lo = nlo;
+          hi = nhi;
+        }
       }
-      if (lane == 0) lam[j] = 0.5 * (lo + hi);
+      if (hl == 0 && has) lam[j] = 0.5 * (lo + hi);
     }
   }
   __syncthreads();
@@ -786,6 +842,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     }
   }
   __syncthreads();
+  PMARK(7);
   // ---- 3. inverse iteration, all vectors independent (TD_BATCH threads at a time); a tight
   //    cluster's iterates come out as independent mixtures of its eigenvectors (distinct
   //    start vectors), which the Rayleigh-Ritz step below resolves
@@ -843,6 +900,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     __syncthreads();
   }
   if (__syncthreads_or(bad)) return 1;
+  PMARK(8);
   // ---- 3b. modified Gram-Schmidt, twice, over the columns of Z (want <= ZW)
   double* cf = scr;  // coefficients
   for (int j = 0; j < want; ++j) {
@@ -874,6 +932,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     for (int r = tid; r < d; r += blockDim.x) ZI(r, j) *= sc;
     __syncthreads();
   }
+  PMARK(9);
   // ---- 3c. Rayleigh-Ritz in span(Z): H = Z^T T Z (T Z formed on the fly), Jacobi, Z <- Z U
   {
     for (int t = tid; t < want * want; t += blockDim.x) {
@@ -934,6 +993,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     }
     __syncthreads();
   }
+  PMARK(10);
   // ---- 4. back-transformation Z <- H_0 ... H_{d-3} Z: a warp owns columns warp + c nw, all of
   //    them updated in one pass over each reflector (read once; no block barriers)
   {
@@ -978,6 +1038,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     }
   }
   __syncthreads();
+  PMARK(11);
   // eigenvectors -> A[:, 0:want], eigenvalues -> ev[0:want] (ascending), ord = identity
   for (int i = warp; i < d; i += nw)
     for (int j = lane; j < want; j += 32) A[i * la + j] = ZI(i, j);
@@ -998,6 +1059,7 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   T* A = S.M0;
   T* B = S.M1;
   T* Li = S.M2;
+  PMARK(1);
   // assemble (M + M^H)/2 of the scaled basis, and ||B||_F
   double fro = 0.0;
   for (int a = BK_WARP; a < d; a += BK_NWARP) {
@@ -1020,6 +1082,7 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   } else {
     if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:193-197
   }
+  PMARK(2);
   // reload B (exact) and factor it for the reduction (sygvd's potrf)
   for (int a = BK_WARP; a < d; a += BK_NWARP) {
     const int ia = S.idx[a];
@@ -1040,10 +1103,12 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   } else {
     if (!smem_cholesky(B, PLD, d)) return 1;  // core.py:198-201
   }
+  PMARK(3);
   if constexpr (kOwnPk<T, PD>)
     packed_lower_inverse(S.pk, d, S.rc, reinterpret_cast<double*>(Li), PLD);  // L still packed in pk
   else
     smem_lower_inverse(B, PLD, Li, PLD, d);
+  PMARK(4);
   smem_gemm<T, PD, false, false, false, false>(Li, PLD, A, PLD, B, PLD, d, d);  // T = Linv A
   __syncthreads();
   smem_gemm<T, PD, false, false, true, true>(B, PLD, Li, PLD, A, PLD, d, d);    // Ared = T Linv^H
@@ -1058,6 +1123,7 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
     if (BK_LANE == 0) real_diag(A[i * PLD + i]);
   }
   __syncthreads();
+  PMARK(5);
   constexpr bool PACKED = kPacked<T, PD>;
   int sweeps = 0;
   // packed triangle: own shared region (large variant) or the dead B (shared variant);
@@ -1078,8 +1144,10 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
       double* v = scr + TD_BATCH * 4 * PD;
       static_assert(kOwnPk<T, PD> || PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1), "td scratch");
       if (tridiag_eig<PD>(reinterpret_cast<double*>(A), PLD, d, want, Z, H, U, scr, v, S) != 0) return 2;
+      PMARK(12);
       smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
       __syncthreads();
+      PMARK(13);
       return 0;
     }
   }
@@ -1179,6 +1247,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
 
   const int j = blockIdx.x;
   const int tid = threadIdx.x;
+  PMARK(0);
   const T* Ar = static_cast<const T*>(P.Araw) + (int64_t)j * P.dmax * P.dmax;
   const T* Br = static_cast<const T*>(P.Braw) + (int64_t)j * P.dmax * P.dmax;
   const int ldr = P.dmax;
@@ -1293,11 +1362,42 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
         double fro2 = 0.0;
         for (int e2 = tid; e2 < d * w; e2 += blockDim.x) fro2 += ab2(T1[(e2 / w) * lw + e2 % w]);
         const double cfro = sqrt(block_sum(fro2, S.red));
-        smem_svals(T2, lw, w, w, S.rc, S);
-        double smin = S.rc[0];
-        for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
+        PMARK(14);
+        // Certificate first: if the Cholesky factorisation of C_X^H C_X - tau I succeeds with
+        // tau = 1e-10 ||C_X||_F^2, then sigma_min(C_X)^2 >= tau up to the factorisation's
+        // backward error (~ w u ||C_X||_F^2, five orders below tau), i.e. sigma_min >=
+        // 0.9e-5 ||C_X||_F; when that already exceeds the reference's bound the decision "no
+        // fallback" is the reference's without the singular values (the one-sided Jacobi below
+        // cost a fifth of this kernel).  Anything else takes the exact path.
+        bool certified = false;
+        {
+          T* G = kOwnPk<T, PD> ? S.M0 : T1 + d * lw;  // w x lw scratch: dead A (large variant) / M2's tail
+          double fx2 = 0.0;
+          for (int e2 = tid; e2 < w * w; e2 += blockDim.x) fx2 += ab2(T2[(e2 / w) * lw + e2 % w]);
+          const double cx2 = block_sum(fx2, S.red);
+          if (isfinite(cx2) && 0.9e-5 * sqrt(cx2) >= kCxFloor * fmax(cfro, 1.0)) {
+            const double tau = 1e-10 * cx2;
+            for (int e2 = tid; e2 < w * w; e2 += blockDim.x) {
+              const int a = e2 / w, b = e2 % w;
+              if (b > a) continue;  // lower triangle, (a, b) = sum_r conj(C_X[r][a]) C_X[r][b]
+              T g = fromR<T>(0.0);
+              for (int r = 0; r < w; ++r) g = fmaT(cj(T2[r * lw + a]), T2[r * lw + b], g);
+              if (a == b) { real_diag(g); g = g - fromR<T>(tau); }
+              G[a * lw + b] = g;
+            }
+            __syncthreads();
+            certified = smem_cholesky(G, lw, w);
+          }
+        }
+        double smin = 0.0;
+        if (!certified) {
+          smem_svals(T2, lw, w, w, S.rc, S);
+          smin = S.rc[0];
+          for (int i = 1; i < w; ++i) smin = fmin(smin, S.rc[i]);
+        }
+        PMARK(15);
         __syncthreads();
-        if (smin < kCxFloor * fmax(cfro, 1.0)) {
+        if (!certified && smin < kCxFloor * fmax(cfro, 1.0)) {
           smem_svals(T1, lw, d, w, S.rc, S);
           double cn = 0.0;
           for (int i = 0; i < w; ++i) cn = fmax(cn, S.rc[i]);
@@ -1335,6 +1435,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) pencil_kernel(const __grid_const
     }
   }
   __syncthreads();
+  PMARK(16);
   if (tid == 0) {
     P.info[4 * j + 0] = fallback;
     P.info[4 * j + 1] = zero_res;
@@ -1489,4 +1590,14 @@ extern "C" int bk_pencil_batched_z(int nb, int d, int ldm, const double* A, cons
                                    double* omega, double* C, int* status, void* ws, int64_t ws_bytes,
                                    void* stream) {
   return pencil_batched<zd>(nb, d, ldm, A, B, want, omega, C, status, ws, ws_bytes, stream);
+}
+
+// profiling builds (-DPPCG_PENCIL_PROFILE): clock64 stamps of subblock 0's phases (32 values); 0 otherwise
+extern "C" int bk_pencil_phase_clocks(long long* out) {
+#ifdef PPCG_PENCIL_PROFILE
+  return cudaMemcpyFromSymbol(out, bk::g_pencil_clk, sizeof(long long) * 32) == cudaSuccess ? 1 : -1;
+#else
+  (void)out;
+  return 0;
+#endif
 }
