@@ -246,3 +246,32 @@ def test_operator_arrays_replaced_after_solve(cuda):
     a._csr.data = a._csr.data * 2.0
     v2 = ppcg_solve(a, opts=opts).values
     np.testing.assert_allclose(v2, 2.0 * v1, rtol=1e-9)
+
+
+def test_result_vectors_pool_never_aliases_live_results(cuda):
+    """The page-locked result pool (ppcg._pinned_take): a solve's vectors stay intact while the
+    caller holds them (or any view of them) -- the next solve gets other memory -- and the
+    buffer is reused once they are dropped; results are the same either way."""
+    import gc
+
+    from paper_1407_7506_b200 import SolverOptions, ppcg_solve, random_hermitian
+    from paper_1407_7506_b200 import ppcg as PP
+
+    a = random_hermitian(400, 0.05, seed=21)
+    b = random_hermitian(400, 0.05, seed=22)
+    opts = SolverOptions(k=6, sbsize=3, tol=1e-8, seed=1, max_iter=60)
+    r1 = ppcg_solve(a, opts=opts)
+    v1 = r1.vectors.copy()
+    view = r1.vectors[5:, :2]          # a view keeps the buffer leased
+    p1 = r1.vectors.ctypes.data
+    del r1
+    gc.collect()
+    r2 = ppcg_solve(b, opts=opts)      # same shape: must not land in the leased buffer
+    assert r2.vectors.ctypes.data != p1
+    assert np.array_equal(view, v1[5:, :2])
+    del view
+    gc.collect()
+    r3 = ppcg_solve(a, opts=opts)
+    assert np.array_equal(r3.vectors, v1) and np.array_equal(r3.values, ppcg_solve(a, opts=opts).values)
+    leased = [e for e in PP._RESULT_POOL if e[1]() is not None]
+    assert len(PP._RESULT_POOL) >= 1 and len(leased) <= len(PP._RESULT_POOL)
