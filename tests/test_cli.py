@@ -46,3 +46,33 @@ def test_solve_and_compare_on_device(cuda, tmp_path, capsys):
         assert (tmp_path / f"c_{s}.csv").exists()
     rc = main(["solve", "--solver", "lobpcg", "--problem", "lap1d:100", "--k", "3", "--max-iter", "2"])
     assert rc == 2
+
+
+@pytest.mark.gpu
+def test_solve_matrix_market_problem_on_device(cuda, tmp_path, capsys):
+    """`--problem mm:<path>` (reference cli.py problem grammar): the solve's reported eigenvalues
+    are those of the file's matrix (dense eigvalsh), trace and JSON report written."""
+    import json
+
+    import numpy as np
+
+    from paper_1407_7506_b200 import random_hermitian
+    from paper_1407_7506_b200.mmio import write_matrix_market
+
+    a = random_hermitian(120, 0.1, seed=77)
+    mm = tmp_path / "a.mtx"
+    write_matrix_market(a, mm)
+    tr = tmp_path / "mm.csv"
+    rc = main(["solve", "--solver", "ppcg", "--problem", f"mm:{mm}", "--k", "4", "--tol", "1e-9",
+               "--max-iter", "500", "--trace-out", str(tr), "--json"])
+    assert rc == 0
+    out = capsys.readouterr().out
+    assert "status: converged" in out
+    vals = [float(ln) for ln in out.split("eigenvalues:")[1].split()]
+    lam = np.linalg.eigvalsh(a.to_dense())[:4]
+    assert np.allclose(vals, lam, rtol=1e-8, atol=1e-10)
+    iters = int(out.split("iterations:")[1].split()[0])
+    rows = parse_trace_csv(tr)
+    assert rows and rows[-1].iteration == iters
+    doc = json.loads((tmp_path / "mm.csv.json").read_text())
+    assert doc["schema"] == "blockeig-trace-v1" and len(doc["records"]) == len(rows)
