@@ -261,6 +261,21 @@ static void launch_recombine(const RecombParams& R, unsigned nrt, int nb, int nc
     const char* e = getenv("PPCG_RECOMB_MINB");
     return e ? atoi(e) : 5;
   }();
+  if constexpr (NT >= 64) {
+    // 64-column tiles (q = 64: configs 3-5) hold twice the accumulators: 208 registers without
+    // a cap, and the 96 of five CTAs per SM cost 2 KB of spills per thread.  Three CTAs per SM
+    // (164 registers, no spills) measured at config 3: 23.1 ms (5 CTAs) / 14.4 (4) / 9.8 (3) /
+    // 11.9 (2)
+    static const int minb64 = [] {
+      const char* e = getenv("PPCG_RECOMB_MINB64");
+      return e ? atoi(e) : 3;
+    }();
+    if (minb64 == 5) launch_recombine_m<NT, 5>(R, nrt, nb, nct, st);
+    else if (minb64 == 2) launch_recombine_m<NT, 2>(R, nrt, nb, nct, st);
+    else if (minb64 == 4) launch_recombine_m<NT, 4>(R, nrt, nb, nct, st);
+    else launch_recombine_m<NT, 3>(R, nrt, nb, nct, st);
+    return;
+  }
   if (minb == 5) launch_recombine_m<NT, 5>(R, nrt, nb, nct, st);
   else if (minb == 6) launch_recombine_m<NT, 6>(R, nrt, nb, nct, st);
   else launch_recombine_m<NT, 1>(R, nrt, nb, nct, st);
