@@ -1,5 +1,6 @@
 """Per-iteration GPU kernel-time breakdown of the config-2 solver (torch.profiler / CUPTI),
-over a window of steady-state iterations.  usage: python tools/iter_breakdown.py [cfg] [skip] [count]"""
+over a window of steady-state iterations.
+usage: python tools/iter_breakdown.py [cfg] [skip] [count] [N (grid edge override)] [k override]"""
 import collections
 import json
 import os
@@ -15,7 +16,10 @@ from paper_1407_7506_b200.problems import config_problem, jacobi_preconditioner 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 count = int(sys.argv[3]) if len(sys.argv) > 3 else 10
-a, k, q, tol = config_problem(cfg)
+kw = {"N": int(sys.argv[4])} if len(sys.argv) > 4 else {}
+a, k, q, tol = config_problem(cfg, **kw)
+if len(sys.argv) > 5:
+    k = int(sys.argv[5])
 s = PPCGSolver(a, jacobi_preconditioner(a), None, SolverOptions(k=k, sbsize=q, tol=tol, max_iter=10**6)).start()
 for _ in range(skip):
     s.step()
