@@ -62,8 +62,11 @@ __global__ void k_expand_coef(int k_act, int q, int nparts, const double* __rest
 // fragment loads conflict-free.
 constexpr int R_KC = 16, R_STAGES = 3, R_LA = R_KC + 4;
 
+// SEQ (several column tiles per CTA, earlier tiles' outputs staged): a two-stage ring, so that
+// two CTAs fit an SM beside the 64 KB of staging (one 4-warp CTA per SM left the DMMA pipe idle)
 template <int NT, int MINB = 1, bool SEQ = false>
 __global__ void __launch_bounds__(R_THREADS, MINB) recombine_kernel(const __grid_constant__ RecombParams P) {
+  constexpr int R_STAGES = SEQ ? 2 : bk::R_STAGES;
   constexpr int LB = NT + 4, WN = NT / 8;
   constexpr int IN_STAGE = R_BM * R_LA, CF_STAGE = R_KC * LB;
   extern __shared__ __align__(16) double sm[];
@@ -248,9 +251,9 @@ static void launch_recombine_m(const RecombParams& R, unsigned nrt, int nb, int 
 // in-place P' over several column tiles: one CTA per (row tile, subblock, side) runs the tiles
 template <int NT>
 static void launch_recombine_seq(const RecombParams& R, unsigned nrt, int nb, int nct, cudaStream_t st) {
-  const int smem = (R_STAGES * (R_BM * R_LA + R_KC * (NT + 4)) + (nct - 1) * 2 * R_BM * NT) * (int)sizeof(double);
-  cudaFuncSetAttribute(recombine_kernel<NT, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  recombine_kernel<NT, 1, true><<<dim3(nrt, nb, 2), R_THREADS, smem, st>>>(R);
+  const int smem = (2 * (R_BM * R_LA + R_KC * (NT + 4)) + (nct - 1) * 2 * R_BM * NT) * (int)sizeof(double);
+  cudaFuncSetAttribute(recombine_kernel<NT, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  recombine_kernel<NT, 2, true><<<dim3(nrt, nb, 2), R_THREADS, smem, st>>>(R);
 }
 
 template <int NT>
