@@ -504,6 +504,9 @@ template <class T, int PD>
 constexpr bool kPacked = std::is_same<T, double>::value && (PD > PD_<T>::v);
 template <class T, int PD>
 constexpr bool kOwnPk = kPacked<T, PD> && (PD > PD_<T>::v);
+// complex large variant: Hermitian tridiagonal route (tridiag_eig<zd>), Z / H / U in shared memory
+template <class T, int PD>
+constexpr bool kZtd = std::is_same<T, zd>::value && (PD > PD_<T>::v);
 
 // per-CTA global workspace: A, B/C, Linv of the large variant, and the rotation log
 template <class T, int PD>
@@ -675,9 +678,18 @@ BK_DEV double td_start(int j, int i) {
   return (double)(h & 0xffffff) / (double)0x800000 - 1.0;
 }
 
-template <int PD>
-BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H, double* U, double* scr, double* v,
-                       PSmem<double>& S) {
+BK_DEV zd warp_sum(zd v) { return {warp_sum(v.re), warp_sum(v.im)}; }
+
+// T = double: real symmetric A.  T = zd (large variant): complex Hermitian A reduced to a REAL
+// symmetric tridiagonal matrix by complex Householder reflectors (zhetd2's scheme: H_k = I - tau_k
+// v_k v_k^H with a real off-diagonal beta_k; d - 1 reflectors, the last one only rotates the
+// phase of the last off-diagonal), the same real bisection / inverse iteration / Rayleigh-Ritz,
+// and a complex back-transformation.  Reflector k is kept unscaled in row k's upper part and
+// tau_k on the (dead) diagonal.
+template <class T, int PD>
+BK_DEV int tridiag_eig(T* A, int la, int d, int want, double* Z, double* H, double* U, double* scr, double* v,
+                       PSmem<T>& S) {
+  constexpr bool CPLX = std::is_same<T, zd>::value;
   constexpr int ZW = td_zw<PD>(), HL = ZW + 1;
   const int tid = threadIdx.x, lane = BK_LANE, warp = BK_WARP, nw = BK_NWARP;
   // Z (d x ZW) with the column index XOR-swizzled by the row: a warp walking a column (lanes
@@ -685,8 +697,73 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
   // of ZW = 32 doubles would otherwise put a whole column in one bank
 #define ZI(r, c) Z[(r) * ZW + ((c) ^ ((r) & 31))]
   double* dg = S.rc;              // diagonal of T (rc and rs are contiguous: PD doubles)
-  double* e = A + (d - 1) * la;   // off-diagonal of T in the dead lower part of row d - 1
+  double* e = reinterpret_cast<double*>(A + (d - 1) * la);  // off-diagonal of T in the dead lower part of row d - 1
   double* p = scr;                // tau A22 v (v: reflector of the current column)
+  if constexpr (CPLX) {
+    // ---- 1 (complex). work vectors in the Z region (shared memory, unused until phase 2)
+    zd* vz = reinterpret_cast<zd*>(Z);
+    zd* pz = vz + PD;
+    double* zred = S.ev;  // per-warp partials of p^H v (ev is free until the shifts are set)
+    for (int k = 0; k < d - 1; ++k) {
+      const int m = d - k - 1;
+      if (warp == 0) {
+        double s2 = 0.0;
+        for (int i = 1 + lane; i < m; i += 32) s2 += ab2(A[(k + 1 + i) * la + k]);
+        s2 = warp_sum(s2);
+        const zd alpha = A[(k + 1) * la + k];
+        double beta = alpha.re;
+        zd tau = {0.0, 0.0}, scal = {0.0, 0.0};
+        if (s2 > 0.0 || alpha.im != 0.0) {
+          beta = -copysign(sqrt(alpha.re * alpha.re + alpha.im * alpha.im + s2), alpha.re);
+          tau = {(beta - alpha.re) / beta, -alpha.im / beta};
+          const double dr = alpha.re - beta, di = alpha.im, dn = dr * dr + di * di;
+          scal = {dr / dn, -di / dn};  // 1 / (alpha - beta)
+        }
+        for (int i = lane; i < m; i += 32) vz[i] = i == 0 ? zd{1.0, 0.0} : A[(k + 1 + i) * la + k] * scal;
+        __syncwarp();
+        if (lane == 0) {
+          S.red[28] = tau.re;
+          S.red[29] = tau.im;
+          dg[k] = A[k * la + k].re;
+          e[k] = beta;  // column k below the diagonal is dead from here on
+        }
+      }
+      __syncthreads();
+      const zd tau = {S.red[28], S.red[29]};
+      if (tau.re != 0.0 || tau.im != 0.0) {
+        zd pv = {0.0, 0.0};  // sum conj(p_i) v_i
+        for (int i = warp; i < m; i += nw) {
+          const zd* row = A + (k + 1 + i) * la + (k + 1);
+          zd s_ = {0.0, 0.0};
+          for (int j = lane; j < m; j += 32) s_ = fmaT(row[j], vz[j], s_);
+          s_ = tau * warp_sum(s_);
+          if (lane == 0) pz[i] = s_;
+          pv = fmaT(cj(s_), vz[i], pv);
+        }
+        if (lane == 0) {
+          zred[2 * warp] = pv.re;
+          zred[2 * warp + 1] = pv.im;
+        }
+        __syncthreads();
+        zd pvt = {0.0, 0.0};
+        for (int w = 0; w < nw; ++w) pvt = pvt + zd{zred[2 * w], zred[2 * w + 1]};
+        const zd a2 = (-0.5 * tau) * pvt;  // -1/2 tau (p^H v)
+        for (int i = warp; i < m; i += nw) {
+          const zd vi = vz[i], wi = pz[i] + a2 * vi;
+          zd* row = A + (k + 1 + i) * la + (k + 1);
+          for (int j = lane; j < m; j += 32) {
+            const zd wj = pz[j] + a2 * vz[j];
+            zd x = row[j] - (vi * cj(wj) + wi * cj(vz[j]));  // A22 -= v w^H + w v^H
+            if (i == j) x.im = 0.0;
+            row[j] = x;
+          }
+        }
+      }
+      for (int i = tid; i < m; i += blockDim.x) A[k * la + k + 1 + i] = vz[i];
+      if (tid == 0) A[k * la + k] = tau;  // (its real part went to dg[k])
+      __syncthreads();
+    }
+  } else {
   // ---- 1. tridiagonalisation; the scaled reflector sqrt(tau) v_k goes to row k's upper part
   for (int k = 0; k < d - 2; ++k) {
     const int m = d - k - 1;
@@ -766,12 +843,15 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     for (int i = tid; i < m; i += blockDim.x) A[k * la + k + 1 + i] = st * v[i];
     __syncthreads();
   }
+  }  // real / complex tridiagonalisation
   if (tid == 0) {
-    if (d >= 2) {
-      dg[d - 2] = A[(d - 2) * la + d - 2];
-      e[d - 2] = A[(d - 1) * la + d - 2];
+    if constexpr (!CPLX) {
+      if (d >= 2) {
+        dg[d - 2] = rl(A[(d - 2) * la + d - 2]);
+        e[d - 2] = rl(A[(d - 1) * la + d - 2]);
+      }
     }
-    dg[d - 1] = A[(d - 1) * la + d - 1];
+    dg[d - 1] = rl(A[(d - 1) * la + d - 1]);
     // Gershgorin interval, 1-norm, pivmin (dstebz)
     double gl = 1e300, gu = -1e300, onenrm = 0.0, emax2 = 1.0;
     for (int i = 0; i < d; ++i) {
@@ -957,7 +1037,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
       H[b * HL + a] = h;
     }
     __syncthreads();
-    smem_jacobi<double>(H, HL, U, HL, want, true, S);  // (uses rc/rs/pp/pq: dg is dead now)
+    smem_jacobi<double>(H, HL, U, HL, want, true, reinterpret_cast<PSmem<double>&>(S));  // (uses rc/rs/pp/pq: dg is dead now)
     __syncthreads();
     for (int i = tid; i < want; i += blockDim.x) {
       const double vi = H[i * HL + i];
@@ -994,6 +1074,36 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
     __syncthreads();
   }
   PMARK(10);
+  if constexpr (CPLX) {
+    // ---- 4 (complex). Q Z with Q = H_0 ... H_{d-2}, H_k = I - tau_k v_k v_k^H: the complex
+    //    vectors are built column-major in the (global, L2-resident) scratch -- a warp owns its
+    //    columns, lanes walk the rows -- and copied to A[:, 0:want] once every reflector is done
+    zd* ZcT = reinterpret_cast<zd*>(scr);  // [want][PD]
+    for (int j = warp; j < want; j += nw)
+      for (int i = lane; i < d; i += 32) ZcT[j * PD + i] = zd{ZI(i, j), 0.0};
+    __syncwarp();
+    for (int j = warp; j < want; j += nw) {
+      zd* zc = ZcT + j * PD;
+      for (int k = d - 2; k >= 0; --k) {
+        const zd tau = A[k * la + k];
+        if (tau.re == 0.0 && tau.im == 0.0) continue;
+        const int m = d - k - 1;
+        const zd* vk = A + k * la + k + 1;
+        zd dot = {0.0, 0.0};
+        for (int i = lane; i < m; i += 32) dot = fmaT(cj(vk[i]), zc[k + 1 + i], dot);
+        dot = tau * warp_sum(dot);
+        for (int i = lane; i < m; i += 32) zc[k + 1 + i] = zc[k + 1 + i] - vk[i] * dot;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    PMARK(11);
+    for (int i = warp; i < d; i += nw)
+      for (int j = lane; j < want; j += 32) A[i * la + j] = ZcT[j * PD + i];
+    for (int j = tid; j < want; j += blockDim.x) S.ord[j] = j;  // ev set by the Rayleigh-Ritz step
+    __syncthreads();
+    return 0;
+  } else {
   // ---- 4. back-transformation Z <- H_0 ... H_{d-3} Z: a warp owns columns warp + c nw, all of
   //    them updated in one pass over each reflector (read once; no block barriers)
   {
@@ -1045,6 +1155,7 @@ BK_DEV int tridiag_eig(double* A, int la, int d, int want, double* Z, double* H,
   for (int j = tid; j < want; j += blockDim.x) S.ord[j] = j;  // ev set by the Rayleigh-Ritz step
   __syncthreads();
   return 0;
+  }  // real / complex back-transformation
 #undef TD_U
 #undef ZI
 }
@@ -1130,20 +1241,21 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
   // the rebuilt eigenvector columns go to the same region / the dead A
   double* const pkbuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(B);
   double* const ebuf = kOwnPk<T, PD> ? S.pk : reinterpret_cast<double*>(A);
-  if constexpr (std::is_same<T, double>::value) {
+  if constexpr (std::is_same<T, double>::value || kZtd<T, PD>) {
     if (td && want <= td_zw<PD>() && d >= 4) {
       // tridiagonal route: eigenvectors land in A[:, 0:want], ev/ord set (see tridiag_eig)
       constexpr int ZW = td_zw<PD>(), HL = ZW + 1;
+      constexpr bool OWN = kOwnPk<T, PD> || kZtd<T, PD>;  // Z, H, U have their own shared region
       double* Bd = reinterpret_cast<double*>(B);
       // Z, H, U in shared memory: the dead B (shared variant) or the packed-triangle region
-      // (large variant); inverse-iteration scratch aliases H / U there, or lives in B (global)
-      double* Z = kOwnPk<T, PD> ? S.pk : Bd;
+      // (large variants); inverse-iteration scratch aliases H / U there, or lives in B (global)
+      double* Z = OWN ? S.pk : Bd;
       double* H = Z + PD * ZW;
       double* U = H + ZW * HL;
-      double* scr = kOwnPk<T, PD> ? Bd : H;
+      double* scr = OWN ? Bd : H;
       double* v = scr + TD_BATCH * 4 * PD;
-      static_assert(kOwnPk<T, PD> || PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1), "td scratch");
-      if (tridiag_eig<PD>(reinterpret_cast<double*>(A), PLD, d, want, Z, H, U, scr, v, S) != 0) return 2;
+      static_assert(OWN || PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1), "td scratch");
+      if (tridiag_eig<T, PD>(A, PLD, d, want, Z, H, U, scr, v, S) != 0) return 2;
       PMARK(12);
       smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
       __syncthreads();
@@ -1452,6 +1564,7 @@ static int p_smem_bytes() {
           (2 * PD + PD + 8 + ((PD + 3) & ~3)) * (int)sizeof(int);
   // the packed-triangle region (large real variant) also holds the tridiagonal route's Z, H, U
   if (kOwnPk<T, PD>) b += max(PD * (PD + 1) / 2, PD * td_zw<PD>() + 2 * td_zw<PD>() * (td_zw<PD>() + 1)) * (int)sizeof(double);
+  if (kZtd<T, PD>) b += (PD * td_zw<PD>() + 2 * td_zw<PD>() * (td_zw<PD>() + 1)) * (int)sizeof(double);
   return b;
 }
 
@@ -1468,7 +1581,7 @@ static void launch_variant(const PencilParams& P, cudaStream_t st) {
   cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        p_smem_bytes<T, PD, GMEM>());
   // the complex large variant streams its matrices through L1: keep the carveout small
-  if (GMEM && !kOwnPk<T, PD>)
+  if (GMEM && !kOwnPk<T, PD> && !kZtd<T, PD>)
     cudaFuncSetAttribute(pencil_kernel<T, PD, GMEM>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
   pencil_kernel<T, PD, GMEM><<<P.nb, P_THREADS, p_smem_bytes<T, PD, GMEM>(), st>>>(P);
 }
