@@ -763,6 +763,78 @@ BK_DEV int tridiag_eig(T* A, int la, int d, int want, double* Z, double* H, doub
       if (tid == 0) A[k * la + k] = tau;  // (its real part went to dg[k])
       __syncthreads();
     }
+  } else if constexpr (kOwnPk<T, PD>) {
+    // ---- 1 (real large variant). The trailing matrix as a packed lower triangle in the shared
+    //    region that holds Z afterwards (entry (i, j <= i) at i (i + 1) / 2 + j), the reflector
+    //    and p = tau A22 v beside it: the symv reads a row's left part contiguously and its
+    //    right part down the column, the rank-2 update touches the triangle only -- the square
+    //    in global memory (L2) is read once and only receives the reflectors.
+    double* tri = S.pk;
+    double* vs = tri + PD * (PD + 1) / 2;
+    double* ps = vs + PD;
+    static_assert(PD * (PD + 1) / 2 + 2 * PD <= PD * ZW + 2 * ZW * (ZW + 1), "packed tridiagonalisation scratch");
+    auto off = [](int i) { return i * (i + 1) / 2; };
+    for (int i = warp; i < d; i += nw)
+      for (int j = lane; j <= i; j += 32) tri[off(i) + j] = A[i * la + j];
+    __syncthreads();
+    for (int k = 0; k < d - 2; ++k) {
+      const int m = d - k - 1;
+      if (warp == 0) {
+        double s2 = 0.0;
+        for (int i = 1 + lane; i < m; i += 32) {
+          const double xi = tri[off(k + 1 + i) + k];
+          s2 += xi * xi;
+        }
+        s2 = warp_sum(s2);
+        const double alpha = tri[off(k + 1) + k];
+        double beta = alpha, tau = 0.0, scal = 0.0;
+        if (s2 > 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        for (int i = lane; i < m; i += 32) vs[i] = i == 0 ? 1.0 : tri[off(k + 1 + i) + k] * scal;
+        __syncwarp();
+        if (lane == 0) {
+          S.red[28] = tau;
+          dg[k] = tri[off(k) + k];
+          e[k] = beta;
+        }
+      }
+      __syncthreads();
+      const double tau = S.red[28];
+      if (tau != 0.0) {
+        double pv = 0.0;
+        for (int i = warp; i < m; i += nw) {
+          const int r = k + 1 + i;
+          const double* row = tri + off(r) + (k + 1);
+          double s_ = 0.0;
+          for (int j = lane; j < m; j += 32) s_ += (j <= i ? row[j] : tri[off(k + 1 + j) + r]) * vs[j];
+          s_ = warp_sum(s_) * tau;
+          if (lane == 0) ps[i] = s_;
+          pv += s_ * vs[i];
+        }
+        if (lane == 0) S.red[warp] = pv;
+        __syncthreads();
+        double pvt = 0.0;
+        for (int w = 0; w < nw; ++w) pvt += S.red[w];
+        const double a2 = -0.5 * tau * pvt;
+        for (int i = warp; i < m; i += nw) {
+          const double vi = vs[i], wi = ps[i] + a2 * vi;
+          double* row = tri + off(k + 1 + i) + (k + 1);
+          for (int j = lane; j <= i; j += 32) row[j] -= vi * (ps[j] + a2 * vs[j]) + wi * vs[j];
+        }
+      }
+      const double st = sqrt(tau);
+      for (int i = tid; i < m; i += blockDim.x) A[k * la + k + 1 + i] = st * vs[i];
+      __syncthreads();
+    }
+    if (tid == 0 && d >= 2) {  // the last 2 x 2 block, where the common code below reads it
+      A[(d - 2) * la + d - 2] = tri[off(d - 2) + d - 2];
+      A[(d - 1) * la + d - 2] = tri[off(d - 1) + d - 2];
+      A[(d - 1) * la + d - 1] = tri[off(d - 1) + d - 1];
+    }
+    __syncthreads();
   } else {
   // ---- 1. tridiagonalisation; the scaled reflector sqrt(tau) v_k goes to row k's upper part
   for (int k = 0; k < d - 2; ++k) {

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4 > gpurun_out/tests.log
-timeout 1500 python tools/iter_breakdown.py 5 2 3 64 1024 > gpurun_out/breakdown5s_c.log 2>&1
+timeout 1200 python -m pytest tests/test_kernels_gpu.py tests/test_solver_gpu.py tests/test_golden_gpu.py tests/test_fullsize_gpu.py -m gpu -q -x 2>&1 | tail -6 > gpurun_out/ptd_tests.log
+timeout 600 python tools/pencil_batch_time.py > gpurun_out/pencil_batch.txt 2>&1
