@@ -653,6 +653,9 @@ BK_DEV void replay_rotations(double* E, int le, int d, const int* sel, int want,
 // Z (PD x ZW), H and U (ZW x (ZW + 1)) in shared memory; scr (TD_BATCH x 4 PD) and v (PD) may
 // alias H / U (inverse iteration finishes before the Rayleigh-Ritz step).
 constexpr int TD_BATCH = 16;
+// inverse-iteration batch: the large variants keep the scratch in global memory (room for 32
+// independent LU solves at once: want = 64 in two batches instead of four)
+template <int PD> constexpr int td_batch() { return PD > 96 ? 32 : TD_BATCH; }
 template <int PD> constexpr int td_zw() { return PD <= 96 ? 32 : 64; }
 
 BK_DEV int sturm_count(const double* dg, const double* e, int n, double x, double pivmin) {
@@ -1000,12 +1003,13 @@ BK_DEV int tridiag_eig(T* A, int la, int d, int want, double* Z, double* H, doub
   //    start vectors), which the Rayleigh-Ritz step below resolves
   const double tiny = DBL_EPSILON * fmax(S.red[27], DBL_MIN);
   int bad = 0;
-  for (int b0 = 0; b0 < want; b0 += TD_BATCH) {
+  constexpr int TDB = td_batch<PD>();
+  for (int b0 = 0; b0 < want; b0 += TDB) {
     const int j = b0 + tid;
-    if (tid < TD_BATCH && j < want) {
+    if (tid < TDB && j < want) {
       // per-thread arrays interleaved across the batch (element i of thread t at
       // (4 i + a) TD_BATCH + t): the batch's simultaneous accesses are consecutive words
-#define TD_U(a, i) scr[(4 * (i) + (a)) * TD_BATCH + tid]
+#define TD_U(a, i) scr[(4 * (i) + (a)) * TDB + tid]
       const double lj = shift[j];
       for (int i = 0; i < d; ++i) TD_U(3, i) = td_start(j, i);
       for (int iter = 0; iter < 2 && !bad; ++iter) {
@@ -1325,8 +1329,10 @@ BK_DEV int pencil_attempt_impl(const T* Ar, const T* Br, int ldr, int d, int wan
       double* H = Z + PD * ZW;
       double* U = H + ZW * HL;
       double* scr = OWN ? Bd : H;
-      double* v = scr + TD_BATCH * 4 * PD;
-      static_assert(OWN || PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1), "td scratch");
+      double* v = scr + td_batch<PD>() * 4 * PD;
+      static_assert(OWN ? (td_batch<PD>() * 4 * PD + PD <= PD * (PD + 1))
+                        : (td_batch<PD>() == TD_BATCH && PD * ZW + TD_BATCH * 4 * PD + PD <= PD * (PD + 1)),
+                    "td scratch");
       if (tridiag_eig<T, PD>(A, PLD, d, want, Z, H, U, scr, v, S) != 0) return 2;
       PMARK(12);
       smem_gemm<T, PD, true, true, false, false>(Li, PLD, A, PLD, B, PLD, d, d, want);
