@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_kernels_gpu.py tests/test_solver_gpu.py tests/test_golden_gpu.py tests/test_fullsize_gpu.py -m gpu -q -x 2>&1 | tail -6 > gpurun_out/ptd_tests.log
-timeout 600 python tools/pencil_batch_time.py > gpurun_out/pencil_batch.txt 2>&1
+PPCG_B200_LIB=$PWD/paper_1407_7506_b200/libppcg_b200_prof.so timeout 900 python tools/pencil_phases.py 5 3 64 512 > gpurun_out/pencil_phases5.txt 2>&1
+PPCG_B200_LIB=$PWD/paper_1407_7506_b200/libppcg_b200_prof.so timeout 900 python tools/pencil_phases.py 3 3 > gpurun_out/pencil_phases3.txt 2>&1

@@ -1,6 +1,6 @@
 """Phase clocks of the subblock pencil kernel (subblock 0) on live solver state.  Needs a
 profiling build of the library (pencil.cu compiled with -DPPCG_PENCIL_PROFILE):
-  PPCG_B200_LIB=.../libppcg_b200_prof.so python tools/pencil_phases.py [cfg] [steps]"""
+  PPCG_B200_LIB=.../libppcg_b200_prof.so python tools/pencil_phases.py [cfg] [steps] [N] [k]"""
 import ctypes
 import os
 import sys
@@ -14,7 +14,10 @@ from paper_1407_7506_b200.problems import config_problem, jacobi_preconditioner 
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-a, k, q, tol = config_problem(cfg)
+kw = {"N": int(sys.argv[3])} if len(sys.argv) > 3 else {}
+a, k, q, tol = config_problem(cfg, **kw)
+if len(sys.argv) > 4:
+    k = int(sys.argv[4])
 s = PPCGSolver(a, jacobi_preconditioner(a), None, SolverOptions(k=k, sbsize=q, tol=tol, max_iter=10 ** 6)).start()
 lib = ctypes.CDLL(_lib.LIB_PATH)
 lib.bk_pencil_phase_clocks.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
