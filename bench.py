@@ -49,8 +49,8 @@ def hbm_peak():
 
 
 NCU_SOURCE = "profiles/ncu_summary.json (ncu --set full capture of the same kernels on the live config-2 state)"
-NCU_OZ_SOURCE = ("profiles/ncu_ozaki_r02.json (ncu --set full --clock-control none of the emulated products on "
-                 "config-2 shapes, tools/oz_one.py)")
+NCU_OZ_SOURCE = ("profiles/ncu_summary_r02g.json (ncu --set full --clock-control none of the bench's own roofline "
+                 "launches on the live config-2 state, tools/roofline_capture.py; else profiles/ncu_ozaki_r02.json)")
 # digit products per FP64 multiply-add in the emulation (csrc/ozaki.cu: 8 digits, pairs i + j <= 7)
 OZ_PRODUCTS = 36
 
@@ -66,7 +66,13 @@ def ncu_traffic(kernel):
 
 
 def ncu_oz(kernel, key="dram_bytes_per_launch"):
-    """A per-launch figure of an emulated-FP64 kernel from profiles/ncu_ozaki_r02.json."""
+    """A per-launch figure of an emulated-FP64 kernel from the committed ncu summaries (the latest
+    capture of the bench's own launches first)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r02g.json")))
+        return d["kernels"][kernel][key]
+    except Exception:
+        pass
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_ozaki_r02.json")))
         for name, runs in d["kernels"].items():  # template arguments vary (k_oz_ts<32>)
