@@ -125,6 +125,9 @@ int bk_subblock_grams_z(int64_t n, int k_act, int q, int has_p, const double* X,
  * Returns the previous mode (mode < 0: query only). */
 int bk_pencil_set_eig(int mode);
 int bk_pencil_max_dim(void);
+/* Profiling builds only (pencil.cu compiled with -DPPCG_PENCIL_PROFILE): clock64 stamps of subblock 0's
+ * phases in the last pencil launch (32 values; tools/pencil_phases.py).  Returns 1, or 0 in normal builds. */
+int bk_pencil_phase_clocks(long long* out);
 /* global workspace for nb pencils of dimension dmax (0 when d <= 96 real / 64 complex, which
  * run entirely in shared memory; larger ones keep their matrices and, real, the Jacobi
  * rotation log here); pass it as ws/ws_bytes below */

@@ -61,6 +61,7 @@ _SIGS = {
     "bk_subblock_grams_z": (c_int, [c_i64, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, c_i64,
                                     vp, vp, vp, vp, vp, c_i64, vp]),
     "bk_pencil_max_dim": (c_int, []),
+    "bk_pencil_phase_clocks": (c_int, [vp]),
     "bk_pencil_set_eig": (c_int, [c_int]),
     "bk_pencil_ws_bytes": (c_i64, [c_int, c_int, c_int]),
     "bk_block_assemble": (c_int, [c_int, c_int, vp, vp, vp, vp, c_i64, vp, vp, c_i64, vp]),
